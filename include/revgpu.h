@@ -1,0 +1,136 @@
+/*
+ * revgpu.h — C ABI of the B200-native reversible-AD gradient kernels.
+ *
+ * The reference (`revlang`, /root/reference/pkg/src/revlang) is a pure-Python
+ * interpreter with no FFI; its hot path is `autodiff.gradient`
+ * (autodiff.py:136-180): run f forward, wrap outputs in GVar cells, seed,
+ * run the mechanically inverted ~f in gradient mode (numerics.py:435-505
+ * adjoint rules), check the primal restoration.  Each entry point below
+ * replaces that call for one registered program, batched over independent
+ * inputs, as ONE fused forward + reverse-sweep kernel with no tape.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the function name ends in
+ *     `_host`; buffers are caller-owned, C-contiguous, row-major.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous; they do not synchronise unless noted.
+ *   - Return value: RL_OK, a positive revlang error class (only from the
+ *     `_host` calls and argument validation), or a negative usage/CUDA error.
+ *   - Per-element reversibility failures are reported in `fail[i]` (one of
+ *     the positive codes; 0 = ok), never by aborting the batch: a kernel
+ *     cannot throw.  `counters` (device, uint64) accumulate
+ *     [0] = total loop trips / work units, [1] = number of failed elements.
+ *   - No global mutable state: the library is re-entrant across streams
+ *     and host threads.
+ */
+#ifndef REVGPU_H
+#define REVGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_ABI_VERSION 1
+
+/* Status / per-element failure codes.  Positive codes name the revlang
+ * exception class the reference interpreter raises for the same input
+ * (revlang/errors.py). */
+enum rl_status {
+  RL_OK = 0,
+  RL_ERR_POSTCONDITION = 1, /* PostconditionMismatch  errors.py:64; interpreter.py:764-792 */
+  RL_ERR_DIRTY_ANCILLA = 2, /* DirtyAncilla           errors.py:68; interpreter.py:738-745 */
+  RL_ERR_DOMAIN = 3,        /* RevDomainError         errors.py:87; values.py:343-431      */
+  RL_ERR_ITERATOR = 4,      /* LoopIteratorMutated    errors.py:75; interpreter.py:863-884 */
+  RL_ERR_RESTORE = 5,       /* RevError "backward pass failed to restore" autodiff.py:169-172 */
+  RL_ERR_FUEL = 6,          /* FuelExhausted          errors.py:95; interpreter.py:461-466 */
+  RL_ERR_KIND = 7,          /* KindError              errors.py:111                        */
+  RL_ERR_INDEX = 8,         /* IndexOutOfBounds       errors.py:103; values.py:172-183     */
+  RL_ERR_OVERFLOW = 9,      /* Python OverflowError from math.exp (values.py:362)          */
+  RL_ERR_INVALID = -1,      /* bad argument: null pointer, negative size, bad shape        */
+  RL_ERR_CUDA = -2,         /* CUDA runtime error (see rl_last_error())                    */
+  RL_ERR_NO_DEVICE = -3     /* no sm_100 device visible                                     */
+};
+
+int rl_abi_version(void);
+const char *rl_strerror(int code);
+/* Message of the last negative status on the calling host thread. */
+const char *rl_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Bessel J_nu(z) power series (programs/besselj.rnl).
+ * Replaces: gradient(p, GradRequest("besselj", [0.0, nu, z[i]])) for every i
+ *   (autodiff.py:136; default seed out!.g = 1.0, autodiff.py:99-110).
+ * Outputs: J[i] = primal out!, dJdz[i] = z.g for out!.g = seed, fail[i].
+ * thr: the loop threshold literal of the program (1e-16); tol: the
+ * ExecOptions.float_tolerance (interpreter.py:39, 1e-9); max_trips: fuel cap
+ * on series terms (FuelExhausted beyond it); invcheck: ExecOptions.invcheck.
+ * counters[0] += sum of series trips, counters[1] += failed elements.
+ * ---------------------------------------------------------------------- */
+int rl_besselj_grad_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, uint8_t *fail, unsigned long long *counters,
+                        void *stream);
+
+/* Same computation from HOST buffers (pageable or pinned): chunked
+ * host->device copies, kernels and device->host copies pipelined on the
+ * library's own streams on `device`.  Synchronous.  Writes sum_trips /
+ * n_failed if non-NULL.  This is the entry a reference-side FFI binds. */
+int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                             double seed, int64_t max_trips, int32_t invcheck, double *J,
+                             double *dJdz, uint8_t *fail, unsigned long long *sum_trips,
+                             unsigned long long *n_failed, int32_t device);
+
+/* ------------------------------------------------------------------------
+ * ADBench bundle adjustment Jacobian (programs/ba.rnl).
+ * Replaces, per observation i with (c, p) = obs[i]:
+ *   gradient(p, GradRequest("ba_proj", [0,0,cams[c],X[p],w[i],feats[i]],
+ *            seeds=[("e1!",(),1)] / [("e2!",(),1)], wrt=["cam","X","w"]))
+ *   and gradient(p, GradRequest("ba_weight", [0.0, w[i]])).
+ * cams: n_cams x 11, X: n_pts x 3, w: n_obs, feats: n_obs x 2,
+ * obs: n_obs x 2 int32 (camera index, point index; 0-based).
+ * J: n_obs x 31 = [de1/d(cam,X,w) (15), de2/d(cam,X,w) (15), d(1-w^2)/dw].
+ * err (optional, may be NULL): n_obs x 3 = [e1, e2, 1 - w^2].
+ * Out-of-range indices set fail[i] = RL_ERR_INDEX (values.py:172-183).
+ * ---------------------------------------------------------------------- */
+int rl_ba_jac_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                  const double *X, const double *w, const double *feats, const int32_t *obs,
+                  double tol, int32_t invcheck, double *err, double *J, uint8_t *fail,
+                  unsigned long long *counters, void *stream);
+
+int rl_ba_jac_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                       const double *X, const double *w, const double *feats,
+                       const int32_t *obs, double tol, int32_t invcheck, double *err,
+                       double *J, uint8_t *fail, unsigned long long *n_failed, int32_t device);
+
+/* ------------------------------------------------------------------------
+ * ADBench GMM objective gradient (programs/gmm.rnl).
+ * Replaces: gradient(p, GradRequest("gmm", [0.0, alphas, means, icf, x,
+ *   zeros..., gamma, m, cst], wrt=["alphas","means","icf"])).
+ * alphas: K, means: K x d, icf: K x d(d+1)/2 (d log-diagonal entries, then the
+ * strict lower triangle column by column), x: N x d (this call's points).
+ * out (device, 1 + K + K*d + K*d(d+1)/2 doubles, OVERWRITTEN):
+ *   [err, g_alphas, g_means, g_icf].  With add_param_terms = 0 only the
+ *   per-point terms of this shard are produced (for a sum-allreduce across
+ *   ranks); with 1 the parameter-only terms (-N_total*lse(alphas), Wishart
+ *   prior, cst) are added too.  fail: N per-point flags.
+ * ws: device workspace of rl_gmm_workspace_bytes() bytes.
+ * ---------------------------------------------------------------------- */
+size_t rl_gmm_workspace_bytes(int32_t d, int32_t K, int64_t N);
+int rl_gmm_grad_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
+                    const double *means, const double *icf, const double *x, double gamma,
+                    int32_t m, double cst, double tol, int32_t invcheck,
+                    int32_t add_param_terms, double *out, uint8_t *fail,
+                    unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
+
+int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                         const double *means, const double *icf, const double *x, double gamma,
+                         int32_t m, double cst, double tol, int32_t invcheck, double *out,
+                         unsigned long long *n_failed, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REVGPU_H */

@@ -1,0 +1,187 @@
+"""Golden-vector generator: runs the REFERENCE revlang interpreter.
+
+Test infrastructure only (never imported by the product package).  It
+imports the read-only reference package in place from
+/root/reference/pkg/src, executes `revlang.gradient` (autodiff.py:136-180)
+over the three benchmark programs shipped in
+paper_2003_04617_b200/programs/*.rnl, and writes seeded inputs plus the
+reference outputs to tests/golden/*.npz.  Those fixtures pin both the C
+oracle (oracle/revoracle.c) and the CUDA kernels; the GPU box has no
+/root/reference, so only the .npz files travel.
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden.py [bessel|ba|gmm ...]
+"""
+
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROG_DIR = os.path.join(REPO, "paper_2003_04617_b200", "programs")
+OUT_DIR = os.path.join(REPO, "tests", "golden")
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, REF_SRC)
+from revlang import ExecOptions, GradRequest, gradient, parse_program  # noqa: E402
+from revlang.errors import RevLangError  # noqa: E402
+from revlang.values import Array  # noqa: E402
+
+
+def _prog(name):
+    with open(os.path.join(PROG_DIR, name)) as fh:
+        return parse_program(fh.read(), name)
+
+
+def _err_name(fn):
+    try:
+        return fn(), ""
+    except RevLangError as err:
+        return None, type(err).__name__
+
+
+# --------------------------------------------------------------------------
+# Bessel J_nu: C1 (1,000 z ~ U(0.1, 10), seed 0, nu = 2) plus other orders,
+# edge arguments and the domain errors of z <= 0.
+# --------------------------------------------------------------------------
+
+def gen_bessel():
+    p = _prog("besselj.rnl")
+    cases = []
+    z_c1 = np.random.default_rng(0).uniform(0.1, 10.0, 1000)
+    cases += [(2, float(z)) for z in z_c1]
+    rng = np.random.default_rng(10)
+    for nu in (0, 1, 3, 5):
+        cases += [(nu, float(z)) for z in rng.uniform(0.05, 12.0, 64)]
+    edge = [1e-300, 1e-12, 1e-3, 0.1, 1.0, 2.404825557695773, 5.135622301840683,
+            10.0, 15.0, 20.0, 30.0, 0.0, -1.0, -1e-300]
+    for nu in (0, 2, 7):
+        cases += [(nu, z) for z in edge]
+    nus = np.array([c[0] for c in cases], np.int32)
+    zs = np.array([c[1] for c in cases], np.float64)
+    J = np.full(len(cases), np.nan)
+    dz = np.full(len(cases), np.nan)
+    errs = []
+    t0 = time.perf_counter()
+    for i, (nu, z) in enumerate(cases):
+        res, en = _err_name(lambda: gradient(p, GradRequest("besselj", [0.0, nu, z])))
+        if res is not None:
+            primal, g = res
+            J[i], dz[i] = primal[0], g["z"]
+        errs.append(en)
+    dt = time.perf_counter() - t0
+    np.savez_compressed(os.path.join(OUT_DIR, "bessel.npz"), nu=nus, z=zs, J=J,
+                        dJdz=dz, err=np.array(errs), thr=1e-16, tol=1e-9)
+    print(f"bessel: {len(cases)} cases in {dt:.1f}s, errors={sum(1 for e in errs if e)}")
+
+
+# --------------------------------------------------------------------------
+# Bundle adjustment: per-observation 2 x 15 Jacobian block and the weight
+# derivative, two seeded gradient passes per observation.
+# --------------------------------------------------------------------------
+
+def ba_inputs(rng, n_obs):
+    cams = np.empty((n_obs, 11))
+    cams[:, 0:3] = rng.normal(0.0, 0.3, (n_obs, 3))
+    cams[:, 3:6] = rng.normal(0.0, 1.0, (n_obs, 3))
+    cams[:, 6] = rng.uniform(500.0, 600.0, n_obs)
+    cams[:, 7:9] = rng.uniform(0.0, 1.0, (n_obs, 2))
+    cams[:, 9:11] = rng.normal(0.0, 0.01, (n_obs, 2))
+    X = rng.normal(0.0, 1.0, (n_obs, 3))
+    X[:, 2] += 10.0
+    w = rng.uniform(0.0, 1.0, n_obs)
+    feat = rng.uniform(0.0, 100.0, (n_obs, 2))
+    return cams, X, w, feat
+
+
+def gen_ba():
+    p = _prog("ba.rnl")
+    n_obs = 48
+    cams, X, w, feat = ba_inputs(np.random.default_rng(3), n_obs)
+    cams[5, 0:3] = 0.0          # zero rotation: the else branch (no rodrigues)
+    cams[17, 0:3] = [0.0, 0.0, 1e-3]
+    J = np.full((n_obs, 2, 15), np.nan)
+    e = np.full((n_obs, 2), np.nan)
+    wj = np.full(n_obs, np.nan)
+    errs = []
+    opts = ExecOptions()
+    t0 = time.perf_counter()
+    for o in range(n_obs):
+        args = [0.0, 0.0, Array.vector(cams[o].tolist()), Array.vector(X[o].tolist()),
+                float(w[o]), float(feat[o, 0]), float(feat[o, 1])]
+        en = ""
+        for r, seed in enumerate(("e1!", "e2!")):
+            res, en = _err_name(lambda: gradient(p, GradRequest(
+                "ba_proj", args, seeds=[(seed, (), 1.0)], wrt=["cam", "X", "w"]), opts))
+            if res is None:
+                break
+            primal, g = res
+            e[o] = primal[0], primal[1]
+            J[o, r] = g["cam"].data + g["X"].data + [g["w"]]
+        res, en2 = _err_name(lambda: gradient(p, GradRequest("ba_weight", [0.0, float(w[o])]), opts))
+        if res is not None:
+            wj[o] = res[1]["w"]
+        errs.append(en or en2)
+    dt = time.perf_counter() - t0
+    np.savez_compressed(os.path.join(OUT_DIR, "ba.npz"), cams=cams, X=X, w=w, feat=feat,
+                        J=J, e=e, wjac=wj, err=np.array(errs))
+    print(f"ba: {n_obs} observations in {dt:.1f}s")
+
+
+# --------------------------------------------------------------------------
+# GMM: small (d, K, N) cases through the full reversible objective.
+# --------------------------------------------------------------------------
+
+def gmm_constants(d, K, N, gamma, m):
+    n = d + m + 1
+    lgd = 0.25 * d * (d - 1) * math.log(math.pi) + sum(
+        math.lgamma(0.5 * n + 0.5 * (1 - j)) for j in range(1, d + 1))
+    C = n * d * (math.log(gamma) - 0.5 * math.log(2.0)) - lgd
+    return -N * d * 0.5 * math.log(2.0 * math.pi) - K * C
+
+
+def gmm_inputs(rng, d, K, N):
+    alphas = rng.normal(0.0, 1.0, K)
+    means = rng.uniform(0.0, 1.0, (K, d))
+    icf = rng.normal(0.0, 1.0, (K, d * (d + 1) // 2)) * 0.5
+    x = rng.uniform(0.0, 1.0, (N, d))
+    return alphas, means, icf, x
+
+
+def gen_gmm():
+    p = _prog("gmm.rnl")
+    out = {}
+    cases = [(3, 2, 4, 1.0, 0), (5, 4, 20, 1.0, 0), (8, 5, 10, 1.3, 2),
+             (4, 3, 64, 1.0, 0), (16, 6, 6, 0.7, 1), (2, 1, 5, 1.0, 0)]
+    t0 = time.perf_counter()
+    for ci, (d, K, N, gamma, m) in enumerate(cases):
+        alphas, means, icf, x = gmm_inputs(np.random.default_rng(100 + ci), d, K, N)
+        cst = gmm_constants(d, K, N, gamma, m)
+        A = lambda a: Array.matrix(a.tolist()) if a.ndim == 2 else Array.vector(a.tolist())
+        Z = lambda *s: A(np.zeros(s))
+        args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), Z(K),
+                float(gamma), int(m), float(cst)]
+        res, en = _err_name(lambda: gradient(p, GradRequest(
+            "gmm", args, wrt=["alphas", "means", "icf"])))
+        assert res is not None, en
+        primal, g = res
+        pre = f"c{ci}_"
+        out.update({pre + "dims": np.array([d, K, N, m]), pre + "gamma": gamma, pre + "cst": cst,
+                    pre + "alphas": alphas, pre + "means": means, pre + "icf": icf, pre + "x": x,
+                    pre + "err": primal[0],
+                    pre + "g_alphas": np.array(g["alphas"].data),
+                    pre + "g_means": np.array(g["means"].data).reshape(K, d),
+                    pre + "g_icf": np.array(g["icf"].data).reshape(K, -1)})
+    out["ncases"] = len(cases)
+    np.savez_compressed(os.path.join(OUT_DIR, "gmm.npz"), **out)
+    print(f"gmm: {len(cases)} cases in {time.perf_counter() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT_DIR, exist_ok=True)
+    which = sys.argv[1:] or ["bessel", "ba", "gmm"]
+    for w in which:
+        globals()["gen_" + w]()

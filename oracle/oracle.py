@@ -1,0 +1,124 @@
+"""ctypes front end of the C oracle (oracle/revoracle.c) — TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) may import this module.  The product package
+(paper_2003_04617_b200) never does: it has no CPU path.
+
+Each function restates `revlang.gradient` (reference autodiff.py:136-180)
+for one benchmark program; see revoracle.c for the statement-level
+citations.  The oracle is pinned bit-for-bit against golden vectors that
+the reference interpreter itself produced (tests/golden, made by
+oracle/gen_golden.py).
+"""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_u8_p = ctypes.POINTER(ctypes.c_uint8)
+_c_i32_p = ctypes.POINTER(ctypes.c_int32)
+_lib = None
+
+
+def build(force=False):
+    """Compile revoracle.c with gcc (no contraction, no fast-math)."""
+    src = os.path.join(HERE, "revoracle.c")
+    if not force and os.path.exists(LIB_PATH) and \
+            os.path.getmtime(LIB_PATH) >= os.path.getmtime(src):
+        return LIB_PATH
+    subprocess.check_call(["make", "-s", "-C", HERE])
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.orc_besselj_grad.restype = ctypes.c_int
+        L.orc_besselj_grad.argtypes = [
+            ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_long, ctypes.c_int, _c_double_p, _c_double_p,
+            ctypes.POINTER(ctypes.c_long)]
+        L.orc_besselj_grad_batch.restype = ctypes.c_long
+        L.orc_besselj_grad_batch.argtypes = [
+            ctypes.c_int, _c_double_p, ctypes.c_long, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_long, ctypes.c_int, _c_double_p, _c_double_p, _c_u8_p]
+        L.orc_ba_obs.restype = ctypes.c_int
+        L.orc_ba_obs.argtypes = [_c_double_p, _c_double_p, ctypes.c_double, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                 _c_double_p, _c_double_p]
+        L.orc_ba_jac_batch.restype = ctypes.c_long
+        L.orc_ba_jac_batch.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_long, _c_double_p, _c_double_p, _c_double_p,
+            _c_double_p, _c_i32_p, ctypes.c_double, ctypes.c_int, _c_double_p, _c_double_p,
+            _c_u8_p]
+        L.orc_gmm_grad.restype = ctypes.c_int
+        L.orc_gmm_grad.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
+            _c_double_p, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+            ctypes.c_int, _c_double_p, _c_double_p, _c_double_p, _c_double_p]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(_c_double_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# status codes (include/revgpu.h) -> reference exception class names
+ERROR_NAMES = {0: "", 1: "PostconditionMismatch", 2: "DirtyAncilla", 3: "RevDomainError",
+               4: "LoopIteratorMutated", 5: "RevError", 6: "FuelExhausted", 7: "KindError",
+               8: "IndexOutOfBounds", 9: "OverflowError"}
+
+
+def besselj_grad(nu, z, thr=1e-16, tol=1e-9, seed=1.0, max_trips=10**8, invcheck=True):
+    """Batch over z (each element independent): returns J, dJdz, fail, sum_trips."""
+    z = _f64(np.atleast_1d(z))
+    n = z.size
+    J = np.empty(n)
+    dz = np.empty(n)
+    fail = np.zeros(n, np.uint8)
+    total = lib().orc_besselj_grad_batch(
+        int(nu), _dp(z), n, thr, tol, seed, int(max_trips), int(bool(invcheck)), _dp(J),
+        _dp(dz), fail.ctypes.data_as(_c_u8_p))
+    return J, dz, fail, int(total)
+
+
+def ba_jac(cams, X, w, feats, obs, tol=1e-9, invcheck=True):
+    """Per-observation Jacobian rows: J (p, 31), err (p, 3), fail (p,)."""
+    cams, X, w, feats = _f64(cams), _f64(X), _f64(w), _f64(feats)
+    obs = np.ascontiguousarray(obs, dtype=np.int32)
+    p = w.size
+    J = np.empty((p, 31))
+    err = np.empty((p, 3))
+    fail = np.zeros(p, np.uint8)
+    lib().orc_ba_jac_batch(cams.shape[0], X.shape[0], p, _dp(cams), _dp(X), _dp(w),
+                           _dp(feats), obs.ctypes.data_as(_c_i32_p), tol, int(bool(invcheck)),
+                           _dp(err), _dp(J), fail.ctypes.data_as(_c_u8_p))
+    return J, err, fail
+
+
+def gmm_grad(alphas, means, icf, x, gamma, m, cst, tol=1e-9, invcheck=True):
+    """Returns (rc, err, g_alphas, g_means, g_icf)."""
+    alphas, means, icf, x = _f64(alphas), _f64(means), _f64(icf), _f64(x)
+    K, d = means.shape
+    N = x.shape[0]
+    err = ctypes.c_double(np.nan)
+    ga = np.zeros(K)
+    gm = np.zeros((K, d))
+    gi = np.zeros(icf.shape)
+    rc = lib().orc_gmm_grad(d, K, N, _dp(alphas), _dp(means), _dp(icf), _dp(x), float(gamma),
+                            int(m), float(cst), tol, int(bool(invcheck)), ctypes.byref(err),
+                            _dp(ga), _dp(gm), _dp(gi))
+    return rc, err.value, ga, gm, gi
