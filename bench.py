@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the reversible-AD gradient kernels on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bessel|ba|gmm|gmm_large]
+
+Default workload: BASELINE.json configs[1], the Bessel J_2 gradient over a
+batch of 2^26 inputs z ~ U(0.1, 10) (seed 1), sharded over the ranks
+(strong scaling: the 2^26 batch is fixed, each rank takes a contiguous
+slice; no collective on the data path).  A "step" = one fused forward +
+reverse-sweep kernel over the rank's slice, inputs resident in HBM
+(512 MiB > 126 MB L2, so no flush is needed between steps).
+
+Printed (rank 0, one JSON line): value = whole-job gradient evals/s from
+the device time (CUDA events, max over ranks); e2e = the same metric
+through the C-ABI host-buffer entry (pinned host z in, J/dJdz/fail out,
+copies inside the timed region); roofline of the dominant kernel against
+the in-run measured FP64 DFMA peak; cpu_baseline = the C oracle port
+(oracle/, the reference algorithm) on a bounded sample over all host
+threads; clocks sampled with nvidia-smi during the timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation
+(the oracle port — the reference itself is pure Python and cannot travel
+to the GPU box) on the same workload, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+THR = 1e-16
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["bessel", "ba", "gmm", "gmm_large"], default="bessel")
+    ap.add_argument("--n", type=int, default=None, help="override the batch size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# environment / distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Dist:
+    def __init__(self, backend):
+        import torch
+        import torch.distributed as dist
+        self.rank, self.world, self.local = dist_env()
+        self.dist = dist if self.world > 1 else None
+        self.torch = torch
+        if self.dist is not None:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend)
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, x):
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64,
+                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64,
+                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons every 200 ms while running."""
+
+    QUERY = ("index,uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid=None):
+        self.uuid = uuid
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+               "-lms", "200"]
+        if self.uuid:
+            cmd[1:1] = ["-i", self.uuid]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 10:
+                continue
+            try:
+                sm.append(float(parts[2]))
+                smax.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[6:10]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_weights():
+    p = os.path.join(REPO, "profiles", "fp64_weights.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return None
+
+
+def fp64_peak_tflops():
+    """In-run DFMA-bound microkernel (tools/fp64probe.cu): MEASURED_PEAKS.json
+    carries no FP64 figure and B200_PROFILING.md states no FP64 fallback."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(REPO, "tools", "libfp64probe.so"))
+    lib.probe_dfma_peak.restype = ctypes.c_double
+    lib.probe_dfma_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+    ms = ctypes.c_float(0)
+    best = 0.0
+    for _ in range(3):
+        best = max(best, lib.probe_dfma_peak(20000, ctypes.byref(ms)))
+    return best, float(ms.value)
+
+
+# ---------------------------------------------------------------------------
+# Bessel workload (configs[1])
+# ---------------------------------------------------------------------------
+
+BESSEL_N = 1 << 26
+BESSEL_NU = 2
+
+
+def bessel_flops(n, sum_trips, nu, w):
+    """Algorithmic FP64 flops of one launch (DESIGN.md §Bessel roofline):
+    per series trip  forward 3 add + exp + 1 add; reverse 1 add + 1 mul +
+    1 add + 3 add + 1 add + exp  -> 11 + 2 w_exp;
+    per element      log(z) + 5 + 2 nu + exp  (prologue) and
+                     12 + 3 nu + div (epilogue)."""
+    per_trip = 11 + 2 * w["exp"]
+    per_elem = w["log"] + w["exp"] + w["div"] + 17 + 5 * nu
+    return sum_trips * per_trip + n * per_elem
+
+
+def bessel_inputs(torch, n_total, rank, world, device):
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
+    g = torch.Generator(device=device)
+    g.manual_seed(1)
+    z = torch.empty(n_total, dtype=torch.float64, device=device)
+    z.uniform_(0.1, 10.0, generator=g)
+    return z[lo:hi].contiguous(), lo, hi
+
+
+def run_bessel_ours(args, D):
+    import torch
+
+    import paper_2003_04617_b200 as rg
+    from paper_2003_04617_b200 import kernels
+
+    dev = torch.device("cuda", D.local)
+    torch.cuda.set_device(dev)
+    n_total = args.n or BESSEL_N
+    z, lo, hi = bessel_inputs(torch, n_total, D.rank, D.world, dev)
+    n = z.numel()
+    J = torch.empty_like(z)
+    dz = torch.empty_like(z)
+    fail = torch.empty(n, dtype=torch.uint8, device=dev)
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    out = (J, dz, fail)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        kernels.besselj_grad(z, BESSEL_NU, out=out, counters=counters)
+    torch.cuda.synchronize()
+    counters.zero_()
+    props = torch.cuda.get_device_properties(dev)
+    sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
+    sampler.start()
+    time.sleep(0.25)
+    D.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        kernels.besselj_grad(z, BESSEL_NU, out=out, counters=counters)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = sampler.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    ms_step = D.max(ms_total / args.steps)
+    sum_trips = int(counters[0].item()) // args.steps
+    n_failed = int(counters[1].item()) // args.steps
+    value = n_total / (ms_step * 1e-3)
+
+    # parity spot check of this run's outputs against the oracle (rank 0 sample)
+    parity = None
+    if D.rank == 0:
+        parity = bessel_spot_parity(z, J, dz, fail)
+
+    # roofline of k_besselj_grad (the only kernel of the step)
+    w = load_weights()
+    peak, peak_ms = fp64_peak_tflops()
+    roof = None
+    if w is not None:
+        fl = D.sum(bessel_flops(n, sum_trips, BESSEL_NU, w))
+        achieved = fl / (ms_step * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(peak, 3),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": "in-run DFMA microkernel (tools/fp64probe.cu); no FP64 "
+                               "figure in MEASURED_PEAKS.json or B200_PROFILING.md",
+                "flops_per_launch": fl, "weights": w.get("source", "profiles/fp64_weights.json")}
+        tr = load_traffic("k_besselj_grad")
+        if tr:
+            roof["traffic"] = tr
+    e2e = None
+    if not args.no_e2e:
+        e2e = bessel_e2e(torch, z, args, D, n_total)
+    res = {
+        "metric": "gradient evals/sec", "value": round(value, 1), "unit": "grads/s",
+        "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic z ~ U(0.1, 10), seed 1",
+        "config": {"workload": "bessel_j2_grad_2^26", "n_total": n_total, "nu": BESSEL_NU,
+                   "thr": THR, "per_rank": n, "parallelism": f"shard{D.world}",
+                   "l2": "inputs 512 MiB > 126 MB L2; no flush"},
+        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
+        "clocks": clocks, "sum_trips_per_step": D.sum(sum_trips),
+        "failed_per_step": D.sum(n_failed), "parity_sample": parity,
+    }
+    return res
+
+
+def bessel_spot_parity(z, J, dz, fail, m=4096):
+    """The GPU outputs of the timed run vs the oracle on a strided sample."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    idx = np.linspace(0, z.numel() - 1, m).astype(np.int64)
+    zs = z.cpu().numpy()[idx]
+    Jo, dzo, fo, _ = O.besselj_grad(BESSEL_NU, zs)
+    Jg, dzg = J.cpu().numpy()[idx], dz.cpu().numpy()[idx]
+    fg = fail.cpu().numpy()[idx]
+    err = lambda a, b: float(np.max(np.abs(a - b) / (np.abs(b) + 1e-2)))  # noqa: E731
+    return {"n": m, "max_rel_J": err(Jg, Jo), "max_rel_dJdz": err(dzg, dzo),
+            "flags_equal": bool(np.array_equal(fg, fo))}
+
+
+def bessel_e2e(torch, z, args, D, n_total):
+    """Host buffers through the C-ABI `_host` entry: H2D + kernels + D2H."""
+    from paper_2003_04617_b200 import kernels
+    n = z.numel()
+    zh = z.cpu().pin_memory()
+    Jh = torch.empty(n, dtype=torch.float64).pin_memory()
+    dzh = torch.empty(n, dtype=torch.float64).pin_memory()
+    fh = torch.empty(n, dtype=torch.uint8).pin_memory()
+    outs = (Jh.numpy(), dzh.numpy(), fh.numpy())
+    zn = zh.numpy()
+    steps = max(2, min(args.steps, 5))
+    kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.local)
+    D.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.local)
+    dt = D.max((time.perf_counter() - t0) / steps)
+    return {"value": round(n_total / dt, 1), "unit": "grads/s", "h2d_bytes_per_step": 8 * n_total,
+            "d2h_bytes_per_step": 17 * n_total, "ms_per_step": round(dt * 1e3, 3),
+            "path": "rl_besselj_grad_f64_host (pinned host buffers, 3-stream pipeline)"}
+
+
+def bessel_cpu(target_s=10.0, n_max=1 << 22):
+    """The oracle port over all host threads on a bounded sample."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    rng = np.random.default_rng(1)
+    cores = os.cpu_count() or 1
+    n = 4096
+    while True:
+        z = rng.uniform(0.1, 10.0, n)
+        t0 = time.perf_counter()
+        O.besselj_grad(BESSEL_NU, z)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= n_max:
+            break
+        n = min(n_max, max(n * 2, int(n * target_s / max(dt, 1e-3))))
+    threads = int(os.environ.get("OMP_NUM_THREADS", cores))
+    return {"value": round(n / dt, 1), "unit": "grads/s", "cores": threads, "kind": "port",
+            "sample": f"{n} z ~ U(0.1,10) of the 2^26 workload, all 4 reference sweeps with "
+                      f"checks (oracle/revoracle.c), {dt:.2f} s"}
+
+
+def load_traffic(kernel):
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh).get(kernel)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        if args.workload != "bessel":
+            print(json.dumps({"impl": "reference", "unavailable":
+                              f"reference arm implemented for the bessel workload only"}))
+            return 0
+        base = bessel_cpu(target_s=max(3.0, min(20.0, 2.0 * args.steps)))
+        res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "grads/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(1e3 * (args.n or BESSEL_N) / base["value"], 3),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic z ~ U(0.1, 10), seed 1",
+               "config": {"workload": "bessel_j2_grad_2^26", "n_total": args.n or BESSEL_N,
+                          "nu": BESSEL_NU, "thr": THR},
+               "impl": "reference", "cpu_baseline": base,
+               "e2e": {"value": base["value"], "unit": "grads/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(res))
+        return 0
+
+    D = Dist("nccl")
+    if args.workload == "bessel":
+        res = run_bessel_ours(args, D)
+        if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = bessel_cpu()
+    else:
+        raise SystemExit(f"workload {args.workload} not wired yet")
+    if D.rank == 0:
+        print(json.dumps(res))
+    D.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -93,12 +93,14 @@ int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr,
  * obs: n_obs x 2 int32 (camera index, point index; 0-based).
  * J: n_obs x 31 = [de1/d(cam,X,w) (15), de2/d(cam,X,w) (15), d(1-w^2)/dw].
  * err (optional, may be NULL): n_obs x 3 = [e1, e2, 1 - w^2].
+ * Jfeat (optional, may be NULL): n_obs x 4 = [de1/df1, de1/df2, de2/df1,
+ * de2/df2], the feature columns of the reference's full jacobian().
  * Out-of-range indices set fail[i] = RL_ERR_INDEX (values.py:172-183).
  * ---------------------------------------------------------------------- */
 int rl_ba_jac_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
                   const double *X, const double *w, const double *feats, const int32_t *obs,
-                  double tol, int32_t invcheck, double *err, double *J, uint8_t *fail,
-                  unsigned long long *counters, void *stream);
+                  double tol, int32_t invcheck, double *err, double *J, double *Jfeat,
+                  uint8_t *fail, unsigned long long *counters, void *stream);
 
 int rl_ba_jac_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
                        const double *X, const double *w, const double *feats,

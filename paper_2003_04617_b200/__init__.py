@@ -1,0 +1,37 @@
+"""paper_2003_04617_b200 — B200-native reversible-AD gradient kernels.
+
+The data-parallel hot path of arXiv 2003.04617 (NiLang) as re-stated by the
+reference `revlang` package: forward run, uncompute and adjoint sweep of a
+reversible program, independently over a large batch, compiled to ONE
+sm_100a kernel per program with no tape (include/revgpu.h).
+
+Public surface (mirrors `revlang.__init__`, reference __init__.py:8-31, for
+the gradient path):
+  parse_program, load_example, Program, GradRequest, ExecOptions,
+  gradient, jacobian, the revlang error classes;
+plus the batched device API over torch CUDA tensors:
+  besselj_grad, ba_jacobian, gmm_grad (kernels.py) and the data-parallel
+  helpers in parallel.py.
+"""
+
+from .autodiff import ExecOptions, GradRequest, gradient, jacobian
+from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
+                     KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
+                     PostconditionMismatch, RevDomainError, RevError, RevLangError,
+                     UnknownExample, UnknownFunction, UnsupportedProgram)
+from .kernels import (BAResult, BesselResult, GMMResult, ba_jacobian, besselj_grad,
+                      besselj_grad_host, gmm_grad)
+from .programs import CATALOG, Program, entry_function, load_example, parse_program
+from .values import Array
+
+__all__ = [
+    "AliasedArguments", "Array", "BAResult", "BesselResult", "CATALOG", "DirtyAncilla",
+    "ExecOptions", "FuelExhausted", "GMMResult", "GradRequest", "IndexOutOfBounds",
+    "KindError", "LoopIteratorMutated", "MissingAdjoint", "NativeLibraryError",
+    "PostconditionMismatch", "Program", "RevDomainError", "RevError", "RevLangError",
+    "UnknownExample", "UnknownFunction", "UnsupportedProgram", "ba_jacobian", "besselj_grad",
+    "besselj_grad_host", "entry_function", "gmm_grad", "gradient", "jacobian",
+    "load_example", "parse_program",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,343 @@
+"""Drop-in `gradient` / `jacobian` (reference autodiff.py) executed on the GPU.
+
+`gradient(program, GradRequest(fname, args, seeds, wrt), opts)` has the
+reference's signature and return structure — (primal outputs, {param:
+cotangent structure}) with Int leaves -> None (autodiff.py:136-180) — but
+runs the registered program's fused forward + reverse-sweep kernel on
+`cuda:<current device>` instead of interpreting it.  Reversibility failures
+detected on device raise the reference's exception classes.
+
+Differences to the reference, all documented in DESIGN.md:
+  * only registered programs run (UnsupportedProgram otherwise; no CPU path);
+  * binary64 only (ExecOptions.float_dtype must be None), no tracing;
+  * seeds on input leaves are added to the returned cotangent (as the
+    reference's GVar initial value would be); several output seeds on BA
+    are combined linearly on the host;
+  * for gmm, the cotangents of the scratch arguments, x, ga and cst are not
+    produced (wrt=None reports err!, alphas, means, icf).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels
+from .errors import KindError, UnknownFunction, UnsupportedProgram, error_for_code
+from .programs import as_program
+from .values import like, to_numpy
+
+
+@dataclass
+class GradRequest:
+    fname: str
+    args: list
+    seeds: list = None   # (param_name, leaf_path, cotangent); default: first param's leaf
+    wrt: list = None     # parameter names to report (default: all the kernel provides)
+
+
+@dataclass
+class ExecOptions:
+    """Reference ExecOptions (interpreter.py:37-50).  invcheck and
+    float_tolerance drive the on-device checks; max_steps caps the series
+    loop; trace / float_dtype are not available on the device path."""
+    invcheck: bool = True
+    float_tolerance: float = 1e-9
+    max_steps: int = 500_000_000
+    trace: bool = False
+    gradient_mode: bool = False
+    float_dtype: object = None
+    trace_sink: object = None
+
+    def __post_init__(self):
+        if self.float_tolerance < 0:
+            raise ValueError("float_tolerance must be non-negative")
+        if self.max_steps <= 0:
+            raise ValueError("max_steps must be positive")
+
+
+def _check_opts(opts):
+    opts = opts or ExecOptions()
+    if opts.float_dtype is not None:
+        raise KindError("device kernels compute in binary64; float_dtype is not supported")
+    if opts.trace:
+        raise KindError("statement tracing is an interpreter feature; not available on device")
+    return opts
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise UnsupportedProgram("no CUDA device: the revgpu kernels have no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _is_int(v):
+    return isinstance(v, (int, np.integer)) and not isinstance(v, bool)
+
+
+def _is_float(v):
+    return isinstance(v, (float, np.floating))
+
+
+def _seed_map(seeds, names, default_name):
+    """{(param, path): value}, last one wins (reference _apply_seed)."""
+    if seeds is None:
+        return {(default_name, ()): 1.0}
+    out = {}
+    for pname, path, val in seeds:
+        if pname not in names:
+            raise KindError(f"seed names unknown parameter {pname!r}")
+        if isinstance(val, complex):
+            raise KindError("seed complex outputs per component (re/im paths)")
+        out[(pname, tuple(path))] = float(val)
+    return out
+
+
+def _report(wrt, names, available):
+    report = wrt if wrt is not None else [n for n in names if n in available]
+    for p in report:
+        if p not in names:
+            raise KindError(f"wrt names unknown parameter {p!r}")
+        if p not in available:
+            raise KindError(f"the device kernel does not produce the cotangent of {p!r}")
+    return report
+
+
+def _path_index(path, shape):
+    """1-based ('idx', (i, j)) path -> flat 0-based offset."""
+    if len(path) != 1 or path[0][0] != "idx":
+        raise KindError(f"unsupported leaf path {path!r}")
+    idx = path[0][1]
+    off = 0
+    for i, n in zip(idx, shape):
+        if not 1 <= i <= n:
+            raise KindError(f"seed index {i} out of bounds 1..{n}")
+        off = off * n + (i - 1)
+    return off
+
+
+# ---------------------------------------------------------------------------
+# besselj(out!, nu, z)
+# ---------------------------------------------------------------------------
+
+def _grad_besselj(fdef, req, opts):
+    names = fdef.param_names()
+    if len(req.args) != 3:
+        raise KindError(f"besselj takes 3 arguments, got {len(req.args)}")
+    out0, nu, z = req.args
+    if not _is_int(nu):
+        raise KindError("nu must be an Int")
+    if not (_is_float(out0) or _is_int(out0)) or not (_is_float(z) or _is_int(z)):
+        raise KindError("out! and z must be real scalars")
+    seeds = _seed_map(req.seeds, names, names[0])
+    out_seed, z_seed = 0.0, 0.0
+    for (p, path), v in seeds.items():
+        if path:
+            raise KindError("besselj arguments are scalars (empty leaf path)")
+        if p == names[0]:
+            out_seed = v
+        elif p == names[2] and _is_float(z):
+            z_seed = v
+        else:
+            raise KindError("seed target is not a differentiable leaf")
+    dev = _device()
+    zt = torch.tensor([float(z)], dtype=torch.float64, device=dev)
+    r = kernels.besselj_grad(zt, int(nu), seed=out_seed, thr=fdef.constants.get("thr", 1e-16),
+                             tol=opts.float_tolerance, invcheck=opts.invcheck,
+                             max_steps=opts.max_steps)
+    code = int(r.fail[0].item())
+    if code:
+        raise error_for_code(code, "besselj")
+    J = float(r.J[0].item())
+    primal_out = float(out0) + J
+    if not abs((primal_out - J) - float(out0)) <= opts.float_tolerance:
+        raise error_for_code(5, "besselj")
+    grads_all = {names[0]: out_seed, names[1]: None,
+                 names[2]: (z_seed + float(r.dJdz[0].item())) if _is_float(z) else None}
+    report = _report(req.wrt, names, grads_all)
+    return [primal_out, nu, z], {p: grads_all[p] for p in report}
+
+
+# ---------------------------------------------------------------------------
+# ba_proj(e1!, e2!, cam, X, w, f1, f2) and ba_weight(e!, w)
+# ---------------------------------------------------------------------------
+
+def _ba_device_call(cam, X, w, f1, f2, opts):
+    dev = _device()
+    t = lambda a: torch.as_tensor(np.asarray(a, np.float64), device=dev)  # noqa: E731
+    r = kernels.ba_jacobian(t(cam.reshape(1, 11)), t(X.reshape(1, 3)), t([w]), t([[f1, f2]]),
+                            torch.zeros((1, 2), dtype=torch.int32, device=dev),
+                            tol=opts.float_tolerance, invcheck=opts.invcheck, want_err=True,
+                            want_feat=True)
+    code = int(r.fail[0].item())
+    if code:
+        raise error_for_code(code, "ba_proj")
+    return (r.J[0].cpu().numpy(), r.err[0].cpu().numpy(), r.Jfeat[0].cpu().numpy())
+
+
+def _grad_ba_proj(fdef, req, opts):
+    names = fdef.param_names()
+    if len(req.args) != 7:
+        raise KindError(f"ba_proj takes 7 arguments, got {len(req.args)}")
+    e1, e2, cam, X, w, f1, f2 = req.args
+    camv = to_numpy(cam, "cam", 1)
+    Xv = to_numpy(X, "X", 1)
+    if camv.shape != (11,) or Xv.shape != (3,):
+        raise KindError("cam must have 11 entries and X 3")
+    J, err, Jf = _ba_device_call(camv, Xv, float(w), float(f1), float(f2), opts)
+    seeds = _seed_map(req.seeds, names, names[0])
+    a = seeds.get((names[0], ()), 0.0)
+    b = seeds.get((names[1], ()), 0.0)
+    g15 = a * J[0:15] + b * J[15:30]
+    gcam, gX, gw = g15[0:11].copy(), g15[11:14].copy(), float(g15[14])
+    gf1 = a * Jf[0] + b * Jf[2]
+    gf2 = a * Jf[1] + b * Jf[3]
+    for (p, path), v in seeds.items():
+        if p in (names[0], names[1]):
+            continue
+        if p == names[2]:
+            gcam[_path_index(path, (11,))] += v
+        elif p == names[3]:
+            gX[_path_index(path, (3,))] += v
+        elif p == names[4]:
+            gw += v
+        elif p == names[5]:
+            gf1 += v
+        elif p == names[6]:
+            gf2 += v
+    grads_all = {names[0]: a, names[1]: b, names[2]: like(cam, gcam), names[3]: like(X, gX),
+                 names[4]: gw, names[5]: gf1, names[6]: gf2}
+    report = _report(req.wrt, names, grads_all)
+    primal = [float(e1) + err[0], float(e2) + err[1], cam, X, w, f1, f2]
+    return primal, {p: grads_all[p] for p in report}
+
+
+def _grad_ba_weight(fdef, req, opts):
+    names = fdef.param_names()
+    if len(req.args) != 2:
+        raise KindError(f"ba_weight takes 2 arguments, got {len(req.args)}")
+    e0, w = req.args
+    cam = np.zeros(11)
+    cam[6] = 1.0
+    J, err, _ = _ba_device_call(cam, np.array([0.0, 0.0, 1.0]), float(w), 0.0, 0.0, opts)
+    seeds = _seed_map(req.seeds, names, names[0])
+    a = seeds.get((names[0], ()), 0.0)
+    gw = a * J[30] + seeds.get((names[1], ()), 0.0)
+    grads_all = {names[0]: a, names[1]: gw}
+    report = _report(req.wrt, names, grads_all)
+    return [float(e0) + err[2], w], {p: grads_all[p] for p in report}
+
+
+# ---------------------------------------------------------------------------
+# gmm(err!, alphas, means, icf, x, qd!, sq!, xc!, qxc!, mt!, dm!, ga, wm, cst)
+# ---------------------------------------------------------------------------
+
+def _grad_gmm(fdef, req, opts):
+    names = fdef.param_names()
+    if len(req.args) != 14:
+        raise KindError(f"gmm takes 14 arguments, got {len(req.args)}")
+    err0, alphas, means, icf, x = req.args[:5]
+    scratch = req.args[5:11]
+    ga, wm, cst = req.args[11:14]
+    al = to_numpy(alphas, "alphas", 1)
+    mu = to_numpy(means, "means", 2)
+    ic = to_numpy(icf, "icf", 2)
+    xv = to_numpy(x, "x", 2)
+    K, d = mu.shape
+    for nm, s in zip(names[5:11], scratch):
+        sv = to_numpy(s, nm)
+        if np.any(sv != 0.0):
+            raise KindError(f"scratch argument {nm!r} must be zero on entry")
+    if not _is_int(wm):
+        raise KindError("wm must be an Int")
+    seeds = _seed_map(req.seeds, names, names[0])
+    a = 0.0
+    for (p, path), v in seeds.items():
+        if p == names[0] and not path:
+            a = v
+        else:
+            raise KindError("only the err! output can be seeded on the device path")
+    dev = _device()
+    t = lambda v: torch.as_tensor(v, device=dev)  # noqa: E731
+    r = kernels.gmm_grad(t(al), t(mu), t(ic), t(xv), float(ga), int(wm), float(cst),
+                         tol=opts.float_tolerance, invcheck=opts.invcheck)
+    fails = r.fail.cpu().numpy()
+    if fails.any():
+        raise error_for_code(int(fails[np.nonzero(fails)[0][0]]), "gmm")
+    E = float(r.err.item())
+    grads_all = {names[0]: a,
+                 names[1]: like(alphas, a * r.g_alphas.cpu().numpy()),
+                 names[2]: like(means, a * r.g_means.cpu().numpy()),
+                 names[3]: like(icf, a * r.g_icf.cpu().numpy())}
+    report = _report(req.wrt, names, grads_all)
+    primal = [float(err0) + E] + list(req.args[1:])
+    return primal, {p: grads_all[p] for p in report}
+
+
+_HANDLERS = {"besselj": _grad_besselj, "ba_proj": _grad_ba_proj,
+             "ba_weight": _grad_ba_weight, "gmm": _grad_gmm}
+
+
+def _resolve(program, fname):
+    prog = as_program(program)
+    fdef = prog.functions.get(fname)
+    if fdef is None:
+        raise UnknownFunction(f"no function named {fname!r}")
+    if fdef.kernel is None or fdef.kernel.handler not in _HANDLERS:
+        raise UnsupportedProgram(
+            f"function {fname!r} has no registered device kernel (registered: "
+            "besselj, ba_proj, ba_weight, gmm); there is no CPU fallback")
+    return fdef
+
+
+def gradient(program, req, opts=None):
+    """Reference `gradient` (autodiff.py:136) on the device."""
+    opts = _check_opts(opts)
+    fdef = _resolve(program, req.fname)
+    return _HANDLERS[fdef.kernel.handler](fdef, req, opts)
+
+
+def _leaves(v):
+    """Number of differentiable leaves (None for Int)."""
+    if _is_int(v) or isinstance(v, bool):
+        return 0
+    if _is_float(v):
+        return 1
+    return int(np.asarray(to_numpy(v, "arg")).size)
+
+
+def _flat(g, v):
+    if _is_int(v) or isinstance(v, bool):
+        return []
+    if g is None:
+        return [0.0] * _leaves(v)
+    if _is_float(v):
+        return [float(g)]
+    return list(to_numpy(g, "grad").ravel())
+
+
+def jacobian(program, fname, args, opts=None):
+    """Reference `jacobian` (autodiff.py:197-213): one gradient per
+    differentiable leaf of every argument; rows x columns over all leaves."""
+    opts = _check_opts(opts)
+    fdef = _resolve(program, fname)
+    if fdef.kernel.handler == "gmm":
+        raise KindError("the full gmm jacobian (over x and scratch) is not produced on device")
+    names = fdef.param_names()
+    rows = []
+    for pi, pname in enumerate(names):
+        v = args[pi]
+        n = _leaves(v)
+        for li in range(n):
+            if _is_float(v):
+                path = ()
+            else:
+                shape = to_numpy(v, pname).shape
+                path = (("idx", tuple(int(i) + 1 for i in np.unravel_index(li, shape))),)
+            _, grads = gradient(program, GradRequest(fname, args, seeds=[(pname, path, 1.0)],
+                                                     wrt=None), opts)
+            row = []
+            for pj, nj in enumerate(names):
+                row += _flat(grads.get(nj), args[pj])
+            rows.append(row)
+    return np.array(rows, dtype=float)

@@ -1,0 +1,356 @@
+// capi.cu — the extern "C" boundary (include/revgpu.h): status strings,
+// error plumbing, per-device table upload, the device-pointer entry points
+// and the host-buffer (`_host`) entry points that pipeline chunks of
+// host->device copy, kernel and device->host copy over three streams.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rl {
+
+// kernels (besselj.cu, ba.cu, gmm.cu)
+int besselj_tables_init();
+int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double tol, double seed,
+                   int64_t max_trips, int32_t invcheck, double *J, double *dJdz, uint8_t *fail,
+                   unsigned long long *counters, cudaStream_t st);
+int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, const double *X,
+              const double *w, const double *feats, const int32_t *obs, double tol,
+              int32_t invcheck, double *err, double *J, double *Jfeat, uint8_t *fail,
+              unsigned long long *counters, cudaStream_t st);
+size_t gmm_workspace_bytes(int32_t d, int32_t K, int64_t N);
+int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
+               const double *means, const double *icf, const double *x, double gamma, int32_t m,
+               double cst, double tol, int32_t invcheck, int32_t add_param_terms, double *out,
+               uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
+               cudaStream_t st);
+
+static thread_local char g_last_error[512];
+
+int set_error(int code, const char *msg) {
+  snprintf(g_last_error, sizeof g_last_error, "%s", msg);
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+  if (e == cudaSuccess) return RL_OK;
+  snprintf(g_last_error, sizeof g_last_error, "%s: %s (%s)", where, cudaGetErrorString(e),
+           cudaGetErrorName(e));
+  return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? RL_ERR_NO_DEVICE
+                                                                     : RL_ERR_CUDA;
+}
+
+constexpr int MAX_DEV = 64;
+
+int ensure_device_tables() {
+  static std::once_flag once[MAX_DEV];
+  static int status[MAX_DEV];
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc) return rc;
+  if (dev < 0 || dev >= MAX_DEV) return set_error(RL_ERR_INVALID, "device ordinal out of range");
+  std::call_once(once[dev], [dev] {
+    cudaDeviceProp prop;
+    int r = cuda_status(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    if (!r && prop.major != 10)
+      r = set_error(RL_ERR_NO_DEVICE, "revgpu is built for sm_100a (B200); device is not cc 10.x");
+    if (!r) r = besselj_tables_init();
+    status[dev] = r;
+  });
+  return status[dev];
+}
+
+int sm_count() {
+  static int cache[MAX_DEV];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= MAX_DEV) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline: chunk i's H2D, kernel and D2H are issued on stream
+// i % NS; device buffers come from the stream-ordered pool allocator.
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void *p = nullptr;
+  cudaStream_t st = nullptr;
+  int alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    return cuda_status(cudaMallocAsync(&p, bytes ? bytes : 1, s), "cudaMallocAsync");
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+struct Pipeline {
+  static constexpr int NS = 3;
+  cudaStream_t st[NS] = {nullptr, nullptr, nullptr};
+  int dev_prev = -1;
+  int init(int device) {
+    cudaGetDevice(&dev_prev);
+    int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+    if (rc) return rc;
+    for (auto &s : st) {
+      rc = cuda_status(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+      if (rc) return rc;
+    }
+    return RL_OK;
+  }
+  int finish() {
+    int rc = RL_OK;
+    for (auto &s : st)
+      if (s) {
+        int r = cuda_status(cudaStreamSynchronize(s), "pipeline sync");
+        if (!rc) rc = r;
+      }
+    return rc;
+  }
+  ~Pipeline() {
+    for (auto &s : st)
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    if (dev_prev >= 0) cudaSetDevice(dev_prev);
+  }
+};
+
+}  // namespace rl
+
+using namespace rl;
+
+extern "C" {
+
+int rl_abi_version(void) { return RL_ABI_VERSION; }
+
+const char *rl_strerror(int code) {
+  switch (code) {
+    case RL_OK: return "ok";
+    case RL_ERR_POSTCONDITION: return "PostconditionMismatch";
+    case RL_ERR_DIRTY_ANCILLA: return "DirtyAncilla";
+    case RL_ERR_DOMAIN: return "RevDomainError";
+    case RL_ERR_ITERATOR: return "LoopIteratorMutated";
+    case RL_ERR_RESTORE: return "RevError";
+    case RL_ERR_FUEL: return "FuelExhausted";
+    case RL_ERR_KIND: return "KindError";
+    case RL_ERR_INDEX: return "IndexOutOfBounds";
+    case RL_ERR_OVERFLOW: return "OverflowError";
+    case RL_ERR_INVALID: return "invalid argument";
+    case RL_ERR_CUDA: return "CUDA error";
+    case RL_ERR_NO_DEVICE: return "no usable sm_100 device";
+    default: return "unknown status";
+  }
+}
+
+const char *rl_last_error(void) { return g_last_error; }
+
+int rl_besselj_grad_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, uint8_t *fail, unsigned long long *counters,
+                        void *stream) {
+  return launch_besselj(nu, z, n, thr, tol, seed, max_trips, invcheck, J, dJdz, fail, counters,
+                        as_stream(stream));
+}
+
+int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                             double seed, int64_t max_trips, int32_t invcheck, double *J,
+                             double *dJdz, uint8_t *fail, unsigned long long *sum_trips,
+                             unsigned long long *n_failed, int32_t device) {
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_besselj_grad_f64_host: bad argument");
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  const int64_t CH = int64_t(1) << 22;  // 4 Mi elements = 32 MiB of z per chunk
+  const int64_t nch = (n + CH - 1) / CH;
+  const int64_t bufn = std::min<int64_t>(CH, std::max<int64_t>(n, 1));
+  DevBuf dz[Pipeline::NS], dJ[Pipeline::NS], dg[Pipeline::NS], df[Pipeline::NS], dc;
+  for (int s = 0; s < Pipeline::NS && s < std::max<int64_t>(nch, 1); s++) {
+    if ((rc = dz[s].alloc(bufn * 8, pl.st[s])) || (rc = dJ[s].alloc(bufn * 8, pl.st[s])) ||
+        (rc = dg[s].alloc(bufn * 8, pl.st[s])) || (rc = df[s].alloc(bufn, pl.st[s])))
+      return rc;
+  }
+  if ((rc = dc.alloc(2 * sizeof(unsigned long long) * Pipeline::NS, pl.st[0]))) return rc;
+  auto *cnt = (unsigned long long *)dc.p;
+  if ((rc = cuda_status(cudaMemsetAsync(cnt, 0, 2 * 8 * Pipeline::NS, pl.st[0]), "memset")))
+    return rc;
+  if ((rc = pl.finish())) return rc;  // counters zeroed before any stream uses them
+  for (int64_t c = 0; c < nch; c++) {
+    const int s = (int)(c % Pipeline::NS);
+    const int64_t off = c * CH, m = std::min(CH, n - off);
+    cudaStream_t st = pl.st[s];
+    if ((rc = cuda_status(cudaMemcpyAsync(dz[s].p, z + off, m * 8, cudaMemcpyHostToDevice, st),
+                          "H2D z")))
+      return rc;
+    if ((rc = launch_besselj(nu, (double *)dz[s].p, m, thr, tol, seed, max_trips, invcheck,
+                             (double *)dJ[s].p, (double *)dg[s].p, (uint8_t *)df[s].p,
+                             cnt + 2 * s, st)))
+      return rc;
+    if ((rc = cuda_status(cudaMemcpyAsync(J + off, dJ[s].p, m * 8, cudaMemcpyDeviceToHost, st),
+                          "D2H J")) ||
+        (rc = cuda_status(cudaMemcpyAsync(dJdz + off, dg[s].p, m * 8, cudaMemcpyDeviceToHost, st),
+                          "D2H dJdz")) ||
+        (rc = cuda_status(cudaMemcpyAsync(fail + off, df[s].p, m, cudaMemcpyDeviceToHost, st),
+                          "D2H fail")))
+      return rc;
+  }
+  if ((rc = pl.finish())) return rc;
+  unsigned long long h[2 * Pipeline::NS];
+  if ((rc = cuda_status(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost), "D2H counters")))
+    return rc;
+  unsigned long long tr = 0, nf = 0;
+  for (int s = 0; s < Pipeline::NS; s++) {
+    tr += h[2 * s];
+    nf += h[2 * s + 1];
+  }
+  if (sum_trips) *sum_trips = tr;
+  if (n_failed) *n_failed = nf;
+  return RL_OK;
+}
+
+int rl_ba_jac_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                  const double *X, const double *w, const double *feats, const int32_t *obs,
+                  double tol, int32_t invcheck, double *err, double *J, double *Jfeat,
+                  uint8_t *fail, unsigned long long *counters, void *stream) {
+  return launch_ba(n_cams, n_pts, n_obs, cams, X, w, feats, obs, tol, invcheck, err, J, Jfeat,
+                   fail, counters, as_stream(stream));
+}
+
+int rl_ba_jac_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                       const double *X, const double *w, const double *feats,
+                       const int32_t *obs, double tol, int32_t invcheck, double *err,
+                       double *J, uint8_t *fail, unsigned long long *n_failed, int32_t device) {
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 ||
+      (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !J || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_ba_jac_f64_host: bad argument");
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  // cameras and points are replicated once; observations stream in chunks
+  DevBuf dcam, dX, dc;
+  if ((rc = dcam.alloc((size_t)n_cams * 11 * 8, pl.st[0])) ||
+      (rc = dX.alloc((size_t)n_pts * 3 * 8, pl.st[0])) ||
+      (rc = dc.alloc(2 * 8 * Pipeline::NS, pl.st[0])))
+    return rc;
+  auto *cnt = (unsigned long long *)dc.p;
+  if ((rc = cuda_status(cudaMemcpyAsync(dcam.p, cams, (size_t)n_cams * 88, cudaMemcpyHostToDevice,
+                                        pl.st[0]), "H2D cams")) ||
+      (rc = cuda_status(cudaMemcpyAsync(dX.p, X, (size_t)n_pts * 24, cudaMemcpyHostToDevice,
+                                        pl.st[0]), "H2D X")) ||
+      (rc = cuda_status(cudaMemsetAsync(cnt, 0, 2 * 8 * Pipeline::NS, pl.st[0]), "memset")))
+    return rc;
+  if ((rc = pl.finish())) return rc;
+  const int64_t CH = int64_t(1) << 18;
+  const int64_t nch = (n_obs + CH - 1) / CH;
+  const int64_t bufn = std::min<int64_t>(CH, std::max<int64_t>(n_obs, 1));
+  DevBuf dw[Pipeline::NS], df2[Pipeline::NS], dob[Pipeline::NS], dJ[Pipeline::NS],
+      de[Pipeline::NS], dfl[Pipeline::NS];
+  for (int s = 0; s < Pipeline::NS && s < std::max<int64_t>(nch, 1); s++) {
+    if ((rc = dw[s].alloc(bufn * 8, pl.st[s])) || (rc = df2[s].alloc(bufn * 16, pl.st[s])) ||
+        (rc = dob[s].alloc(bufn * 8, pl.st[s])) || (rc = dJ[s].alloc(bufn * 31 * 8, pl.st[s])) ||
+        (rc = de[s].alloc(err ? bufn * 24 : 8, pl.st[s])) || (rc = dfl[s].alloc(bufn, pl.st[s])))
+      return rc;
+  }
+  for (int64_t c = 0; c < nch; c++) {
+    const int s = (int)(c % Pipeline::NS);
+    const int64_t off = c * CH, m = std::min(CH, n_obs - off);
+    cudaStream_t st = pl.st[s];
+    if ((rc = cuda_status(cudaMemcpyAsync(dw[s].p, w + off, m * 8, cudaMemcpyHostToDevice, st),
+                          "H2D w")) ||
+        (rc = cuda_status(cudaMemcpyAsync(df2[s].p, feats + 2 * off, m * 16,
+                                          cudaMemcpyHostToDevice, st), "H2D feats")) ||
+        (rc = cuda_status(cudaMemcpyAsync(dob[s].p, obs + 2 * off, m * 8, cudaMemcpyHostToDevice,
+                                          st), "H2D obs")))
+      return rc;
+    if ((rc = launch_ba(n_cams, n_pts, m, (double *)dcam.p, (double *)dX.p, (double *)dw[s].p,
+                        (double *)df2[s].p, (int32_t *)dob[s].p, tol, invcheck,
+                        err ? (double *)de[s].p : nullptr, (double *)dJ[s].p, nullptr,
+                        (uint8_t *)dfl[s].p, cnt + 2 * s, st)))
+      return rc;
+    if ((rc = cuda_status(cudaMemcpyAsync(J + 31 * off, dJ[s].p, m * 31 * 8,
+                                          cudaMemcpyDeviceToHost, st), "D2H J")) ||
+        (rc = cuda_status(cudaMemcpyAsync(fail + off, dfl[s].p, m, cudaMemcpyDeviceToHost, st),
+                          "D2H fail")))
+      return rc;
+    if (err && (rc = cuda_status(cudaMemcpyAsync(err + 3 * off, de[s].p, m * 24,
+                                                 cudaMemcpyDeviceToHost, st), "D2H err")))
+      return rc;
+  }
+  if ((rc = pl.finish())) return rc;
+  unsigned long long h[2 * Pipeline::NS];
+  if ((rc = cuda_status(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost), "D2H counters")))
+    return rc;
+  unsigned long long nf = 0;
+  for (int s = 0; s < Pipeline::NS; s++) nf += h[2 * s + 1];
+  if (n_failed) *n_failed = nf;
+  return RL_OK;
+}
+
+size_t rl_gmm_workspace_bytes(int32_t d, int32_t K, int64_t N) {
+  return gmm_workspace_bytes(d, K, N);
+}
+
+int rl_gmm_grad_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
+                    const double *means, const double *icf, const double *x, double gamma,
+                    int32_t m, double cst, double tol, int32_t invcheck,
+                    int32_t add_param_terms, double *out, uint8_t *fail,
+                    unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
+  return launch_gmm(d, K, N, N_total, alphas, means, icf, x, gamma, m, cst, tol, invcheck,
+                    add_param_terms, out, fail, counters, ws, ws_bytes, as_stream(stream));
+}
+
+int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                         const double *means, const double *icf, const double *x, double gamma,
+                         int32_t m, double cst, double tol, int32_t invcheck, double *out,
+                         unsigned long long *n_failed, int32_t device) {
+  if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || (N > 0 && !x) || !out)
+    return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64_host: bad argument");
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  cudaStream_t st = pl.st[0];
+  const size_t P = (size_t)d * (d + 1) / 2;
+  const size_t nout = 1 + K + (size_t)K * d + (size_t)K * P;
+  const size_t wsb = gmm_workspace_bytes(d, K, N);
+  DevBuf da, dm, di, dx, dout, dfl, dws, dc;
+  if ((rc = da.alloc(K * 8, st)) || (rc = dm.alloc((size_t)K * d * 8, st)) ||
+      (rc = di.alloc((size_t)K * P * 8, st)) || (rc = dx.alloc((size_t)N * d * 8, st)) ||
+      (rc = dout.alloc(nout * 8, st)) || (rc = dfl.alloc(N, st)) || (rc = dws.alloc(wsb, st)) ||
+      (rc = dc.alloc(16, st)))
+    return rc;
+  if ((rc = cuda_status(cudaMemcpyAsync(da.p, alphas, K * 8, cudaMemcpyHostToDevice, st), "H2D")) ||
+      (rc = cuda_status(cudaMemcpyAsync(dm.p, means, (size_t)K * d * 8, cudaMemcpyHostToDevice, st),
+                        "H2D")) ||
+      (rc = cuda_status(cudaMemcpyAsync(di.p, icf, (size_t)K * P * 8, cudaMemcpyHostToDevice, st),
+                        "H2D")) ||
+      (rc = cuda_status(cudaMemcpyAsync(dx.p, x, (size_t)N * d * 8, cudaMemcpyHostToDevice, st),
+                        "H2D")) ||
+      (rc = cuda_status(cudaMemsetAsync(dc.p, 0, 16, st), "memset")))
+    return rc;
+  if ((rc = launch_gmm(d, K, N, N, (double *)da.p, (double *)dm.p, (double *)di.p,
+                       (double *)dx.p, gamma, m, cst, tol, invcheck, 1, (double *)dout.p,
+                       (uint8_t *)dfl.p, (unsigned long long *)dc.p, dws.p, wsb, st)))
+    return rc;
+  unsigned long long h[2];
+  if ((rc = cuda_status(cudaMemcpyAsync(out, dout.p, nout * 8, cudaMemcpyDeviceToHost, st),
+                        "D2H out")) ||
+      (rc = cuda_status(cudaMemcpyAsync(h, dc.p, 16, cudaMemcpyDeviceToHost, st), "D2H counters")))
+    return rc;
+  if ((rc = pl.finish())) return rc;
+  if (n_failed) *n_failed = h[1];
+  return RL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// common.cuh — shared device/host helpers for the revgpu kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/revgpu.h"
+
+namespace rl {
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+// Host-computed natural-log table log(i), i in [0, LOGTAB_N), filled from the
+// host C library (bit-identical to CPython's math.log, which the reference's
+// s_log calls: values.py:365-372).  Integer logs are the whole transcendental
+// cost of the series' integer divisions (`s /= k`, `s /= kn`).
+constexpr int LOGTAB_N = 4096;
+
+// Record a CUDA error for rl_last_error() and map it to RL_ERR_CUDA.
+int cuda_status(cudaError_t e, const char *where);
+int set_error(int code, const char *msg);
+
+// Upload constant tables for the current device (idempotent, thread-safe).
+int ensure_device_tables();
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+
+// Block-wide sum of two counters and one atomicAdd per block.
+template <int BLOCK>
+__device__ __forceinline__ void block_add_counters(unsigned long long a, unsigned long long b,
+                                                   unsigned long long *counters) {
+  __shared__ unsigned long long red[2][BLOCK / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(FULL_MASK, a, o);
+    b += __shfl_down_sync(FULL_MASK, b, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sa = 0, sb = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; w++) {
+      sa += red[0][w];
+      sb += red[1][w];
+    }
+    if (counters) {
+      if (sa) atomicAdd(&counters[0], sa);
+      if (sb) atomicAdd(&counters[1], sb);
+    }
+  }
+}
+
+}  // namespace rl

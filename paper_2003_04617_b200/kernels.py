@@ -1,0 +1,229 @@
+"""Batched device entry points over torch CUDA tensors.
+
+Each function launches ONE fused forward + reverse-sweep kernel of
+librevgpu.so on the current torch stream (no synchronisation) and returns
+device tensors.  These are the batched counterparts of the reference's
+per-call `gradient` (autodiff.py:136-180): element i of every output equals
+what `gradient(program, GradRequest(fname, args_i))` returns for the i-th
+input, within the tolerance stated in DESIGN.md, and `fail[i]` carries the
+revlang error class the reference would raise for it (include/revgpu.h).
+
+torch is used for device memory and streams only; the arithmetic is in the
+CUDA kernels.  No CPU path exists: non-CUDA inputs raise.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from .errors import KindError
+
+F64 = torch.float64
+# ExecOptions.max_steps (reference interpreter.py:40) -> series-term cap.
+# One series term costs ~12 statement ticks in each of the 4 reference
+# sweeps; the cap is the corresponding trip count.
+TICKS_PER_TRIP = 48
+
+
+def _stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _require_cuda(name, t, dtype=F64, ndim=None, last=None):
+    if not isinstance(t, torch.Tensor):
+        raise KindError(f"{name} must be a torch tensor on a CUDA device")
+    if not t.is_cuda:
+        raise KindError(f"{name} must live on a CUDA device (no CPU path exists)")
+    if t.dtype != dtype:
+        raise KindError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise KindError(f"{name} must have {ndim} dimensions, got shape {tuple(t.shape)}")
+    if last is not None and t.shape[-1] != last:
+        raise KindError(f"{name} must have trailing dimension {last}, got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+@dataclass
+class BesselResult:
+    J: torch.Tensor          # primal out! per element
+    dJdz: torch.Tensor       # z cotangent (out!.g = seed)
+    fail: torch.Tensor       # uint8 status per element (0 = ok)
+    counters: torch.Tensor   # int64[2] device: [sum of series trips, failed elements]
+
+    @property
+    def sum_trips(self):
+        return int(self.counters[0].item())
+
+    @property
+    def n_failed(self):
+        return int(self.counters[1].item())
+
+
+def besselj_grad(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
+                 max_steps=500_000_000, out=None, counters=None):
+    """J_nu(z) and dJ/dz for every element of z (CUDA float64) in one kernel.
+
+    Batched `gradient(load_example("besselj"), GradRequest("besselj",
+    [0.0, nu, z_i]))`.  `out` = (J, dJdz, fail) preallocated tensors, and
+    `counters` an int64[2] device tensor accumulated in place (not reset),
+    let a caller avoid allocation (e.g. under CUDA-graph capture)."""
+    z = _require_cuda("z", z)
+    n = z.numel()
+    if out is None:
+        J = torch.empty_like(z)
+        dz = torch.empty_like(z)
+        fail = torch.empty(z.shape, dtype=torch.uint8, device=z.device)
+    else:
+        J, dz, fail = out
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=z.device)
+    L = _native.lib()
+    rc = L.rl_besselj_grad_f64(int(nu), _ptr(z), n, float(thr), float(tol), float(seed),
+                               max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)),
+                               _ptr(J), _ptr(dz), _ptr(fail), _ptr(counters), _stream_handle())
+    _native.check(rc, "rl_besselj_grad_f64")
+    return BesselResult(J, dz, fail, counters)
+
+
+def besselj_grad_host(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
+                      max_steps=500_000_000, device=None, out=None):
+    """Host-buffer entry (numpy float64 or CPU tensor in, numpy out): the
+    C-ABI `_host` call pipelines the copies with the kernel.  Synchronous."""
+    import numpy as np
+
+    zh = np.ascontiguousarray(z.numpy() if isinstance(z, torch.Tensor) else z, dtype=np.float64)
+    n = zh.size
+    if out is None:
+        J = np.empty(n)
+        dz = np.empty(n)
+        fail = np.empty(n, np.uint8)
+    else:
+        J, dz, fail = out
+    trips = ctypes.c_ulonglong(0)
+    nfail = ctypes.c_ulonglong(0)
+    dev = torch.cuda.current_device() if device is None else int(device)
+    L = _native.lib()
+    rc = L.rl_besselj_grad_f64_host(int(nu), zh.ctypes.data, n, float(thr), float(tol),
+                                    float(seed), max(1, int(max_steps) // TICKS_PER_TRIP),
+                                    int(bool(invcheck)), J.ctypes.data, dz.ctypes.data,
+                                    fail.ctypes.data, ctypes.byref(trips), ctypes.byref(nfail),
+                                    dev)
+    _native.check(rc, "rl_besselj_grad_f64_host")
+    return J, dz, fail, int(trips.value), int(nfail.value)
+
+
+@dataclass
+class BAResult:
+    J: torch.Tensor          # (p, 31): [de1/d(cam,X,w), de2/d(cam,X,w), d(1-w^2)/dw]
+    err: torch.Tensor        # (p, 3) residuals [e1, e2, 1 - w^2] or None
+    Jfeat: torch.Tensor      # (p, 4) feature columns or None
+    fail: torch.Tensor
+    counters: torch.Tensor
+
+    @property
+    def n_failed(self):
+        return int(self.counters[1].item())
+
+
+def ba_jacobian(cams, X, w, feats, obs, *, tol=1e-9, invcheck=True, want_err=True,
+                want_feat=False, out=None, counters=None):
+    """ADBench BA reprojection Jacobian blocks for every observation.
+
+    Batched 2x `gradient(load_example("ba_proj"), GradRequest("ba_proj",
+    [0, 0, cams[c_i], X[p_i], w_i, f_i1, f_i2], seeds=[e1!|e2!], wrt=[cam, X, w]))`
+    plus `gradient(.., "ba_weight", [0, w_i])`; obs[i] = (c_i, p_i), 0-based."""
+    cams = _require_cuda("cams", cams, ndim=2, last=11)
+    X = _require_cuda("X", X, ndim=2, last=3)
+    w = _require_cuda("w", w, ndim=1)
+    feats = _require_cuda("feats", feats, ndim=2, last=2)
+    obs = _require_cuda("obs", obs, dtype=torch.int32, ndim=2, last=2)
+    p = w.shape[0]
+    if feats.shape[0] != p or obs.shape[0] != p:
+        raise KindError("w, feats and obs must have the same number of observations")
+    dev = w.device
+    if out is None:
+        J = torch.empty((p, 31), dtype=F64, device=dev)
+        err = torch.empty((p, 3), dtype=F64, device=dev) if want_err else None
+        Jf = torch.empty((p, 4), dtype=F64, device=dev) if want_feat else None
+        fail = torch.empty(p, dtype=torch.uint8, device=dev)
+    else:
+        J, err, Jf, fail = out
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    L = _native.lib()
+    rc = L.rl_ba_jac_f64(cams.shape[0], X.shape[0], p, _ptr(cams), _ptr(X), _ptr(w), _ptr(feats),
+                         _ptr(obs), float(tol), int(bool(invcheck)), _ptr(err), _ptr(J), _ptr(Jf),
+                         _ptr(fail), _ptr(counters), _stream_handle())
+    _native.check(rc, "rl_ba_jac_f64")
+    return BAResult(J, err, Jf, fail, counters)
+
+
+@dataclass
+class GMMResult:
+    err: torch.Tensor        # () objective
+    g_alphas: torch.Tensor   # (K,)
+    g_means: torch.Tensor    # (K, d)
+    g_icf: torch.Tensor      # (K, d(d+1)/2)
+    fail: torch.Tensor       # (N,) per point
+    counters: torch.Tensor
+    packed: torch.Tensor     # the contiguous [err, g_alphas, g_means, g_icf] vector
+
+    @property
+    def n_failed(self):
+        return int(self.counters[1].item())
+
+
+def gmm_packed_size(d, K):
+    return 1 + K + K * d + K * d * (d + 1) // 2
+
+
+def unpack_gmm(packed, d, K, fail=None, counters=None):
+    P = d * (d + 1) // 2
+    o = 1
+    ga = packed[o:o + K]
+    o += K
+    gm = packed[o:o + K * d].view(K, d)
+    o += K * d
+    gi = packed[o:o + K * P].view(K, P)
+    return GMMResult(packed[0], ga, gm, gi, fail, counters, packed)
+
+
+def gmm_grad(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
+             add_param_terms=True, tol=1e-9, invcheck=True, workspace=None, counters=None):
+    """ADBench GMM objective and its gradient w.r.t. (alphas, means, icf).
+
+    `gradient(load_example("gmm"), GradRequest("gmm", [0.0, alphas, means,
+    icf, x, zeros.., gamma, m, cst], wrt=["alphas","means","icf"]))` with the
+    points x on this device.  For a data-parallel shard pass
+    add_param_terms=(rank == 0) and N_total = the global point count, then
+    sum `result.packed` across ranks (see parallel.gmm_grad_distributed)."""
+    alphas = _require_cuda("alphas", alphas, ndim=1)
+    means = _require_cuda("means", means, ndim=2)
+    K, d = means.shape
+    icf = _require_cuda("icf", icf, ndim=2, last=d * (d + 1) // 2)
+    x = _require_cuda("x", x, ndim=2, last=d)
+    if alphas.shape[0] != K or icf.shape[0] != K:
+        raise KindError("alphas, means and icf must agree on K")
+    N = x.shape[0]
+    dev = x.device
+    L = _native.lib()
+    wsb = L.rl_gmm_workspace_bytes(d, K, N)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    packed = torch.empty(gmm_packed_size(d, K), dtype=F64, device=dev)
+    fail = torch.empty(N, dtype=torch.uint8, device=dev)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    rc = L.rl_gmm_grad_f64(d, K, N, int(N if N_total is None else N_total), _ptr(alphas),
+                           _ptr(means), _ptr(icf), _ptr(x), float(gamma), int(m), float(cst),
+                           float(tol), int(bool(invcheck)), int(bool(add_param_terms)),
+                           _ptr(packed), _ptr(fail), _ptr(counters), _ptr(workspace),
+                           workspace.numel(), _stream_handle())
+    _native.check(rc, "rl_gmm_grad_f64")
+    return unpack_gmm(packed, d, K, fail, counters)

@@ -1,0 +1,158 @@
+"""Bessel J_nu gradient kernel (rl_besselj_grad_f64) vs the reference.
+
+Parity bar (FP64): |gpu - ref| <= 1e-10 |ref| + 1e-12 (conftest.close); the
+only arithmetic differences are the device exp()/log(z) (<= 1 ulp) — the
+integer logs come from a host libm table.  Error classes (the reference's
+exceptions) must match exactly."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2003_04617_b200 as rg
+from conftest import close
+from oracle import ERROR_NAMES
+
+pytestmark = pytest.mark.gpu
+
+
+def run(z, nu, dev, **kw):
+    zt = torch.as_tensor(np.asarray(z, np.float64), device=dev)
+    r = rg.besselj_grad(zt, nu, **kw)
+    torch.cuda.synchronize()
+    return r.J.cpu().numpy(), r.dJdz.cpu().numpy(), r.fail.cpu().numpy(), r
+
+
+def test_golden_vectors_all_orders(cuda, golden):
+    g = golden("bessel")
+    for nu in np.unique(g["nu"]):
+        m = g["nu"] == nu
+        J, dz, fail, _ = run(g["z"][m], int(nu), cuda)
+        names = np.array([ERROR_NAMES[int(f)] for f in fail])
+        assert np.array_equal(names, g["err"][m]), (nu, names, g["err"][m])
+        ok = g["err"][m] == ""
+        assert close(J[ok], g["J"][m][ok]).all()
+        assert close(dz[ok], g["dJdz"][m][ok]).all()
+
+
+def test_config1_matches_reference(cuda, golden):
+    g = golden("bessel")
+    z = g["z"][:1000]
+    J, dz, fail, r = run(z, 2, cuda)
+    assert not fail.any() and r.n_failed == 0
+    assert close(J, g["J"][:1000]).all() and close(dz, g["dJdz"][:1000]).all()
+
+
+def test_random_batch_vs_oracle_with_trip_counts(cuda, oracle):
+    z = np.random.default_rng(11).uniform(0.1, 10.0, 65536)
+    J, dz, fail, r = run(z, 2, cuda)
+    Jo, dzo, fo, trips = oracle.besselj_grad(2, z)
+    assert np.array_equal(fail, fo)
+    assert close(J, Jo).all() and close(dz, dzo).all()
+    # integer work: total series trips (sum over elements) bit-exact
+    assert r.sum_trips == trips
+
+
+@pytest.mark.parametrize("nu", [0, 1, 3, 5, 8])
+def test_orders_vs_oracle(cuda, oracle, nu):
+    z = np.random.default_rng(nu).uniform(0.05, 14.0, 4099)  # ragged size
+    J, dz, fail, r = run(z, nu, cuda)
+    Jo, dzo, fo, trips = oracle.besselj_grad(nu, z)
+    assert np.array_equal(fail, fo)
+    ok = fo == 0
+    assert close(J[ok], Jo[ok]).all() and close(dz[ok], dzo[ok]).all()
+
+
+def test_edge_inputs_and_error_classes(cuda, oracle):
+    z = np.array([0.0, -1.0, -0.0, np.nan, np.inf, 1e-300, 1e-12, 20.0, 30.0, 800.0, 1.0])
+    for nu in (0, 2, -1):
+        J, dz, fail, _ = run(z, nu, cuda, max_steps=48 * 5000)
+        Jo, dzo, fo, _ = oracle.besselj_grad(nu, z, max_trips=5000)
+        assert np.array_equal(fail, fo), (nu, fail, fo)
+        ok = fo == 0
+        assert close(J[ok], Jo[ok]).all() and close(dz[ok], dzo[ok]).all()
+
+
+def test_empty_and_single(cuda):
+    J, dz, fail, r = run(np.zeros(0), 2, cuda)
+    assert J.size == 0 and r.sum_trips == 0
+    J, dz, fail, _ = run([2.5], 2, cuda)
+    assert fail[0] == 0
+
+
+def test_checks_are_observers(cuda):
+    z = np.random.default_rng(3).uniform(0.1, 10.0, 10000)
+    a = run(z, 2, cuda, invcheck=True)
+    b = run(z, 2, cuda, invcheck=False)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_seed_scales_the_cotangent(cuda):
+    z = np.random.default_rng(4).uniform(0.1, 10.0, 1000)
+    a = run(z, 2, cuda, seed=1.0)
+    b = run(z, 2, cuda, seed=-2.5)
+    assert close(b[1], -2.5 * a[1], rtol=1e-14, atol=0).all()
+
+
+def test_threshold_parameter(cuda, oracle):
+    z = np.random.default_rng(6).uniform(0.1, 10.0, 3000)
+    J, dz, fail, r = run(z, 2, cuda, thr=1e-8)
+    Jo, dzo, fo, trips = oracle.besselj_grad(2, z, thr=1e-8)
+    assert np.array_equal(fail, fo) and r.sum_trips == trips
+    assert close(J, Jo).all() and close(dz, dzo).all()
+
+
+def test_host_entry_matches_device_entry(cuda):
+    z = np.random.default_rng(8).uniform(0.1, 10.0, (1 << 22) + 12345)  # > 1 pipeline chunk
+    J, dz, fail, _ = run(z, 2, cuda)
+    Jh, dzh, fh, trips, nfail = rg.besselj_grad_host(z, 2)
+    assert np.array_equal(J, Jh) and np.array_equal(dz, dzh) and np.array_equal(fail, fh)
+    assert nfail == 0 and trips > 0
+
+
+def test_large_batch_properties(cuda, oracle):
+    """Full configs[1] size (2^26): every element restores (fail == 0), the
+    trip total matches the oracle's on a strided sample scaled up, and a
+    strided sample matches the oracle."""
+    n = 1 << 26
+    g = torch.Generator(device=cuda)
+    g.manual_seed(1)
+    z = torch.empty(n, dtype=torch.float64, device=cuda).uniform_(0.1, 10.0, generator=g)
+    r = rg.besselj_grad(z, 2)
+    torch.cuda.synchronize()
+    assert r.n_failed == 0
+    assert int((r.fail != 0).sum().item()) == 0
+    idx = torch.linspace(0, n - 1, 20000, device=cuda).long()
+    zs = z[idx].cpu().numpy()
+    Jo, dzo, fo, _ = oracle.besselj_grad(2, zs)
+    assert close(r.J[idx].cpu().numpy(), Jo).all()
+    assert close(r.dJdz[idx].cpu().numpy(), dzo).all()
+    # mean trip count of U(0.1, 10) at thr 1e-16 is ~16.3
+    assert 15.5 < r.sum_trips / n < 17.0
+
+
+def test_dropin_gradient_matches_reference_goldens(cuda, golden):
+    g = golden("bessel")
+    p = rg.load_example("besselj")
+    for i in range(0, 1000, 97):
+        primal, grads = rg.gradient(p, rg.GradRequest("besselj", [0.0, 2, float(g["z"][i])]))
+        assert primal[1] == 2 and primal[2] == g["z"][i]
+        assert close(primal[0], g["J"][i]) and close(grads["z"], g["dJdz"][i])
+        assert grads["out!"] == 1.0 and grads["nu"] is None
+
+
+def test_dropin_gradient_raises_reference_errors(cuda):
+    p = rg.load_example("besselj")
+    with pytest.raises(rg.RevDomainError):
+        rg.gradient(p, rg.GradRequest("besselj", [0.0, 2, -1.0]))
+    with pytest.raises(rg.DirtyAncilla):
+        rg.gradient(p, rg.GradRequest("besselj", [0.0, 2, 30.0]))
+    with pytest.raises(rg.KindError):
+        rg.gradient(p, rg.GradRequest("besselj", [0.0, 2, 1.0], seeds=[("nu", (), 1.0)]))
+
+
+def test_rejects_cpu_tensors(cuda):
+    with pytest.raises(rg.KindError):
+        rg.besselj_grad(torch.ones(3, dtype=torch.float64))
+    with pytest.raises(rg.KindError):
+        rg.besselj_grad(torch.ones(3, dtype=torch.float32, device=cuda))
