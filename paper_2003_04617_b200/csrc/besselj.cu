@@ -13,159 +13,266 @@
 // re-executes bit-identical primal arithmetic in them (ancillas restart from
 // their exact declared values, arguments are never written, and in sweep 3
 // every accumulated cotangent is zero), so sweep 4 performs exactly the
-// same checks sweep 2 would (this is the "dead uncompute" elision the paper
-// allows).  All reversibility checks of the reference are
+// same checks sweep 2 would (the "dead uncompute" elision the paper allows,
+// PAPER.md:650-651).  All reversibility checks of the reference are
 // evaluated on device, in the reference's order, into a per-element flag:
 //   loop entry/iteration postconditions  interpreter.py:772-797
 //   ancilla releases |v - decl| <= tol    interpreter.py:717-748, 365-395
 //   domain/overflow of log/exp            values.py:343-372
 //
 // Arithmetic is the reference's operation sequence (this file is compiled
-// with -fmad=false: no contraction, IEEE add/mul/div), so the only
-// differences to the CPU oracle are the device exp()/log(z) (<= 1 ulp).
-// Integer logs log(k), log(k + nu) come from a host-computed table.
+// with -fmad=false: no contraction, IEEE add/mul/div).  Integer logs
+// log(k), log(k + nu) come from a host libm table (bit-identical to the
+// reference); exp is fexp.cuh (0.5 ulp + O(2^-60), bit-identical to the
+// host libm in ~99.8% of calls, <= 1 ulp otherwise); log(z) and the final
+// division are libdevice (<= 1 ulp / correctly rounded).
 //
-// Scheduling (v1): one element per thread, grid-stride; the series loop of a
-// warp runs to the warp's longest trip count, and the reverse loop is
-// aligned on the same warp-uniform k so the log table is a broadcast read.
+// Scheduling.  The series trip count T(z) is non-decreasing in z (every
+// term grows with z), and a warp runs as long as its longest lane.  Each
+// block therefore takes a chunk of C = BLOCK*M elements, counting-sorts it
+// in shared memory by a z bucket (one smem atomic + scan per element), and
+// each 32-lane round processes 32 neighbours in z order: lanes then have
+// (nearly) equal trip counts and the loops run converged, with a
+// warp-uniform k (the log table is a broadcast constant-cache read).  Warp
+// w takes rounds w, w + W, ... so every warp gets the same mix of small
+// and large z.  Results go back to the original order through shared
+// memory and leave with coalesced stores.
 #include <math.h>
 
 #include "common.cuh"
+#include "fexp.cuh"
 
 namespace rl {
 
 __constant__ double c_logtab[LOGTAB_N];
 constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit for bit
+__constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
+
+constexpr int BJ_BLOCK = 256;
+constexpr int BJ_M = 4;
+constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
+constexpr int BJ_NB = 256;              // z buckets
+constexpr int BJ_WARPS = BJ_BLOCK / 32;
 
 __device__ __forceinline__ double logi(int i) {
   return i < LOGTAB_N ? c_logtab[i] : log((double)i);
 }
 
-__device__ __forceinline__ bool exp_overflowed(double t, double x) {
-  return isinf(t) && isfinite(x);
+// exp with the reference's overflow semantics (math.exp raises
+// OverflowError for a finite argument whose result overflows)
+__device__ __forceinline__ double rexp(double x, const Exp2Tab *tab, int &code) {
+  if (x >= -708.0 && x <= 709.0) return fexp_core(x, tab);
+  const double t = exp(x);
+  if (isinf(t) && isfinite(x) && !code) code = RL_ERR_OVERFLOW;
+  return t;
 }
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_besselj_grad(
+__device__ __forceinline__ int zbucket(double z) {
+  if (!(z > 0.0)) return 0;
+  return z < 21.0 ? (int)(z * 12.0) : BJ_NB - 1;
+}
+
+struct BJOut {
+  double J, dz;
+  int code, T;
+};
+
+// One element; all 32 lanes of the warp call it together (`valid` false for
+// padding lanes), because the loops are warp-synchronous.
+__device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, double thr,
+                                                 double tol, double seed, long long max_trips,
+                                                 int chk, const Exp2Tab *tab) {
+  int code = 0;
+  // ---------------- sweep 1: forward routine ----------------
+  if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
+  const double logz = (valid && !code) ? log(z) : 0.0;
+  double lz = 0.0 + logz;
+  double halfz = 0.0 + lz;                               // halfz *= lz
+  halfz = halfz - LN2;                                   // halfz /= 2
+  double h2 = 0.0 + halfz;                               // halfz2 *= halfz (x2)
+  h2 = h2 + halfz;
+  double s = 0.0;
+  for (int q = 1; q <= nu; q++) {                        // for i = 1:1:nu
+    s = s + halfz;
+    s = s - logi(q);
+  }
+  double t = rexp(s, tab, code);                         // acc += convert(s)
+  double acc = 0.0 + t;
+  int T = 0;
+  bool go = valid && !code && (t > thr);                 // while (s > thr, k != 0)
+  int kk = 0;                                            // warp-uniform k
+  while (__any_sync(FULL_MASK, go)) {
+    kk++;
+    if (go) {
+      if (T >= max_trips) {
+        code = RL_ERR_FUEL;
+        go = false;
+      } else if (kk + nu <= 0) {                         // s /= kn with kn <= 0
+        code = RL_ERR_DOMAIN;
+        go = false;
+      } else {
+        T = kk;
+        s = s + h2;                                      // s *= halfz2
+        s = s - logi(kk);                                // s /= k
+        s = s - logi(kk + nu);                           // s /= kn
+        t = rexp(s, tab, code);
+        acc = (kk & 1) ? acc - t : acc + t;              // if (k % 2 == 0, ~)
+        go = !code && t > thr;
+      }
+    }
+  }
+  BJOut o;
+  o.J = 0.0 + acc;                                       // out! += acc
+  o.T = T;
+  const bool fwd_ok = valid && !code;
+
+  // ---------------- sweep 4: ~routine with adjoints ----------------
+  const double accg = 0.0 + (1.0 * seed) * 1.0;          // out! -= acc: acc.g += out.g
+  double sg = 0.0, h2g = 0.0, hzg = 0.0, lzg = 0.0, zg = 0.0;
+  if (fwd_ok && chk && t > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
+  const int Tmax = __reduce_max_sync(FULL_MASK, fwd_ok ? T : 0);
+  for (int k = Tmax; k >= 1; k--) {                      // aligned: k warp-uniform
+    if (fwd_ok && k <= T) {
+      if (k & 1) {                                       // inverse if
+        acc = acc + t;
+        sg = sg + (-1.0 * accg) * t;
+      } else {
+        acc = acc - t;
+        sg = sg + (1.0 * accg) * t;
+      }
+      s = s + logi(k + nu);                              // s *= kn
+      s = s + logi(k);                                   // s *= k
+      s = s - h2;                                        // s /= halfz2
+      h2g = h2g + 1.0 * sg;
+      t = rexp(s, tab, code);
+      if (!code && chk && !(t > thr)) code = RL_ERR_POSTCONDITION;
+    }
+  }
+  if (fwd_ok) {
+    acc = acc - t;                                       // acc -= convert(s)
+    sg = sg + (1.0 * accg) * t;
+    for (int q = nu; q >= 1; q--) {                      // for i = nu:-1:1
+      s = s + logi(q);
+      s = s - halfz;
+      hzg = hzg + 1.0 * sg;
+    }
+    h2 = h2 - halfz;                                     // halfz2 /= halfz (x2)
+    hzg = hzg + 1.0 * h2g;
+    h2 = h2 - halfz;
+    hzg = hzg + 1.0 * h2g;
+    halfz = halfz + LN2;                                 // halfz *= 2
+    halfz = halfz - lz;                                  // halfz /= lz
+    lzg = lzg + 1.0 * hzg;
+    lz = lz - logz;                                      // lz /= convert(z)
+    zg = zg + (1.0 * lzg) / z;
+    if (chk && !code) {                                  // releases
+      if (fabs(acc - 0.0) > tol || fabs(s - 0.0) > tol || fabs(h2 - 0.0) > tol ||
+          fabs(halfz - 0.0) > tol || fabs(lz - 0.0) > tol)
+        code = RL_ERR_DIRTY_ANCILLA;
+    }
+  }
+  const double qnan = __longlong_as_double(0x7ff8000000000000ULL);
+  if (!fwd_ok) o.J = qnan;
+  o.dz = fwd_ok ? zg : qnan;
+  o.code = code;
+  return o;
+}
+
+__global__ void __launch_bounds__(BJ_BLOCK, 4) k_besselj_grad(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, double *__restrict__ Jout, double *__restrict__ dzout,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
-  const int lane = threadIdx.x & 31;
+  __shared__ Exp2Tab s_tab[64];
+  __shared__ int s_hist[BJ_NB];
+  __shared__ int s_wsum[BJ_WARPS];
+  __shared__ double s_z[BJ_C];
+  __shared__ double s_J[BJ_C];
+  __shared__ double s_dz[BJ_C];
+  __shared__ uint16_t s_idx[BJ_C];
+  __shared__ uint8_t s_fail[BJ_C];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 64) s_tab[tid] = c_exp2tab[tid];
   unsigned long long trips_sum = 0, nfail = 0;
-  const long long stride = (long long)gridDim.x * BLOCK;
-  for (long long base = (long long)blockIdx.x * BLOCK + (threadIdx.x & ~31); base < n;
-       base += stride) {
-    const long long i = base + lane;
-    const bool valid = i < n;
-    const double z = valid ? __ldg(zin + i) : 1.0;
-    int code = 0;
 
-    // ---------------- sweep 1: forward routine ----------------
-    if (!(z > 0.0)) code = RL_ERR_DOMAIN;               // lz *= convert(z)
-    const double logz = code ? 0.0 : log(z);
-    double lz = 0.0 + logz;
-    double halfz = 0.0 + lz;                             // halfz *= lz
-    halfz = halfz - LN2;                                 // halfz /= 2
-    double h2 = 0.0 + halfz;                             // halfz2 *= halfz (x2)
-    h2 = h2 + halfz;
-    double s = 0.0;
-    for (int q = 1; q <= nu; q++) {                      // for i = 1:1:nu
-      s = s + halfz;
-      s = s - logi(q);
+  for (long long base = (long long)blockIdx.x * BJ_C; base < n;
+       base += (long long)gridDim.x * BJ_C) {
+    const int cnt = (int)(n - base < BJ_C ? n - base : BJ_C);
+    // 1. bucket histogram (rank within bucket from the atomic)
+    for (int b = tid; b < BJ_NB; b += BJ_BLOCK) s_hist[b] = 0;
+    __syncthreads();
+    double zr[BJ_M];
+    int key[BJ_M], rnk[BJ_M];
+#pragma unroll
+    for (int m = 0; m < BJ_M; m++) {
+      const int e = m * BJ_BLOCK + tid;
+      if (e < cnt) {
+        zr[m] = __ldcs(zin + base + e);
+        key[m] = zbucket(zr[m]);
+        rnk[m] = atomicAdd(&s_hist[key[m]], 1);
+      }
     }
-    double t = exp(s);                                   // acc += convert(s)
-    if (!code && exp_overflowed(t, s)) code = RL_ERR_OVERFLOW;
-    double acc = 0.0 + t;
-    int T = 0;
-    bool go = valid && !code && (t > thr);               // while (s > thr, k != 0)
-    int kk = 0;                                          // warp-uniform k
-    while (__any_sync(FULL_MASK, go)) {
-      kk++;
-      if (go) {
-        if (T >= max_trips) {
-          code = RL_ERR_FUEL;
-          go = false;
-        } else {
-          T++;
-          const int kn = kk + nu;
-          s = s + h2;                                    // s *= halfz2
-          s = s - logi(kk);                              // s /= k
-          if (kn <= 0) {                                 // s /= kn
-            code = RL_ERR_DOMAIN;
-            go = false;
-          } else {
-            s = s - logi(kn);
-            t = exp(s);
-            if (exp_overflowed(t, s)) {
-              code = RL_ERR_OVERFLOW;
-              go = false;
-            } else {
-              acc = (kk & 1) ? acc - t : acc + t;        // if (k % 2 == 0, ~)
-              go = t > thr;
-            }
-          }
+    __syncthreads();
+    // 2. exclusive scan of the 256 buckets (one per thread)
+    {
+      const int v = s_hist[tid];
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_wsum[warp] = x;
+      __syncthreads();
+      int off = 0;
+#pragma unroll
+      for (int w = 0; w < BJ_WARPS; w++) off += w < warp ? s_wsum[w] : 0;
+      __syncthreads();
+      s_hist[tid] = off + x - v;
+    }
+    __syncthreads();
+    // 3. scatter into z order
+#pragma unroll
+    for (int m = 0; m < BJ_M; m++) {
+      const int e = m * BJ_BLOCK + tid;
+      if (e < cnt) {
+        const int pos = s_hist[key[m]] + rnk[m];
+        s_z[pos] = zr[m];
+        s_idx[pos] = (uint16_t)e;
+      }
+    }
+    __syncthreads();
+    // 4. rounds of 32 z-neighbours; warp w takes rounds w, w + 8, ...
+#pragma unroll 1
+    for (int r = warp; r < BJ_C / 32; r += BJ_WARPS) {
+      const int pos = r * 32 + lane;
+      const bool valid = pos < cnt;
+      if (__any_sync(FULL_MASK, valid)) {
+        const double z = valid ? s_z[pos] : 1.0;
+        const BJOut o = besselj_element(z, valid, nu, thr, tol, seed, max_trips, chk, s_tab);
+        if (valid) {
+          const int oi = s_idx[pos];
+          s_J[oi] = o.J;
+          s_dz[oi] = o.dz;
+          s_fail[oi] = (uint8_t)o.code;
+          trips_sum += (unsigned long long)o.T;
+          nfail += o.code != 0;
         }
       }
     }
-    const double Jv = 0.0 + acc;                         // out! += acc
-    const bool fwd_ok = valid && !code;
-
-    // ---------------- sweep 4: ~routine with adjoints ----------------
-    const double accg = 0.0 + (1.0 * seed) * 1.0;        // out! -= acc: acc.g += out.g
-    double sg = 0.0, h2g = 0.0, hzg = 0.0, lzg = 0.0, zg = 0.0;
-    if (fwd_ok && chk && t > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
-    const int Tmax = __reduce_max_sync(FULL_MASK, fwd_ok ? T : 0);
-    for (int k = Tmax; k >= 1; k--) {                    // aligned: k warp-uniform
-      if (fwd_ok && k <= T) {
-        if (k & 1) {                                     // inverse if
-          acc = acc + t;
-          sg = sg + (-1.0 * accg) * t;
-        } else {
-          acc = acc - t;
-          sg = sg + (1.0 * accg) * t;
-        }
-        const int kn = k + nu;
-        s = s + logi(kn);                                // s *= kn
-        s = s + logi(k);                                 // s *= k
-        s = s - h2;                                      // s /= halfz2
-        h2g = h2g + 1.0 * sg;
-        t = exp(s);
-        if (!code && exp_overflowed(t, s)) code = RL_ERR_OVERFLOW;
-        if (!code && chk && !(t > thr)) code = RL_ERR_POSTCONDITION;
+    __syncthreads();
+    // 5. coalesced stores in the original order
+#pragma unroll
+    for (int m = 0; m < BJ_M; m++) {
+      const int e = m * BJ_BLOCK + tid;
+      if (e < cnt) {
+        __stcs(Jout + base + e, s_J[e]);
+        __stcs(dzout + base + e, s_dz[e]);
+        fail[base + e] = s_fail[e];
       }
     }
-    if (fwd_ok) {
-      acc = acc - t;                                     // acc -= convert(s)
-      sg = sg + (1.0 * accg) * t;
-      for (int q = nu; q >= 1; q--) {                    // for i = nu:-1:1
-        s = s + logi(q);
-        s = s - halfz;
-        hzg = hzg + 1.0 * sg;
-      }
-      h2 = h2 - halfz;                                   // halfz2 /= halfz (x2)
-      hzg = hzg + 1.0 * h2g;
-      h2 = h2 - halfz;
-      hzg = hzg + 1.0 * h2g;
-      halfz = halfz + LN2;                               // halfz *= 2
-      halfz = halfz - lz;                                // halfz /= lz
-      lzg = lzg + 1.0 * hzg;
-      lz = lz - logz;                                    // lz /= convert(z)
-      zg = zg + (1.0 * lzg) / z;
-      if (chk && !code) {                                // releases
-        if (fabs(acc - 0.0) > tol || fabs(s - 0.0) > tol || fabs(h2 - 0.0) > tol ||
-            fabs(halfz - 0.0) > tol || fabs(lz - 0.0) > tol)
-          code = RL_ERR_DIRTY_ANCILLA;
-      }
-    }
-    if (valid) {
-      Jout[i] = fwd_ok ? Jv : __longlong_as_double(0x7ff8000000000000ULL);
-      dzout[i] = fwd_ok ? zg : __longlong_as_double(0x7ff8000000000000ULL);
-      fail[i] = (uint8_t)code;
-      trips_sum += (unsigned long long)T;
-      nfail += code != 0;
-    }
+    __syncthreads();
   }
-  block_add_counters<BLOCK>(trips_sum, nfail, counters);
+  block_add_counters<BJ_BLOCK>(trips_sum, nfail, counters);
 }
 
 static int upload_logtab() {
@@ -177,8 +284,6 @@ static int upload_logtab() {
 
 int besselj_tables_init() { return upload_logtab(); }
 
-constexpr int BJ_BLOCK = 256;
-
 int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double tol, double seed,
                    int64_t max_trips, int32_t invcheck, double *J, double *dJdz, uint8_t *fail,
                    unsigned long long *counters, cudaStream_t st) {
@@ -188,15 +293,15 @@ int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double to
   if (rc) return rc;
   if (n == 0) return RL_OK;
   int blocks_per_sm = 0;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &blocks_per_sm, k_besselj_grad<BJ_BLOCK>, BJ_BLOCK, 0),
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj_grad,
+                                                                 BJ_BLOCK, 0),
                    "occupancy");
   if (rc) return rc;
-  long long want = (n + BJ_BLOCK - 1) / BJ_BLOCK;
-  long long cap = (long long)sm_count() * blocks_per_sm;
-  int grid = (int)(want < cap ? want : cap);
-  k_besselj_grad<BJ_BLOCK><<<grid, BJ_BLOCK, 0, st>>>(nu, z, n, thr, tol, seed, max_trips,
-                                                      invcheck ? 1 : 0, J, dJdz, fail, counters);
+  const long long want = (n + BJ_C - 1) / BJ_C;
+  const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+  const int grid = (int)(want < cap ? want : cap);
+  k_besselj_grad<<<grid, BJ_BLOCK, 0, st>>>(nu, z, n, thr, tol, seed, max_trips,
+                                            invcheck ? 1 : 0, J, dJdz, fail, counters);
   return cuda_status(cudaGetLastError(), "k_besselj_grad launch");
 }
 

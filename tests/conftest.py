@@ -44,3 +44,17 @@ def close(a, b, rtol=1e-10, atol=1e-12):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return np.abs(a - b) <= rtol * np.abs(b) + atol
+
+
+def close_series(a, b, nu, z, rtol=1e-10):
+    """Bessel parity bar: 1e-10 relative plus an absolute floor of 1e-13 x
+    the series' absolute scale I_nu(z) + I_nu'(z) (the sum of |terms| and of
+    |d term/dz|): cancellation in the alternating series makes the absolute
+    error of ANY binary64 evaluation — the reference's included — scale with
+    it, and a 1-ulp difference in log(z) moves every term by ~(2k+nu) ulp."""
+    import scipy.special as sp
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    z = np.asarray(z, np.float64)
+    scale = sp.iv(nu, z) + np.abs(sp.ivp(nu, z))
+    return np.abs(a - b) <= rtol * np.abs(b) + 1e-13 * scale

@@ -1,0 +1,33 @@
+// Host check of csrc/fexp.cuh against the C library exp (glibc), which is
+// what CPython's math.exp — and so the reference — uses.
+// usage: fexp_test N lo hi seed  -> prints "n equal max_ulp"
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+
+#include "../paper_2003_04617_b200/csrc/fexp.cuh"
+
+static const rl::Exp2Tab TAB[64] = RL_EXP2_TABLE_INIT;
+
+int main(int argc, char **argv) {
+  long n = atol(argv[1]);
+  double lo = atof(argv[2]), hi = atof(argv[3]);
+  std::mt19937_64 g(atol(argv[4]));
+  std::uniform_real_distribution<double> U(lo, hi);
+  long eq = 0;
+  double maxulp = 0;
+  for (long i = 0; i < n; i++) {
+    double x = U(g);
+    double a = rl::fexp_core(x, TAB), b = exp(x);
+    if (memcmp(&a, &b, 8) == 0) {
+      eq++;
+    } else {
+      double u = fabs(a - b) / (nextafter(b, INFINITY) - b);
+      if (u > maxulp) maxulp = u;
+    }
+  }
+  printf("%ld %ld %.3f\n", n, eq, maxulp);
+  return 0;
+}
