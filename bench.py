@@ -358,6 +358,171 @@ def load_traffic(kernel):
 
 
 # ---------------------------------------------------------------------------
+# BA workload (configs[3], ba20 shape)
+# ---------------------------------------------------------------------------
+
+BA_N, BA_M, BA_P = 1723, 156502, 678718
+
+
+def ba_synthetic(n_cams, n_pts, n_obs, seed=3):
+    rng = np.random.default_rng(seed)
+    cams = np.empty((n_cams, 11))
+    cams[:, 0:3] = rng.normal(0.0, 0.3, (n_cams, 3))
+    cams[:, 3:6] = rng.normal(0.0, 1.0, (n_cams, 3))
+    cams[:, 6] = rng.uniform(500.0, 600.0, n_cams)
+    cams[:, 7:9] = rng.uniform(0.0, 1.0, (n_cams, 2))
+    cams[:, 9:11] = rng.normal(0.0, 0.01, (n_cams, 2))
+    X = rng.normal(0.0, 1.0, (n_pts, 3))
+    X[:, 2] += 10.0
+    w = rng.uniform(0.0, 1.0, n_obs)
+    feats = rng.uniform(0.0, 100.0, (n_obs, 2))
+    i = np.arange(n_obs)
+    obs = np.stack([i % n_cams, i % n_pts], 1).astype(np.int32)
+    return cams, X, w, feats, obs
+
+
+def ba_bytes(n_cams, n_pts, p):
+    """Algorithmic HBM bytes of one Jacobian launch (DESIGN.md §BA roofline):
+    read obs (8) + w (8) + feats (16) per observation, every camera (88) and
+    point (24) once; write the 31-double Jacobian row (248)."""
+    return p * (8 + 8 + 16 + 248) + n_cams * 88 + n_pts * 24
+
+
+def run_ba_ours(args, D):
+    import torch
+
+    from paper_2003_04617_b200 import kernels
+    dev = torch.device("cuda", D.local)
+    torch.cuda.set_device(dev)
+    p_total = args.n or BA_P
+    cams, X, w, feats, obs = ba_synthetic(BA_N, BA_M, p_total)
+    lo, hi = p_total * D.rank // D.world, p_total * (D.rank + 1) // D.world
+    t = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
+    dc, dX, dw, df, do = t(cams), t(X), t(w[lo:hi]), t(feats[lo:hi]), t(obs[lo:hi])
+    p = hi - lo
+    J = torch.empty((p, 31), dtype=torch.float64, device=dev)
+    fail = torch.empty(p, dtype=torch.uint8, device=dev)
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = (J, None, None, fail)
+    for _ in range(max(args.warmup, 3)):
+        kernels.ba_jacobian(dc, dX, dw, df, do, want_err=False, out=out, counters=counters)
+    torch.cuda.synchronize()
+    props = torch.cuda.get_device_properties(dev)
+    sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
+    sampler.start()
+    time.sleep(0.25)
+    D.barrier()
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for a, b in evs:
+        flush.fill_(1)                      # evict L2 (inputs are 26 MB < 126 MB L2)
+        a.record(stream)
+        kernels.ba_jacobian(dc, dX, dw, df, do, want_err=False, out=out, counters=counters)
+        b.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms_step = D.max(ms)
+    n_failed = D.sum(int(counters[1].item()))
+    value = 1.0 / (ms_step * 1e-3)
+    byts = ba_bytes(BA_N, BA_M, p)
+    achieved = D.sum(byts) / (ms_step * 1e-3) / 1e9
+    peak = measured_hbm()
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": load_traffic("k_ba_jac"),
+            "bytes_per_launch": D.sum(byts), "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    parity = None
+    if D.rank == 0:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle as O
+        idx = np.linspace(0, p - 1, 2000).astype(np.int64)
+        Jo, _, fo = O.ba_jac(cams, X, w[lo:hi][idx], feats[lo:hi][idx], obs[lo:hi][idx])
+        Jg = J.cpu().numpy()[idx]
+        sc = np.max(np.abs(Jo), axis=1, keepdims=True)
+        parity = {"n": 2000, "max_err_over_rowscale": float(np.max(np.abs(Jg - Jo) / sc)),
+                  "flags_equal": bool(np.array_equal(fail.cpu().numpy()[idx], fo))}
+    e2e = None
+    if not args.no_e2e:
+        e2e = ba_e2e(cams, X, w[lo:hi], feats[lo:hi], obs[lo:hi], args, D)
+    return {
+        "metric": "Jacobian evals/sec", "value": round(value, 2), "unit": "jacobians/s",
+        "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic ba20-shaped problem, seed 3",
+        "config": {"workload": "ba20_jacobian", "n_cams": BA_N, "n_pts": BA_M, "n_obs": p_total,
+                   "per_rank": p, "parallelism": f"shard{D.world}",
+                   "l2": "256 MiB L2 flush before every timed launch; per-launch CUDA events"},
+        "obs_per_s": round(p_total / (ms_step * 1e-3), 1),
+        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
+        "failed_per_step": n_failed // args.steps, "parity_sample": parity,
+    }
+
+
+def ba_e2e(cams, X, w, feats, obs, args, D):
+    import ctypes
+
+    import torch
+
+    from paper_2003_04617_b200 import _native
+    L = _native.lib()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hc, hX, hw, hf, ho = pin(cams), pin(X), pin(w), pin(feats), pin(obs)
+    p = w.size
+    hJ = torch.empty((p, 31), dtype=torch.float64).pin_memory()
+    hfl = torch.empty(p, dtype=torch.uint8).pin_memory()
+    nf = ctypes.c_ulonglong()
+
+    def call():
+        rc = L.rl_ba_jac_f64_host(cams.shape[0], X.shape[0], p, hc.data_ptr(), hX.data_ptr(),
+                                  hw.data_ptr(), hf.data_ptr(), ho.data_ptr(), 1e-9, 1, None,
+                                  hJ.data_ptr(), hfl.data_ptr(), ctypes.byref(nf), D.local)
+        _native.check(rc, "rl_ba_jac_f64_host")
+    call()
+    D.barrier()
+    steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    dt = D.max((time.perf_counter() - t0) / steps)
+    h2d = cams.nbytes + X.nbytes + D.sum(w.nbytes + feats.nbytes + obs.nbytes)
+    return {"value": round(1.0 / dt, 2), "unit": "jacobians/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(D.sum(hJ.numel() * 8 + p)),
+            "ms_per_step": round(dt * 1e3, 3),
+            "path": "rl_ba_jac_f64_host (pinned host buffers, 3-stream pipeline)"}
+
+
+def ba_cpu(target_s=10.0):
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    cams, X, w, feats, obs = ba_synthetic(BA_N, BA_M, BA_P)
+    n = 2048
+    while True:
+        t0 = time.perf_counter()
+        O.ba_jac(cams, X, w[:n], feats[:n], obs[:n])
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= BA_P:
+            break
+        n = min(BA_P, max(n * 2, int(n * target_s / max(dt, 1e-3))))
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    rate = n / dt
+    return {"value": round(rate / BA_P, 4), "unit": "jacobians/s", "cores": cores, "kind": "port",
+            "obs_per_s": round(rate, 1),
+            "sample": f"{n} of the {BA_P} observations (2 seeded passes + weight each, all "
+                      f"reference sweeps and checks, oracle/revoracle.c), {dt:.2f} s"}
+
+
+def measured_hbm():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    return 6650.0  # B200_PROFILING.md fallback
+
+
+# ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
 
@@ -390,6 +555,10 @@ def main():
         res = run_bessel_ours(args, D)
         if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = bessel_cpu()
+    elif args.workload == "ba":
+        res = run_ba_ours(args, D)
+        if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = ba_cpu()
     else:
         raise SystemExit(f"workload {args.workload} not wired yet")
     if D.rank == 0:
