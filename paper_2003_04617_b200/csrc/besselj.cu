@@ -47,6 +47,7 @@ namespace rl {
 __constant__ double c_logtab[LOGTAB_N];
 constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit for bit
 __constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
+__constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 
 constexpr int BJ_BLOCK = 256;
 constexpr int BJ_M = 4;
@@ -54,17 +55,47 @@ constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
 constexpr int BJ_NB = 256;              // z buckets
 constexpr int BJ_WARPS = BJ_BLOCK / 32;
 
+// 2^(i/64) table, copied to shared memory per block (lane-varying index)
+__shared__ Exp2Tab s_exp2tab[64];
+
 __device__ __forceinline__ double logi(int i) {
   return i < LOGTAB_N ? c_logtab[i] : log((double)i);
 }
 
+template <bool TAB>
+__device__ __forceinline__ double logk(int i) {
+  return TAB ? c_logtab[i] : logi(i);
+}
+
+struct ExpR {
+  double t;
+  int code;
+};
+
 // exp with the reference's overflow semantics (math.exp raises
 // OverflowError for a finite argument whose result overflows)
-__device__ __forceinline__ double rexp(double x, const Exp2Tab *tab, int &code) {
-  if (x >= -708.0 && x <= 709.0) return fexp_core(x, tab);
-  const double t = exp(x);
-  if (isinf(t) && isfinite(x) && !code) code = RL_ERR_OVERFLOW;
-  return t;
+__device__ __forceinline__ ExpR rexp_slow(double x) {
+  ExpR r;
+  r.t = exp(x);
+  r.code = (isinf(r.t) && isfinite(x)) ? RL_ERR_OVERFLOW : 0;
+  return r;
+}
+
+// Two exp flavours.  FAST: table exp only, and the lane records whether any
+// argument left (-708, 708) (integer test on the high word, no branch);
+// such lanes — only elements whose series terms overflow or underflow,
+// i.e. z in the hundreds — are recomputed by the CAREFUL flavour, which
+// takes libdevice's exp outside the range and reports the reference's
+// OverflowError.
+template <bool CAREFUL>
+__device__ __forceinline__ ExpR rexp(double x, bool &bad) {
+  ExpR r;
+  const bool out = (__double2hiint(x) & 0x7fffffff) >= 0x40862000;
+  if (CAREFUL && out) return rexp_slow(x);
+  r.t = fexp_core(x, s_exp2tab, c_expk);
+  r.code = 0;
+  if (!CAREFUL) bad = bad || out;
+  return r;
 }
 
 __device__ __forceinline__ int zbucket(double z) {
@@ -75,19 +106,82 @@ __device__ __forceinline__ int zbucket(double z) {
 struct BJOut {
   double J, dz;
   int code, T;
+  bool bad;
 };
 
+// One forward series trip at (warp-uniform) k; ODD = 1 / 0 when k is known
+// to be odd / even (static sign of the alternating series), -1 otherwise.
+// PRED: only lanes with `act` advance.
+template <bool CAREFUL, bool TAB, bool PRED, int ODD>
+__device__ __forceinline__ void fwd_trip(int k, int nu, double h2, double thr, bool &act,
+                                         double &s, double &t, double &acc, int &T, int &code,
+                                         bool &bad) {
+  const double l1 = logk<TAB>(k);
+  const double l2 = logk<TAB>(k + nu);
+  double sn = s + h2;                                    // s *= halfz2
+  sn = sn - l1;                                          // s /= k
+  sn = sn - l2;                                          // s /= kn
+  const ExpR e = rexp<CAREFUL>(sn, bad);
+  // if (k % 2 == 0, ~): even k adds, odd k subtracts
+  const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
+  const double an = odd ? acc - e.t : acc + e.t;
+  if (!PRED || act) {
+    s = sn;
+    t = e.t;
+    acc = an;
+    T = k;
+    if (CAREFUL) code = e.code;
+    act = (!CAREFUL || !e.code) && e.t > thr;
+  }
+}
+
+// One reverse trip at (warp-uniform) k for lanes with k <= T (PRED) or
+// all lanes (the caller guarantees every live lane has k <= T).
+template <bool CAREFUL, bool TAB, bool PRED, int ODD>
+__device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, double paccg,
+                                         double naccg, int chk, bool live, int T, double &acc,
+                                         double &sg, double &s, double &h2g, double &t,
+                                         int &code, bool &bad) {
+  const double l2 = logk<TAB>(k + nu);
+  const double l1 = logk<TAB>(k);
+  // inverse if: odd k: acc += convert(s) (sign -1); even: acc -= convert(s)
+  const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
+  const double an = odd ? acc + t : acc - t;
+  const double sgn = sg + (odd ? naccg : paccg) * t;
+  double sn = s + l2;                                    // s *= kn
+  sn = sn + l1;                                          // s *= k
+  sn = sn - h2;                                          // s /= halfz2
+  const double h2gn = h2g + 1.0 * sgn;
+  const ExpR e = rexp<CAREFUL>(sn, bad);
+  if (!PRED || k <= T) {
+    acc = an;
+    sg = sgn;
+    s = sn;
+    h2g = h2gn;
+    t = e.t;
+    const int c = (CAREFUL && e.code) ? e.code
+                                      : ((chk && !(e.t > thr)) ? RL_ERR_POSTCONDITION : 0);
+    if (live && !code) code = c;
+  }
+}
+
 // One element; all 32 lanes of the warp call it together (`valid` false for
-// padding lanes), because the loops are warp-synchronous.
+// padding lanes), because the loops are warp-synchronous: the trip index k
+// is warp-uniform.  Lanes are z-sorted, so their trip counts (nearly)
+// agree: the loops run unpredicated while every live lane is active and
+// fall back to predicated trips only for the tail.
+// ktab (uniform) = last k with k + nu inside the log table; kfuel = the
+// fuel cap on trips.
+template <bool CAREFUL>
 __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, double thr,
-                                                 double tol, double seed, long long max_trips,
-                                                 int chk, const Exp2Tab *tab) {
+                                                 double tol, double seed, int ktab, int kfuel,
+                                                 int chk) {
   int code = 0;
+  bool bad = false;
   // ---------------- sweep 1: forward routine ----------------
   if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
   const double logz = (valid && !code) ? log(z) : 0.0;
-  double lz = 0.0 + logz;
-  double halfz = 0.0 + lz;                               // halfz *= lz
+  double halfz = 0.0 + (0.0 + logz);                     // lz = 0 + log z; halfz *= lz
   halfz = halfz - LN2;                                   // halfz /= 2
   double h2 = 0.0 + halfz;                               // halfz2 *= halfz (x2)
   h2 = h2 + halfz;
@@ -96,31 +190,51 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     s = s + halfz;
     s = s - logi(q);
   }
-  double t = rexp(s, tab, code);                         // acc += convert(s)
-  double acc = 0.0 + t;
+  asm volatile("" : "+d"(h2));  // keep h2 live: no per-trip rematerialisation
+  double t, acc;
+  {
+    const ExpR e = rexp<CAREFUL>(s, bad);                // acc += convert(s)
+    t = e.t;
+    if (!code) code = e.code;
+    acc = 0.0 + t;
+  }
   int T = 0;
-  bool go = valid && !code && (t > thr);                 // while (s > thr, k != 0)
-  int kk = 0;                                            // warp-uniform k
-  while (__any_sync(FULL_MASK, go)) {
-    kk++;
-    if (go) {
-      if (T >= max_trips) {
-        code = RL_ERR_FUEL;
-        go = false;
-      } else if (kk + nu <= 0) {                         // s /= kn with kn <= 0
-        code = RL_ERR_DOMAIN;
-        go = false;
-      } else {
-        T = kk;
-        s = s + h2;                                      // s *= halfz2
-        s = s - logi(kk);                                // s /= k
-        s = s - logi(kk + nu);                           // s /= kn
-        t = rexp(s, tab, code);
-        acc = (kk & 1) ? acc - t : acc + t;              // if (k % 2 == 0, ~)
-        go = !code && t > thr;
-      }
+  bool act = valid && !code && (t > thr);                // while (s > thr, k != 0)
+  const bool dead = !valid || code;                      // state irrelevant from here
+  const int code0 = code;
+  int k = 0;
+  if (nu < 0 && __any_sync(FULL_MASK, act)) {            // first trip: s /= kn, kn <= 0
+    if (act) code = kfuel > 0 ? RL_ERR_DOMAIN : RL_ERR_FUEL;
+    act = false;
+  }
+  const int kend = ktab < kfuel ? ktab : kfuel;
+  // main phase: every non-dead lane still active -> no predication; two
+  // trips per iteration (odd, even) so the series sign is static
+  if (__all_sync(FULL_MASK, act || dead)) {
+    while (k + 2 <= kend) {
+      fwd_trip<CAREFUL, true, false, 1>(k + 1, nu, h2, thr, act, s, t, acc, T, code, bad);
+      k++;
+      if (!__all_sync(FULL_MASK, act || dead)) break;
+      fwd_trip<CAREFUL, true, false, 0>(k + 1, nu, h2, thr, act, s, t, acc, T, code, bad);
+      k++;
+      if (!__all_sync(FULL_MASK, act || dead)) break;
+    }
+    if (dead) {                                          // undo the unpredicated trips
+      act = false;
+      T = 0;
+      code = code0;
     }
   }
+  // tail: predicated
+  while (k < kend && __any_sync(FULL_MASK, act)) {
+    k++;
+    fwd_trip<CAREFUL, true, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code, bad);
+  }
+  while (k < kfuel && __any_sync(FULL_MASK, act)) {      // beyond the table (huge nu / T)
+    k++;
+    fwd_trip<CAREFUL, false, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code, bad);
+  }
+  if (act) code = RL_ERR_FUEL;                           // still running at the fuel cap
   BJOut o;
   o.J = 0.0 + acc;                                       // out! += acc
   o.T = T;
@@ -128,29 +242,37 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
 
   // ---------------- sweep 4: ~routine with adjoints ----------------
   const double accg = 0.0 + (1.0 * seed) * 1.0;          // out! -= acc: acc.g += out.g
-  double sg = 0.0, h2g = 0.0, hzg = 0.0, lzg = 0.0, zg = 0.0;
+  const double paccg = 1.0 * accg, naccg = -1.0 * accg;
+  double sg = 0.0, h2g = 0.0;
   if (fwd_ok && chk && t > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
   const int Tmax = __reduce_max_sync(FULL_MASK, fwd_ok ? T : 0);
-  for (int k = Tmax; k >= 1; k--) {                      // aligned: k warp-uniform
-    if (fwd_ok && k <= T) {
-      if (k & 1) {                                       // inverse if
-        acc = acc + t;
-        sg = sg + (-1.0 * accg) * t;
-      } else {
-        acc = acc - t;
-        sg = sg + (1.0 * accg) * t;
-      }
-      s = s + logi(k + nu);                              // s *= kn
-      s = s + logi(k);                                   // s *= k
-      s = s - h2;                                        // s /= halfz2
-      h2g = h2g + 1.0 * sg;
-      t = rexp(s, tab, code);
-      if (!code && chk && !(t > thr)) code = RL_ERR_POSTCONDITION;
-    }
+  const unsigned Tmin = __reduce_min_sync(FULL_MASK, fwd_ok ? (unsigned)T : 0x7fffffffu);
+  int kr = Tmax;
+  for (; kr > ktab; kr--)                                // beyond the table
+    rev_trip<CAREFUL, false, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
+                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
+  for (; kr > (int)Tmin; kr--)                           // tail: predicated
+    rev_trip<CAREFUL, true, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
+                                      fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
+  if (kr >= 1 && !(kr & 1)) {                            // align: pairs start at odd k
+    rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                      h2g, t, code, bad);
+    kr--;
   }
+  for (; kr >= 2; kr -= 2) {                             // main: every live lane active
+    rev_trip<CAREFUL, true, false, 1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                      h2g, t, code, bad);
+    rev_trip<CAREFUL, true, false, 0>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, bad);
+  }
+  if (kr == 1)
+    rev_trip<CAREFUL, true, false, 1>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                      h2g, t, code, bad);
+  double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
     sg = sg + (1.0 * accg) * t;
+    double hzg = 0.0;
     for (int q = nu; q >= 1; q--) {                      // for i = nu:-1:1
       s = s + logi(q);
       s = s - halfz;
@@ -160,9 +282,10 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     hzg = hzg + 1.0 * h2g;
     h2 = h2 - halfz;
     hzg = hzg + 1.0 * h2g;
+    double lz = 0.0 + logz;
     halfz = halfz + LN2;                                 // halfz *= 2
     halfz = halfz - lz;                                  // halfz /= lz
-    lzg = lzg + 1.0 * hzg;
+    const double lzg = 0.0 + 1.0 * hzg;
     lz = lz - logz;                                      // lz /= convert(z)
     zg = zg + (1.0 * lzg) / z;
     if (chk && !code) {                                  // releases
@@ -175,14 +298,16 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   if (!fwd_ok) o.J = qnan;
   o.dz = fwd_ok ? zg : qnan;
   o.code = code;
+  o.bad = valid && bad;
   return o;
 }
 
-__global__ void __launch_bounds__(BJ_BLOCK, 4) k_besselj_grad(
+__global__ void __launch_bounds__(BJ_BLOCK, 3) k_besselj_grad(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, double *__restrict__ Jout, double *__restrict__ dzout,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
-  __shared__ Exp2Tab s_tab[64];
+  const int ktab = LOGTAB_N - 1 - (nu > 0 ? nu : 0);
+  const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
   __shared__ int s_wsum[BJ_WARPS];
   __shared__ double s_z[BJ_C];
@@ -191,7 +316,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, 4) k_besselj_grad(
   __shared__ uint16_t s_idx[BJ_C];
   __shared__ uint8_t s_fail[BJ_C];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 64) s_tab[tid] = c_exp2tab[tid];
+  if (tid < 64) s_exp2tab[tid] = c_exp2tab[tid];
   unsigned long long trips_sum = 0, nfail = 0;
 
   for (long long base = (long long)blockIdx.x * BJ_C; base < n;
@@ -248,7 +373,11 @@ __global__ void __launch_bounds__(BJ_BLOCK, 4) k_besselj_grad(
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {
         const double z = valid ? s_z[pos] : 1.0;
-        const BJOut o = besselj_element(z, valid, nu, thr, tol, seed, max_trips, chk, s_tab);
+        BJOut o = besselj_element<false>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk);
+        if (__any_sync(FULL_MASK, o.bad)) {              // |exp arg| >= 708 somewhere
+          const BJOut c = besselj_element<true>(z, o.bad, nu, thr, tol, seed, ktab, kfuel, chk);
+          if (o.bad) o = c;
+        }
         if (valid) {
           const int oi = s_idx[pos];
           s_J[oi] = o.J;

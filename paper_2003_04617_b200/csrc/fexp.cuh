@@ -9,7 +9,7 @@
 // reproduces, is correctly rounded in practice; tests/test_fexp.py
 // measures the agreement).  12 FP64 instructions (21 flops) and one 16-byte
 // table read, against ~18.5 instructions (31.5 flops, profiles/
-// fp64_weights.json) for libdevice exp.  Arguments outside [-708, 709]
+// fp64_weights.json) for libdevice exp.  Arguments outside (-708, 708)
 // (subnormal results, overflow) take libdevice's exp.
 //
 // Host-compilable (tests/test_fexp.py builds it with g++ and compares bit
@@ -103,22 +103,42 @@ constexpr double EXP_LN2_64_HI = 0x1.62e42fefa3000p-7;
 constexpr double EXP_LN2_64_LO = 0x1.3de6af278ece6p-48;
 constexpr double EXP_SHIFT = 0x1.8p52;
 
-RL_HD double fexp_core(double x, const Exp2Tab *tab) {
-  // x in [-708, 709]: the caller guarantees the range
-  const double t = fma(x, EXP_INV_LN2_64, EXP_SHIFT);
+// Constants as a struct so that device code can keep them in __constant__
+// memory (they become DFMA constant-bank operands instead of immediates
+// that need two uniform moves each).
+struct ExpConsts {
+  double inv_ln2_64, ln2_64_hi_neg, ln2_64_lo_neg, shift, c6, c5, c4, c3, c2;
+};
+#define RL_EXP_CONSTS_INIT \
+  {EXP_INV_LN2_64, -EXP_LN2_64_HI, -EXP_LN2_64_LO, EXP_SHIFT, 1.0 / 720.0, 1.0 / 120.0, \
+   1.0 / 24.0, 1.0 / 6.0, 0.5}
+
+// `tab` must point to shared memory in device code.
+RL_HD double fexp_core(double x, const Exp2Tab *tab, const ExpConsts &K) {
+  // x in (-708, 708): the caller guarantees the range
+  const double t = fma(x, K.inv_ln2_64, K.shift);
   int64_t tb;
   memcpy(&tb, &t, 8);
   const int j = (int)(int32_t)(uint32_t)tb;          // round(x * 64 / ln2)
-  const double jd = t - EXP_SHIFT;
-  double r = fma(jd, -EXP_LN2_64_HI, x);
-  r = fma(jd, -EXP_LN2_64_LO, r);
-  double q = fma(1.0 / 720.0, r, 1.0 / 120.0);
-  q = fma(q, r, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
+  const double jd = t - K.shift;
+  double r = fma(jd, K.ln2_64_hi_neg, x);
+  r = fma(jd, K.ln2_64_lo_neg, r);
+  double q = fma(K.c6, r, K.c5);
+  q = fma(q, r, K.c4);
+  q = fma(q, r, K.c3);
+  q = fma(q, r, K.c2);
   const double r2 = r * r;
   const double p = fma(q, r2, r);                    // e^r - 1
+#if defined(__CUDA_ARCH__)
+  // 32-bit shared-window address: one LDS.128, no generic-address setup
+  double ehi, elo;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];"
+      : "=d"(ehi), "=d"(elo)
+      : "r"((unsigned)__cvta_generic_to_shared(tab) + (unsigned)((j & 63) << 4)));
+  const Exp2Tab e{ehi, elo};
+#else
   const Exp2Tab e = tab[j & 63];
+#endif
   double res = e.hi + fma(e.hi, p, e.lo);
   // scale by 2^(j >> 6): integer add into the exponent field
   int64_t rb;

@@ -126,7 +126,7 @@ def test_large_batch_properties(cuda, oracle):
     torch.cuda.synchronize()
     assert r.n_failed == 0
     assert int((r.fail != 0).sum().item()) == 0
-    idx = torch.linspace(0, n - 1, 20000, device=cuda).long()
+    idx = torch.linspace(0, n - 1, 20000, dtype=torch.float64, device=cuda).long()
     zs = z[idx].cpu().numpy()
     Jo, dzo, fo, _ = oracle.besselj_grad(2, zs)
     assert close_series(r.J[idx].cpu().numpy(), Jo, 2, zs).all()

@@ -34,7 +34,81 @@ __global__ void k_unary(int which, const double *x, double *out, int reps) {
   out[i] = acc;
 }
 
+// FP64 tensor-core throughput: independent mma.sync accumulators per warp.
+__global__ void __launch_bounds__(256) k_dmma_m8n8k4(double *out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; j++) c[j][0] = c[j][1] = 0.0;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) s += c[j][0] + c[j][1];
+  if (s == 1234.5678) out[0] = s;
+}
+
+__global__ void __launch_bounds__(256) k_dmma_m16n8k16(double *out, int iters) {
+  double a[8], b[4];
+#pragma unroll
+  for (int j = 0; j < 8; j++) a[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll
+  for (int j = 0; j < 4; j++) b[j] = 1.0 - threadIdx.x * 1e-4 - j * 1e-5;
+  double c[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]), "+d"(c[j][2]), "+d"(c[j][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]),
+                     "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) s += c[j][0] + c[j][1] + c[j][2] + c[j][3];
+  if (s == 1234.5678) out[0] = s;
+}
+
 extern "C" {
+
+// which: 0 = m8n8k4 (512 flop/mma), 1 = m16n8k16 (4096 flop/mma); TFLOP/s
+double probe_dmma_peak(int which, int iters, float *ms_out) {
+  int dev = 0, sms = 0, bps = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (which == 0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dmma_m8n8k4, 256, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dmma_m16n8k16, 256, 0);
+  double *out;
+  cudaMalloc(&out, 8);
+  dim3 grid(sms * bps), block(256);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int rep = 0; rep < 2; rep++) {
+    cudaEventRecord(a);
+    if (which == 0) k_dmma_m8n8k4<<<grid, block>>>(out, iters);
+    else k_dmma_m16n8k16<<<grid, block>>>(out, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(out);
+  if (ms_out) *ms_out = ms;
+  const double per_mma = which == 0 ? 2.0 * 8 * 8 * 4 : 2.0 * 16 * 8 * 16;
+  const double mmas = (double)iters * (which == 0 ? 8 : 4) * grid.x * (block.x / 32);
+  return mmas * per_mma / (ms * 1e-3) / 1e12;
+}
+
 
 // Returns achieved FP64 TFLOP/s (2 flops per DFMA) of a kernel lasting ~ms.
 double probe_dfma_peak(int iters, float *ms_out) {

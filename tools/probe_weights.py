@@ -19,5 +19,10 @@ ms = ctypes.c_float()
 for it in (2000, 20000, 50000):
     t = lib.probe_dfma_peak(it, ctypes.byref(ms))
     print(f"dfma peak iters={it}: {t:.2f} TFLOP/s in {ms.value:.2f} ms")
+lib.probe_dmma_peak.restype = ctypes.c_double
+lib.probe_dmma_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+for which, name in ((0, "m8n8k4"), (1, "m16n8k16")):
+    t = lib.probe_dmma_peak(which, 4000, ctypes.byref(ms))
+    print(f"dmma {name}: {t:.2f} TFLOP/s in {ms.value:.2f} ms")
 print(f"THREADS={THREADS} REPS={REPS}")
 sys.exit(0)
