@@ -110,7 +110,7 @@ struct ExpConsts {
   double inv_ln2_64, ln2_64_hi_neg, ln2_64_lo_neg, shift, c6, c5, c4, c3, c2;
 };
 #define RL_EXP_CONSTS_INIT \
-  {EXP_INV_LN2_64, -EXP_LN2_64_HI, -EXP_LN2_64_LO, EXP_SHIFT, 1.0 / 720.0, 1.0 / 120.0, \
+  {rl::EXP_INV_LN2_64, -rl::EXP_LN2_64_HI, -rl::EXP_LN2_64_LO, rl::EXP_SHIFT, 1.0 / 720.0, 1.0 / 120.0, \
    1.0 / 24.0, 1.0 / 6.0, 0.5}
 
 // `tab` must point to shared memory in device code.
