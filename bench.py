@@ -523,6 +523,174 @@ def measured_hbm():
 
 
 # ---------------------------------------------------------------------------
+# GMM workloads (configs[2] d=64 K=25 N=1e4; configs[4] d=128 K=200 N=1e6)
+# ---------------------------------------------------------------------------
+
+GMM_CFG = {"gmm": (64, 25, 10000, 2), "gmm_large": (128, 200, 1000000, 4)}
+
+
+def gmm_constants(d, K, N, gamma, m):
+    import math
+    n = d + m + 1
+    lgd = 0.25 * d * (d - 1) * math.log(math.pi) + sum(
+        math.lgamma(0.5 * n + 0.5 * (1 - j)) for j in range(1, d + 1))
+    C = n * d * (math.log(gamma) - 0.5 * math.log(2.0)) - lgd
+    return -N * d * 0.5 * math.log(2.0 * math.pi) - K * C
+
+
+def gmm_flops(d, K, N, w):
+    """W = 4 N K (d^2 + 3d + 3) + N K (2 w_exp + 8) + 2 N w_log
+    (forward + reverse recompute + 2 adjoint mat-vec passes per point and
+    component, plus the logsumexp)."""
+    return 4.0 * N * K * (d * d + 3 * d + 3) + N * K * (2 * w["exp_libdevice"] + 8) + \
+        2.0 * N * w["log"]
+
+
+def run_gmm_ours(args, D):
+    import torch
+
+    from paper_2003_04617_b200 import _native, kernels
+    dev = torch.device("cuda", D.local)
+    torch.cuda.set_device(dev)
+    d, K, N, seed = GMM_CFG[args.workload]
+    N = args.n or N
+    gamma, m = 1.0, 0
+    cst = gmm_constants(d, K, N, gamma, m)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    alphas = torch.randn(K, dtype=torch.float64, device=dev, generator=g)
+    means = torch.rand((K, d), dtype=torch.float64, device=dev, generator=g)
+    icf = torch.randn((K, d * (d + 1) // 2), dtype=torch.float64, device=dev, generator=g) * 0.5
+    lo, hi = N * D.rank // D.world, N * (D.rank + 1) // D.world
+    x = torch.empty((hi - lo, d), dtype=torch.float64, device=dev)
+    # the rank's slice of one global x ~ U(0,1) (generated in 1M-row pieces)
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(seed + 1)
+    row = 0
+    while row < hi:
+        n = min(1 << 20, N - row)
+        blk = torch.rand((n, d), dtype=torch.float64, device=dev, generator=gx)
+        a, b = max(row, lo), min(row + n, hi)
+        if a < b:
+            x[a - lo:b - lo] = blk[a - row:b - row]
+        row += n
+    L = _native.lib()
+    ws = torch.empty(max(1, L.rl_gmm_workspace_bytes(d, K, hi - lo)), dtype=torch.uint8, device=dev)
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def step():
+        r = kernels.gmm_grad(alphas, means, icf, x, gamma, m, cst, N_total=N,
+                             add_param_terms=(D.rank == 0), workspace=ws, counters=counters)
+        if D.dist is not None:
+            D.dist.all_reduce(r.packed)        # the one collective: parameter adjoints
+        return r
+
+    for _ in range(max(args.warmup, 3)):
+        r = step()
+    torch.cuda.synchronize()
+    props = torch.cuda.get_device_properties(dev)
+    sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
+    sampler.start()
+    time.sleep(0.25)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    D.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for a, b in evs:
+        flush.fill_(1)                      # evict L2 between evaluations
+        a.record(stream)
+        r = step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms_step = D.max(ms)
+    w = load_weights()
+    peak, _ = fp64_peak_tflops()
+    roof = None
+    if w is not None:
+        fl = gmm_flops(d, K, N, w)
+        P = d * (d + 1) // 2
+        executed = 2.0 * 3 * N * K * P
+        roof = {"bound": "fp64", "achieved": round(fl / (ms_step * 1e-3) / 1e12, 3),
+                "peak": round(peak, 3), "unit": "TFLOP/s",
+                "frac": round(fl / (ms_step * 1e-3) / 1e12 / peak, 4), "traffic": None,
+                "flops_per_eval_survey_W": fl,
+                "mat_vec_flops_executed": executed,
+                "executed_frac": round(executed / (ms_step * 1e-3) / 1e12 / peak, 4),
+                "peak_source": "in-run DFMA microkernel (tools/fp64probe.cu)"}
+    parity = None
+    if D.rank == 0 and args.workload == "gmm" and D.world == 1:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle as O
+        t0 = time.perf_counter()
+        rc, e, ga, gm, gi = O.gmm_grad(alphas.cpu().numpy(), means.cpu().numpy(),
+                                       icf.cpu().numpy(), x.cpu().numpy(), gamma, m, cst)
+        dt_cpu = time.perf_counter() - t0
+        rel = lambda a, b: float(np.max(np.abs(a - b)) / np.max(np.abs(b)))  # noqa: E731
+        parity = {"oracle_rc": rc, "rel_err": abs(float(r.err.item()) - e) / abs(e),
+                  "max_rel_alphas": rel(r.g_alphas.cpu().numpy(), ga),
+                  "max_rel_means": rel(r.g_means.cpu().numpy(), gm),
+                  "max_rel_icf": rel(r.g_icf.cpu().numpy(), gi), "oracle_s": round(dt_cpu, 2)}
+    res = {
+        "metric": "gradient evals/sec", "value": round(1e3 / ms_step, 3), "unit": "evals/s",
+        "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic alphas~N(0,1), means~U(0,1), icf~N(0,.5^2), x~U(0,1), seed {seed}",
+        "config": {"workload": f"gmm_d{d}_K{K}_N{N}", "d": d, "K": K, "N": N,
+                   "per_rank": hi - lo, "parallelism": f"dp{D.world}+allreduce",
+                   "l2": "256 MiB L2 flush before every evaluation"},
+        "roofline": roof, "gpu_launches": 6 * args.steps, "clocks": clocks,
+        "failed_per_step": D.sum(int(counters[1].item())) // (args.steps + max(args.warmup, 3)),
+        "parity_sample": parity,
+    }
+    if not args.no_e2e and D.world == 1:
+        res["e2e"] = gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D)
+    if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline and parity is not None:
+        res["cpu_baseline"] = {"value": round(1.0 / parity["oracle_s"], 5), "unit": "evals/s",
+                               "cores": 1, "kind": "port",
+                               "sample": f"one full evaluation (N={N}) of the sequential oracle "
+                                         "(all 4 reference sweeps, 8 mat-vec passes per point "
+                                         "and component; scratch shared across points, so it "
+                                         "does not parallelise)"}
+    return res
+
+
+def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
+    import ctypes
+
+    import torch
+
+    from paper_2003_04617_b200 import _native
+    L = _native.lib()
+    K, d = means.shape
+    N = x.shape[0]
+    ha, hm, hi_ = alphas.cpu(), means.cpu(), icf.cpu()
+    hx = x.cpu().pin_memory()
+    out = torch.empty(1 + K + K * d + K * d * (d + 1) // 2, dtype=torch.float64).pin_memory()
+    nf = ctypes.c_ulonglong()
+
+    def call():
+        rc = L.rl_gmm_grad_f64_host(d, K, N, ha.data_ptr(), hm.data_ptr(), hi_.data_ptr(),
+                                    hx.data_ptr(), gamma, m, cst, 1e-9, 1, out.data_ptr(),
+                                    ctypes.byref(nf), D.local)
+        _native.check(rc, "rl_gmm_grad_f64_host")
+    call()
+    steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": round(1.0 / dt, 3), "unit": "evals/s",
+            "h2d_bytes_per_step": int(hx.numel() * 8 + (ha.numel() + hm.numel() + hi_.numel()) * 8),
+            "d2h_bytes_per_step": int(out.numel() * 8), "ms_per_step": round(dt * 1e3, 3),
+            "path": "rl_gmm_grad_f64_host (host buffers; allocates its device workspace per call)"}
+
+
+# ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
 
@@ -559,6 +727,8 @@ def main():
         res = run_ba_ours(args, D)
         if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = ba_cpu()
+    elif args.workload in GMM_CFG:
+        res = run_gmm_ours(args, D)
     else:
         raise SystemExit(f"workload {args.workload} not wired yet")
     if D.rank == 0:

@@ -50,10 +50,11 @@ __constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
 __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 
 constexpr int BJ_BLOCK = 256;
-constexpr int BJ_M = 4;
+constexpr int BJ_M = 8;
 constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
 constexpr int BJ_NB = 256;              // z buckets
 constexpr int BJ_WARPS = BJ_BLOCK / 32;
+constexpr int BJ_SMEM = BJ_C * (3 * 8 + 2 + 1);          // dynamic smem per block
 
 // 2^(i/64) table, copied to shared memory per block (lane-varying index)
 __shared__ Exp2Tab s_exp2tab[64];
@@ -208,16 +209,47 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     act = false;
   }
   const int kend = ktab < kfuel ? ktab : kfuel;
-  // main phase: every non-dead lane still active -> no predication; two
-  // trips per iteration (odd, even) so the series sign is static
-  if (__all_sync(FULL_MASK, act || dead)) {
+  // main phase: every non-dead lane still active -> no predication.  Two
+  // trips (odd k+1, even k+2) are computed speculatively per warp vote: the
+  // term s of trip k+2 does not depend on exp() of trip k+1, so the two exp
+  // chains overlap; a lane whose loop ended at k+1 keeps its trip-(k+1)
+  // state and discards trip k+2.
+  if (!CAREFUL && __all_sync(FULL_MASK, act || dead)) {
     while (k + 2 <= kend) {
-      fwd_trip<CAREFUL, true, false, 1>(k + 1, nu, h2, thr, act, s, t, acc, T, code, bad);
-      k++;
-      if (!__all_sync(FULL_MASK, act || dead)) break;
-      fwd_trip<CAREFUL, true, false, 0>(k + 1, nu, h2, thr, act, s, t, acc, T, code, bad);
-      k++;
-      if (!__all_sync(FULL_MASK, act || dead)) break;
+      double s1 = s + h2;                                // trip k+1 (odd)
+      s1 = s1 - c_logtab[k + 1];
+      s1 = s1 - c_logtab[k + 1 + nu];
+      double s2 = s1 + h2;                               // trip k+2 (even)
+      s2 = s2 - c_logtab[k + 2];
+      s2 = s2 - c_logtab[k + 2 + nu];
+      const double t1 = rexp<CAREFUL>(s1, bad).t;
+      const double t2 = rexp<CAREFUL>(s2, bad).t;
+      const double a1 = acc - t1;                        // odd k subtracts
+      const double a2 = a1 + t2;                         // even k adds
+      const bool act1 = t1 > thr, act2 = t2 > thr;
+      if (__all_sync(FULL_MASK, (act1 && act2) || dead)) {
+        s = s2;
+        t = t2;
+        acc = a2;
+        k += 2;
+        T = k;
+        continue;
+      }
+      if (act1) {
+        s = s2;
+        t = t2;
+        acc = a2;
+        T = k + 2;
+        act = act2;
+      } else {
+        s = s1;
+        t = t1;
+        acc = a1;
+        T = k + 1;
+        act = false;
+      }
+      k += 2;
+      break;
     }
     if (dead) {                                          // undo the unpredicated trips
       act = false;
@@ -310,11 +342,12 @@ __global__ void __launch_bounds__(BJ_BLOCK, 3) k_besselj_grad(
   const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
   __shared__ int s_wsum[BJ_WARPS];
-  __shared__ double s_z[BJ_C];
-  __shared__ double s_J[BJ_C];
-  __shared__ double s_dz[BJ_C];
-  __shared__ uint16_t s_idx[BJ_C];
-  __shared__ uint8_t s_fail[BJ_C];
+  extern __shared__ __align__(16) double bj_dyn[];     // BJ_SMEM bytes
+  double *s_z = bj_dyn;
+  double *s_J = s_z + BJ_C;
+  double *s_dz = s_J + BJ_C;
+  uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dz + BJ_C);
+  uint8_t *s_fail = reinterpret_cast<uint8_t *>(s_idx + BJ_C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 64) s_exp2tab[tid] = c_exp2tab[tid];
   unsigned long long trips_sum = 0, nfail = 0;
@@ -422,14 +455,17 @@ int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double to
   if (rc) return rc;
   if (n == 0) return RL_OK;
   int blocks_per_sm = 0;
+  rc = cuda_status(cudaFuncSetAttribute(k_besselj_grad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        BJ_SMEM), "smem attr");
+  if (rc) return rc;
   rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj_grad,
-                                                                 BJ_BLOCK, 0),
+                                                                 BJ_BLOCK, BJ_SMEM),
                    "occupancy");
   if (rc) return rc;
   const long long want = (n + BJ_C - 1) / BJ_C;
   const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   const int grid = (int)(want < cap ? want : cap);
-  k_besselj_grad<<<grid, BJ_BLOCK, 0, st>>>(nu, z, n, thr, tol, seed, max_trips,
+  k_besselj_grad<<<grid, BJ_BLOCK, BJ_SMEM, st>>>(nu, z, n, thr, tol, seed, max_trips,
                                             invcheck ? 1 : 0, J, dJdz, fail, counters);
   return cuda_status(cudaGetLastError(), "k_besselj_grad launch");
 }
