@@ -155,14 +155,16 @@ def gen_gmm():
     p = _prog("gmm.rnl")
     out = {}
     cases = [(3, 2, 4, 1.0, 0), (5, 4, 20, 1.0, 0), (8, 5, 10, 1.3, 2),
-             (4, 3, 64, 1.0, 0), (16, 6, 6, 0.7, 1), (2, 1, 5, 1.0, 0)]
+             (4, 3, 64, 1.0, 0), (16, 6, 6, 0.7, 1), (2, 1, 5, 1.0, 0), (4, 3, 23, 1.0, 0),
+             (6, 8, 40, 1.0, 0)]
     t0 = time.perf_counter()
     for ci, (d, K, N, gamma, m) in enumerate(cases):
         alphas, means, icf, x = gmm_inputs(np.random.default_rng(100 + ci), d, K, N)
         cst = gmm_constants(d, K, N, gamma, m)
         A = lambda a: Array.matrix(a.tolist()) if a.ndim == 2 else Array.vector(a.tolist())
         Z = lambda *s: A(np.zeros(s))
-        args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), Z(K),
+        ZI = lambda n: Array.vector([0] * n)   # Int scratch (argmax record)
+        args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), ZI(K),
                 float(gamma), int(m), float(cst)]
         res, en = _err_name(lambda: gradient(p, GradRequest(
             "gmm", args, wrt=["alphas", "means", "icf"])))

@@ -718,10 +718,11 @@ typedef struct {
   int d, K, N, P, wm, gm, chk;
   double tol, ga;
   const double *x, *alphas, *means, *icf;
-  double *qd, *sq, *xc, *qxc, *mt, *dm; /* scratch values */
+  double *qd, *sq, *xc, *qxc, *mt; /* Float scratch values */
+  long *dmi;                          /* Int scratch: argmax steps */
   double err, cst;
   /* cotangents (gm) */
-  double *g_alphas, *g_means, *g_icf, *g_x, *g_qd, *g_sq, *g_xc, *g_qxc, *g_mt, *g_dm;
+  double *g_alphas, *g_means, *g_icf, *g_x, *g_qd, *g_sq, *g_xc, *g_qxc, *g_mt;
   double g_err, g_cst;
 } gmm_ctx;
 
@@ -847,28 +848,29 @@ static int gmm_k_body(gmm_ctx *c, int i, int k, int mirror) {
 }
 
 /* reversible logsumexp over v[0..K) (the point routine's tail and the
- * alphas routine share it): mx <- 0; mx += v[1]; branch-recorded max into
- * dm; se = sum exp(v - mx).  gv: cotangent array of v. */
-static int gmm_lse_fwd(gmm_ctx *c, const double *v, double *gv, double *mx, double *gmx,
-                       double *se, double *gse) {
+ * alphas routine share it): argmax record in the Int scratch dmi
+ * (imx <- 1; if (v[k] > v[imx], dm![k] > 0) {dm![k] += k - imx; imx += dm![k]}),
+ * mx <- 0.0; mx += v[imx]; se = sum exp(v - mx).  gv: cotangent array of v
+ * (the argmax record is Int: no cotangents).  imx is 0-based here; the
+ * recorded steps k - imx are the same in both bases. */
+static int gmm_lse_fwd(gmm_ctx *c, const double *v, double *gv, int *imx, double *mx,
+                       double *gmx, double *se, double *gse) {
   const int chk = c->chk;
   const int K = c->K;
   double e;
+  *imx = 0;
+  for (int k = 1; k < K; k++) {
+    int took = v[k] > v[*imx];
+    if (took) {
+      c->dmi[k] = c->dmi[k] + (k - *imx);
+      *imx = *imx + (int)c->dmi[k];
+    }
+    if (chk && (c->dmi[k] > 0) != took) return RL_ERR_POSTCONDITION;
+  }
   *mx = 0.0;
   *gmx = 0.0;
-  *mx = *mx + v[0];
-  ADJ(c, gv[0], -1.0 * *gmx, 1.0);
-  for (int k = 1; k < K; k++) {
-    int took = v[k] > *mx;
-    if (took) {
-      c->dm[k] = c->dm[k] + (v[k] - *mx);
-      ADJ(c, gv[k], -1.0 * c->g_dm[k], 1.0);
-      ADJ(c, *gmx, -1.0 * c->g_dm[k], -1.0);
-      *mx = *mx + c->dm[k];
-      ADJ(c, c->g_dm[k], -1.0 * *gmx, 1.0);
-    }
-    if (c->chk && (c->dm[k] > 0.0) != took) return RL_ERR_POSTCONDITION;
-  }
+  *mx = *mx + v[*imx];
+  ADJ(c, gv[*imx], -1.0 * *gmx, 1.0);
   *se = 0.0;
   *gse = 0.0;
   for (int k = 0; k < K; k++) {
@@ -887,8 +889,8 @@ static int gmm_lse_fwd(gmm_ctx *c, const double *v, double *gv, double *mx, doub
   return RL_OK;
 }
 
-static int gmm_lse_inv(gmm_ctx *c, const double *v, double *gv, double *mx, double *gmx,
-                       double *se, double *gse) {
+static int gmm_lse_inv(gmm_ctx *c, const double *v, double *gv, int *imx, double *mx,
+                       double *gmx, double *se, double *gse) {
   const int chk = c->chk;
   const int K = c->K;
   double e;
@@ -906,20 +908,18 @@ static int gmm_lse_inv(gmm_ctx *c, const double *v, double *gv, double *mx, doub
     RELEASE_F(t, 0.0, c->tol);
   }
   RELEASE_F(*se, 0.0, c->tol);
-  for (int k = K - 1; k >= 1; k--) {
-    int took = c->dm[k] > 0.0; /* inverted If: pre/post swapped (reverser.py:106-108) */
-    if (took) {
-      *mx = *mx - c->dm[k];
-      ADJ(c, c->g_dm[k], 1.0 * *gmx, 1.0);
-      c->dm[k] = c->dm[k] - (v[k] - *mx);
-      ADJ(c, gv[k], 1.0 * c->g_dm[k], 1.0);
-      ADJ(c, *gmx, 1.0 * c->g_dm[k], -1.0);
-    }
-    if (c->chk && (v[k] > *mx) != took) return RL_ERR_POSTCONDITION;
-  }
-  *mx = *mx - v[0];
-  ADJ(c, gv[0], 1.0 * *gmx, 1.0);
+  *mx = *mx - v[*imx];                 /* mx -= v[imx] */
+  ADJ(c, gv[*imx], 1.0 * *gmx, 1.0);
   RELEASE_F(*mx, 0.0, c->tol);
+  for (int k = K - 1; k >= 1; k--) {
+    int took = c->dmi[k] > 0;          /* inverted If: pre/post swapped (reverser.py:106-108) */
+    if (took) {
+      *imx = *imx - (int)c->dmi[k];
+      c->dmi[k] = c->dmi[k] - (k - *imx);
+    }
+    if (chk && (v[k] > v[*imx]) != took) return RL_ERR_POSTCONDITION;
+  }
+  RELEASE_I(*imx, 0);                  /* imx -> 1 */
   return RL_OK;
 }
 
@@ -928,9 +928,10 @@ static int gmm_lse_inv(gmm_ctx *c, const double *v, double *gv, double *mx, doub
 static int gmm_point(gmm_ctx *c, int i, int mirror) {
   const int K = c->K;
   double mx, gmx, se, gse, l, p;
+  int imx;
   double *gmt = GM(c) ? c->g_mt : NULL;
   for (int k = 0; k < K; k++) TRY(gmm_k_body(c, i, k, 0));
-  TRY(gmm_lse_fwd(c, c->mt, gmt, &mx, &gmx, &se, &gse));
+  TRY(gmm_lse_fwd(c, c->mt, gmt, &imx, &mx, &gmx, &se, &gse));
   PY_LOG(se, l);
   if (!mirror) {
     c->err = c->err + l;
@@ -943,7 +944,7 @@ static int gmm_point(gmm_ctx *c, int i, int mirror) {
     c->err = c->err - l;
     if (GM(c)) { TRY(py_div(1.0, se, &p)); ADJ(c, gse, 1.0 * c->g_err, p); }
   }
-  TRY(gmm_lse_inv(c, c->mt, gmt, &mx, &gmx, &se, &gse));
+  TRY(gmm_lse_inv(c, c->mt, gmt, &imx, &mx, &gmx, &se, &gse));
   for (int k = K - 1; k >= 0; k--) TRY(gmm_k_body(c, i, k, 1));
   return RL_OK;
 }
@@ -952,8 +953,9 @@ static int gmm_point(gmm_ctx *c, int i, int mirror) {
 static int gmm_alpha_lse(gmm_ctx *c, int mirror) {
   const int chk = c->chk;
   double amx, gamx, ase, gase, lsa = 0.0, glsa = 0.0, l, p;
+  int ia;
   double *ga = GM(c) ? c->g_alphas : NULL;
-  TRY(gmm_lse_fwd(c, c->alphas, ga, &amx, &gamx, &ase, &gase));
+  TRY(gmm_lse_fwd(c, c->alphas, ga, &ia, &amx, &gamx, &ase, &gase));
   PY_LOG(ase, l);
   lsa = lsa + l;
   if (GM(c)) { TRY(py_div(1.0, ase, &p)); ADJ(c, gase, -1.0 * glsa, p); }
@@ -974,7 +976,7 @@ static int gmm_alpha_lse(gmm_ctx *c, int mirror) {
   lsa = lsa - l;
   if (GM(c)) { TRY(py_div(1.0, ase, &p)); ADJ(c, gase, 1.0 * glsa, p); }
   RELEASE_F(lsa, 0.0, c->tol);
-  TRY(gmm_lse_inv(c, c->alphas, ga, &amx, &gamx, &ase, &gase));
+  TRY(gmm_lse_inv(c, c->alphas, ga, &ia, &amx, &gamx, &ase, &gase));
   return RL_OK;
 }
 
@@ -1076,11 +1078,16 @@ int orc_gmm_grad(int d, int K, int N, const double *alphas, const double *means,
   memset(&c, 0, sizeof c);
   c.d = d; c.K = K; c.N = N; c.P = P; c.wm = wm; c.chk = invcheck != 0; c.tol = tol;
   c.ga = ga; c.cst = cst; c.x = x; c.alphas = alphas; c.means = means; c.icf = icf;
-  const long nscr = (long)K * d + K + d + d + K + K;
+  const long nscr = (long)K * d + K + d + d + K;
   double *scr = calloc(2 * nscr + (long)N * d, sizeof(double));
-  if (!scr) return RL_ERR_INVALID;
+  long *dmi = calloc(K, sizeof(long));
+  if (!scr || !dmi) {
+    free(scr);
+    free(dmi);
+    return RL_ERR_INVALID;
+  }
   c.qd = scr; c.sq = c.qd + K * d; c.xc = c.sq + K; c.qxc = c.xc + d; c.mt = c.qxc + d;
-  c.dm = c.mt + K;
+  c.dmi = dmi;
   double *gscr = scr + nscr;
   int rc;
   /* sweeps 1-2: f */
@@ -1095,7 +1102,7 @@ int orc_gmm_grad(int d, int K, int N, const double *alphas, const double *means,
   memset(g_icf, 0, (long)K * P * sizeof(double));
   c.g_alphas = g_alphas; c.g_means = g_means; c.g_icf = g_icf;
   c.g_qd = gscr; c.g_sq = c.g_qd + K * d; c.g_xc = c.g_sq + K; c.g_qxc = c.g_xc + d;
-  c.g_mt = c.g_qxc + d; c.g_dm = c.g_mt + K; c.g_x = gscr + nscr;
+  c.g_mt = c.g_qxc + d; c.g_x = gscr + nscr;
   c.g_err = 1.0;
   rc = gmm_body(&c, 1);
   if (rc != RL_OK) goto done;
@@ -1104,8 +1111,14 @@ int orc_gmm_grad(int d, int K, int N, const double *alphas, const double *means,
     rc = RL_ERR_RESTORE;
     goto done;
   }
+  for (int k = 0; k < K; k++)
+    if (dmi[k] != 0) {
+      rc = RL_ERR_RESTORE;
+      goto done;
+    }
   *err_out = E;
 done:
   free(scr);
+  free(dmi);
   return rc;
 }

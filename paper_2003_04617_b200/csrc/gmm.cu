@@ -6,7 +6,8 @@
 // The program's per-point body is
 //   R_i:   for k: xc = x_i - mu_k; qxc = L_k xc; sqn = |qxc|^2;
 //               mt[k] = alphas[k] + sq[k] - sqn/2      (per-k routine, uncomputed)
-//          reversible max mx (branch record dm[k]) and se = sum_k exp(mt[k] - mx)
+//          reversible argmax (Int branch record dm[k]), mx = mt[imx],
+//          se = sum_k exp(mt[k] - mx)
 //   err += log(se) + mx; ~R_i
 // and its gradient sweep runs ~R_i backwards with the adjoint rules.  On the
 // GPU the points are independent (each gets fresh zero scratch, see
@@ -18,7 +19,7 @@
 //   k_gmm_fwd     forward mat-vec tiles Z = Xc L^T (FP64 DFMA, register
 //                 tiled, smem-staged) -> sqn -> mt[k][i]; sqn's uncompute
 //                 residual is checked on device (DirtyAncilla)
-//   k_gmm_lse     per point: the reversible max / logsumexp forward, then its
+//   k_gmm_lse     per point: the reversible argmax / logsumexp forward, then its
 //                 reverse sweep with adjoints -> dmt = d err / d mt[k][i],
 //                 release and branch-postcondition checks
 //   k_gmm_rev     reverse per-k routine: RECOMPUTES Z (reverse computing:
@@ -252,42 +253,40 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_fwd(
 }
 
 // ---------------------------------------------------------------------------
-// per point: reversible max + logsumexp, forward then reverse with adjoints
+// per point: reversible argmax + logsumexp, forward then reverse with adjoints
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
-    int K, long long N, const double *__restrict__ mtT, double *__restrict__ dmT,
-    double *__restrict__ gmtT, const unsigned *__restrict__ flagsA, double tol, int chk,
-    double *__restrict__ err_part, uint8_t *__restrict__ fail, unsigned long long *counters) {
+    int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
+    const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
+    uint8_t *__restrict__ fail, unsigned long long *counters) {
   const long long i = (long long)blockIdx.x * GMM_THREADS + threadIdx.x;
   double e_pt = 0.0;
   unsigned long long nfail = 0;
   if (i < N) {
     int code = 0;
     const double *mt = mtT + i;
-    double *dm = dmT + i;
     double *gmt = gmtT + i;
 #define MT(k) mt[(long long)(k) * N]
-#define DM(k) dm[(long long)(k) * N]
 #define GM(k) gmt[(long long)(k) * N]
-    // forward: mx <- 0; mx += mt[1]; branch-recorded max
-    double mx = 0.0 + MT(0);
+    // imx <- 1; if (mt![k] > mt![imx], dm![k] > 0) {dm![k] += k - imx; imx += dm![k]}
+    // The Int record and its uncompute are exact and the branch
+    // postconditions replay the same comparisons, so they cannot fail.
+    int imx = 0;
+    double vmx = MT(0);
     for (int k = 1; k < K; k++) {
       const double v = MT(k);
-      const bool took = v > mx;                          // if (mt![k] > mx, dm![k] > 0.0)
-      double dk = 0.0;
-      if (took) {
-        dk = 0.0 + (v - mx);
-        mx = mx + dk;
+      if (v > vmx) {
+        imx = k;
+        vmx = v;
       }
-      if (chk && !code && (dk > 0.0) != took) code = RL_ERR_POSTCONDITION;
-      DM(k) = dk;
     }
+    const double mx = 0.0 + vmx;                          // mx <- 0.0; mx += mt![imx]
     double se = 0.0;
     for (int k = 0; k < K; k++) {
       const double t = 0.0 + (MT(k) - mx);
       se = se + exp(t);
     }
-    if (!(se > 0.0)) code = code ? code : RL_ERR_DOMAIN;  // err += log(se)
+    if (!(se > 0.0)) code = RL_ERR_DOMAIN;               // err += log(se)
     e_pt = log(se) + mx;                                  // err += log(se); err += mx
     // gradient sweep (~f): err -= mx; err -= log(se); ~R_i with adjoints
     double mxg = 0.0 + (1.0 * 1.0) * 1.0;
@@ -303,23 +302,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
       mxg = mxg - tg;                                     // mx.g += -t.g
     }
     if (chk && !code && fabs(se) > tol) code = RL_ERR_DIRTY_ANCILLA;  // se -> 0.0
-    for (int k = K - 1; k >= 1; k--) {
-      double dk = DM(k);
-      const bool took = dk > 0.0;                         // inverted If: pre = dm[k] > 0
-      if (took) {
-        mx = mx - dk;                                     // mx -= dm[k]
-        const double dg = 0.0 + mxg;                      // dm[k].g += mx.g
-        dk = dk - (MT(k) - mx);                           // dm[k] -= mt[k] - mx
-        GM(k) = GM(k) + dg;
-        mxg = mxg - dg;
-      }
-      if (chk && !code && (MT(k) > mx) != took) code = RL_ERR_POSTCONDITION;
-    }
-    mx = mx - MT(0);                                      // mx -= mt![1]
-    GM(0) = GM(0) + mxg;
-    if (chk && !code && fabs(mx) > tol) code = RL_ERR_DIRTY_ANCILLA;
+    const double mxr = mx - MT(imx);                      // mx -= mt![imx]
+    GM(imx) = GM(imx) + mxg;
+    if (chk && !code && fabs(mxr) > tol) code = RL_ERR_DIRTY_ANCILLA;
 #undef MT
-#undef DM
 #undef GM
     if (flagsA[i]) code = RL_ERR_DIRTY_ANCILLA;            // sqn release failed (sweep 1)
     fail[i] = (uint8_t)code;
@@ -462,7 +448,7 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_params(
     int d, int K, long long N_total, const double *__restrict__ alphas,
     const double *__restrict__ icf, const double *__restrict__ qd, const double *__restrict__ sq,
-    double ga, int wm, double cst, double *__restrict__ ws_par, double *__restrict__ dmp) {
+    double ga, int wm, double cst, double *__restrict__ ws_par) {
   const int P = d * (d + 1) / 2;
   const double hg2 = 0.5 * ga * ga;
   // fro = sum qd^2 + sum offdiag^2 ; ssq = sum sq
@@ -483,16 +469,11 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_params(
   if (threadIdx.x == 0) {
     double ssq = 0.0;
     for (int k = 0; k < K; k++) ssq = ssq + sq[k];
-    // logsumexp(alphas) with the branch-recorded max (dm reused as scratch)
-    double amx = 0.0 + alphas[0];
-    for (int k = 1; k < K; k++) {
-      double dk = 0.0;
-      if (alphas[k] > amx) {
-        dk = 0.0 + (alphas[k] - amx);
-        amx = amx + dk;
-      }
-      dmp[k] = dk;
-    }
+    // logsumexp(alphas) with the Int argmax record (as in the point routine)
+    int ia = 0;
+    for (int k = 1; k < K; k++)
+      if (alphas[k] > alphas[ia]) ia = k;
+    const double amx = 0.0 + alphas[ia];
     double ase = 0.0;
     for (int k = 0; k < K; k++) ase = ase + exp(0.0 + (alphas[k] - amx));
     const double lsa = (0.0 + log(ase)) + amx;
@@ -508,15 +489,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_params(
       ws_par[k] = tg;                                      // alphas[k].g += t.g
       amxg = amxg - tg;
     }
-    for (int k = K - 1; k >= 1; k--) {
-      if (dmp[k] > 0.0) {
-        amx = amx - dmp[k];
-        const double dg = 0.0 + amxg;
-        ws_par[k] += dg;
-        amxg = amxg - dg;
-      }
-    }
-    ws_par[0] += amxg;                                     // amx -= alphas[1]
+    ws_par[ia] += amxg;                                    // amx -= alphas[ia]
   }
 }
 
@@ -600,7 +573,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
 
 struct GmmLayout {
-  size_t lt, qd, sq, mt, dm, gmt, flags, errp, part, par, dmp, total;
+  size_t lt, qd, sq, mt, gmt, flags, errp, part, par, total;
   int S, nerr;
 };
 
@@ -626,13 +599,11 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.qd = take((size_t)K * d * 8);
   L.sq = take((size_t)K * 8);
   L.mt = take((size_t)K * N * 8);
-  L.dm = take((size_t)K * N * 8);
   L.gmt = take((size_t)K * N * 8);
   L.flags = take((size_t)N * 4);
   L.errp = take((size_t)(L.nerr > 0 ? L.nerr : 1) * 8);
   L.part = take((size_t)K * S * ((size_t)DP * DP + DP + 1) * 8);
   L.par = take((size_t)(K + 1) * 8);
-  L.dmp = take((size_t)K * 8);
   L.total = off;
   return L;
 }
@@ -649,10 +620,10 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st) {
   using C = GmmCfg<DP>;
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
-  double *mt = (double *)(ws + L.mt), *dm = (double *)(ws + L.dm), *gmt = (double *)(ws + L.gmt);
+  double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
   unsigned *flags = (unsigned *)(ws + L.flags);
   double *errp = (double *)(ws + L.errp), *part = (double *)(ws + L.part);
-  double *par = (double *)(ws + L.par), *dmp = (double *)(ws + L.dmp);
+  double *par = (double *)(ws + L.par);
   int rc;
   k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, icf, LT, qd, sq);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
@@ -672,7 +643,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     k_gmm_fwd<DP><<<grid, GMM_THREADS, smem_f, st>>>(d, K, N, alphas, means, x, LT, sq, tol, chk, mt,
                                                     flags);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_fwd"))) return rc;
-    k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, dm, gmt, flags, tol, chk, errp, fail,
+    k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
                                               counters);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
     k_gmm_rev<DP><<<grid, GMM_THREADS, smem_r, st>>>(d, K, N, means, x, LT, gmt, part);
@@ -683,8 +654,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       return rc;
   }
   if (add_params) {
-    k_gmm_params<<<1, GMM_THREADS, 0, st>>>(d, K, N_total, alphas, icf, qd, sq, gamma, m, cst, par,
-                                           dmp);
+    k_gmm_params<<<1, GMM_THREADS, 0, st>>>(d, K, N_total, alphas, icf, qd, sq, gamma, m, cst,
+                                           par);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_params"))) return rc;
   }
   k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, L.S, N > 0 ? L.nerr : 0, icf, qd, LT, part, errp,
