@@ -72,7 +72,8 @@ template <int DP>
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const double *__restrict__ icf,
                                                           double *__restrict__ LT,
                                                           double *__restrict__ qd,
-                                                          double *__restrict__ sq) {
+                                                          double *__restrict__ sq,
+                                                          double *__restrict__ fro) {
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
   const double *ic = icf + (long long)k * P;
@@ -102,7 +103,25 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const do
       sq[k] = s;
     }
   }
-  for (int j = threadIdx.x; j < d; j += GMM_THREADS) qd[(long long)k * d + j] = exp(ic[j]);
+  // qd and this component's share of the prior's Frobenius sum:
+  // fro += abs2(qd![k, j]) (j <= d) or abs2(icf[k, j]) (j > d)
+  double f = 0.0;
+  for (int j = threadIdx.x; j < P; j += GMM_THREADS) {
+    double v = ic[j];
+    if (j < d) {
+      v = exp(v);
+      qd[(long long)k * d + j] = v;
+    }
+    f = fma(v, v, f);
+  }
+  __shared__ double red[GMM_THREADS];
+  red[threadIdx.x] = f;
+  __syncthreads();
+  for (int o = GMM_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fro[k] = red[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -445,27 +464,13 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
 // parameter-only terms: -N lse(alphas) (reversible max, as in the program),
 // Wishart prior, cst.  ws_par = [g_alpha_param (K), err_param]
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(GMM_THREADS) k_gmm_params(
+__global__ void __launch_bounds__(32) k_gmm_params(
     int d, int K, long long N_total, const double *__restrict__ alphas,
-    const double *__restrict__ icf, const double *__restrict__ qd, const double *__restrict__ sq,
-    double ga, int wm, double cst, double *__restrict__ ws_par) {
-  const int P = d * (d + 1) / 2;
+    const double *__restrict__ fro_k, const double *__restrict__ sq, double ga, int wm, double cst,
+    double *__restrict__ ws_par) {
   const double hg2 = 0.5 * ga * ga;
-  // fro = sum qd^2 + sum offdiag^2 ; ssq = sum sq
   double fro = 0.0;
-  for (long long e = threadIdx.x; e < (long long)K * P; e += GMM_THREADS) {
-    const int k = (int)(e / P), j = (int)(e - (long long)k * P);
-    const double v = j < d ? qd[(long long)k * d + j] : icf[e];
-    fro = fma(v, v, fro);
-  }
-  __shared__ double red[GMM_THREADS];
-  red[threadIdx.x] = fro;
-  __syncthreads();
-  for (int o = GMM_THREADS / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  fro = red[0];
+  for (int k = 0; k < K; k++) fro = fro + fro_k[k];
   if (threadIdx.x == 0) {
     double ssq = 0.0;
     for (int k = 0; k < K; k++) ssq = ssq + sq[k];
@@ -573,7 +578,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
 
 struct GmmLayout {
-  size_t lt, qd, sq, mt, gmt, flags, errp, part, par, total;
+  size_t lt, qd, sq, fro, mt, gmt, flags, errp, part, par, total;
   int S, nerr;
 };
 
@@ -598,6 +603,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.lt = take((size_t)K * lt_size(DP) * 8);
   L.qd = take((size_t)K * d * 8);
   L.sq = take((size_t)K * 8);
+  L.fro = take((size_t)K * 8);
   L.mt = take((size_t)K * N * 8);
   L.gmt = take((size_t)K * N * 8);
   L.flags = take((size_t)N * 4);
@@ -620,12 +626,13 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st) {
   using C = GmmCfg<DP>;
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
+  double *fro = (double *)(ws + L.fro);
   double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
   unsigned *flags = (unsigned *)(ws + L.flags);
   double *errp = (double *)(ws + L.errp), *part = (double *)(ws + L.part);
   double *par = (double *)(ws + L.par);
   int rc;
-  k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, icf, LT, qd, sq);
+  k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, icf, LT, qd, sq, fro);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
     if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
@@ -654,8 +661,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       return rc;
   }
   if (add_params) {
-    k_gmm_params<<<1, GMM_THREADS, 0, st>>>(d, K, N_total, alphas, icf, qd, sq, gamma, m, cst,
-                                           par);
+    k_gmm_params<<<1, 32, 0, st>>>(d, K, N_total, alphas, fro, sq, gamma, m, cst, par);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_params"))) return rc;
   }
   k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, L.S, N > 0 ? L.nerr : 0, icf, qd, LT, part, errp,
