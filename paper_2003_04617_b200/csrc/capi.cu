@@ -102,6 +102,13 @@ struct Pipeline {
     cudaGetDevice(&dev_prev);
     int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
     if (rc) return rc;
+    // keep freed stream-ordered allocations in the pool between calls (the
+    // default threshold 0 returns them to the driver at every sync)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     for (auto &s : st) {
       rc = cuda_status(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
       if (rc) return rc;
