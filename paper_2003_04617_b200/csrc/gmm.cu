@@ -38,6 +38,8 @@
 // differ from the sequential reference in rounding only (tests: 1e-10).
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rl {
@@ -45,28 +47,35 @@ namespace rl {
 constexpr int GMM_THREADS = 256;
 constexpr int GMM_WARPS = GMM_THREADS / 32;
 
-template <int DP>
+// Tile geometry.  DP = d padded to 32/64/128; TP = points per tile.  The
+// factor L_k^T lives in shared memory in 16-row blocks: block kb (rows
+// kb..kb+15) stores columns kb..DP-1 with row length RL = DP - kb + 4 (the
+// upper triangle incl. the diagonal qd; a > b entries inside a block are
+// stored zeros).  Row strides that are 4 (mod 16) doubles make every DMMA
+// fragment load conflict-free.
+template <int DP, int TP>
 struct GmmCfg {
-  static constexpr int TP = DP == 128 ? 64 : (DP == 64 ? 128 : 256);  // points per tile
-  static constexpr int PPL = TP / 32;                                  // points per lane
-  static constexpr int GW = DP / 16;            // columns per group (16 groups, 2 per warp)
-  static constexpr int XS = TP + 2;             // padded row stride of the [DP][TP] tiles
-  static constexpr int MT = DP / 16;            // M micro-tile edge (16 x 16 thread grid)
+  static constexpr int NT = DP / 8;            // n-tiles (8 columns) of Z
+  static constexpr int NP = NT / 2;            // column-tile pairs {j, NT-1-j}
+  static constexpr int WPP = GMM_WARPS / NP;   // warps per pair
+  static constexpr int MT = TP / 16;           // m-tiles (16 points)
+  static constexpr int MTW = MT / WPP;         // m-tiles per warp
+  static constexpr int XS = DP + 4;            // x tile row stride  [TP][XS]
+  static constexpr int GS = TP + 4;            // qxc.g tile stride  [DP][GS]
+  static_assert(MT % WPP == 0, "tile shape");
 };
 
-__host__ __device__ constexpr int lt_size(int DP) {
-  int s = 0;
-  for (int a = 0; a < DP; a++) s += DP - (a & ~7);
-  return s;
+__host__ __device__ constexpr int ltb_off(int DP, int kb) {
+  // sum over 16-row blocks before kb of 16 * (DP - kb' + 4)
+  return 16 * ((kb / 16) * (DP + 4) - 8 * (kb / 16) * (kb / 16 - 1));
 }
-__host__ __device__ constexpr int lt_rowoff(int DP, int a) {
-  // sum_{a' < a} (DP - (a' & ~7))
-  int q = a >> 3, r = a & 7;
-  return 8 * (q * DP - 4 * q * (q - 1)) + r * (DP - 8 * q);
+__host__ __device__ constexpr int ltb_size(int DP) { return ltb_off(DP, DP); }
+__host__ __device__ constexpr int ltb_idx(int DP, int a, int b) {
+  return ltb_off(DP, a & ~15) + (a & 15) * (DP - (a & ~15) + 4) + (b - (a & ~15));
 }
 
 // ---------------------------------------------------------------------------
-// prep: qd, sq (the top @routine) and packed L^T per component
+// prep: qd, sq (the top @routine), L^T in the block layout, Frobenius share
 // ---------------------------------------------------------------------------
 template <int DP>
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const double *__restrict__ icf,
@@ -77,13 +86,15 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const do
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
   const double *ic = icf + (long long)k * P;
-  constexpr int LTS = lt_size(DP);
+  constexpr int LTS = ltb_size(DP);
   double *lt = LT + (long long)k * LTS;
   for (int e = threadIdx.x; e < LTS; e += GMM_THREADS) {
-    // invert the packed index e -> (a, b)
-    int a = 0;
-    while (a + 1 < DP && lt_rowoff(DP, a + 1) <= e) a++;
-    const int b = (a & ~7) + (e - lt_rowoff(DP, a));
+    // invert e -> (a, b): block, row in block, column
+    int q = 0;
+    while (q + 1 < DP / 16 && ltb_off(DP, 16 * (q + 1)) <= e) q++;
+    const int kb = 16 * q, rl = DP - kb + 4;
+    const int r = e - ltb_off(DP, kb);
+    const int a = kb + r / rl, b = kb + r % rl;
     double v = 0.0;
     if (a < d && b < d) {
       if (b == a) {
@@ -96,12 +107,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const do
     }
     lt[e] = v;
   }
-  if (threadIdx.x < 32) {
+  if (threadIdx.x == 0) {
     double s = 0.0;
-    if (threadIdx.x == 0) {
-      for (int j = 0; j < d; j++) s = s + ic[j];         // sq[k] += icf[k, j] (in order)
-      sq[k] = s;
-    }
+    for (int j = 0; j < d; j++) s = s + ic[j];           // sq[k] += icf[k, j] (in order)
+    sq[k] = s;
   }
   // qd and this component's share of the prior's Frobenius sum:
   // fro += abs2(qd![k, j]) (j <= d) or abs2(icf[k, j]) (j > d)
@@ -125,150 +134,171 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const do
 }
 
 // ---------------------------------------------------------------------------
-// shared tile loaders and the Z = Xc L^T tile product
+// async copies, the FP64 tensor-core MMA and the Z = Xc L^T tile product
 // ---------------------------------------------------------------------------
-template <int DP>
-__device__ __forceinline__ void load_xct(double *__restrict__ xct, const double *__restrict__ x,
-                                         const double *__restrict__ mu, int d, long long p0,
-                                         long long N) {
-  using C = GmmCfg<DP>;
-  // x rows are d doubles; walk the tile's TP*d doubles linearly (coalesced)
-  const long long rows = N - p0 < C::TP ? N - p0 : C::TP;
-  const int tot = C::TP * DP;
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// D (16x8) += A (16x16, row) * B (16x8, col) in FP64 on the tensor cores.
+// Fragments (lane = t0 + 4 t1):  a[v0 + 2 v1] = A[t1 + 8 v0][t0 + 4 v1],
+// b[v] = B[t0 + 4 v][t1],  c[v0 + 2 v1] = C[t1 + 8 v1][2 t0 + v0].
+__device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// issue the async copy of tile [p0, p0 + TP) of x into xs ([TP][XS]; rows
+// past N are zero-filled, padding columns d..DP-1 are never written)
+template <int DP, int TP>
+__device__ __forceinline__ void load_x_async(double *__restrict__ xs, const double *__restrict__ x,
+                                             int d, long long p0, long long N) {
+  using C = GmmCfg<DP, TP>;
+  const int tot = TP * d;
   for (int e = threadIdx.x; e < tot; e += GMM_THREADS) {
-    const int p = e / DP, a = e - p * DP;
-    double v = 0.0;
-    if (p < rows && a < d) v = x[(p0 + p) * d + a] - mu[a];  // xc[j] += x[i, j] - means[k, j]
-    xct[a * C::XS + p] = v;
+    const int p = e / d, a = e - p * d;
+    const bool in = p0 + p < N;
+    cp_async8(xs + p * C::XS + a, x + (in ? (p0 + p) * d + a : 0), in ? 8 : 0);
   }
 }
 
-// acc[p][h][c]: lane's PPL points x (group h of the warp: 0 -> group w,
-// 1 -> group 15-w) x GW columns
-template <int DP>
-__device__ __forceinline__ void tile_z(const double *__restrict__ lt, const double *__restrict__ xct,
-                                       double (&acc)[GmmCfg<DP>::PPL][2][GmmCfg<DP>::GW]) {
-  using C = GmmCfg<DP>;
+// Z tile: acc[m][h] (m-tile m of this warp, column tile h: 0 -> j1, 1 -> j2)
+// = sum_a Xc[p][a] L^T[a][b] over the upper triangle (k-steps ks <= j/2).
+// xc = x - mu is formed while loading the A fragments (xc[j] += x[i,j] - means[k,j]).
+template <int DP, int TP>
+__device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const double *__restrict__ xs,
+                                          const double *__restrict__ mu,
+                                          double (&acc)[GmmCfg<DP, TP>::MTW][2][4]) {
+  using C = GmmCfg<DP, TP>;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c1 = w * C::GW, c2 = (15 - w) * C::GW;
+  const int t0 = lane & 3, t1 = lane >> 2;
+  const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
+  const int j1 = pi, j2 = C::NT - 1 - pi;
 #pragma unroll
-  for (int p = 0; p < C::PPL; p++)
+  for (int m = 0; m < C::MTW; m++)
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int c = 0; c < C::GW; c++) acc[p][h][c] = 0.0;
-  const double *xrow = xct + lane * C::PPL;
-  const int amax1 = c1 + C::GW, amax2 = c2 + C::GW;
-#pragma unroll 2
-  for (int a = 0; a < amax1; a++) {
-    double xv[C::PPL], l1[C::GW], l2[C::GW];
+      for (int v = 0; v < 4; v++) acc[m][h][v] = 0.0;
+  const int ks_end = j2 / 2, ks1 = j1 / 2;
+#pragma unroll 1
+  for (int ks = 0; ks <= ks_end; ks++) {
+    const int kb = 16 * ks, rl = DP - kb + 4;
+    const double *ltb = lt + ltb_off(DP, kb) - kb;       // row a: ltb + (a - kb) * rl + b
+    double b1[4], b2[4];
 #pragma unroll
-    for (int p = 0; p < C::PPL; p += 2) {
-      const double2 t = *reinterpret_cast<const double2 *>(xrow + a * C::XS + p);
-      xv[p] = t.x;
-      xv[p + 1] = t.y;
+    for (int v = 0; v < 4; v++) {
+      const double *row = ltb + (t0 + 4 * v) * rl;
+      b2[v] = row[8 * j2 + t1];
+      b1[v] = ks <= ks1 ? row[8 * j1 + t1] : 0.0;
     }
-    const double *lr = lt + lt_rowoff(DP, a) - (a & ~7);
+    double muv[4];
 #pragma unroll
-    for (int c = 0; c < C::GW; c += 2) {
-      const double2 u = *reinterpret_cast<const double2 *>(lr + c1 + c);
-      const double2 v = *reinterpret_cast<const double2 *>(lr + c2 + c);
-      l1[c] = u.x;
-      l1[c + 1] = u.y;
-      l2[c] = v.x;
-      l2[c + 1] = v.y;
+    for (int v1 = 0; v1 < 4; v1++) muv[v1] = mu[kb + t0 + 4 * v1];
+#pragma unroll
+    for (int m = 0; m < C::MTW; m++) {
+      const int pb = 16 * (mw + m);
+      double af[8];
+#pragma unroll
+      for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+        for (int v0 = 0; v0 < 2; v0++)
+          af[v0 + 2 * v1] = xs[(pb + t1 + 8 * v0) * C::XS + kb + t0 + 4 * v1] - muv[v1];
+      dmma16816(acc[m][1], af, b2);
+      if (ks <= ks1) dmma16816(acc[m][0], af, b1);
     }
-#pragma unroll
-    for (int p = 0; p < C::PPL; p++)
-#pragma unroll
-      for (int c = 0; c < C::GW; c++) {
-        acc[p][0][c] = fma(xv[p], l1[c], acc[p][0][c]);
-        acc[p][1][c] = fma(xv[p], l2[c], acc[p][1][c]);
-      }
-  }
-#pragma unroll 2
-  for (int a = amax1; a < amax2; a++) {
-    double xv[C::PPL], l2[C::GW];
-#pragma unroll
-    for (int p = 0; p < C::PPL; p += 2) {
-      const double2 t = *reinterpret_cast<const double2 *>(xrow + a * C::XS + p);
-      xv[p] = t.x;
-      xv[p + 1] = t.y;
-    }
-    const double *lr = lt + lt_rowoff(DP, a) - (a & ~7);
-#pragma unroll
-    for (int c = 0; c < C::GW; c += 2) {
-      const double2 v = *reinterpret_cast<const double2 *>(lr + c2 + c);
-      l2[c] = v.x;
-      l2[c + 1] = v.y;
-    }
-#pragma unroll
-    for (int p = 0; p < C::PPL; p++)
-#pragma unroll
-      for (int c = 0; c < C::GW; c++) acc[p][1][c] = fma(xv[p], l2[c], acc[p][1][c]);
   }
 }
 
 template <int DP>
-__device__ __forceinline__ void copy_lt(double *__restrict__ lt_s, const double *__restrict__ lt_g) {
-  constexpr int n2 = lt_size(DP) / 2;
-  const double2 *src = reinterpret_cast<const double2 *>(lt_g);
-  double2 *dst = reinterpret_cast<double2 *>(lt_s);
-  for (int e = threadIdx.x; e < n2; e += GMM_THREADS) dst[e] = src[e];
+__device__ __forceinline__ void copy_lt_async(double *__restrict__ lt_s, const double *__restrict__ lt_g) {
+  constexpr int n2 = ltb_size(DP) / 2;
+  for (int e = threadIdx.x; e < n2; e += GMM_THREADS) cp_async16(lt_s + 2 * e, lt_g + 2 * e);
 }
 
 // ---------------------------------------------------------------------------
 // forward: mt[k][i] = alphas[k] + sq[k] - |L_k (x_i - mu_k)|^2 / 2
 // ---------------------------------------------------------------------------
-template <int DP>
+template <int DP, int TP>
 __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_fwd(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
     double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA) {
-  using C = GmmCfg<DP>;
+  using C = GmmCfg<DP, TP>;
   extern __shared__ __align__(16) double smem[];
   double *lt_s = smem;
-  double *xct = lt_s + lt_size(DP);
-  double *sqp = xct + DP * C::XS;  // [GMM_WARPS][TP]
+  double *xs0 = lt_s + ltb_size(DP);
+  double *xs1 = xs0 + TP * C::XS;
+  double *mu = xs1 + TP * C::XS;                 // [DP], zero padded
+  double *sqp = mu + DP;                         // [NP][TP]
   const int k = blockIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  copy_lt<DP>(lt_s, LT + (long long)k * lt_size(DP));
-  const double *mu = means + (long long)k * d;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int t0 = lane & 3, t1 = lane >> 2;
+  const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
+  copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
+  for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;  // padding stays zero
+  for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
-  const long long ntiles = (N + C::TP - 1) / C::TP;
-  for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y) {
-    const long long p0 = tile * C::TP;
+  const long long ntiles = (N + TP - 1) / TP;
+  __syncthreads();
+  long long tile = blockIdx.y;
+  if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+  cp_commit();
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.y) {
+    const long long nxt = tile + gridDim.y;
+    if (nxt < ntiles) load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_xct<DP>(xct, x, mu, d, p0, N);
+    const double *xs = buf ? xs1 : xs0;
+    double acc[C::MTW][2][4];
+    tile_z_tc<DP, TP>(lt_s, xs, mu, acc);
+    // sqn partial over this warp's 16 columns, per point (sqn += abs2(qxc[j]))
+#pragma unroll
+    for (int m = 0; m < C::MTW; m++)
+#pragma unroll
+      for (int v1 = 0; v1 < 2; v1++) {
+        double s = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++) s = fma(acc[m][h][v0 + 2 * v1], acc[m][h][v0 + 2 * v1], s);
+        s += __shfl_xor_sync(FULL_MASK, s, 1);
+        s += __shfl_xor_sync(FULL_MASK, s, 2);
+        if (t0 == 0) sqp[pi * TP + 16 * (mw + m) + t1 + 8 * v1] = s;
+      }
     __syncthreads();
-    double acc[C::PPL][2][C::GW];
-    tile_z<DP>(lt_s, xct, acc);
-    // sqn partial of this warp's columns, per point (sqn += abs2(qxc[j]))
-#pragma unroll
-    for (int p = 0; p < C::PPL; p++) {
-      double s = 0.0;
-#pragma unroll
-      for (int h = 0; h < 2; h++)
-#pragma unroll
-        for (int c = 0; c < C::GW; c++) s = fma(acc[p][h][c], acc[p][h][c], s);
-      sqp[w * C::TP + lane * C::PPL + p] = s;
-    }
-    __syncthreads();
-    for (int p = threadIdx.x; p < C::TP; p += GMM_THREADS) {
-      const long long i = p0 + p;
+    for (int p = tid; p < TP; p += GMM_THREADS) {
+      const long long i = tile * TP + p;
       if (i >= N) continue;
       double sqn = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < GMM_WARPS; ww++) sqn = sqn + sqp[ww * C::TP + p];
+      for (int q = 0; q < C::NP; q++) sqn = sqn + sqp[q * TP + p];
       // the inner routine's uncompute: sqn -= abs2(qxc[j]) in reverse, then
       // the release check sqn -> 0.0 (interpreter.py:738-745)
       double res = sqn;
 #pragma unroll
-      for (int ww = GMM_WARPS - 1; ww >= 0; ww--) res = res - sqp[ww * C::TP + p];
+      for (int q = C::NP - 1; q >= 0; q--) res = res - sqp[q * TP + p];
       if (chk && fabs(res) > tol) atomicOr(&flagsA[i], 1u);
       mtT[(long long)k * N + i] = base_mt - sqn * 0.5;    // mt -= sqn * 0.5
     }
+    buf ^= 1;
   }
+  cp_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -343,116 +373,169 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
 }
 
 // ---------------------------------------------------------------------------
-// reverse: recompute Z, qxc.g = (-dmt/2)(2 Z); accumulate M = G^T Xc and
-// sum_i G_i over the block's points (registers), then write the partial.
+// reverse: recompute Z (no tape), qxc.g = (-dmt/2)(2 Z); accumulate the
+// factor adjoint M = sum_i qxc.g_i xc_i^T (lower triangle, 16x8 DMMA tiles
+// held in registers across all of the block's points) and sum_i qxc.g_i.
 // ---------------------------------------------------------------------------
 template <int DP>
+struct MTiles {  // lower-triangle 16x8 tiles (i, j), j <= 2i + 1, dealt to the warps
+  static constexpr int NI = DP / 16;
+  static constexpr int COUNT = NI * (NI + 1);            // sum_i (2 i + 2)
+  static constexpr int PER = (COUNT + GMM_WARPS - 1) / GMM_WARPS;
+};
+
+template <int DP>
+__device__ __forceinline__ void mtile_ij(int t, int &i, int &j) {
+  // t-th tile in row-major order over i, j <= 2i + 1
+  i = 0;
+  while (t >= 2 * i + 2) {
+    t -= 2 * i + 2;
+    i++;
+  }
+  j = t;
+}
+
+template <int DP, int TP>
 __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ x,
     const double *__restrict__ LT, const double *__restrict__ gmtT,
     double *__restrict__ part /* [K][S][DP*DP + DP + 1] */) {
-  using C = GmmCfg<DP>;
+  using C = GmmCfg<DP, TP>;
+  using MTL = MTiles<DP>;
   extern __shared__ __align__(16) double smem[];
   double *lt_s = smem;
-  double *xct = lt_s + lt_size(DP);
-  double *gt = xct + DP * C::XS;       // [DP][XS]: qxc.g transposed
-  double *cg = gt + DP * C::XS;        // [TP]: sqn.g per point
-  double *red = cg + C::TP;            // [GMM_WARPS]
+  double *xs0 = lt_s + ltb_size(DP);
+  double *xs1 = xs0 + TP * C::XS;
+  double *gt = xs1 + TP * C::XS;        // [DP][GS]: qxc.g transposed
+  double *mu = gt + DP * C::GS;         // [DP]
+  double *cg = mu + DP;                 // [TP]: sqn.g per point
+  double *red = cg + TP;                // [GMM_WARPS]
   const int k = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  copy_lt<DP>(lt_s, LT + (long long)k * lt_size(DP));
-  const double *mu = means + (long long)k * d;
+  const int t0 = lane & 3, t1 = lane >> 2;
+  const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
+  const int j1 = pi, j2 = C::NT - 1 - pi;
+  copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
+  for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;
+  for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const double *gm = gmtT + (long long)k * N;
-  // M tile of this thread: rows b = bi + 16 r, cols a = ai + 16 c (interleaved
-  // so that the smem reads of a warp spread over the banks)
-  const int bi = tid >> 4, ai = tid & 15;
-  double M[C::MT][C::MT];
+  // this warp's factor-adjoint tiles
+  int ti[MTL::PER], tj[MTL::PER];
+  double M[MTL::PER][4];
 #pragma unroll
-  for (int r = 0; r < C::MT; r++)
+  for (int q = 0; q < MTL::PER; q++) {
+    const int t = w * MTL::PER + q;
+    if (t < MTL::COUNT) {
+      mtile_ij<DP>(t, ti[q], tj[q]);
+    } else {
+      ti[q] = -1;
+      tj[q] = 0;
+    }
 #pragma unroll
-    for (int c = 0; c < C::MT; c++) M[r][c] = 0.0;
-  double gs[2][C::GW];
-#pragma unroll
-  for (int h = 0; h < 2; h++)
-#pragma unroll
-    for (int c = 0; c < C::GW; c++) gs[h][c] = 0.0;
+    for (int v = 0; v < 4; v++) M[q][v] = 0.0;
+  }
+  double gs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};            // column sums (h, v0)
   double sgm = 0.0;
-  const int c1 = w * C::GW, c2 = (15 - w) * C::GW;
-  const long long ntiles = (N + C::TP - 1) / C::TP;
-  for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y) {
-    const long long p0 = tile * C::TP;
-    __syncthreads();
-    load_xct<DP>(xct, x, mu, d, p0, N);
-    for (int p = tid; p < C::TP; p += GMM_THREADS) {
+  const long long ntiles = (N + TP - 1) / TP;
+  __syncthreads();
+  long long tile = blockIdx.y;
+  if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+  cp_commit();
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.y) {
+    const long long p0 = tile * TP;
+    const long long nxt = tile + gridDim.y;
+    if (nxt < ntiles) load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+    cp_commit();
+    for (int p = tid; p < TP; p += GMM_THREADS) {
       const long long i = p0 + p;
       const double g = i < N ? gm[i] : 0.0;
       sgm += g;                                           // alphas.g, sq.g += mt.g
       cg[p] = 0.0 + (-1.0 * g) * 0.5;                     // mt += sqn*0.5: sqn.g += -mt.g/2
     }
+    cp_wait<1>();
     __syncthreads();
-    double acc[C::PPL][2][C::GW];
-    tile_z<DP>(lt_s, xct, acc);                           // recompute qxc
+    const double *xs = buf ? xs1 : xs0;
+    double acc[C::MTW][2][4];
+    tile_z_tc<DP, TP>(lt_s, xs, mu, acc);                 // recompute qxc
     // qxc.g[j] = sqn.g * (2 qxc[j]) -> smem (transposed) and column sums
 #pragma unroll
-    for (int p = 0; p < C::PPL; p++) {
-      const int pp = lane * C::PPL + p;
-      const double c = cg[pp];
+    for (int m = 0; m < C::MTW; m++)
 #pragma unroll
-      for (int h = 0; h < 2; h++)
+      for (int v1 = 0; v1 < 2; v1++) {
+        const int pp = 16 * (mw + m) + t1 + 8 * v1;
+        const double c = cg[pp];
 #pragma unroll
-        for (int cc = 0; cc < C::GW; cc++) {
-          const double g = c * (2.0 * acc[p][h][cc]);
-          gs[h][cc] += g;
-          gt[((h ? c2 : c1) + cc) * C::XS + pp] = g;
-        }
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++) {
+            const double g = c * (2.0 * acc[m][h][v0 + 2 * v1]);
+            gs[h][v0] += g;
+            gt[(8 * (h ? j2 : j1) + 2 * t0 + v0) * C::GS + pp] = g;
+          }
+      }
+    __syncthreads();
+    // M[b][a] += sum_p G[p][b] Xc[p][a]: A = G^T (b x p), B = Xc (p x a)
+#pragma unroll
+    for (int ks = 0; ks < TP / 16; ks++) {
+      const int pb = 16 * ks;
+#pragma unroll
+      for (int q = 0; q < MTL::PER; q++) {
+        if (ti[q] < 0) continue;
+        const int rb = 16 * ti[q], cb = 8 * tj[q];
+        double af[8], bf[4];
+#pragma unroll
+        for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++)
+            af[v0 + 2 * v1] = gt[(rb + t1 + 8 * v0) * C::GS + pb + t0 + 4 * v1];
+        const double mua = mu[cb + t1];
+#pragma unroll
+        for (int v = 0; v < 4; v++) bf[v] = xs[(pb + t0 + 4 * v) * C::XS + cb + t1] - mua;
+        dmma16816(M[q], af, bf);
+      }
     }
     __syncthreads();
-    // M[b][a] += sum_p G[p][b] Xc[p][a]   (factor adjoint, lower triangle used)
-#pragma unroll 1
-    for (int p = 0; p < C::TP; p += 2) {
-      double gv[C::MT][2], xv[C::MT][2];
-#pragma unroll
-      for (int r = 0; r < C::MT; r++) {
-        const double2 t = *reinterpret_cast<const double2 *>(gt + (bi + 16 * r) * C::XS + p);
-        gv[r][0] = t.x;
-        gv[r][1] = t.y;
-        const double2 u = *reinterpret_cast<const double2 *>(xct + (ai + 16 * r) * C::XS + p);
-        xv[r][0] = u.x;
-        xv[r][1] = u.y;
-      }
-#pragma unroll
-      for (int r = 0; r < C::MT; r++)
-#pragma unroll
-        for (int c = 0; c < C::MT; c++) {
-          M[r][c] = fma(gv[r][0], xv[c][0], M[r][c]);
-          M[r][c] = fma(gv[r][1], xv[c][1], M[r][c]);
-        }
-    }
+    buf ^= 1;
   }
-  // write this block's partial
+  cp_wait<0>();
+  // write this block's partial: M tiles, column sums, sum of mt.g
   const int S = gridDim.y;
   const long long PW = (long long)DP * DP + DP + 1;
   double *out = part + ((long long)k * S + blockIdx.y) * PW;
 #pragma unroll
-  for (int r = 0; r < C::MT; r++)
+  for (int q = 0; q < MTL::PER; q++) {
+    if (ti[q] < 0) continue;
+    const int rb = 16 * ti[q], cb = 8 * tj[q];
 #pragma unroll
-    for (int c = 0; c < C::MT; c++) out[(bi + 16 * r) * DP + (ai + 16 * c)] = M[r][c];
-  // column sums: reduce gs over the warp's lanes (all lanes share the columns)
+    for (int v1 = 0; v1 < 2; v1++)
+#pragma unroll
+      for (int v0 = 0; v0 < 2; v0++)
+        out[(long long)(rb + t1 + 8 * v1) * DP + cb + 2 * t0 + v0] = M[q][v0 + 2 * v1];
+  }
+  // column sums: reduce over the lanes holding the same columns (t1) and over
+  // the warps sharing the column pair
+  __syncthreads();
+  double *colsum = gt;                                    // reuse: [WPP][DP]
 #pragma unroll
   for (int h = 0; h < 2; h++)
 #pragma unroll
-    for (int cc = 0; cc < C::GW; cc++) {
-      double v = gs[h][cc];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL_MASK, v, o);
-      if (lane == 0) out[(long long)DP * DP + (h ? c2 : c1) + cc] = v;
+    for (int v0 = 0; v0 < 2; v0++) {
+      double v = gs[h][v0];
+      v += __shfl_xor_sync(FULL_MASK, v, 4);
+      v += __shfl_xor_sync(FULL_MASK, v, 8);
+      v += __shfl_xor_sync(FULL_MASK, v, 16);
+      if (t1 == 0) colsum[(w % C::WPP) * DP + 8 * (h ? j2 : j1) + 2 * t0 + v0] = v;
     }
-  // sum of mt.g over the block's points
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sgm += __shfl_down_sync(FULL_MASK, sgm, o);
-  __syncthreads();
   if (lane == 0) red[w] = sgm;
   __syncthreads();
+  for (int b = tid; b < DP; b += GMM_THREADS) {
+    double v = 0.0;
+    for (int q = 0; q < C::WPP; q++) v += colsum[q * DP + b];
+    out[(long long)DP * DP + b] = v;
+  }
   if (tid == 0) {
     double s = 0.0;
     for (int ww = 0; ww < GMM_WARPS; ww++) s += red[ww];
@@ -530,11 +613,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     g_alpha[k] = ga_k;
   }
   // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a)
-  const double *lt = LT + (long long)k * lt_size(DP);
+  const double *lt = LT + (long long)k * ltb_size(DP);
   for (int a = threadIdx.x; a < d; a += GMM_THREADS) {
-    const double *lr = lt + lt_rowoff(DP, a) - (a & ~7);
     double s = 0.0;
-    for (int b = a; b < d; b++) s = fma(gsum[b], lr[b], s);
+    for (int b = a; b < d; b++) s = fma(gsum[b], lt[ltb_idx(DP, a, b)], s);
     g_means[(long long)k * d + a] = -s;
   }
   // icf.g: diag = sq.g + qd.g exp(icf); offdiag = M[b][a] (+ prior)
@@ -576,10 +658,43 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
 // host side
 // ---------------------------------------------------------------------------
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
+// points per tile: forward / reverse (the reverse also stages qxc.g)
+static int tpf_of(int) { return 64; }
+static int tpr_of(int DP) { return DP == 32 ? 64 : 32; }
+
+template <int DP, int TP>
+static constexpr size_t smem_fwd() {
+  using C = GmmCfg<DP, TP>;
+  return ((size_t)ltb_size(DP) + 2 * (size_t)TP * C::XS + DP + (size_t)C::NP * TP) * 8;
+}
+template <int DP, int TP>
+static constexpr size_t smem_rev() {
+  using C = GmmCfg<DP, TP>;
+  return ((size_t)ltb_size(DP) + 2 * (size_t)TP * C::XS + (size_t)DP * C::GS + DP + TP +
+          GMM_WARPS) * 8;
+}
+
+// split of the points into S chunks per component so that K*S CTAs fill
+// whole waves of `slots` concurrent CTAs (tail-wave efficiency), S <= tiles
+static int choose_split(int K, long long ntiles, int slots, int smax) {
+  int best = 1;
+  double best_eff = -1.0;
+  for (int S = 1; S <= smax && S <= ntiles; S++) {
+    const long long items = (long long)K * S;
+    const long long waves = (items + slots - 1) / slots;
+    const double eff = (double)items / (double)(waves * slots);
+    // prefer fuller waves; among near-equal, fewer partials
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = S;
+    }
+  }
+  return best;
+}
 
 struct GmmLayout {
   size_t lt, qd, sq, fro, mt, gmt, flags, errp, part, par, total;
-  int S, nerr;
+  int Sf, Sr, nerr;
 };
 
 static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
@@ -587,12 +702,14 @@ static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 static GmmLayout gmm_layout(int d, int K, long long N) {
   GmmLayout L{};
   const int DP = dp_of(d);
-  const int TP = DP == 128 ? 64 : (DP == 64 ? 128 : 256);
-  const long long ntiles = (N + TP - 1) / TP;
-  int S = (int)((2 * 148 + K - 1) / K);
-  if (S < 1) S = 1;
-  if (S > ntiles) S = (int)(ntiles > 0 ? ntiles : 1);
-  L.S = S;
+  const long long ntf = (N + tpf_of(DP) - 1) / tpf_of(DP);
+  const long long ntr = (N + tpr_of(DP) - 1) / tpr_of(DP);
+  const int slots = 148 * (DP == 128 ? 1 : 2);
+  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, slots, 64);
+  // each reverse CTA writes a (DP^2 + DP + 1)-double partial: cap them at 256 MB
+  const long long pw = (long long)DP * DP + DP + 1;
+  int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
+  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, slots, smax);
   L.nerr = (int)((N + GMM_THREADS - 1) / GMM_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -600,7 +717,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
     off += al(bytes);
     return o;
   };
-  L.lt = take((size_t)K * lt_size(DP) * 8);
+  L.lt = take((size_t)K * ltb_size(DP) * 8);
   L.qd = take((size_t)K * d * 8);
   L.sq = take((size_t)K * 8);
   L.fro = take((size_t)K * 8);
@@ -608,7 +725,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.gmt = take((size_t)K * N * 8);
   L.flags = take((size_t)N * 4);
   L.errp = take((size_t)(L.nerr > 0 ? L.nerr : 1) * 8);
-  L.part = take((size_t)K * S * ((size_t)DP * DP + DP + 1) * 8);
+  L.part = take((size_t)K * L.Sr * (size_t)pw * 8);
   L.par = take((size_t)(K + 1) * 8);
   L.total = off;
   return L;
@@ -624,7 +741,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    const double *means, const double *icf, const double *x, double gamma, int m,
                    double cst, double tol, int chk, int add_params, double *out, uint8_t *fail,
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st) {
-  using C = GmmCfg<DP>;
+  constexpr int TPF = 64, TPR = DP == 32 ? 64 : 32;
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
   double *fro = (double *)(ws + L.fro);
   double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
@@ -634,37 +751,36 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   int rc;
   k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, icf, LT, qd, sq, fro);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
-  if (N > 0) {
-    if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
-      return rc;
-    const size_t smem_f = ((size_t)lt_size(DP) + (size_t)DP * C::XS + GMM_WARPS * C::TP) * 8;
-    const size_t smem_r = ((size_t)lt_size(DP) + 2 * (size_t)DP * C::XS + C::TP + GMM_WARPS) * 8;
-    if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_fwd<DP>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem_f), "smem attr fwd")) ||
-        (rc = cuda_status(cudaFuncSetAttribute(k_gmm_rev<DP>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem_r), "smem attr rev")))
-      return rc;
-    dim3 grid(K, L.S);
-    k_gmm_fwd<DP><<<grid, GMM_THREADS, smem_f, st>>>(d, K, N, alphas, means, x, LT, sq, tol, chk, mt,
-                                                    flags);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_fwd"))) return rc;
-    k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
-                                              counters);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
-    k_gmm_rev<DP><<<grid, GMM_THREADS, smem_r, st>>>(d, K, N, means, x, LT, gmt, part);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_rev"))) return rc;
-  } else {
-    if ((rc = cuda_status(cudaMemsetAsync(part, 0, (size_t)K * L.S * ((size_t)DP * DP + DP + 1) * 8,
-                                          st), "memset part")))
-      return rc;
-  }
   if (add_params) {
     k_gmm_params<<<1, 32, 0, st>>>(d, K, N_total, alphas, fro, sq, gamma, m, cst, par);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_params"))) return rc;
   }
-  k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, L.S, N > 0 ? L.nerr : 0, icf, qd, LT, part, errp,
+  if (N > 0) {
+    if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
+      return rc;
+    constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
+    static_assert(sf <= 227 * 1024 && sr <= 227 * 1024, "shared memory budget");
+    if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_fwd<DP, TPF>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sf), "smem attr fwd")) ||
+        (rc = cuda_status(cudaFuncSetAttribute(k_gmm_rev<DP, TPR>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sr), "smem attr rev")))
+      return rc;
+    k_gmm_fwd<DP, TPF><<<dim3(K, L.Sf), GMM_THREADS, sf, st>>>(d, K, N, alphas, means, x, LT, sq,
+                                                               tol, chk, mt, flags);
+    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_fwd"))) return rc;
+    k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
+                                              counters);
+    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
+    k_gmm_rev<DP, TPR><<<dim3(K, L.Sr), GMM_THREADS, sr, st>>>(d, K, N, means, x, LT, gmt, part);
+    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_rev"))) return rc;
+  } else {
+    if ((rc = cuda_status(cudaMemsetAsync(part, 0, (size_t)K * L.Sr * ((size_t)DP * DP + DP + 1) * 8,
+                                          st), "memset part")))
+      return rc;
+  }
+  k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, LT, part, errp,
                                              par, gamma, m, add_params, out);
   return cuda_status(cudaGetLastError(), "k_gmm_final");
 }
