@@ -177,10 +177,10 @@ __device__ __forceinline__ void load_x_async(double *__restrict__ xs, const doub
 
 // Z tile: acc[m][h] (m-tile m of this warp, column tile h: 0 -> j1, 1 -> j2)
 // = sum_a Xc[p][a] L^T[a][b] over the upper triangle (k-steps ks <= j/2).
-// xc = x - mu is formed while loading the A fragments (xc[j] += x[i,j] - means[k,j]).
+// xs already holds xc = x - mu (see center_tile).  All fragments of a
+// k-step are loaded before its MMAs so the loads overlap.
 template <int DP, int TP>
 __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const double *__restrict__ xs,
-                                          const double *__restrict__ mu,
                                           double (&acc)[GmmCfg<DP, TP>::MTW][2][4]) {
   using C = GmmCfg<DP, TP>;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -194,32 +194,43 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
 #pragma unroll
       for (int v = 0; v < 4; v++) acc[m][h][v] = 0.0;
   const int ks_end = j2 / 2, ks1 = j1 / 2;
+  const double *xl = xs + (16 * mw + t1) * C::XS + t0;
 #pragma unroll 1
   for (int ks = 0; ks <= ks_end; ks++) {
     const int kb = 16 * ks, rl = DP - kb + 4;
-    const double *ltb = lt + ltb_off(DP, kb) - kb;       // row a: ltb + (a - kb) * rl + b
+    const double *ltb = lt + ltb_off(DP, kb) - kb + t0 * rl + t1;  // + 4v*rl + 8j
     double b1[4], b2[4];
+    double af[C::MTW][8];
 #pragma unroll
     for (int v = 0; v < 4; v++) {
-      const double *row = ltb + (t0 + 4 * v) * rl;
-      b2[v] = row[8 * j2 + t1];
-      b1[v] = ks <= ks1 ? row[8 * j1 + t1] : 0.0;
+      b2[v] = ltb[4 * v * rl + 8 * j2];
+      b1[v] = ltb[4 * v * rl + 8 * j1];
     }
-    double muv[4];
 #pragma unroll
-    for (int v1 = 0; v1 < 4; v1++) muv[v1] = mu[kb + t0 + 4 * v1];
-#pragma unroll
-    for (int m = 0; m < C::MTW; m++) {
-      const int pb = 16 * (mw + m);
-      double af[8];
+    for (int m = 0; m < C::MTW; m++)
 #pragma unroll
       for (int v1 = 0; v1 < 4; v1++)
 #pragma unroll
         for (int v0 = 0; v0 < 2; v0++)
-          af[v0 + 2 * v1] = xs[(pb + t1 + 8 * v0) * C::XS + kb + t0 + 4 * v1] - muv[v1];
-      dmma16816(acc[m][1], af, b2);
-      if (ks <= ks1) dmma16816(acc[m][0], af, b1);
+          af[m][v0 + 2 * v1] = xl[(16 * m + 8 * v0) * C::XS + kb + 4 * v1];
+#pragma unroll
+    for (int m = 0; m < C::MTW; m++) dmma16816(acc[m][1], af[m], b2);
+    if (ks <= ks1) {
+#pragma unroll
+      for (int m = 0; m < C::MTW; m++) dmma16816(acc[m][0], af[m], b1);
     }
+  }
+}
+
+// xc[j] += x[i, j] - means[k, j], formed once per tile in shared memory
+// (padding columns hold 0 - 0; rows past N are discarded downstream)
+template <int DP, int TP>
+__device__ __forceinline__ void center_tile(double *__restrict__ xs, const double *__restrict__ mu,
+                                            int d) {
+  using C = GmmCfg<DP, TP>;
+  for (int e = threadIdx.x; e < TP * d; e += GMM_THREADS) {
+    const int p = e / d, a = e - p * d;
+    xs[p * C::XS + a] = xs[p * C::XS + a] - mu[a];
   }
 }
 
@@ -264,9 +275,11 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_fwd(
     cp_commit();
     cp_wait<1>();
     __syncthreads();
-    const double *xs = buf ? xs1 : xs0;
+    double *xs = buf ? xs1 : xs0;
+    center_tile<DP, TP>(xs, mu, d);
+    __syncthreads();
     double acc[C::MTW][2][4];
-    tile_z_tc<DP, TP>(lt_s, xs, mu, acc);
+    tile_z_tc<DP, TP>(lt_s, xs, acc);
     // sqn partial over this warp's 16 columns, per point (sqn += abs2(qxc[j]))
 #pragma unroll
     for (int m = 0; m < C::MTW; m++)
@@ -455,9 +468,11 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
     }
     cp_wait<1>();
     __syncthreads();
-    const double *xs = buf ? xs1 : xs0;
+    double *xs = buf ? xs1 : xs0;
+    center_tile<DP, TP>(xs, mu, d);
+    __syncthreads();
     double acc[C::MTW][2][4];
-    tile_z_tc<DP, TP>(lt_s, xs, mu, acc);                 // recompute qxc
+    tile_z_tc<DP, TP>(lt_s, xs, acc);                     // recompute qxc
     // qxc.g[j] = sqn.g * (2 qxc[j]) -> smem (transposed) and column sums
 #pragma unroll
     for (int m = 0; m < C::MTW; m++)
@@ -479,19 +494,23 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
 #pragma unroll
     for (int ks = 0; ks < TP / 16; ks++) {
       const int pb = 16 * ks;
+      double af[8];
+      int cur_i = -1;
 #pragma unroll
       for (int q = 0; q < MTL::PER; q++) {
         if (ti[q] < 0) continue;
         const int rb = 16 * ti[q], cb = 8 * tj[q];
-        double af[8], bf[4];
+        if (ti[q] != cur_i) {                             // tiles of one row block share A
+          cur_i = ti[q];
 #pragma unroll
-        for (int v1 = 0; v1 < 4; v1++)
+          for (int v1 = 0; v1 < 4; v1++)
 #pragma unroll
-          for (int v0 = 0; v0 < 2; v0++)
-            af[v0 + 2 * v1] = gt[(rb + t1 + 8 * v0) * C::GS + pb + t0 + 4 * v1];
-        const double mua = mu[cb + t1];
+            for (int v0 = 0; v0 < 2; v0++)
+              af[v0 + 2 * v1] = gt[(rb + t1 + 8 * v0) * C::GS + pb + t0 + 4 * v1];
+        }
+        double bf[4];
 #pragma unroll
-        for (int v = 0; v < 4; v++) bf[v] = xs[(pb + t0 + 4 * v) * C::XS + cb + t1] - mua;
+        for (int v = 0; v < 4; v++) bf[v] = xs[(pb + t0 + 4 * v) * C::XS + cb + t1];
         dmma16816(M[q], af, bf);
       }
     }
