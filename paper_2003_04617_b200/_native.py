@@ -13,7 +13,8 @@ import threading
 from .errors import NativeLibraryError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "librevgpu.so")
+# REVGPU_LIB: build-variant override (kernel tuning experiments only)
+LIB_PATH = os.environ.get("REVGPU_LIB") or os.path.join(PKG_DIR, "librevgpu.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 RL_OK = 0

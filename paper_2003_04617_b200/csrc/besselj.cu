@@ -49,6 +49,12 @@ constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit f
 __constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
 __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 
+#ifndef BJ_SPEC
+#define BJ_SPEC 2          // speculative trips per warp vote (ILP of the exp chains)
+#endif
+#ifndef BJ_MINB
+#define BJ_MINB 3          // __launch_bounds__ min blocks per SM (register budget)
+#endif
 constexpr int BJ_BLOCK = 256;
 constexpr int BJ_M = 8;
 constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
@@ -215,6 +221,50 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   // chains overlap; a lane whose loop ended at k+1 keeps its trip-(k+1)
   // state and discards trip k+2.
   if (!CAREFUL && __all_sync(FULL_MASK, act || dead)) {
+#if BJ_SPEC == 4
+    while (k + 4 <= kend) {                              // k even: trips odd, even, odd, even
+      double s1 = s + h2;
+      s1 = s1 - c_logtab[k + 1];
+      s1 = s1 - c_logtab[k + 1 + nu];
+      double s2 = s1 + h2;
+      s2 = s2 - c_logtab[k + 2];
+      s2 = s2 - c_logtab[k + 2 + nu];
+      double s3 = s2 + h2;
+      s3 = s3 - c_logtab[k + 3];
+      s3 = s3 - c_logtab[k + 3 + nu];
+      double s4 = s3 + h2;
+      s4 = s4 - c_logtab[k + 4];
+      s4 = s4 - c_logtab[k + 4 + nu];
+      const double t1 = rexp<CAREFUL>(s1, bad).t;
+      const double t2 = rexp<CAREFUL>(s2, bad).t;
+      const double t3 = rexp<CAREFUL>(s3, bad).t;
+      const double t4 = rexp<CAREFUL>(s4, bad).t;
+      const double a1 = acc - t1;
+      const double a2 = a1 + t2;
+      const double a3 = a2 - t3;
+      const double a4 = a3 + t4;
+      const bool act1 = t1 > thr, act2 = t2 > thr, act3 = t3 > thr, act4 = t4 > thr;
+      if (__all_sync(FULL_MASK, (act1 && act2 && act3 && act4) || dead)) {
+        s = s4;
+        t = t4;
+        acc = a4;
+        k += 4;
+        T = k;
+        continue;
+      }
+      if (!act1) {
+        s = s1; t = t1; acc = a1; T = k + 1; act = false;
+      } else if (!act2) {
+        s = s2; t = t2; acc = a2; T = k + 2; act = false;
+      } else if (!act3) {
+        s = s3; t = t3; acc = a3; T = k + 3; act = false;
+      } else {
+        s = s4; t = t4; acc = a4; T = k + 4; act = act4;
+      }
+      k += 4;
+      break;
+    }
+#else
     while (k + 2 <= kend) {
       double s1 = s + h2;                                // trip k+1 (odd)
       s1 = s1 - c_logtab[k + 1];
@@ -251,6 +301,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
       k += 2;
       break;
     }
+#endif
     if (dead) {                                          // undo the unpredicated trips
       act = false;
       T = 0;
@@ -286,6 +337,21 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   for (; kr > (int)Tmin; kr--)                           // tail: predicated
     rev_trip<CAREFUL, true, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
+#if BJ_SPEC == 4
+  for (; kr >= 1 && (kr & 3); kr--)                      // align: quads start at k = 0 mod 4
+    rev_trip<CAREFUL, true, false, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                       h2g, t, code, bad);
+  for (; kr >= 4; kr -= 4) {                             // main: every live lane active
+    rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                      h2g, t, code, bad);
+    rev_trip<CAREFUL, true, false, 1>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, bad);
+    rev_trip<CAREFUL, true, false, 0>(kr - 2, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, bad);
+    rev_trip<CAREFUL, true, false, 1>(kr - 3, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, bad);
+  }
+#else
   if (kr >= 1 && !(kr & 1)) {                            // align: pairs start at odd k
     rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
@@ -300,6 +366,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   if (kr == 1)
     rev_trip<CAREFUL, true, false, 1>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
+#endif
   double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
@@ -334,7 +401,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   return o;
 }
 
-__global__ void __launch_bounds__(BJ_BLOCK, 3) k_besselj_grad(
+__global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj_grad(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, double *__restrict__ Jout, double *__restrict__ dzout,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
