@@ -13,6 +13,10 @@
 //            b = e2!).  Each lane's accumulation order is the reference's,
 //            so lane a / lane b equal the two separate passes bit for bit.
 //
+// (The two seed lanes run on two adjacent threads: the primal sweep is
+// duplicated, which is cheap, and each thread carries one cotangent lane —
+// half the live registers, twice the resident warps.)
+//
 // Sweeps 2 and 3 are elided (bit-identical primal recomputation, zero
 // cotangents; see besselj.cu).  rodrigues' own uncompute, which the
 // reference runs inside sweep 1's call (and again inside the uncall of
@@ -32,45 +36,52 @@
 
 namespace rl {
 
+// One cotangent lane per thread: the two threads of an observation carry
+// the e1! and e2! seeds (the reference's two gradient passes).
 struct G2 {
-  double a, b;
+  double a;
 };
 
-// g += (sign * gy) * p for both lanes (numerics.py:419-486)
+// g += (sign * gy) * p (numerics.py:419-486)
 #define GACC(g, sg, p)                  \
   do {                                  \
     const double _p = (p);              \
     (g).a = (g).a + (sg).a * _p;        \
-    (g).b = (g).b + (sg).b * _p;        \
   } while (0)
 
-__device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a, -g.b}; }
-__device__ __forceinline__ G2 zero2() { return G2{0.0, 0.0}; }
+__device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a}; }
+__device__ __forceinline__ G2 zero2() { return G2{0.0}; }
 
-constexpr int BA_BLOCK = 128;
+#ifndef BA_MINB
+#define BA_MINB 4          // __launch_bounds__ min blocks per SM (register budget)
+#endif
+constexpr int BA_BLOCK = 128;               // 64 observations x 2 seed lanes
+constexpr int BA_OBS = BA_BLOCK / 2;
 constexpr int BA_ROW = 31;
 
 template <bool WANT_ERR, bool WANT_FEAT>
-__global__ void __launch_bounds__(BA_BLOCK) k_ba_jac(
+__global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     int n_cams, int n_pts, long long n_obs, const double *__restrict__ cams,
     const double *__restrict__ Xs, const double *__restrict__ ws,
     const double *__restrict__ feats, const int2 *__restrict__ obs, double tol, int chk,
     double *__restrict__ err_out, double *__restrict__ J_out, double *__restrict__ Jf_out,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
-  __shared__ __align__(16) double tile[BA_BLOCK * BA_ROW];
+  __shared__ __align__(16) double tile[BA_OBS * BA_ROW];
   unsigned long long nfail = 0;
-  for (long long blk0 = (long long)blockIdx.x * BA_BLOCK; blk0 < n_obs;
-       blk0 += (long long)gridDim.x * BA_BLOCK) {
-    const long long i = blk0 + threadIdx.x;
+  const int lane2 = threadIdx.x & 1;                  // 0: seed e1!, 1: seed e2!
+  const int ol = threadIdx.x >> 1;                    // observation within the block
+  for (long long blk0 = (long long)blockIdx.x * BA_OBS; blk0 < n_obs;
+       blk0 += (long long)gridDim.x * BA_OBS) {
+    const long long i = blk0 + ol;
     const bool valid = i < n_obs;
-    double row[BA_ROW];
+    double row[16];                                   // this lane's 15 entries (+ weight)
     int code_final = 0;
     if (valid) {
       const int2 o = __ldg(obs + i);
       if (o.x < 0 || o.x >= n_cams || o.y < 0 || o.y >= n_pts) {
         code_final = RL_ERR_INDEX;
 #pragma unroll
-        for (int j = 0; j < BA_ROW; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
+        for (int j = 0; j < 16; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
       } else {
         const double *cp = cams + 11 * (long long)o.x;
         double c[11];
@@ -155,7 +166,7 @@ __global__ void __launch_bounds__(BA_BLOCK) k_ba_jac(
         const double e2 = 0.0 + w * d2;
 
         // ---------------- sweep 3's middle: e2! -= w*d2; e1! -= w*d1 ----------------
-        const G2 ge1{1.0, 0.0}, ge2{0.0, 1.0};
+        const G2 ge1{lane2 ? 0.0 : 1.0}, ge2{lane2 ? 1.0 : 0.0};
         G2 gw = zero2(), gd1 = zero2(), gd2 = zero2();
         GACC(gw, ge2, d2);
         GACC(gd2, ge2, w);
@@ -369,42 +380,36 @@ __global__ void __launch_bounds__(BA_BLOCK) k_ba_jac(
         code_final = code_rod ? code_rod : (code1 ? code1 : code4);
 
 #pragma unroll
-        for (int j = 0; j < 11; j++) {
-          row[j] = gc[j].a;
-          row[15 + j] = gc[j].b;
-        }
+        for (int j = 0; j < 11; j++) row[j] = gc[j].a;
         row[11] = gX0.a;
         row[12] = gX1.a;
         row[13] = gX2.a;
         row[14] = gw.a;
-        row[26] = gX0.b;
-        row[27] = gX1.b;
-        row[28] = gX2.b;
-        row[29] = gw.b;
-        row[30] = gww;
-        if (WANT_ERR) {
+        row[15] = gww;
+        if (WANT_ERR && !lane2) {
           err_out[3 * i] = e1;
           err_out[3 * i + 1] = e2;
           err_out[3 * i + 2] = EW;
         }
         if (WANT_FEAT) {
-          Jf_out[4 * i] = gf1.a;
-          Jf_out[4 * i + 1] = gf2.a;
-          Jf_out[4 * i + 2] = gf1.b;
-          Jf_out[4 * i + 3] = gf2.b;
+          Jf_out[4 * i + 2 * lane2] = gf1.a;
+          Jf_out[4 * i + 2 * lane2 + 1] = gf2.a;
         }
       }
-      fail[i] = (uint8_t)code_final;
-      nfail += code_final != 0;
+      if (!lane2) {
+        fail[i] = (uint8_t)code_final;
+        nfail += code_final != 0;
+      }
     }
     // stage the block's rows and write them out with coalesced 16-byte stores
     __syncthreads();
     if (valid) {
 #pragma unroll
-      for (int j = 0; j < BA_ROW; j++) tile[threadIdx.x * BA_ROW + j] = row[j];
+      for (int j = 0; j < 15; j++) tile[ol * BA_ROW + 15 * lane2 + j] = row[j];
+      if (!lane2) tile[ol * BA_ROW + 30] = row[15];
     }
     __syncthreads();
-    const long long rows = n_obs - blk0 < BA_BLOCK ? n_obs - blk0 : BA_BLOCK;
+    const long long rows = n_obs - blk0 < BA_OBS ? n_obs - blk0 : BA_OBS;
     const int nd = (int)rows * BA_ROW;
     double *dst = J_out + blk0 * BA_ROW;
     if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -438,7 +443,7 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
   rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
                    "occupancy");
   if (rc) return rc;
-  long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
+  long long want = (n_obs + BA_OBS - 1) / BA_OBS;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
   kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,

@@ -50,10 +50,10 @@ __constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
 __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 
 #ifndef BJ_SPEC
-#define BJ_SPEC 2          // speculative trips per warp vote (ILP of the exp chains)
+#define BJ_SPEC 4          // speculative trips per warp vote (ILP of the exp chains)
 #endif
 #ifndef BJ_MINB
-#define BJ_MINB 3          // __launch_bounds__ min blocks per SM (register budget)
+#define BJ_MINB 2          // __launch_bounds__ min blocks per SM (register budget)
 #endif
 constexpr int BJ_BLOCK = 256;
 constexpr int BJ_M = 8;
