@@ -13,10 +13,6 @@
 //            b = e2!).  Each lane's accumulation order is the reference's,
 //            so lane a / lane b equal the two separate passes bit for bit.
 //
-// (The two seed lanes run on two adjacent threads: the primal sweep is
-// duplicated, which is cheap, and each thread carries one cotangent lane —
-// half the live registers, twice the resident warps.)
-//
 // Sweeps 2 and 3 are elided (bit-identical primal recomputation, zero
 // cotangents; see besselj.cu).  rodrigues' own uncompute, which the
 // reference runs inside sweep 1's call (and again inside the uncall of
@@ -36,27 +32,25 @@
 
 namespace rl {
 
-// One cotangent lane per thread: the two threads of an observation carry
-// the e1! and e2! seeds (the reference's two gradient passes).
 struct G2 {
-  double a;
+  double a, b;
 };
 
-// g += (sign * gy) * p (numerics.py:419-486)
+// g += (sign * gy) * p for both lanes (numerics.py:419-486)
 #define GACC(g, sg, p)                  \
   do {                                  \
     const double _p = (p);              \
     (g).a = (g).a + (sg).a * _p;        \
+    (g).b = (g).b + (sg).b * _p;        \
   } while (0)
 
-__device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a}; }
-__device__ __forceinline__ G2 zero2() { return G2{0.0}; }
+__device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a, -g.b}; }
+__device__ __forceinline__ G2 zero2() { return G2{0.0, 0.0}; }
 
 #ifndef BA_MINB
-#define BA_MINB 4          // __launch_bounds__ min blocks per SM (register budget)
+#define BA_MINB 3          // __launch_bounds__ min blocks per SM (register budget)
 #endif
-constexpr int BA_BLOCK = 128;               // 64 observations x 2 seed lanes
-constexpr int BA_OBS = BA_BLOCK / 2;
+constexpr int BA_BLOCK = 128;
 constexpr int BA_ROW = 31;
 
 template <bool WANT_ERR, bool WANT_FEAT>
@@ -66,22 +60,20 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     const double *__restrict__ feats, const int2 *__restrict__ obs, double tol, int chk,
     double *__restrict__ err_out, double *__restrict__ J_out, double *__restrict__ Jf_out,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
-  __shared__ __align__(16) double tile[BA_OBS * BA_ROW];
+  __shared__ __align__(16) double tile[BA_BLOCK * BA_ROW];
   unsigned long long nfail = 0;
-  const int lane2 = threadIdx.x & 1;                  // 0: seed e1!, 1: seed e2!
-  const int ol = threadIdx.x >> 1;                    // observation within the block
-  for (long long blk0 = (long long)blockIdx.x * BA_OBS; blk0 < n_obs;
-       blk0 += (long long)gridDim.x * BA_OBS) {
-    const long long i = blk0 + ol;
+  for (long long blk0 = (long long)blockIdx.x * BA_BLOCK; blk0 < n_obs;
+       blk0 += (long long)gridDim.x * BA_BLOCK) {
+    const long long i = blk0 + threadIdx.x;
     const bool valid = i < n_obs;
-    double row[16];                                   // this lane's 15 entries (+ weight)
+    double row[BA_ROW];
     int code_final = 0;
     if (valid) {
       const int2 o = __ldg(obs + i);
       if (o.x < 0 || o.x >= n_cams || o.y < 0 || o.y >= n_pts) {
         code_final = RL_ERR_INDEX;
 #pragma unroll
-        for (int j = 0; j < 16; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
+        for (int j = 0; j < BA_ROW; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
       } else {
         const double *cp = cams + 11 * (long long)o.x;
         double c[11];
@@ -106,11 +98,18 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
         // rodrigues' routine values (recomputed bit-identically in sweep 4)
         double th = 0, ct = 0, st = 0, ti = 0, w1 = 0, w2 = 0, w3 = 0, cc1 = 0, cc2 = 0, cc3 = 0,
                dt = 0, omc = 0, tmp = 0;
+        // sqrt(sqt), sin/cos(th) and 1/th are evaluated once: the reference
+        // re-evaluates them in its uncompute with the same arguments, i.e.
+        // bit-identical values, so sweep 4 reuses them
+        double sq_t = 0, s_th = 0, c_th = 0, inv_th = 0;
         if (took) {
-          th = 0.0 + sqrt(sqt);
-          ct = 0.0 + cos(th);
-          st = 0.0 + sin(th);
-          ti = 0.0 + 1.0 / th;
+          sq_t = sqrt(sqt);
+          th = 0.0 + sq_t;
+          sincos(th, &s_th, &c_th);
+          inv_th = 1.0 / th;
+          ct = 0.0 + c_th;
+          st = 0.0 + s_th;
+          ti = 0.0 + inv_th;
           w1 = 0.0 + c[0] * ti;
           w2 = 0.0 + c[1] * ti;
           w3 = 0.0 + c[2] * ti;
@@ -166,7 +165,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
         const double e2 = 0.0 + w * d2;
 
         // ---------------- sweep 3's middle: e2! -= w*d2; e1! -= w*d1 ----------------
-        const G2 ge1{lane2 ? 0.0 : 1.0}, ge2{lane2 ? 1.0 : 0.0};
+        const G2 ge1{1.0, 0.0}, ge2{0.0, 1.0};
         G2 gw = zero2(), gd1 = zero2(), gd2 = zero2();
         GACC(gw, ge2, d2);
         GACC(gd2, ge2, w);
@@ -311,16 +310,16 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
           GACC(gti, gw1, c[0]);
           if (chk && !code_rod && (fabs(w3) > tol || fabs(w2) > tol || fabs(w1) > tol))
             code_rod = RL_ERR_DIRTY_ANCILLA;
-          ti = ti - 1.0 / th;
+          ti = ti - inv_th;
           GACC(gth, gti, -(1.0 / (th * th)));
-          st = st - sin(th);
-          GACC(gth, gst, cos(th));
-          ct = ct - cos(th);
-          GACC(gth, gct, -sin(th));
+          st = st - s_th;
+          GACC(gth, gst, c_th);
+          ct = ct - c_th;
+          GACC(gth, gct, -s_th);
           if (chk && !code_rod && (fabs(ti) > tol || fabs(st) > tol || fabs(ct) > tol))
             code_rod = RL_ERR_DIRTY_ANCILLA;
-          th = th - sqrt(sqt);
-          GACC(gsqt, gth, 0.5 / sqrt(sqt));
+          th = th - sq_t;
+          GACC(gsqt, gth, 0.5 / sq_t);
           if (chk && !code_rod && fabs(th) > tol) code_rod = RL_ERR_DIRTY_ANCILLA;
         } else {
           r3 = r3 + c[1] * x1;
@@ -380,36 +379,42 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
         code_final = code_rod ? code_rod : (code1 ? code1 : code4);
 
 #pragma unroll
-        for (int j = 0; j < 11; j++) row[j] = gc[j].a;
+        for (int j = 0; j < 11; j++) {
+          row[j] = gc[j].a;
+          row[15 + j] = gc[j].b;
+        }
         row[11] = gX0.a;
         row[12] = gX1.a;
         row[13] = gX2.a;
         row[14] = gw.a;
-        row[15] = gww;
-        if (WANT_ERR && !lane2) {
+        row[26] = gX0.b;
+        row[27] = gX1.b;
+        row[28] = gX2.b;
+        row[29] = gw.b;
+        row[30] = gww;
+        if (WANT_ERR) {
           err_out[3 * i] = e1;
           err_out[3 * i + 1] = e2;
           err_out[3 * i + 2] = EW;
         }
         if (WANT_FEAT) {
-          Jf_out[4 * i + 2 * lane2] = gf1.a;
-          Jf_out[4 * i + 2 * lane2 + 1] = gf2.a;
+          Jf_out[4 * i] = gf1.a;
+          Jf_out[4 * i + 1] = gf2.a;
+          Jf_out[4 * i + 2] = gf1.b;
+          Jf_out[4 * i + 3] = gf2.b;
         }
       }
-      if (!lane2) {
-        fail[i] = (uint8_t)code_final;
-        nfail += code_final != 0;
-      }
+      fail[i] = (uint8_t)code_final;
+      nfail += code_final != 0;
     }
     // stage the block's rows and write them out with coalesced 16-byte stores
     __syncthreads();
     if (valid) {
 #pragma unroll
-      for (int j = 0; j < 15; j++) tile[ol * BA_ROW + 15 * lane2 + j] = row[j];
-      if (!lane2) tile[ol * BA_ROW + 30] = row[15];
+      for (int j = 0; j < BA_ROW; j++) tile[threadIdx.x * BA_ROW + j] = row[j];
     }
     __syncthreads();
-    const long long rows = n_obs - blk0 < BA_OBS ? n_obs - blk0 : BA_OBS;
+    const long long rows = n_obs - blk0 < BA_BLOCK ? n_obs - blk0 : BA_BLOCK;
     const int nd = (int)rows * BA_ROW;
     double *dst = J_out + blk0 * BA_ROW;
     if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -443,7 +448,7 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
   rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
                    "occupancy");
   if (rc) return rc;
-  long long want = (n_obs + BA_OBS - 1) / BA_OBS;
+  long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
   kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
