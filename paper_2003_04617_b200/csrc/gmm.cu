@@ -27,9 +27,10 @@
 //                 qxc.g = (-dmt/2)(2 Z), and accumulates the factor adjoint
 //                 M = sum_i qxc.g_i xc_i^T (lower triangle) and sum_i qxc.g_i
 //                 in registers across the block's points
-//   k_gmm_params  parameter-only terms (-N lse(alphas), Wishart prior, cst)
-//   k_gmm_final   per component: deterministic reduction of the block
-//                 partials, the chain through qd = exp(icf) and sq, means.g =
+//                 (prep's block 0 also evaluates -N lse(alphas) and its
+//                 gradient; the Wishart prior and cst are added in final)
+//   k_gmm_reduce  deterministic, coalesced sum of the reverse CTAs' partials
+//   k_gmm_final   per component: the chain through qd = exp(icf) and sq, means.g =
 //                 -L^T sum_i qxc.g_i (linearity: sum_i xc.g_i = L^T sum_i qxc.g_i)
 //
 // The uncompute of qxc (qxc -= L xc) is dead (its value only feeds the
@@ -77,12 +78,41 @@ __host__ __device__ constexpr int ltb_idx(int DP, int a, int b) {
 // ---------------------------------------------------------------------------
 // prep: qd, sq (the top @routine), L^T in the block layout, Frobenius share
 // ---------------------------------------------------------------------------
+// -N lse(alphas) with the Int argmax record, as in the program: par[k] =
+// its alphas.g share, par[K] = -N * lsa (one thread)
+__device__ void gmm_alpha_lse(int K, long long N_total, const double *__restrict__ alphas,
+                              double *__restrict__ par) {
+  int ia = 0;
+  for (int k = 1; k < K; k++)
+    if (alphas[k] > alphas[ia]) ia = k;
+  const double amx = 0.0 + alphas[ia];
+  double ase = 0.0;
+  for (int k = 0; k < K; k++) ase = ase + exp(0.0 + (alphas[k] - amx));
+  const double lsa = (0.0 + log(ase)) + amx;
+  const double nn = (double)N_total;
+  par[K] = -(nn * lsa);
+  // gradient: err += nn*lsa (inverse): lsa.g = -nn; then ~routine
+  const double lsag = 0.0 + (-1.0 * 1.0) * nn;
+  double amxg = 0.0 + lsag;                              // lsa -= amx
+  const double aseg = 0.0 + lsag * (1.0 / ase);          // lsa -= log(ase)
+  for (int k = K - 1; k >= 0; k--) {
+    const double ex = exp(0.0 + (alphas[k] - amx));
+    const double tg = 0.0 + aseg * ex;                   // ase -= exp(t)
+    par[k] = tg;                                         // alphas[k].g += t.g
+    amxg = amxg - tg;
+  }
+  par[ia] += amxg;                                       // amx -= alphas[ia]
+}
+
 template <int DP>
-__global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const double *__restrict__ icf,
+__global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long long N_total,
+                                                          const double *__restrict__ alphas,
+                                                          const double *__restrict__ icf,
                                                           double *__restrict__ LT,
                                                           double *__restrict__ qd,
                                                           double *__restrict__ sq,
-                                                          double *__restrict__ fro) {
+                                                          double *__restrict__ fro,
+                                                          double *__restrict__ par) {
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
   const double *ic = icf + (long long)k * P;
@@ -112,6 +142,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, const do
     for (int j = 0; j < d; j++) s = s + ic[j];           // sq[k] += icf[k, j] (in order)
     sq[k] = s;
   }
+  if (k == 0 && threadIdx.x == 32 && par) gmm_alpha_lse(K, N_total, alphas, par);
   // qd and this component's share of the prior's Frobenius sum:
   // fro += abs2(qd![k, j]) (j <= d) or abs2(icf[k, j]) (j > d)
   double f = 0.0;
@@ -563,41 +594,19 @@ __global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
 }
 
 // ---------------------------------------------------------------------------
-// parameter-only terms: -N lse(alphas) (reversible max, as in the program),
-// Wishart prior, cst.  ws_par = [g_alpha_param (K), err_param]
+// deterministic reduction of the reverse CTAs' partials over the S splits:
+// red[k][e] = sum_s part[k][s][e] (coalesced along e)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(32) k_gmm_params(
-    int d, int K, long long N_total, const double *__restrict__ alphas,
-    const double *__restrict__ fro_k, const double *__restrict__ sq, double ga, int wm, double cst,
-    double *__restrict__ ws_par) {
-  const double hg2 = 0.5 * ga * ga;
-  double fro = 0.0;
-  for (int k = 0; k < K; k++) fro = fro + fro_k[k];
-  if (threadIdx.x == 0) {
-    double ssq = 0.0;
-    for (int k = 0; k < K; k++) ssq = ssq + sq[k];
-    // logsumexp(alphas) with the Int argmax record (as in the point routine)
-    int ia = 0;
-    for (int k = 1; k < K; k++)
-      if (alphas[k] > alphas[ia]) ia = k;
-    const double amx = 0.0 + alphas[ia];
-    double ase = 0.0;
-    for (int k = 0; k < K; k++) ase = ase + exp(0.0 + (alphas[k] - amx));
-    const double lsa = (0.0 + log(ase)) + amx;
-    const double nn = (double)N_total;
-    ws_par[K] = -(nn * lsa) + hg2 * fro - (double)wm * ssq + cst;
-    // gradient: err += nn*lsa (inverse): lsa.g = -nn; then ~routine
-    const double lsag = 0.0 + (-1.0 * 1.0) * nn;
-    double amxg = 0.0 + lsag;                              // lsa -= amx
-    const double aseg = 0.0 + lsag * (1.0 / ase);          // lsa -= log(ase)
-    for (int k = K - 1; k >= 0; k--) {
-      const double ex = exp(0.0 + (alphas[k] - amx));
-      const double tg = 0.0 + aseg * ex;                   // ase -= exp(t)
-      ws_par[k] = tg;                                      // alphas[k].g += t.g
-      amxg = amxg - tg;
-    }
-    ws_par[ia] += amxg;                                    // amx -= alphas[ia]
-  }
+__global__ void __launch_bounds__(GMM_THREADS) k_gmm_reduce(int S, long long PW,
+                                                            const double *__restrict__ part,
+                                                            double *__restrict__ red) {
+  const int k = blockIdx.y;
+  const long long e = (long long)blockIdx.x * GMM_THREADS + threadIdx.x;
+  if (e >= PW) return;
+  const double *pk = part + (long long)k * S * PW + e;
+  double s = 0.0;
+  for (int j = 0; j < S; j++) s += pk[(long long)j * PW];
+  red[(long long)k * PW + e] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -606,9 +615,10 @@ __global__ void __launch_bounds__(32) k_gmm_params(
 template <int DP>
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     int d, int K, int S, int nerr, const double *__restrict__ icf, const double *__restrict__ qd,
+    const double *__restrict__ sq, const double *__restrict__ fro_k,
     const double *__restrict__ LT, const double *__restrict__ part,
     const double *__restrict__ err_part, const double *__restrict__ ws_par, double ga, int wm,
-    int add_params, double *__restrict__ out) {
+    double cst, int add_params, double *__restrict__ out) {
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
   const long long PW = (long long)DP * DP + DP + 1;
@@ -618,8 +628,8 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
   double *g_alpha = out + 1;
   double *g_means = out + 1 + K;
   double *g_icf = out + 1 + K + (long long)K * d;
-  const double *pk = part + (long long)k * S * PW;
-  // column sums of qxc.g and sum of mt.g, reduced over the S partials in order
+  const double *pk = part + (long long)k * S * PW;     // reduced partials: S == 1
+  // column sums of qxc.g and sum of mt.g
   for (int b = threadIdx.x; b <= DP; b += GMM_THREADS) {
     double s = 0.0;
     for (int j = 0; j < S; j++) s += pk[j * PW + (long long)DP * DP + b];
@@ -669,7 +679,16 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
   if (k == 0 && threadIdx.x == 0) {
     double e = 0.0;
     for (int j = 0; j < nerr; j++) e += err_part[j];
-    out[0] = e + (add_params ? ws_par[K] : 0.0);
+    if (add_params) {
+      // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst)
+      double fro = 0.0, ssq = 0.0;
+      for (int kk = 0; kk < K; kk++) {
+        fro = fro + fro_k[kk];
+        ssq = ssq + sq[kk];
+      }
+      e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
+    }
+    out[0] = e;
   }
 }
 
@@ -712,7 +731,7 @@ static int choose_split(int K, long long ntiles, int slots, int smax) {
 }
 
 struct GmmLayout {
-  size_t lt, qd, sq, fro, mt, gmt, flags, errp, part, par, total;
+  size_t lt, qd, sq, fro, mt, gmt, flags, errp, part, red, par, total;
   int Sf, Sr, nerr;
 };
 
@@ -745,6 +764,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.flags = take((size_t)N * 4);
   L.errp = take((size_t)(L.nerr > 0 ? L.nerr : 1) * 8);
   L.part = take((size_t)K * L.Sr * (size_t)pw * 8);
+  L.red = take((size_t)K * (size_t)pw * 8);
   L.par = take((size_t)(K + 1) * 8);
   L.total = off;
   return L;
@@ -766,14 +786,12 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
   unsigned *flags = (unsigned *)(ws + L.flags);
   double *errp = (double *)(ws + L.errp), *part = (double *)(ws + L.part);
+  double *redp = (double *)(ws + L.red);
   double *par = (double *)(ws + L.par);
   int rc;
-  k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, icf, LT, qd, sq, fro);
+  k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
+                                            add_params ? par : nullptr);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
-  if (add_params) {
-    k_gmm_params<<<1, 32, 0, st>>>(d, K, N_total, alphas, fro, sq, gamma, m, cst, par);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_params"))) return rc;
-  }
   if (N > 0) {
     if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
       return rc;
@@ -799,8 +817,12 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                                           st), "memset part")))
       return rc;
   }
-  k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, LT, part, errp,
-                                             par, gamma, m, add_params, out);
+  const long long PW = (long long)DP * DP + DP + 1;
+  k_gmm_reduce<<<dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K), GMM_THREADS, 0, st>>>(
+      L.Sr, PW, part, redp);
+  if ((rc = cuda_status(cudaGetLastError(), "k_gmm_reduce"))) return rc;
+  k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, 1, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT,
+                                             redp, errp, par, gamma, m, cst, add_params, out);
   return cuda_status(cudaGetLastError(), "k_gmm_final");
 }
 
