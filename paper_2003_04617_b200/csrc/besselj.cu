@@ -337,21 +337,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   for (; kr > (int)Tmin; kr--)                           // tail: predicated
     rev_trip<CAREFUL, true, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
-#if BJ_SPEC == 4
-  for (; kr >= 1 && (kr & 3); kr--)                      // align: quads start at k = 0 mod 4
-    rev_trip<CAREFUL, true, false, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
-                                       h2g, t, code, bad);
-  for (; kr >= 4; kr -= 4) {                             // main: every live lane active
-    rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
-                                      h2g, t, code, bad);
-    rev_trip<CAREFUL, true, false, 1>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
-                                      s, h2g, t, code, bad);
-    rev_trip<CAREFUL, true, false, 0>(kr - 2, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
-                                      s, h2g, t, code, bad);
-    rev_trip<CAREFUL, true, false, 1>(kr - 3, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
-                                      s, h2g, t, code, bad);
-  }
-#else
+  // the reverse loop is counted (no votes): pairs already overlap the exp chains
   if (kr >= 1 && !(kr & 1)) {                            // align: pairs start at odd k
     rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
@@ -366,7 +352,6 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   if (kr == 1)
     rev_trip<CAREFUL, true, false, 1>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
-#endif
   double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
