@@ -48,7 +48,7 @@ __device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a, -g.b}; }
 __device__ __forceinline__ G2 zero2() { return G2{0.0, 0.0}; }
 
 #ifndef BA_MINB
-#define BA_MINB 3          // __launch_bounds__ min blocks per SM (register budget)
+#define BA_MINB 4          // __launch_bounds__ min blocks per SM (register budget)
 #endif
 constexpr int BA_BLOCK = 128;
 constexpr int BA_ROW = 31;
