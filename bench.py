@@ -350,10 +350,15 @@ def bessel_cpu(target_s=10.0, n_max=1 << 22):
 
 
 def load_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture at the
+    bench's problem size (profiles/traffic.json, tools/make_traffic.py)."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as fh:
-            return json.load(fh).get(kernel)
+            d = json.load(fh)
+        for k, v in d.items():
+            if not k.startswith("_") and (k == kernel or k.startswith(kernel + "<")):
+                return v
     return None
 
 

@@ -9,7 +9,7 @@ timeout 900 python bench.py --workload gmm > gpurun_out/bench_gmm.json 2> gpurun
 timeout 900 python bench.py --workload gmm_large --steps 3 --warmup 3 --no-e2e > gpurun_out/bench_gmm_large.json 2> gpurun_out/bench_gmm_large.err; echo "bench gmm_large rc=$?"
 timeout 300 python tools/probe_weights.py > gpurun_out/probe_plain.log 2>&1
 if [ "${NO_NCU:-0}" = "1" ]; then exit 0; fi
-SMALL="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --n 16777216"
+SMALL="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 BA="python bench.py --workload ba --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 GMM="python bench.py --workload gmm --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 300 $SMALL > gpurun_out/bench_small.json 2>&1 && \
