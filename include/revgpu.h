@@ -132,6 +132,32 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          int32_t m, double cst, double tol, int32_t invcheck, double *out,
                          unsigned long long *n_failed, int32_t device);
 
+/* ------------------------------------------------------------------------
+ * run / uncall / objective-only ("-O") entries: the primal sweeps of the same
+ * programs with every reversibility check, no cotangents.
+ *
+ * rl_besselj_run_f64 replaces run(p, "besselj", [out_in[i], nu, z[i]])
+ * (direction +1, interpreter.py:1021) or uncall(...) (direction -1,
+ * interpreter.py:1026): out[i] = out_in[i] +/- J_nu(z[i]); out_in may be NULL
+ * (zeros).  rl_ba_residuals_f64: run of ba_proj and ba_weight on zero
+ * outputs, err = n_obs x 3 [e1, e2, 1 - w^2].  rl_gmm_objective_f64: run of
+ * gmm, err[0] = the objective (per-point terms of this shard, plus the
+ * parameter terms when add_param_terms); same workspace as the gradient.
+ * ---------------------------------------------------------------------- */
+int rl_besselj_run_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                       int64_t max_trips, int32_t invcheck, int32_t direction,
+                       const double *out_in, double *out, uint8_t *fail,
+                       unsigned long long *counters, void *stream);
+int rl_ba_residuals_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                        const double *X, const double *w, const double *feats,
+                        const int32_t *obs, double tol, int32_t invcheck, double *err,
+                        uint8_t *fail, unsigned long long *counters, void *stream);
+int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
+                         const double *means, const double *icf, const double *x, double gamma,
+                         int32_t m, double cst, double tol, int32_t invcheck,
+                         int32_t add_param_terms, double *err, uint8_t *fail,
+                         unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

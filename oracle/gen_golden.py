@@ -26,7 +26,7 @@ OUT_DIR = os.path.join(REPO, "tests", "golden")
 
 sys.dont_write_bytecode = True
 sys.path.insert(0, REF_SRC)
-from revlang import ExecOptions, GradRequest, gradient, parse_program  # noqa: E402
+from revlang import ExecOptions, GradRequest, gradient, parse_program, run, uncall  # noqa: E402
 from revlang.errors import RevLangError  # noqa: E402
 from revlang.values import Array  # noqa: E402
 
@@ -182,8 +182,44 @@ def gen_gmm():
     print(f"gmm: {len(cases)} cases in {time.perf_counter() - t0:.1f}s")
 
 
+# --------------------------------------------------------------------------
+# run / uncall (reference interpreter.py:1021-1028) with non-zero outputs
+# --------------------------------------------------------------------------
+
+def gen_run():
+    pb = _prog("besselj.rnl")
+    rng = np.random.default_rng(20)
+    z = rng.uniform(0.1, 10.0, 200)
+    out0 = rng.normal(0.0, 1.0, 200)
+    r_run, r_unc, errs = np.full(200, np.nan), np.full(200, np.nan), []
+    z[7], z[8] = -2.0, 25.0              # RevDomainError, DirtyAncilla
+    for i in range(200):
+        a, en = _err_name(lambda: run(pb, "besselj", [float(out0[i]), 2, float(z[i])]))
+        b, en2 = _err_name(lambda: uncall(pb, "besselj", [float(out0[i]), 2, float(z[i])]))
+        if a is not None:
+            r_run[i] = a[0]
+        if b is not None:
+            r_unc[i] = b[0]
+        errs.append(en or en2)
+    pa = _prog("ba.rnl")
+    cams, X, w, feat = ba_inputs(np.random.default_rng(21), 16)
+    e_in = np.random.default_rng(22).normal(0.0, 1.0, (16, 2))
+    ba_run = np.full((16, 2), np.nan)
+    ba_unc = np.full((16, 2), np.nan)
+    for o in range(16):
+        args = [float(e_in[o, 0]), float(e_in[o, 1]), Array.vector(cams[o].tolist()),
+                Array.vector(X[o].tolist()), float(w[o]), float(feat[o, 0]), float(feat[o, 1])]
+        a = run(pa, "ba_proj", args)
+        b = uncall(pa, "ba_proj", args)
+        ba_run[o], ba_unc[o] = a[:2], b[:2]
+    np.savez_compressed(os.path.join(OUT_DIR, "run.npz"), bj_z=z, bj_out0=out0, bj_run=r_run,
+                        bj_uncall=r_unc, bj_err=np.array(errs), ba_cams=cams, ba_X=X, ba_w=w,
+                        ba_feat=feat, ba_e_in=e_in, ba_run=ba_run, ba_uncall=ba_unc)
+    print("run/uncall goldens written")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
-    which = sys.argv[1:] or ["bessel", "ba", "gmm"]
+    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run"]
     for w in which:
         globals()["gen_" + w]()

@@ -19,13 +19,16 @@ from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBo
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
                      UnknownExample, UnknownFunction, UnsupportedProgram)
-from .kernels import (BAResult, BesselResult, GMMResult, ba_jacobian, besselj_grad,
-                      besselj_grad_host, gmm_grad)
+from .interp import CheckReport, check_reversibility, run, uncall
+from .kernels import (BAResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_residuals,
+                      besselj_grad, besselj_grad_host, besselj_run, gmm_grad, gmm_objective)
 from .programs import CATALOG, Program, entry_function, load_example, parse_program
 from .values import Array
 
 __all__ = [
-    "AliasedArguments", "Array", "BAResult", "BesselResult", "CATALOG", "DirtyAncilla",
+    "AliasedArguments", "Array", "BAResult", "BesselResult", "CATALOG", "CheckReport",
+    "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
+    "gmm_objective", "run", "uncall",
     "ExecOptions", "FuelExhausted", "GMMResult", "GradRequest", "IndexOutOfBounds",
     "KindError", "LoopIteratorMutated", "MissingAdjoint", "NativeLibraryError",
     "PostconditionMismatch", "Program", "RevDomainError", "RevError", "RevLangError",

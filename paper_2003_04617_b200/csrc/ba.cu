@@ -36,12 +36,15 @@ struct G2 {
   double a, b;
 };
 
-// g += (sign * gy) * p for both lanes (numerics.py:419-486)
+// g += (sign * gy) * p for both lanes (numerics.py:419-486); compiled out in
+// the residual-only (run) instantiation
 #define GACC(g, sg, p)                  \
   do {                                  \
-    const double _p = (p);              \
-    (g).a = (g).a + (sg).a * _p;        \
-    (g).b = (g).b + (sg).b * _p;        \
+    if (GRAD) {                         \
+      const double _p = (p);            \
+      (g).a = (g).a + (sg).a * _p;      \
+      (g).b = (g).b + (sg).b * _p;      \
+    }                                   \
   } while (0)
 
 __device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a, -g.b}; }
@@ -53,7 +56,10 @@ __device__ __forceinline__ G2 zero2() { return G2{0.0, 0.0}; }
 constexpr int BA_BLOCK = 128;
 constexpr int BA_ROW = 31;
 
-template <bool WANT_ERR, bool WANT_FEAT>
+// GRAD: the Jacobian (sweeps 1 + 4 with two cotangent lanes).  !GRAD: run
+// of ba_proj / ba_weight on zero outputs — the residuals [e1, e2, 1 - w^2]
+// with every check of the primal sweeps (the objective-only kernel).
+template <bool WANT_ERR, bool WANT_FEAT, bool GRAD = true>
 __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     int n_cams, int n_pts, long long n_obs, const double *__restrict__ cams,
     const double *__restrict__ Xs, const double *__restrict__ ws,
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
           err_out[3 * i + 1] = e2;
           err_out[3 * i + 2] = EW;
         }
-        if (WANT_FEAT) {
+        if (WANT_FEAT && GRAD) {
           Jf_out[4 * i] = gf1.a;
           Jf_out[4 * i + 1] = gf2.a;
           Jf_out[4 * i + 2] = gf1.b;
@@ -407,6 +413,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
       fail[i] = (uint8_t)code_final;
       nfail += code_final != 0;
     }
+    if (!GRAD) continue;
     // stage the block's rows and write them out with coalesced 16-byte stores
     __syncthreads();
     if (valid) {
@@ -455,6 +462,32 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
                                   J, Jfeat, fail, counters);
   return cuda_status(cudaGetLastError(), "k_ba_jac launch");
+}
+
+int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                        const double *X, const double *w, const double *feats,
+                        const int32_t *obs, double tol, int32_t invcheck, double *err,
+                        uint8_t *fail, unsigned long long *counters, cudaStream_t st) {
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 ||
+      (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !err || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_ba_residuals_f64: bad argument");
+  if ((reinterpret_cast<uintptr_t>(feats) & 15) || (reinterpret_cast<uintptr_t>(obs) & 7))
+    return set_error(RL_ERR_INVALID, "rl_ba_residuals_f64: feats must be 16-byte and obs 8-byte aligned");
+  int rc = ensure_device_tables();
+  if (rc) return rc;
+  if (n_obs == 0) return RL_OK;
+  auto kern = k_ba_jac<true, false, false>;
+  int bps = 0;
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
+                   "occupancy");
+  if (rc) return rc;
+  long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
+  long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
+  int grid = (int)(want < cap ? want : cap);
+  kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+                                  reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
+                                  nullptr, nullptr, fail, counters);
+  return cuda_status(cudaGetLastError(), "k_ba_jac (residuals) launch");
 }
 
 }  // namespace rl

@@ -143,8 +143,9 @@ __device__ __forceinline__ void fwd_trip(int k, int nu, double h2, double thr, b
 }
 
 // One reverse trip at (warp-uniform) k for lanes with k <= T (PRED) or
-// all lanes (the caller guarantees every live lane has k <= T).
-template <bool CAREFUL, bool TAB, bool PRED, int ODD>
+// all lanes (the caller guarantees every live lane has k <= T).  With
+// !GRAD (run / uncall / objective only) the cotangents are not carried.
+template <bool CAREFUL, bool TAB, bool PRED, int ODD, bool GRAD = true>
 __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, double paccg,
                                          double naccg, int chk, bool live, int T, double &acc,
                                          double &sg, double &s, double &h2g, double &t,
@@ -154,11 +155,11 @@ __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, d
   // inverse if: odd k: acc += convert(s) (sign -1); even: acc -= convert(s)
   const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
   const double an = odd ? acc + t : acc - t;
-  const double sgn = sg + (odd ? naccg : paccg) * t;
+  const double sgn = GRAD ? sg + (odd ? naccg : paccg) * t : 0.0;
   double sn = s + l2;                                    // s *= kn
   sn = sn + l1;                                          // s *= k
   sn = sn - h2;                                          // s /= halfz2
-  const double h2gn = h2g + 1.0 * sgn;
+  const double h2gn = GRAD ? h2g + 1.0 * sgn : 0.0;
   const ExpR e = rexp<CAREFUL>(sn, bad);
   if (!PRED || k <= T) {
     acc = an;
@@ -179,7 +180,7 @@ __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, d
 // fall back to predicated trips only for the tail.
 // ktab (uniform) = last k with k + nu inside the log table; kfuel = the
 // fuel cap on trips.
-template <bool CAREFUL>
+template <bool CAREFUL, bool GRAD>
 __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, double thr,
                                                  double tol, double seed, int ktab, int kfuel,
                                                  int chk) {
@@ -332,30 +333,30 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   const unsigned Tmin = __reduce_min_sync(FULL_MASK, fwd_ok ? (unsigned)T : 0x7fffffffu);
   int kr = Tmax;
   for (; kr > ktab; kr--)                                // beyond the table
-    rev_trip<CAREFUL, false, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
+    rev_trip<CAREFUL, false, true, -1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
                                        fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
   for (; kr > (int)Tmin; kr--)                           // tail: predicated
-    rev_trip<CAREFUL, true, true, -1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
+    rev_trip<CAREFUL, true, true, -1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
   // the reverse loop is counted (no votes): pairs already overlap the exp chains
   if (kr >= 1 && !(kr & 1)) {                            // align: pairs start at odd k
-    rev_trip<CAREFUL, true, false, 0>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+    rev_trip<CAREFUL, true, false, 0, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
     kr--;
   }
   for (; kr >= 2; kr -= 2) {                             // main: every live lane active
-    rev_trip<CAREFUL, true, false, 1>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+    rev_trip<CAREFUL, true, false, 1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
-    rev_trip<CAREFUL, true, false, 0>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+    rev_trip<CAREFUL, true, false, 0, GRAD>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
                                       s, h2g, t, code, bad);
   }
   if (kr == 1)
-    rev_trip<CAREFUL, true, false, 1>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+    rev_trip<CAREFUL, true, false, 1, GRAD>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, bad);
   double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
-    sg = sg + (1.0 * accg) * t;
+    if (GRAD) sg = sg + (1.0 * accg) * t;
     double hzg = 0.0;
     for (int q = nu; q >= 1; q--) {                      // for i = nu:-1:1
       s = s + logi(q);
@@ -371,7 +372,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     halfz = halfz - lz;                                  // halfz /= lz
     const double lzg = 0.0 + 1.0 * hzg;
     lz = lz - logz;                                      // lz /= convert(z)
-    zg = zg + (1.0 * lzg) / z;
+    if (GRAD) zg = zg + (1.0 * lzg) / z;
     if (chk && !code) {                                  // releases
       if (fabs(acc - 0.0) > tol || fabs(s - 0.0) > tol || fabs(h2 - 0.0) > tol ||
           fabs(halfz - 0.0) > tol || fabs(lz - 0.0) > tol)
@@ -386,10 +387,15 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   return o;
 }
 
-__global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj_grad(
+// GRAD: gradient (sweeps 1 + 4, Jout = J, dzout = dJ/dz).  !GRAD: run /
+// uncall of besselj (Jout = out_in + sign * J with every check of the two
+// primal sweeps; dzout unused): the objective-only ("-O") kernel.
+template <bool GRAD>
+__global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
-    long long max_trips, int chk, double *__restrict__ Jout, double *__restrict__ dzout,
-    uint8_t *__restrict__ fail, unsigned long long *counters) {
+    long long max_trips, int chk, const double *__restrict__ out_in, double sign,
+    double *__restrict__ Jout, double *__restrict__ dzout, uint8_t *__restrict__ fail,
+    unsigned long long *counters) {
   const int ktab = LOGTAB_N - 1 - (nu > 0 ? nu : 0);
   const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
@@ -458,9 +464,10 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj_grad(
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {
         const double z = valid ? s_z[pos] : 1.0;
-        BJOut o = besselj_element<false>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk);
+        BJOut o = besselj_element<false, GRAD>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk);
         if (__any_sync(FULL_MASK, o.bad)) {              // |exp arg| >= 708 somewhere
-          const BJOut c = besselj_element<true>(z, o.bad, nu, thr, tol, seed, ktab, kfuel, chk);
+          const BJOut c =
+              besselj_element<true, GRAD>(z, o.bad, nu, thr, tol, seed, ktab, kfuel, chk);
           if (o.bad) o = c;
         }
         if (valid) {
@@ -479,8 +486,14 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj_grad(
     for (int m = 0; m < BJ_M; m++) {
       const int e = m * BJ_BLOCK + tid;
       if (e < cnt) {
-        __stcs(Jout + base + e, s_J[e]);
-        __stcs(dzout + base + e, s_dz[e]);
+        if (GRAD) {
+          __stcs(Jout + base + e, s_J[e]);
+          __stcs(dzout + base + e, s_dz[e]);
+        } else {
+          // out! += acc (run) / out! -= acc (uncall): one IEEE add, like the reference
+          const double o0 = out_in ? __ldcs(out_in + base + e) : 0.0;
+          __stcs(Jout + base + e, sign > 0 ? o0 + s_J[e] : o0 - s_J[e]);
+        }
         fail[base + e] = s_fail[e];
       }
     }
@@ -498,28 +511,49 @@ static int upload_logtab() {
 
 int besselj_tables_init() { return upload_logtab(); }
 
-int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double tol, double seed,
-                   int64_t max_trips, int32_t invcheck, double *J, double *dJdz, uint8_t *fail,
-                   unsigned long long *counters, cudaStream_t st) {
-  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)) || max_trips < 0)
-    return set_error(RL_ERR_INVALID, "rl_besselj_grad_f64: bad argument");
+template <bool GRAD>
+static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                            double seed, int64_t max_trips, int32_t invcheck,
+                            const double *out_in, double sign, double *J, double *dJdz,
+                            uint8_t *fail, unsigned long long *counters, cudaStream_t st) {
   int rc = ensure_device_tables();
   if (rc) return rc;
   if (n == 0) return RL_OK;
   int blocks_per_sm = 0;
-  rc = cuda_status(cudaFuncSetAttribute(k_besselj_grad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  rc = cuda_status(cudaFuncSetAttribute(k_besselj<GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         BJ_SMEM), "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj_grad,
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj<GRAD>,
                                                                  BJ_BLOCK, BJ_SMEM),
                    "occupancy");
   if (rc) return rc;
   const long long want = (n + BJ_C - 1) / BJ_C;
   const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   const int grid = (int)(want < cap ? want : cap);
-  k_besselj_grad<<<grid, BJ_BLOCK, BJ_SMEM, st>>>(nu, z, n, thr, tol, seed, max_trips,
-                                            invcheck ? 1 : 0, J, dJdz, fail, counters);
-  return cuda_status(cudaGetLastError(), "k_besselj_grad launch");
+  k_besselj<GRAD><<<grid, BJ_BLOCK, BJ_SMEM, st>>>(nu, z, n, thr, tol, seed, max_trips,
+                                                   invcheck ? 1 : 0, out_in, sign, J, dJdz, fail,
+                                                   counters);
+  return cuda_status(cudaGetLastError(), "k_besselj launch");
+}
+
+int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double tol, double seed,
+                   int64_t max_trips, int32_t invcheck, double *J, double *dJdz, uint8_t *fail,
+                   unsigned long long *counters, cudaStream_t st) {
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)) || max_trips < 0)
+    return set_error(RL_ERR_INVALID, "rl_besselj_grad_f64: bad argument");
+  return launch_besselj_t<true>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0, J,
+                                dJdz, fail, counters, st);
+}
+
+int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                       int64_t max_trips, int32_t invcheck, int32_t direction,
+                       const double *out_in, double *out, uint8_t *fail,
+                       unsigned long long *counters, cudaStream_t st) {
+  if (n < 0 || (n > 0 && (!z || !out || !fail)) || max_trips < 0 ||
+      (direction != 1 && direction != -1))
+    return set_error(RL_ERR_INVALID, "rl_besselj_run_f64: bad argument");
+  return launch_besselj_t<false>(nu, z, n, thr, tol, 0.0, max_trips, invcheck, out_in,
+                                 (double)direction, out, nullptr, fail, counters, st);
 }
 
 }  // namespace rl

@@ -28,7 +28,15 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
                const double *means, const double *icf, const double *x, double gamma, int32_t m,
                double cst, double tol, int32_t invcheck, int32_t add_param_terms, double *out,
                uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
-               cudaStream_t st);
+               cudaStream_t st, int grad);
+int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                       int64_t max_trips, int32_t invcheck, int32_t direction,
+                       const double *out_in, double *out, uint8_t *fail,
+                       unsigned long long *counters, cudaStream_t st);
+int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                        const double *X, const double *w, const double *feats,
+                        const int32_t *obs, double tol, int32_t invcheck, double *err,
+                        uint8_t *fail, unsigned long long *counters, cudaStream_t st);
 
 static thread_local char g_last_error[512];
 
@@ -315,7 +323,32 @@ int rl_gmm_grad_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const doub
                     int32_t add_param_terms, double *out, uint8_t *fail,
                     unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
   return launch_gmm(d, K, N, N_total, alphas, means, icf, x, gamma, m, cst, tol, invcheck,
-                    add_param_terms, out, fail, counters, ws, ws_bytes, as_stream(stream));
+                    add_param_terms, out, fail, counters, ws, ws_bytes, as_stream(stream), 1);
+}
+
+int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
+                         const double *means, const double *icf, const double *x, double gamma,
+                         int32_t m, double cst, double tol, int32_t invcheck,
+                         int32_t add_param_terms, double *err, uint8_t *fail,
+                         unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
+  return launch_gmm(d, K, N, N_total, alphas, means, icf, x, gamma, m, cst, tol, invcheck,
+                    add_param_terms, err, fail, counters, ws, ws_bytes, as_stream(stream), 0);
+}
+
+int rl_besselj_run_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                       int64_t max_trips, int32_t invcheck, int32_t direction,
+                       const double *out_in, double *out, uint8_t *fail,
+                       unsigned long long *counters, void *stream) {
+  return launch_besselj_run(nu, z, n, thr, tol, max_trips, invcheck, direction, out_in, out, fail,
+                            counters, as_stream(stream));
+}
+
+int rl_ba_residuals_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                        const double *X, const double *w, const double *feats,
+                        const int32_t *obs, double tol, int32_t invcheck, double *err,
+                        uint8_t *fail, unsigned long long *counters, void *stream) {
+  return launch_ba_residuals(n_cams, n_pts, n_obs, cams, X, w, feats, obs, tol, invcheck, err,
+                             fail, counters, as_stream(stream));
 }
 
 int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
@@ -348,7 +381,7 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
     return rc;
   if ((rc = launch_gmm(d, K, N, N, (double *)da.p, (double *)dm.p, (double *)di.p,
                        (double *)dx.p, gamma, m, cst, tol, invcheck, 1, (double *)dout.p,
-                       (uint8_t *)dfl.p, (unsigned long long *)dc.p, dws.p, wsb, st)))
+                       (uint8_t *)dfl.p, (unsigned long long *)dc.p, dws.p, wsb, st, 1)))
     return rc;
   unsigned long long h[2];
   if ((rc = cuda_status(cudaMemcpyAsync(out, dout.p, nout * 8, cudaMemcpyDeviceToHost, st),

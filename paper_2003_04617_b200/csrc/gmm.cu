@@ -693,6 +693,28 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
 }
 
 // ---------------------------------------------------------------------------
+// objective only: out[0] = sum of the point terms (+ parameter terms)
+// ---------------------------------------------------------------------------
+__global__ void k_gmm_err(int K, int nerr, const double *__restrict__ err_part,
+                          const double *__restrict__ sq, const double *__restrict__ fro_k,
+                          const double *__restrict__ ws_par, double ga, int wm, double cst,
+                          int add_params, double *__restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double e = 0.0;
+  for (int j = 0; j < nerr; j++) e += err_part[j];
+  if (add_params) {
+    const double hg2 = 0.5 * ga * ga;
+    double fro = 0.0, ssq = 0.0;
+    for (int kk = 0; kk < K; kk++) {
+      fro = fro + fro_k[kk];
+      ssq = ssq + sq[kk];
+    }
+    e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
+  }
+  out[0] = e;
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
@@ -737,6 +759,12 @@ struct GmmLayout {
 
 static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 
+struct GmmLayout;
+static int launch_gmm_err_only(int K, const GmmLayout &L, long long N, const double *errp,
+                               const double *sq, const double *fro, const double *par,
+                               double gamma, int m, double cst, int add_params, double *out,
+                               cudaStream_t st);
+
 static GmmLayout gmm_layout(int d, int K, long long N) {
   GmmLayout L{};
   const int DP = dp_of(d);
@@ -770,16 +798,27 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   return L;
 }
 
+static int launch_gmm_err_only(int K, const GmmLayout &L, long long N, const double *errp,
+                               const double *sq, const double *fro, const double *par,
+                               double gamma, int m, double cst, int add_params, double *out,
+                               cudaStream_t st) {
+  k_gmm_err<<<1, 32, 0, st>>>(K, N > 0 ? L.nerr : 0, errp, sq, fro, par, gamma, m, cst,
+                              add_params, out);
+  return cuda_status(cudaGetLastError(), "k_gmm_err");
+}
+
 size_t gmm_workspace_bytes(int32_t d, int32_t K, int64_t N) {
   if (d <= 0 || d > 128 || K <= 0 || N < 0) return 0;
   return gmm_layout(d, K, N).total;
 }
 
+// grad == 0: objective only (prep, forward tiles, logsumexp; out[0] = err)
 template <int DP>
 static int run_gmm(int d, int K, long long N, long long N_total, const double *alphas,
                    const double *means, const double *icf, const double *x, double gamma, int m,
                    double cst, double tol, int chk, int add_params, double *out, uint8_t *fail,
-                   unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st) {
+                   unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st,
+                   int grad = 1) {
   constexpr int TPF = 64, TPR = DP == 32 ? 64 : 32;
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
   double *fro = (double *)(ws + L.fro);
@@ -810,8 +849,12 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
                                               counters);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
+    if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
+                                         add_params, out, st);
     k_gmm_rev<DP, TPR><<<dim3(K, L.Sr), GMM_THREADS, sr, st>>>(d, K, N, means, x, LT, gmt, part);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_rev"))) return rc;
+  } else if (!grad) {
+    return launch_gmm_err_only(K, L, 0, errp, sq, fro, par, gamma, m, cst, add_params, out, st);
   } else {
     if ((rc = cuda_status(cudaMemsetAsync(part, 0, (size_t)K * L.Sr * ((size_t)DP * DP + DP + 1) * 8,
                                           st), "memset part")))
@@ -830,7 +873,7 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
                const double *means, const double *icf, const double *x, double gamma, int32_t m,
                double cst, double tol, int32_t invcheck, int32_t add_param_terms, double *out,
                uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
-               cudaStream_t st) {
+               cudaStream_t st, int grad) {
   if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || !out || (N > 0 && (!x || !fail)))
     return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64: bad argument");
   if (d > 128) return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64: d > 128 is not supported");
@@ -844,12 +887,12 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
   const long long Nt = N_total > 0 ? N_total : N;
   if (DP == 32)
     return run_gmm<32>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                       add_param_terms, out, fail, counters, (char *)ws, L, st);
+                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
   if (DP == 64)
     return run_gmm<64>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                       add_param_terms, out, fail, counters, (char *)ws, L, st);
+                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
   return run_gmm<128>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                      add_param_terms, out, fail, counters, (char *)ws, L, st);
+                      add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
 }
 
 }  // namespace rl

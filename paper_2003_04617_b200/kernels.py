@@ -227,3 +227,87 @@ def gmm_grad(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
                            workspace.numel(), _stream_handle())
     _native.check(rc, "rl_gmm_grad_f64")
     return unpack_gmm(packed, d, K, fail, counters)
+
+
+# ---------------------------------------------------------------------------
+# run / uncall / objective-only entries (primal sweeps with every check)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RunResult:
+    out: torch.Tensor        # updated output argument per element
+    fail: torch.Tensor
+    counters: torch.Tensor
+
+    @property
+    def n_failed(self):
+        return int(self.counters[1].item())
+
+
+def besselj_run(z, nu=2, *, out_in=None, direction=1, thr=1e-16, tol=1e-9, invcheck=True,
+                max_steps=500_000_000, counters=None):
+    """Batched `run(p, "besselj", [out_in_i, nu, z_i])` (direction +1,
+    interpreter.py:1021) or `uncall(...)` (direction -1, :1026):
+    out = out_in +/- J_nu(z), with every check of the primal sweeps.  Also the
+    objective-only ("-O") timing of the Bessel program."""
+    z = _require_cuda("z", z)
+    if out_in is not None:
+        out_in = _require_cuda("out_in", out_in)
+        if out_in.shape != z.shape:
+            raise KindError("out_in must have the shape of z")
+    out = torch.empty_like(z)
+    fail = torch.empty(z.shape, dtype=torch.uint8, device=z.device)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=z.device)
+    rc = _native.lib().rl_besselj_run_f64(
+        int(nu), _ptr(z), z.numel(), float(thr), float(tol),
+        max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)), int(direction),
+        _ptr(out_in), _ptr(out), _ptr(fail), _ptr(counters), _stream_handle())
+    _native.check(rc, "rl_besselj_run_f64")
+    return RunResult(out, fail, counters)
+
+
+def ba_residuals(cams, X, w, feats, obs, *, tol=1e-9, invcheck=True, counters=None):
+    """Batched run of ba_proj / ba_weight on zero outputs: (p, 3) residuals
+    [e1, e2, 1 - w^2] — the BA objective-only kernel."""
+    cams = _require_cuda("cams", cams, ndim=2, last=11)
+    X = _require_cuda("X", X, ndim=2, last=3)
+    w = _require_cuda("w", w, ndim=1)
+    feats = _require_cuda("feats", feats, ndim=2, last=2)
+    obs = _require_cuda("obs", obs, dtype=torch.int32, ndim=2, last=2)
+    p = w.shape[0]
+    err = torch.empty((p, 3), dtype=F64, device=w.device)
+    fail = torch.empty(p, dtype=torch.uint8, device=w.device)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=w.device)
+    rc = _native.lib().rl_ba_residuals_f64(
+        cams.shape[0], X.shape[0], p, _ptr(cams), _ptr(X), _ptr(w), _ptr(feats), _ptr(obs),
+        float(tol), int(bool(invcheck)), _ptr(err), _ptr(fail), _ptr(counters), _stream_handle())
+    _native.check(rc, "rl_ba_residuals_f64")
+    return RunResult(err, fail, counters)
+
+
+def gmm_objective(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
+                  add_param_terms=True, tol=1e-9, invcheck=True, workspace=None, counters=None):
+    """Batched run of gmm: the objective only ("-O"), a 0-d tensor."""
+    alphas = _require_cuda("alphas", alphas, ndim=1)
+    means = _require_cuda("means", means, ndim=2)
+    K, d = means.shape
+    icf = _require_cuda("icf", icf, ndim=2, last=d * (d + 1) // 2)
+    x = _require_cuda("x", x, ndim=2, last=d)
+    N = x.shape[0]
+    L = _native.lib()
+    wsb = L.rl_gmm_workspace_bytes(d, K, N)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    err = torch.empty(1, dtype=F64, device=x.device)
+    fail = torch.empty(N, dtype=torch.uint8, device=x.device)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=x.device)
+    rc = L.rl_gmm_objective_f64(d, K, N, int(N if N_total is None else N_total), _ptr(alphas),
+                                _ptr(means), _ptr(icf), _ptr(x), float(gamma), int(m), float(cst),
+                                float(tol), int(bool(invcheck)), int(bool(add_param_terms)),
+                                _ptr(err), _ptr(fail), _ptr(counters), _ptr(workspace),
+                                workspace.numel(), _stream_handle())
+    _native.check(rc, "rl_gmm_objective_f64")
+    return RunResult(err[0], fail, counters)
