@@ -160,6 +160,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def time_device(fn, steps, flush=None):
+    """Mean device ms of fn() over `steps` launches (CUDA events on the current
+    stream; optional L2 flush between launches, outside the events)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        if flush is not None:
+            flush.fill_(1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    return tot / steps
+
+
 def load_weights():
     p = os.path.join(REPO, "profiles", "fp64_weights.json")
     if os.path.exists(p):
@@ -274,6 +295,10 @@ def run_bessel_ours(args, D):
         tr = load_traffic("k_besselj_grad")
         if tr:
             roof["traffic"] = tr
+    # objective only ("-O", the paper's objective timing): run of besselj
+    o_ms = D.max(time_device(lambda: kernels.besselj_run(z, BESSEL_NU), max(3, args.steps // 4)))
+    objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
+                 "kernel": "k_besselj<false> (rl_besselj_run_f64)"}
     e2e = None
     if not args.no_e2e:
         e2e = bessel_e2e(torch, z, args, D, n_total)
@@ -288,6 +313,7 @@ def run_bessel_ours(args, D):
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clocks, "sum_trips_per_step": D.sum(sum_trips),
         "failed_per_step": D.sum(n_failed), "parity_sample": parity,
+        "objective_only": objective,
     }
     return res
 
@@ -449,6 +475,22 @@ def run_ba_ours(args, D):
         sc = np.max(np.abs(Jo), axis=1, keepdims=True)
         parity = {"n": 2000, "max_err_over_rowscale": float(np.max(np.abs(Jg - Jo) / sc)),
                   "flags_equal": bool(np.array_equal(fail.cpu().numpy()[idx], fo))}
+    o_ms = D.max(time_device(lambda: kernels.ba_residuals(dc, dX, dw, df, do),
+                             max(3, args.steps // 4), flush))
+    objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
+                 "kernel": "k_ba_jac<true,false,false> (rl_ba_residuals_f64)"}
+    # the same Jacobian as ADBench's BASparseMat (CSR values + int32 pattern)
+    csr_out = (torch.empty(3 * p + 1, dtype=torch.int32, device=dev),
+               torch.empty(31 * p, dtype=torch.int32, device=dev),
+               torch.empty(31 * p, dtype=torch.float64, device=dev), fail, None)
+    c_ms = D.max(time_device(lambda: kernels.ba_jacobian_csr(
+        dc, dX, dw, df, do, obs_offset=lo, n_obs_total=p_total, out=csr_out, counters=counters),
+        max(3, args.steps // 4), flush))
+    c_bytes = byts + p * (31 * 4 + 3 * 4) + 4
+    csr = {"ms_per_step": round(c_ms, 4), "kernel": "k_ba_jac<..,CSR> (rl_ba_jac_csr_f64)",
+           "bytes_per_launch": D.sum(c_bytes),
+           "achieved_gbs": round(D.sum(c_bytes) / (c_ms * 1e-3) / 1e9, 1),
+           "frac": round(D.sum(c_bytes) / (c_ms * 1e-3) / 1e9 / peak, 4)}
     e2e = None
     if not args.no_e2e:
         e2e = ba_e2e(cams, X, w[lo:hi], feats[lo:hi], obs[lo:hi], args, D)
@@ -463,6 +505,7 @@ def run_ba_ours(args, D):
         "obs_per_s": round(p_total / (ms_step * 1e-3), 1),
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
         "failed_per_step": n_failed // args.steps, "parity_sample": parity,
+        "objective_only": objective, "csr_jacobian": csr,
     }
 
 
@@ -626,6 +669,12 @@ def run_gmm_ours(args, D):
                 "mat_vec_flops_executed": executed,
                 "executed_frac": round(executed / (ms_step * 1e-3) / 1e12 / peak, 4),
                 "peak_source": "in-run DFMA microkernel (tools/fp64probe.cu)"}
+    o_ms = D.max(time_device(
+        lambda: kernels.gmm_objective(alphas, means, icf, x, gamma, m, cst, N_total=N,
+                                      add_param_terms=(D.rank == 0), workspace=ws),
+        max(2, args.steps // 2), flush))
+    objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
+                 "kernel": "k_gmm_prep/fwd/lse/err (rl_gmm_objective_f64)"}
     parity = None
     if D.rank == 0 and args.workload == "gmm" and D.world == 1:
         sys.path.insert(0, os.path.join(REPO, "oracle"))
@@ -652,7 +701,7 @@ def run_gmm_ours(args, D):
                    "l2": "256 MiB L2 flush before every evaluation"},
         "roofline": roof, "gpu_launches": 6 * args.steps, "clocks": clocks,
         "failed_per_step": D.sum(int(counters[1].item())) // (args.steps + max(args.warmup, 3)),
-        "parity_sample": parity,
+        "parity_sample": parity, "objective_only": objective,
     }
     if not args.no_e2e and D.world == 1:
         res["e2e"] = gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D)

@@ -158,6 +158,38 @@ int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const
                          int32_t add_param_terms, double *err, uint8_t *fail,
                          unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
 
+/* ----------------------------------------------------------------------
+ * BA Jacobian in ADBench's sparse layout (BASparseMat, CSR with int row
+ * pointers and column indices).  Same values as
+ * rl_ba_jac_f64 (the reference's two seeded gradient(p, GradRequest(
+ * "ba_proj", ...)) calls + gradient of ba_weight, autodiff.py:136-180),
+ * stored as ADBench's insert_reproj_err_block / insert_w_err_block build
+ * it: nrows = 3P, ncols = 11 n_cams + 3 n_pts + P, nnz = 31P;
+ *   rows 2i, 2i+1 (i < P): 15 entries each — cols 11c..11c+10 (camera c),
+ *     11 n_cams + 3p .. +2 (point p), 11 n_cams + 3 n_pts + i (weight i);
+ *   row 2P + i: one entry, col 11 n_cams + 3 n_pts + i, value -2 w_i.
+ * A call may produce one shard of the observations: obs_offset is the
+ * global index of obs[0] and n_obs_total = P.  The shard's arrays are its
+ * two pieces of the global arrays, concatenated:
+ *   vals/cols [31 n_obs]   = global [30 off, 30 (off+n_obs)) ++ [30P + off, 30P + off + n_obs)
+ *   rows [3 n_obs + 1]     = global rows [2 off, 2 (off+n_obs)) ++ [2P + off, 2P + off + n_obs]
+ * (with obs_offset = 0 and n_obs_total = n_obs these are exactly the
+ * BASparseMat arrays).  rows and cols are both NULL (values only: the
+ * pattern depends on obs alone) or both non-NULL.  Errors: RL_ERR_INVALID
+ * when 31P or ncols does not fit int32; per-observation codes in fail[] as
+ * for rl_ba_jac_f64.  The _host variant takes whole-problem host arrays.
+ * ---------------------------------------------------------------------- */
+int rl_ba_jac_csr_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offset,
+                      int64_t n_obs_total, const double *cams, const double *X, const double *w,
+                      const double *feats, const int32_t *obs, double tol, int32_t invcheck,
+                      double *err, int32_t *rows, int32_t *cols, double *vals, uint8_t *fail,
+                      unsigned long long *counters, void *stream);
+int rl_ba_jac_csr_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                           const double *X, const double *w, const double *feats,
+                           const int32_t *obs, double tol, int32_t invcheck, int32_t *rows,
+                           int32_t *cols, double *vals, uint8_t *fail,
+                           unsigned long long *n_failed, int32_t device);
+
 #ifdef __cplusplus
 }
 #endif

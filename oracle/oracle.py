@@ -122,3 +122,48 @@ def gmm_grad(alphas, means, icf, x, gamma, m, cst, tol=1e-9, invcheck=True):
                             int(m), float(cst), tol, int(bool(invcheck)), ctypes.byref(err),
                             _dp(ga), _dp(gm), _dp(gi))
     return rc, err.value, ga, gm, gi
+
+
+def ba_sparse(n_cams, n_pts, obs, J31):
+    """ADBench's BASparseMat built from per-observation Jacobian rows —
+    TEST INFRASTRUCTURE (the checker of rl_ba_jac_csr_f64).
+
+    Restates ADBench (github.com/microsoft/ADBench, src/cpp/shared/ba.h/.cpp
+    `BASparseMat`; not part of /root/reference, which stops at the dense
+    per-observation gradients): the constructor pushes rows = [0];
+    `insert_reproj_err_block(i, cam, pt, J)` with J the column-major 2x15
+    block (J[2*col + row]) appends two rows of 15 — 11 camera columns
+    11*cam + k, 3 point columns 11*n + 3*pt + k, the weight column
+    11*n + 3*m + i — for every observation in order; then
+    `insert_w_err_block(i, w_d)` appends one row per observation with the
+    single column 11*n + 3*m + i.  Plain loops on purpose: the kernel's
+    indexing is checked against this, not against a vectorised copy of
+    itself.  Layout unpinned against ADBench files (none are available
+    here); values are pinned through the reference goldens of ba_jac."""
+    obs = np.asarray(obs)
+    p = obs.shape[0]
+    rows, cols, vals = [0], [], []
+    for i in range(p):
+        cam, pt = int(obs[i, 0]), int(obs[i, 1])
+        # our row: [de1/dcam(11) de1/dX(3) de1/dw | de2/dcam de2/dX de2/dw | dwerr/dw]
+        Jcm = [0.0] * 30
+        for col in range(15):
+            Jcm[2 * col] = J31[i, col]
+            Jcm[2 * col + 1] = J31[i, 15 + col]
+        rows.append(rows[-1] + 15)
+        rows.append(rows[-1] + 15)
+        for r in range(2):
+            for k in range(11):
+                cols.append(11 * cam + k)
+                vals.append(Jcm[2 * k + r])
+            for k in range(3):
+                cols.append(11 * n_cams + 3 * pt + k)
+                vals.append(Jcm[22 + 2 * k + r])
+            cols.append(11 * n_cams + 3 * n_pts + i)
+            vals.append(Jcm[28 + r])
+    for i in range(p):
+        rows.append(rows[-1] + 1)
+        cols.append(11 * n_cams + 3 * n_pts + i)
+        vals.append(J31[i, 30])
+    return (np.array(rows, np.int32), np.array(cols, np.int32), np.array(vals, np.float64),
+            (3 * p, 11 * n_cams + 3 * n_pts + p))

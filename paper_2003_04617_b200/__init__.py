@@ -20,13 +20,14 @@ from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBo
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
                      UnknownExample, UnknownFunction, UnsupportedProgram)
 from .interp import CheckReport, check_reversibility, run, uncall
-from .kernels import (BAResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_residuals,
+from .kernels import (BACsr, BAResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_jacobian_csr,
+                      ba_jacobian_csr_host, ba_residuals,
                       besselj_grad, besselj_grad_host, besselj_run, gmm_grad, gmm_objective)
 from .programs import CATALOG, Program, entry_function, load_example, parse_program
 from .values import Array
 
 __all__ = [
-    "AliasedArguments", "Array", "BAResult", "BesselResult", "CATALOG", "CheckReport",
+    "AliasedArguments", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",
     "ExecOptions", "FuelExhausted", "GMMResult", "GradRequest", "IndexOutOfBounds",

@@ -59,14 +59,28 @@ constexpr int BA_ROW = 31;
 // GRAD: the Jacobian (sweeps 1 + 4 with two cotangent lanes).  !GRAD: run
 // of ba_proj / ba_weight on zero outputs — the residuals [e1, e2, 1 - w^2]
 // with every check of the primal sweeps (the objective-only kernel).
-template <bool WANT_ERR, bool WANT_FEAT, bool GRAD = true>
+//
+// CSR: write the Jacobian as this shard's part of ADBench's BASparseMat
+// (see BaCsr) instead of dense (p, 31) rows.
+struct BaCsr {
+  int32_t *rows;   // [2 p_l + p_l + 1] global row pointers (nullptr: values only)
+  int32_t *cols;   // [31 p_l] global column indices   (nullptr: values only)
+  double *vals;    // [31 p_l]
+  long long off;   // global index of this shard's first observation
+  long long P;     // global number of observations
+  int col_pt;      // 11 n: first point column
+  int col_w;       // 11 n + 3 m: first weight column
+};
+
+template <bool WANT_ERR, bool WANT_FEAT, bool GRAD = true, bool CSR = false>
 __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     int n_cams, int n_pts, long long n_obs, const double *__restrict__ cams,
     const double *__restrict__ Xs, const double *__restrict__ ws,
     const double *__restrict__ feats, const int2 *__restrict__ obs, double tol, int chk,
     double *__restrict__ err_out, double *__restrict__ J_out, double *__restrict__ Jf_out,
-    uint8_t *__restrict__ fail, unsigned long long *counters) {
+    uint8_t *__restrict__ fail, unsigned long long *counters, BaCsr csr) {
   __shared__ __align__(16) double tile[BA_BLOCK * BA_ROW];
+  __shared__ int2 otile[CSR ? BA_BLOCK : 1];
   unsigned long long nfail = 0;
   for (long long blk0 = (long long)blockIdx.x * BA_BLOCK; blk0 < n_obs;
        blk0 += (long long)gridDim.x * BA_BLOCK) {
@@ -76,8 +90,10 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     int code_final = 0;
     if (valid) {
       const int2 o = __ldg(obs + i);
+      if (CSR) otile[threadIdx.x] = o;
       if (o.x < 0 || o.x >= n_cams || o.y < 0 || o.y >= n_pts) {
         code_final = RL_ERR_INDEX;
+        if (CSR) otile[threadIdx.x] = make_int2(-1, -1);
 #pragma unroll
         for (int j = 0; j < BA_ROW; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
       } else {
@@ -422,6 +438,40 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     }
     __syncthreads();
     const long long rows = n_obs - blk0 < BA_BLOCK ? n_obs - blk0 : BA_BLOCK;
+    if (CSR) {
+      // ADBench BASparseMat::insert_reproj_err_block order: per observation two
+      // rows of 15 (cam 11 | point 3 | weight 1), then all weight rows
+      // (insert_w_err_block) after the 2P reprojection rows.
+      const int nr = (int)rows * 30;
+      double *dv = csr.vals + blk0 * 30;
+      int32_t *dc = csr.cols ? csr.cols + blk0 * 30 : nullptr;
+      for (int k = threadIdx.x; k < nr; k += BA_BLOCK) {
+        const int ob = k / 30, j = k - 30 * ob;
+        dv[k] = tile[ob * BA_ROW + j];
+        if (dc) {
+          const int jj = j < 15 ? j : j - 15;
+          const int2 o = otile[ob];
+          int col;
+          if (jj < 11) col = o.x < 0 ? -1 : 11 * o.x + jj;
+          else if (jj < 14) col = o.y < 0 ? -1 : csr.col_pt + 3 * o.y + (jj - 11);
+          else col = csr.col_w + (int)(csr.off + blk0 + ob);
+          dc[k] = col;
+        }
+      }
+      if (threadIdx.x < rows) {
+        const long long t = blk0 + threadIdx.x;           // local observation
+        const long long g = csr.off + t;                   // global observation
+        csr.vals[n_obs * 30 + t] = tile[threadIdx.x * BA_ROW + 30];
+        if (csr.cols) {
+          csr.cols[n_obs * 30 + t] = csr.col_w + (int)g;
+          csr.rows[2 * t] = (int32_t)(30 * g);
+          csr.rows[2 * t + 1] = (int32_t)(30 * g + 15);
+          csr.rows[2 * n_obs + t] = (int32_t)(30 * csr.P + g);
+          if (t == n_obs - 1) csr.rows[3 * n_obs] = (int32_t)(30 * csr.P + g + 1);
+        }
+      }
+      continue;
+    }
     const int nd = (int)rows * BA_ROW;
     double *dst = J_out + blk0 * BA_ROW;
     if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -460,7 +510,7 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
   int grid = (int)(want < cap ? want : cap);
   kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
-                                  J, Jfeat, fail, counters);
+                                  J, Jfeat, fail, counters, BaCsr{});
   return cuda_status(cudaGetLastError(), "k_ba_jac launch");
 }
 
@@ -486,8 +536,48 @@ int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doub
   int grid = (int)(want < cap ? want : cap);
   kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
-                                  nullptr, nullptr, fail, counters);
+                                  nullptr, nullptr, fail, counters, BaCsr{});
   return cuda_status(cudaGetLastError(), "k_ba_jac (residuals) launch");
+}
+
+int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offset,
+                  int64_t n_obs_total, const double *cams, const double *X, const double *w,
+                  const double *feats, const int32_t *obs, double tol, int32_t invcheck,
+                  double *err, int32_t *rows, int32_t *cols, double *vals, uint8_t *fail,
+                  unsigned long long *counters, cudaStream_t st) {
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 || obs_offset < 0 || n_obs_total < obs_offset + n_obs ||
+      (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !vals || !fail)) ||
+      ((rows == nullptr) != (cols == nullptr)))
+    return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64: bad argument");
+  // BASparseMat holds int row pointers / column indices
+  const long long ncols = 11LL * n_cams + 3LL * n_pts + n_obs_total;
+  if (31LL * n_obs_total > INT32_MAX || ncols > INT32_MAX)
+    return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64: nnz or ncols exceeds int32 (BASparseMat)");
+  if ((reinterpret_cast<uintptr_t>(feats) & 15) || (reinterpret_cast<uintptr_t>(obs) & 7))
+    return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64: feats must be 16-byte and obs 8-byte aligned");
+  int rc = ensure_device_tables();
+  if (rc) return rc;
+  if (n_obs == 0) {
+    if (rows) {
+      const int32_t end = (int32_t)(30 * n_obs_total + obs_offset);
+      return cuda_status(cudaMemcpyAsync(rows, &end, sizeof end, cudaMemcpyHostToDevice, st),
+                         "rows terminator");
+    }
+    return RL_OK;
+  }
+  auto kern = err ? k_ba_jac<true, false, true, true> : k_ba_jac<false, false, true, true>;
+  int bps = 0;
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
+                   "occupancy");
+  if (rc) return rc;
+  long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
+  long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
+  int grid = (int)(want < cap ? want : cap);
+  BaCsr csr{rows, cols, vals, obs_offset, n_obs_total, 11 * n_cams, 11 * n_cams + 3 * n_pts};
+  kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+                                  reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
+                                  nullptr, nullptr, fail, counters, csr);
+  return cuda_status(cudaGetLastError(), "k_ba_jac (csr) launch");
 }
 
 }  // namespace rl

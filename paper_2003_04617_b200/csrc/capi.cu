@@ -37,6 +37,11 @@ int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doub
                         const double *X, const double *w, const double *feats,
                         const int32_t *obs, double tol, int32_t invcheck, double *err,
                         uint8_t *fail, unsigned long long *counters, cudaStream_t st);
+int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offset,
+                  int64_t n_obs_total, const double *cams, const double *X, const double *w,
+                  const double *feats, const int32_t *obs, double tol, int32_t invcheck,
+                  double *err, int32_t *rows, int32_t *cols, double *vals, uint8_t *fail,
+                  unsigned long long *counters, cudaStream_t st);
 
 static thread_local char g_last_error[512];
 
@@ -349,6 +354,106 @@ int rl_ba_residuals_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doub
                         uint8_t *fail, unsigned long long *counters, void *stream) {
   return launch_ba_residuals(n_cams, n_pts, n_obs, cams, X, w, feats, obs, tol, invcheck, err,
                              fail, counters, as_stream(stream));
+}
+
+int rl_ba_jac_csr_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offset,
+                      int64_t n_obs_total, const double *cams, const double *X, const double *w,
+                      const double *feats, const int32_t *obs, double tol, int32_t invcheck,
+                      double *err, int32_t *rows, int32_t *cols, double *vals, uint8_t *fail,
+                      unsigned long long *counters, void *stream) {
+  return launch_ba_csr(n_cams, n_pts, n_obs, obs_offset, n_obs_total, cams, X, w, feats, obs, tol,
+                       invcheck, err, rows, cols, vals, fail, counters, as_stream(stream));
+}
+
+int rl_ba_jac_csr_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                           const double *X, const double *w, const double *feats,
+                           const int32_t *obs, double tol, int32_t invcheck, int32_t *rows,
+                           int32_t *cols, double *vals, uint8_t *fail,
+                           unsigned long long *n_failed, int32_t device) {
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 || !vals || ((rows == nullptr) != (cols == nullptr)) ||
+      (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64_host: bad argument");
+  if (31LL * n_obs > INT32_MAX || 11LL * n_cams + 3LL * n_pts + n_obs > INT32_MAX)
+    return set_error(RL_ERR_INVALID,
+                     "rl_ba_jac_csr_f64_host: nnz or ncols exceeds int32 (BASparseMat)");
+  if (rows) rows[3 * n_obs] = (int32_t)(31 * n_obs);
+  if (n_obs == 0) return RL_OK;
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  DevBuf dcam, dX, dc;
+  if ((rc = dcam.alloc((size_t)n_cams * 11 * 8, pl.st[0])) ||
+      (rc = dX.alloc((size_t)n_pts * 3 * 8, pl.st[0])) ||
+      (rc = dc.alloc(2 * 8 * Pipeline::NS, pl.st[0])))
+    return rc;
+  auto *cnt = (unsigned long long *)dc.p;
+  if ((rc = cuda_status(cudaMemcpyAsync(dcam.p, cams, (size_t)n_cams * 88, cudaMemcpyHostToDevice,
+                                        pl.st[0]), "H2D cams")) ||
+      (rc = cuda_status(cudaMemcpyAsync(dX.p, X, (size_t)n_pts * 24, cudaMemcpyHostToDevice,
+                                        pl.st[0]), "H2D X")) ||
+      (rc = cuda_status(cudaMemsetAsync(cnt, 0, 2 * 8 * Pipeline::NS, pl.st[0]), "memset")))
+    return rc;
+  if ((rc = pl.finish())) return rc;
+  // each chunk is launched as a shard (obs_offset = chunk start, total = n_obs):
+  // its local [reprojection | weight] parts land in the two halves of the
+  // global arrays
+  const int64_t CH = int64_t(1) << 18;
+  const int64_t nch = (n_obs + CH - 1) / CH;
+  const int64_t bufn = std::min<int64_t>(CH, n_obs);
+  DevBuf dw[Pipeline::NS], df2[Pipeline::NS], dob[Pipeline::NS], dv[Pipeline::NS],
+      dr[Pipeline::NS], dcl[Pipeline::NS], dfl[Pipeline::NS];
+  for (int s = 0; s < Pipeline::NS && s < nch; s++) {
+    if ((rc = dw[s].alloc(bufn * 8, pl.st[s])) || (rc = df2[s].alloc(bufn * 16, pl.st[s])) ||
+        (rc = dob[s].alloc(bufn * 8, pl.st[s])) || (rc = dv[s].alloc(bufn * 31 * 8, pl.st[s])) ||
+        (rc = dr[s].alloc(rows ? (bufn * 3 + 1) * 4 : 4, pl.st[s])) ||
+        (rc = dcl[s].alloc(rows ? bufn * 31 * 4 : 4, pl.st[s])) ||
+        (rc = dfl[s].alloc(bufn, pl.st[s])))
+      return rc;
+  }
+  for (int64_t c = 0; c < nch; c++) {
+    const int s = (int)(c % Pipeline::NS);
+    const int64_t off = c * CH, m = std::min(CH, n_obs - off);
+    cudaStream_t st = pl.st[s];
+    if ((rc = cuda_status(cudaMemcpyAsync(dw[s].p, w + off, m * 8, cudaMemcpyHostToDevice, st),
+                          "H2D w")) ||
+        (rc = cuda_status(cudaMemcpyAsync(df2[s].p, feats + 2 * off, m * 16,
+                                          cudaMemcpyHostToDevice, st), "H2D feats")) ||
+        (rc = cuda_status(cudaMemcpyAsync(dob[s].p, obs + 2 * off, m * 8, cudaMemcpyHostToDevice,
+                                          st), "H2D obs")))
+      return rc;
+    int32_t *r = rows ? (int32_t *)dr[s].p : nullptr, *cl = rows ? (int32_t *)dcl[s].p : nullptr;
+    if ((rc = launch_ba_csr(n_cams, n_pts, m, off, n_obs, (double *)dcam.p, (double *)dX.p,
+                            (double *)dw[s].p, (double *)df2[s].p, (int32_t *)dob[s].p, tol,
+                            invcheck, nullptr, r, cl, (double *)dv[s].p, (uint8_t *)dfl[s].p,
+                            cnt + 2 * s, st)))
+      return rc;
+    const double *v = (const double *)dv[s].p;
+    if ((rc = cuda_status(cudaMemcpyAsync(vals + 30 * off, v, m * 30 * 8, cudaMemcpyDeviceToHost,
+                                          st), "D2H vals")) ||
+        (rc = cuda_status(cudaMemcpyAsync(vals + 30 * n_obs + off, v + 30 * m, m * 8,
+                                          cudaMemcpyDeviceToHost, st), "D2H vals (w)")) ||
+        (rc = cuda_status(cudaMemcpyAsync(fail + off, dfl[s].p, m, cudaMemcpyDeviceToHost, st),
+                          "D2H fail")))
+      return rc;
+    if (rows &&
+        ((rc = cuda_status(cudaMemcpyAsync(cols + 30 * off, cl, m * 30 * 4,
+                                           cudaMemcpyDeviceToHost, st), "D2H cols")) ||
+         (rc = cuda_status(cudaMemcpyAsync(cols + 30 * n_obs + off, cl + 30 * m, m * 4,
+                                           cudaMemcpyDeviceToHost, st), "D2H cols (w)")) ||
+         (rc = cuda_status(cudaMemcpyAsync(rows + 2 * off, r, m * 2 * 4, cudaMemcpyDeviceToHost,
+                                           st), "D2H rows")) ||
+         (rc = cuda_status(cudaMemcpyAsync(rows + 2 * n_obs + off, r + 2 * m, m * 4,
+                                           cudaMemcpyDeviceToHost, st), "D2H rows (w)"))))
+      return rc;
+  }
+  if ((rc = pl.finish())) return rc;
+  unsigned long long h[2 * Pipeline::NS];
+  if ((rc = cuda_status(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost), "D2H counters")))
+    return rc;
+  unsigned long long nf = 0;
+  for (int s = 0; s < Pipeline::NS; s++) nf += h[2 * s + 1];
+  if (n_failed) *n_failed = nf;
+  return RL_OK;
 }
 
 int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,

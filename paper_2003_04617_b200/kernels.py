@@ -311,3 +311,91 @@ def gmm_objective(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=Non
                                 workspace.numel(), _stream_handle())
     _native.check(rc, "rl_gmm_objective_f64")
     return RunResult(err[0], fail, counters)
+
+
+@dataclass
+class BACsr:
+    """The BA Jacobian in ADBench's BASparseMat layout (CSR, int32 indices):
+    nrows = 3P (2 reprojection rows per observation, then one weight row per
+    observation), ncols = 11 n_cams + 3 n_pts + P, nnz = 31P.  For a shard
+    (obs_offset > 0 or n_obs_total > n_obs) the arrays are the shard's two
+    pieces of the global arrays concatenated (include/revgpu.h)."""
+    rows: object            # int32 [3 n_obs + 1] or None (values only)
+    cols: object            # int32 [31 n_obs]    or None
+    vals: object            # float64 [31 n_obs]
+    fail: object            # uint8 [n_obs]
+    shape: tuple            # (nrows, ncols) of the global matrix
+    counters: object = None  # device counters, or the host call's failure count
+    err: object = None      # (n_obs, 3) residuals when want_err
+
+    def to_scipy(self):
+        """scipy.sparse.csr_matrix of a whole-problem result."""
+        import numpy as np
+        import scipy.sparse as sp
+
+        f = (lambda t: t.cpu().numpy()) if isinstance(self.vals, torch.Tensor) else np.asarray
+        return sp.csr_matrix((f(self.vals), f(self.cols), f(self.rows)), shape=self.shape)
+
+
+def _ba_shape(n_cams, n_pts, P):
+    return (3 * P, 11 * n_cams + 3 * n_pts + P)
+
+
+def ba_jacobian_csr(cams, X, w, feats, obs, *, obs_offset=0, n_obs_total=None, pattern=True,
+                    tol=1e-9, invcheck=True, want_err=False, out=None, counters=None):
+    """ba_jacobian stored as ADBench's BASparseMat (CSR).  `pattern=False`
+    skips the row pointers / column indices (they depend on obs only)."""
+    cams = _require_cuda("cams", cams, ndim=2, last=11)
+    X = _require_cuda("X", X, ndim=2, last=3)
+    w = _require_cuda("w", w, ndim=1)
+    feats = _require_cuda("feats", feats, ndim=2, last=2)
+    obs = _require_cuda("obs", obs, dtype=torch.int32, ndim=2, last=2)
+    p = w.shape[0]
+    if feats.shape[0] != p or obs.shape[0] != p:
+        raise KindError("w, feats and obs must have the same number of observations")
+    P = p + obs_offset if n_obs_total is None else int(n_obs_total)
+    dev = w.device
+    if out is None:
+        vals = torch.empty(31 * p, dtype=F64, device=dev)
+        rows = torch.empty(3 * p + 1, dtype=torch.int32, device=dev) if pattern else None
+        cols = torch.empty(31 * p, dtype=torch.int32, device=dev) if pattern else None
+        fail = torch.empty(p, dtype=torch.uint8, device=dev)
+        err = torch.empty((p, 3), dtype=F64, device=dev) if want_err else None
+    else:
+        rows, cols, vals, fail, err = out
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    L = _native.lib()
+    rc = L.rl_ba_jac_csr_f64(cams.shape[0], X.shape[0], p, int(obs_offset), P, _ptr(cams), _ptr(X),
+                             _ptr(w), _ptr(feats), _ptr(obs), float(tol), int(bool(invcheck)),
+                             _ptr(err), _ptr(rows), _ptr(cols), _ptr(vals), _ptr(fail),
+                             _ptr(counters), _stream_handle())
+    _native.check(rc, "rl_ba_jac_csr_f64")
+    return BACsr(rows, cols, vals, fail, _ba_shape(cams.shape[0], X.shape[0], P), counters, err)
+
+
+def ba_jacobian_csr_host(cams, X, w, feats, obs, *, pattern=True, tol=1e-9, invcheck=True,
+                         device=None):
+    """Host-buffer entry (numpy in, numpy out) of ba_jacobian_csr for a whole
+    problem: the C-ABI `_host` call pipelines the copies with the kernel."""
+    import numpy as np
+
+    c = lambda a, t: np.ascontiguousarray(a.numpy() if isinstance(a, torch.Tensor) else a,  # noqa
+                                          dtype=t)
+    cams, X, w, feats = (c(a, np.float64) for a in (cams, X, w, feats))
+    obs = c(obs, np.int32)
+    p = w.size
+    vals = np.empty(31 * p)
+    rows = np.empty(3 * p + 1, np.int32) if pattern else None
+    cols = np.empty(31 * p, np.int32) if pattern else None
+    fail = np.empty(p, np.uint8)
+    nfail = ctypes.c_ulonglong(0)
+    dev = torch.cuda.current_device() if device is None else int(device)
+    L = _native.lib()
+    rc = L.rl_ba_jac_csr_f64_host(cams.shape[0], X.shape[0], p, cams.ctypes.data, X.ctypes.data,
+                                  w.ctypes.data, feats.ctypes.data, obs.ctypes.data, float(tol),
+                                  int(bool(invcheck)), None if rows is None else rows.ctypes.data,
+                                  None if cols is None else cols.ctypes.data, vals.ctypes.data,
+                                  fail.ctypes.data, ctypes.byref(nfail), dev)
+    _native.check(rc, "rl_ba_jac_csr_f64_host")
+    return BACsr(rows, cols, vals, fail, _ba_shape(cams.shape[0], X.shape[0], p), int(nfail.value))
