@@ -46,8 +46,19 @@ namespace rl {
 
 __constant__ double c_logtab[LOGTAB_N];
 constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit for bit
-__constant__ Exp2Tab c_exp2tab[64] = RL_EXP2_TABLE_INIT;
+#ifndef BJ_EXPN
+#define BJ_EXPN 1024       // exp table size: 64 (degree-6 polynomial) or 1024 (degree 4)
+#endif
+#if BJ_EXPN == 1024
+__device__ Exp2Tab g_exp2tab[1024] = RL_EXP2_TABLE_INIT_1024;
+__constant__ ExpConsts1024 c_expk = RL_EXP_CONSTS_1024_INIT;
+#else
+__device__ Exp2Tab g_exp2tab[64] = RL_EXP2_TABLE_INIT;
 __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
+#endif
+#ifndef BJ_REVU
+#define BJ_REVU 2          // reverse-sweep trips per loop iteration (2 or 4; measured equal)
+#endif
 
 #ifndef BJ_SPEC
 #define BJ_SPEC 4          // speculative trips per warp vote (ILP of the exp chains)
@@ -60,18 +71,25 @@ constexpr int BJ_M = 8;
 constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
 constexpr int BJ_NB = 256;              // z buckets
 constexpr int BJ_WARPS = BJ_BLOCK / 32;
-constexpr int BJ_SMEM = BJ_C * (3 * 8 + 2 + 1);          // dynamic smem per block
+// dynamic smem per block: prefetch buffer + sorted z + J + dz (doubles),
+// original index (u16) and status (u8) per chunk element
+constexpr int BJ_SMEM = BJ_C * (4 * 8 + 2 + 1);
 
-// 2^(i/64) table, copied to shared memory per block (lane-varying index)
-__shared__ Exp2Tab s_exp2tab[64];
+// 2^(i/N) table, copied to shared memory per block (lane-varying index)
+__shared__ Exp2Tab s_exp2tab[BJ_EXPN];
+// (log k, log(k + nu)) for k < BJ_KP: one broadcast 16-byte shared load per
+// series trip (k is warp-uniform) instead of two indexed constant loads
+constexpr int BJ_KP = 512;
+__shared__ double2 s_logpair[BJ_KP];
 
 __device__ __forceinline__ double logi(int i) {
   return i < LOGTAB_N ? c_logtab[i] : log((double)i);
 }
 
+// (log k, log(k + nu)); TAB: k < BJ_KP (shared-memory pair table)
 template <bool TAB>
-__device__ __forceinline__ double logk(int i) {
-  return TAB ? c_logtab[i] : logi(i);
+__device__ __forceinline__ double2 logpair(int k, int nu) {
+  return TAB ? s_logpair[k] : make_double2(logi(k), logi(k + nu));
 }
 
 struct ExpR {
@@ -88,20 +106,22 @@ __device__ __forceinline__ ExpR rexp_slow(double x) {
   return r;
 }
 
-// Two exp flavours.  FAST: table exp only, and the lane records whether any
-// argument left (-708, 708) (integer test on the high word, no branch);
-// such lanes — only elements whose series terms overflow or underflow,
-// i.e. z in the hundreds — are recomputed by the CAREFUL flavour, which
-// takes libdevice's exp outside the range and reports the reference's
-// OverflowError.
+// Two exp flavours.  FAST: table exp only, no range test: every argument of
+// an element that passes the up-front safety bound (besselj_element) lies in
+// (-700, 700).  Elements that fail the bound — only z in the hundreds, z
+// below ~1e-140, or extreme nu / thr — are recomputed by the CAREFUL
+// flavour, which tests every argument, takes libdevice's exp outside
+// (-708, 708) and reports the reference's OverflowError.
 template <bool CAREFUL>
-__device__ __forceinline__ ExpR rexp(double x, bool &bad) {
+__device__ __forceinline__ ExpR rexp(double x) {
   ExpR r;
-  const bool out = (__double2hiint(x) & 0x7fffffff) >= 0x40862000;
-  if (CAREFUL && out) return rexp_slow(x);
+  if (CAREFUL && (__double2hiint(x) & 0x7fffffff) >= 0x40862000) return rexp_slow(x);
+#if BJ_EXPN == 1024
+  r.t = fexp1024_core(x, s_exp2tab, c_expk);
+#else
   r.t = fexp_core(x, s_exp2tab, c_expk);
+#endif
   r.code = 0;
-  if (!CAREFUL) bad = bad || out;
   return r;
 }
 
@@ -121,14 +141,12 @@ struct BJOut {
 // PRED: only lanes with `act` advance.
 template <bool CAREFUL, bool TAB, bool PRED, int ODD>
 __device__ __forceinline__ void fwd_trip(int k, int nu, double h2, double thr, bool &act,
-                                         double &s, double &t, double &acc, int &T, int &code,
-                                         bool &bad) {
-  const double l1 = logk<TAB>(k);
-  const double l2 = logk<TAB>(k + nu);
+                                         double &s, double &t, double &acc, int &T, int &code) {
+  const double2 L = logpair<TAB>(k, nu);
   double sn = s + h2;                                    // s *= halfz2
-  sn = sn - l1;                                          // s /= k
-  sn = sn - l2;                                          // s /= kn
-  const ExpR e = rexp<CAREFUL>(sn, bad);
+  sn = sn - L.x;                                         // s /= k
+  sn = sn - L.y;                                         // s /= kn
+  const ExpR e = rexp<CAREFUL>(sn);
   // if (k % 2 == 0, ~): even k adds, odd k subtracts
   const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
   const double an = odd ? acc - e.t : acc + e.t;
@@ -145,13 +163,17 @@ __device__ __forceinline__ void fwd_trip(int k, int nu, double h2, double thr, b
 // One reverse trip at (warp-uniform) k for lanes with k <= T (PRED) or
 // all lanes (the caller guarantees every live lane has k <= T).  With
 // !GRAD (run / uncall / objective only) the cotangents are not carried.
+// Unpredicated FAST trips do not touch `code`: they AND their postcondition
+// into `ok` (one predicated compare), which the caller turns into the
+// reference's PostconditionMismatch after the loop — the same first-failure
+// result, since no other check can fire in between.
 template <bool CAREFUL, bool TAB, bool PRED, int ODD, bool GRAD = true>
 __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, double paccg,
                                          double naccg, int chk, bool live, int T, double &acc,
                                          double &sg, double &s, double &h2g, double &t,
-                                         int &code, bool &bad) {
-  const double l2 = logk<TAB>(k + nu);
-  const double l1 = logk<TAB>(k);
+                                         int &code, bool &ok) {
+  const double2 L = logpair<TAB>(k, nu);
+  const double l2 = L.y, l1 = L.x;
   // inverse if: odd k: acc += convert(s) (sign -1); even: acc -= convert(s)
   const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
   const double an = odd ? acc + t : acc - t;
@@ -159,17 +181,21 @@ __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, d
   double sn = s + l2;                                    // s *= kn
   sn = sn + l1;                                          // s *= k
   sn = sn - h2;                                          // s /= halfz2
-  const double h2gn = GRAD ? h2g + 1.0 * sgn : 0.0;
-  const ExpR e = rexp<CAREFUL>(sn, bad);
+  const double h2gn = GRAD ? h2g + sgn : 0.0;              // h2g += 1.0 * sg (x*1.0 == x exactly)
+  const ExpR e = rexp<CAREFUL>(sn);
   if (!PRED || k <= T) {
     acc = an;
     sg = sgn;
     s = sn;
     h2g = h2gn;
     t = e.t;
-    const int c = (CAREFUL && e.code) ? e.code
-                                      : ((chk && !(e.t > thr)) ? RL_ERR_POSTCONDITION : 0);
-    if (live && !code) code = c;
+    if (!CAREFUL && !PRED) {
+      ok = ok && e.t > thr;
+    } else {
+      const int c = (CAREFUL && e.code) ? e.code
+                                        : ((chk && !(e.t > thr)) ? RL_ERR_POSTCONDITION : 0);
+      if (live && !code) code = c;
+    }
   }
 }
 
@@ -178,14 +204,23 @@ __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, d
 // is warp-uniform.  Lanes are z-sorted, so their trip counts (nearly)
 // agree: the loops run unpredicated while every live lane is active and
 // fall back to predicated trips only for the tail.
-// ktab (uniform) = last k with k + nu inside the log table; kfuel = the
-// fuel cap on trips.
+// ktab (uniform) = last k of the shared log-pair table; kfuel = the fuel
+// cap on trips; sfloor = log(thr) - 2 log(kfuel + |nu| + 1) (host).
+//
+// Safety bound of the FAST flavour (no per-exp range test).  Every exp
+// argument whose result is kept is a series log-term s_k: s_0 (tested), and
+// s_k = s_{k-1} + h2 - log k - log(k + nu) where trip k only runs after
+// exp(s_{k-1}) > thr, so s_k > log(thr) + h2 - 2 log(k + |nu|) >= h2 + sfloor;
+// from above s_k <= log I_nu(z) <= z.  The reverse sweep walks the same s
+// values back (to rounding).  So z < 700, |s_0| < 700 and h2 + sfloor > -700
+// keep every argument inside (-700, 700); other elements (and thr <= 0 or
+// NaN) are flagged `bad` and recomputed CAREFUL.  Speculative trips past a
+// lane's end are discarded, so their arguments need no bound.
 template <bool CAREFUL, bool GRAD>
 __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, double thr,
                                                  double tol, double seed, int ktab, int kfuel,
-                                                 int chk) {
+                                                 int chk, double sfloor) {
   int code = 0;
-  bool bad = false;
   // ---------------- sweep 1: forward routine ----------------
   if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
   const double logz = (valid && !code) ? log(z) : 0.0;
@@ -201,11 +236,13 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   asm volatile("" : "+d"(h2));  // keep h2 live: no per-trip rematerialisation
   double t, acc;
   {
-    const ExpR e = rexp<CAREFUL>(s, bad);                // acc += convert(s)
+    const ExpR e = rexp<CAREFUL>(s);                     // acc += convert(s)
     t = e.t;
     if (!code) code = e.code;
     acc = 0.0 + t;
   }
+  const bool bad = !CAREFUL && valid && !code &&
+                   !(z < 700.0 && s > -700.0 && s < 700.0 && h2 + sfloor > -700.0);
   int T = 0;
   bool act = valid && !code && (t > thr);                // while (s > thr, k != 0)
   const bool dead = !valid || code;                      // state irrelevant from here
@@ -221,25 +258,27 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   // term s of trip k+2 does not depend on exp() of trip k+1, so the two exp
   // chains overlap; a lane whose loop ended at k+1 keeps its trip-(k+1)
   // state and discards trip k+2.
-  if (!CAREFUL && __all_sync(FULL_MASK, act || dead)) {
+  if (!CAREFUL && __all_sync(FULL_MASK, act || dead) && __any_sync(FULL_MASK, act)) {
 #if BJ_SPEC == 4
     while (k + 4 <= kend) {                              // k even: trips odd, even, odd, even
+      const double2 L1 = s_logpair[k + 1], L2 = s_logpair[k + 2];
+      const double2 L3 = s_logpair[k + 3], L4 = s_logpair[k + 4];
       double s1 = s + h2;
-      s1 = s1 - c_logtab[k + 1];
-      s1 = s1 - c_logtab[k + 1 + nu];
+      s1 = s1 - L1.x;
+      s1 = s1 - L1.y;
       double s2 = s1 + h2;
-      s2 = s2 - c_logtab[k + 2];
-      s2 = s2 - c_logtab[k + 2 + nu];
+      s2 = s2 - L2.x;
+      s2 = s2 - L2.y;
       double s3 = s2 + h2;
-      s3 = s3 - c_logtab[k + 3];
-      s3 = s3 - c_logtab[k + 3 + nu];
+      s3 = s3 - L3.x;
+      s3 = s3 - L3.y;
       double s4 = s3 + h2;
-      s4 = s4 - c_logtab[k + 4];
-      s4 = s4 - c_logtab[k + 4 + nu];
-      const double t1 = rexp<CAREFUL>(s1, bad).t;
-      const double t2 = rexp<CAREFUL>(s2, bad).t;
-      const double t3 = rexp<CAREFUL>(s3, bad).t;
-      const double t4 = rexp<CAREFUL>(s4, bad).t;
+      s4 = s4 - L4.x;
+      s4 = s4 - L4.y;
+      const double t1 = rexp<CAREFUL>(s1).t;
+      const double t2 = rexp<CAREFUL>(s2).t;
+      const double t3 = rexp<CAREFUL>(s3).t;
+      const double t4 = rexp<CAREFUL>(s4).t;
       const double a1 = acc - t1;
       const double a2 = a1 + t2;
       const double a3 = a2 - t3;
@@ -267,14 +306,15 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     }
 #else
     while (k + 2 <= kend) {
+      const double2 L1 = s_logpair[k + 1], L2 = s_logpair[k + 2];
       double s1 = s + h2;                                // trip k+1 (odd)
-      s1 = s1 - c_logtab[k + 1];
-      s1 = s1 - c_logtab[k + 1 + nu];
+      s1 = s1 - L1.x;
+      s1 = s1 - L1.y;
       double s2 = s1 + h2;                               // trip k+2 (even)
-      s2 = s2 - c_logtab[k + 2];
-      s2 = s2 - c_logtab[k + 2 + nu];
-      const double t1 = rexp<CAREFUL>(s1, bad).t;
-      const double t2 = rexp<CAREFUL>(s2, bad).t;
+      s2 = s2 - L2.x;
+      s2 = s2 - L2.y;
+      const double t1 = rexp<CAREFUL>(s1).t;
+      const double t2 = rexp<CAREFUL>(s2).t;
       const double a1 = acc - t1;                        // odd k subtracts
       const double a2 = a1 + t2;                         // even k adds
       const bool act1 = t1 > thr, act2 = t2 > thr;
@@ -312,11 +352,11 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   // tail: predicated
   while (k < kend && __any_sync(FULL_MASK, act)) {
     k++;
-    fwd_trip<CAREFUL, true, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code, bad);
+    fwd_trip<CAREFUL, true, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code);
   }
   while (k < kfuel && __any_sync(FULL_MASK, act)) {      // beyond the table (huge nu / T)
     k++;
-    fwd_trip<CAREFUL, false, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code, bad);
+    fwd_trip<CAREFUL, false, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code);
   }
   if (act) code = RL_ERR_FUEL;                           // still running at the fuel cap
   BJOut o;
@@ -328,31 +368,45 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   const double accg = 0.0 + (1.0 * seed) * 1.0;          // out! -= acc: acc.g += out.g
   const double paccg = 1.0 * accg, naccg = -1.0 * accg;
   double sg = 0.0, h2g = 0.0;
+  bool ok = true;                                        // postconditions of unpredicated trips
   if (fwd_ok && chk && t > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
   const int Tmax = __reduce_max_sync(FULL_MASK, fwd_ok ? T : 0);
   const unsigned Tmin = __reduce_min_sync(FULL_MASK, fwd_ok ? (unsigned)T : 0x7fffffffu);
   int kr = Tmax;
   for (; kr > ktab; kr--)                                // beyond the table
     rev_trip<CAREFUL, false, true, -1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
-                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
+                                       fwd_ok ? T : 0, acc, sg, s, h2g, t, code, ok);
   for (; kr > (int)Tmin; kr--)                           // tail: predicated
     rev_trip<CAREFUL, true, true, -1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok,
-                                      fwd_ok ? T : 0, acc, sg, s, h2g, t, code, bad);
+                                      fwd_ok ? T : 0, acc, sg, s, h2g, t, code, ok);
   // the reverse loop is counted (no votes): pairs already overlap the exp chains
   if (kr >= 1 && !(kr & 1)) {                            // align: pairs start at odd k
     rev_trip<CAREFUL, true, false, 0, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
-                                      h2g, t, code, bad);
+                                      h2g, t, code, ok);
     kr--;
   }
+#if BJ_REVU == 4
+  for (; kr >= 4; kr -= 4) {                             // main, 4 trips: the exp chains overlap
+    rev_trip<CAREFUL, true, false, 1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
+                                      h2g, t, code, ok);
+    rev_trip<CAREFUL, true, false, 0, GRAD>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, ok);
+    rev_trip<CAREFUL, true, false, 1, GRAD>(kr - 2, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, ok);
+    rev_trip<CAREFUL, true, false, 0, GRAD>(kr - 3, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
+                                      s, h2g, t, code, ok);
+  }
+#endif
   for (; kr >= 2; kr -= 2) {                             // main: every live lane active
     rev_trip<CAREFUL, true, false, 1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
-                                      h2g, t, code, bad);
+                                      h2g, t, code, ok);
     rev_trip<CAREFUL, true, false, 0, GRAD>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg,
-                                      s, h2g, t, code, bad);
+                                      s, h2g, t, code, ok);
   }
   if (kr == 1)
     rev_trip<CAREFUL, true, false, 1, GRAD>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
-                                      h2g, t, code, bad);
+                                      h2g, t, code, ok);
+  if (!CAREFUL && chk && fwd_ok && !ok && !code) code = RL_ERR_POSTCONDITION;
   double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
@@ -395,26 +449,47 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, const double *__restrict__ out_in, double sign,
     double *__restrict__ Jout, double *__restrict__ dzout, uint8_t *__restrict__ fail,
-    unsigned long long *counters) {
-  const int ktab = LOGTAB_N - 1 - (nu > 0 ? nu : 0);
+    unsigned long long *counters, double sfloor) {
+  const int ktab = BJ_KP - 1;
   const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
   __shared__ int s_wsum[BJ_WARPS];
   extern __shared__ __align__(16) double bj_dyn[];     // BJ_SMEM bytes
-  double *s_z = bj_dyn;
+  double *s_zin = bj_dyn;                              // cp.async target: next chunk's z
+  double *s_z = s_zin + BJ_C;
   double *s_J = s_z + BJ_C;
   double *s_dz = s_J + BJ_C;
   uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dz + BJ_C);
   uint8_t *s_fail = reinterpret_cast<uint8_t *>(s_idx + BJ_C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 64) s_exp2tab[tid] = c_exp2tab[tid];
+  for (int i = tid; i < BJ_EXPN; i += BJ_BLOCK) s_exp2tab[i] = g_exp2tab[i];
+  for (int k = tid; k < BJ_KP; k += BJ_BLOCK)
+    s_logpair[k] = make_double2(logi(k), k + nu >= 0 ? logi(k + nu) : __longlong_as_double(0x7ff8000000000000ULL));
   unsigned long long trips_sum = 0, nfail = 0;
+  // z chunks are prefetched into shared memory with cp.async one chunk
+  // ahead, so the DRAM latency of the next chunk hides behind this one's
+  // series work
+  const unsigned zin_s = (unsigned)__cvta_generic_to_shared(s_zin);
+  auto prefetch = [&](long long b) {
+    if (b >= n) return;
+    const int c = (int)(n - b < BJ_C ? n - b : BJ_C);
+#pragma unroll
+    for (int m = 0; m < BJ_M; m++) {
+      const int e = m * BJ_BLOCK + tid;
+      if (e < c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(zin_s + 8u * e),
+                     "l"(zin + b + e) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch((long long)blockIdx.x * BJ_C);
 
   for (long long base = (long long)blockIdx.x * BJ_C; base < n;
        base += (long long)gridDim.x * BJ_C) {
     const int cnt = (int)(n - base < BJ_C ? n - base : BJ_C);
     // 1. bucket histogram (rank within bucket from the atomic)
     for (int b = tid; b < BJ_NB; b += BJ_BLOCK) s_hist[b] = 0;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     double zr[BJ_M];
     int key[BJ_M], rnk[BJ_M];
@@ -422,12 +497,13 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     for (int m = 0; m < BJ_M; m++) {
       const int e = m * BJ_BLOCK + tid;
       if (e < cnt) {
-        zr[m] = __ldcs(zin + base + e);
+        zr[m] = s_zin[e];                              // each thread reads what it copied
         key[m] = zbucket(zr[m]);
         rnk[m] = atomicAdd(&s_hist[key[m]], 1);
       }
     }
     __syncthreads();
+    prefetch(base + (long long)gridDim.x * BJ_C);
     // 2. exclusive scan of the 256 buckets (one per thread)
     {
       const int v = s_hist[tid];
@@ -464,10 +540,11 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {
         const double z = valid ? s_z[pos] : 1.0;
-        BJOut o = besselj_element<false, GRAD>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk);
+        BJOut o = besselj_element<false, GRAD>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk,
+                                               sfloor);
         if (__any_sync(FULL_MASK, o.bad)) {              // |exp arg| >= 708 somewhere
           const BJOut c =
-              besselj_element<true, GRAD>(z, o.bad, nu, thr, tol, seed, ktab, kfuel, chk);
+              besselj_element<true, GRAD>(z, o.bad, nu, thr, tol, seed, ktab, kfuel, chk, sfloor);
           if (o.bad) o = c;
         }
         if (valid) {
@@ -530,9 +607,12 @@ static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, 
   const long long want = (n + BJ_C - 1) / BJ_C;
   const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   const int grid = (int)(want < cap ? want : cap);
+  // FAST-flavour safety bound (besselj_element): log(thr) - 2 log(kfuel + |nu| + 1)
+  const double kfuel = (double)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
+  const double sfloor = log(thr) - 2.0 * log(kfuel + fabs((double)nu) + 1.0);
   k_besselj<GRAD><<<grid, BJ_BLOCK, BJ_SMEM, st>>>(nu, z, n, thr, tol, seed, max_trips,
                                                    invcheck ? 1 : 0, out_in, sign, J, dJdz, fail,
-                                                   counters);
+                                                   counters, sfloor);
   return cuda_status(cudaGetLastError(), "k_besselj launch");
 }
 

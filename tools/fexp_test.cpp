@@ -1,6 +1,6 @@
 // Host check of csrc/fexp.cuh against the C library exp (glibc), which is
 // what CPython's math.exp — and so the reference — uses.
-// usage: fexp_test N lo hi seed  -> prints "n equal max_ulp"
+// usage: fexp_test N lo hi seed [tablesize 64|1024] -> prints "n equal max_ulp"
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -11,17 +11,21 @@
 
 static const rl::Exp2Tab TAB[64] = RL_EXP2_TABLE_INIT;
 static const rl::ExpConsts KC = RL_EXP_CONSTS_INIT;
+static const rl::Exp2Tab TAB1024[1024] = RL_EXP2_TABLE_INIT_1024;
+static const rl::ExpConsts1024 KC1024 = RL_EXP_CONSTS_1024_INIT;
 
 int main(int argc, char **argv) {
   long n = atol(argv[1]);
   double lo = atof(argv[2]), hi = atof(argv[3]);
   std::mt19937_64 g(atol(argv[4]));
+  const bool big = argc > 5 && atoi(argv[5]) == 1024;
   std::uniform_real_distribution<double> U(lo, hi);  // |x| < 708
   long eq = 0;
   double maxulp = 0;
   for (long i = 0; i < n; i++) {
     double x = U(g);
-    double a = rl::fexp_core(x, TAB, KC), b = exp(x);
+    double a = big ? rl::fexp1024_core(x, TAB1024, KC1024) : rl::fexp_core(x, TAB, KC);
+    double b = exp(x);
     if (memcmp(&a, &b, 8) == 0) {
       eq++;
     } else {
