@@ -117,7 +117,18 @@ __device__ __forceinline__ ExpR rexp(double x) {
   ExpR r;
   if (CAREFUL && (__double2hiint(x) & 0x7fffffff) >= 0x40862000) return rexp_slow(x);
 #if BJ_EXPN == 1024
-  r.t = fexp1024_core(x, s_exp2tab, c_expk);
+  // entry address = base + (i << 4): one IMAD from the masked index (the
+  // compiler's own form is shift, mask, add)
+  r.t = fexp1024(x,
+                 [](int i) {
+                   double2 v;
+                   asm("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %2, 16, %3;\n\t"
+                       "ld.shared.v2.f64 {%0, %1}, [a];\n\t}"
+                       : "=d"(v.x), "=d"(v.y)
+                       : "r"(i), "r"((unsigned)__cvta_generic_to_shared(s_exp2tab)));
+                   return v;
+                 },
+                 c_expk);
 #else
   r.t = fexp_core(x, s_exp2tab, c_expk);
 #endif

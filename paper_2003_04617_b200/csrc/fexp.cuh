@@ -23,8 +23,13 @@
 
 #ifdef __CUDACC__
 #define RL_HD __host__ __device__ __forceinline__
+#define RL_HDM __host__ __device__ __forceinline__
 #else
 #define RL_HD static inline
+#define RL_HDM inline
+struct double2 {
+  double x, y;
+};
 #endif
 
 namespace rl {
@@ -167,7 +172,11 @@ struct ExpConsts1024 {
   {RL_EXP_INV_LN2_1024, -RL_EXP_LN2_1024_HI, -RL_EXP_LN2_1024_LO, rl::EXP_SHIFT, 1.0 / 24.0, \
    1.0 / 6.0, 0.5}
 
-RL_HD double fexp1024_core(double x, const Exp2Tab *tab, const ExpConsts1024 &K) {
+// `tab(i)` returns entry i as a double2 {hi, lo}: device code passes an
+// accessor of a static __shared__ array, so the load is one LDS with an
+// immediate base (a generic pointer would cost a runtime base add).
+template <class TabFn>
+RL_HD double fexp1024(double x, TabFn tab, const ExpConsts1024 &K) {
   const double t = fma(x, K.inv_ln2_n, K.shift);
   int64_t tb;
   memcpy(&tb, &t, 8);
@@ -179,16 +188,15 @@ RL_HD double fexp1024_core(double x, const Exp2Tab *tab, const ExpConsts1024 &K)
   q = fma(q, r, K.c2);
   const double r2 = r * r;
   const double p = fma(q, r2, r);                    // e^r - 1
-#if defined(__CUDA_ARCH__)
-  const double2 e2 = reinterpret_cast<const double2 *>(tab)[j & 1023];
-  const Exp2Tab e{e2.x, e2.y};
-#else
-  const Exp2Tab e = tab[j & 1023];
-#endif
-  const double res = e.hi + fma(e.hi, p, e.lo);
+  const auto e = tab(j & 1023);
+  const double res = e.x + fma(e.x, p, e.y);
   // scale by 2^m, m = j >> 10: integer add into the exponent field
 #if defined(__CUDA_ARCH__)
-  return __hiloint2double(__double2hiint(res) + ((j >> 10) << 20), __double2loint(res));
+  int hi;
+  asm("{\n\t.reg .s32 m;\n\tshr.s32 m, %1, 10;\n\tmad.lo.s32 %0, m, 1048576, %2;\n\t}"
+      : "=r"(hi)
+      : "r"(j), "r"(__double2hiint(res)));
+  return __hiloint2double(hi, __double2loint(res));
 #else
   int64_t rb;
   memcpy(&rb, &res, 8);
@@ -197,6 +205,20 @@ RL_HD double fexp1024_core(double x, const Exp2Tab *tab, const ExpConsts1024 &K)
   memcpy(&out, &rb, 8);
   return out;
 #endif
+}
+
+struct Exp2TabFn {
+  const Exp2Tab *tab;
+  RL_HDM double2 operator()(int i) const {
+    double2 v;
+    v.x = tab[i].hi;
+    v.y = tab[i].lo;
+    return v;
+  }
+};
+
+RL_HD double fexp1024_core(double x, const Exp2Tab *tab, const ExpConsts1024 &K) {
+  return fexp1024(x, Exp2TabFn{tab}, K);
 }
 
 }  // namespace rl
