@@ -52,6 +52,9 @@ constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit f
 #if BJ_EXPN == 1024
 __device__ Exp2Tab g_exp2tab[1024] = RL_EXP2_TABLE_INIT_1024;
 __constant__ ExpConsts1024 c_expk = RL_EXP_CONSTS_1024_INIT;
+#elif BJ_EXPN == 256
+__device__ Exp2Tab g_exp2tab[256] = RL_EXP2_TABLE_INIT_256;
+__constant__ ExpConsts256 c_expk = RL_EXP_CONSTS_256_INIT;
 #else
 __device__ Exp2Tab g_exp2tab[64] = RL_EXP2_TABLE_INIT;
 __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
@@ -66,8 +69,10 @@ __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 #ifndef BJ_MINB
 #define BJ_MINB 2          // __launch_bounds__ min blocks per SM (register budget)
 #endif
+#ifndef BJ_M
+#define BJ_M 8             // chunk = BJ_M elements per thread (z-sorted per chunk)
+#endif
 constexpr int BJ_BLOCK = 256;
-constexpr int BJ_M = 8;
 constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
 constexpr int BJ_NB = 256;              // z buckets
 constexpr int BJ_WARPS = BJ_BLOCK / 32;
@@ -75,8 +80,16 @@ constexpr int BJ_WARPS = BJ_BLOCK / 32;
 // original index (u16) and status (u8) per chunk element
 constexpr int BJ_SMEM = BJ_C * (4 * 8 + 2 + 1);
 
-// 2^(i/N) table, copied to shared memory per block (lane-varying index)
-__shared__ Exp2Tab s_exp2tab[BJ_EXPN];
+// 2^(i/N) table, copied to shared memory per block (lane-varying index).
+// The 256-entry form is replicated 8x with entry (i, c) at 16-byte slot
+// 8 i + c and lane l reading copy c = l & 7: the 8 lanes of a quarter-warp
+// then always hit 8 different bank groups (conflict-free 16-byte loads).
+#if BJ_EXPN == 256
+constexpr int BJ_EXPREP = 8;
+#else
+constexpr int BJ_EXPREP = 1;
+#endif
+__shared__ __align__(16) Exp2Tab s_exp2tab[BJ_EXPN * BJ_EXPREP];   // 16-byte loads
 // (log k, log(k + nu)) for k < BJ_KP: one broadcast 16-byte shared load per
 // series trip (k is warp-uniform) instead of two indexed constant loads
 constexpr int BJ_KP = 512;
@@ -115,6 +128,10 @@ __device__ __forceinline__ ExpR rexp_slow(double x) {
 template <bool CAREFUL>
 __device__ __forceinline__ ExpR rexp(double x) {
   ExpR r;
+#if BJ_EXPN == 256
+  const unsigned lanebase =
+      (unsigned)__cvta_generic_to_shared(s_exp2tab) + ((threadIdx.x & 7u) << 4);
+#endif
   if (CAREFUL && (__double2hiint(x) & 0x7fffffff) >= 0x40862000) return rexp_slow(x);
 #if BJ_EXPN == 1024
   // entry address = base + (i << 4): one IMAD from the masked index (the
@@ -129,6 +146,17 @@ __device__ __forceinline__ ExpR rexp(double x) {
                    return v;
                  },
                  c_expk);
+#elif BJ_EXPN == 256
+  r.t = fexp256(x,
+                [lanebase](int i) {
+                  double2 v;
+                  asm("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %2, 128, %3;\n\t"
+                      "ld.shared.v2.f64 {%0, %1}, [a];\n\t}"
+                      : "=d"(v.x), "=d"(v.y)
+                      : "r"(i), "r"(lanebase));
+                  return v;
+                },
+                c_expk);
 #else
   r.t = fexp_core(x, s_exp2tab, c_expk);
 #endif
@@ -465,6 +493,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
   const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
   __shared__ int s_wsum[BJ_WARPS];
+  __shared__ int s_round;
   extern __shared__ __align__(16) double bj_dyn[];     // BJ_SMEM bytes
   double *s_zin = bj_dyn;                              // cp.async target: next chunk's z
   double *s_z = s_zin + BJ_C;
@@ -473,7 +502,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
   uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dz + BJ_C);
   uint8_t *s_fail = reinterpret_cast<uint8_t *>(s_idx + BJ_C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < BJ_EXPN; i += BJ_BLOCK) s_exp2tab[i] = g_exp2tab[i];
+  for (int i = tid; i < BJ_EXPN * BJ_EXPREP; i += BJ_BLOCK) s_exp2tab[i] = g_exp2tab[i / BJ_EXPREP];
   for (int k = tid; k < BJ_KP; k += BJ_BLOCK)
     s_logpair[k] = make_double2(logi(k), k + nu >= 0 ? logi(k + nu) : __longlong_as_double(0x7ff8000000000000ULL));
   unsigned long long trips_sum = 0, nfail = 0;
@@ -500,6 +529,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     const int cnt = (int)(n - base < BJ_C ? n - base : BJ_C);
     // 1. bucket histogram (rank within bucket from the atomic)
     for (int b = tid; b < BJ_NB; b += BJ_BLOCK) s_hist[b] = 0;
+    if (tid == 0) s_round = 0;
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     double zr[BJ_M];
@@ -544,9 +574,16 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
       }
     }
     __syncthreads();
-    // 4. rounds of 32 z-neighbours; warp w takes rounds w, w + 8, ...
+    // 4. rounds of 32 z-neighbours, handed out dynamically from the largest z
+    //    down (longest first), so the block's warps reach the barrier together
+    const int nrounds = (cnt + 31) >> 5;
 #pragma unroll 1
-    for (int r = warp; r < BJ_C / 32; r += BJ_WARPS) {
+    for (;;) {
+      int got = 0;
+      if (lane == 0) got = atomicAdd(&s_round, 1);
+      got = __shfl_sync(FULL_MASK, got, 0);
+      if (got >= nrounds) break;
+      const int r = nrounds - 1 - got;
       const int pos = r * 32 + lane;
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {

@@ -20,6 +20,7 @@
 #include <string.h>
 
 #include "exp2tab_1024.inc"
+#include "exp2tab_256.inc"
 
 #ifdef __CUDACC__
 #define RL_HD __host__ __device__ __forceinline__
@@ -34,7 +35,7 @@ struct double2 {
 
 namespace rl {
 
-struct Exp2Tab {
+struct alignas(16) Exp2Tab {
   double hi, lo;
 };
 
@@ -207,6 +208,48 @@ RL_HD double fexp1024(double x, TabFn tab, const ExpConsts1024 &K) {
 #endif
 }
 
+// 256-entry variant: |r| <= ln2/512, degree-5 polynomial (truncation 1e-20
+// relative), 11 FP64 instructions.  The kernel stores the table replicated
+// per lane-in-quarter-warp so that its 16-byte loads are bank-conflict free.
+struct ExpConsts256 {
+  double inv_ln2_n, ln2_n_hi_neg, ln2_n_lo_neg, shift, c5, c4, c3, c2;
+};
+#define RL_EXP_CONSTS_256_INIT \
+  {RL_EXP_INV_LN2_256, -RL_EXP_LN2_256_HI, -RL_EXP_LN2_256_LO, rl::EXP_SHIFT, 1.0 / 120.0, \
+   1.0 / 24.0, 1.0 / 6.0, 0.5}
+
+template <class TabFn>
+RL_HD double fexp256(double x, TabFn tab, const ExpConsts256 &K) {
+  const double t = fma(x, K.inv_ln2_n, K.shift);
+  int64_t tb;
+  memcpy(&tb, &t, 8);
+  const int j = (int)(int32_t)(uint32_t)tb;          // round(x * 256 / ln2)
+  const double jd = t - K.shift;
+  double r = fma(jd, K.ln2_n_hi_neg, x);
+  r = fma(jd, K.ln2_n_lo_neg, r);
+  double q = fma(K.c5, r, K.c4);
+  q = fma(q, r, K.c3);
+  q = fma(q, r, K.c2);
+  const double r2 = r * r;
+  const double p = fma(q, r2, r);                    // e^r - 1
+  const auto e = tab(j & 255);
+  const double res = e.x + fma(e.x, p, e.y);
+#if defined(__CUDA_ARCH__)
+  int hi;
+  asm("{\n\t.reg .s32 m;\n\tshr.s32 m, %1, 8;\n\tmad.lo.s32 %0, m, 1048576, %2;\n\t}"
+      : "=r"(hi)
+      : "r"(j), "r"(__double2hiint(res)));
+  return __hiloint2double(hi, __double2loint(res));
+#else
+  int64_t rb;
+  memcpy(&rb, &res, 8);
+  rb += (int64_t)(j >> 8) * ((int64_t)1 << 52);
+  double out;
+  memcpy(&out, &rb, 8);
+  return out;
+#endif
+}
+
 struct Exp2TabFn {
   const Exp2Tab *tab;
   RL_HDM double2 operator()(int i) const {
@@ -219,6 +262,10 @@ struct Exp2TabFn {
 
 RL_HD double fexp1024_core(double x, const Exp2Tab *tab, const ExpConsts1024 &K) {
   return fexp1024(x, Exp2TabFn{tab}, K);
+}
+
+RL_HD double fexp256_core(double x, const Exp2Tab *tab, const ExpConsts256 &K) {
+  return fexp256(x, Exp2TabFn{tab}, K);
 }
 
 }  // namespace rl

@@ -11,7 +11,7 @@ def test_fexp_within_one_ulp_and_mostly_bit_identical(tmp_path):
     exe = str(tmp_path / "fexp_test")
     subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-o", exe,
                            os.path.join(REPO, "tools", "fexp_test.cpp")])
-    for tab in ("64", "1024"):                      # fexp_core / fexp1024_core (the kernel's)
+    for tab in ("64", "256", "1024"):                      # fexp_core / fexp1024_core (the kernel's)
         for lo, hi, seed in ((-40.0, 10.0, 1), (-707.0, 707.0, 2), (-1e-3, 1e-3, 3)):
             n, eq, maxulp = subprocess.check_output(
                 [exe, "2000000", str(lo), str(hi), str(seed), tab], text=True).split()
