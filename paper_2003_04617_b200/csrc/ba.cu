@@ -51,10 +51,15 @@ __device__ __forceinline__ G2 neg(G2 g) { return G2{-g.a, -g.b}; }
 __device__ __forceinline__ G2 zero2() { return G2{0.0, 0.0}; }
 
 #ifndef BA_MINB
-#define BA_MINB 4          // __launch_bounds__ min blocks per SM (register budget)
+#define BA_MINB 10         // blocks per SM: up to 204 registers, no spills
 #endif
-constexpr int BA_BLOCK = 128;
+#ifndef BA_BLOCK_SZ
+#define BA_BLOCK_SZ 32     // one warp per block (measured best: tools/build_variants.sh sweep)
+#endif
+constexpr int BA_BLOCK = BA_BLOCK_SZ;
 constexpr int BA_ROW = 31;
+constexpr int BA_STAGE = 17;       // staged inputs per observation: cam 11, X 3, w, feat 2
+constexpr int BA_SMEM = (BA_ROW + BA_STAGE) * BA_BLOCK * 8;   // dynamic smem per block
 
 // GRAD: the Jacobian (sweeps 1 + 4 with two cotangent lanes).  !GRAD: run
 // of ba_proj / ba_weight on zero outputs — the residuals [e1, e2, 1 - w^2]
@@ -79,33 +84,76 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     const double *__restrict__ feats, const int2 *__restrict__ obs, double tol, int chk,
     double *__restrict__ err_out, double *__restrict__ J_out, double *__restrict__ Jf_out,
     uint8_t *__restrict__ fail, unsigned long long *counters, BaCsr csr) {
-  __shared__ __align__(16) double tile[BA_BLOCK * BA_ROW];
+  // dynamic smem: the J row tile (31 doubles per observation), then the
+  // per-thread input stage (17 doubles per observation, [17][BA_BLOCK])
+  extern __shared__ __align__(16) double ba_dyn[];
+  double *tile = ba_dyn;
+  double *stage = ba_dyn + BA_BLOCK * BA_ROW;
   __shared__ int2 otile[CSR ? BA_BLOCK : 1];
   unsigned long long nfail = 0;
-  for (long long blk0 = (long long)blockIdx.x * BA_BLOCK; blk0 < n_obs;
-       blk0 += (long long)gridDim.x * BA_BLOCK) {
-    const long long i = blk0 + threadIdx.x;
+  const long long stride = (long long)gridDim.x * BA_BLOCK;
+  const int tid = threadIdx.x;
+  // Software pipeline: each thread gathers the camera row, point, weight and
+  // feature of its NEXT observation (one block-stride ahead) into its own
+  // stage slots with cp.async while it computes the current one, and holds
+  // the observation index two strides ahead in a register.  The stage is
+  // private per thread (no block barrier); the next gather is issued only
+  // after every staged value of the current observation has been consumed.
+  const unsigned st_s = (unsigned)__cvta_generic_to_shared(stage) + 8u * tid;
+  auto cp8 = [&](int slot, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(st_s + 8u * BA_BLOCK * slot),
+                 "l"(src) : "memory");
+  };
+  auto gather = [&](long long i, int2 o) {
+    if (i < n_obs) {
+      if (o.x >= 0 && o.x < n_cams && o.y >= 0 && o.y < n_pts) {
+        const double *cp = cams + 11 * (long long)o.x;
+#pragma unroll
+        for (int j = 0; j < 11; j++) cp8(j, cp + j);
+        const double *xp = Xs + 3 * (long long)o.y;
+        cp8(11, xp);
+        cp8(12, xp + 1);
+        cp8(13, xp + 2);
+      }
+      cp8(14, ws + i);
+      cp8(15, feats + 2 * i);
+      cp8(16, feats + 2 * i + 1);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto sget = [&](int slot) { return stage[BA_BLOCK * slot + tid]; };
+  const long long blk_first = (long long)blockIdx.x * BA_BLOCK;
+  int2 o_cur = blk_first + tid < n_obs ? __ldg(obs + blk_first + tid) : make_int2(0, 0);
+  gather(blk_first + tid, o_cur);
+  int2 o_nxt = blk_first + stride + tid < n_obs ? __ldg(obs + blk_first + stride + tid)
+                                                : make_int2(0, 0);
+  for (long long blk0 = blk_first; blk0 < n_obs; blk0 += stride) {
+    const long long i = blk0 + tid;
     const bool valid = i < n_obs;
     double row[BA_ROW];
     int code_final = 0;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const int2 o = o_cur;
+    const long long i_next = i + stride;
+    auto prefetch_next = [&]() {
+      gather(i_next, o_nxt);
+      o_cur = o_nxt;
+      o_nxt = i_next + stride < n_obs ? __ldg(obs + i_next + stride) : make_int2(0, 0);
+    };
+    const bool in_range = o.x >= 0 && o.x < n_cams && o.y >= 0 && o.y < n_pts;
     if (valid) {
-      const int2 o = __ldg(obs + i);
-      if (CSR) otile[threadIdx.x] = o;
-      if (o.x < 0 || o.x >= n_cams || o.y < 0 || o.y >= n_pts) {
+      if (!in_range) {
         code_final = RL_ERR_INDEX;
-        if (CSR) otile[threadIdx.x] = make_int2(-1, -1);
+        prefetch_next();
 #pragma unroll
         for (int j = 0; j < BA_ROW; j++) row[j] = __longlong_as_double(0x7ff8000000000000ULL);
       } else {
-        const double *cp = cams + 11 * (long long)o.x;
         double c[11];
 #pragma unroll
-        for (int j = 0; j < 11; j++) c[j] = __ldg(cp + j);
-        const double *xp = Xs + 3 * (long long)o.y;
-        const double X0 = __ldg(xp), X1 = __ldg(xp + 1), X2 = __ldg(xp + 2);
-        const double w = __ldg(ws + i);
-        const double2 f = __ldg(reinterpret_cast<const double2 *>(feats) + i);
-        const double f1 = f.x, f2 = f.y;
+        for (int j = 0; j < 11; j++) c[j] = sget(j);
+        const double X0 = sget(11), X1 = sget(12), X2 = sget(13);
+        const double w = sget(14);
+        const double f1 = sget(15), f2 = sget(16);
         int code1 = 0, code_rod = 0, code4 = 0;
 
         // ------------------------- sweep 1 -------------------------
@@ -185,6 +233,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
         d2 = d2 - f2;
         const double e1 = 0.0 + w * d1;
         const double e2 = 0.0 + w * d2;
+        prefetch_next();                  // every staged input has been consumed
 
         // ---------------- sweep 3's middle: e2! -= w*d2; e1! -= w*d1 ----------------
         const G2 ge1{1.0, 0.0}, ge2{0.0, 1.0};
@@ -428,13 +477,21 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
       }
       fail[i] = (uint8_t)code_final;
       nfail += code_final != 0;
+    } else {
+      prefetch_next();
     }
     if (!GRAD) continue;
-    // stage the block's rows and write them out with coalesced 16-byte stores
+    // stage the block's rows and write them out: one TMA bulk store of the
+    // whole tile (the block's rows are one contiguous run of J), issued by
+    // one thread and overlapping the next observation's compute; otherwise
+    // (CSR, a partial block, misaligned J) coalesced 16-byte stores
+    if (!CSR && tid == 0)                  // previous bulk store has read the tile
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncthreads();
     if (valid) {
 #pragma unroll
       for (int j = 0; j < BA_ROW; j++) tile[threadIdx.x * BA_ROW + j] = row[j];
+      if (CSR) otile[threadIdx.x] = in_range ? o : make_int2(-1, -1);
     }
     __syncthreads();
     const long long rows = n_obs - blk0 < BA_BLOCK ? n_obs - blk0 : BA_BLOCK;
@@ -474,7 +531,14 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     }
     const int nd = (int)rows * BA_ROW;
     double *dst = J_out + blk0 * BA_ROW;
-    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    if (rows == BA_BLOCK && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"((unsigned)__cvta_generic_to_shared(tile)), "r"(nd * 8) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
       const int nv = nd >> 1;
       double2 *d2p = reinterpret_cast<double2 *>(dst);
       const double2 *s2p = reinterpret_cast<const double2 *>(tile);
@@ -484,6 +548,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
       for (int k = threadIdx.x; k < nd; k += BA_BLOCK) dst[k] = tile[k];
     }
   }
+  if (!CSR && GRAD && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   block_add_counters<BA_BLOCK>(0, nfail, counters);
 }
 
@@ -502,13 +567,16 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
   auto kern = err ? (Jfeat ? k_ba_jac<true, true> : k_ba_jac<true, false>)
                   : (Jfeat ? k_ba_jac<false, true> : k_ba_jac<false, false>);
   int bps = 0;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
+                   "smem attr");
+  if (rc) return rc;
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+  kern<<<grid, BA_BLOCK, BA_SMEM, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
                                   J, Jfeat, fail, counters, BaCsr{});
   return cuda_status(cudaGetLastError(), "k_ba_jac launch");
@@ -528,13 +596,16 @@ int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doub
   if (n_obs == 0) return RL_OK;
   auto kern = k_ba_jac<true, false, false>;
   int bps = 0;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
+                   "smem attr");
+  if (rc) return rc;
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+  kern<<<grid, BA_BLOCK, BA_SMEM, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
                                   nullptr, nullptr, fail, counters, BaCsr{});
   return cuda_status(cudaGetLastError(), "k_ba_jac (residuals) launch");
@@ -567,14 +638,17 @@ int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offs
   }
   auto kern = err ? k_ba_jac<true, false, true, true> : k_ba_jac<false, false, true, true>;
   int bps = 0;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, 0),
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
+                   "smem attr");
+  if (rc) return rc;
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
   BaCsr csr{rows, cols, vals, obs_offset, n_obs_total, 11 * n_cams, 11 * n_cams + 3 * n_pts};
-  kern<<<grid, BA_BLOCK, 0, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+  kern<<<grid, BA_BLOCK, BA_SMEM, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
                                   nullptr, nullptr, fail, counters, csr);
   return cuda_status(cudaGetLastError(), "k_ba_jac (csr) launch");
