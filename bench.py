@@ -102,18 +102,44 @@ class Dist:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons every 200 ms while running."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    (pynvml, every ~2 ms in a thread, so even a few-ms region gets samples),
+    with nvidia-smi -lms 200 as the fallback when NVML is unavailable."""
 
     QUERY = ("index,uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, uuid=None):
         self.uuid = uuid
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.samples = []
+        self.stop_evt = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        if self.uuid:
+            try:
+                return pynvml, pynvml.nvmlDeviceGetHandleByUUID(self.uuid)
+            except pynvml.NVMLError:
+                pass
+        idx = int((os.environ.get("CUDA_VISIBLE_DEVICES") or "0").split(",")[0] or 0) \
+            if (os.environ.get("CUDA_VISIBLE_DEVICES") or "0").split(",")[0].isdigit() else 0
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
 
     def start(self):
+        try:
+            self.nv = self._nvml_handle()
+        except Exception:  # noqa: BLE001 - NVML missing: fall back to nvidia-smi
+            self.nv = None
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         cmd = ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
                "-lms", "200"]
         if self.uuid:
@@ -126,12 +152,38 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        time.sleep(0.25)                   # nvidia-smi needs a moment for its first line
+
+    def _poll(self):
+        nv, h = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop_evt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, smax, {k for k, b in bits.items() if r & b}))
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_evt.set()
+            self.thread.join(timeout=2)
+            if not self.samples:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            reasons = set().union(*(x[2] for x in self.samples))
+            return {"sm_mhz": statistics.median(x[0] for x in self.samples),
+                    "sm_max_mhz": max(x[1] for x in self.samples), "reasons": sorted(reasons),
+                    "samples": len(self.samples), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -141,7 +193,6 @@ class ClockSampler:
             self.proc.kill()
         self.thread.join(timeout=2)
         sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 10:
@@ -151,13 +202,13 @@ class ClockSampler:
                 smax.append(float(parts[3]))
             except ValueError:
                 continue
-            for nm, flag in zip(names, parts[6:10]):
+            for nm, flag in zip(self.NAMES, parts[6:10]):
                 if flag.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 def time_device(fn, steps, flush=None):
@@ -257,7 +308,6 @@ def run_bessel_ours(args, D):
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
-    time.sleep(0.25)
     D.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -292,7 +342,7 @@ def run_bessel_ours(args, D):
                 "peak_source": "in-run DFMA microkernel (tools/fp64probe.cu); no FP64 "
                                "figure in MEASURED_PEAKS.json or B200_PROFILING.md",
                 "flops_per_launch": fl, "weights": w.get("source", "profiles/fp64_weights.json")}
-        tr = load_traffic("k_besselj_grad")
+        tr = load_traffic("k_besselj<1>")
         if tr:
             roof["traffic"] = tr
     # objective only ("-O", the paper's objective timing): run of besselj
@@ -354,7 +404,7 @@ def bessel_e2e(torch, z, args, D, n_total):
             "path": "rl_besselj_grad_f64_host (pinned host buffers, 3-stream pipeline)"}
 
 
-def bessel_cpu(target_s=10.0, n_max=1 << 22):
+def bessel_cpu(target_s=2.0, n_max=1 << 24):
     """The oracle port over all host threads on a bounded sample."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as O
@@ -383,7 +433,8 @@ def load_traffic(kernel):
         with open(p) as fh:
             d = json.load(fh)
         for k, v in d.items():
-            if not k.startswith("_") and (k == kernel or k.startswith(kernel + "<")):
+            if not k.startswith("_") and (k == kernel or k.startswith(kernel + "<")
+                                          or k.replace("rl::", "") == kernel):
                 return v
     return None
 
@@ -442,7 +493,6 @@ def run_ba_ours(args, D):
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
-    time.sleep(0.25)
     D.barrier()
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -542,24 +592,25 @@ def ba_e2e(cams, X, w, feats, obs, args, D):
             "path": "rl_ba_jac_f64_host (pinned host buffers, 3-stream pipeline)"}
 
 
-def ba_cpu(target_s=10.0):
+def ba_cpu(target_s=2.0):
+    """Whole Jacobians (all observations) repeated until ~target_s of wall time
+    over all host threads."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as O
     cams, X, w, feats, obs = ba_synthetic(BA_N, BA_M, BA_P)
-    n = 2048
+    reps = 0
+    t0 = time.perf_counter()
     while True:
-        t0 = time.perf_counter()
-        O.ba_jac(cams, X, w[:n], feats[:n], obs[:n])
+        O.ba_jac(cams, X, w, feats, obs)
+        reps += 1
         dt = time.perf_counter() - t0
-        if dt >= target_s or n >= BA_P:
+        if dt >= target_s:
             break
-        n = min(BA_P, max(n * 2, int(n * target_s / max(dt, 1e-3))))
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    rate = n / dt
-    return {"value": round(rate / BA_P, 4), "unit": "jacobians/s", "cores": cores, "kind": "port",
-            "obs_per_s": round(rate, 1),
-            "sample": f"{n} of the {BA_P} observations (2 seeded passes + weight each, all "
-                      f"reference sweeps and checks, oracle/revoracle.c), {dt:.2f} s"}
+    return {"value": round(reps / dt, 4), "unit": "jacobians/s", "cores": cores, "kind": "port",
+            "obs_per_s": round(reps * BA_P / dt, 1),
+            "sample": f"{reps} full Jacobians ({BA_P} observations each: 2 seeded passes + "
+                      f"weight, all reference sweeps and checks, oracle/revoracle.c), {dt:.2f} s"}
 
 
 def measured_hbm():
@@ -639,7 +690,6 @@ def run_gmm_ours(args, D):
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
-    time.sleep(0.25)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     D.barrier()
@@ -746,6 +796,27 @@ def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
             "path": "rl_gmm_grad_f64_host (host buffers; allocates its device workspace per call)"}
 
 
+def gmm_cpu(workload):
+    """One full gradient evaluation of configs[2] on the sequential C oracle
+    (all four reference sweeps; the reference's shared scratch makes the
+    points sequential, so one thread)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    d, K, N, seed = GMM_CFG["gmm"]
+    rng = np.random.default_rng(seed)
+    alphas = rng.standard_normal(K)
+    means = rng.random((K, d))
+    icf = rng.standard_normal((K, d * (d + 1) // 2)) * 0.5
+    x = rng.random((N, d))
+    cst = gmm_constants(d, K, N, 1.0, 0)
+    t0 = time.perf_counter()
+    O.gmm_grad(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+    dt = time.perf_counter() - t0
+    return {"value": round(1.0 / dt, 5), "unit": "evals/s", "cores": 1, "kind": "port",
+            "sample": f"one full evaluation of configs[2] (d={d}, K={K}, N={N}) on the sequential "
+                      f"oracle (oracle/revoracle.c), {dt:.2f} s"}
+
+
 # ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
@@ -756,21 +827,36 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        if args.workload != "bessel":
+        if args.workload == "gmm_large":
             print(json.dumps({"impl": "reference", "unavailable":
-                              f"reference arm implemented for the bessel workload only"}))
+                              "configs[4] on the sequential CPU oracle is ~13 core-years per "
+                              "evaluation (SURVEY.md §8(d)); timed at configs[2] instead"}))
             return 0
-        base = bessel_cpu(target_s=max(3.0, min(20.0, 2.0 * args.steps)))
-        res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "grads/s",
-               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": round(1e3 * (args.n or BESSEL_N) / base["value"], 3),
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "f64", "data": "synthetic z ~ U(0.1, 10), seed 1",
-               "config": {"workload": "bessel_j2_grad_2^26", "n_total": args.n or BESSEL_N,
-                          "nu": BESSEL_NU, "thr": THR},
-               "impl": "reference", "cpu_baseline": base,
-               "e2e": {"value": base["value"], "unit": "grads/s", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0}}
+        if args.workload == "bessel":
+            base = bessel_cpu(target_s=max(2.0, min(20.0, 0.5 * args.steps)))
+            res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "grads/s",
+                   "ms_per_step": round(1e3 * (args.n or BESSEL_N) / base["value"], 3),
+                   "scaling": "strong", "data": "synthetic z ~ U(0.1, 10), seed 1",
+                   "config": {"workload": "bessel_j2_grad_2^26", "n_total": args.n or BESSEL_N,
+                              "nu": BESSEL_NU, "thr": THR}}
+        elif args.workload == "ba":
+            base = ba_cpu(target_s=max(2.0, min(20.0, 0.5 * args.steps)))
+            res = {"metric": "Jacobian evals/sec", "value": base["value"], "unit": "jacobians/s",
+                   "ms_per_step": round(1e3 / base["value"], 3), "scaling": "strong",
+                   "data": "synthetic ba20-shaped problem, seed 3",
+                   "config": {"workload": "ba20_jacobian", "n_cams": BA_N, "n_pts": BA_M,
+                              "n_obs": BA_P}}
+        else:
+            base = gmm_cpu(args.workload)
+            res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "evals/s",
+                   "ms_per_step": round(1e3 / base["value"], 3), "scaling": "strong",
+                   "data": "synthetic, seed 2",
+                   "config": {"workload": "gmm_d64_K25_N1e4_grad"}}
+        res.update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                    "higher_is_better": True, "vs_baseline": None, "dtype": "f64",
+                    "impl": "reference", "cpu_baseline": base,
+                    "e2e": {"value": base["value"], "unit": base["unit"],
+                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
         print(json.dumps(res))
         return 0
 

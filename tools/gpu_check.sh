@@ -16,10 +16,16 @@ timeout 300 $SMALL > gpurun_out/bench_small.json 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_besselj -s 3 -c 1 \
     -o gpurun_out/prof_bessel $SMALL > gpurun_out/ncu_full.log 2>&1
 echo "bessel ncu rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_bessel.csv $SMALL > gpurun_out/ncu_launches_bessel.log 2>&1
+echo "bessel launches rc=$?"
 timeout 300 $BA > gpurun_out/bench_ba_small.json 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ba_jac -s 3 -c 1 \
     -o gpurun_out/prof_ba $BA > gpurun_out/ncu_full_ba.log 2>&1
 echo "ba ncu rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_ba.csv $BA > gpurun_out/ncu_launches_ba.log 2>&1
+echo "ba launches rc=$?"
 timeout 300 $GMM > gpurun_out/bench_gmm_small.json 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_gmm.csv $GMM > gpurun_out/ncu_launches_gmm.log 2>&1 && \

@@ -9,7 +9,7 @@ from ncu_summary import summarise  # noqa: E402
 
 out = {"_source": "ncu --set full --clock-control none (dram__bytes_read.sum + dram__bytes_write.sum)",
        "_captures": {}}
-for name, rep in [("k_besselj_grad", "gpurun_out/prof_bessel.ncu-rep"),
+for name, rep in [("k_besselj", "gpurun_out/prof_bessel.ncu-rep"),
                   ("k_ba_jac", "gpurun_out/prof_ba.ncu-rep"),
                   ("k_gmm", "gpurun_out/prof_gmm.ncu-rep")]:
     try:
