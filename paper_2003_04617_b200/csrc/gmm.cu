@@ -45,6 +45,18 @@
 
 namespace rl {
 
+#ifndef GMM_TPR64
+#define GMM_TPR64 32       // reverse tile (points) for DP = 64
+#endif
+#ifndef GMM_REV_MINB
+#define GMM_REV_MINB 2     // reverse CTAs per SM (launch bounds) for DP <= 64
+#endif
+#ifndef GMM_TPF
+#define GMM_TPF 64         // forward tile (points) for DP = 64
+#endif
+#ifndef GMM_FWD_MINB
+#define GMM_FWD_MINB 2     // forward CTAs per SM (launch bounds) for DP <= 64
+#endif
 constexpr int GMM_THREADS = 256;
 constexpr int GMM_WARPS = GMM_THREADS / 32;
 
@@ -80,28 +92,44 @@ __host__ __device__ constexpr int ltb_idx(int DP, int a, int b) {
 // ---------------------------------------------------------------------------
 // -N lse(alphas) with the Int argmax record, as in the program: par[k] =
 // its alphas.g share, par[K] = -N * lsa (one thread)
+// alphas' reversible logsumexp and its adjoint, whole block (block 0 of
+// k_gmm_prep); `sa` = K doubles of shared scratch.  The sums run in the
+// reference's order on one thread; the exps and adjoints run in parallel.
 __device__ void gmm_alpha_lse(int K, long long N_total, const double *__restrict__ alphas,
-                              double *__restrict__ par) {
-  int ia = 0;
-  for (int k = 1; k < K; k++)
-    if (alphas[k] > alphas[ia]) ia = k;
-  const double amx = 0.0 + alphas[ia];
-  double ase = 0.0;
-  for (int k = 0; k < K; k++) ase = ase + exp(0.0 + (alphas[k] - amx));
-  const double lsa = (0.0 + log(ase)) + amx;
-  const double nn = (double)N_total;
-  par[K] = -(nn * lsa);
-  // gradient: err += nn*lsa (inverse): lsa.g = -nn; then ~routine
-  const double lsag = 0.0 + (-1.0 * 1.0) * nn;
-  double amxg = 0.0 + lsag;                              // lsa -= amx
-  const double aseg = 0.0 + lsag * (1.0 / ase);          // lsa -= log(ase)
-  for (int k = K - 1; k >= 0; k--) {
-    const double ex = exp(0.0 + (alphas[k] - amx));
-    const double tg = 0.0 + aseg * ex;                   // ase -= exp(t)
-    par[k] = tg;                                         // alphas[k].g += t.g
-    amxg = amxg - tg;
+                              double *__restrict__ par, double *sa) {
+  __shared__ double s_amx, s_aseg;
+  __shared__ int s_ia;
+  for (int k = threadIdx.x; k < K; k += GMM_THREADS) sa[k] = alphas[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ia = 0;
+    for (int k = 1; k < K; k++)
+      if (sa[k] > sa[ia]) ia = k;
+    s_ia = ia;
+    s_amx = 0.0 + sa[ia];
   }
-  par[ia] += amxg;                                       // amx -= alphas[ia]
+  __syncthreads();
+  const double amx = s_amx;
+  for (int k = threadIdx.x; k < K; k += GMM_THREADS) sa[k] = exp(0.0 + (sa[k] - amx));
+  __syncthreads();
+  const double nn = (double)N_total;
+  const double lsag = 0.0 + (-1.0 * 1.0) * nn;          // err += nn*lsa (inverse): lsa.g = -nn
+  if (threadIdx.x == 0) {
+    double ase = 0.0;
+    for (int k = 0; k < K; k++) ase = ase + sa[k];
+    const double lsa = (0.0 + log(ase)) + amx;
+    par[K] = -(nn * lsa);
+    s_aseg = 0.0 + lsag * (1.0 / ase);                   // lsa -= log(ase)
+  }
+  __syncthreads();
+  const double aseg = s_aseg;
+  for (int k = threadIdx.x; k < K; k += GMM_THREADS) par[k] = 0.0 + aseg * sa[k];  // ase -= exp(t)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double amxg = 0.0 + lsag;                            // lsa -= amx
+    for (int k = K - 1; k >= 0; k--) amxg = amxg - (0.0 + aseg * sa[k]);
+    par[s_ia] += amxg;                                   // amx -= alphas[ia]
+  }
 }
 
 template <int DP>
@@ -115,7 +143,13 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
                                                           double *__restrict__ par) {
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
-  const double *ic = icf + (long long)k * P;
+  extern __shared__ __align__(16) double prep_dyn[];     // icf row (P), then K scratch
+  double *ic = prep_dyn;
+  {
+    const double *icg = icf + (long long)k * P;          // one coalesced pass
+    for (int j = threadIdx.x; j < P; j += GMM_THREADS) ic[j] = icg[j];
+  }
+  __syncthreads();
   constexpr int LTS = ltb_size(DP);
   double *lt = LT + (long long)k * LTS;
   for (int e = threadIdx.x; e < LTS; e += GMM_THREADS) {
@@ -142,7 +176,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
     for (int j = 0; j < d; j++) s = s + ic[j];           // sq[k] += icf[k, j] (in order)
     sq[k] = s;
   }
-  if (k == 0 && threadIdx.x == 32 && par) gmm_alpha_lse(K, N_total, alphas, par);
+  if (k == 0 && par) gmm_alpha_lse(K, N_total, alphas, par, prep_dyn + P);
   // qd and this component's share of the prior's Frobenius sum:
   // fro += abs2(qd![k, j]) (j <= d) or abs2(icf[k, j]) (j > d)
   double f = 0.0;
@@ -275,7 +309,7 @@ __device__ __forceinline__ void copy_lt_async(double *__restrict__ lt_s, const d
 // forward: mt[k][i] = alphas[k] + sq[k] - |L_k (x_i - mu_k)|^2 / 2
 // ---------------------------------------------------------------------------
 template <int DP, int TP>
-__global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_fwd(
+__global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_gmm_fwd(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
     double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA) {
@@ -440,7 +474,7 @@ __device__ __forceinline__ void mtile_ij(int t, int &i, int &j) {
 }
 
 template <int DP, int TP>
-__global__ void __launch_bounds__(GMM_THREADS, 1) k_gmm_rev(
+__global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_gmm_rev(
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ x,
     const double *__restrict__ LT, const double *__restrict__ gmtT,
     double *__restrict__ part /* [K][S][DP*DP + DP + 1] */) {
@@ -605,8 +639,24 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_reduce(int S, long long PW,
   if (e >= PW) return;
   const double *pk = part + (long long)k * S * PW + e;
   double s = 0.0;
+#pragma unroll 8
   for (int j = 0; j < S; j++) s += pk[(long long)j * PW];
   red[(long long)k * PW + e] = s;
+}
+
+// sum of the per-block point objectives into red[0] (whole block; the same
+// order in k_gmm_final and k_gmm_err, so the objective-only run reproduces
+// the gradient's objective bit for bit)
+__device__ __forceinline__ void sum_err_parts(int nerr, const double *__restrict__ err_part,
+                                              double *red) {
+  double e = 0.0;
+  for (int j = threadIdx.x; j < nerr; j += GMM_THREADS) e += err_part[j];
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int o = GMM_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -641,54 +691,73 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     const double ga_k = sg + (add_params ? ws_par[k] : 0.0);
     g_alpha[k] = ga_k;
   }
-  // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a)
+  // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a):
+  // GMM_THREADS / DP lanes per row, shuffle-reduced
   const double *lt = LT + (long long)k * ltb_size(DP);
-  for (int a = threadIdx.x; a < d; a += GMM_THREADS) {
+  {
+    constexpr int LR = GMM_THREADS / DP;                 // lanes per row: 8, 4, 2
+    const int a = threadIdx.x / LR, l = threadIdx.x % LR;
     double s = 0.0;
-    for (int b = a; b < d; b++) s = fma(gsum[b], lt[ltb_idx(DP, a, b)], s);
-    g_means[(long long)k * d + a] = -s;
+    if (a < d)
+#pragma unroll 4
+      for (int b = a + l; b < d; b += LR) s = fma(gsum[b], lt[ltb_idx(DP, a, b)], s);
+#pragma unroll
+    for (int o = LR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if (a < d && l == 0) g_means[(long long)k * d + a] = -s;
   }
-  // icf.g: diag = sq.g + qd.g exp(icf); offdiag = M[b][a] (+ prior)
+  // icf.g: diag = sq.g + qd.g exp(icf); offdiag = M[b][a] (+ prior).  The
+  // threads walk M's lower triangle (b >= a) in its stored row-major order,
+  // so the partial reads coalesce; icf index: diag j = a, off-diagonal
+  // (row b, col a) of the column-major strict lower triangle j = d + a d -
+  // a (a + 1) / 2 + (b - a - 1)
   const double sqg = sg + (add_params ? -(double)wm : 0.0);
-  for (int j = threadIdx.x; j < P; j += GMM_THREADS) {
-    int b, a;
-    if (j < d) {
-      b = a = j;
-    } else {
-      // column-major strict lower triangle index -> (b, a)
-      int r = j - d;
-      a = 0;
-      while (r >= d - 1 - a) {
-        r -= d - 1 - a;
-        a++;
-      }
-      b = a + 1 + r;
-    }
-    double m = 0.0;
-    for (int s = 0; s < S; s++) m += pk[s * PW + (long long)b * DP + a];
+  const int T = d * (d + 1) / 2;
+#pragma unroll 2
+  for (int e = threadIdx.x; e < T; e += GMM_THREADS) {
+    int b = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    if (b * (b + 1) / 2 > e) b--;
+    if ((b + 1) * (b + 2) / 2 <= e) b++;
+    const int a = e - b * (b + 1) / 2;
+    const double m = pk[(long long)b * DP + a];
     double g;
-    if (j < d) {
+    if (a == b) {
+      const int j = a;
       const double q = qd[(long long)k * d + j];
       const double qdg = (add_params ? hg2 * (2.0 * q) : 0.0) + m;
       g = (0.0 + sqg) + qdg * exp(icf[(long long)k * P + j]);
+      g_icf[(long long)k * P + j] = g;
     } else {
+      const int j = d + a * d - a * (a + 1) / 2 + (b - a - 1);
       g = (add_params ? hg2 * (2.0 * icf[(long long)k * P + j]) : 0.0) + m;
+      g_icf[(long long)k * P + j] = g;
     }
-    g_icf[(long long)k * P + j] = g;
   }
-  if (k == 0 && threadIdx.x == 0) {
-    double e = 0.0;
-    for (int j = 0; j < nerr; j++) e += err_part[j];
-    if (add_params) {
-      // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst)
-      double fro = 0.0, ssq = 0.0;
-      for (int kk = 0; kk < K; kk++) {
-        fro = fro + fro_k[kk];
-        ssq = ssq + sq[kk];
+  __shared__ double ered[GMM_THREADS];
+  if (k == 0) {
+    sum_err_parts(nerr, err_part, ered);
+    // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst);
+    // fro and ssq summed in component order from shared-memory chunks
+    __shared__ double cfro[GMM_THREADS], csq[GMM_THREADS];
+    double fro = 0.0, ssq = 0.0;
+    for (int k0 = 0; add_params && k0 < K; k0 += GMM_THREADS) {
+      const int kk = k0 + threadIdx.x;
+      if (kk < K) {
+        cfro[threadIdx.x] = fro_k[kk];
+        csq[threadIdx.x] = sq[kk];
       }
-      e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int q = 0; q < GMM_THREADS && k0 + q < K; q++) {
+          fro = fro + cfro[q];
+          ssq = ssq + csq[q];
+        }
+      __syncthreads();
     }
-    out[0] = e;
+    if (threadIdx.x == 0) {
+      double e = ered[0];
+      if (add_params) e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
+      out[0] = e;
+    }
   }
 }
 
@@ -699,9 +768,10 @@ __global__ void k_gmm_err(int K, int nerr, const double *__restrict__ err_part,
                           const double *__restrict__ sq, const double *__restrict__ fro_k,
                           const double *__restrict__ ws_par, double ga, int wm, double cst,
                           int add_params, double *__restrict__ out) {
+  __shared__ double ered[GMM_THREADS];
+  sum_err_parts(nerr, err_part, ered);
   if (threadIdx.x != 0) return;
-  double e = 0.0;
-  for (int j = 0; j < nerr; j++) e += err_part[j];
+  double e = ered[0];
   if (add_params) {
     const double hg2 = 0.5 * ga * ga;
     double fro = 0.0, ssq = 0.0;
@@ -719,8 +789,14 @@ __global__ void k_gmm_err(int K, int nerr, const double *__restrict__ err_part,
 // ---------------------------------------------------------------------------
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
 // points per tile: forward / reverse (the reverse also stages qxc.g)
-static int tpf_of(int) { return 64; }
-static int tpr_of(int DP) { return DP == 32 ? 64 : 32; }
+static constexpr int tpf_c(int DP) { return DP == 64 ? GMM_TPF : 64; }
+static int tpf_of(int DP) { return tpf_c(DP); }
+static constexpr int tpr_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? GMM_TPR64 : 32); }
+static int tpr_of(int DP) { return tpr_c(DP); }
+// concurrent CTAs per SM the split assumes: forward 2 (DP <= 64), reverse
+// GMM_REV_MINB (DP <= 64); DP = 128 runs one CTA per SM
+static int fwd_per_sm(int DP) { return DP == 128 ? 1 : GMM_FWD_MINB; }
+static int rev_per_sm(int DP) { return DP == 128 ? 1 : GMM_REV_MINB; }
 
 template <int DP, int TP>
 static constexpr size_t smem_fwd() {
@@ -770,12 +846,11 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   const int DP = dp_of(d);
   const long long ntf = (N + tpf_of(DP) - 1) / tpf_of(DP);
   const long long ntr = (N + tpr_of(DP) - 1) / tpr_of(DP);
-  const int slots = 148 * (DP == 128 ? 1 : 2);
-  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, slots, 64);
+  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * fwd_per_sm(DP), 64);
   // each reverse CTA writes a (DP^2 + DP + 1)-double partial: cap them at 256 MB
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
-  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, slots, smax);
+  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * rev_per_sm(DP), smax);
   L.nerr = (int)((N + GMM_THREADS - 1) / GMM_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -802,7 +877,7 @@ static int launch_gmm_err_only(int K, const GmmLayout &L, long long N, const dou
                                const double *sq, const double *fro, const double *par,
                                double gamma, int m, double cst, int add_params, double *out,
                                cudaStream_t st) {
-  k_gmm_err<<<1, 32, 0, st>>>(K, N > 0 ? L.nerr : 0, errp, sq, fro, par, gamma, m, cst,
+  k_gmm_err<<<1, GMM_THREADS, 0, st>>>(K, N > 0 ? L.nerr : 0, errp, sq, fro, par, gamma, m, cst,
                               add_params, out);
   return cuda_status(cudaGetLastError(), "k_gmm_err");
 }
@@ -819,7 +894,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    double cst, double tol, int chk, int add_params, double *out, uint8_t *fail,
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st,
                    int grad = 1) {
-  constexpr int TPF = 64, TPR = DP == 32 ? 64 : 32;
+  constexpr int TPF = tpf_c(DP), TPR = tpr_c(DP);
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
   double *fro = (double *)(ws + L.fro);
   double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
@@ -828,8 +903,13 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   double *redp = (double *)(ws + L.red);
   double *par = (double *)(ws + L.par);
   int rc;
-  k_gmm_prep<DP><<<K, GMM_THREADS, 0, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
-                                            add_params ? par : nullptr);
+  const size_t sp = ((size_t)d * (d + 1) / 2 + K) * 8;
+  if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_prep<DP>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp),
+                        "smem attr prep")))
+    return rc;
+  k_gmm_prep<DP><<<K, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
+                                             add_params ? par : nullptr);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
     if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
