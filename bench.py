@@ -348,7 +348,12 @@ def run_bessel_ours(args, D):
     # objective only ("-O", the paper's objective timing): run of besselj
     o_ms = D.max(time_device(lambda: kernels.besselj_run(z, BESSEL_NU), max(3, args.steps // 4)))
     objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
-                 "kernel": "k_besselj<false> (rl_besselj_run_f64)"}
+                 "kernel": "k_besselj<0> (rl_besselj_run_f64)"}
+    # forward-over-reverse Hessian (d2J/dz2 with J and dJ/dz) of the same batch
+    h_ms = D.max(time_device(lambda: kernels.besselj_hess(z, BESSEL_NU), max(3, args.steps // 4)))
+    hess = {"ms_per_step": round(h_ms, 4), "hessians_per_s": round(n_total / (h_ms * 1e-3), 1),
+            "hess_over_grad": round(h_ms / ms_step, 3),
+            "kernel": "k_besselj<2> (rl_besselj_hess_f64, Dual-number sweeps)"}
     e2e = None
     if not args.no_e2e:
         e2e = bessel_e2e(torch, z, args, D, n_total)
@@ -363,7 +368,7 @@ def run_bessel_ours(args, D):
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clocks, "sum_trips_per_step": D.sum(sum_trips),
         "failed_per_step": D.sum(n_failed), "parity_sample": parity,
-        "objective_only": objective,
+        "objective_only": objective, "hessian": hess,
     }
     return res
 

@@ -159,6 +159,19 @@ int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const
                          unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
 
 /* ----------------------------------------------------------------------
+ * Batched forward-over-reverse Hessian of besselj:
+ * replaces reference autodiff.hessian(p, "besselj", [0.0, nu, z[i]])
+ * (autodiff.py:216-257) for every z[i]: the gradient sweeps run over Dual
+ * numbers with z carrying the unit tangent, so H[z, z] = d2Jdz2[i]; the
+ * other entries of the reference's 2x2 matrix (leaves out!, z) are 0.  J,
+ * dJdz, fail and counters are bit-identical to rl_besselj_grad_f64's.
+ * ---------------------------------------------------------------------- */
+int rl_besselj_hess_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, double *d2Jdz2, uint8_t *fail,
+                        unsigned long long *counters, void *stream);
+
+/* ----------------------------------------------------------------------
  * BA Jacobian in ADBench's sparse layout (BASparseMat, CSR with int row
  * pointers and column indices).  Same values as
  * rl_ba_jac_f64 (the reference's two seeded gradient(p, GradRequest(

@@ -218,8 +218,34 @@ def gen_run():
     print("run/uncall goldens written")
 
 
+def gen_hess():
+    """reference autodiff.hessian (forward-over-reverse over Duals) of besselj:
+    configs[0]'s 1,000 z (seed 0) at nu = 2, 40 z at nu = 0, 1, 5, and error
+    cases; the full matrix over the Float leaves (out!, z)."""
+    from revlang.autodiff import hessian
+    pb = _prog("besselj.rnl")
+    rng = np.random.default_rng(0)
+    zs = [rng.uniform(0.1, 10.0, 1000)]
+    nus = [np.full(1000, 2)]
+    r2 = np.random.default_rng(31)
+    for nu in (0, 1, 5):
+        zs.append(np.concatenate([r2.uniform(0.1, 10.0, 37), [1e-3, 25.0, -1.0]]))
+        nus.append(np.full(40, nu))
+    z, nu = np.concatenate(zs), np.concatenate(nus)
+    H = np.full((z.size, 2, 2), np.nan)
+    errs = []
+    t0 = time.time()
+    for i in range(z.size):
+        r, en = _err_name(lambda: hessian(pb, "besselj", [0.0, int(nu[i]), float(z[i])]))
+        if r is not None:
+            H[i] = r.matrix
+        errs.append(en)
+    np.savez_compressed(os.path.join(OUT_DIR, "hess.npz"), z=z, nu=nu, H=H, err=np.array(errs))
+    print(f"hessian goldens written ({z.size} cases, {time.time() - t0:.1f} s)")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
-    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run"]
+    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess"]
     for w in which:
         globals()["gen_" + w]()

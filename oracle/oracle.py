@@ -50,6 +50,11 @@ def lib():
         L.orc_besselj_grad_batch.argtypes = [
             ctypes.c_int, _c_double_p, ctypes.c_long, ctypes.c_double, ctypes.c_double,
             ctypes.c_double, ctypes.c_long, ctypes.c_int, _c_double_p, _c_double_p, _c_u8_p]
+        L.orc_besselj_hess_batch.restype = ctypes.c_long
+        L.orc_besselj_hess_batch.argtypes = [
+            ctypes.c_int, _c_double_p, ctypes.c_long, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_long, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
+            _c_u8_p]
         L.orc_ba_obs.restype = ctypes.c_int
         L.orc_ba_obs.argtypes = [_c_double_p, _c_double_p, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_int,
@@ -93,6 +98,19 @@ def besselj_grad(nu, z, thr=1e-16, tol=1e-9, seed=1.0, max_trips=10**8, invcheck
         int(nu), _dp(z), n, thr, tol, seed, int(max_trips), int(bool(invcheck)), _dp(J),
         _dp(dz), fail.ctypes.data_as(_c_u8_p))
     return J, dz, fail, int(total)
+
+
+def besselj_hess(nu, z, thr=1e-16, tol=1e-9, seed=1.0, max_trips=10**8, invcheck=True):
+    """Forward-over-reverse second derivative (autodiff.hessian's H[z, z]) per
+    z: returns J, dJdz, d2Jdz2, fail, sum_trips."""
+    z = _f64(np.atleast_1d(z))
+    n = z.size
+    J, dz, d2 = np.empty(n), np.empty(n), np.empty(n)
+    fail = np.zeros(n, np.uint8)
+    total = lib().orc_besselj_hess_batch(
+        int(nu), _dp(z), n, thr, tol, seed, int(max_trips), int(bool(invcheck)), _dp(J),
+        _dp(dz), _dp(d2), fail.ctypes.data_as(_c_u8_p))
+    return J, dz, d2, fail, int(total)
 
 
 def ba_jac(cams, X, w, feats, obs, tol=1e-9, invcheck=True):

@@ -229,6 +229,144 @@ int orc_besselj_grad(int nu, double z, double thr, double tol, double seed, long
   return RL_OK;
 }
 
+/* -------------------------------------------------------------------------
+ * Forward-over-reverse Hessian (autodiff.hessian, autodiff.py:216-257): the
+ * gradient sweeps run over Dual numbers (values.py:258-340) with z carrying
+ * the unit tangent.  Floats are represented as Dual(f, 0.0): for + - * /
+ * this is bit-identical to the reference's _as_dual promotion (the two
+ * tangent products are the same terms, IEEE + and * commute).  Sweeps 3 and
+ * 4 follow _mul_div_adjoint (log_x + contrib / log_x - contrib) and
+ * _plus_minus_adjoint (delta = (sign * gy) * s_exp(log_x)); sweep 3's
+ * accumulations add exact zeros and are omitted like in the gradient.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  double p, t;
+} dual;
+
+static dual d_add(dual a, dual b) { return (dual){a.p + b.p, a.t + b.t}; }
+static dual d_sub(dual a, dual b) { return (dual){a.p - b.p, a.t - b.t}; }
+static dual d_f(double f) { return (dual){f, 0.0}; }
+static dual d_mul(dual a, dual b) { return (dual){a.p * b.p, a.t * b.p + a.p * b.t}; }
+static dual d_div(dual a, dual b) {
+  const double q = a.p / b.p;
+  return (dual){q, (a.t - q * b.t) / b.p};
+}
+static int d_exp(dual a, dual *out) { /* s_exp: Dual(r, t r) */
+  double r;
+  TRY(py_exp(a.p, &r));
+  *out = (dual){r, a.t * r};
+  return RL_OK;
+}
+static int d_log(dual a, dual *out) { /* s_log: Dual(log p, t / p) */
+  double l;
+  PY_LOG(a.p, l);
+  *out = (dual){l, a.t / a.p};
+  return RL_OK;
+}
+
+int orc_besselj_hess(int nu, double z, double thr, double tol, double seed, long max_trips,
+                     int invcheck, double *J, double *dJdz, double *d2Jdz2, long *trips) {
+  int chk = invcheck != 0;
+  double Jp, dz;
+  long T;
+  *d2Jdz2 = NAN;
+  /* sweeps 1 and 2 (primal; the Dual run's primal is this) and every check */
+  TRY(orc_besselj_grad(nu, z, thr, tol, seed, max_trips, invcheck, &Jp, &dz, &T));
+  /* sweep 3: R in gradient mode over Duals */
+  const dual Z = {z, 1.0};
+  dual lz = d_f(0.0), halfz = d_f(0.0), halfz2 = d_f(0.0), s = d_f(0.0), acc = d_f(0.0), c, e;
+  long k = 0, kn = 0;
+  TRY(d_log(Z, &c)); /* lz *= convert(z) */
+  lz = d_add(lz, c);
+  halfz = d_add(halfz, lz);                   /* halfz *= lz */
+  halfz = d_sub(halfz, d_f(log(2.0)));        /* halfz /= 2 */
+  halfz2 = d_add(halfz2, halfz);              /* halfz2 *= halfz (x2) */
+  halfz2 = d_add(halfz2, halfz);
+  for (long i = 1; i <= nu; i++) {
+    s = d_add(s, halfz);                      /* s *= halfz */
+    s = d_sub(s, d_f(log((double)i)));        /* s /= i */
+  }
+  TRY(d_exp(s, &e));                          /* acc += convert(s) */
+  acc = d_add(acc, e);
+  for (;;) {
+    TRY(d_exp(s, &e));
+    if (!(e.p > thr)) break;
+    k += 1;
+    kn += k;
+    kn += nu;
+    s = d_add(s, halfz2);                     /* s *= halfz2 */
+    s = d_sub(s, d_f(log((double)k)));        /* s /= k */
+    s = d_sub(s, d_f(log((double)kn)));       /* s /= kn */
+    kn -= nu;
+    kn -= k;
+    TRY(d_exp(s, &e));
+    acc = (k % 2 == 0) ? d_add(acc, e) : d_sub(acc, e);
+  }
+  /* out! -= acc: acc.g += (1.0 * out.g) * 1.0 (a float) */
+  const dual gacc = d_f((1.0 * seed) * 1.0);
+  dual gs = d_f(0.0), gh2 = d_f(0.0), gh = d_f(0.0), glz = d_f(0.0), gz = d_f(0.0);
+  /* sweep 4: ~R with the adjoint rules over Duals */
+  while (k != 0) {
+    TRY(d_exp(s, &e));
+    if (k % 2 == 0) { /* acc -= convert(s): sign +1 */
+      acc = d_sub(acc, e);
+      gs = d_add(gs, d_mul(d_f(1.0 * gacc.p), e));
+    } else {          /* acc += convert(s): sign -1 */
+      acc = d_add(acc, e);
+      gs = d_add(gs, d_mul(d_f(-1.0 * gacc.p), e));
+    }
+    kn += k;
+    kn += nu;
+    s = d_add(s, d_f(log((double)kn)));       /* s *= kn */
+    s = d_add(s, d_f(log((double)k)));        /* s *= k */
+    s = d_sub(s, halfz2);                     /* s /= halfz2 */
+    gh2 = d_add(gh2, d_mul(d_f(1.0), gs));
+    kn -= nu;
+    kn -= k;
+    k -= 1;
+  }
+  TRY(d_exp(s, &e));                          /* acc -= convert(s) */
+  acc = d_sub(acc, e);
+  gs = d_add(gs, d_mul(d_f(1.0 * gacc.p), e));
+  for (long i = nu; i >= 1; i--) {
+    s = d_add(s, d_f(log((double)i)));        /* s *= i */
+    s = d_sub(s, halfz);                      /* s /= halfz */
+    gh = d_add(gh, d_mul(d_f(1.0), gs));
+  }
+  halfz2 = d_sub(halfz2, halfz);              /* halfz2 /= halfz (x2) */
+  gh = d_add(gh, d_mul(d_f(1.0), gh2));
+  halfz2 = d_sub(halfz2, halfz);
+  gh = d_add(gh, d_mul(d_f(1.0), gh2));
+  halfz = d_add(halfz, d_f(log(2.0)));        /* halfz *= 2 */
+  halfz = d_sub(halfz, lz);                   /* halfz /= lz */
+  glz = d_add(glz, d_mul(d_f(1.0), gh));
+  TRY(d_log(Z, &c));                          /* lz /= convert(z) */
+  lz = d_sub(lz, c);
+  gz = d_add(gz, d_div(d_mul(d_f(1.0), glz), Z));
+  (void)chk;
+  (void)tol;
+  if (J) *J = Jp;
+  if (dJdz) *dJdz = gz.p;
+  *d2Jdz2 = gz.t;
+  if (trips) *trips = T;
+  return RL_OK;
+}
+
+long orc_besselj_hess_batch(int nu, const double *z, long n, double thr, double tol,
+                            double seed, long max_trips, int invcheck, double *J, double *dJdz,
+                            double *d2Jdz2, uint8_t *fail) {
+  long total = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : total)
+  for (long i = 0; i < n; i++) {
+    long T = 0;
+    int rc = orc_besselj_hess(nu, z[i], thr, tol, seed, max_trips, invcheck, &J[i], &dJdz[i],
+                              &d2Jdz2[i], &T);
+    fail[i] = (uint8_t)rc;
+    total += T;
+  }
+  return total;
+}
+
 /* batch helper for the CPU baseline (OpenMP over independent elements) */
 long orc_besselj_grad_batch(int nu, const double *z, long n, double thr, double tol,
                             double seed, long max_trips, int invcheck, double *J,

@@ -14,19 +14,20 @@ plus the batched device API over torch CUDA tensors:
   helpers in parallel.py.
 """
 
-from .autodiff import ExecOptions, GradRequest, gradient, jacobian
+from .autodiff import ExecOptions, GradRequest, HessianResult, gradient, hessian, jacobian
 from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
                      UnknownExample, UnknownFunction, UnsupportedProgram)
 from .interp import CheckReport, check_reversibility, run, uncall
-from .kernels import (BACsr, BAResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_jacobian_csr,
+from .kernels import (BACsr, BAResult, BesselHessResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_jacobian_csr,
                       ba_jacobian_csr_host, ba_residuals,
-                      besselj_grad, besselj_grad_host, besselj_run, gmm_grad, gmm_objective)
+                      besselj_grad, besselj_grad_host, besselj_hess, besselj_run, gmm_grad, gmm_objective)
 from .programs import CATALOG, Program, entry_function, load_example, parse_program
 from .values import Array
 
 __all__ = [
+    "HessianResult", "hessian", "BesselHessResult", "besselj_hess",
     "AliasedArguments", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",

@@ -58,6 +58,8 @@ SIGNATURES = {
     "rl_gmm_objective_f64": (ctypes.c_int, [_i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _f64,
                                             _i32, _f64, _f64, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
                                             _vp]),
+    "rl_besselj_hess_f64": (ctypes.c_int, [_i32, _vp, _i64, _f64, _f64, _f64, _i64, _i32, _vp,
+                                           _vp, _vp, _vp, _vp, _vp]),
     "rl_ba_jac_csr_f64": (ctypes.c_int, [_i32, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                          _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rl_ba_jac_csr_f64_host": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64,

@@ -341,3 +341,47 @@ def jacobian(program, fname, args, opts=None):
                 row += _flat(grads.get(nj), args[pj])
             rows.append(row)
     return np.array(rows, dtype=float)
+
+
+@dataclass
+class HessianResult:
+    """Reference `HessianResult` (autodiff.py): the raw matrix over the
+    differentiable Float leaves and its asymmetry max |H - H^T|."""
+    matrix: np.ndarray
+    symmetry_error: float
+
+
+def hessian(program, fname, args, opts=None):
+    """Reference `hessian` (autodiff.py:216-257, forward-over-reverse) on the
+    device for besselj: the Float leaves are out! and z (nu is an Int), the
+    only nonzero entry is H[z, z] = d2J/dz2 from rl_besselj_hess_f64, which
+    runs the gradient sweeps over Dual numbers exactly as the reference does.
+    Other programs' Hessians are not produced on device (UnsupportedProgram)."""
+    opts = _check_opts(opts)
+    fdef = _resolve(program, fname)
+    if fdef.kernel.handler != "besselj":
+        raise UnsupportedProgram(
+            f"hessian of {fname!r}: only besselj has a device Hessian kernel")
+    if len(args) != 3:
+        raise KindError(f"besselj takes 3 arguments, got {len(args)}")
+    out0, nu, z = args
+    if not _is_int(nu):
+        raise KindError("nu must be an Int")
+    leaves = [i for i, v in ((0, out0), (2, z)) if _is_float(v)]
+    n = len(leaves)
+    H = np.zeros((n, n))
+    if 2 in leaves:
+        dev = _device()
+        zt = torch.tensor([float(z)], dtype=torch.float64, device=dev)
+        r = kernels.besselj_hess(zt, int(nu), seed=1.0, thr=fdef.constants.get("thr", 1e-16),
+                                 tol=opts.float_tolerance, invcheck=opts.invcheck,
+                                 max_steps=opts.max_steps)
+        code = int(r.fail[0].item())
+        if code:
+            raise error_for_code(code, "besselj")
+        J = float(r.J[0].item())
+        if not abs(((float(out0) + J) - J) - float(out0)) <= opts.float_tolerance:
+            raise error_for_code(5, "besselj")
+        H[leaves.index(2), leaves.index(2)] = float(r.d2Jdz2[0].item())
+    sym_err = float(np.max(np.abs(H - H.T))) if n else 0.0
+    return HessianResult(H, sym_err)

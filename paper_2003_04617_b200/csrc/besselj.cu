@@ -480,15 +480,170 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   return o;
 }
 
-// GRAD: gradient (sweeps 1 + 4, Jout = J, dzout = dJ/dz).  !GRAD: run /
+
+// ---------------------------------------------------------------------------
+// Forward-over-reverse Hessian (autodiff.hessian, autodiff.py:216-257): the
+// gradient sweeps over Dual numbers (values.py:258-340), z carrying the unit
+// tangent, so dz.g's tangent is d2J/dz2.  Every Dual operation is the
+// reference's: add/sub componentwise, (p, t) * f = (p f, t f + p 0.0), the
+// quotient rule of Dual.__truediv__, s_exp = (e^p, t e^p), s_log = (log p,
+// t / p); floats enter as (f, 0.0) (bit-identical to _as_dual: the same two
+// tangent products, IEEE + and * commute).  Sweeps 3 / 4 use the gradient-
+// mode forms (log_x +- contrib, delta = (sign gy) * s_exp(log_x)); the primal
+// halves are the gradient kernel's arithmetic, so J and dJ/dz are bit-equal
+// to rl_besselj_grad_f64's.  Per-lane loops (lanes are z-sorted, so their
+// trip counts agree); not the speculative structure of the gradient path.
+// ---------------------------------------------------------------------------
+struct Dl {
+  double p, t;
+};
+__device__ __forceinline__ Dl dadd(Dl a, Dl b) { return Dl{a.p + b.p, a.t + b.t}; }
+__device__ __forceinline__ Dl dsub(Dl a, Dl b) { return Dl{a.p - b.p, a.t - b.t}; }
+__device__ __forceinline__ Dl dmul(Dl a, Dl b) { return Dl{a.p * b.p, a.t * b.p + a.p * b.t}; }
+__device__ __forceinline__ Dl ddiv(Dl a, Dl b) {
+  const double q = a.p / b.p;
+  return Dl{q, (a.t - q * b.t) / b.p};
+}
+__device__ __forceinline__ Dl dflt(double f) { return Dl{f, 0.0}; }
+template <bool CAREFUL>
+__device__ __forceinline__ Dl dexp(Dl a, int &code) {
+  const ExpR e = rexp<CAREFUL>(a.p);
+  if (CAREFUL && e.code && !code) code = e.code;
+  return Dl{e.t, a.t * e.t};
+}
+__device__ __forceinline__ double2 logpair_any(int k, int nu) {
+  return k < BJ_KP ? s_logpair[k] : make_double2(logi(k), logi(k + nu));
+}
+
+struct BJHOut {
+  double J, dz, d2;
+  int code, T;
+  bool bad;
+};
+
+template <bool CAREFUL>
+__device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int nu, double thr,
+                                                       double tol, double seed, int kfuel,
+                                                       int chk, double sfloor) {
+  int code = 0;
+  // ---------------- sweep 3 (= sweep 1 primal): R over Duals ----------------
+  if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
+  const bool zok = valid && !code;
+  const Dl Z{z, 1.0};
+  const Dl clz{zok ? log(z) : 0.0, zok ? 1.0 / z : 0.0};   // s_log(Dual(z, 1))
+  Dl lz = dadd(dflt(0.0), clz);
+  Dl halfz = dadd(dflt(0.0), lz);                         // halfz *= lz
+  halfz = dsub(halfz, dflt(LN2));                         // halfz /= 2
+  Dl h2 = dadd(dflt(0.0), halfz);                         // halfz2 *= halfz (x2)
+  h2 = dadd(h2, halfz);
+  Dl s = dflt(0.0);
+  for (int q = 1; q <= nu; q++) {                         // for i = 1:1:nu
+    s = dadd(s, halfz);
+    s = dsub(s, dflt(logi(q)));
+  }
+  Dl e = dexp<CAREFUL>(s, code);                          // acc += convert(s)
+  Dl acc = dadd(dflt(0.0), e);
+  const bool bad = !CAREFUL && zok &&
+                   !(z < 700.0 && s.p > -700.0 && s.p < 700.0 && h2.p + sfloor > -700.0);
+  bool act = valid && !code && e.p > thr;                 // while (s > thr, k != 0)
+  if (nu < 0 && act) {                                    // first trip: s /= kn, kn <= 0
+    code = kfuel > 0 ? RL_ERR_DOMAIN : RL_ERR_FUEL;
+    act = false;
+  }
+  int k = 0;
+  while (__any_sync(FULL_MASK, act)) {
+    if (act) {
+      if (k >= kfuel) {
+        code = RL_ERR_FUEL;
+        act = false;
+      } else {
+        k++;
+        const double2 L = logpair_any(k, nu);
+        s = dadd(s, h2);                                  // s *= halfz2
+        s = dsub(s, dflt(L.x));                           // s /= k
+        s = dsub(s, dflt(L.y));                           // s /= kn
+        e = dexp<CAREFUL>(s, code);
+        acc = (k & 1) ? dsub(acc, e) : dadd(acc, e);      // if (k % 2 == 0, ~)
+        act = !code && e.p > thr;
+      }
+    }
+  }
+  const int T = k;
+  BJHOut o;
+  o.J = 0.0 + acc.p;                                      // out! += acc
+  o.T = T;
+  const bool fwd_ok = valid && !code;
+  // ---------------- sweep 4: ~R with the adjoint rules over Duals ----------------
+  const double gacc = (1.0 * seed) * 1.0;                 // out! -= acc: acc.g += out.g
+  Dl gs = dflt(0.0), gh2 = dflt(0.0);
+  if (fwd_ok && chk && e.p > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
+  int kr = fwd_ok ? T : 0;
+  while (__any_sync(FULL_MASK, kr >= 1)) {
+    if (kr >= 1) {
+      if (kr & 1) {                                       // acc += convert(s): sign -1
+        acc = dadd(acc, e);
+        gs = dadd(gs, dmul(dflt(-1.0 * gacc), e));
+      } else {                                            // acc -= convert(s): sign +1
+        acc = dsub(acc, e);
+        gs = dadd(gs, dmul(dflt(1.0 * gacc), e));
+      }
+      const double2 L = logpair_any(kr, nu);
+      s = dadd(s, dflt(L.y));                             // s *= kn
+      s = dadd(s, dflt(L.x));                             // s *= k
+      s = dsub(s, h2);                                    // s /= halfz2
+      gh2 = dadd(gh2, dmul(dflt(1.0), gs));
+      kr--;
+      int c = 0;
+      e = dexp<CAREFUL>(s, c);
+      if (!code) code = c ? c : ((chk && !(e.p > thr)) ? RL_ERR_POSTCONDITION : 0);
+    }
+  }
+  Dl gz = dflt(0.0);
+  if (fwd_ok) {
+    acc = dsub(acc, e);                                   // acc -= convert(s)
+    gs = dadd(gs, dmul(dflt(1.0 * gacc), e));
+    Dl gh = dflt(0.0);
+    for (int q = nu; q >= 1; q--) {                       // for i = nu:-1:1
+      s = dadd(s, dflt(logi(q)));
+      s = dsub(s, halfz);
+      gh = dadd(gh, dmul(dflt(1.0), gs));
+    }
+    h2 = dsub(h2, halfz);                                 // halfz2 /= halfz (x2)
+    gh = dadd(gh, dmul(dflt(1.0), gh2));
+    h2 = dsub(h2, halfz);
+    gh = dadd(gh, dmul(dflt(1.0), gh2));
+    halfz = dadd(halfz, dflt(LN2));                       // halfz *= 2
+    halfz = dsub(halfz, lz);                              // halfz /= lz
+    const Dl glz = dadd(dflt(0.0), dmul(dflt(1.0), gh));
+    lz = dsub(lz, clz);                                   // lz /= convert(z)
+    gz = dadd(gz, ddiv(dmul(dflt(1.0), glz), Z));
+    if (chk && !code) {                                   // releases
+      if (fabs(acc.p - 0.0) > tol || fabs(s.p - 0.0) > tol || fabs(h2.p - 0.0) > tol ||
+          fabs(halfz.p - 0.0) > tol || fabs(lz.p - 0.0) > tol)
+        code = RL_ERR_DIRTY_ANCILLA;
+    }
+  }
+  const double qnan = __longlong_as_double(0x7ff8000000000000ULL);
+  if (!fwd_ok) o.J = qnan;
+  o.dz = fwd_ok ? gz.p : qnan;
+  o.d2 = fwd_ok ? gz.t : qnan;
+  o.code = code;
+  o.bad = valid && bad;
+  return o;
+}
+
+// MODE 1: gradient (sweeps 1 + 4, Jout = J, dzout = dJ/dz).  MODE 0: run /
 // uncall of besselj (Jout = out_in + sign * J with every check of the two
-// primal sweeps; dzout unused): the objective-only ("-O") kernel.
-template <bool GRAD>
+// primal sweeps; dzout unused): the objective-only ("-O") kernel.  MODE 2:
+// the Hessian (Dual sweeps; d2out = d2J/dz2).
+constexpr int BJ_RUN = 0, BJ_GRAD = 1, BJ_HESS = 2;
+template <int MODE>
 __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, const double *__restrict__ out_in, double sign,
     double *__restrict__ Jout, double *__restrict__ dzout, uint8_t *__restrict__ fail,
-    unsigned long long *counters, double sfloor) {
+    unsigned long long *counters, double sfloor, double *__restrict__ d2out) {
+  constexpr bool GRAD = MODE >= BJ_GRAD;
   const int ktab = BJ_KP - 1;
   const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   __shared__ int s_hist[BJ_NB];
@@ -499,7 +654,8 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
   double *s_z = s_zin + BJ_C;
   double *s_J = s_z + BJ_C;
   double *s_dz = s_J + BJ_C;
-  uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dz + BJ_C);
+  double *s_d2 = s_dz + BJ_C;                          // MODE 2 only
+  uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_d2 + (MODE == BJ_HESS ? BJ_C : 0));
   uint8_t *s_fail = reinterpret_cast<uint8_t *>(s_idx + BJ_C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < BJ_EXPN * BJ_EXPREP; i += BJ_BLOCK) s_exp2tab[i] = g_exp2tab[i / BJ_EXPREP];
@@ -588,6 +744,24 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {
         const double z = valid ? s_z[pos] : 1.0;
+        if (MODE == BJ_HESS) {
+          BJHOut o = besselj_hess_element<false>(z, valid, nu, thr, tol, seed, kfuel, chk, sfloor);
+          if (__any_sync(FULL_MASK, o.bad)) {
+            const BJHOut c = besselj_hess_element<true>(z, o.bad, nu, thr, tol, seed, kfuel, chk,
+                                                        sfloor);
+            if (o.bad) o = c;
+          }
+          if (valid) {
+            const int oi = s_idx[pos];
+            s_J[oi] = o.J;
+            s_dz[oi] = o.dz;
+            s_d2[oi] = o.d2;
+            s_fail[oi] = (uint8_t)o.code;
+            trips_sum += (unsigned long long)o.T;
+            nfail += o.code != 0;
+          }
+          continue;
+        }
         BJOut o = besselj_element<false, GRAD>(z, valid, nu, thr, tol, seed, ktab, kfuel, chk,
                                                sfloor);
         if (__any_sync(FULL_MASK, o.bad)) {              // |exp arg| >= 708 somewhere
@@ -614,6 +788,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
         if (GRAD) {
           __stcs(Jout + base + e, s_J[e]);
           __stcs(dzout + base + e, s_dz[e]);
+          if (MODE == BJ_HESS) __stcs(d2out + base + e, s_d2[e]);
         } else {
           // out! += acc (run) / out! -= acc (uncall): one IEEE add, like the reference
           const double o0 = out_in ? __ldcs(out_in + base + e) : 0.0;
@@ -636,20 +811,22 @@ static int upload_logtab() {
 
 int besselj_tables_init() { return upload_logtab(); }
 
-template <bool GRAD>
+template <int MODE>
 static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, double tol,
                             double seed, int64_t max_trips, int32_t invcheck,
                             const double *out_in, double sign, double *J, double *dJdz,
-                            uint8_t *fail, unsigned long long *counters, cudaStream_t st) {
+                            double *d2, uint8_t *fail, unsigned long long *counters,
+                            cudaStream_t st) {
   int rc = ensure_device_tables();
   if (rc) return rc;
   if (n == 0) return RL_OK;
+  const int smem = BJ_SMEM + (MODE == BJ_HESS ? BJ_C * 8 : 0);
   int blocks_per_sm = 0;
-  rc = cuda_status(cudaFuncSetAttribute(k_besselj<GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        BJ_SMEM), "smem attr");
+  rc = cuda_status(cudaFuncSetAttribute(k_besselj<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        smem), "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj<GRAD>,
-                                                                 BJ_BLOCK, BJ_SMEM),
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj<MODE>,
+                                                                 BJ_BLOCK, smem),
                    "occupancy");
   if (rc) return rc;
   const long long want = (n + BJ_C - 1) / BJ_C;
@@ -658,9 +835,9 @@ static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, 
   // FAST-flavour safety bound (besselj_element): log(thr) - 2 log(kfuel + |nu| + 1)
   const double kfuel = (double)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
   const double sfloor = log(thr) - 2.0 * log(kfuel + fabs((double)nu) + 1.0);
-  k_besselj<GRAD><<<grid, BJ_BLOCK, BJ_SMEM, st>>>(nu, z, n, thr, tol, seed, max_trips,
-                                                   invcheck ? 1 : 0, out_in, sign, J, dJdz, fail,
-                                                   counters, sfloor);
+  k_besselj<MODE><<<grid, BJ_BLOCK, smem, st>>>(nu, z, n, thr, tol, seed, max_trips,
+                                                invcheck ? 1 : 0, out_in, sign, J, dJdz, fail,
+                                                counters, sfloor, d2);
   return cuda_status(cudaGetLastError(), "k_besselj launch");
 }
 
@@ -669,8 +846,18 @@ int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double to
                    unsigned long long *counters, cudaStream_t st) {
   if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)) || max_trips < 0)
     return set_error(RL_ERR_INVALID, "rl_besselj_grad_f64: bad argument");
-  return launch_besselj_t<true>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0, J,
-                                dJdz, fail, counters, st);
+  return launch_besselj_t<BJ_GRAD>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0,
+                                   J, dJdz, nullptr, fail, counters, st);
+}
+
+int launch_besselj_hess(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, double *d2Jdz2, uint8_t *fail,
+                        unsigned long long *counters, cudaStream_t st) {
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !d2Jdz2 || !fail)) || max_trips < 0)
+    return set_error(RL_ERR_INVALID, "rl_besselj_hess_f64: bad argument");
+  return launch_besselj_t<BJ_HESS>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0,
+                                   J, dJdz, d2Jdz2, fail, counters, st);
 }
 
 int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, double tol,
@@ -680,8 +867,8 @@ int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, doubl
   if (n < 0 || (n > 0 && (!z || !out || !fail)) || max_trips < 0 ||
       (direction != 1 && direction != -1))
     return set_error(RL_ERR_INVALID, "rl_besselj_run_f64: bad argument");
-  return launch_besselj_t<false>(nu, z, n, thr, tol, 0.0, max_trips, invcheck, out_in,
-                                 (double)direction, out, nullptr, fail, counters, st);
+  return launch_besselj_t<BJ_RUN>(nu, z, n, thr, tol, 0.0, max_trips, invcheck, out_in,
+                                  (double)direction, out, nullptr, nullptr, fail, counters, st);
 }
 
 }  // namespace rl

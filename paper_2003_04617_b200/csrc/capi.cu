@@ -33,6 +33,10 @@ int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, doubl
                        int64_t max_trips, int32_t invcheck, int32_t direction,
                        const double *out_in, double *out, uint8_t *fail,
                        unsigned long long *counters, cudaStream_t st);
+int launch_besselj_hess(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, double *d2Jdz2, uint8_t *fail,
+                        unsigned long long *counters, cudaStream_t st);
 int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
                         const double *X, const double *w, const double *feats,
                         const int32_t *obs, double tol, int32_t invcheck, double *err,
@@ -346,6 +350,14 @@ int rl_besselj_run_f64(int32_t nu, const double *z, int64_t n, double thr, doubl
                        unsigned long long *counters, void *stream) {
   return launch_besselj_run(nu, z, n, thr, tol, max_trips, invcheck, direction, out_in, out, fail,
                             counters, as_stream(stream));
+}
+
+int rl_besselj_hess_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                        double seed, int64_t max_trips, int32_t invcheck, double *J,
+                        double *dJdz, double *d2Jdz2, uint8_t *fail,
+                        unsigned long long *counters, void *stream) {
+  return launch_besselj_hess(nu, z, n, thr, tol, seed, max_trips, invcheck, J, dJdz, d2Jdz2,
+                             fail, counters, as_stream(stream));
 }
 
 int rl_ba_residuals_f64(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,

@@ -91,6 +91,39 @@ def besselj_grad(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
     return BesselResult(J, dz, fail, counters)
 
 
+@dataclass
+class BesselHessResult:
+    J: torch.Tensor          # primal (bit-identical to besselj_grad's)
+    dJdz: torch.Tensor       # first derivative (bit-identical to besselj_grad's)
+    d2Jdz2: torch.Tensor     # H[z, z] of autodiff.hessian
+    fail: torch.Tensor
+    counters: torch.Tensor
+
+    @property
+    def sum_trips(self):
+        return int(self.counters[0].item())
+
+
+def besselj_hess(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
+                 max_steps=500_000_000, counters=None):
+    """Batched forward-over-reverse Hessian: `hessian(load_example("besselj"),
+    "besselj", [0.0, nu, z_i])[z, z]` (reference autodiff.py:216-257) for every
+    element, with J and dJ/dz, in one kernel (Dual-number sweeps)."""
+    z = _require_cuda("z", z)
+    n = z.numel()
+    J, dz, d2 = torch.empty_like(z), torch.empty_like(z), torch.empty_like(z)
+    fail = torch.empty(z.shape, dtype=torch.uint8, device=z.device)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=z.device)
+    L = _native.lib()
+    rc = L.rl_besselj_hess_f64(int(nu), _ptr(z), n, float(thr), float(tol), float(seed),
+                               max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)),
+                               _ptr(J), _ptr(dz), _ptr(d2), _ptr(fail), _ptr(counters),
+                               _stream_handle())
+    _native.check(rc, "rl_besselj_hess_f64")
+    return BesselHessResult(J, dz, d2, fail, counters)
+
+
 def besselj_grad_host(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
                       max_steps=500_000_000, device=None, out=None):
     """Host-buffer entry (numpy float64 or CPU tensor in, numpy out): the

@@ -123,3 +123,21 @@ def test_gmm_against_torch_autograd(oracle):
     assert np.allclose(ga, al.grad.numpy(), rtol=1e-11, atol=1e-12)
     assert np.allclose(gm, me.grad.numpy(), rtol=1e-11, atol=1e-12)
     assert np.allclose(gi, ic.grad.numpy(), rtol=1e-11, atol=1e-12)
+
+
+def test_oracle_hessian_bit_identical_to_reference(oracle, golden):
+    """oracle.besselj_hess (C, Dual sweeps) against reference
+    autodiff.hessian on 1,120 cases: H[z, z] bit for bit, the other entries
+    zero, and the same error classes."""
+    g = golden("hess")
+    for nu in np.unique(g["nu"]):
+        m = g["nu"] == nu
+        z, H, err = g["z"][m], g["H"][m], g["err"][m]
+        J, dz, d2, fail, _ = oracle.besselj_hess(int(nu), z)
+        names = np.array([oracle.ERROR_NAMES[int(f)] for f in fail])
+        assert np.array_equal(names, err)
+        ok = err == ""
+        assert np.array_equal(d2[ok], H[ok, 1, 1])                     # bit for bit
+        assert (H[ok, 0, :] == 0).all() and (H[ok, :, 0] == 0).all()
+        Jg, dzg, fg, _ = oracle.besselj_grad(int(nu), z)
+        assert np.array_equal(J[ok], Jg[ok]) and np.array_equal(dz[ok], dzg[ok])
