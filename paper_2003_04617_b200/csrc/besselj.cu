@@ -270,7 +270,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   double s = 0.0;
   for (int q = 1; q <= nu; q++) {                        // for i = 1:1:nu
     s = s + halfz;
-    s = s - logi(q);
+    s = s - (q < BJ_KP ? s_logpair[q].x : logi(q));
   }
   asm volatile("" : "+d"(h2));  // keep h2 live: no per-trip rematerialisation
   double t, acc;
@@ -452,7 +452,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     if (GRAD) sg = sg + (1.0 * accg) * t;
     double hzg = 0.0;
     for (int q = nu; q >= 1; q--) {                      // for i = nu:-1:1
-      s = s + logi(q);
+      s = s + (q < BJ_KP ? s_logpair[q].x : logi(q));
       s = s - halfz;
       hzg = hzg + 1.0 * sg;
     }
@@ -732,13 +732,16 @@ __global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
     __syncthreads();
     // 4. rounds of 32 z-neighbours, handed out dynamically from the largest z
     //    down (longest first), so the block's warps reach the barrier together
+    //    (the next round's ticket is drawn one round ahead, off the
+    //    critical path)
     const int nrounds = (cnt + 31) >> 5;
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(&s_round, 1);
 #pragma unroll 1
     for (;;) {
-      int got = 0;
-      if (lane == 0) got = atomicAdd(&s_round, 1);
-      got = __shfl_sync(FULL_MASK, got, 0);
+      const int got = __shfl_sync(FULL_MASK, ticket, 0);
       if (got >= nrounds) break;
+      if (lane == 0) ticket = atomicAdd(&s_round, 1);
       const int r = nrounds - 1 - got;
       const int pos = r * 32 + lane;
       const bool valid = pos < cnt;
