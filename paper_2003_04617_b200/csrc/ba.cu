@@ -60,6 +60,7 @@ constexpr int BA_BLOCK = BA_BLOCK_SZ;
 constexpr int BA_ROW = 31;
 constexpr int BA_STAGE = 17;       // staged inputs per observation: cam 11, X 3, w, feat 2
 constexpr int BA_SMEM = (BA_ROW + BA_STAGE) * BA_BLOCK * 8;   // dynamic smem per block
+constexpr int BA_SMEM_CSR = BA_SMEM + (31 + 3) * BA_BLOCK * 4;  // + int32 cols / row pointers
 
 // GRAD: the Jacobian (sweeps 1 + 4 with two cotangent lanes).  !GRAD: run
 // of ba_proj / ba_weight on zero outputs — the residuals [e1, e2, 1 - w^2]
@@ -89,7 +90,6 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
   extern __shared__ __align__(16) double ba_dyn[];
   double *tile = ba_dyn;
   double *stage = ba_dyn + BA_BLOCK * BA_ROW;
-  __shared__ int2 otile[CSR ? BA_BLOCK : 1];
   unsigned long long nfail = 0;
   const long long stride = (long long)gridDim.x * BA_BLOCK;
   const int tid = threadIdx.x;
@@ -485,50 +485,77 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
     // whole tile (the block's rows are one contiguous run of J), issued by
     // one thread and overlapping the next observation's compute; otherwise
     // (CSR, a partial block, misaligned J) coalesced 16-byte stores
-    if (!CSR && tid == 0)                  // previous bulk store has read the tile
+    if (tid == 0)                          // previous bulk stores have read the tile
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();
-    if (valid) {
-#pragma unroll
-      for (int j = 0; j < BA_ROW; j++) tile[threadIdx.x * BA_ROW + j] = row[j];
-      if (CSR) otile[threadIdx.x] = in_range ? o : make_int2(-1, -1);
-    }
     __syncthreads();
     const long long rows = n_obs - blk0 < BA_BLOCK ? n_obs - blk0 : BA_BLOCK;
     if (CSR) {
       // ADBench BASparseMat::insert_reproj_err_block order: per observation two
       // rows of 15 (cam 11 | point 3 | weight 1), then all weight rows
-      // (insert_w_err_block) after the 2P reprojection rows.
-      const int nr = (int)rows * 30;
-      double *dv = csr.vals + blk0 * 30;
-      int32_t *dc = csr.cols ? csr.cols + blk0 * 30 : nullptr;
-      for (int k = threadIdx.x; k < nr; k += BA_BLOCK) {
-        const int ob = k / 30, j = k - 30 * ob;
-        dv[k] = tile[ob * BA_ROW + j];
-        if (dc) {
-          const int jj = j < 15 ? j : j - 15;
-          const int2 o = otile[ob];
-          int col;
-          if (jj < 11) col = o.x < 0 ? -1 : 11 * o.x + jj;
-          else if (jj < 14) col = o.y < 0 ? -1 : csr.col_pt + 3 * o.y + (jj - 11);
-          else col = csr.col_w + (int)(csr.off + blk0 + ob);
-          dc[k] = col;
-        }
-      }
-      if (threadIdx.x < rows) {
-        const long long t = blk0 + threadIdx.x;           // local observation
-        const long long g = csr.off + t;                   // global observation
-        csr.vals[n_obs * 30 + t] = tile[threadIdx.x * BA_ROW + 30];
+      // (insert_w_err_block) after the 2P reprojection rows.  The block's
+      // values, column indices and row pointers are staged in shared memory
+      // in their CSR order (each piece one contiguous run of the output) and
+      // leave as bulk stores where the run is 16-byte aligned and sized.
+      double *vA = tile, *vW = tile + BA_BLOCK * 30;
+      int32_t *cA = reinterpret_cast<int32_t *>(tile + BA_BLOCK * BA_ROW + BA_BLOCK * BA_STAGE);
+      int32_t *cW = cA + BA_BLOCK * 30, *rA = cW + BA_BLOCK, *rW = rA + 2 * BA_BLOCK;
+      if (valid) {
+        const long long g = csr.off + i;                   // global observation
+#pragma unroll
+        for (int j = 0; j < 30; j++) vA[tid * 30 + j] = row[j];
+        vW[tid] = row[30];
         if (csr.cols) {
-          csr.cols[n_obs * 30 + t] = csr.col_w + (int)g;
-          csr.rows[2 * t] = (int32_t)(30 * g);
-          csr.rows[2 * t + 1] = (int32_t)(30 * g + 15);
-          csr.rows[2 * n_obs + t] = (int32_t)(30 * csr.P + g);
-          if (t == n_obs - 1) csr.rows[3 * n_obs] = (int32_t)(30 * csr.P + g + 1);
+          const int cc = in_range ? 11 * o.x : -1, cp = in_range ? csr.col_pt + 3 * o.y : -1;
+          const int cw = csr.col_w + (int)g;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+#pragma unroll
+            for (int j = 0; j < 11; j++) cA[tid * 30 + 15 * h + j] = cc < 0 ? -1 : cc + j;
+#pragma unroll
+            for (int j = 0; j < 3; j++) cA[tid * 30 + 15 * h + 11 + j] = cp < 0 ? -1 : cp + j;
+            cA[tid * 30 + 15 * h + 14] = cw;
+          }
+          cW[tid] = cw;
+          rA[2 * tid] = (int32_t)(30 * g);
+          rA[2 * tid + 1] = (int32_t)(30 * g + 15);
+          rW[tid] = (int32_t)(30 * csr.P + g);
+          if (i == n_obs - 1) csr.rows[3 * n_obs] = (int32_t)(30 * csr.P + g + 1);
         }
       }
+      __syncthreads();
+      const int nr = (int)rows;
+      auto put = [&](void *dst, const void *src, int bytes, int esz) {
+        // bulk store when 16-byte aligned and sized, else a cooperative copy
+        if (((reinterpret_cast<uintptr_t>(dst) | (unsigned)bytes) & 15) == 0) {
+          if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes) : "memory");
+          }
+        } else if (esz == 8) {
+          for (int k = tid; k < bytes / 8; k += BA_BLOCK)
+            static_cast<double *>(dst)[k] = static_cast<const double *>(src)[k];
+        } else {
+          for (int k = tid; k < bytes / 4; k += BA_BLOCK)
+            static_cast<int32_t *>(dst)[k] = static_cast<const int32_t *>(src)[k];
+        }
+      };
+      put(csr.vals + blk0 * 30, vA, nr * 240, 8);
+      put(csr.vals + n_obs * 30 + blk0, vW, nr * 8, 8);
+      if (csr.cols) {
+        put(csr.cols + blk0 * 30, cA, nr * 120, 4);
+        put(csr.cols + n_obs * 30 + blk0, cW, nr * 4, 4);
+        put(csr.rows + 2 * blk0, rA, nr * 8, 4);
+        put(csr.rows + 2 * n_obs + blk0, rW, nr * 4, 4);
+      }
+      if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       continue;
     }
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < BA_ROW; j++) tile[threadIdx.x * BA_ROW + j] = row[j];
+    }
+    __syncthreads();
     const int nd = (int)rows * BA_ROW;
     double *dst = J_out + blk0 * BA_ROW;
     if (rows == BA_BLOCK && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -548,7 +575,7 @@ __global__ void __launch_bounds__(BA_BLOCK, BA_MINB) k_ba_jac(
       for (int k = threadIdx.x; k < nd; k += BA_BLOCK) dst[k] = tile[k];
     }
   }
-  if (!CSR && GRAD && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (GRAD && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   block_add_counters<BA_BLOCK>(0, nfail, counters);
 }
 
@@ -638,17 +665,17 @@ int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offs
   }
   auto kern = err ? k_ba_jac<true, false, true, true> : k_ba_jac<false, false, true, true>;
   int bps = 0;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
+  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM_CSR),
                    "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
+  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM_CSR),
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
   long long cap = (long long)sm_count() * (bps > 0 ? bps : 1);
   int grid = (int)(want < cap ? want : cap);
   BaCsr csr{rows, cols, vals, obs_offset, n_obs_total, 11 * n_cams, 11 * n_cams + 3 * n_pts};
-  kern<<<grid, BA_BLOCK, BA_SMEM, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
+  kern<<<grid, BA_BLOCK, BA_SMEM_CSR, st>>>(n_cams, n_pts, n_obs, cams, X, w, feats,
                                   reinterpret_cast<const int2 *>(obs), tol, invcheck ? 1 : 0, err,
                                   nullptr, nullptr, fail, counters, csr);
   return cuda_status(cudaGetLastError(), "k_ba_jac (csr) launch");
