@@ -210,6 +210,11 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16z(void *smem, const void *gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -227,16 +232,27 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
 }
 
 // issue the async copy of tile [p0, p0 + TP) of x into xs ([TP][XS]; rows
-// past N are zero-filled, padding columns d..DP-1 are never written)
+// past N are zero-filled, padding columns d..DP-1 are never written).  The
+// loop runs over the compile-time-padded [TP][DP/2] grid of column pairs
+// (shift / mask indexing, no division by the runtime d); pairs move as one
+// 16-byte copy when the rows are 16-byte aligned (d even).
 template <int DP, int TP>
 __device__ __forceinline__ void load_x_async(double *__restrict__ xs, const double *__restrict__ x,
                                              int d, long long p0, long long N) {
   using C = GmmCfg<DP, TP>;
-  const int tot = TP * d;
-  for (int e = threadIdx.x; e < tot; e += GMM_THREADS) {
-    const int p = e / d, a = e - p * d;
+  const bool vec = !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
+  for (int e = threadIdx.x; e < TP * (DP / 2); e += GMM_THREADS) {
+    const int p = e / (DP / 2), a = 2 * (e % (DP / 2));
+    if (a >= d) continue;
     const bool in = p0 + p < N;
-    cp_async8(xs + p * C::XS + a, x + (in ? (p0 + p) * d + a : 0), in ? 8 : 0);
+    const double *src = x + (in ? (p0 + p) * d + a : 0);
+    double *dst = xs + p * C::XS + a;
+    if (vec) {
+      cp_async16z(dst, src, in ? 16 : 0);
+    } else {
+      cp_async8(dst, src, in ? 8 : 0);
+      if (a + 1 < d) cp_async8(dst + 1, src + (in ? 1 : 0), in ? 8 : 0);
+    }
   }
 }
 
@@ -288,13 +304,15 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
 }
 
 // xc[j] += x[i, j] - means[k, j], formed once per tile in shared memory
-// (padding columns hold 0 - 0; rows past N are discarded downstream)
+// over all DP columns (padding columns hold 0 - 0; rows past N are
+// discarded downstream); shift / mask indexing
 template <int DP, int TP>
 __device__ __forceinline__ void center_tile(double *__restrict__ xs, const double *__restrict__ mu,
-                                            int d) {
+                                            int) {
   using C = GmmCfg<DP, TP>;
-  for (int e = threadIdx.x; e < TP * d; e += GMM_THREADS) {
-    const int p = e / d, a = e - p * d;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < TP * DP; e += GMM_THREADS) {
+    const int p = e / DP, a = e % DP;
     xs[p * C::XS + a] = xs[p * C::XS + a] - mu[a];
   }
 }
