@@ -254,6 +254,17 @@ def fp64_peak_tflops():
     return best, float(ms.value)
 
 
+def dmma_peak_tflops():
+    """In-run FP64 tensor-core (DMMA mma.sync.m16n8k16.f64) microkernel: the
+    peak of the unit GMM's tile products run on (tools/fp64probe.cu)."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(REPO, "tools", "libfp64probe.so"))
+    lib.probe_dmma_peak.restype = ctypes.c_double
+    lib.probe_dmma_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+    ms = ctypes.c_float(0)
+    return max(lib.probe_dmma_peak(1, 2000, ctypes.byref(ms)) for _ in range(3))
+
+
 # ---------------------------------------------------------------------------
 # Bessel workload (configs[1])
 # ---------------------------------------------------------------------------
@@ -711,7 +722,11 @@ def run_gmm_ours(args, D):
     ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     ms_step = D.max(ms)
     w = load_weights()
-    peak, _ = fp64_peak_tflops()
+    # GMM's mat-vec work runs on the FP64 tensor cores: the roofline peak is
+    # the larger of the measured DMMA and DFMA peaks (the DMMA one)
+    dfma, _ = fp64_peak_tflops()
+    dmma = dmma_peak_tflops()
+    peak = max(dfma, dmma)
     roof = None
     if w is not None:
         fl = gmm_flops(d, K, N, w)
@@ -723,7 +738,8 @@ def run_gmm_ours(args, D):
                 "flops_per_eval_survey_W": fl,
                 "mat_vec_flops_executed": executed,
                 "executed_frac": round(executed / (ms_step * 1e-3) / 1e12 / peak, 4),
-                "peak_source": "in-run DFMA microkernel (tools/fp64probe.cu)"}
+                "peak_source": "max of in-run DMMA m16n8k16 (%.1f TF) and DFMA (%.1f TF) "
+                               "microkernels (tools/fp64probe.cu)" % (dmma, dfma)}
     o_ms = D.max(time_device(
         lambda: kernels.gmm_objective(alphas, means, icf, x, gamma, m, cst, N_total=N,
                                       add_param_terms=(D.rank == 0), workspace=ws),
