@@ -645,7 +645,7 @@ int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offs
                   unsigned long long *counters, cudaStream_t st) {
   if (n_obs < 0 || n_cams < 0 || n_pts < 0 || obs_offset < 0 || n_obs_total < obs_offset + n_obs ||
       (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !vals || !fail)) ||
-      ((rows == nullptr) != (cols == nullptr)))
+      (cols && !rows) || (rows && !cols && n_obs > 0))
     return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64: bad argument");
   // BASparseMat holds int row pointers / column indices
   const long long ncols = 11LL * n_cams + 3LL * n_pts + n_obs_total;

@@ -382,7 +382,7 @@ int rl_ba_jac_csr_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const d
                            const int32_t *obs, double tol, int32_t invcheck, int32_t *rows,
                            int32_t *cols, double *vals, uint8_t *fail,
                            unsigned long long *n_failed, int32_t device) {
-  if (n_obs < 0 || n_cams < 0 || n_pts < 0 || !vals || ((rows == nullptr) != (cols == nullptr)) ||
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 || !vals || (cols && !rows) || (rows && !cols && n_obs > 0) ||
       (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !fail)))
     return set_error(RL_ERR_INVALID, "rl_ba_jac_csr_f64_host: bad argument");
   if (31LL * n_obs > INT32_MAX || 11LL * n_cams + 3LL * n_pts + n_obs > INT32_MAX)

@@ -400,11 +400,12 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
 // ---------------------------------------------------------------------------
 // per point: reversible argmax + logsumexp, forward then reverse with adjoints
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
+constexpr int LSE_THREADS = 64;   // points per k_gmm_lse block: N/64 blocks spread over the SMs
+__global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
-  const long long i = (long long)blockIdx.x * GMM_THREADS + threadIdx.x;
+  const long long i = (long long)blockIdx.x * LSE_THREADS + threadIdx.x;
   double e_pt = 0.0;
   unsigned long long nfail = 0;
   if (i < N) {
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
     // postconditions replay the same comparisons, so they cannot fail.
     int imx = 0;
     double vmx = MT(0);
+#pragma unroll 4
     for (int k = 1; k < K; k++) {
       const double v = MT(k);
       if (v > vmx) {
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
     }
     const double mx = 0.0 + vmx;                          // mx <- 0.0; mx += mt![imx]
     double se = 0.0;
+#pragma unroll 4
     for (int k = 0; k < K; k++) {
       const double t = 0.0 + (MT(k) - mx);
       se = se + exp(t);
@@ -436,6 +439,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
     // gradient sweep (~f): err -= mx; err -= log(se); ~R_i with adjoints
     double mxg = 0.0 + (1.0 * 1.0) * 1.0;
     const double seg = 0.0 + (1.0 * 1.0) * (1.0 / se);
+#pragma unroll 4
     for (int k = K - 1; k >= 0; k--) {
       double t = 0.0 + (MT(k) - mx);
       const double ex = exp(t);
@@ -457,15 +461,15 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_lse(
     nfail = code != 0;
   }
   // deterministic block sum of the per-point objective terms
-  __shared__ double red[GMM_THREADS];
+  __shared__ double red[LSE_THREADS];
   red[threadIdx.x] = e_pt;
   __syncthreads();
-  for (int o = GMM_THREADS / 2; o > 0; o >>= 1) {
+  for (int o = LSE_THREADS / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
   if (threadIdx.x == 0) err_part[blockIdx.x] = red[0];
-  block_add_counters<GMM_THREADS>(0, nfail, counters);
+  block_add_counters<LSE_THREADS>(0, nfail, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -869,7 +873,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
   L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * rev_per_sm(DP), smax);
-  L.nerr = (int)((N + GMM_THREADS - 1) / GMM_THREADS);
+  L.nerr = (int)((N + LSE_THREADS - 1) / LSE_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -944,7 +948,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     k_gmm_fwd<DP, TPF><<<dim3(K, L.Sf), GMM_THREADS, sf, st>>>(d, K, N, alphas, means, x, LT, sq,
                                                                tol, chk, mt, flags);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_fwd"))) return rc;
-    k_gmm_lse<<<L.nerr, GMM_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
+    k_gmm_lse<<<L.nerr, LSE_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
                                               counters);
     if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
     if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
