@@ -47,6 +47,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="GMM: launch the step's kernels directly instead of as a CUDA graph")
     ap.add_argument("--workload", choices=["bessel", "ba", "gmm", "gmm_large"], default="bessel")
     ap.add_argument("--n", type=int, default=None, help="override the batch size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -703,6 +705,16 @@ def run_gmm_ours(args, D):
     for _ in range(max(args.warmup, 3)):
         r = step()
     torch.cuda.synchronize()
+    # the step's launches (prep, memset, fwd, lse, rev, reduce, final) are
+    # replayed as one CUDA graph: no per-launch host latency between them
+    graph = None
+    if not args.no_graph and D.dist is None:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            r = step()
+        graph.replay()
+        torch.cuda.synchronize()
+    run_step = graph.replay if graph is not None else step
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
@@ -714,7 +726,7 @@ def run_gmm_ours(args, D):
     for a, b in evs:
         flush.fill_(1)                      # evict L2 between evaluations
         a.record(stream)
-        r = step()
+        run_step()
         b.record(stream)
     torch.cuda.synchronize()
     D.barrier()
@@ -768,6 +780,7 @@ def run_gmm_ours(args, D):
         "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic alphas~N(0,1), means~U(0,1), icf~N(0,.5^2), x~U(0,1), seed {seed}",
         "config": {"workload": f"gmm_d{d}_K{K}_N{N}", "d": d, "K": K, "N": N,
+                   "cuda_graph": graph is not None,
                    "per_rank": hi - lo, "parallelism": f"dp{D.world}+allreduce",
                    "l2": "256 MiB L2 flush before every evaluation"},
         "roofline": roof, "gpu_launches": 6 * args.steps, "clocks": clocks,
