@@ -51,6 +51,9 @@ namespace rl {
 #ifndef GMM_REV_MINB
 #define GMM_REV_MINB 2     // reverse CTAs per SM (launch bounds) for DP <= 64
 #endif
+#ifndef GMM_SPLIT_HYST
+#define GMM_SPLIT_HYST 0.03  // wave-efficiency gain needed to take a larger point split (measured)
+#endif
 #ifndef GMM_TPF
 #define GMM_TPF 64         // forward tile (points) for DP = 64
 #endif
@@ -842,7 +845,7 @@ static int choose_split(int K, long long ntiles, int slots, int smax) {
     const long long waves = (items + slots - 1) / slots;
     const double eff = (double)items / (double)(waves * slots);
     // prefer fuller waves; among near-equal, fewer partials
-    if (eff > best_eff + 0.02) {
+    if (eff > best_eff + GMM_SPLIT_HYST) {
       best_eff = eff;
       best = S;
     }
