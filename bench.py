@@ -76,7 +76,12 @@ class Dist:
         self.torch = torch
         if self.dist is not None:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend)
+            if backend == "nccl" and torch.cuda.is_available():
+                # bind this rank to its GPU before the communicator is created
+                torch.cuda.set_device(self.local)
+                dist.init_process_group(backend, device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(backend)
 
     def barrier(self):
         if self.dist is not None:
@@ -861,6 +866,9 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
+        # all host threads for the oracle port (torchrun exports OMP_NUM_THREADS=1;
+        # libgomp reads it when liboracle.so loads, which happens below)
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
         if args.workload == "gmm_large":
             print(json.dumps({"impl": "reference", "unavailable":
                               "configs[4] on the sequential CPU oracle is ~13 core-years per "
