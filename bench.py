@@ -813,7 +813,7 @@ def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
     L = _native.lib()
     K, d = means.shape
     N = x.shape[0]
-    ha, hm, hi_ = alphas.cpu(), means.cpu(), icf.cpu()
+    ha, hm, hi_ = alphas.cpu().pin_memory(), means.cpu().pin_memory(), icf.cpu().pin_memory()
     hx = x.cpu().pin_memory()
     out = torch.empty(1 + K + K * d + K * d * (d + 1) // 2, dtype=torch.float64).pin_memory()
     nf = ctypes.c_ulonglong()
@@ -832,7 +832,8 @@ def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
     return {"value": round(1.0 / dt, 3), "unit": "evals/s",
             "h2d_bytes_per_step": int(hx.numel() * 8 + (ha.numel() + hm.numel() + hi_.numel()) * 8),
             "d2h_bytes_per_step": int(out.numel() * 8), "ms_per_step": round(dt * 1e3, 3),
-            "path": "rl_gmm_grad_f64_host (host buffers; allocates its device workspace per call)"}
+            "path": "rl_gmm_grad_f64_host (pinned host buffers; device buffers and workspace "
+                    "from the stream-ordered pool, cached streams)"}
 
 
 def gmm_cpu(workload):

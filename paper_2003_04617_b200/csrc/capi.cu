@@ -112,24 +112,34 @@ struct DevBuf {
 };
 
 struct Pipeline {
+  // The three streams of the host-buffer entries are created once per
+  // (host thread, device) and reused by every call: creating and destroying
+  // streams per call cost more than a small GMM evaluation.
   static constexpr int NS = 3;
   cudaStream_t st[NS] = {nullptr, nullptr, nullptr};
   int dev_prev = -1;
   int init(int device) {
     cudaGetDevice(&dev_prev);
+    if (device < 0 || device >= MAX_DEV) return set_error(RL_ERR_INVALID, "bad device ordinal");
     int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
     if (rc) return rc;
-    // keep freed stream-ordered allocations in the pool between calls (the
-    // default threshold 0 returns them to the driver at every sync)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    static thread_local cudaStream_t cache[MAX_DEV][NS];
+    static thread_local bool made[MAX_DEV];
+    if (!made[device]) {
+      // keep freed stream-ordered allocations in the pool between calls (the
+      // default threshold 0 returns them to the driver at every sync)
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      for (auto &s : cache[device]) {
+        rc = cuda_status(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+        if (rc) return rc;
+      }
+      made[device] = true;
     }
-    for (auto &s : st) {
-      rc = cuda_status(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
-      if (rc) return rc;
-    }
+    for (int i = 0; i < NS; i++) st[i] = cache[device][i];
     return RL_OK;
   }
   int finish() {
@@ -143,10 +153,7 @@ struct Pipeline {
   }
   ~Pipeline() {
     for (auto &s : st)
-      if (s) {
-        cudaStreamSynchronize(s);
-        cudaStreamDestroy(s);
-      }
+      if (s) cudaStreamSynchronize(s);
     if (dev_prev >= 0) cudaSetDevice(dev_prev);
   }
 };
