@@ -545,9 +545,14 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
   cp_commit();
   int buf = 0;
+  // Three barriers per tile: the next tile's prefetch is issued after the
+  // top barrier (whose arrival means every warp has finished reading that
+  // buffer in the previous tile's M product), so no end-of-tile barrier.
   for (; tile < ntiles; tile += gridDim.y) {
     const long long p0 = tile * TP;
     const long long nxt = tile + gridDim.y;
+    cp_wait<0>();                                         // this tile's x (own copies)
+    __syncthreads();
     if (nxt < ntiles) load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
     cp_commit();
     for (int p = tid; p < TP; p += GMM_THREADS) {
@@ -556,8 +561,6 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
       sgm += g;                                           // alphas.g, sq.g += mt.g
       cg[p] = 0.0 + (-1.0 * g) * 0.5;                     // mt += sqn*0.5: sqn.g += -mt.g/2
     }
-    cp_wait<1>();
-    __syncthreads();
     double *xs = buf ? xs1 : xs0;
     center_tile<DP, TP>(xs, mu, d);
     __syncthreads();
@@ -604,7 +607,6 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
         dmma16816(M[q], af, bf);
       }
     }
-    __syncthreads();
     buf ^= 1;
   }
   cp_wait<0>();
