@@ -206,7 +206,7 @@ __device__ __forceinline__ void fwd_trip(int k, int nu, double h2, double thr, b
 // into `ok` (one predicated compare), which the caller turns into the
 // reference's PostconditionMismatch after the loop — the same first-failure
 // result, since no other check can fire in between.
-template <bool CAREFUL, bool TAB, bool PRED, int ODD, bool GRAD = true>
+template <bool CAREFUL, bool TAB, bool PRED, int ODD, bool GRAD = true, bool UNIT = false>
 __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, double paccg,
                                          double naccg, int chk, bool live, int T, double &acc,
                                          double &sg, double &s, double &h2g, double &t,
@@ -216,7 +216,8 @@ __device__ __forceinline__ void rev_trip(int k, int nu, double h2, double thr, d
   // inverse if: odd k: acc += convert(s) (sign -1); even: acc -= convert(s)
   const bool odd = ODD == 1 || (ODD < 0 && (k & 1));
   const double an = odd ? acc + t : acc - t;
-  const double sgn = GRAD ? sg + (odd ? naccg : paccg) * t : 0.0;
+  // UNIT (acc.g == 1.0 exactly): (+-1.0) * t == +-t, so sg +- t is the same sum
+  const double sgn = !GRAD ? 0.0 : UNIT ? (odd ? sg - t : sg + t) : sg + (odd ? naccg : paccg) * t;
   double sn = s + l2;                                    // s *= kn
   sn = sn + l1;                                          // s *= k
   sn = sn - h2;                                          // s /= halfz2
@@ -436,6 +437,14 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
                                       s, h2g, t, code, ok);
   }
 #endif
+  if (accg == 1.0) {                                     // the default seed (uniform branch)
+    for (; kr >= 2; kr -= 2) {                           // main: every live lane active
+      rev_trip<CAREFUL, true, false, 1, GRAD, true>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T,
+                                                    acc, sg, s, h2g, t, code, ok);
+      rev_trip<CAREFUL, true, false, 0, GRAD, true>(kr - 1, nu, h2, thr, paccg, naccg, chk, fwd_ok,
+                                                    T, acc, sg, s, h2g, t, code, ok);
+    }
+  }
   for (; kr >= 2; kr -= 2) {                             // main: every live lane active
     rev_trip<CAREFUL, true, false, 1, GRAD>(kr, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, ok);
