@@ -14,7 +14,8 @@ plus the batched device API over torch CUDA tensors:
   helpers in parallel.py.
 """
 
-from .autodiff import ExecOptions, GradRequest, HessianResult, gradient, hessian, jacobian
+from .autodiff import (ExecOptions, GradRequest, HessianResult, gradient, gradient_batch,
+                       hessian, jacobian)
 from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
@@ -27,7 +28,7 @@ from .programs import CATALOG, Program, entry_function, load_example, parse_prog
 from .values import Array
 
 __all__ = [
-    "HessianResult", "hessian", "BesselHessResult", "besselj_hess",
+    "HessianResult", "hessian", "gradient_batch", "BesselHessResult", "besselj_hess",
     "AliasedArguments", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",

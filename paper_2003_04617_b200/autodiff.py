@@ -385,3 +385,120 @@ def hessian(program, fname, args, opts=None):
         H[leaves.index(2), leaves.index(2)] = float(r.d2Jdz2[0].item())
     sym_err = float(np.max(np.abs(H - H.T))) if n else 0.0
     return HessianResult(H, sym_err)
+
+
+# ---------------------------------------------------------------------------
+# gradient_batch: the batched facade over the device kernels
+# ---------------------------------------------------------------------------
+
+def _batch_tensor(inputs, name, n=None, shape=(), default=None, dev=None):
+    v = inputs.get(name, default)
+    if v is None:
+        raise KindError(f"gradient_batch: missing input {name!r}")
+    if not isinstance(v, torch.Tensor):
+        t = torch.as_tensor(v, dtype=torch.float64, device=dev)
+        return t.expand((n,) + shape).contiguous() if t.dim() == 0 else t
+    if not v.is_cuda or v.dtype != torch.float64:
+        raise KindError(f"gradient_batch: {name!r} must be a CUDA float64 tensor")
+    return v.contiguous()
+
+
+def gradient_batch(program, fname, inputs, seeds=None, wrt=None, opts=None, return_codes=False):
+    """Batched `gradient` (SURVEY.md §8(b) "Signatures to keep"): every entry
+    of `inputs` (param name -> CUDA float64 tensor with a leading batch
+    dimension, or a scalar broadcast to all rows; Int parameters such as
+    besselj's nu are plain ints) supplies row i of the arguments, and row i of
+    the returned tensors equals `gradient(program, GradRequest(fname, args_i,
+    seeds, wrt))` (same kernels, same arithmetic).  Returns (primal: dict,
+    grads: dict, restored: BoolTensor); no per-row exception is raised —
+    restored[i] is False where row i's reference call would raise, and with
+    `return_codes` a 4th value carries the revlang error code per row
+    (errors.CODE_NAMES).  besselj, ba_proj and ba_weight; gmm is one
+    evaluation over all points (use gradient / gmm_grad)."""
+    opts = _check_opts(opts)
+    fdef = _resolve(program, fname)
+    names = fdef.param_names()
+    h = fdef.kernel.handler
+    dev = _device()
+    seedmap = _seed_map(seeds, names, names[0])
+    for (p, path) in seedmap:
+        if path:
+            raise KindError("gradient_batch seeds address whole (scalar or per-row) leaves")
+    if h == "besselj":
+        nu = inputs.get(names[1])
+        if isinstance(nu, torch.Tensor):
+            if nu.numel() == 0 or not bool((nu == nu.flatten()[0]).all()):
+                raise KindError("gradient_batch: besselj's nu must be one Int for the batch")
+            nu = int(nu.flatten()[0].item())
+        if not _is_int(nu):
+            raise KindError("nu must be an Int")
+        z = _batch_tensor(inputs, names[2], dev=dev)
+        n = z.shape[0]
+        out0 = _batch_tensor(inputs, names[0], n, default=0.0, dev=dev)
+        a, zs = seedmap.get((names[0], ()), 0.0), seedmap.get((names[2], ()), 0.0)
+        r = kernels.besselj_grad(z, int(nu), seed=a, thr=fdef.constants.get("thr", 1e-16),
+                                 tol=opts.float_tolerance, invcheck=opts.invcheck,
+                                 max_steps=opts.max_steps)
+        out = out0 + r.J
+        code = r.fail.to(torch.int32)
+        rest = ((out - r.J) - out0).abs() <= opts.float_tolerance    # autodiff.py:169-172
+        code = torch.where((code == 0) & ~rest, torch.full_like(code, 5), code)
+        primal = {names[0]: out, names[1]: int(nu), names[2]: z}
+        grads_all = {names[0]: torch.full_like(z, a), names[2]: zs + r.dJdz}
+    elif h in ("ba_proj", "ba_weight"):
+        if h == "ba_proj":
+            w = _batch_tensor(inputs, names[4], dev=dev)
+            n = w.shape[0]
+            cam = _batch_tensor(inputs, names[2], n, (11,), dev=dev)
+            X = _batch_tensor(inputs, names[3], n, (3,), dev=dev)
+            f1 = _batch_tensor(inputs, names[5], n, dev=dev)
+            f2 = _batch_tensor(inputs, names[6], n, dev=dev)
+            if cam.shape != (n, 11) or X.shape != (n, 3):
+                raise KindError("cam must be (n, 11) and X (n, 3)")
+            idx = torch.arange(n, dtype=torch.int32, device=dev)
+            obs = torch.stack([idx, idx], 1).contiguous()
+            feats = torch.stack([f1, f2], 1).contiguous()
+        else:
+            w = _batch_tensor(inputs, names[1], dev=dev)
+            n = w.shape[0]
+            cam = torch.zeros((1, 11), dtype=torch.float64, device=dev)
+            cam[0, 6] = 1.0
+            X = torch.tensor([[0.0, 0.0, 1.0]], dtype=torch.float64, device=dev)
+            obs = torch.zeros((n, 2), dtype=torch.int32, device=dev)
+            feats = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+        r = kernels.ba_jacobian(cam, X, w, feats, obs, tol=opts.float_tolerance,
+                                invcheck=opts.invcheck, want_err=True, want_feat=True)
+        code = r.fail.to(torch.int32)
+        J, Jf, err = r.J, r.Jfeat, r.err
+        if h == "ba_proj":
+            a = seedmap.get((names[0], ()), 0.0)
+            b = seedmap.get((names[1], ()), 0.0)
+            g15 = a * J[:, 0:15] + b * J[:, 15:30]
+            gcam, gX, gw = g15[:, 0:11].clone(), g15[:, 11:14].clone(), g15[:, 14].clone()
+            gf1 = a * Jf[:, 0] + b * Jf[:, 2]
+            gf2 = a * Jf[:, 1] + b * Jf[:, 3]
+            extra = {names[4]: gw, names[5]: gf1, names[6]: gf2}
+            for (p, _), v in seedmap.items():
+                if p in extra:
+                    extra[p] += v
+                elif p in (names[2], names[3]):
+                    raise KindError("gradient_batch: seed cam / X per component via gradient()")
+            e1 = _batch_tensor(inputs, names[0], n, default=0.0, dev=dev)
+            e2 = _batch_tensor(inputs, names[1], n, default=0.0, dev=dev)
+            primal = {names[0]: e1 + err[:, 0], names[1]: e2 + err[:, 1], names[2]: cam,
+                      names[3]: X, names[4]: w, names[5]: f1, names[6]: f2}
+            grads_all = {names[0]: torch.full_like(w, a), names[1]: torch.full_like(w, b),
+                         names[2]: gcam, names[3]: gX, **extra}
+        else:
+            a = seedmap.get((names[0], ()), 0.0)
+            e0 = _batch_tensor(inputs, names[0], n, default=0.0, dev=dev)
+            primal = {names[0]: e0 + err[:, 2], names[1]: w}
+            grads_all = {names[0]: torch.full_like(w, a),
+                         names[1]: a * J[:, 30] + seedmap.get((names[1], ()), 0.0)}
+    else:
+        raise KindError(f"gradient_batch: {fname!r} is one evaluation over all its points "
+                        "(use gradient or gmm_grad)")
+    report = _report(wrt, names, grads_all)
+    restored = code == 0
+    out = (primal, {p: grads_all[p] for p in report}, restored)
+    return out + (code,) if return_codes else out
