@@ -42,7 +42,24 @@ def _require_cuda(name, t, dtype=F64, ndim=None, last=None):
         raise KindError(f"{name} must have {ndim} dimensions, got shape {tuple(t.shape)}")
     if last is not None and t.shape[-1] != last:
         raise KindError(f"{name} must have trailing dimension {last}, got {tuple(t.shape)}")
+    if t.device.index != torch.cuda.current_device():
+        raise KindError(f"{name} is on {t.device} but the current device is "
+                        f"cuda:{torch.cuda.current_device()} (use torch.cuda.device(...))")
     return t.contiguous()
+
+
+def _check_out(name, t, like, dtype=F64, numel=None):
+    """Caller-provided output buffers are written in place: they must be
+    contiguous, of the right dtype and size, on the inputs' device."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.device != like.device or t.dtype != dtype:
+        raise KindError(f"out tensor {name} must be a {dtype} tensor on {like.device}")
+    if not t.is_contiguous():
+        raise KindError(f"out tensor {name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise KindError(f"out tensor {name} must have {numel} elements, got {t.numel()}")
+    return t
 
 
 def _ptr(t):
@@ -80,9 +97,11 @@ def besselj_grad(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
         dz = torch.empty_like(z)
         fail = torch.empty(z.shape, dtype=torch.uint8, device=z.device)
     else:
-        J, dz, fail = out
+        J, dz, fail = (_check_out("J", out[0], z, numel=n), _check_out("dJdz", out[1], z, numel=n),
+                       _check_out("fail", out[2], z, torch.uint8, n))
     if counters is None:
         counters = torch.zeros(2, dtype=torch.int64, device=z.device)
+    counters = _check_out("counters", counters, z, torch.int64, 2)
     L = _native.lib()
     rc = L.rl_besselj_grad_f64(int(nu), _ptr(z), n, float(thr), float(tol), float(seed),
                                max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)),
@@ -186,9 +205,13 @@ def ba_jacobian(cams, X, w, feats, obs, *, tol=1e-9, invcheck=True, want_err=Tru
         Jf = torch.empty((p, 4), dtype=F64, device=dev) if want_feat else None
         fail = torch.empty(p, dtype=torch.uint8, device=dev)
     else:
-        J, err, Jf, fail = out
+        J, err, Jf, fail = (_check_out("J", out[0], w, numel=31 * p),
+                            _check_out("err", out[1], w, numel=3 * p),
+                            _check_out("Jfeat", out[2], w, numel=4 * p),
+                            _check_out("fail", out[3], w, torch.uint8, p))
     if counters is None:
         counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    counters = _check_out("counters", counters, w, torch.int64, 2)
     L = _native.lib()
     rc = L.rl_ba_jac_f64(cams.shape[0], X.shape[0], p, _ptr(cams), _ptr(X), _ptr(w), _ptr(feats),
                          _ptr(obs), float(tol), int(bool(invcheck)), _ptr(err), _ptr(J), _ptr(Jf),
@@ -247,12 +270,15 @@ def gmm_grad(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
     dev = x.device
     L = _native.lib()
     wsb = L.rl_gmm_workspace_bytes(d, K, N)
+    if workspace is not None:
+        _check_out("workspace", workspace, x, torch.uint8)
     if workspace is None or workspace.numel() < wsb:
         workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
     packed = torch.empty(gmm_packed_size(d, K), dtype=F64, device=dev)
     fail = torch.empty(N, dtype=torch.uint8, device=dev)
     if counters is None:
         counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    counters = _check_out("counters", counters, x, torch.int64, 2)
     rc = L.rl_gmm_grad_f64(d, K, N, int(N if N_total is None else N_total), _ptr(alphas),
                            _ptr(means), _ptr(icf), _ptr(x), float(gamma), int(m), float(cst),
                            float(tol), int(bool(invcheck)), int(bool(add_param_terms)),
@@ -331,6 +357,8 @@ def gmm_objective(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=Non
     N = x.shape[0]
     L = _native.lib()
     wsb = L.rl_gmm_workspace_bytes(d, K, N)
+    if workspace is not None:
+        _check_out("workspace", workspace, x, torch.uint8)
     if workspace is None or workspace.numel() < wsb:
         workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
     err = torch.empty(1, dtype=F64, device=x.device)
@@ -395,7 +423,14 @@ def ba_jacobian_csr(cams, X, w, feats, obs, *, obs_offset=0, n_obs_total=None, p
         fail = torch.empty(p, dtype=torch.uint8, device=dev)
         err = torch.empty((p, 3), dtype=F64, device=dev) if want_err else None
     else:
-        rows, cols, vals, fail, err = out
+        rows, cols, vals, fail, err = (
+            _check_out("rows", out[0], w, torch.int32, 3 * p + 1),
+            _check_out("cols", out[1], w, torch.int32, 31 * p),
+            _check_out("vals", out[2], w, numel=31 * p),
+            _check_out("fail", out[3], w, torch.uint8, p),
+            _check_out("err", out[4], w, numel=3 * p))
+        if (rows is None) != (cols is None):
+            raise KindError("rows and cols are both given or both None")
     if counters is None:
         counters = torch.zeros(2, dtype=torch.int64, device=dev)
     L = _native.lib()

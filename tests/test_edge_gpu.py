@@ -67,3 +67,17 @@ def test_csr_odd_sizes_fall_back_correctly(cuda, oracle):
         assert np.array_equal(r.cols.cpu().numpy(), cols)
         v = r.vals.cpu().numpy()
         assert np.allclose(v, vals, rtol=1e-10, atol=1e-13 * np.abs(vals).max())
+
+
+def test_out_buffers_and_devices_are_validated(cuda):
+    z = torch.rand(100, dtype=torch.float64, device=cuda) + 0.1
+    J = torch.empty(200, dtype=torch.float64, device=cuda)[::2]          # non-contiguous
+    dz = torch.empty(100, dtype=torch.float64, device=cuda)
+    fail = torch.empty(100, dtype=torch.uint8, device=cuda)
+    with pytest.raises(rg.KindError):
+        rg.besselj_grad(z, 2, out=(J, dz, fail))
+    with pytest.raises(rg.KindError):
+        rg.besselj_grad(z, 2, out=(dz, dz, fail.to(torch.int32)))
+    ok = rg.besselj_grad(z, 2, out=(torch.empty_like(z), dz, fail))
+    torch.cuda.synchronize()
+    assert ok.dJdz is dz and not ok.fail.any()
