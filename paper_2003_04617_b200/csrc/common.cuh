@@ -8,6 +8,13 @@
 
 namespace rl {
 
+// Programmatic dependent launch: a kernel launched with the
+// ProgrammaticStreamSerialization attribute may start while its
+// predecessor drains; it waits here (no-op for ordinary launches) before
+// touching anything the predecessor writes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
 // Host-computed natural-log table log(i), i in [0, LOGTAB_N), filled from the

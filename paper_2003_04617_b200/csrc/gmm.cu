@@ -143,8 +143,15 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
                                                           double *__restrict__ qd,
                                                           double *__restrict__ sq,
                                                           double *__restrict__ fro,
-                                                          double *__restrict__ par) {
+                                                          double *__restrict__ par,
+                                                          unsigned *__restrict__ flags,
+                                                          long long N) {
   const int k = blockIdx.x;
+  // the per-point release flags of k_gmm_fwd start at 0 (replaces a memset,
+  // so the launch chain stays kernel-to-kernel for PDL)
+  for (long long i = (long long)blockIdx.x * GMM_THREADS + threadIdx.x; i < N;
+       i += (long long)gridDim.x * GMM_THREADS)
+    flags[i] = 0u;
   const int P = d * (d + 1) / 2;
   extern __shared__ __align__(16) double prep_dyn[];     // icf row (P), then K scratch
   double *ic = prep_dyn;
@@ -334,6 +341,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
     double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA) {
+  pdl_wait();
+
   using C = GmmCfg<DP, TP>;
   extern __shared__ __align__(16) double smem[];
   double *lt_s = smem;
@@ -408,6 +417,8 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
     uint8_t *__restrict__ fail, unsigned long long *counters) {
+  pdl_wait();
+
   const long long i = (long long)blockIdx.x * LSE_THREADS + threadIdx.x;
   double e_pt = 0.0;
   unsigned long long nfail = 0;
@@ -503,6 +514,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ x,
     const double *__restrict__ LT, const double *__restrict__ gmtT,
     double *__restrict__ part /* [K][S][DP*DP + DP + 1] */) {
+  pdl_wait();
+
   using C = GmmCfg<DP, TP>;
   using MTL = MTiles<DP>;
   extern __shared__ __align__(16) double smem[];
@@ -661,6 +674,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_reduce(int S, long long PW,
                                                             const double *__restrict__ part,
                                                             double *__restrict__ red) {
+  pdl_wait();
+
   const int k = blockIdx.y;
   const long long e = (long long)blockIdx.x * GMM_THREADS + threadIdx.x;
   if (e >= PW) return;
@@ -696,6 +711,8 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     const double *__restrict__ LT, const double *__restrict__ part,
     const double *__restrict__ err_part, const double *__restrict__ ws_par, double ga, int wm,
     double cst, int add_params, double *__restrict__ out) {
+  pdl_wait();
+
   const int k = blockIdx.x;
   const int P = d * (d + 1) / 2;
   const long long PW = (long long)DP * DP + DP + 1;
@@ -795,6 +812,8 @@ __global__ void k_gmm_err(int K, int nerr, const double *__restrict__ err_part,
                           const double *__restrict__ sq, const double *__restrict__ fro_k,
                           const double *__restrict__ ws_par, double ga, int wm, double cst,
                           int add_params, double *__restrict__ out) {
+  pdl_wait();
+
   __shared__ double ered[GMM_THREADS];
   sum_err_parts(nerr, err_part, ered);
   if (threadIdx.x != 0) return;
@@ -915,6 +934,23 @@ size_t gmm_workspace_bytes(int32_t d, int32_t K, int64_t N) {
 }
 
 // grad == 0: objective only (prep, forward tiles, logsumexp; out[0] = err)
+// launch with programmatic stream serialization (see pdl_wait)
+template <typename... KArgs, typename... Args>
+static int launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                      size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
+}
+
 template <int DP>
 static int run_gmm(int d, int K, long long N, long long N_total, const double *alphas,
                    const double *means, const double *icf, const double *x, double gamma, int m,
@@ -936,11 +972,9 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                         "smem attr prep")))
     return rc;
   k_gmm_prep<DP><<<K, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
-                                             add_params ? par : nullptr);
+                                             add_params ? par : nullptr, flags, N);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
-    if ((rc = cuda_status(cudaMemsetAsync(flags, 0, (size_t)N * 4, st), "memset flags")))
-      return rc;
     constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
     static_assert(sf <= 227 * 1024 && sr <= 227 * 1024, "shared memory budget");
     if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_fwd<DP, TPF>,
@@ -950,16 +984,17 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)sr), "smem attr rev")))
       return rc;
-    k_gmm_fwd<DP, TPF><<<dim3(K, L.Sf), GMM_THREADS, sf, st>>>(d, K, N, alphas, means, x, LT, sq,
-                                                               tol, chk, mt, flags);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_fwd"))) return rc;
-    k_gmm_lse<<<L.nerr, LSE_THREADS, 0, st>>>(K, N, mt, gmt, flags, tol, chk, errp, fail,
-                                              counters);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_lse"))) return rc;
+    if ((rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
+                         d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags)))
+      return rc;
+    if ((rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st, K, N, mt,
+                         gmt, flags, tol, chk, errp, fail, counters)))
+      return rc;
     if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
                                          add_params, out, st);
-    k_gmm_rev<DP, TPR><<<dim3(K, L.Sr), GMM_THREADS, sr, st>>>(d, K, N, means, x, LT, gmt, part);
-    if ((rc = cuda_status(cudaGetLastError(), "k_gmm_rev"))) return rc;
+    if ((rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
+                         d, K, N, means, x, LT, gmt, part)))
+      return rc;
   } else if (!grad) {
     return launch_gmm_err_only(K, L, 0, errp, sq, fro, par, gamma, m, cst, add_params, out, st);
   } else {
@@ -968,12 +1003,13 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       return rc;
   }
   const long long PW = (long long)DP * DP + DP + 1;
-  k_gmm_reduce<<<dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K), GMM_THREADS, 0, st>>>(
-      L.Sr, PW, part, redp);
-  if ((rc = cuda_status(cudaGetLastError(), "k_gmm_reduce"))) return rc;
-  k_gmm_final<DP><<<K, GMM_THREADS, 0, st>>>(d, K, 1, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT,
-                                             redp, errp, par, gamma, m, cst, add_params, out);
-  return cuda_status(cudaGetLastError(), "k_gmm_final");
+  if ((rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
+                       dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K),
+                       dim3(GMM_THREADS), 0, st, L.Sr, PW, part, redp)))
+    return rc;
+  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K), dim3(GMM_THREADS), 0, st, d, K, 1,
+                    N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, redp, errp, par, gamma, m, cst,
+                    add_params, out);
 }
 
 int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
