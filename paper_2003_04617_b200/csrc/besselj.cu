@@ -64,13 +64,13 @@ __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 #endif
 
 #ifndef BJ_SPEC
-#define BJ_SPEC 4          // speculative trips per warp vote (ILP of the exp chains)
+#define BJ_SPEC 2          // speculative trips per warp vote (2: fewer live registers -> 3 CTAs/SM, measured best)
 #endif
 #ifndef BJ_MINB
-#define BJ_MINB 2          // __launch_bounds__ min blocks per SM (register budget)
+#define BJ_MINB 3          // __launch_bounds__ min blocks per SM (80 registers, no spills)
 #endif
 #ifndef BJ_M
-#define BJ_M 8             // chunk = BJ_M elements per thread (z-sorted per chunk)
+#define BJ_M 5             // chunk = BJ_M elements per thread (z-sorted per chunk; 3 CTAs/SM fit)
 #endif
 constexpr int BJ_BLOCK = 256;
 constexpr int BJ_C = BJ_BLOCK * BJ_M;  // elements per chunk
@@ -647,7 +647,7 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
 // the Hessian (Dual sweeps; d2out = d2J/dz2).
 constexpr int BJ_RUN = 0, BJ_GRAD = 1, BJ_HESS = 2;
 template <int MODE>
-__global__ void __launch_bounds__(BJ_BLOCK, BJ_MINB) k_besselj(
+__global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
     long long max_trips, int chk, const double *__restrict__ out_in, double sign,
     double *__restrict__ Jout, double *__restrict__ dzout, uint8_t *__restrict__ fail,
