@@ -244,8 +244,47 @@ def gen_hess():
     print(f"hessian goldens written ({z.size} cases, {time.time() - t0:.1f} s)")
 
 
+def gen_codegen():
+    """reference gradient() of the codegen test programs (tests/golden/codegen/*.rnl):
+    per row the primal outputs, the cotangents of the Float parameters and the
+    error class (default seed: the first parameter)."""
+    cases = {
+        "mul_acc": (["y!", "a", "b"], {}, 64),
+        "sink": (["out!", "x", "y"], {"n": 3}, 64),
+        "wloop": (["acc!", "x"], {"n": 5}, 48),
+    }
+    out = {}
+    for fn, (floats, ints, n) in cases.items():
+        prog = parse_program(open(os.path.join(OUT_DIR, "codegen", fn + ".rnl")).read())
+        rng = np.random.default_rng(sum(map(ord, fn)))
+        X = rng.uniform(0.05, 1.8, (n, len(floats)))
+        X[:, 0] = rng.normal(size=n)
+        if fn == "sink":
+            X[3, 2], X[7, 1] = -0.5, -0.3          # RevDomainError rows (log y, log x)
+        names = floats + list(ints)
+        P, G = np.full((n, len(floats)), np.nan), np.full((n, len(floats)), np.nan)
+        errs = []
+        for i in range(n):
+            args = [float(v) for v in X[i]]
+            call = []
+            pn = prog.get(fn).param_names()
+            for nm in pn:
+                call.append(ints[nm] if nm in ints else args[floats.index(nm)])
+            r, en = _err_name(lambda: gradient(prog, GradRequest(fn, call)))
+            errs.append(en)
+            if r is not None:
+                prim, grads = r
+                for j, nm in enumerate(floats):
+                    P[i, j] = prim[pn.index(nm)]
+                    G[i, j] = grads[nm]
+        out[fn + "_x"], out[fn + "_primal"], out[fn + "_grad"] = X, P, G
+        out[fn + "_err"] = np.array(errs)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen.npz"), **out)
+    print("codegen goldens written")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
-    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess"]
+    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen"]
     for w in which:
         globals()["gen_" + w]()

@@ -20,6 +20,7 @@ from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBo
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
                      UnknownExample, UnknownFunction, UnsupportedProgram)
+from .codegen import CompiledFunction, compile_function
 from .interp import CheckReport, check_reversibility, run, uncall
 from .kernels import (BACsr, BAResult, BesselHessResult, BesselResult, GMMResult, RunResult, ba_jacobian, ba_jacobian_csr,
                       ba_jacobian_csr_host, ba_residuals,
@@ -28,7 +29,7 @@ from .programs import CATALOG, Program, entry_function, load_example, parse_prog
 from .values import Array
 
 __all__ = [
-    "HessianResult", "hessian", "gradient_batch", "BesselHessResult", "besselj_hess",
+    "HessianResult", "hessian", "gradient_batch", "CompiledFunction", "compile_function", "BesselHessResult", "besselj_hess",
     "AliasedArguments", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",
