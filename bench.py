@@ -369,6 +369,19 @@ def run_bessel_ours(args, D):
                  "kernel": "k_besselj<0> (rl_besselj_run_f64)"}
     # forward-over-reverse Hessian (d2J/dz2 with J and dJ/dz) of the same batch
     h_ms = D.max(time_device(lambda: kernels.besselj_hess(z, BESSEL_NU), max(3, args.steps // 4)))
+    # the same gradient through the generic .rnl -> CUDA compiler (codegen.py)
+    generic = None
+    try:
+        from paper_2003_04617_b200 import codegen
+        ck = codegen.compile_function(open(os.path.join(REPO, "paper_2003_04617_b200", "programs",
+                                                        "besselj.rnl")).read(),
+                                      "besselj", int_params=("nu",))
+        g_ms = D.max(time_device(lambda: ck.gradient({"out!": 0.0, "z": z, "nu": BESSEL_NU}),
+                                 max(2, args.steps // 8)))
+        generic = {"ms_per_step": round(g_ms, 4), "over_handwritten": round(g_ms / ms_step, 2),
+                   "kernel": "codegen.compile_function(programs/besselj.rnl)"}
+    except Exception as err:  # noqa: BLE001 - reported, not fatal to the bench line
+        generic = {"unavailable": str(err)[:200]}
     hess = {"ms_per_step": round(h_ms, 4), "hessians_per_s": round(n_total / (h_ms * 1e-3), 1),
             "hess_over_grad": round(h_ms / ms_step, 3),
             "kernel": "k_besselj<2> (rl_besselj_hess_f64, Dual-number sweeps)"}
@@ -386,7 +399,7 @@ def run_bessel_ours(args, D):
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clocks, "sum_trips_per_step": D.sum(sum_trips),
         "failed_per_step": D.sum(n_failed), "parity_sample": parity,
-        "objective_only": objective, "hessian": hess,
+        "objective_only": objective, "hessian": hess, "generic_codegen": generic,
     }
     return res
 
