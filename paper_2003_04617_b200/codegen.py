@@ -30,7 +30,7 @@ rejected at compile time (UnsupportedProgram), as are the static aliasing
 patterns the reference rejects at run time (AliasedArguments).
 
 The kernel is built with nvcc for sm_100a into a cache directory
-($REVGPU_CODEGEN_CACHE, default ~/.cache/revgpu-codegen) and bound with
+($REVGPU_CODEGEN_CACHE, default paper_2003_04617_b200/_codegen_cache) and bound with
 ctypes; libdevice's exp/log/sin/cos/pow stand for the host libm (<= 1-2 ulp).
 """
 
@@ -1125,8 +1125,10 @@ extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, 
 # ---------------------------------------------------------------------------
 
 def _cache_dir():
+    # in-tree by default (next to librevgpu.so), so generated kernels load from
+    # the repository like the hand-written ones; $REVGPU_CODEGEN_CACHE overrides
     d = os.environ.get("REVGPU_CODEGEN_CACHE") or os.path.join(
-        os.path.expanduser("~"), ".cache", "revgpu-codegen")
+        os.path.dirname(os.path.abspath(__file__)), "_codegen_cache")
     os.makedirs(d, exist_ok=True)
     return d
 
