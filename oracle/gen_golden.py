@@ -262,8 +262,10 @@ def gen_codegen():
         if fn == "sink":
             X[3, 2], X[7, 1] = -0.5, -0.3          # RevDomainError rows (log y, log x)
         names = floats + list(ints)
+        from revlang.autodiff import hessian
         P, G = np.full((n, len(floats)), np.nan), np.full((n, len(floats)), np.nan)
-        errs = []
+        H = np.full((n, len(floats), len(floats)), np.nan)
+        errs, herrs = [], []
         for i in range(n):
             args = [float(v) for v in X[i]]
             call = []
@@ -272,6 +274,10 @@ def gen_codegen():
                 call.append(ints[nm] if nm in ints else args[floats.index(nm)])
             r, en = _err_name(lambda: gradient(prog, GradRequest(fn, call)))
             errs.append(en)
+            h, hn = _err_name(lambda: hessian(prog, fn, call))
+            herrs.append(hn)
+            if h is not None:
+                H[i] = h.matrix
             if r is not None:
                 prim, grads = r
                 for j, nm in enumerate(floats):
@@ -279,6 +285,7 @@ def gen_codegen():
                     G[i, j] = grads[nm]
         out[fn + "_x"], out[fn + "_primal"], out[fn + "_grad"] = X, P, G
         out[fn + "_err"] = np.array(errs)
+        out[fn + "_hess"], out[fn + "_hess_err"] = H, np.array(herrs)
     np.savez_compressed(os.path.join(OUT_DIR, "codegen.npz"), **out)
     print("codegen goldens written")
 

@@ -581,6 +581,63 @@ __device__ __forceinline__ double g_pow(double a, double b, int &c) {
   if ((a == 0.0 && b < 0.0) || (a < 0.0 && b != floor(b))) { if (!c) c = RC_DOMAIN; return 0.0; }
   return pow(a, b);
 }
+// ---- Dual numbers (reference values.py:258-431): the Hessian build runs the
+// same generated code with R = Dl.  Doubles promote to Dl(d, 0) (_as_dual);
+// comparisons and (double) see the primal (Dual.__float__ / __lt__ ...).
+struct Dl {
+  double p, t;
+  __device__ __forceinline__ Dl() : p(0.0), t(0.0) {}
+  __device__ __forceinline__ Dl(double a, double b = 0.0) : p(a), t(b) {}
+  __device__ __forceinline__ explicit operator double() const { return p; }
+};
+__device__ __forceinline__ Dl operator+(Dl a, Dl b) { return Dl(a.p + b.p, a.t + b.t); }
+__device__ __forceinline__ Dl operator-(Dl a, Dl b) { return Dl(a.p - b.p, a.t - b.t); }
+__device__ __forceinline__ Dl operator*(Dl a, Dl b) { return Dl(a.p * b.p, a.t * b.p + a.p * b.t); }
+__device__ __forceinline__ Dl operator/(Dl a, Dl b) {
+  const double q = a.p / b.p;
+  return Dl(q, (a.t - q * b.t) / b.p);
+}
+__device__ __forceinline__ Dl operator-(Dl a) { return Dl(-a.p, -a.t); }
+__device__ __forceinline__ Dl operator+(Dl a, double b) { return a + Dl(b); }
+__device__ __forceinline__ Dl operator+(double a, Dl b) { return Dl(a) + b; }
+__device__ __forceinline__ Dl operator-(Dl a, double b) { return a - Dl(b); }
+__device__ __forceinline__ Dl operator-(double a, Dl b) { return Dl(a) - b; }
+__device__ __forceinline__ Dl operator*(Dl a, double b) { return a * Dl(b); }
+__device__ __forceinline__ Dl operator*(double a, Dl b) { return Dl(a) * b; }
+__device__ __forceinline__ Dl operator/(Dl a, double b) { return a / Dl(b); }
+__device__ __forceinline__ Dl operator/(double a, Dl b) { return Dl(a) / b; }
+__device__ __forceinline__ double rl_p(double x) { return x; }
+__device__ __forceinline__ double rl_p(Dl x) { return x.p; }
+__device__ __forceinline__ double rl_t(double) { return 0.0; }
+__device__ __forceinline__ double rl_t(Dl x) { return x.t; }
+__device__ __forceinline__ Dl g_div(Dl a, Dl b, int &c) {
+  if (b.p == 0.0) { if (!c) c = RC_DOMAIN; return Dl(0.0); }
+  return a / b;
+}
+__device__ __forceinline__ Dl g_sqrt(Dl x, int &c) {
+  if (x.p <= 0.0 && x.t != 0.0) { if (!c) c = RC_DOMAIN; return Dl(0.0); }
+  const double r = g_sqrt(x.p, c);
+  return Dl(r, x.t / (2.0 * r));
+}
+__device__ __forceinline__ Dl g_log(Dl x, int &c) { return Dl(g_log(x.p, c), x.t / x.p); }
+__device__ __forceinline__ Dl g_exp(Dl x, int &c) {
+  const double r = g_exp(x.p, c);
+  return Dl(r, x.t * r);
+}
+__device__ __forceinline__ Dl sin(Dl x) { return Dl(sin(x.p), x.t * cos(x.p)); }
+__device__ __forceinline__ Dl cos(Dl x) { return Dl(cos(x.p), -x.t * sin(x.p)); }
+__device__ __forceinline__ double g_abs(double x, int &) { return fabs(x); }
+__device__ __forceinline__ Dl g_abs(Dl x, int &c) {
+  if (x.p == 0.0 && x.t != 0.0) { if (!c) c = RC_DOMAIN; return Dl(0.0); }
+  return Dl(fabs(x.p), x.p >= 0.0 ? x.t : -x.t);
+}
+__device__ __forceinline__ Dl g_pow(Dl a, Dl b, int &c) {
+  const double r = g_pow(a.p, b.p, c);
+  double t = 0.0;
+  if (a.t != 0.0) t = t + b.p * g_pow(a.p, b.p - 1.0, c) * a.t;
+  if (b.t != 0.0) t = t + r * g_log(a.p, c) * b.t;
+  return Dl(r, t);
+}
 __device__ __forceinline__ long long g_imod(long long a, long long b, int &c) {
   if (b == 0) { if (!c) c = RC_DOMAIN; return 0; }
   long long r = a % b;
@@ -693,27 +750,29 @@ class _Emitter:
             f = e.f
             if f == "ulog":
                 (a, _), = args
-                return f"g_log((double)({a}), code)", "u"
+                return f"g_log(R({a}), code)", "u"
             if f in ("sqrt", "exp", "log"):
                 (a, _), = args
-                return f"g_{f}((double)({a}), code)", "f"
+                return f"g_{f}(R({a}), code)", "f"
             if f in ("sin", "cos"):
                 (a, _), = args
-                return f"{f}((double)({a}))", "f"
+                return f"{f}(R({a}))", "f"
             if f == "abs":
                 (a, k), = args
-                return (f"llabs({a})" if k == "i" else f"fabs({a})"), k
+                return (f"(({a}) < 0 ? -({a}) : ({a}))" if k == "i" else f"g_abs(R({a}), code)"), k
             if f == "abs2":
                 (a, k), = args
                 return f"(({a}) * ({a}))", k
             if f == "float":
                 (a, _), = args
-                return f"((double)({a}))", "f"
+                return f"R((double)({a}))", "f"          # float(Dual) is its primal
             if f in ("min", "max"):
                 (a, ka), (b, kb) = args
                 if ka == "i" and kb == "i":
                     return f"({f}({a}, {b}))", "i"
-                return f"f{f}((double)({a}), (double)({b}))", "f"
+                # Python min/max keep the chosen operand (primal comparison)
+                cmp = "<" if f == "min" else ">"
+                return f"((double)R({b}) {cmp} (double)R({a}) ? R({b}) : R({a}))", "f"
             raise UnsupportedProgram(f"codegen: expression function {f!r} is not supported")
         if isinstance(e, Bin):
             ls, lk = self.expr(e.l)
@@ -724,17 +783,17 @@ class _Emitter:
             if op in ("==", "!=", "<", "<=", ">", ">="):
                 if lk == "i" and rk == "i":
                     return f"(({ls}) {op} ({rs}))", "b"
-                return f"((double)({ls}) {op} (double)({rs}))", "b"
+                return f"((double)R({ls}) {op} (double)R({rs}))", "b"
             k = self.expr_kind(e)
             if op == "%":
                 return f"g_imod({ls}, {rs}, code)", "i"
             if op == "/":
-                return f"g_div((double)({ls}), (double)({rs}), code)", "f"
+                return f"g_div(R({ls}), R({rs}), code)", "f"
             if op == "^":
-                return f"g_pow((double)({ls}), (double)({rs}), code)", "f"
+                return f"g_pow(R({ls}), R({rs}), code)", "f"
             if k == "i":
                 return f"(({ls}) {op} ({rs}))", "i"
-            return f"((double)({ls}) {op} (double)({rs}))", "f"
+            return f"(R({ls}) {op} R({rs}))", "f"
         raise UnsupportedProgram(f"codegen: bad expression {e!r}")
 
     def cond(self, e):
@@ -760,7 +819,7 @@ class _Emitter:
         if k == "u":
             return f"g_exp(v_{_cid(a.name)}, code)"
         if k == "i":
-            return f"((double)v_{_cid(a.name)})"
+            return f"R((double)v_{_cid(a.name)})"
         return f"v_{_cid(a.name)}"
 
     def tracked(self, a):
@@ -770,25 +829,25 @@ class _Emitter:
         if fname == "identity":
             return xs[0]
         if fname == "add":
-            return f"({xs[0]} + {xs[1]})"
+            return f"(R({xs[0]}) + R({xs[1]}))"
         if fname == "sub":
-            return f"({xs[0]} - {xs[1]})"
+            return f"(R({xs[0]}) - R({xs[1]}))"
         if fname == "mul":
-            return f"({xs[0]} * {xs[1]})"
+            return f"(R({xs[0]}) * R({xs[1]}))"
         if fname == "div":
-            return f"g_div({xs[0]}, {xs[1]}, code)"
+            return f"g_div(R({xs[0]}), R({xs[1]}), code)"
         if fname == "pow":
-            return f"g_pow({xs[0]}, {xs[1]}, code)"
+            return f"g_pow(R({xs[0]}), R({xs[1]}), code)"
         if fname == "neg":
-            return f"(-{xs[0]})"
+            return f"(-R({xs[0]}))"
         if fname == "abs":
-            return f"fabs({xs[0]})"
+            return f"g_abs({xs[0]}, code)"
         if fname == "abs2":
-            return f"({xs[0]} * {xs[0]})"
+            return f"(R({xs[0]}) * R({xs[0]}))"
         if fname in ("sqrt", "log", "exp"):
-            return f"g_{fname}({xs[0]}, code)"
+            return f"g_{fname}(R({xs[0]}), code)"
         if fname in ("sin", "cos"):
-            return f"{fname}({xs[0]})"
+            return f"{fname}(R({xs[0]}))"
         raise UnsupportedProgram(f"codegen: instruction function {fname!r} is not supported")
 
     def partials(self, fname, xs):
@@ -802,27 +861,29 @@ class _Emitter:
         if fname == "mul":
             return [xs[1], xs[0]]
         if fname == "div":
-            return [f"g_div(1.0, {xs[1]}, code)", f"(-g_div({xs[0]}, {xs[1]} * {xs[1]}, code))"]
+            return [f"g_div(R(1.0), R({xs[1]}), code)",
+                    f"(-g_div(R({xs[0]}), R({xs[1]}) * R({xs[1]}), code))"]
         if fname == "pow":
-            first = f"({xs[1]} * g_pow({xs[0]}, {xs[1]} - 1.0, code))"
-            second = f"(({xs[0]}) > 0.0 ? g_pow({xs[0]}, {xs[1]}, code) * g_log({xs[0]}, code) : NAN)"
+            first = f"({xs[1]} * g_pow(R({xs[0]}), R({xs[1]}) - 1.0, code))"
+            second = (f"((double)R({xs[0]}) > 0.0 ? g_pow(R({xs[0]}), R({xs[1]}), code) * "
+                      f"g_log(R({xs[0]}), code) : R(NAN))")
             return [first, ("POW2", second, xs[0])]
         if fname == "neg":
             return ["-1.0"]
         if fname == "abs":
-            return [("ABS", f"(({xs[0]}) > 0.0 ? 1.0 : -1.0)", xs[0])]
+            return [("ABS", f"((double)R({xs[0]}) > 0.0 ? 1.0 : -1.0)", xs[0])]
         if fname == "abs2":
-            return [f"(2.0 * {xs[0]})"]
+            return [f"(2.0 * R({xs[0]}))"]
         if fname == "sqrt":
-            return [f"g_div(0.5, g_sqrt({xs[0]}, code), code)"]
+            return [f"g_div(R(0.5), g_sqrt(R({xs[0]}), code), code)"]
         if fname == "exp":
-            return [f"g_exp({xs[0]}, code)"]
+            return [f"g_exp(R({xs[0]}), code)"]
         if fname == "log":
-            return [f"g_div(1.0, {xs[0]}, code)"]
+            return [f"g_div(R(1.0), R({xs[0]}), code)"]
         if fname == "sin":
-            return [f"cos({xs[0]})"]
+            return [f"cos(R({xs[0]}))"]
         if fname == "cos":
-            return [f"(-sin({xs[0]}))"]
+            return [f"(-sin(R({xs[0]})))"]
         raise UnsupportedProgram(f"codegen: no gradient rule for {fname!r}")
 
     # statements -------------------------------------------------------
@@ -853,7 +914,7 @@ class _Emitter:
             else:
                 # _ancilla_residual: |cur - decl| > tol fails (NaN passes); ULog by exponent
                 d = self.new("d")
-                self.w(f"{{ const double {d} = fabs(v_{_cid(s.name)} - (double)({val}));")
+                self.w(f"{{ const double {d} = fabs(rl_p(v_{_cid(s.name)} - R({val})));")
                 self.w(f"  if (chk && {d} > tol) {{ code = RC_DIRTY; goto {label}; }} }}")
         elif isinstance(s, If):
             took = self.new("took")
@@ -953,14 +1014,14 @@ class _Emitter:
                 xs = [self.atom_real(a) for a in args]
                 fv = self.apply_fn(s.fname, xs)
             fvv = self.new("fv")
-            self.w(f"{{ const double {fvv} = {fv};")
+            self.w(f"{{ const R {fvv} = {fv};")
             self.w(f"  if (code) goto {label};")
             self.w(f"  v_{T} = v_{T} {'+' if s.op == '+=' else '-'} {fvv}; }}")
             if not grad:
                 return
             sign = "1.0" if s.op == "-=" else "-1.0"
             sg = self.new("sg")
-            self.w(f"{{ const double {sg} = {sign} * g_{T};")
+            self.w(f"{{ const R {sg} = {sign} * g_{T};")
             if s.fname == "convert":
                 (a,) = args
                 if self.tracked(a):
@@ -977,7 +1038,8 @@ class _Emitter:
                     A = _cid(a.name)
                     if isinstance(p, tuple):
                         tag, pv, x0 = p
-                        cond = f"({x0}) == 0.0" if tag == "ABS" else f"!(({x0}) > 0.0)"
+                        cond = (f"(double)R({x0}) == 0.0" if tag == "ABS"
+                                else f"!((double)R({x0}) > 0.0)")
                         self.w(f"  if ({cond}) {{ if (!code) code = RC_DOMAIN; goto {label}; }}")
                         p = pv
                     self.w(f"  g_{A} = g_{A} + {sg} * {p};")
@@ -997,7 +1059,7 @@ class _Emitter:
                 raise UnsupportedProgram("codegen: *= / /= take one argument under differentiation")
             contrib = f"g_log({self.apply_fn(s.fname, [self.atom_real(a) for a in args])}, code)"
         cv = self.new("c")
-        self.w(f"{{ const double {cv} = {contrib};")
+        self.w(f"{{ const R {cv} = {contrib};")
         self.w(f"  if (code) goto {label};")
         self.w(f"  v_{T} = v_{T} {'+' if s.op == '*=' else '-'} {cv}; }}")
         if not grad:
@@ -1032,8 +1094,12 @@ def _collect_vars(stmts, acc):
     return acc
 
 
-def generate(src, fname, int_params=()):
-    """CUDA source of the batched gradient kernel of `fname`, and its layout."""
+def generate(src, fname, int_params=(), mode="grad"):
+    """CUDA source of the batched gradient (mode "grad") or forward-over-reverse
+    Hessian-column (mode "hess": the same code over Dual numbers, tangent on
+    the Float parameter `dir`) kernel of `fname`, and its layout."""
+    if mode not in ("grad", "hess"):
+        raise KindError(f"codegen mode {mode!r}")
     fns = _Parser(src).program()
     if fname not in fns:
         raise UnsupportedProgram(f"codegen: no function named {fname!r}")
@@ -1059,18 +1125,21 @@ def generate(src, fname, int_params=()):
             raise UnsupportedProgram(f"codegen: {v!r} shadows a parameter")
         k = allk.get(v, "f")
         decl.append(f"    long long v_{_cid(v)} = 0;" if k == "i"
-                    else f"    double v_{_cid(v)} = 0.0, g_{_cid(v)} = 0.0;")
+                    else f"    R v_{_cid(v)} = R(0.0), g_{_cid(v)} = R(0.0);")
     NF, NI = len(floats), len(ints)
-    L = [_PRELUDE, f"extern \"C\" __global__ void rlg_kernel(long long n, const double *__restrict__ fin,"
-                   " const long long *__restrict__ iin, const double *__restrict__ seeds,"
-                   " double tol, int chk, long long fuel, double *__restrict__ fout,"
-                   " double *__restrict__ gout, unsigned char *__restrict__ fail) {",
+    L = [_PRELUDE, "typedef Dl R;" if mode == "hess" else "typedef double R;",
+         f"extern \"C\" __global__ void rlg_kernel(long long n, const double *__restrict__ fin,"
+         " const long long *__restrict__ iin, const double *__restrict__ seeds,"
+         " double tol, int chk, long long fuel, double *__restrict__ fout,"
+         " double *__restrict__ gout, unsigned char *__restrict__ fail, int dir,"
+         " double *__restrict__ hout) {",
          "  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;"
          " i += (long long)gridDim.x * blockDim.x) {",
          "    int code = 0;", "    long long ticks = 0;"]
     for j, p in enumerate(floats):
-        L.append(f"    const double in_{_cid(p)} = fin[{j}LL * n + i];")
-        L.append(f"    double v_{_cid(p)} = in_{_cid(p)}, g_{_cid(p)} = 0.0;")
+        L.append(f"    const R in_{_cid(p)} = R(fin[{j}LL * n + i]"
+                 + (f", dir == {j} ? 1.0 : 0.0);" if mode == "hess" else ");"))
+        L.append(f"    R v_{_cid(p)} = in_{_cid(p)}, g_{_cid(p)} = R(0.0);")
     for j, p in enumerate(ints):
         L.append(f"    long long v_{_cid(p)} = iin[{j}];")
     L += decl
@@ -1080,23 +1149,27 @@ def generate(src, fname, int_params=()):
     L.append("    if (code) {")
     for j, p in enumerate(floats):
         L.append(f"      fout[{j}LL * n + i] = NAN; gout[{j}LL * n + i] = NAN;")
+        if mode == "hess":
+            L.append(f"      hout[{j}LL * n + i] = NAN;")
     L.append("      fail[i] = (unsigned char)code; continue; }")
     for j, p in enumerate(floats):
-        L.append(f"    fout[{j}LL * n + i] = v_{_cid(p)};")
+        L.append(f"    fout[{j}LL * n + i] = rl_p(v_{_cid(p)});")
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
     for j, p in enumerate(floats):
-        L.append(f"    g_{_cid(p)} = seeds[{j}];")
+        L.append(f"    g_{_cid(p)} = R(seeds[{j}]);            // coerce_to_kind: Dual(seed, 0)")
     L.append("    ticks = 0;")
     L += em_g.lines
     L.append("  grad_done:")
     L.append("    if (!code) {      // the backward pass must restore every argument")
     for p in floats:
-        L.append(f"      if (!(fabs(v_{_cid(p)} - in_{_cid(p)}) <= tol)) code = RC_REV;")
+        L.append(f"      if (!(fabs(rl_p(v_{_cid(p)}) - rl_p(in_{_cid(p)})) <= tol)) code = RC_REV;")
     for j, p in enumerate(ints):
         L.append(f"      if (v_{_cid(p)} != iin[{j}]) code = RC_REV;")
     L.append("    }")
     for j, p in enumerate(floats):
-        L.append(f"    gout[{j}LL * n + i] = code ? NAN : g_{_cid(p)};")
+        L.append(f"    gout[{j}LL * n + i] = code ? NAN : rl_p(g_{_cid(p)});")
+        if mode == "hess":
+            L.append(f"    hout[{j}LL * n + i] = code ? NAN : rl_t(g_{_cid(p)});")
     L.append("    if (code) {")
     for j, p in enumerate(floats):
         L.append(f"      fout[{j}LL * n + i] = NAN;")
@@ -1107,13 +1180,13 @@ def generate(src, fname, int_params=()):
     L.append(r"""
 extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, const double *seeds,
                           double tol, int chk, long long fuel, double *fout, double *gout,
-                          unsigned char *fail, void *stream) {
+                          unsigned char *fail, int dir, double *hout, void *stream) {
   if (n <= 0) return 0;
   const int block = 128;
   long long grid = (n + block - 1) / block;
   if (grid > 148 * 16) grid = 148 * 16;
   rlg_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(n, fin, iin, seeds, tol, chk, fuel,
-                                                                fout, gout, fail);
+                                                                fout, gout, fail, dir, hout);
   return (int)cudaGetLastError();
 }
 """)
@@ -1170,14 +1243,42 @@ class CompiledFunction:
 
     def __init__(self, source_text, fname, int_params=()):
         self.fname = fname
+        self._text, self._ints = source_text, tuple(int_params)
         self.source, self.floats, self.ints = generate(source_text, fname, int_params)
-        self.path = build(self.source)
-        self._lib = ctypes.CDLL(self.path)
-        self._lib.rlg_launch.restype = ctypes.c_int
-        self._lib.rlg_launch.argtypes = [ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
-            ctypes.c_double, ctypes.c_int, ctypes.c_longlong] + [ctypes.c_void_p] * 4
+        self._lib = self._load(self.source)
+        self._hlib = None
+
+    @staticmethod
+    def _load(source):
+        lib = ctypes.CDLL(build(source))
+        lib.rlg_launch.restype = ctypes.c_int
+        lib.rlg_launch.argtypes = [ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
+            ctypes.c_double, ctypes.c_int, ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        return lib
+
+    def hessian(self, inputs, tol=1e-9, invcheck=True, max_steps=10**9):
+        """Batched reference `hessian(program, fname, args_i)` (autodiff.py:
+        216-257) over the Float parameters: the gradient sweeps over Dual
+        numbers, one launch per tangent direction.  Returns (H, fail) with H
+        of shape (n, F, F), H[:, k, j] = d(cotangent k) / d(parameter j)."""
+        if self._hlib is None:
+            src, _, _ = generate(self._text, self.fname, self._ints, mode="hess")
+            self._hlib = self._load(src)
+        cols = []
+        fail = None
+        for j in range(len(self.floats)):
+            _, _, f, h = self._run(self._hlib, inputs, None, tol, invcheck, max_steps, dir_=j)
+            cols.append(h)
+            fail = f if fail is None else torch.maximum(fail, f)
+        H = torch.stack(cols, -1).permute(1, 0, 2).contiguous()   # (n, F_k, F_j)
+        return H, fail
 
     def gradient(self, inputs, seeds=None, tol=1e-9, invcheck=True, max_steps=10**9):
+        primal, grads, fail, _ = self._run(self._lib, inputs, seeds, tol, invcheck, max_steps)
+        return primal, grads, fail
+
+    def _run(self, lib, inputs, seeds, tol, invcheck, max_steps, dir_=-1):
         if not torch.cuda.is_available():
             raise UnsupportedProgram("codegen kernels need a CUDA device (no CPU path)")
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -1217,17 +1318,19 @@ class CompiledFunction:
                           device=dev)
         fout = torch.empty_like(fin)
         gout = torch.empty_like(fin)
+        hout = torch.empty_like(fin) if dir_ >= 0 else None
         fail = torch.empty(n, dtype=torch.uint8, device=dev)
-        rc = self._lib.rlg_launch(n, fin.data_ptr(), iin.data_ptr(), sv.data_ptr(), float(tol),
-                                  int(bool(invcheck)), int(max_steps), fout.data_ptr(),
-                                  gout.data_ptr(), fail.data_ptr(),
-                                  torch.cuda.current_stream().cuda_stream)
+        rc = lib.rlg_launch(n, fin.data_ptr(), iin.data_ptr(), sv.data_ptr(), float(tol),
+                            int(bool(invcheck)), int(max_steps), fout.data_ptr(), gout.data_ptr(),
+                            fail.data_ptr(), int(dir_),
+                            hout.data_ptr() if hout is not None else None,
+                            torch.cuda.current_stream().cuda_stream)
         if rc:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
         primal = {p: fout[j] for j, p in enumerate(self.floats)}
         primal.update({p: inputs[p] for p in self.ints})
         grads = {p: gout[j] for j, p in enumerate(self.floats)}
-        return primal, grads, fail
+        return primal, grads, fail, hout
 
 
 def compile_function(source_text, fname, int_params=()):

@@ -81,3 +81,44 @@ def test_generated_kernel_checks(cuda):
     _, _, fail = k.gradient({"y!": 0.0, "x": x})
     torch.cuda.synchronize()
     assert fail.cpu().tolist() == [0, 2]                 # x = 0 releases cleanly; DirtyAncilla
+
+
+@pytest.mark.parametrize("fn", list(CASES))
+def test_generated_hessian_matches_reference(cuda, golden, fn):
+    """The same generated code over Dual numbers: reference hessian()
+    (forward-over-reverse) for every program, one launch per direction."""
+    floats, ints, exact = CASES[fn]
+    g = golden("codegen")
+    X, H, E = g[fn + "_x"], g[fn + "_hess"], g[fn + "_hess_err"]
+    k = codegen.compile_function(src(fn), fn, int_params=tuple(ints))
+    inputs = {nm: torch.as_tensor(X[:, j].copy(), device=cuda) for j, nm in enumerate(floats)}
+    inputs.update(ints)
+    Hg, fail = k.hessian(inputs)
+    torch.cuda.synchronize()
+    names = np.array([ERROR_NAMES[int(c)] for c in fail.cpu().numpy()])
+    assert np.array_equal(names, E)
+    ok = E == ""
+    Hd = Hg.cpu().numpy()[ok]
+    if exact:
+        assert np.array_equal(Hd, H[ok])
+    else:
+        assert np.allclose(Hd, H[ok], rtol=1e-11, atol=1e-12)
+
+
+def test_generic_besselj_hessian_matches_reference(cuda, golden):
+    from test_hess_gpu import tol_d2
+    g = golden("hess")
+    m = g["nu"] == 2
+    z = g["z"][m][:200]
+    k = codegen.compile_function(open(os.path.join(REPO, "paper_2003_04617_b200", "programs",
+                                                   "besselj.rnl")).read(),
+                                 "besselj", int_params=("nu",))
+    Hg, fail = k.hessian({"out!": 0.0, "z": torch.as_tensor(z, device=cuda), "nu": 2})
+    torch.cuda.synchronize()
+    err = g["err"][m][:200]
+    assert np.array_equal(np.array([ERROR_NAMES[int(c)] for c in fail.cpu().numpy()]), err)
+    ok = err == ""
+    ref = g["H"][m][:200][ok]
+    Hd = Hg.cpu().numpy()[ok]
+    assert (Hd[:, 0, :] == 0).all() and (Hd[:, :, 0] == 0).all()
+    assert (np.abs(Hd[:, 1, 1] - ref[:, 1, 1]) <= tol_d2(ref[:, 1, 1], z[ok], 2)).all()
