@@ -1207,9 +1207,11 @@ def _cache_dir():
 
 
 def _nvcc():
+    import shutil
     for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
-        if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
-            return c
+        path = c if c and os.path.isabs(c) else (shutil.which(c) if c else None)
+        if path and os.path.exists(path):
+            return path
     raise NativeLibraryError("nvcc not found (codegen compiles generated kernels with it)")
 
 
