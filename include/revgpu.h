@@ -49,6 +49,8 @@ enum rl_status {
   RL_ERR_KIND = 7,          /* KindError              errors.py:111                        */
   RL_ERR_INDEX = 8,         /* IndexOutOfBounds       errors.py:103; values.py:172-183     */
   RL_ERR_OVERFLOW = 9,      /* Python OverflowError from math.exp (values.py:362)          */
+  RL_ERR_ALIAS = 10,        /* AliasedArguments (generated kernels) interpreter.py:624-658 */
+  RL_ERR_ASSERT = 11,       /* AssertFailed @safe assert (generated kernels)               */
   RL_ERR_INVALID = -1,      /* bad argument: null pointer, negative size, bad shape        */
   RL_ERR_CUDA = -2,         /* CUDA runtime error (see rl_last_error())                    */
   RL_ERR_NO_DEVICE = -3     /* no sm_100 device visible                                     */

@@ -290,8 +290,85 @@ def gen_codegen():
     print("codegen goldens written")
 
 
+def _leaves_of(value, shape):
+    """Flatten a scalar / Array value (or its cotangent structure) in leaf order."""
+    if not shape:
+        return [np.nan if value is None else float(value)]
+    return [np.nan if v is None else float(v) for v in value.data]
+
+
+def gen_codegen_arrays():
+    """reference gradient() / hessian() of the array test programs
+    (tests/golden/codegen/{quad,mix}.rnl).  Rows hold the Float leaves in
+    codegen's column order (parameters in order, array cells row-major)."""
+    from revlang.autodiff import hessian
+    from revlang.values import Array
+    cases = {
+        # name: (file, fn, [(param, shape or None)], ints, seeds, rows, hessian?)
+        "quad": ("quad", "quad", [("q!", ()), ("r!", (3,)), ("A", (3, 3)), ("u", (3,))],
+                 {}, None, 40, True),
+        "quad_bad": ("quad", "quad", [("q!", ()), ("r!", (2,)), ("A", (3, 2)), ("u", (2,))],
+                     {}, None, 4, False),
+    }
+    xseed = [("x", (("idx", (1,)),), 1.0), ("x", (("idx", (3,)),), -0.5)]
+    for k, m in ((1, 2), (3, 3), (5, 1), (2, 4)):
+        cases[f"mix_fwd_{k}{m}"] = ("mix", "mix_fwd", [("x", (4,))], {"k": k, "m": m}, xseed,
+                                    6, False)
+    for k, m in ((1, 2), (3, 3), (0, 1)):
+        cases[f"mix_grad_{k}{m}"] = ("mix", "mix_grad", [("y!", ()), ("x", (4,))],
+                                     {"k": k, "m": m}, None, 6, True)
+    cases["mix_arity"] = ("mix", "mix_arity", [("y!", ()), ("x", (4,))], {"k": 1}, None, 4,
+                          False)
+    out = {}
+    for case, (file, fn, fparams, ints, seeds, n, with_h) in cases.items():
+        prog = parse_program(open(os.path.join(OUT_DIR, "codegen", file + ".rnl")).read())
+        pn = prog.get(fn).param_names()
+        sizes = [int(np.prod(shp)) if shp else 1 for _, shp in fparams]
+        NL = sum(sizes)
+        rng = np.random.default_rng(sum(map(ord, case)))
+        X = rng.uniform(-1.5, 1.5, (n, NL))
+        P, G = np.full((n, NL), np.nan), np.full((n, NL), np.nan)
+        H = np.full((n, NL, NL), np.nan)
+        errs, herrs = [], []
+        for i in range(n):
+            vals, b = {}, 0
+            for (nm, shp), sz in zip(fparams, sizes):
+                row = [float(v) for v in X[i, b:b + sz]]
+                b += sz
+                if not shp:
+                    vals[nm] = row[0]
+                elif len(shp) == 1:
+                    vals[nm] = Array.vector(row)
+                else:
+                    vals[nm] = Array.matrix([row[r * shp[1]:(r + 1) * shp[1]]
+                                             for r in range(shp[0])])
+            call = [ints[nm] if nm in ints else vals[nm] for nm in pn]
+            r, en = _err_name(lambda: gradient(prog, GradRequest(fn, call, seeds=seeds)))
+            errs.append(en)
+            if r is not None:
+                prim, grads = r
+                pl, gl = [], []
+                for nm, shp in fparams:
+                    pl += _leaves_of(prim[pn.index(nm)], shp)
+                    gl += _leaves_of(grads[nm], shp)
+                P[i], G[i] = pl, gl
+            if with_h:
+                h, hn = _err_name(lambda: hessian(prog, fn, call))
+                herrs.append(hn)
+                if h is not None:
+                    H[i] = h.matrix
+        out[case + "_x"], out[case + "_primal"], out[case + "_grad"] = X, P, G
+        out[case + "_err"] = np.array(errs)
+        if with_h:
+            out[case + "_hess"], out[case + "_hess_err"] = H, np.array(herrs)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_arrays.npz"), **out)
+    print("codegen array goldens written:",
+          {c: sorted(set(out[c + "_err"])) for c in cases})
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
-    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen"]
+    which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
+                              "codegen_arrays"]
     for w in which:
         globals()["gen_" + w]()

@@ -84,7 +84,8 @@ def _f64(a):
 # status codes (include/revgpu.h) -> reference exception class names
 ERROR_NAMES = {0: "", 1: "PostconditionMismatch", 2: "DirtyAncilla", 3: "RevDomainError",
                4: "LoopIteratorMutated", 5: "RevError", 6: "FuelExhausted", 7: "KindError",
-               8: "IndexOutOfBounds", 9: "OverflowError"}
+               8: "IndexOutOfBounds", 9: "OverflowError", 10: "AliasedArguments",
+               11: "AssertFailed"}
 
 
 def besselj_grad(nu, z, thr=1e-16, tol=1e-9, seed=1.0, max_trips=10**8, invcheck=True):

@@ -72,7 +72,7 @@ def _tokenize(src):
             while j < n and (src[j].isalnum() or src[j] == "_"):
                 j += 1
             word = src[i:j]
-            if word not in ("@routine", "~@routine"):
+            if word not in ("@routine", "~@routine", "@safe"):
                 raise UnsupportedProgram(f"codegen: macro {word!r} is not supported")
             toks.append(("macro", word))
             i = j
@@ -138,6 +138,18 @@ class Var:
 
 
 @dataclass(frozen=True)
+class IView:
+    name: str
+    idx: tuple             # Int index expressions (1-based)
+
+
+@dataclass(frozen=True)
+class Safe:
+    kind: str              # "assert" | "print"
+    exprs: tuple
+
+
+@dataclass(frozen=True)
 class Un:
     op: str
     e: object
@@ -159,7 +171,7 @@ class Call:
 @dataclass(frozen=True)
 class Instr:
     op: str
-    target: str
+    target: object         # Var / IView
     fname: str
     args: tuple            # Lit / Var atoms
 
@@ -220,6 +232,7 @@ class _Parser:
     def __init__(self, src):
         self.t = _tokenize(src)
         self.i = 0
+        self.arrays = {}
 
     @property
     def cur(self):
@@ -254,16 +267,22 @@ class _Parser:
             fname = self.name()
             self.expect("punct", "(")
             params = []
+            arrays = set()
             while not self.at("punct", ")"):
-                params.append(self.name())
+                pn = self.name()
+                params.append(pn)
                 if self.at("punct", "::"):
-                    raise UnsupportedProgram("codegen: array / typed parameters are not supported")
+                    self.adv()
+                    if self.name() != "array":
+                        raise UnsupportedProgram("codegen: only ::array parameters are supported")
+                    arrays.add(pn)
                 if self.at("punct", ","):
                     self.adv()
             self.adv()
             body = self.block(("end",))
             self.expect("name", "end")
             fns[fname] = (tuple(params), body)
+            self.arrays[fname] = arrays
         return fns
 
     def block(self, stops):
@@ -280,6 +299,19 @@ class _Parser:
         if self.at("macro", "~@routine"):
             self.adv()
             return REnd()
+        if self.at("macro", "@safe"):
+            self.adv()
+            kind = self.name()
+            if kind not in ("assert", "print"):
+                raise UnsupportedProgram("codegen: @safe takes assert(...) or print(...)")
+            self.expect("punct", "(")
+            exprs = []
+            while not self.at("punct", ")"):
+                exprs.append(self.expr())
+                if self.at("punct", ","):
+                    self.adv()
+            self.adv()
+            return Safe(kind, tuple(exprs))
         if self.at("name", "begin"):
             self.adv()
             body = self.block(("end",))
@@ -333,14 +365,13 @@ class _Parser:
         target = self.name()
         if self.at("punct", "("):
             raise UnsupportedProgram("codegen: function calls / SWAP / ROT are not supported")
-        if self.at("punct", "["):
-            raise UnsupportedProgram("codegen: indexed views are not supported")
-        if self.at("punct", "<-"):
-            self.adv()
-            return Alloc(target, self.expr())
-        if self.at("punct", "->"):
-            self.adv()
-            return Dealloc(target, self.expr())
+        tview = self.index_tail(target)
+        if self.at("punct", "<-") or self.at("punct", "->"):
+            if isinstance(tview, IView):
+                raise UnsupportedProgram("codegen: only a plain name can be (de)allocated")
+            alloc = self.adv()[1] == "<-"
+            return (Alloc if alloc else Dealloc)(target, self.expr())
+        target = tview
         if self.cur[0] == "punct" and self.cur[1] in ("+=", "-=", "*=", "/="):
             op = self.adv()[1]
             fname, args = self.instr_rhs()
@@ -355,10 +386,22 @@ class _Parser:
             return Lit(-self.adv()[1])
         if self.at("name", "true") or self.at("name", "false"):
             raise UnsupportedProgram("codegen: Bool cells are not supported")
-        v = self.name()
-        if self.at("punct", "[") or self.at("punct", "."):
-            raise UnsupportedProgram("codegen: indexed views are not supported")
-        return Var(v)
+        return self.index_tail(self.name())
+
+    def index_tail(self, name):
+        """name or name[i, j] (a view); field views are not supported."""
+        if self.at("punct", "."):
+            raise UnsupportedProgram("codegen: field views are not supported")
+        if not self.at("punct", "["):
+            return Var(name)
+        self.adv()
+        idx = []
+        while not self.at("punct", "]"):
+            idx.append(self.expr())
+            if self.at("punct", ","):
+                self.adv()
+        self.adv()
+        return IView(name, tuple(idx))
 
     def instr_rhs(self):
         if self.cur[0] == "name" and self.cur[1] not in _KEYWORDS and self.peek() == ("punct", "("):
@@ -452,9 +495,7 @@ class _Parser:
                     self.adv()
             self.adv()
             return Call(v, tuple(args))
-        if self.at("punct", "[") or self.at("punct", "."):
-            raise UnsupportedProgram("codegen: indexed views are not supported")
-        return Var(v)
+        return self.index_tail(v)
 
 
 # ---------------------------------------------------------------------------
@@ -488,6 +529,8 @@ def _invert(s):
         return While(s.post, s.pre, _invert_list(s.body))
     if isinstance(s, For):
         return For(s.var, s.b, _neg_expr(s.s), s.a, _invert_list(s.body))
+    if isinstance(s, Safe):
+        return s                       # irreversible external statement: re-executed as is
     if isinstance(s, tuple):
         return _invert_list(s)
     raise UnsupportedProgram(f"codegen: cannot invert {s!r}")
@@ -638,6 +681,23 @@ __device__ __forceinline__ Dl g_pow(Dl a, Dl b, int &c) {
   if (b.t != 0.0) t = t + r * g_log(a.p, c) * b.t;
   return Dl(r, t);
 }
+#define RC_INDEX 8
+#define RC_ALIAS 10
+#define RC_ASSERT 11
+// Array._offset (values.py:172-183): 1-based, row-major, IndexOutOfBounds
+__device__ __forceinline__ long long rl_off1(long long i, long long n, int &c) {
+  if (i < 1 || i > n) { if (!c) c = RC_INDEX; return 0; }
+  return i - 1;
+}
+__device__ __forceinline__ long long rl_off2(long long i, long long n1, long long j, long long n2,
+                                             int &c) {
+  if (i < 1 || i > n1 || j < 1 || j > n2) { if (!c) c = RC_INDEX; return 0; }
+  return (i - 1) * n2 + (j - 1);
+}
+__device__ __forceinline__ long long rl_offbad(int &c) {   // wrong number of indices
+  if (!c) c = RC_INDEX;
+  return 0;
+}
 __device__ __forceinline__ long long g_imod(long long a, long long b, int &c) {
   if (b == 0) { if (!c) c = RC_DOMAIN; return 0; }
   long long r = a % b;
@@ -657,10 +717,22 @@ def _c_double(v):
     return float(v).hex()
 
 
+@dataclass(frozen=True)
+class _Ref:
+    """A storage cell an instruction touches: C lvalues of its value and
+    cotangent, its kind, the root name and (array cells) the offset temp."""
+    v: str
+    g: str
+    kind: str
+    root: str
+    off: object = None
+
+
 class _Emitter:
-    def __init__(self, params, kinds, body, fname):
+    def __init__(self, params, kinds, body, fname, shapes=None):
         self.params = params
-        self.kinds = dict(kinds)      # name -> "f" | "u" | "i"
+        self.kinds = dict(kinds)      # name -> "f" | "u" | "i"  ("a": Float array param)
+        self.shapes = dict(shapes or {})
         self.body = body
         self.fname = fname
         self.lines = []
@@ -673,7 +745,45 @@ class _Emitter:
         k = self.kinds.get(name)
         if k is None:
             raise UnsupportedProgram(f"codegen: {name!r} is used before it is allocated")
+        if k == "a":
+            raise KindError(f"{name!r} is an array; index it (instructions and expressions "
+                            "take scalar cells)")
         return k
+
+    def offset(self, v):
+        """C expression of the row-major offset of view v (Array._offset,
+        values.py:172-183); an out-of-range index sets RC_INDEX."""
+        shape = self.shapes.get(v.name)
+        if shape is None:
+            raise KindError(f"{v.name!r} is not an array parameter")
+        idx = [self.int_expr(e, "array index") for e in v.idx]
+        if len(idx) != len(shape):
+            return "rl_offbad(code)"
+        if len(idx) == 1:
+            return f"rl_off1({idx[0]}, {shape[0]}LL, code)"
+        return f"rl_off2({idx[0]}, {shape[0]}LL, {idx[1]}, {shape[1]}LL, code)"
+
+    def view_ref(self, a):
+        """_Ref of an instruction operand; array offsets land in temps (the
+        reference's readers evaluate indices in operand order)."""
+        if isinstance(a, IView):
+            o = self.new("o")
+            self.w(f"const long long {o} = {self.offset(a)};")
+            c = _cid(a.name)
+            return _Ref(f"v_{c}[{o}]", f"g_{c}[{o}]", "f", a.name, o)
+        k = self.kind(a.name)
+        c = _cid(a.name)
+        return _Ref(f"v_{c}", f"g_{c}", k, a.name)
+
+    def alias(self, a, b, label):
+        """_alias_checks (interpreter.py:624-657): same root and overlapping
+        storage ids -> AliasedArguments, at run time like the reference."""
+        if a is None or b is None or a.root != b.root:
+            return
+        if a.off is None or b.off is None:
+            self.w(f"if (!code) code = RC_ALIAS; goto {label};")
+        else:
+            self.w(f"if ({a.off} == {b.off}) {{ code = RC_ALIAS; goto {label}; }}")
 
     def infer_alloc(self, name, e):
         k = "u" if isinstance(e, Call) and e.f == "ulog" else self.expr_kind(e)
@@ -691,11 +801,15 @@ class _Emitter:
         if isinstance(e, Var):
             k = self.kind(e.name)
             return "f" if k == "u" else k
+        if isinstance(e, IView):
+            return "f"
         if isinstance(e, Un):
             return self.expr_kind(e.e)
         if isinstance(e, Call):
             if e.f == "ulog":
                 return "u"
+            if e.f in ("length", "size"):
+                return "i"
             if e.f in ("min", "max"):
                 ks = {self.expr_kind(a) for a in e.args}
                 return "i" if ks == {"i"} else "f"
@@ -742,9 +856,33 @@ class _Emitter:
             if k == "u":
                 return f"g_exp(v_{_cid(e.name)}, code)", "f"       # to_real(ULog)
             return f"v_{_cid(e.name)}", k
+        if isinstance(e, IView):
+            return f"v_{_cid(e.name)}[{self.offset(e)}]", "f"
         if isinstance(e, Un):
             s, k = self.expr(e.e)
             return f"(-{s})", k
+        if isinstance(e, Call) and e.f in ("length", "size"):
+            # numerics._expr_length / _expr_size: shapes are compile-time here
+            a0 = e.args[0] if e.args else None
+            if not isinstance(a0, Var) or a0.name not in self.shapes:
+                raise KindError(f"{e.f}() needs an array")
+            shape = self.shapes[a0.name]
+            if e.f == "length":
+                if len(e.args) != 1:
+                    raise KindError("length() takes one array")
+                return f"{math.prod(shape)}LL", "i"
+            if len(e.args) != 2:
+                raise KindError("size() takes an array and a dimension")
+            d0 = e.args[1]
+            if isinstance(d0, Lit) and isinstance(d0.v, int) and not isinstance(d0.v, bool):
+                if 1 <= d0.v <= len(shape):
+                    return f"{shape[d0.v - 1]}LL", "i"
+                return "rl_offbad(code)", "i"
+            d = self.int_expr(d0, "size dimension")
+            tab = ", ".join(f"{n}LL" for n in shape)
+            return (f"([&]() -> long long {{ const long long d_ = {d}; const long long s_[] = {{{tab}}};"
+                    f" if (d_ < 1 || d_ > {len(shape)}) {{ if (!code) code = RC_INDEX; return 0; }}"
+                    f" return s_[d_ - 1]; }}())"), "i"
         if isinstance(e, Call):
             args = [self.expr(a) for a in e.args]
             f = e.f
@@ -809,21 +947,21 @@ class _Emitter:
         return s
 
     # instruction atoms ------------------------------------------------
-    def atom_real(self, a):
+    def atom_real(self, a, r):
         """The real value of an instruction argument (_arg_real)."""
         if isinstance(a, Lit):
             if isinstance(a.v, bool):
                 raise UnsupportedProgram("codegen: Bool arguments are not supported")
             return _c_double(a.v)
-        k = self.kind(a.name)
-        if k == "u":
-            return f"g_exp(v_{_cid(a.name)}, code)"
-        if k == "i":
-            return f"R((double)v_{_cid(a.name)})"
-        return f"v_{_cid(a.name)}"
+        if r.kind == "u":
+            return f"g_exp({r.v}, code)"
+        if r.kind == "i":
+            return f"R((double){r.v})"
+        return r.v
 
-    def tracked(self, a):
-        return isinstance(a, Var) and self.kind(a.name) in ("f", "u")
+    @staticmethod
+    def tracked(r):
+        return r is not None and r.kind in ("f", "u")
 
     def apply_fn(self, fname, xs):
         if fname == "identity":
@@ -894,7 +1032,16 @@ class _Emitter:
     def stmt(self, s, grad, label):
         if isinstance(s, Instr):
             self.instr(s, grad, label)
+        elif isinstance(s, Safe):
+            if s.kind != "assert":
+                raise UnsupportedProgram("codegen: @safe print has no device equivalent")
+            for e in s.exprs:                 # interpreter.py:800-811
+                c = self.cond(e)
+                self.w(f"{{ const bool ok = {c}; if (code) goto {label};")
+                self.w(f"  if (!ok) {{ code = RC_ASSERT; goto {label}; }} }}")
         elif isinstance(s, Alloc):
+            if s.name in self.shapes:
+                raise UnsupportedProgram(f"codegen: {s.name!r} shadows a parameter")
             self.infer_alloc(s.name, s.e)
             k = self.kinds[s.name]
             val, vk = self.expr(s.e)
@@ -983,66 +1130,75 @@ class _Emitter:
             raise UnsupportedProgram(f"codegen: unsupported statement {s!r}")
 
     def instr(self, s, grad, label):
-        t = s.target
-        tk = self.kind(t)
+        self.w("{")
+        self.depth += 1
+        self.instr_body(s, grad, label)
+        self.depth -= 1
+        self.w("}")
+
+    def instr_body(self, s, grad, label):
         args = s.args
-        for a in args:
-            if isinstance(a, Var) and a.name == t:
-                raise AliasedArguments("an instruction's target may not alias its inputs")
-        if grad:
-            names = [a.name for a in args if isinstance(a, Var)]
-            if len(names) != len(set(names)):
-                raise AliasedArguments("shared reads are rejected under differentiation "
-                                       "(rewrite y += x * x as y += x ^ 2)")
-        T = _cid(t)
+        # readers first (target, then inputs: index errors), then the alias
+        # checks (interpreter.py:887-948)
+        tr = self.view_ref(s.target)
+        refs = [None if isinstance(a, Lit) else self.view_ref(a) for a in args]
+        if tr.off is not None or any(r is not None and r.off is not None for r in refs):
+            self.fail_check(label)
+        for r in refs:
+            self.alias(tr, r, label)          # an instruction's target may not alias its inputs
+        if grad:                              # shared reads under differentiation
+            for i in range(len(refs)):
+                for j in range(i + 1, len(refs)):
+                    self.alias(refs[i], refs[j], label)
+        tk = tr.kind
+        TV, TG = tr.v, tr.g
         if s.op in ("+=", "-="):
             if tk == "u":
                 raise KindError("+=/-= on a logarithmic number")
             if tk == "i":
                 if s.fname not in ("identity", "add", "sub", "neg") or any(
                         isinstance(a, Lit) and isinstance(a.v, float) or
-                        (isinstance(a, Var) and self.kind(a.name) != "i") for a in args):
+                        (r is not None and r.kind != "i") for a, r in zip(args, refs)):
                     raise UnsupportedProgram("codegen: Int targets take Int +, - and identity")
-                xs = [(f"{a.v}LL" if isinstance(a, Lit) else f"v_{_cid(a.name)}") for a in args]
+                xs = [(f"{a.v}LL" if isinstance(a, Lit) else r.v) for a, r in zip(args, refs)]
                 fv = self.apply_fn(s.fname, xs)
-                self.w(f"v_{T} = v_{T} {'+' if s.op == '+=' else '-'} ({fv});")
+                self.w(f"{TV} = {TV} {'+' if s.op == '+=' else '-'} ({fv});")
                 return
             if s.fname == "convert":
                 (a,), xs = args, None
-                fv = self.atom_real(a)
+                fv = self.atom_real(a, refs[0])
             else:
-                xs = [self.atom_real(a) for a in args]
+                xs = [self.atom_real(a, r) for a, r in zip(args, refs)]
                 fv = self.apply_fn(s.fname, xs)
             fvv = self.new("fv")
             self.w(f"{{ const R {fvv} = {fv};")
             self.w(f"  if (code) goto {label};")
-            self.w(f"  v_{T} = v_{T} {'+' if s.op == '+=' else '-'} {fvv}; }}")
+            self.w(f"  {TV} = {TV} {'+' if s.op == '+=' else '-'} {fvv}; }}")
             if not grad:
                 return
             sign = "1.0" if s.op == "-=" else "-1.0"
             sg = self.new("sg")
-            self.w(f"{{ const R {sg} = {sign} * g_{T};")
+            self.w(f"{{ const R {sg} = {sign} * {TG};")
             if s.fname == "convert":
-                (a,) = args
-                if self.tracked(a):
-                    if self.kind(a.name) == "u":
+                r = refs[0]
+                if self.tracked(r):
+                    if r.kind == "u":
                         # d value / d exponent = value
-                        self.w(f"  g_{_cid(a.name)} = g_{_cid(a.name)} + {sg} * g_exp(v_{_cid(a.name)}, code);")
+                        self.w(f"  {r.g} = {r.g} + {sg} * g_exp({r.v}, code);")
                     else:
-                        self.w(f"  g_{_cid(a.name)} = g_{_cid(a.name)} + {sg};")
+                        self.w(f"  {r.g} = {r.g} + {sg};")
             else:
                 parts = self.partials(s.fname, xs)
-                for a, p in zip(args, parts):
-                    if not self.tracked(a):
+                for r, p in zip(refs, parts):
+                    if not self.tracked(r):
                         continue
-                    A = _cid(a.name)
                     if isinstance(p, tuple):
                         tag, pv, x0 = p
                         cond = (f"(double)R({x0}) == 0.0" if tag == "ABS"
                                 else f"!((double)R({x0}) > 0.0)")
                         self.w(f"  if ({cond}) {{ if (!code) code = RC_DOMAIN; goto {label}; }}")
                         p = pv
-                    self.w(f"  g_{A} = g_{A} + {sg} * {p};")
+                    self.w(f"  {r.g} = {r.g} + {sg} * {p};")
             self.w(f"  if (code) goto {label}; }}")
             return
         # *= and /= : the target is a logarithmic number
@@ -1050,28 +1206,29 @@ class _Emitter:
             raise KindError(f"{s.op} target must be a logarithmic number")
         if s.fname in ("identity", "convert"):
             (a,) = args
-            if isinstance(a, Var) and self.kind(a.name) == "u":
-                contrib = f"v_{_cid(a.name)}"
+            r = refs[0]
+            if r is not None and r.kind == "u":
+                contrib = r.v
             else:
-                contrib = f"g_log({self.atom_real(a)}, code)"
+                contrib = f"g_log({self.atom_real(a, r)}, code)"
         else:
             if len(args) != 1 and grad:
                 raise UnsupportedProgram("codegen: *= / /= take one argument under differentiation")
-            contrib = f"g_log({self.apply_fn(s.fname, [self.atom_real(a) for a in args])}, code)"
+            contrib = f"g_log({self.apply_fn(s.fname, [self.atom_real(a, r) for a, r in zip(args, refs)])}, code)"
         cv = self.new("c")
         self.w(f"{{ const R {cv} = {contrib};")
         self.w(f"  if (code) goto {label};")
-        self.w(f"  v_{T} = v_{T} {'+' if s.op == '*=' else '-'} {cv}; }}")
+        self.w(f"  {TV} = {TV} {'+' if s.op == '*=' else '-'} {cv}; }}")
         if not grad:
             return
         (a,) = args
-        if self.tracked(a):
+        r = refs[0]
+        if self.tracked(r):
             sign = "1.0" if s.op == "/=" else "-1.0"
-            A = _cid(a.name)
-            if self.kind(a.name) == "u":
-                self.w(f"g_{A} = g_{A} + {sign} * g_{T};")
+            if r.kind == "u":
+                self.w(f"{r.g} = {r.g} + {sign} * {TG};")
             else:
-                self.w(f"g_{A} = g_{A} + g_div({sign} * g_{T}, {self.atom_real(a)}, code);")
+                self.w(f"{r.g} = {r.g} + g_div({sign} * {TG}, {self.atom_real(a, r)}, code);")
                 self.fail_check(label)
 
 
@@ -1094,27 +1251,59 @@ def _collect_vars(stmts, acc):
     return acc
 
 
-def generate(src, fname, int_params=(), mode="grad"):
+def _leaf_paths(shape):
+    """autodiff.leaf_paths (autodiff.py:41-63) of a Float array of `shape`."""
+    if len(shape) == 1:
+        return [(("idx", (i,)),) for i in range(1, shape[0] + 1)]
+    return [(("idx", (i, j)),) for i in range(1, shape[0] + 1) for j in range(1, shape[1] + 1)]
+
+
+def _check_shapes(arrays, declared, params):
+    shapes = {}
+    for p, shp in dict(arrays or {}).items():
+        if p not in params:
+            raise KindError(f"array_shapes names unknown parameter {p!r}")
+        shp = tuple(int(v) for v in (shp if isinstance(shp, (tuple, list)) else (shp,)))
+        if len(shp) not in (1, 2) or min(shp) < 1:
+            raise KindError(f"{p}: arrays are 1-d or 2-d with positive extents, got {shp}")
+        shapes[p] = shp
+    for p in declared:
+        if p not in shapes:
+            raise KindError(f"{p!r} is declared ::array; give its shape in array_shapes")
+    return shapes
+
+
+def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     """CUDA source of the batched gradient (mode "grad") or forward-over-reverse
     Hessian-column (mode "hess": the same code over Dual numbers, tangent on
-    the Float parameter `dir`) kernel of `fname`, and its layout."""
+    the Float leaf `dir`) kernel of `fname`, and its layout: (source, float
+    parameters, Int parameters, leaves) where leaves lists (parameter, leaf
+    path) in the kernel's column order (scalars: path ())."""
     if mode not in ("grad", "hess"):
         raise KindError(f"codegen mode {mode!r}")
-    fns = _Parser(src).program()
+    parser = _Parser(src)
+    fns = parser.program()
     if fname not in fns:
         raise UnsupportedProgram(f"codegen: no function named {fname!r}")
     params, body = fns[fname]
     int_params = set(int_params)
-    kinds = {p: ("i" if p in int_params else "f") for p in params}
+    shapes = _check_shapes(array_shapes, parser.arrays.get(fname, ()), params)
+    if int_params & set(shapes):
+        raise KindError("a parameter cannot be both Int and an array")
+    kinds = {p: ("a" if p in shapes else "i" if p in int_params else "f") for p in params}
     fwd = _expand(body)
     inv = _expand(_invert_list(body))
-    floats = [p for p in params if kinds[p] == "f"]
+    floats = [p for p in params if kinds[p] != "i"]
     ints = [p for p in params if kinds[p] == "i"]
+    leaves, base = [], {}
+    for p in floats:
+        base[p] = len(leaves)
+        leaves += [(p, path) for path in (_leaf_paths(shapes[p]) if p in shapes else [()])]
     locals_ = sorted(_collect_vars(fwd, set()) | _collect_vars(inv, set()))
-    em_f = _Emitter(params, kinds, fwd, fname)
+    em_f = _Emitter(params, kinds, fwd, fname, shapes)
     em_f.depth = 2
     em_f.stmts(fwd, False, "fwd_done")
-    em_g = _Emitter(params, dict(em_f.kinds), inv, fname)
+    em_g = _Emitter(params, dict(em_f.kinds), inv, fname, shapes)
     em_g.depth = 2
     em_g.stmts(inv, True, "grad_done")
     allk = dict(em_f.kinds)
@@ -1126,8 +1315,9 @@ def generate(src, fname, int_params=(), mode="grad"):
         k = allk.get(v, "f")
         decl.append(f"    long long v_{_cid(v)} = 0;" if k == "i"
                     else f"    R v_{_cid(v)} = R(0.0), g_{_cid(v)} = R(0.0);")
-    NF, NI = len(floats), len(ints)
-    L = [_PRELUDE, "typedef Dl R;" if mode == "hess" else "typedef double R;",
+    NL = len(leaves)
+    hess = mode == "hess"
+    L = [_PRELUDE, "typedef Dl R;" if hess else "typedef double R;",
          f"extern \"C\" __global__ void rlg_kernel(long long n, const double *__restrict__ fin,"
          " const long long *__restrict__ iin, const double *__restrict__ seeds,"
          " double tol, int chk, long long fuel, double *__restrict__ fout,"
@@ -1136,43 +1326,60 @@ def generate(src, fname, int_params=(), mode="grad"):
          "  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;"
          " i += (long long)gridDim.x * blockDim.x) {",
          "    int code = 0;", "    long long ticks = 0;"]
-    for j, p in enumerate(floats):
-        L.append(f"    const R in_{_cid(p)} = R(fin[{j}LL * n + i]"
-                 + (f", dir == {j} ? 1.0 : 0.0);" if mode == "hess" else ");"))
-        L.append(f"    R v_{_cid(p)} = in_{_cid(p)}, g_{_cid(p)} = R(0.0);")
+    # columns: leaf b of every element at fin[b * n + i] (coalesced across the batch)
+    for p in floats:
+        b, c = base[p], _cid(p)
+        if p in shapes:
+            m = math.prod(shapes[p])
+            L.append(f"    R v_{c}[{m}], g_{c}[{m}];")
+            L.append(f"    for (int e = 0; e < {m}; ++e) {{")
+            L.append(f"      v_{c}[e] = R(fin[({b}LL + e) * n + i]"
+                     + (f", dir == {b} + e ? 1.0 : 0.0);" if hess else ");"))
+            L.append(f"      g_{c}[e] = R(0.0); }}")
+        else:
+            L.append(f"    R v_{c} = R(fin[{b}LL * n + i]"
+                     + (f", dir == {b} ? 1.0 : 0.0)" if hess else ")") + f", g_{c} = R(0.0);")
     for j, p in enumerate(ints):
         L.append(f"    long long v_{_cid(p)} = iin[{j}];")
     L += decl
+
+    def each_leaf(fmt):
+        """C lines applying fmt(col_expr, value_lvalue, grad_lvalue) to every leaf."""
+        out = []
+        for p in floats:
+            b, c = base[p], _cid(p)
+            if p in shapes:
+                m = math.prod(shapes[p])
+                out.append(f"    for (int e = 0; e < {m}; ++e) {{ "
+                           + fmt(f"({b}LL + e)", f"v_{c}[e]", f"g_{c}[e]") + " }")
+            else:
+                out.append("    " + fmt(f"{b}LL", f"v_{c}", f"g_{c}"))
+        return out
+
     L.append("    // ---- run_function (plain forward) ----")
     L += em_f.lines
     L.append("  fwd_done:")
     L.append("    if (code) {")
-    for j, p in enumerate(floats):
-        L.append(f"      fout[{j}LL * n + i] = NAN; gout[{j}LL * n + i] = NAN;")
-        if mode == "hess":
-            L.append(f"      hout[{j}LL * n + i] = NAN;")
+    L.append(f"      for (int e = 0; e < {NL}; ++e) {{ fout[e * n + i] = NAN; gout[e * n + i] = NAN;"
+             + (" hout[e * n + i] = NAN;" if hess else "") + " }")
     L.append("      fail[i] = (unsigned char)code; continue; }")
-    for j, p in enumerate(floats):
-        L.append(f"    fout[{j}LL * n + i] = rl_p(v_{_cid(p)});")
+    L += each_leaf(lambda col, v, g: f"fout[{col} * n + i] = rl_p({v});")
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
-    for j, p in enumerate(floats):
-        L.append(f"    g_{_cid(p)} = R(seeds[{j}]);            // coerce_to_kind: Dual(seed, 0)")
+    L.append("    // coerce_to_kind: a seed enters as Dual(seed, 0)")
+    L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);")
     L.append("    ticks = 0;")
     L += em_g.lines
     L.append("  grad_done:")
     L.append("    if (!code) {      // the backward pass must restore every argument")
-    for p in floats:
-        L.append(f"      if (!(fabs(rl_p(v_{_cid(p)}) - rl_p(in_{_cid(p)})) <= tol)) code = RC_REV;")
+    L += ["  " + x for x in each_leaf(
+        lambda col, v, g: f"if (!(fabs(rl_p({v}) - fin[{col} * n + i]) <= tol)) code = RC_REV;")]
     for j, p in enumerate(ints):
         L.append(f"      if (v_{_cid(p)} != iin[{j}]) code = RC_REV;")
     L.append("    }")
-    for j, p in enumerate(floats):
-        L.append(f"    gout[{j}LL * n + i] = code ? NAN : rl_p(g_{_cid(p)});")
-        if mode == "hess":
-            L.append(f"    hout[{j}LL * n + i] = code ? NAN : rl_t(g_{_cid(p)});")
+    L += each_leaf(lambda col, v, g: f"gout[{col} * n + i] = code ? NAN : rl_p({g});"
+                   + (f" hout[{col} * n + i] = code ? NAN : rl_t({g});" if hess else ""))
     L.append("    if (code) {")
-    for j, p in enumerate(floats):
-        L.append(f"      fout[{j}LL * n + i] = NAN;")
+    L.append(f"      for (int e = 0; e < {NL}; ++e) fout[e * n + i] = NAN;")
     L.append("    }")
     L.append("    fail[i] = (unsigned char)code;")
     L.append("  }")
@@ -1190,7 +1397,7 @@ extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, 
   return (int)cudaGetLastError();
 }
 """)
-    return "\n".join(L), floats, ints
+    return "\n".join(L), floats, ints, leaves
 
 
 # ---------------------------------------------------------------------------
@@ -1238,15 +1445,24 @@ class CompiledFunction:
     """A reversible function compiled to one batched CUDA kernel.
 
     `gradient(inputs, seeds)` is the batched `gradient(program,
-    GradRequest(fname, args_i, seeds))`: every Float parameter takes a CUDA
-    float64 tensor (one row per element) or a scalar, every Int parameter a
-    Python int; returns (primal outputs, gradients, fail codes) as dicts of
-    tensors keyed by parameter name (Int parameters carry no gradient)."""
+    GradRequest(fname, args_i, seeds))`: a Float parameter takes a CUDA
+    float64 tensor (one row per element) or a scalar, a Float array
+    parameter (shape fixed at compile time through `array_shapes`) a tensor
+    of shape (n, *shape) or one value of shape `shape` shared by every
+    element, an Int parameter a Python int.  Seeds are the reference's
+    (parameter, leaf path, cotangent) triples (autodiff.py:29-31; array
+    cells: ((\"idx\", (i,)),) or ((\"idx\", (i, j)),), 1-based).  Returns
+    (primal outputs, gradients, fail codes): dicts of tensors keyed by
+    parameter name (arrays keep their shape; Int parameters carry no
+    gradient)."""
 
-    def __init__(self, source_text, fname, int_params=()):
+    def __init__(self, source_text, fname, int_params=(), array_shapes=None):
         self.fname = fname
-        self._text, self._ints = source_text, tuple(int_params)
-        self.source, self.floats, self.ints = generate(source_text, fname, int_params)
+        self._text, self._ints, self._shapes = source_text, tuple(int_params), array_shapes
+        self.source, self.floats, self.ints, self.leaves = generate(
+            source_text, fname, int_params, array_shapes=array_shapes)
+        self.params = _Parser(source_text).program()[fname][0]
+        self.shapes = _check_shapes(array_shapes, (), self.params)
         self._lib = self._load(self.source)
         self._hlib = None
 
@@ -1259,37 +1475,51 @@ class CompiledFunction:
             ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
         return lib
 
+    def _default_seeds(self):
+        """autodiff.default_seeds (autodiff.py:99-110): the first parameter's
+        single leaf."""
+        first = self.params[0]
+        paths = [path for p, path in self.leaves if p == first]
+        if not paths:
+            raise KindError(f"first argument {first!r} has no differentiable leaf; "
+                            "pass explicit seeds")
+        if len(paths) > 1:
+            raise KindError(f"first argument {first!r} is not scalar; pass explicit seeds")
+        return [(first, paths[0], 1.0)]
+
     def hessian(self, inputs, tol=1e-9, invcheck=True, max_steps=10**9):
         """Batched reference `hessian(program, fname, args_i)` (autodiff.py:
-        216-257) over the Float parameters: the gradient sweeps over Dual
-        numbers, one launch per tangent direction.  Returns (H, fail) with H
-        of shape (n, F, F), H[:, k, j] = d(cotangent k) / d(parameter j)."""
+        216-257) over the Float leaves (self.leaves order): the gradient
+        sweeps over Dual numbers, one launch per tangent direction.  Returns
+        (H, fail) with H of shape (n, NL, NL), H[:, k, j] = d(cotangent of
+        leaf k) / d(leaf j)."""
+        self._default_seeds()                 # the reference seeds by default
         if self._hlib is None:
-            src, _, _ = generate(self._text, self.fname, self._ints, mode="hess")
+            src = generate(self._text, self.fname, self._ints, mode="hess",
+                           array_shapes=self._shapes)[0]
             self._hlib = self._load(src)
         cols = []
         fail = None
-        for j in range(len(self.floats)):
+        for j in range(len(self.leaves)):
             _, _, f, h = self._run(self._hlib, inputs, None, tol, invcheck, max_steps, dir_=j)
             cols.append(h)
             fail = f if fail is None else torch.maximum(fail, f)
-        H = torch.stack(cols, -1).permute(1, 0, 2).contiguous()   # (n, F_k, F_j)
+        H = torch.stack(cols, -1).permute(1, 0, 2).contiguous()   # (n, NL_k, NL_j)
         return H, fail
 
     def gradient(self, inputs, seeds=None, tol=1e-9, invcheck=True, max_steps=10**9):
         primal, grads, fail, _ = self._run(self._lib, inputs, seeds, tol, invcheck, max_steps)
         return primal, grads, fail
 
-    def _run(self, lib, inputs, seeds, tol, invcheck, max_steps, dir_=-1):
-        if not torch.cuda.is_available():
-            raise UnsupportedProgram("codegen kernels need a CUDA device (no CPU path)")
-        dev = torch.device("cuda", torch.cuda.current_device())
+    def _columns(self, inputs, dev):
+        """(NL, n) leaf columns of the Float inputs."""
         n = None
         for p in self.floats:
             v = inputs.get(p)
-            if isinstance(v, torch.Tensor):
-                if not v.is_cuda or v.dtype != torch.float64 or v.dim() != 1:
-                    raise KindError(f"{p} must be a 1-D CUDA float64 tensor")
+            shp = self.shapes.get(p, ())
+            if isinstance(v, torch.Tensor) and v.dim() == len(shp) + 1:
+                if not v.is_cuda or v.dtype != torch.float64 or tuple(v.shape[1:]) != shp:
+                    raise KindError(f"{p} must be a CUDA float64 tensor of shape (n, *{shp})")
                 n = v.shape[0] if n is None else n
                 if v.shape[0] != n:
                     raise KindError("all batched inputs need the same length")
@@ -1297,10 +1527,25 @@ class CompiledFunction:
             n = 1
         cols = []
         for p in self.floats:
+            shp = self.shapes.get(p, ())
+            m = math.prod(shp)
             v = inputs.get(p, 0.0)
-            cols.append(v.contiguous() if isinstance(v, torch.Tensor)
-                        else torch.full((n,), float(v), dtype=torch.float64, device=dev))
-        fin = torch.stack(cols) if cols else torch.zeros((0, n), dtype=torch.float64, device=dev)
+            if isinstance(v, torch.Tensor) and v.dim() == len(shp) + 1:
+                cols.append(v.reshape(n, m).t())
+            else:
+                t = torch.as_tensor(v, dtype=torch.float64).to(dev)
+                if tuple(t.shape) != shp:
+                    raise KindError(f"{p} must have shape {shp} (or (n, *{shp}))")
+                cols.append(t.reshape(m, 1).expand(m, n))
+        if not cols:
+            return n, torch.zeros((0, n), dtype=torch.float64, device=dev)
+        return n, torch.cat(cols).contiguous()
+
+    def _run(self, lib, inputs, seeds, tol, invcheck, max_steps, dir_=-1):
+        if not torch.cuda.is_available():
+            raise UnsupportedProgram("codegen kernels need a CUDA device (no CPU path)")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        n, fin = self._columns(inputs, dev)
         ivals = []
         for p in self.ints:
             v = inputs.get(p)
@@ -1308,16 +1553,16 @@ class CompiledFunction:
                 raise KindError(f"{p} must be an Int")
             ivals.append(v)
         iin = torch.tensor(ivals or [0], dtype=torch.int64, device=dev)
-        sd = {self.floats[0]: 1.0} if seeds is None else {}
-        if seeds is not None:
-            for pname, path, val in seeds:
-                if pname not in self.floats or path:
-                    raise KindError(f"seed target {pname!r} is not a Float scalar parameter")
-                sd[pname] = float(val)
-        if seeds is None and not self.floats:
-            raise KindError("no differentiable parameter to seed")
-        sv = torch.tensor([sd.get(p, 0.0) for p in self.floats] or [0.0], dtype=torch.float64,
-                          device=dev)
+        col = {leaf: k for k, leaf in enumerate(self.leaves)}
+        sv = [0.0] * max(1, len(self.leaves))
+        for pname, path, val in (self._default_seeds() if seeds is None else seeds):
+            if pname not in self.params:
+                raise KindError(f"seed names unknown parameter {pname!r}")
+            key = (pname, tuple((a, tuple(b)) for a, b in path))
+            if key not in col:
+                raise KindError("seed target is not a differentiable leaf")
+            sv[col[key]] = float(val)
+        sv = torch.tensor(sv, dtype=torch.float64, device=dev)
         fout = torch.empty_like(fin)
         gout = torch.empty_like(fin)
         hout = torch.empty_like(fin) if dir_ >= 0 else None
@@ -1329,13 +1574,18 @@ class CompiledFunction:
                             torch.cuda.current_stream().cuda_stream)
         if rc:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
-        primal = {p: fout[j] for j, p in enumerate(self.floats)}
+        primal, grads, b = {}, {}, 0
+        for p in self.floats:
+            shp = self.shapes.get(p, ())
+            m = math.prod(shp)
+            primal[p] = fout[b:b + m].t().reshape((n,) + shp)
+            grads[p] = gout[b:b + m].t().reshape((n,) + shp)
+            b += m
         primal.update({p: inputs[p] for p in self.ints})
-        grads = {p: gout[j] for j, p in enumerate(self.floats)}
         return primal, grads, fail, hout
 
 
-def compile_function(source_text, fname, int_params=()):
+def compile_function(source_text, fname, int_params=(), array_shapes=None):
     """Compile function `fname` of reversible-DSL source to a batched CUDA
     gradient kernel (see CompiledFunction)."""
-    return CompiledFunction(source_text, fname, int_params)
+    return CompiledFunction(source_text, fname, int_params, array_shapes)

@@ -76,6 +76,10 @@ class IndexOutOfBounds(RevError):
     pass
 
 
+class AssertFailed(RevError):
+    pass
+
+
 class KindError(RevError):
     pass
 
@@ -113,11 +117,14 @@ _CODE_CLASSES = {
     7: KindError,
     8: IndexOutOfBounds,
     9: OverflowError,  # CPython math.exp raises OverflowError (values.py:362)
+    10: AliasedArguments,
+    11: AssertFailed,
 }
 
 CODE_NAMES = {0: "", 1: "PostconditionMismatch", 2: "DirtyAncilla", 3: "RevDomainError",
               4: "LoopIteratorMutated", 5: "RevError", 6: "FuelExhausted", 7: "KindError",
-              8: "IndexOutOfBounds", 9: "OverflowError"}
+              8: "IndexOutOfBounds", 9: "OverflowError", 10: "AliasedArguments",
+              11: "AssertFailed"}
 
 _MESSAGES = {
     1: "branch or loop postcondition mismatch",
@@ -129,6 +136,8 @@ _MESSAGES = {
     7: "value-kind mismatch",
     8: "index out of bounds",
     9: "math range error",
+    10: "instruction arguments share storage",
+    11: "@safe assertion failed",
 }
 
 

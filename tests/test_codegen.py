@@ -8,18 +8,17 @@ import pytest
 
 from conftest import REPO
 from paper_2003_04617_b200 import codegen
-from paper_2003_04617_b200.errors import AliasedArguments, UnsupportedProgram
+from paper_2003_04617_b200.errors import KindError, UnsupportedProgram
 
 
 def src(name):
     return open(os.path.join(REPO, "tests", "golden", "codegen", name + ".rnl")).read()
 
 
-@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop"])
+@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix"])
 def test_inversion_is_an_involution(name):
-    fns = codegen._Parser(src(name)).program()
-    (params, body), = fns.values()
-    assert codegen._invert_list(codegen._invert_list(body)) == body
+    for params, body in codegen._Parser(src(name)).program().values():
+        assert codegen._invert_list(codegen._invert_list(body)) == body
 
 
 def test_besselj_parses_and_expands():
@@ -33,23 +32,47 @@ def test_besselj_parses_and_expands():
 
 
 def test_unsupported_constructs_are_rejected():
-    for text in ("fn f(y!::array, x)\n y![1] += x\nend\n",
-                 "fn f(y!, x)\n g(y!, x)\nend\n",
-                 "fn f(y!, x)\n y! += 1.0fx\nend\n"):
+    for text in ("fn f(y!, x)\n g(y!, x)\nend\n",
+                 "fn f(y!, x)\n y! += 1.0fx\nend\n",
+                 "fn f(y!, x)\n y!.re += x\nend\n",
+                 "fn f(y!, x)\n @safe print(x)\nend\n"):
         with pytest.raises(UnsupportedProgram):
             codegen.generate(text, "f")
 
 
-def test_static_aliasing_is_rejected():
-    with pytest.raises(AliasedArguments):
-        codegen.generate("fn f(y!, x)\n y! += x * x\nend\n", "f")
-    with pytest.raises(AliasedArguments):
-        codegen.generate("fn f(y!, x)\n y! += y! * x\nend\n", "f")
+def test_array_shapes_are_required_and_checked():
+    text = "fn f(y!::array, x)\n y![1] += x\nend\n"
+    with pytest.raises(KindError):                      # ::array without a shape
+        codegen.generate(text, "f")
+    with pytest.raises(KindError):
+        codegen.generate(text, "f", array_shapes={"y!": (2, 2, 2)})
+    with pytest.raises(KindError):                      # whole array as an operand
+        codegen.generate("fn f(y!, x::array)\n y! += x\nend\n", "f", array_shapes={"x": 3})
+    src_, floats, ints, leaves = codegen.generate(text, "f", array_shapes={"y!": (2, 3)})
+    assert floats == ["y!", "x"] and ints == []
+    assert leaves[:2] == [("y!", (("idx", (1, 1)),)), ("y!", (("idx", (1, 2)),))]
+    assert leaves[-1] == ("x", ()) and len(leaves) == 7
+
+
+def test_aliasing_is_checked_at_run_time():
+    """interpreter.py:624-657: same-root operands raise AliasedArguments when
+    the instruction runs (a branch never taken never raises), so the checks
+    are emitted into the kernel rather than rejected at compile time."""
+    src_ = codegen.generate("fn f(y!, x)\n y! += x * x\nend\n", "f")[0]
+    fwd, grad = src_.split("uncall_function")
+    assert "RC_ALIAS" not in fwd.split("run_function")[1] and "RC_ALIAS" in grad
+    src_ = codegen.generate("fn f(y!, x)\n y! += y! * x\nend\n", "f")[0]
+    assert "RC_ALIAS" in src_.split("run_function")[1].split("uncall_function")[0]
+    src_ = codegen.generate(src("mix"), "mix_fwd", ("k", "m"), array_shapes={"x": 4})[0]
+    assert "if (o1 == o2) { code = RC_ALIAS;" in src_
 
 
 def test_generated_source_compiles_for_sm100a(tmp_path, monkeypatch):
     monkeypatch.setenv("REVGPU_CODEGEN_CACHE", str(tmp_path))
-    source, floats, ints = codegen.generate(src("sink"), "sink", ("n",))
+    source, floats, ints, _ = codegen.generate(src("sink"), "sink", ("n",))
     assert floats == ["out!", "x", "y"] and ints == ["n"]
     so = codegen.build(source)
     assert os.path.exists(so)
+    source = codegen.generate(src("quad"), "quad", array_shapes={"r!": 3, "A": (3, 3), "u": 3},
+                              mode="hess")[0]
+    assert os.path.exists(codegen.build(source))
