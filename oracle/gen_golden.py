@@ -252,6 +252,7 @@ def gen_codegen():
         "mul_acc": (["y!", "a", "b"], {}, 64),
         "sink": (["out!", "x", "y"], {"n": 3}, 64),
         "wloop": (["acc!", "x"], {"n": 5}, 48),
+        "prims": (["a!", "b!", "c!", "th"], {"n!": 3}, 40),
     }
     out = {}
     for fn, (floats, ints, n) in cases.items():
@@ -366,9 +367,36 @@ def gen_codegen_arrays():
           {c: sorted(set(out[c + "_err"])) for c in cases})
 
 
+def gen_codegen_programs():
+    """reference hessian() of the paper programs themselves (programs/gmm.rnl
+    case c5 of gmm.npz, programs/ba.rnl observations 0-3 of ba.npz), for the
+    generic compiler's Dual-number kernels (gradient parity uses gmm.npz /
+    ba.npz directly)."""
+    from revlang.autodiff import hessian
+    out = {}
+    G = np.load(os.path.join(OUT_DIR, "gmm.npz"))
+    pre = "c5_"
+    d, K, N, m = (int(v) for v in G[pre + "dims"])
+    A = lambda a: Array.matrix(a.tolist()) if a.ndim == 2 else Array.vector(a.tolist())  # noqa
+    Z = lambda *s: A(np.zeros(s))  # noqa: E731
+    args = [0.0, A(G[pre + "alphas"]), A(G[pre + "means"]), A(G[pre + "icf"]), A(G[pre + "x"]),
+            Z(K, d), Z(K), Z(d), Z(d), Z(K), Array.vector([0] * K), float(G[pre + "gamma"]), m,
+            float(G[pre + "cst"])]
+    out["gmm_c5_hess"] = hessian(_prog("gmm.rnl"), "gmm", args).matrix
+    B = np.load(os.path.join(OUT_DIR, "ba.npz"))
+    Hs = []
+    for o in range(4):
+        args = [0.0, 0.0, Array.vector(B["cams"][o].tolist()), Array.vector(B["X"][o].tolist()),
+                float(B["w"][o]), float(B["feat"][o, 0]), float(B["feat"][o, 1])]
+        Hs.append(hessian(_prog("ba.rnl"), "ba_proj", args).matrix)
+    out["ba_hess"] = np.array(Hs)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_programs.npz"), **out)
+    print("codegen program hessians:", {k: v.shape for k, v in out.items()})
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
-                              "codegen_arrays"]
+                              "codegen_arrays", "codegen_programs"]
     for w in which:
         globals()["gen_" + w]()

@@ -42,6 +42,7 @@ import subprocess
 import tempfile
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from .errors import AliasedArguments, KindError, NativeLibraryError, UnsupportedProgram
@@ -147,6 +148,28 @@ class IView:
 class Safe:
     kind: str              # "assert" | "print"
     exprs: tuple
+
+
+@dataclass(frozen=True)
+class PCall:
+    """A statement call: a primitive (SWAP / ROT / IROT / NEG / INC / DEC) or
+    a user function, `uncall` for the ~f(...) form (reference FnCall /
+    UncallFn, reverser.py:96-103)."""
+    f: str
+    args: tuple            # views
+    uncall: bool = False
+
+
+@dataclass(frozen=True)
+class ArgCheck:
+    """Entry checks of an inlined call (interpreter.py:969-978): the strict
+    alias pairs over its argument views, then their reads (bounds)."""
+    views: tuple
+
+
+# numerics.py:30-33
+PRIM_ARITY = {"SWAP": 2, "ROT": 3, "IROT": 3, "NEG": 1, "INC": 1, "DEC": 1}
+PRIM_INV = {"SWAP": "SWAP", "ROT": "IROT", "IROT": "ROT", "NEG": "NEG", "INC": "DEC", "DEC": "INC"}
 
 
 @dataclass(frozen=True)
@@ -361,10 +384,13 @@ class _Parser:
             self.expect("name", "end")
             return For(var, a, s, b, body)
         if self.at("punct", "~"):
-            raise UnsupportedProgram("codegen: function (un)calls are not supported")
+            self.adv()
+            return PCall(self.name(), self.call_args(), True)
         target = self.name()
         if self.at("punct", "("):
-            raise UnsupportedProgram("codegen: function calls / SWAP / ROT are not supported")
+            if target == "XOR":
+                raise UnsupportedProgram("codegen: xor= / XOR (discrete kinds) are not supported")
+            return PCall(target, self.call_args(), False)
         tview = self.index_tail(target)
         if self.at("punct", "<-") or self.at("punct", "->"):
             if isinstance(tview, IView):
@@ -387,6 +413,16 @@ class _Parser:
         if self.at("name", "true") or self.at("name", "false"):
             raise UnsupportedProgram("codegen: Bool cells are not supported")
         return self.index_tail(self.name())
+
+    def call_args(self):
+        self.expect("punct", "(")
+        views = []
+        while not self.at("punct", ")"):
+            views.append(self.index_tail(self.name()))
+            if self.at("punct", ","):
+                self.adv()
+        self.adv()
+        return tuple(views)
 
     def index_tail(self, name):
         """name or name[i, j] (a view); field views are not supported."""
@@ -531,6 +567,10 @@ def _invert(s):
         return For(s.var, s.b, _neg_expr(s.s), s.a, _invert_list(s.body))
     if isinstance(s, Safe):
         return s                       # irreversible external statement: re-executed as is
+    if isinstance(s, PCall):           # reverser.py:96-103
+        if s.f in PRIM_INV:
+            return PCall(PRIM_INV[s.f], s.args, False)
+        return PCall(s.f, s.args, not s.uncall)
     if isinstance(s, tuple):
         return _invert_list(s)
     raise UnsupportedProgram(f"codegen: cannot invert {s!r}")
@@ -583,6 +623,149 @@ def _expand(stmts):
     if pending:
         raise UnsupportedProgram("codegen: routine block is never closed")
     return tuple(out)
+
+
+# ---------------------------------------------------------------------------
+# call inlining: a user call runs the callee's (or, for ~f, its inverse's)
+# expanded body with the parameters bound to the argument views and fresh
+# local names — the reference's fresh Frame per call with copy-in/copy-out
+# (interpreter.py:969-989), equivalent because the strict alias check keeps
+# the argument cells disjoint
+# ---------------------------------------------------------------------------
+
+def _expr_names(e, acc):
+    if isinstance(e, Var):
+        acc.add(e.name)
+    elif isinstance(e, IView):
+        acc.add(e.name)
+        for x in e.idx:
+            _expr_names(x, acc)
+    elif isinstance(e, Un):
+        _expr_names(e.e, acc)
+    elif isinstance(e, Bin):
+        _expr_names(e.l, acc)
+        _expr_names(e.r, acc)
+    elif isinstance(e, Call):
+        for x in e.args:
+            _expr_names(x, acc)
+    return acc
+
+
+def _balanced(stmts, fname):
+    """Every block releases what it allocates (else the reference raises
+    DirtyAncilla for leaked bindings at the call's exit)."""
+    cnt = {}
+    for s in stmts:
+        if isinstance(s, Alloc):
+            cnt[s.name] = cnt.get(s.name, 0) + 1
+        elif isinstance(s, Dealloc):
+            cnt[s.name] = cnt.get(s.name, 0) - 1
+        elif isinstance(s, (For, While)):
+            _balanced(s.body, fname)
+        elif isinstance(s, If):
+            _balanced(s.then, fname)
+            _balanced(s.els, fname)
+    if any(cnt.values()):
+        raise UnsupportedProgram(f"codegen: {fname} does not release every ancilla it allocates "
+                                 "in the same block")
+
+
+class _Inliner:
+    def __init__(self, fns):
+        self.fns = fns
+        self.n = 0
+
+    def run(self, stmts, stack=()):
+        out = []
+        for s in stmts:
+            if isinstance(s, PCall) and s.f not in PRIM_ARITY:
+                out.extend(self.call(s, stack))
+            elif isinstance(s, For):
+                out.append(For(s.var, s.a, s.s, s.b, self.run(s.body, stack)))
+            elif isinstance(s, While):
+                out.append(While(s.pre, s.post, self.run(s.body, stack)))
+            elif isinstance(s, If):
+                out.append(If(s.pre, s.post, self.run(s.then, stack), self.run(s.els, stack)))
+            else:
+                out.append(s)
+        return tuple(out)
+
+    def call(self, s, stack):
+        if s.f not in self.fns:
+            raise UnsupportedProgram(f"codegen: no function named {s.f!r}")
+        if s.f in stack:
+            raise UnsupportedProgram(f"codegen: recursive call of {s.f!r} cannot be inlined")
+        params, body = self.fns[s.f]
+        if len(params) != len(s.args):
+            raise KindError(f"{s.f} takes {len(params)} arguments, got {len(s.args)}")
+        scalars = {a.name for a in s.args if isinstance(a, Var)}
+        for a in s.args:
+            if isinstance(a, IView) and _expr_names(Call("", a.idx), set()) & scalars:
+                raise UnsupportedProgram("codegen: an argument's index uses another argument "
+                                         "of the same call")
+        body = _expand(_invert_list(body) if s.uncall else body)
+        _balanced(body, s.f)
+        self.n += 1
+        env = dict(zip(params, s.args))
+        tag = f"__{s.f}{self.n}"
+        inl = _Subst(env, tag, set(params))
+        return (ArgCheck(s.args),) + self.run(inl.stmts(body), stack + (s.f,))
+
+
+class _Subst:
+    """Parameters -> argument views, callee locals -> fresh names."""
+
+    def __init__(self, env, tag, params):
+        self.env, self.tag, self.params = env, tag, params
+
+    def local(self, n):
+        if n in self.params:
+            raise UnsupportedProgram(f"codegen: parameter {n!r} is (de)allocated or a loop variable")
+        return n + self.tag
+
+    def view(self, v):
+        if isinstance(v, Var):
+            return self.env.get(v.name, Var(v.name + self.tag))
+        if isinstance(v, IView):
+            base = self.env.get(v.name, Var(v.name + self.tag))
+            if not isinstance(base, Var):
+                raise KindError("indexing into a scalar cell")
+            return IView(base.name, tuple(self.e(x) for x in v.idx))
+        return v
+
+    def e(self, x):
+        if isinstance(x, (Var, IView)):
+            return self.view(x)
+        if isinstance(x, Un):
+            return Un(x.op, self.e(x.e))
+        if isinstance(x, Bin):
+            return Bin(x.op, self.e(x.l), self.e(x.r))
+        if isinstance(x, Call):
+            return Call(x.f, tuple(self.e(a) for a in x.args))
+        return x
+
+    def stmts(self, ss):
+        return tuple(self.stmt(s) for s in ss)
+
+    def stmt(self, s):
+        if isinstance(s, Instr):
+            return Instr(s.op, self.view(s.target), s.fname, tuple(self.e(a) for a in s.args))
+        if isinstance(s, Alloc):
+            return Alloc(self.local(s.name), self.e(s.e))
+        if isinstance(s, Dealloc):
+            return Dealloc(self.local(s.name), self.e(s.e))
+        if isinstance(s, For):
+            return For(self.local(s.var), self.e(s.a), self.e(s.s), self.e(s.b), self.stmts(s.body))
+        if isinstance(s, While):
+            return While(self.e(s.pre), self.e(s.post), self.stmts(s.body))
+        if isinstance(s, If):
+            return If(self.e(s.pre), s.post if s.post is SAME else self.e(s.post),
+                      self.stmts(s.then), self.stmts(s.els))
+        if isinstance(s, Safe):
+            return Safe(s.kind, tuple(self.e(x) for x in s.exprs))
+        if isinstance(s, PCall):
+            return PCall(s.f, tuple(self.view(a) for a in s.args), s.uncall)
+        raise UnsupportedProgram(f"codegen: cannot inline {s!r}")
 
 
 # ---------------------------------------------------------------------------
@@ -681,6 +864,7 @@ __device__ __forceinline__ Dl g_pow(Dl a, Dl b, int &c) {
   if (b.t != 0.0) t = t + r * g_log(a.p, c) * b.t;
   return Dl(r, t);
 }
+#define RC_KIND 7
 #define RC_INDEX 8
 #define RC_ALIAS 10
 #define RC_ASSERT 11
@@ -745,32 +929,68 @@ class _Emitter:
         k = self.kinds.get(name)
         if k is None:
             raise UnsupportedProgram(f"codegen: {name!r} is used before it is allocated")
-        if k == "a":
+        if k in ("a", "ai"):
             raise KindError(f"{name!r} is an array; index it (instructions and expressions "
                             "take scalar cells)")
         return k
 
-    def offset(self, v):
+    def cell_kind(self, v):
+        """Kind of a view's cell: array cells are Float ("a") or Int ("ai")."""
+        if isinstance(v, IView):
+            if v.name not in self.shapes:
+                raise KindError(f"{v.name!r} is not an array parameter")
+            return "i" if self.kinds.get(v.name) == "ai" else "f"
+        return self.kind(v.name)
+
+    def offset(self, v, pre=None):
         """C expression of the row-major offset of view v (Array._offset,
-        values.py:172-183); an out-of-range index sets RC_INDEX."""
+        values.py:172-183); an out-of-range index sets RC_INDEX.  `pre`:
+        index values already evaluated into temps."""
         shape = self.shapes.get(v.name)
         if shape is None:
             raise KindError(f"{v.name!r} is not an array parameter")
-        idx = [self.int_expr(e, "array index") for e in v.idx]
+        idx = pre if pre is not None else [self.int_expr(e, "array index") for e in v.idx]
         if len(idx) != len(shape):
             return "rl_offbad(code)"
         if len(idx) == 1:
             return f"rl_off1({idx[0]}, {shape[0]}LL, code)"
         return f"rl_off2({idx[0]}, {shape[0]}LL, {idx[1]}, {shape[1]}LL, code)"
 
-    def view_ref(self, a):
+    def idx_temps(self, a):
+        """Evaluate a view's index expressions into temps (storage ids of
+        the alias checks, interpreter.py:600-622); None for a plain name."""
+        if not isinstance(a, IView):
+            return None
+        out = []
+        for e in a.idx:
+            t = self.new("ix")
+            self.w(f"const long long {t} = {self.int_expr(e, 'array index')};")
+            out.append(t)
+        return out
+
+    def alias_pre(self, views, pres, label):
+        """Strict pairwise alias checks on storage ids, before any read (prim
+        statements and calls, interpreter.py:961-964, 999-1002)."""
+        for i in range(len(views)):
+            for j in range(i + 1, len(views)):
+                a, b = views[i], views[j]
+                if a.name != b.name:
+                    continue
+                if pres[i] is None or pres[j] is None:      # a whole cell / array
+                    self.w(f"if (!code) code = RC_ALIAS; goto {label};")
+                elif len(pres[i]) == len(pres[j]):
+                    same = " && ".join(f"{x} == {y}" for x, y in zip(pres[i], pres[j]))
+                    self.w(f"if ({same}) {{ code = RC_ALIAS; goto {label}; }}")
+
+    def view_ref(self, a, pre=None):
         """_Ref of an instruction operand; array offsets land in temps (the
         reference's readers evaluate indices in operand order)."""
         if isinstance(a, IView):
             o = self.new("o")
-            self.w(f"const long long {o} = {self.offset(a)};")
+            self.w(f"const long long {o} = {self.offset(a, pre)};")
             c = _cid(a.name)
-            return _Ref(f"v_{c}[{o}]", f"g_{c}[{o}]", "f", a.name, o)
+            k = self.cell_kind(a)
+            return _Ref(f"v_{c}[{o}]", f"g_{c}[{o}]" if k == "f" else None, k, a.name, o)
         k = self.kind(a.name)
         c = _cid(a.name)
         return _Ref(f"v_{c}", f"g_{c}", k, a.name)
@@ -802,7 +1022,7 @@ class _Emitter:
             k = self.kind(e.name)
             return "f" if k == "u" else k
         if isinstance(e, IView):
-            return "f"
+            return self.cell_kind(e)
         if isinstance(e, Un):
             return self.expr_kind(e.e)
         if isinstance(e, Call):
@@ -857,7 +1077,7 @@ class _Emitter:
                 return f"g_exp(v_{_cid(e.name)}, code)", "f"       # to_real(ULog)
             return f"v_{_cid(e.name)}", k
         if isinstance(e, IView):
-            return f"v_{_cid(e.name)}[{self.offset(e)}]", "f"
+            return f"v_{_cid(e.name)}[{self.offset(e)}]", self.cell_kind(e)
         if isinstance(e, Un):
             s, k = self.expr(e.e)
             return f"(-{s})", k
@@ -1032,6 +1252,30 @@ class _Emitter:
     def stmt(self, s, grad, label):
         if isinstance(s, Instr):
             self.instr(s, grad, label)
+        elif isinstance(s, ArgCheck):
+            self.w("{")
+            self.depth += 1
+            pres = [self.idx_temps(a) for a in s.views]
+            if any(p is not None for p in pres):
+                self.fail_check(label)
+            self.alias_pre(s.views, pres, label)
+            for a, pre in zip(s.views, pres):              # the readers: bounds
+                if pre is not None:
+                    self.w(f"(void){self.offset(a, pre)};")
+                elif a.name not in self.kinds:
+                    raise UnsupportedProgram(f"codegen: {a.name!r} is used before it is allocated")
+            if any(p is not None for p in pres):
+                self.fail_check(label)
+            self.depth -= 1
+            self.w("}")
+        elif isinstance(s, PCall):
+            if s.f not in PRIM_ARITY:
+                raise UnsupportedProgram(f"codegen: call of {s.f!r} was not inlined")
+            self.w("{")
+            self.depth += 1
+            self.prim(s, grad, label)
+            self.depth -= 1
+            self.w("}")
         elif isinstance(s, Safe):
             if s.kind != "assert":
                 raise UnsupportedProgram("codegen: @safe print has no device equivalent")
@@ -1129,6 +1373,69 @@ class _Emitter:
         else:
             raise UnsupportedProgram(f"codegen: unsupported statement {s!r}")
 
+    def prim(self, s, grad, label):
+        """SWAP / ROT / IROT / NEG / INC / DEC (numerics.py:391-415 plain,
+        :508-537 and :564-571 in gradient mode)."""
+        kind = PRIM_INV[s.f] if s.uncall else s.f
+        if len(s.args) != PRIM_ARITY[s.f]:
+            raise KindError(f"{s.f} takes {PRIM_ARITY[s.f]} arguments")
+        pres = [self.idx_temps(a) for a in s.args]
+        if any(p is not None for p in pres):
+            self.fail_check(label)
+        self.alias_pre(s.args, pres, label)
+        refs = [self.view_ref(a, pre) for a, pre in zip(s.args, pres)]
+        if any(p is not None for p in pres):
+            self.fail_check(label)
+        if kind == "SWAP":
+            a, b = refs
+            if a.kind != b.kind:
+                raise UnsupportedProgram("codegen: SWAP of cells of different kinds")
+            ty = "long long" if a.kind == "i" else "R"
+            t = self.new("sw")
+            self.w(f"{{ const {ty} {t} = {a.v}; {a.v} = {b.v}; {b.v} = {t}; }}")
+            if grad and a.kind != "i":                 # the GVar cells trade places
+                self.w(f"{{ const R {t} = {a.g}; {a.g} = {b.g}; {b.g} = {t}; }}")
+            return
+        if kind == "NEG":
+            (a,) = refs
+            if a.kind == "u":
+                raise UnsupportedProgram("codegen: NEG of a logarithmic number")
+            self.w(f"{a.v} = -{a.v};")
+            if grad and a.kind == "f":                 # _neg_adjoint
+                self.w(f"{a.g} = -{a.g};")
+            return
+        if kind in ("INC", "DEC"):
+            (a,) = refs
+            if a.kind != "i":                          # _prim_plain: Int (or Fixed) only
+                self.w(f"if (!code) code = RC_KIND; goto {label};")
+                return
+            self.w(f"{a.v} = {a.v} {'+' if kind == 'INC' else '-'} 1;")
+            return
+        # ROT / IROT: (a c - b s, a s + b c), theta unchanged
+        a, b, th = refs
+        if a.kind != "f" or b.kind != "f" or th.kind not in ("f", "i"):
+            raise UnsupportedProgram("codegen: ROT / IROT rotate Float cells by a Float or Int angle")
+        thv = th.v if th.kind == "f" else f"R((double){th.v})"
+        n = self.new("r")
+        if not grad:
+            self.w(f"{{ const R th{n} = {thv if kind == 'ROT' else '-' + thv};")
+            self.w(f"  const R c{n} = cos(th{n}), s{n} = sin(th{n});")
+            self.w(f"  const R a{n} = {a.v} * c{n} - {b.v} * s{n}, b{n} = {a.v} * s{n} + {b.v} * c{n};")
+            self.w(f"  {a.v} = a{n}; {b.v} = b{n}; }}")
+            return
+        # _rot_adjoint: IROT is the reverse of a forward ROT by theta
+        self.w(f"{{ const R ax{n} = {a.v}, bx{n} = {b.v}, ga{n} = {a.g}, gb{n} = {b.g};")
+        if kind == "IROT":
+            self.w(f"  const R d{n} = -bx{n} * ga{n} + ax{n} * gb{n};")
+        else:
+            self.w(f"  const R d{n} = bx{n} * ga{n} - ax{n} * gb{n};")
+        if th.kind == "f":
+            self.w(f"  {th.g} = {th.g} + d{n};")
+        self.w(f"  const R th{n} = {('-' + thv) if kind == 'IROT' else thv};")
+        self.w(f"  const R c{n} = cos(th{n}), s{n} = sin(th{n});")
+        self.w(f"  {a.v} = ax{n} * c{n} - bx{n} * s{n}; {b.v} = ax{n} * s{n} + bx{n} * c{n};")
+        self.w(f"  {a.g} = ga{n} * c{n} - gb{n} * s{n}; {b.g} = ga{n} * s{n} + gb{n} * c{n}; }}")
+
     def instr(self, s, grad, label):
         self.w("{")
         self.depth += 1
@@ -1161,7 +1468,8 @@ class _Emitter:
                         (r is not None and r.kind != "i") for a, r in zip(args, refs)):
                     raise UnsupportedProgram("codegen: Int targets take Int +, - and identity")
                 xs = [(f"{a.v}LL" if isinstance(a, Lit) else r.v) for a, r in zip(args, refs)]
-                fv = self.apply_fn(s.fname, xs)
+                fv = {"identity": lambda: xs[0], "add": lambda: f"({xs[0]} + {xs[1]})",
+                      "sub": lambda: f"({xs[0]} - {xs[1]})", "neg": lambda: f"(-{xs[0]})"}[s.fname]()
                 self.w(f"{TV} = {TV} {'+' if s.op == '+=' else '-'} ({fv});")
                 return
             if s.fname == "convert":
@@ -1288,13 +1596,13 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     params, body = fns[fname]
     int_params = set(int_params)
     shapes = _check_shapes(array_shapes, parser.arrays.get(fname, ()), params)
-    if int_params & set(shapes):
-        raise KindError("a parameter cannot be both Int and an array")
-    kinds = {p: ("a" if p in shapes else "i" if p in int_params else "f") for p in params}
-    fwd = _expand(body)
-    inv = _expand(_invert_list(body))
-    floats = [p for p in params if kinds[p] != "i"]
-    ints = [p for p in params if kinds[p] == "i"]
+    kinds = {p: ("ai" if p in shapes and p in int_params else "a" if p in shapes
+                 else "i" if p in int_params else "f") for p in params}
+    inliner = _Inliner(fns)
+    fwd = inliner.run(_expand(body), (fname,))
+    inv = inliner.run(_expand(_invert_list(body)), (fname,))
+    floats = [p for p in params if kinds[p] in ("f", "a")]
+    ints = [p for p in params if kinds[p] in ("i", "ai")]
     leaves, base = [], {}
     for p in floats:
         base[p] = len(leaves)
@@ -1339,8 +1647,17 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
         else:
             L.append(f"    R v_{c} = R(fin[{b}LL * n + i]"
                      + (f", dir == {b} ? 1.0 : 0.0)" if hess else ")") + f", g_{c} = R(0.0);")
-    for j, p in enumerate(ints):
-        L.append(f"    long long v_{_cid(p)} = iin[{j}];")
+    ibase, nib = {}, 0
+    for p in ints:                      # Int values (uniform over the batch) from iin
+        ibase[p] = nib
+        if p in shapes:
+            m = math.prod(shapes[p])
+            L.append(f"    long long v_{_cid(p)}[{m}];")
+            L.append(f"    for (int e = 0; e < {m}; ++e) v_{_cid(p)}[e] = iin[{nib} + e];")
+            nib += m
+        else:
+            L.append(f"    long long v_{_cid(p)} = iin[{nib}];")
+            nib += 1
     L += decl
 
     def each_leaf(fmt):
@@ -1373,8 +1690,12 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     L.append("    if (!code) {      // the backward pass must restore every argument")
     L += ["  " + x for x in each_leaf(
         lambda col, v, g: f"if (!(fabs(rl_p({v}) - fin[{col} * n + i]) <= tol)) code = RC_REV;")]
-    for j, p in enumerate(ints):
-        L.append(f"      if (v_{_cid(p)} != iin[{j}]) code = RC_REV;")
+    for p in ints:
+        if p in shapes:
+            L.append(f"      for (int e = 0; e < {math.prod(shapes[p])}; ++e)"
+                     f" if (v_{_cid(p)}[e] != iin[{ibase[p]} + e]) code = RC_REV;")
+        else:
+            L.append(f"      if (v_{_cid(p)} != iin[{ibase[p]}]) code = RC_REV;")
     L.append("    }")
     L += each_leaf(lambda col, v, g: f"gout[{col} * n + i] = code ? NAN : rl_p({g});"
                    + (f" hout[{col} * n + i] = code ? NAN : rl_t({g});" if hess else ""))
@@ -1549,6 +1870,12 @@ class CompiledFunction:
         ivals = []
         for p in self.ints:
             v = inputs.get(p)
+            if p in self.shapes:
+                a = np.asarray(v)
+                if a.shape != self.shapes[p] or a.dtype.kind not in "iu":
+                    raise KindError(f"{p} must be an Int array of shape {self.shapes[p]}")
+                ivals += [int(x) for x in a.ravel()]
+                continue
             if not isinstance(v, int) or isinstance(v, bool):
                 raise KindError(f"{p} must be an Int")
             ivals.append(v)

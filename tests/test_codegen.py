@@ -15,7 +15,7 @@ def src(name):
     return open(os.path.join(REPO, "tests", "golden", "codegen", name + ".rnl")).read()
 
 
-@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix"])
+@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix", "prims"])
 def test_inversion_is_an_involution(name):
     for params, body in codegen._Parser(src(name)).program().values():
         assert codegen._invert_list(codegen._invert_list(body)) == body
@@ -29,6 +29,19 @@ def test_besselj_parses_and_expands():
     # the routine opens, the middle runs, the routine closes inverted
     assert isinstance(fwd[0], codegen.Alloc) and isinstance(fwd[-1], codegen.Dealloc)
     assert any(isinstance(s, codegen.While) for s in fwd)
+
+
+def test_calls_are_inlined_with_fresh_locals():
+    """programs/ba.rnl calls rodrigues inside a routine: four inlined copies
+    (forward, routine close, and both again in the gradient sweep)."""
+    text = open(os.path.join(REPO, "paper_2003_04617_b200", "programs", "ba.rnl")).read()
+    source = codegen.generate(text, "ba_proj", array_shapes={"cam": 11, "X": 3})[0]
+    for j in range(1, 5):
+        assert f"v_th__rodrigues{j}" in source
+    with pytest.raises(UnsupportedProgram):                 # recursion cannot be inlined
+        codegen.generate("fn f(y!, x)\n f(y!, x)\nend\n", "f")
+    with pytest.raises(UnsupportedProgram):                 # leaks an ancilla (DirtyAncilla)
+        codegen.generate("fn g(y!)\n t <- 0.0\nend\nfn f(y!)\n g(y!)\nend\n", "f")
 
 
 def test_unsupported_constructs_are_rejected():

@@ -18,7 +18,8 @@ from paper_2003_04617_b200 import codegen
 pytestmark = pytest.mark.gpu
 
 CASES = {"mul_acc": (["y!", "a", "b"], {}, True), "sink": (["out!", "x", "y"], {"n": 3}, False),
-         "wloop": (["acc!", "x"], {"n": 5}, True)}
+         "wloop": (["acc!", "x"], {"n": 5}, True),
+         "prims": (["a!", "b!", "c!", "th"], {"n!": 3}, False)}
 
 
 def src(name):

@@ -1,0 +1,116 @@
+"""The paper's three benchmark programs through the GENERIC compiler
+(codegen.py): programs/ba.rnl (calls rodrigues —
+inlined — over Float array parameters), programs/gmm.rnl (Int array scratch,
+INC, argmax branches, routines in loops) and programs/besselj.rnl (in
+test_codegen_gpu.py), compiled from their .rnl source with no hand-written
+kernel, against the reference's own gradient() goldens (tests/golden/ba.npz,
+gmm.npz) and hessian() goldens (codegen_programs.npz).  Transcendental
+programs: libdevice vs host libm (<= 1-2 ulp per call), so tolerances as the
+hand-written kernels' parity tests."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import REPO
+from paper_2003_04617_b200 import codegen
+
+pytestmark = pytest.mark.gpu
+
+
+def prog(name):
+    return open(os.path.join(REPO, "paper_2003_04617_b200", "programs", name + ".rnl")).read()
+
+
+def close(a, b, rel, floor):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b) <= rel * np.abs(b) + floor * max(np.abs(b).max(), 1e-300)
+
+
+def gmm_case(G, ci, n=1):
+    pre = f"c{ci}_"
+    d, K, N, m = (int(v) for v in G[pre + "dims"])
+    P = d * (d + 1) // 2
+    shapes = {"alphas": K, "means": (K, d), "icf": (K, P), "x": (N, d), "qd!": (K, d), "sq!": K,
+              "xc!": d, "qxc!": d, "mt!": K, "dm!": K}
+    inputs = {"err!": 0.0, "alphas": G[pre + "alphas"], "means": G[pre + "means"],
+              "icf": G[pre + "icf"], "qd!": np.zeros((K, d)), "sq!": np.zeros(K),
+              "xc!": np.zeros(d), "qxc!": np.zeros(d), "mt!": np.zeros(K),
+              "dm!": np.zeros(K, np.int64), "ga": float(G[pre + "gamma"]), "wm": m,
+              "cst": float(G[pre + "cst"])}
+    x = torch.as_tensor(G[pre + "x"], device="cuda")
+    inputs["x"] = x.expand(n, N, d).contiguous() if n > 1 else G[pre + "x"]
+    return shapes, inputs
+
+
+@pytest.mark.parametrize("ci", range(8))
+def test_generic_gmm_matches_reference(cuda, golden, ci):
+    G = golden("gmm")
+    shapes, inputs = gmm_case(G, ci, n=2)
+    k = codegen.compile_function(prog("gmm"), "gmm", int_params=("dm!", "wm"),
+                                 array_shapes=shapes)
+    primal, grads, fail = k.gradient(inputs)
+    torch.cuda.synchronize()
+    assert not fail.any()
+    pre = f"c{ci}_"
+    err = primal["err!"].cpu().numpy()
+    assert close(err, np.full(2, float(G[pre + "err"])), 1e-12, 0).all()
+    for nm in ("alphas", "means", "icf"):
+        g = grads[nm].cpu().numpy()
+        for r in range(2):
+            assert close(g[r], G[pre + "g_" + nm], 1e-10, 1e-12).all(), nm
+    # the scratch comes back zero up to round-off (the routines uncompute it,
+    # as in the reference) and x is untouched
+    assert primal["mt!"].abs().max().item() <= 1e-12 and torch.equal(primal["x"], inputs["x"])
+
+
+def test_generic_gmm_hessian(cuda, golden):
+    G = golden("gmm")
+    shapes, inputs = gmm_case(G, 5)
+    k = codegen.compile_function(prog("gmm"), "gmm", int_params=("dm!", "wm"),
+                                 array_shapes=shapes)
+    assert len(k.leaves) == 27
+    H, fail = k.hessian(inputs)
+    torch.cuda.synchronize()
+    assert not fail.any()
+    ref = golden("codegen_programs")["gmm_c5_hess"]
+    assert close(H[0].cpu().numpy(), ref, 1e-10, 1e-12).all()
+
+
+def _ba_inputs(B, cuda, rows=slice(None)):
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a[rows]), device=cuda)  # noqa: E731
+    return {"e1!": 0.0, "e2!": 0.0, "cam": t(B["cams"]), "X": t(B["X"]), "w": t(B["w"]),
+            "f1": t(B["feat"][:, 0]), "f2": t(B["feat"][:, 1])}
+
+
+def test_generic_ba_jacobian_matches_reference(cuda, golden):
+    B = golden("ba")
+    k = codegen.compile_function(prog("ba"), "ba_proj", array_shapes={"cam": 11, "X": 3})
+    inputs = _ba_inputs(B, cuda)
+    for r, seed in enumerate(("e1!", "e2!")):
+        primal, grads, fail = k.gradient(inputs, seeds=[(seed, (), 1.0)])
+        torch.cuda.synchronize()
+        assert not fail.any()
+        J = torch.cat([grads["cam"], grads["X"], grads["w"][:, None]], 1).cpu().numpy()
+        ref = B["J"][:, r, :]
+        for o in range(J.shape[0]):
+            assert close(J[o], ref[o], 1e-11, 1e-13).all(), (seed, o)
+        e = primal[seed].cpu().numpy()
+        assert close(e, B["e"][:, r], 1e-12, 1e-14).all()
+    kw = codegen.compile_function(prog("ba"), "ba_weight")
+    _, g, fail = kw.gradient({"e!": 0.0, "w": inputs["w"]})
+    torch.cuda.synchronize()
+    assert not fail.any() and np.array_equal(g["w"].cpu().numpy(), B["wjac"])
+
+
+def test_generic_ba_hessian(cuda, golden):
+    B = golden("ba")
+    k = codegen.compile_function(prog("ba"), "ba_proj", array_shapes={"cam": 11, "X": 3})
+    H, fail = k.hessian(_ba_inputs(B, cuda, slice(0, 4)))
+    torch.cuda.synchronize()
+    assert not fail.any()
+    ref = golden("codegen_programs")["ba_hess"]
+    for o in range(4):
+        assert close(H[o].cpu().numpy(), ref[o], 1e-9, 1e-11).all(), o
