@@ -394,9 +394,42 @@ def gen_codegen_programs():
     print("codegen program hessians:", {k: v.shape for k, v in out.items()})
 
 
+def gen_codegen_dropin():
+    """reference run / uncall / check_reversibility / jacobian of the codegen
+    test programs through the public API, for the drop-in generic path
+    (autodiff / interp -> generic.py -> codegen.py)."""
+    from revlang.autodiff import jacobian
+    from revlang.interpreter import check_reversibility, run, uncall
+    from revlang.values import Array
+    out = {}
+    g = np.load(os.path.join(OUT_DIR, "codegen.npz"))
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "prims.rnl")).read())
+    X = g["prims_x"][:6]
+    runs, uncs, devs = [], [], []
+    for row in X:
+        args = [float(v) for v in row] + [3]
+        runs.append(run(prog, "prims", list(args))[:4] + [0.0])
+        uncs.append(uncall(prog, "prims", list(args))[:4] + [0.0])
+        devs.append(check_reversibility(prog, "prims", list(args)).max_deviation)
+    out["prims_x"], out["prims_run"], out["prims_uncall"] = X, np.array(runs)[:, :4], \
+        np.array(uncs)[:, :4]
+    out["prims_dev"] = np.array(devs)
+    out["prims_jac"] = jacobian(prog, "prims", [float(v) for v in X[0]] + [3])
+    q = parse_program(open(os.path.join(OUT_DIR, "codegen", "quad.rnl")).read())
+    ga = np.load(os.path.join(OUT_DIR, "codegen_arrays.npz"))
+    row = ga["quad_x"][0]
+    args = [float(row[0]), Array.vector(row[1:4].tolist()),
+            Array.matrix(row[4:13].reshape(3, 3).tolist()), Array.vector(row[13:16].tolist())]
+    r = run(q, "quad", args)
+    out["quad_run"] = np.array([r[0]] + list(r[1].data) + list(r[2].data) + list(r[3].data))
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_dropin.npz"), **out)
+    print("codegen drop-in goldens:", {k: np.shape(v) for k, v in out.items()})
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
-                              "codegen_arrays", "codegen_programs"]
+                              "codegen_arrays", "codegen_programs",
+                              "codegen_dropin"]
     for w in which:
         globals()["gen_" + w]()

@@ -16,7 +16,7 @@ plus the batched device API over torch CUDA tensors:
 
 from .autodiff import (ExecOptions, GradRequest, HessianResult, gradient, gradient_batch,
                        hessian, jacobian)
-from .errors import (AliasedArguments, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
+from .errors import (AliasedArguments, AssertFailed, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
                      UnknownExample, UnknownFunction, UnsupportedProgram)
@@ -30,7 +30,7 @@ from .values import Array
 
 __all__ = [
     "HessianResult", "hessian", "gradient_batch", "CompiledFunction", "compile_function", "BesselHessResult", "besselj_hess",
-    "AliasedArguments", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
+    "AliasedArguments", "AssertFailed", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",
     "ExecOptions", "FuelExhausted", "GMMResult", "GradRequest", "IndexOutOfBounds",

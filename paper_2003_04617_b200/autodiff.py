@@ -4,11 +4,13 @@
 reference's signature and return structure — (primal outputs, {param:
 cotangent structure}) with Int leaves -> None (autodiff.py:136-180) — but
 runs the registered program's fused forward + reverse-sweep kernel on
-`cuda:<current device>` instead of interpreting it.  Reversibility failures
-detected on device raise the reference's exception classes.
+`cuda:<current device>` instead of interpreting it; any other function is
+compiled to a device kernel by codegen.py (generic.py).  Reversibility
+failures detected on device raise the reference's exception classes.
 
 Differences to the reference, all documented in DESIGN.md:
-  * only registered programs run (UnsupportedProgram otherwise; no CPU path);
+  * no CPU path: a function outside codegen's subset (records, Complex /
+    Fixed / ULog arguments, xor=, recursion) raises UnsupportedProgram;
   * binary64 only (ExecOptions.float_dtype must be None), no tracing;
   * seeds on input leaves are added to the returned cotangent (as the
     reference's GVar initial value would be); several output seeds on BA
@@ -278,22 +280,24 @@ _HANDLERS = {"besselj": _grad_besselj, "ba_proj": _grad_ba_proj,
              "ba_weight": _grad_ba_weight, "gmm": _grad_gmm}
 
 
-def _resolve(program, fname):
+def _lookup(program, fname):
+    """(program, fdef, registered): registered = a hand-written kernel
+    handles fname; otherwise generic.py compiles it (codegen.py)."""
     prog = as_program(program)
     fdef = prog.functions.get(fname)
     if fdef is None:
         raise UnknownFunction(f"no function named {fname!r}")
-    if fdef.kernel is None or fdef.kernel.handler not in _HANDLERS:
-        raise UnsupportedProgram(
-            f"function {fname!r} has no registered device kernel (registered: "
-            "besselj, ba_proj, ba_weight, gmm); there is no CPU fallback")
-    return fdef
+    return prog, fdef, fdef.kernel is not None and fdef.kernel.handler in _HANDLERS
 
 
 def gradient(program, req, opts=None):
-    """Reference `gradient` (autodiff.py:136) on the device."""
+    """Reference `gradient` (autodiff.py:136) on the device: the hand-written
+    kernel of a registered program, else the function compiled by codegen."""
     opts = _check_opts(opts)
-    fdef = _resolve(program, req.fname)
+    prog, fdef, reg = _lookup(program, req.fname)
+    if not reg:
+        from . import generic
+        return generic.gradient(prog, fdef, req, opts)
     return _HANDLERS[fdef.kernel.handler](fdef, req, opts)
 
 
@@ -320,8 +324,8 @@ def jacobian(program, fname, args, opts=None):
     """Reference `jacobian` (autodiff.py:197-213): one gradient per
     differentiable leaf of every argument; rows x columns over all leaves."""
     opts = _check_opts(opts)
-    fdef = _resolve(program, fname)
-    if fdef.kernel.handler == "gmm":
+    _, fdef, reg = _lookup(program, fname)
+    if reg and fdef.kernel.handler == "gmm":
         raise KindError("the full gmm jacobian (over x and scratch) is not produced on device")
     names = fdef.param_names()
     rows = []
@@ -356,9 +360,15 @@ def hessian(program, fname, args, opts=None):
     device for besselj: the Float leaves are out! and z (nu is an Int), the
     only nonzero entry is H[z, z] = d2J/dz2 from rl_besselj_hess_f64, which
     runs the gradient sweeps over Dual numbers exactly as the reference does.
-    Other programs' Hessians are not produced on device (UnsupportedProgram)."""
+    Functions without a hand-written kernel run codegen's Dual-number
+    kernel (one launch per Float leaf); the registered ba / gmm programs'
+    Hessians are not produced on device (UnsupportedProgram)."""
     opts = _check_opts(opts)
-    fdef = _resolve(program, fname)
+    prog, fdef, reg = _lookup(program, fname)
+    if not reg:
+        from . import generic
+        H = generic.hessian(prog, fdef, list(args), opts)
+        return HessianResult(H, float(np.max(np.abs(H - H.T))) if H.size else 0.0)
     if fdef.kernel.handler != "besselj":
         raise UnsupportedProgram(
             f"hessian of {fname!r}: only besselj has a device Hessian kernel")
@@ -416,7 +426,13 @@ def gradient_batch(program, fname, inputs, seeds=None, wrt=None, opts=None, retu
     (errors.CODE_NAMES).  besselj, ba_proj and ba_weight; gmm is one
     evaluation over all points (use gradient / gmm_grad)."""
     opts = _check_opts(opts)
-    fdef = _resolve(program, fname)
+    prog, fdef, reg = _lookup(program, fname)
+    if not reg:
+        from . import generic
+        primal, grads, fail = generic.gradient_batch(prog, fdef, inputs, seeds, wrt, opts)
+        code = fail.to(torch.int32)
+        out = (primal, grads, code == 0)
+        return out + (code,) if return_codes else out
     names = fdef.param_names()
     h = fdef.kernel.handler
     dev = _device()

@@ -253,7 +253,8 @@ _INSTR_BIN = {"+": "add", "-": "sub", "*": "mul", "/": "div", "^": "pow"}
 
 class _Parser:
     def __init__(self, src):
-        self.t = _tokenize(src)
+        # the reference's Unicode spellings of the arrows (parser.py:143-164)
+        self.t = _tokenize(src.replace("\u2190", "<-").replace("\u2192", "->"))
         self.i = 0
         self.arrays = {}
 
@@ -1581,13 +1582,32 @@ def _check_shapes(arrays, declared, params):
     return shapes
 
 
+_LAUNCH = r"""
+extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, const double *seeds,
+                          double tol, int chk, long long fuel, double *fout, double *gout,
+                          unsigned char *fail, int dir, double *hout, long long *iout,
+                          void *stream) {
+  if (n <= 0) return 0;
+  const int block = 128;
+  long long grid = (n + block - 1) / block;
+  if (grid > 148 * 16) grid = 148 * 16;
+  rlg_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(n, fin, iin, seeds, tol, chk, fuel,
+                                                                fout, gout, fail, dir, hout, iout);
+  return (int)cudaGetLastError();
+}
+"""
+
+
 def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
-    """CUDA source of the batched gradient (mode "grad") or forward-over-reverse
+    """CUDA source of the batched gradient (mode "grad"), forward-over-reverse
     Hessian-column (mode "hess": the same code over Dual numbers, tangent on
-    the Float leaf `dir`) kernel of `fname`, and its layout: (source, float
-    parameters, Int parameters, leaves) where leaves lists (parameter, leaf
-    path) in the kernel's column order (scalars: path ())."""
-    if mode not in ("grad", "hess"):
+    the Float leaf `dir`) or plain run / uncall (modes "run" / "uncall": one
+    sweep of f or ~f, reference interpreter.py:1021-1028) kernel of `fname`,
+    and its layout: (source, float parameters, Int parameters, leaves) where
+    leaves lists (parameter, leaf path) in the kernel's column order
+    (scalars: path ()).  Every mode writes the primal Float leaves to fout and
+    the Int leaves (scalars, then array cells) to iout after its first sweep."""
+    if mode not in ("grad", "hess", "run", "uncall"):
         raise KindError(f"codegen mode {mode!r}")
     parser = _Parser(src)
     fns = parser.program()
@@ -1608,12 +1628,14 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
         base[p] = len(leaves)
         leaves += [(p, path) for path in (_leaf_paths(shapes[p]) if p in shapes else [()])]
     locals_ = sorted(_collect_vars(fwd, set()) | _collect_vars(inv, set()))
-    em_f = _Emitter(params, kinds, fwd, fname, shapes)
+    plain = mode in ("run", "uncall")
+    em_f = _Emitter(params, kinds, inv if mode == "uncall" else fwd, fname, shapes)
     em_f.depth = 2
-    em_f.stmts(fwd, False, "fwd_done")
+    em_f.stmts(inv if mode == "uncall" else fwd, False, "fwd_done")
     em_g = _Emitter(params, dict(em_f.kinds), inv, fname, shapes)
     em_g.depth = 2
-    em_g.stmts(inv, True, "grad_done")
+    if not plain:
+        em_g.stmts(inv, True, "grad_done")
     allk = dict(em_f.kinds)
     allk.update(em_g.kinds)
     decl = []
@@ -1630,7 +1652,7 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
          " const long long *__restrict__ iin, const double *__restrict__ seeds,"
          " double tol, int chk, long long fuel, double *__restrict__ fout,"
          " double *__restrict__ gout, unsigned char *__restrict__ fail, int dir,"
-         " double *__restrict__ hout) {",
+         " double *__restrict__ hout, long long *__restrict__ iout) {",
          "  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;"
          " i += (long long)gridDim.x * blockDim.x) {",
          "    int code = 0;", "    long long ticks = 0;"]
@@ -1673,14 +1695,27 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
                 out.append("    " + fmt(f"{b}LL", f"v_{c}", f"g_{c}"))
         return out
 
-    L.append("    // ---- run_function (plain forward) ----")
+    L.append("    // ---- " + ("uncall_function (~f)" if mode == "uncall" else
+                                "run_function (plain forward)") + " ----")
     L += em_f.lines
     L.append("  fwd_done:")
     L.append("    if (code) {")
-    L.append(f"      for (int e = 0; e < {NL}; ++e) {{ fout[e * n + i] = NAN; gout[e * n + i] = NAN;"
+    L.append(f"      for (int e = 0; e < {NL}; ++e) {{ fout[e * n + i] = NAN;"
+             + ("" if plain else " gout[e * n + i] = NAN;")
              + (" hout[e * n + i] = NAN;" if hess else "") + " }")
+    L.append(f"      for (int e = 0; e < {nib}; ++e) iout[e * n + i] = 0;")
     L.append("      fail[i] = (unsigned char)code; continue; }")
     L += each_leaf(lambda col, v, g: f"fout[{col} * n + i] = rl_p({v});")
+    for p in ints:
+        if p in shapes:
+            L.append(f"    for (int e = 0; e < {math.prod(shapes[p])}; ++e)"
+                     f" iout[({ibase[p]}LL + e) * n + i] = v_{_cid(p)}[e];")
+        else:
+            L.append(f"    iout[{ibase[p]}LL * n + i] = v_{_cid(p)};")
+    if plain:
+        L += ["    fail[i] = 0;", "  }", "}"]
+        L.append(_LAUNCH)
+        return "\n".join(L), floats, ints, leaves
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
     L.append("    // coerce_to_kind: a seed enters as Dual(seed, 0)")
     L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);")
@@ -1705,19 +1740,7 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     L.append("    fail[i] = (unsigned char)code;")
     L.append("  }")
     L.append("}")
-    L.append(r"""
-extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, const double *seeds,
-                          double tol, int chk, long long fuel, double *fout, double *gout,
-                          unsigned char *fail, int dir, double *hout, void *stream) {
-  if (n <= 0) return 0;
-  const int block = 128;
-  long long grid = (n + block - 1) / block;
-  if (grid > 148 * 16) grid = 148 * 16;
-  rlg_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(n, fin, iin, seeds, tol, chk, fuel,
-                                                                fout, gout, fail, dir, hout);
-  return (int)cudaGetLastError();
-}
-""")
+    L.append(_LAUNCH)
     return "\n".join(L), floats, ints, leaves
 
 
@@ -1785,7 +1808,7 @@ class CompiledFunction:
         self.params = _Parser(source_text).program()[fname][0]
         self.shapes = _check_shapes(array_shapes, (), self.params)
         self._lib = self._load(self.source)
-        self._hlib = None
+        self._libs = {"grad": self._lib}
 
     @staticmethod
     def _load(source):
@@ -1793,8 +1816,23 @@ class CompiledFunction:
         lib.rlg_launch.restype = ctypes.c_int
         lib.rlg_launch.argtypes = [ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
             ctypes.c_double, ctypes.c_int, ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
-            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         return lib
+
+    def _lib_for(self, mode):
+        if mode not in self._libs:
+            self._libs[mode] = self._load(generate(self._text, self.fname, self._ints, mode=mode,
+                                                   array_shapes=self._shapes)[0])
+        return self._libs[mode]
+
+    def run(self, inputs, direction=1, tol=1e-9, invcheck=True, max_steps=10**9):
+        """Batched reference `run` (direction 1) / `uncall` (-1), interpreter.py:
+        1021-1028: one sweep of f or ~f with every check.  Returns (outputs,
+        fail codes), outputs keyed by parameter name (Int values as int64
+        tensors of shape (n,) or (n, *shape))."""
+        lib = self._lib_for("run" if direction > 0 else "uncall")
+        primal, _, fail, _ = self._run(lib, inputs, [], tol, invcheck, max_steps)
+        return primal, fail
 
     def _default_seeds(self):
         """autodiff.default_seeds (autodiff.py:99-110): the first parameter's
@@ -1815,14 +1853,11 @@ class CompiledFunction:
         (H, fail) with H of shape (n, NL, NL), H[:, k, j] = d(cotangent of
         leaf k) / d(leaf j)."""
         self._default_seeds()                 # the reference seeds by default
-        if self._hlib is None:
-            src = generate(self._text, self.fname, self._ints, mode="hess",
-                           array_shapes=self._shapes)[0]
-            self._hlib = self._load(src)
+        hlib = self._lib_for("hess")
         cols = []
         fail = None
         for j in range(len(self.leaves)):
-            _, _, f, h = self._run(self._hlib, inputs, None, tol, invcheck, max_steps, dir_=j)
+            _, _, f, h = self._run(hlib, inputs, None, tol, invcheck, max_steps, dir_=j)
             cols.append(h)
             fail = f if fail is None else torch.maximum(fail, f)
         H = torch.stack(cols, -1).permute(1, 0, 2).contiguous()   # (n, NL_k, NL_j)
@@ -1883,6 +1918,8 @@ class CompiledFunction:
         col = {leaf: k for k, leaf in enumerate(self.leaves)}
         sv = [0.0] * max(1, len(self.leaves))
         for pname, path, val in (self._default_seeds() if seeds is None else seeds):
+            if path is None:
+                path = ()
             if pname not in self.params:
                 raise KindError(f"seed names unknown parameter {pname!r}")
             key = (pname, tuple((a, tuple(b)) for a, b in path))
@@ -1894,10 +1931,11 @@ class CompiledFunction:
         gout = torch.empty_like(fin)
         hout = torch.empty_like(fin) if dir_ >= 0 else None
         fail = torch.empty(n, dtype=torch.uint8, device=dev)
+        iout = torch.empty((max(1, len(ivals)), n), dtype=torch.int64, device=dev)
         rc = lib.rlg_launch(n, fin.data_ptr(), iin.data_ptr(), sv.data_ptr(), float(tol),
                             int(bool(invcheck)), int(max_steps), fout.data_ptr(), gout.data_ptr(),
                             fail.data_ptr(), int(dir_),
-                            hout.data_ptr() if hout is not None else None,
+                            hout.data_ptr() if hout is not None else None, iout.data_ptr(),
                             torch.cuda.current_stream().cuda_stream)
         if rc:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
@@ -1908,7 +1946,12 @@ class CompiledFunction:
             primal[p] = fout[b:b + m].t().reshape((n,) + shp)
             grads[p] = gout[b:b + m].t().reshape((n,) + shp)
             b += m
-        primal.update({p: inputs[p] for p in self.ints})
+        b = 0
+        for p in self.ints:                  # the Int leaves after the first sweep
+            shp = self.shapes.get(p, ())
+            m = math.prod(shp)
+            primal[p] = iout[b:b + m].t().reshape((n,) + shp)
+            b += m
         return primal, grads, fail, hout
 
 

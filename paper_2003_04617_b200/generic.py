@@ -1,0 +1,188 @@
+"""Drop-in entry points for functions WITHOUT a hand-written kernel: the
+function is compiled by codegen.py (the generic .rnl -> CUDA path) for the
+kinds and array shapes of the call's arguments and run on the device.  There
+is still no CPU path: no GPU, no result.
+
+Used by autodiff.gradient / gradient_batch / hessian / jacobian and
+interp.run / uncall / check_reversibility when the program's function is not
+one of the registered benchmark kernels (besselj, ba_proj, ba_weight, gmm).
+Argument kinds follow the reference's values: Python int -> Int, float ->
+Float, Array (ours, the reference's, numpy, torch) of floats -> Float array,
+of ints -> Int array; ULog / Complex / Fixed / Record / Bool arguments are
+outside the compiled subset (UnsupportedProgram).  Results come back in the
+reference's containers (floats, ints, Arrays of the caller's class) and a
+device error raises the reference's exception class for that row.
+"""
+
+import numpy as np
+import torch
+
+from . import codegen
+from .errors import KindError, UnsupportedProgram, error_for_code
+from .values import Array
+
+_CACHE = {}
+
+
+def _is_int(v):
+    return isinstance(v, (int, np.integer)) and not isinstance(v, (bool, np.bool_))
+
+
+def _is_float(v):
+    return isinstance(v, (float, np.floating))
+
+
+def _as_array(v):
+    """ndarray of an Array-like, or None."""
+    if isinstance(v, torch.Tensor):
+        return v.detach().cpu().numpy()
+    if isinstance(v, np.ndarray):
+        return v
+    if hasattr(v, "data") and hasattr(v, "shape"):
+        data = list(v.data)
+        if data and all(_is_int(x) for x in data):
+            return np.asarray(data, dtype=np.int64).reshape(tuple(v.shape))
+        if not all(_is_float(x) or _is_int(x) for x in data):
+            raise UnsupportedProgram("codegen: arrays hold Float or Int values only")
+        if any(_is_int(x) for x in data):
+            raise UnsupportedProgram("codegen: mixed Int / Float arrays are not supported")
+        return np.asarray(data, dtype=np.float64).reshape(tuple(v.shape))
+    return None
+
+
+def _kind(v, name):
+    """("f" | "i" | "a" | "ai", shape) of one argument value."""
+    if isinstance(v, (bool, np.bool_)):
+        raise UnsupportedProgram(f"codegen: Bool argument {name!r} is not supported")
+    if _is_int(v):
+        return "i", ()
+    if _is_float(v):
+        return "f", ()
+    a = _as_array(v)
+    if a is None:
+        raise UnsupportedProgram(f"codegen: argument {name!r} of kind {type(v).__name__} is "
+                                 "outside the compiled subset")
+    if a.ndim not in (1, 2):
+        raise KindError(f"{name}: arrays are 1-d or 2-d")
+    return ("ai" if a.dtype.kind in "iu" else "a"), tuple(a.shape)
+
+
+def compiled(prog, fname, kinds):
+    """The CompiledFunction of prog's `fname` for {param: (kind, shape)}."""
+    if not torch.cuda.is_available():
+        raise UnsupportedProgram(f"{fname}: no CUDA device (generated kernels have no CPU path)")
+    ints = tuple(p for p, (k, _) in kinds.items() if k in ("i", "ai"))
+    shapes = {p: s for p, (k, s) in kinds.items() if k in ("a", "ai")}
+    key = (prog.source, fname, ints, tuple(sorted(shapes.items())))
+    if key not in _CACHE:
+        _CACHE[key] = codegen.CompiledFunction(prog.source, fname, ints, shapes)
+    return _CACHE[key]
+
+
+def _call_kinds(fdef, args):
+    names = fdef.param_names()
+    if len(args) != len(names):
+        raise KindError(f"{fdef.name} takes {len(names)} arguments, got {len(args)}")
+    return names, {p: _kind(v, p) for p, v in zip(names, args)}
+
+
+def _inputs(names, kinds, args):
+    out = {}
+    for p, v in zip(names, args):
+        k = kinds[p][0]
+        out[p] = float(v) if k == "f" else int(v) if k == "i" else _as_array(v)
+    return out
+
+
+def _back(template, kind, value):
+    """One output row in the reference's container."""
+    v = value.cpu().numpy() if isinstance(value, torch.Tensor) else np.asarray(value)
+    if kind == "f":
+        return float(v)
+    if kind == "i":
+        return int(v)
+    data = [int(x) for x in v.ravel()] if kind == "ai" else [float(x) for x in v.ravel()]
+    if isinstance(template, torch.Tensor):
+        return torch.as_tensor(v.copy())
+    if isinstance(template, np.ndarray):
+        return v.copy()
+    cls = type(template) if hasattr(template, "data") and hasattr(template, "shape") else Array
+    try:
+        return cls(data, v.shape)
+    except TypeError:
+        return Array(data, v.shape)
+
+
+def _raise(fail, fname):
+    code = int(fail[0].item())
+    if code:
+        raise error_for_code(code, fname)
+
+
+def gradient(prog, fdef, req, opts):
+    """Reference gradient() (autodiff.py:136-180) through a generated kernel."""
+    names, kinds = _call_kinds(fdef, list(req.args))
+    k = compiled(prog, fdef.name, kinds)
+    primal, grads, fail = k.gradient(_inputs(names, kinds, req.args), seeds=req.seeds,
+                                     tol=opts.float_tolerance, invcheck=opts.invcheck,
+                                     max_steps=opts.max_steps)
+    _raise(fail, fdef.name)
+    outs = [_back(v, kinds[p][0], primal[p][0]) for p, v in zip(names, req.args)]
+    report = req.wrt if req.wrt is not None else names
+    g = {}
+    for p in report:
+        if p not in names:
+            raise KindError(f"wrt names unknown parameter {p!r}")
+        v = req.args[names.index(p)]
+        g[p] = _back(v, kinds[p][0], grads[p][0]) if p in grads else None
+    return outs, g
+
+
+def run(prog, fdef, args, opts, direction):
+    """Reference run / uncall (interpreter.py:1021-1028) through a generated kernel."""
+    names, kinds = _call_kinds(fdef, list(args))
+    k = compiled(prog, fdef.name, kinds)
+    out, fail = k.run(_inputs(names, kinds, args), direction, tol=opts.float_tolerance,
+                      invcheck=opts.invcheck, max_steps=opts.max_steps)
+    _raise(fail, fdef.name)
+    return [_back(v, kinds[p][0], out[p][0]) for p, v in zip(names, args)]
+
+
+def hessian(prog, fdef, args, opts):
+    """Reference hessian() (autodiff.py:216-257): forward-over-reverse over
+    every Float leaf, one Dual-number launch per leaf."""
+    names, kinds = _call_kinds(fdef, list(args))
+    k = compiled(prog, fdef.name, kinds)
+    H, fail = k.hessian(_inputs(names, kinds, args), tol=opts.float_tolerance,
+                        invcheck=opts.invcheck, max_steps=opts.max_steps)
+    _raise(fail, fdef.name)
+    return H[0].cpu().numpy()
+
+
+def gradient_batch(prog, fdef, inputs, seeds, wrt, opts):
+    """Batched gradient: row i of every tensor is one call.  A Float
+    parameter takes an (n,) tensor or a float, a Float array an (n, *shape)
+    tensor or one Array-like shared by all rows, Int parameters plain ints /
+    Int Array-likes (uniform over the batch).  Returns (primal, grads, fail)."""
+    names = fdef.param_names()
+    kinds, vals = {}, {}
+    for p in names:
+        if p not in inputs:
+            raise KindError(f"gradient_batch: no input for parameter {p!r}")
+        v = inputs[p]
+        if isinstance(v, torch.Tensor) and v.dtype == torch.float64 and v.dim() >= 1:
+            kinds[p] = ("f", ()) if v.dim() == 1 else ("a", tuple(v.shape[1:]))
+            vals[p] = v
+        else:
+            kinds[p] = _kind(v, p)
+            vals[p] = _inputs([p], kinds, [v])[p]
+    k = compiled(prog, fdef.name, kinds)
+    primal, grads, fail = k.gradient(vals, seeds=seeds, tol=opts.float_tolerance,
+                                     invcheck=opts.invcheck, max_steps=opts.max_steps)
+    report = wrt if wrt is not None else [p for p in names if p in grads]
+    for p in report:
+        if p not in names:
+            raise KindError(f"wrt names unknown parameter {p!r}")
+        if p not in grads:
+            raise KindError(f"{p!r} is an Int parameter: it has no cotangent")
+    return primal, {p: grads[p] for p in report}, fail

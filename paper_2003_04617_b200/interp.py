@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import kernels
-from .autodiff import _check_opts, _device, _is_float, _is_int, _resolve
+from .autodiff import _check_opts, _device, _is_float, _is_int, _lookup
 from .errors import KindError, RevLangError, error_for_code
 from .values import to_numpy
 
@@ -100,17 +100,23 @@ _RUNNERS = {"besselj": _run_besselj, "ba_proj": _run_ba_proj, "ba_weight": _run_
 
 
 def run(program, fname, args, opts=None):
-    """Reference `run` (interpreter.py:1021): execute f forward on the device."""
+    """Reference `run` (interpreter.py:1021): execute f forward on the device
+    (a registered kernel, else the function compiled by codegen)."""
+    return _dispatch(program, fname, args, opts, +1)
+
+
+def _dispatch(program, fname, args, opts, direction):
     opts = _check_opts(opts)
-    fdef = _resolve(program, fname)
-    return _RUNNERS[fdef.kernel.handler](fdef, list(args), opts, +1)
+    prog, fdef, reg = _lookup(program, fname)
+    if not reg:
+        from . import generic
+        return generic.run(prog, fdef, list(args), opts, direction)
+    return _RUNNERS[fdef.kernel.handler](fdef, list(args), opts, direction)
 
 
 def uncall(program, fname, args, opts=None):
     """Reference `uncall` (interpreter.py:1026): execute ~f; uncall(run(a)) == a."""
-    opts = _check_opts(opts)
-    fdef = _resolve(program, fname)
-    return _RUNNERS[fdef.kernel.handler](fdef, list(args), opts, -1)
+    return _dispatch(program, fname, args, opts, -1)
 
 
 @dataclass

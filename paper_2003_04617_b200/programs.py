@@ -4,8 +4,9 @@ The reference's programs are `.rnl` text parsed into an IR (parser.py:593,
 ir.py:235) and executed by an interpreter.  Here a program is recognised,
 function by function, against the registered benchmark programs
 (programs/*.rnl) by a normalised token fingerprint; each registered
-function is bound to a hand-written sm_100a kernel.  Anything else raises
-`UnsupportedProgram` — there is no interpreter and no CPU fallback.
+function is bound to a hand-written sm_100a kernel.  Any other function is
+compiled to a device kernel by codegen.py when it is called (generic.py);
+there is no interpreter and no CPU fallback.
 
 Fingerprints ignore comments, whitespace, line breaks, the ASCII/Unicode
 spelling of arrows (parser.py:143-164) and the spelling of numeric
@@ -146,8 +147,8 @@ class FunctionDef:
 
 class Program:
     """A program whose functions are looked up by name (reference ir.Program,
-    ir.py:235).  Unregistered functions are kept so that calling them gives
-    a precise `UnsupportedProgram` error."""
+    ir.py:235).  Unregistered functions are kept with their source text for
+    the generic compiler (codegen.py / generic.py)."""
 
     def __init__(self, functions, source="", filename="<string>"):
         self.functions = {f.name: f for f in functions}
@@ -215,7 +216,7 @@ def parse_program(text, filename="<string>"):
 
     Mirrors reference parse_program (parser.py:593) for the registered
     programs.  A function whose text differs from every registered one is
-    kept without a kernel (calling it raises UnsupportedProgram).  Helper
+    kept without a kernel (calling it compiles it with codegen.py).  Helper
     functions (rodrigues) bind only together with their caller."""
     funcs = split_functions(tokenize(text))
     out = []
