@@ -594,10 +594,9 @@ int launch_ba(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams, 
   auto kern = err ? (Jfeat ? k_ba_jac<true, true> : k_ba_jac<true, false>)
                   : (Jfeat ? k_ba_jac<false, true> : k_ba_jac<false, false>);
   int bps = 0;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
-                   "smem attr");
+  rc = smem_attr((const void *)kern, BA_SMEM, "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
+  rc = occupancy(&bps, (const void *)kern, BA_BLOCK, BA_SMEM,
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
@@ -623,10 +622,9 @@ int launch_ba_residuals(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doub
   if (n_obs == 0) return RL_OK;
   auto kern = k_ba_jac<true, false, false>;
   int bps = 0;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM),
-                   "smem attr");
+  rc = smem_attr((const void *)kern, BA_SMEM, "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM),
+  rc = occupancy(&bps, (const void *)kern, BA_BLOCK, BA_SMEM,
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;
@@ -665,10 +663,9 @@ int launch_ba_csr(int32_t n_cams, int32_t n_pts, int64_t n_obs, int64_t obs_offs
   }
   auto kern = err ? k_ba_jac<true, false, true, true> : k_ba_jac<false, false, true, true>;
   int bps = 0;
-  rc = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BA_SMEM_CSR),
-                   "smem attr");
+  rc = smem_attr((const void *)kern, BA_SMEM_CSR, "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, BA_BLOCK, BA_SMEM_CSR),
+  rc = occupancy(&bps, (const void *)kern, BA_BLOCK, BA_SMEM_CSR,
                    "occupancy");
   if (rc) return rc;
   long long want = (n_obs + BA_BLOCK - 1) / BA_BLOCK;

@@ -834,12 +834,9 @@ static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, 
   if (n == 0) return RL_OK;
   const int smem = BJ_SMEM + (MODE == BJ_HESS ? BJ_C * 8 : 0);
   int blocks_per_sm = 0;
-  rc = cuda_status(cudaFuncSetAttribute(k_besselj<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        smem), "smem attr");
+  rc = smem_attr((const void *)k_besselj<MODE>, smem, "smem attr");
   if (rc) return rc;
-  rc = cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_besselj<MODE>,
-                                                                 BJ_BLOCK, smem),
-                   "occupancy");
+  rc = occupancy(&blocks_per_sm, (const void *)k_besselj<MODE>, BJ_BLOCK, smem, "occupancy");
   if (rc) return rc;
   const long long want = (n + BJ_C - 1) / BJ_C;
   const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);

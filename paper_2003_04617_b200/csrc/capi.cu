@@ -7,7 +7,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -63,6 +65,38 @@ int cuda_status(cudaError_t e, const char *where) {
 }
 
 constexpr int MAX_DEV = 64;
+
+int smem_attr(const void *fn, size_t bytes, const char *what) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t &have = done[{fn, dev}];
+  if (have >= bytes) return RL_OK;
+  const int rc = cuda_status(
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), what);
+  if (!rc) have = bytes;
+  return rc;
+}
+
+int occupancy(int *blocks_per_sm, const void *fn, int block, size_t smem, const char *what) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, int, size_t>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_tuple(fn, dev, block, smem);
+  const auto it = done.find(key);
+  if (it != done.end()) {
+    *blocks_per_sm = it->second;
+    return RL_OK;
+  }
+  const int rc = cuda_status(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, block, smem), what);
+  if (!rc) done[key] = *blocks_per_sm;
+  return rc;
+}
 
 int ensure_device_tables() {
   static std::once_flag once[MAX_DEV];

@@ -27,6 +27,12 @@ constexpr int LOGTAB_N = 4096;
 int cuda_status(cudaError_t e, const char *where);
 int set_error(int code, const char *msg);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) / the occupancy query,
+// cached per (function, device[, block, smem]): a host-buffer call or an
+// un-graphed launch chain would otherwise pay them on every evaluation.
+int smem_attr(const void *fn, size_t bytes, const char *what);
+int occupancy(int *blocks_per_sm, const void *fn, int block, size_t smem, const char *what);
+
 // Upload constant tables for the current device (idempotent, thread-safe).
 int ensure_device_tables();
 

@@ -967,32 +967,29 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   double *par = (double *)(ws + L.par);
   int rc;
   const size_t sp = ((size_t)d * (d + 1) / 2 + K) * 8;
-  if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_prep<DP>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp),
-                        "smem attr prep")))
-    return rc;
+  if ((rc = smem_attr((const void *)k_gmm_prep<DP>, sp, "smem attr prep"))) return rc;
+#ifndef GMM_ABLATE
+#define GMM_ABLATE 0   // timing-only builds (tools/build_variants.sh): skip kernels by bit
+#endif
+  if (!(GMM_ABLATE & 1))
   k_gmm_prep<DP><<<K, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
                                              add_params ? par : nullptr, flags, N);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
     constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
     static_assert(sf <= 227 * 1024 && sr <= 227 * 1024, "shared memory budget");
-    if ((rc = cuda_status(cudaFuncSetAttribute(k_gmm_fwd<DP, TPF>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sf), "smem attr fwd")) ||
-        (rc = cuda_status(cudaFuncSetAttribute(k_gmm_rev<DP, TPR>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sr), "smem attr rev")))
+    if ((rc = smem_attr((const void *)k_gmm_fwd<DP, TPF>, sf, "smem attr fwd")) ||
+        (rc = smem_attr((const void *)k_gmm_rev<DP, TPR>, sr, "smem attr rev")))
       return rc;
-    if ((rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
+    if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
                          d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags)))
       return rc;
-    if ((rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st, K, N, mt,
+    if (!(GMM_ABLATE & 2) && (rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st, K, N, mt,
                          gmt, flags, tol, chk, errp, fail, counters)))
       return rc;
     if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
                                          add_params, out, st);
-    if ((rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
+    if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
                          d, K, N, means, x, LT, gmt, part)))
       return rc;
   } else if (!grad) {
@@ -1003,10 +1000,11 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       return rc;
   }
   const long long PW = (long long)DP * DP + DP + 1;
-  if ((rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
+  if (!(GMM_ABLATE & 4) && (rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
                        dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K),
                        dim3(GMM_THREADS), 0, st, L.Sr, PW, part, redp)))
     return rc;
+  if (GMM_ABLATE & 8) return 0;
   return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K), dim3(GMM_THREADS), 0, st, d, K, 1,
                     N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, redp, errp, par, gamma, m, cst,
                     add_params, out);
