@@ -238,7 +238,10 @@ int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr,
   Pipeline pl;
   int rc = pl.init(device);
   if (rc) return rc;
-  const int64_t CH = int64_t(1) << 22;  // 4 Mi elements = 32 MiB of z per chunk
+#ifndef BJ_HOST_CH_LOG2
+#define BJ_HOST_CH_LOG2 22
+#endif
+  const int64_t CH = int64_t(1) << BJ_HOST_CH_LOG2;  // elements per chunk (4 Mi = 32 MiB of z)
   const int64_t nch = (n + CH - 1) / CH;
   const int64_t bufn = std::min<int64_t>(CH, std::max<int64_t>(n, 1));
   DevBuf dz[Pipeline::NS], dJ[Pipeline::NS], dg[Pipeline::NS], df[Pipeline::NS], dc;
