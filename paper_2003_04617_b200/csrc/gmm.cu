@@ -54,6 +54,9 @@ namespace rl {
 #ifndef GMM_SPLIT_HYST
 #define GMM_SPLIT_HYST 0.03  // wave-efficiency gain needed to take a larger point split (measured)
 #endif
+#ifndef GMM_MT_RR
+#define GMM_MT_RR 1        // factor-adjoint tiles dealt round-robin over the warps
+#endif
 #ifndef GMM_TPF
 #define GMM_TPF 64         // forward tile (points) for DP = 64
 #endif
@@ -540,7 +543,14 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   double M[MTL::PER][4];
 #pragma unroll
   for (int q = 0; q < MTL::PER; q++) {
+#if GMM_MT_RR
+    // round-robin: warp w and w + 4 share a scheduler partition, so every
+    // partition gets the same number of tiles (contiguous blocks of PER left
+    // warp 7 without tiles and partitions 0 / 1 with twice partition 3's)
+    const int t = q * GMM_WARPS + w;
+#else
     const int t = w * MTL::PER + q;
+#endif
     if (t < MTL::COUNT) {
       mtile_ij<DP>(t, ti[q], tj[q]);
     } else {
