@@ -804,9 +804,22 @@ __device__ __forceinline__ double g_exp(double x, int &c) {
   if (isinf(r) && isfinite(x)) { if (!c) c = RC_OVERFLOW; }
   return r;
 }
+// CPython float ** float (s_pow, values.py:408-421): x ** 0 and 1 ** y are 1.0,
+// 0 ** negative raises, a finite result that overflows raises OverflowError;
+// otherwise the host's correctly rounded pow().  The exponents whose correctly
+// rounded power is one IEEE operation take it (libdevice pow is not exact
+// there: 3.0 ** 1.0 would come out 1 ulp low).
 __device__ __forceinline__ double g_pow(double a, double b, int &c) {
+  if (b == 0.0 || a == 1.0) return 1.0;
   if ((a == 0.0 && b < 0.0) || (a < 0.0 && b != floor(b))) { if (!c) c = RC_DOMAIN; return 0.0; }
-  return pow(a, b);
+  double r;
+  if (b == 1.0) r = a;
+  else if (b == 2.0) r = a * a;
+  else if (b == -1.0) r = 1.0 / a;
+  else if (b == 0.5) r = a == 0.0 ? 0.0 : sqrt(a);   // pow(-0, 0.5) = +0
+  else r = pow(a, b);
+  if (isinf(r) && isfinite(a) && isfinite(b)) { if (!c) c = RC_OVERFLOW; }
+  return r;
 }
 // ---- Dual numbers (reference values.py:258-431): the Hessian build runs the
 // same generated code with R = Dl.  Doubles promote to Dl(d, 0) (_as_dual);
