@@ -15,7 +15,7 @@ plus the batched device API over torch CUDA tensors:
 """
 
 from .autodiff import (ExecOptions, GradRequest, HessianResult, gradient, gradient_batch,
-                       hessian, jacobian)
+                       finite_difference, hessian, jacobian)
 from .errors import (AliasedArguments, AssertFailed, DirtyAncilla, FuelExhausted, IndexOutOfBounds,
                      KindError, LoopIteratorMutated, MissingAdjoint, NativeLibraryError,
                      PostconditionMismatch, RevDomainError, RevError, RevLangError,
@@ -29,7 +29,7 @@ from .programs import CATALOG, Program, entry_function, load_example, parse_prog
 from .values import Array
 
 __all__ = [
-    "HessianResult", "hessian", "gradient_batch", "CompiledFunction", "compile_function", "BesselHessResult", "besselj_hess",
+    "HessianResult", "finite_difference", "hessian", "gradient_batch", "CompiledFunction", "compile_function", "BesselHessResult", "besselj_hess",
     "AliasedArguments", "AssertFailed", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "run", "uncall",

@@ -186,3 +186,75 @@ def gradient_batch(prog, fdef, inputs, seeds, wrt, opts):
         if p not in grads:
             raise KindError(f"{p!r} is an Int parameter: it has no cotangent")
     return primal, {p: grads[p] for p in report}, fail
+
+
+def _leaf_rows(kinds, names, args):
+    """[(param, flat index or None)] over the Float leaves, leaf_paths order."""
+    out = []
+    for p, v in zip(names, args):
+        k, shp = kinds[p]
+        if k == "f":
+            out.append((p, None))
+        elif k == "a":
+            out += [(p, i) for i in range(int(np.prod(shp)))]
+    return out
+
+
+def finite_difference(prog, fdef, args, h, seeds, opts):
+    """Reference finite_difference (autodiff.py:270-318): central differences
+    of the seeded scalar output per Float input leaf, every perturbed call of
+    one leaf set run as ONE batched launch of the generated run kernel."""
+    names, kinds = _call_kinds(fdef, list(args))
+    k = compiled(prog, fdef.name, kinds)
+    if seeds is None:
+        seeds = k._default_seeds()
+    base = _inputs(names, kinds, args)
+    leaves = _leaf_rows(kinds, names, args)
+    n = 2 * len(leaves)
+    batch, steps = {}, []
+    for p in names:
+        kind, shp = kinds[p]
+        if kind in ("f", "a"):
+            a = np.asarray(base[p], dtype=np.float64)
+            batch[p] = np.broadcast_to(a, (max(n, 1),) + a.shape).copy()
+        else:
+            batch[p] = base[p]
+    for r, (p, i) in enumerate(leaves):
+        col = batch[p] if i is None else batch[p].reshape(n, -1)
+        x = float(base[p]) if i is None else float(np.asarray(base[p]).ravel()[i])
+        up, dn = x + h, x - h
+        steps.append(up - dn)                            # the step actually taken
+        if i is None:
+            col[2 * r], col[2 * r + 1] = up, dn
+        else:
+            col[2 * r, i], col[2 * r + 1, i] = up, dn
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tens = {p: (torch.as_tensor(v, device=dev) if kinds[p][0] in ("f", "a") else v)
+            for p, v in batch.items()}
+    out, fail = k.run(tens, 1, tol=opts.float_tolerance, invcheck=opts.invcheck,
+                      max_steps=opts.max_steps)
+    f = fail.cpu().numpy()
+    if n and f.any():                                   # the reference stops at the first
+        raise error_for_code(int(f[np.nonzero(f)[0][0]]), fdef.name)
+    total = np.zeros(max(n, 1))
+    for pname, path, seed in seeds:                      # seeded_scalar
+        if pname not in names:
+            raise KindError(f"seed names unknown parameter {pname!r}")
+        v = out[pname].cpu().numpy().reshape(max(n, 1), -1)
+        if path:
+            idx = path[0][1]
+            shp = kinds[pname][1]
+            j = int(np.ravel_multi_index(tuple(x - 1 for x in idx), shp))
+        else:
+            j = 0
+        total = total + float(seed) * v[:, j]
+    grads = {}
+    for p, v in zip(names, args):
+        kind, shp = kinds[p]
+        if kind in ("i", "ai"):
+            grads[p] = None
+            continue
+        rows = [r for r, (q, _) in enumerate(leaves) if q == p]
+        vals = [(total[2 * r] - total[2 * r + 1]) / steps[r] for r in rows]
+        grads[p] = float(vals[0]) if kind == "f" else _back(v, "a", np.asarray(vals).reshape(shp))
+    return grads

@@ -83,3 +83,53 @@ def test_adjoint_unit_rules(cuda):
     assert g["x"] == pytest.approx(1.0 / 6.0, rel=1e-15)
     _, g = rg.gradient("fn f(y!, a, b)\ny! += a * b\nend\n", rg.GradRequest("f", [1.0, 6.0, 10.0]))
     assert g["a"] == 10.0 and g["b"] == 6.0
+
+
+def _worst(g, f):
+    """test_acceptance.py _compare_grad_structure: |g - f| / max(|f|, 1e-2)."""
+    w = 0.0
+    for p, fv in f.items():
+        if fv is None or g.get(p) is None:
+            continue
+        a = np.ravel(np.asarray(g[p].data if hasattr(g[p], "data") else g[p], float))
+        b = np.ravel(np.asarray(fv.data if hasattr(fv, "data") else fv, float))
+        w = max(w, float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-2))))
+    return w
+
+
+@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "prims", "quad", "vlen"])
+def test_gradient_matches_central_differences(cuda, golden, name):
+    """test_acceptance.py:131-150 (criterion 4: gradient vs central
+    differences, h = 1e-6, rel err < 1e-5 on 20 points) and :184-196
+    (criterion 7: the arguments are untouched by every gradient call)."""
+    g = golden("codegen")
+    rng = np.random.default_rng(7)
+    ints = {"sink": [3], "wloop": [5], "prims": [3]}.get(name, [])
+    worst = 0.0
+    for trial in range(20):
+        if name == "quad":
+            args = [float(rng.uniform(-1, 1)), rg.Array.vector(rng.uniform(-1, 1, 3).tolist()),
+                    rg.Array.matrix(rng.uniform(-1, 1, (3, 3)).tolist()),
+                    rg.Array.vector(rng.uniform(-1, 1, 3).tolist())]
+        elif name == "vlen":
+            args = [0.0, 0.0, rg.Array.vector(rng.uniform(-1, 1, 7).tolist())]
+        else:
+            ok = np.nonzero(g[name + "_err"] == "")[0]
+            args = [float(v) for v in g[name + "_x"][ok[trial % len(ok)]]] + ints
+        before = [list(a.data) if hasattr(a, "data") else a for a in args]
+        _, grads = rg.gradient(src(name), rg.GradRequest(name, args))
+        fd = rg.finite_difference(src(name), name, args, 1e-6)
+        worst = max(worst, _worst(grads, fd))
+        assert [list(a.data) if hasattr(a, "data") else a for a in args] == before
+    assert worst < 1e-5, worst
+
+
+def test_finite_difference_registered_programs(cuda):
+    """The same check on a registered (hand-written) kernel: besselj."""
+    p = rg.load_example("besselj")
+    args = [0.0, 2, 3.7]
+    _, g = rg.gradient(p, rg.GradRequest("besselj", args))
+    fd = rg.finite_difference(p, "besselj", args, 1e-6)
+    assert fd["nu"] is None and abs(g["z"] - fd["z"]) <= 1e-5 * max(abs(fd["z"]), 1e-2)
+    with pytest.raises(rg.KindError):
+        rg.finite_difference(p, "besselj", args, 0.0)
