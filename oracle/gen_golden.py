@@ -426,10 +426,41 @@ def gen_codegen_dropin():
     print("codegen drop-in goldens:", {k: np.shape(v) for k, v in out.items()})
 
 
+def gen_codegen_nbody():
+    """reference gradient() / run / uncall of tests/golden/codegen/nbody.rnl
+    (nested calls whose view arguments are indexed by a loop variable that is
+    itself an argument; 2-d arrays; routines in the callee): 4 bodies, 3
+    steps, 12 random systems, seeds on pos![1, 1] and vel![2, 3]."""
+    from revlang.interpreter import run, uncall
+    from revlang.values import Array
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "nbody.rnl")).read())
+    rng = np.random.default_rng(11)
+    nb, n = 4, 12
+    X = np.concatenate([rng.uniform(-1, 1, (n, nb * 3)), rng.uniform(-0.2, 0.2, (n, nb * 3)),
+                        rng.uniform(0.5, 1.5, (n, nb)), np.full((n, 1), 0.01)], 1)
+    seeds = [("pos!", (("idx", (1, 1)),), 1.0), ("vel!", (("idx", (2, 3)),), 0.5)]
+    P, G, R, U = [], [], [], []
+    for row in X:
+        pos, vel = row[:12].reshape(nb, 3), row[12:24].reshape(nb, 3)
+        mass, h = row[24:28], float(row[28])
+        args = lambda: [Array.matrix(pos.tolist()), Array.matrix(vel.tolist()),  # noqa: E731
+                        Array.vector(mass.tolist()), h, 3]
+        prim, g = gradient(prog, GradRequest("nbody", args(), seeds=seeds))
+        P.append(list(prim[0].data) + list(prim[1].data))
+        G.append(list(g["pos!"].data) + list(g["vel!"].data) + list(g["mass"].data) + [g["h"]])
+        r = run(prog, "nbody", args())
+        R.append(list(r[0].data) + list(r[1].data))
+        u = uncall(prog, "nbody", args())
+        U.append(list(u[0].data) + list(u[1].data))
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_nbody.npz"), x=X, primal=np.array(P),
+                        grad=np.array(G), run=np.array(R), uncall=np.array(U))
+    print("nbody goldens:", np.array(G).shape)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
-                              "codegen_dropin"]
+                              "codegen_dropin", "codegen_nbody"]
     for w in which:
         globals()["gen_" + w]()

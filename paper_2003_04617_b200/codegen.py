@@ -691,6 +691,41 @@ class _Inliner:
                 out.append(s)
         return tuple(out)
 
+    def writes(self, fname, param, uncall, stack):
+        """May function `fname` (its inverse when `uncall`) write `param`?
+        Instruction targets, primitive and call arguments (followed into the
+        callee), (de)allocations and loop variables are writes."""
+        if fname not in self.fns or fname in stack[:-1]:
+            return True
+        params, body = self.fns[fname]
+
+        def touched(ss):
+            for st in ss:
+                if isinstance(st, Instr) and st.target.name == param:
+                    return True
+                if isinstance(st, (Alloc, Dealloc)) and st.name == param:
+                    return True
+                if isinstance(st, For) and (st.var == param or touched(st.body)):
+                    return True
+                if isinstance(st, While) and touched(st.body):
+                    return True
+                if isinstance(st, If) and (touched(st.then) or touched(st.els)):
+                    return True
+                if isinstance(st, RBegin) and touched(st.body):
+                    return True
+                if isinstance(st, tuple) and touched(st):
+                    return True
+                if isinstance(st, PCall):
+                    for q, a in zip(self.fns.get(st.f, ((),))[0] if st.f not in PRIM_ARITY
+                                    else [None] * len(st.args), st.args):
+                        if a.name != param:
+                            continue
+                        if st.f in PRIM_ARITY or q is None or \
+                                self.writes(st.f, q, st.uncall, stack + (st.f,)):
+                            return True
+            return False
+        return touched(body)
+
     def call(self, s, stack):
         if s.f not in self.fns:
             raise UnsupportedProgram(f"codegen: no function named {s.f!r}")
@@ -699,11 +734,18 @@ class _Inliner:
         params, body = self.fns[s.f]
         if len(params) != len(s.args):
             raise KindError(f"{s.f} takes {len(params)} arguments, got {len(s.args)}")
-        scalars = {a.name for a in s.args if isinstance(a, Var)}
+        # a view argument whose index reads another argument of the call is
+        # exact when inlined only if the callee never writes that parameter
+        # (the reference re-evaluates the index when it writes the view back)
         for a in s.args:
-            if isinstance(a, IView) and _expr_names(Call("", a.idx), set()) & scalars:
-                raise UnsupportedProgram("codegen: an argument's index uses another argument "
-                                         "of the same call")
+            if not isinstance(a, IView):
+                continue
+            used = _expr_names(Call("", a.idx), set())
+            for q, b in zip(params, s.args):
+                if isinstance(b, Var) and b.name in used and \
+                        self.writes(s.f, q, s.uncall, stack + (s.f,)):
+                    raise UnsupportedProgram("codegen: an argument's index uses an argument the "
+                                             "callee writes")
         body = _expand(_invert_list(body) if s.uncall else body)
         _balanced(body, s.f)
         self.n += 1

@@ -89,3 +89,48 @@ def test_generated_source_compiles_for_sm100a(tmp_path, monkeypatch):
     source = codegen.generate(src("quad"), "quad", array_shapes={"r!": 3, "A": (3, 3), "u": 3},
                               mode="hess")[0]
     assert os.path.exists(codegen.build(source))
+
+
+def test_view_argument_indexed_by_another_argument():
+    """kick_pair-style calls: a view argument indexed by a scalar that is
+    also passed is inlined when the callee never writes that parameter."""
+    text = src("nbody")
+    codegen.generate(text, "nbody", ("steps",),
+                     array_shapes={"pos!": (4, 3), "vel!": (4, 3), "mass": 4})
+    bad = ("fn g(y!, k)\n    y! += 1.0\n    k += 1\nend\n"
+           "fn f(x::array, k)\n    g(x[k], k)\nend\n")
+    with pytest.raises(UnsupportedProgram):
+        codegen.generate(bad, "f", ("k",), array_shapes={"x": 3})
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src"),
+                    reason="the reference is only present in the build container")
+def test_reference_catalog_programs_in_the_subset_compile(tmp_path, monkeypatch):
+    """The reference's own catalog (stdlib.CATALOG), pretty-printed by the
+    reference and compiled here: every program whose argument kinds are in
+    the subset generates and builds for sm_100a; Complex / Fixed / bijector
+    programs are rejected with UnsupportedProgram."""
+    import random
+    import sys
+    monkeypatch.setenv("REVGPU_CODEGEN_CACHE", str(tmp_path))
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from revlang.parser import pretty_print
+        from revlang.stdlib import CATALOG, entry_function, load_example, sample_args
+    finally:
+        sys.path.pop(0)
+    from paper_2003_04617_b200 import generic
+    built, rejected = [], []
+    for name in CATALOG:
+        p, fn = load_example(name), entry_function(name)
+        args = sample_args(name, random.Random(1))
+        try:
+            kinds = {nm: generic._kind(v, nm) for nm, v in zip(p.get(fn).param_names(), args)}
+            ints = tuple(k for k, (kk, _) in kinds.items() if kk in ("i", "ai"))
+            shapes = {k: s for k, (kk, s) in kinds.items() if kk in ("a", "ai")}
+            codegen.build(codegen.generate(pretty_print(p), fn, ints, array_shapes=shapes)[0])
+            built.append(name)
+        except UnsupportedProgram:
+            rejected.append(name)
+    assert {"multiplier", "i_affine", "i_umm", "r_norm", "leapfrog_clean",
+            "leapfrog_cumulative"} <= set(built), (built, rejected)

@@ -114,3 +114,31 @@ def test_generic_ba_hessian(cuda, golden):
     ref = golden("codegen_programs")["ba_hess"]
     for o in range(4):
         assert close(H[o].cpu().numpy(), ref[o], 1e-9, 1e-11).all(), o
+
+
+def test_nbody_nested_calls_bit_exact(cuda, golden):
+    """tests/golden/codegen/nbody.rnl: kick -> pull calls whose view
+    arguments vel![a, c] are indexed by the loop variable a passed alongside
+    (inlined: pull never writes a), 2-d arrays, a routine in the callee.
+    Only + - * / sqrt: correctly rounded on both sides, so the batched
+    gradient, run and uncall equal the reference interpreter bit for bit."""
+    from test_codegen_gpu import src
+    g = golden("codegen_nbody")
+    X = g["x"]
+    n = X.shape[0]
+    k = codegen.compile_function(src("nbody"), "nbody", int_params=("steps",),
+                                 array_shapes={"pos!": (4, 3), "vel!": (4, 3), "mass": 4})
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=cuda)  # noqa: E731
+    inputs = {"pos!": t(X[:, :12].reshape(n, 4, 3)), "vel!": t(X[:, 12:24].reshape(n, 4, 3)),
+              "mass": t(X[:, 24:28]), "h": t(X[:, 28]), "steps": 3}
+    seeds = [("pos!", (("idx", (1, 1)),), 1.0), ("vel!", (("idx", (2, 3)),), 0.5)]
+    primal, grads, fail = k.gradient(inputs, seeds=seeds)
+    out, rfail = k.run(inputs, 1)
+    back, ufail = k.run(inputs, -1)
+    torch.cuda.synchronize()
+    assert not fail.any() and not rfail.any() and not ufail.any()
+    flat = lambda d, names: torch.cat([d[p].reshape(n, -1) for p in names], 1).cpu().numpy()  # noqa
+    assert np.array_equal(flat(primal, ["pos!", "vel!"]), g["primal"])
+    assert np.array_equal(flat(grads, ["pos!", "vel!", "mass", "h"]), g["grad"])
+    assert np.array_equal(flat(out, ["pos!", "vel!"]), g["run"])
+    assert np.array_equal(flat(back, ["pos!", "vel!"]), g["uncall"])
