@@ -54,6 +54,9 @@ namespace rl {
 #ifndef GMM_SPLIT_HYST
 #define GMM_SPLIT_HYST 0.03  // wave-efficiency gain needed to take a larger point split (measured)
 #endif
+#ifndef GMM_FUSE_FINAL
+#define GMM_FUSE_FINAL 1   // k_gmm_final sums the reverse partials itself (no k_gmm_reduce)
+#endif
 #ifndef GMM_MT_RR
 #define GMM_MT_RR 1        // factor-adjoint tiles dealt round-robin over the warps
 #endif
@@ -723,7 +726,11 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     double cst, int add_params, double *__restrict__ out) {
   pdl_wait();
 
-  const int k = blockIdx.x;
+  // grid (K, C): CTA (k, c) takes every C-th block of the triangle; c == 0
+  // also alphas.g, means.g and (k == 0) the objective.  The S per-CTA
+  // partials of k_gmm_rev are summed here in k_gmm_reduce's order (0.0 +
+  // p_0 + p_1 + ...), only over the entries used (the lower triangle)
+  const int k = blockIdx.x, c = blockIdx.y, C = gridDim.y;
   const int P = d * (d + 1) / 2;
   const long long PW = (long long)DP * DP + DP + 1;
   const double hg2 = 0.5 * ga * ga;
@@ -732,23 +739,24 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
   double *g_alpha = out + 1;
   double *g_means = out + 1 + K;
   double *g_icf = out + 1 + K + (long long)K * d;
-  const double *pk = part + (long long)k * S * PW;     // reduced partials: S == 1
+  const double *pk = part + (long long)k * S * PW;
   // column sums of qxc.g and sum of mt.g
   for (int b = threadIdx.x; b <= DP; b += GMM_THREADS) {
+    if (c != 0 && b != DP) continue;
     double s = 0.0;
     for (int j = 0; j < S; j++) s += pk[j * PW + (long long)DP * DP + b];
     if (b < DP) gsum[b] = s;
     else sg = s;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (c == 0 && threadIdx.x == 0) {
     const double ga_k = sg + (add_params ? ws_par[k] : 0.0);
     g_alpha[k] = ga_k;
   }
   // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a):
   // GMM_THREADS / DP lanes per row, shuffle-reduced
   const double *lt = LT + (long long)k * ltb_size(DP);
-  {
+  if (c == 0) {
     constexpr int LR = GMM_THREADS / DP;                 // lanes per row: 8, 4, 2
     const int a = threadIdx.x / LR, l = threadIdx.x % LR;
     double s = 0.0;
@@ -767,12 +775,14 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
   const double sqg = sg + (add_params ? -(double)wm : 0.0);
   const int T = d * (d + 1) / 2;
 #pragma unroll 2
-  for (int e = threadIdx.x; e < T; e += GMM_THREADS) {
+  for (int e = c * GMM_THREADS + threadIdx.x; e < T; e += GMM_THREADS * C) {
     int b = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     if (b * (b + 1) / 2 > e) b--;
     if ((b + 1) * (b + 2) / 2 <= e) b++;
     const int a = e - b * (b + 1) / 2;
-    const double m = pk[(long long)b * DP + a];
+    double m = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < S; j++) m += pk[j * PW + (long long)b * DP + a];
     double g;
     if (a == b) {
       const int j = a;
@@ -787,7 +797,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     }
   }
   __shared__ double ered[GMM_THREADS];
-  if (k == 0) {
+  if (k == 0 && c == 0) {
     sum_err_parts(nerr, err_part, ered);
     // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst);
     // fro and ssq summed in component order from shared-memory chunks
@@ -1010,6 +1020,15 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       return rc;
   }
   const long long PW = (long long)DP * DP + DP + 1;
+#if GMM_FUSE_FINAL
+  (void)redp;
+  if (GMM_ABLATE & 8) return 0;
+  // enough (k, c) CTAs for about two per SM, at most 8 per component
+  const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
+  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K, fc), dim3(GMM_THREADS), 0, st, d, K,
+                    L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, part, errp, par, gamma, m, cst,
+                    add_params, out);
+#else
   if (!(GMM_ABLATE & 4) && (rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
                        dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K),
                        dim3(GMM_THREADS), 0, st, L.Sr, PW, part, redp)))
@@ -1018,6 +1037,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K), dim3(GMM_THREADS), 0, st, d, K, 1,
                     N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, redp, errp, par, gamma, m, cst,
                     add_params, out);
+#endif
 }
 
 int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
