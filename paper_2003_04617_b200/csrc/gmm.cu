@@ -54,6 +54,9 @@ namespace rl {
 #ifndef GMM_SPLIT_HYST
 #define GMM_SPLIT_HYST 0.03  // wave-efficiency gain needed to take a larger point split (measured)
 #endif
+#ifndef GMM_ALPHA_BLOCK
+#define GMM_ALPHA_BLOCK 1  // k_gmm_prep: the alphas' logsumexp in its own block (else block 0)
+#endif
 #ifndef GMM_FUSE_FINAL
 #define GMM_FUSE_FINAL 1   // k_gmm_final sums the reverse partials itself (no k_gmm_reduce)
 #endif
@@ -101,8 +104,8 @@ __host__ __device__ constexpr int ltb_idx(int DP, int a, int b) {
 // ---------------------------------------------------------------------------
 // -N lse(alphas) with the Int argmax record, as in the program: par[k] =
 // its alphas.g share, par[K] = -N * lsa (one thread)
-// alphas' reversible logsumexp and its adjoint, whole block (block 0 of
-// k_gmm_prep); `sa` = K doubles of shared scratch.  The sums run in the
+// alphas' reversible logsumexp and its adjoint, whole block (the extra
+// block K of k_gmm_prep); `sa` = K doubles of shared scratch.  The sums run in the
 // reference's order on one thread; the exps and adjoints run in parallel.
 __device__ void gmm_alpha_lse(int K, long long N_total, const double *__restrict__ alphas,
                               double *__restrict__ par, double *sa) {
@@ -160,6 +163,12 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
     flags[i] = 0u;
   const int P = d * (d + 1) / 2;
   extern __shared__ __align__(16) double prep_dyn[];     // icf row (P), then K scratch
+#if GMM_ALPHA_BLOCK
+  if (k == K) {                  // the extra block: the alphas' reversible logsumexp,
+    if (par) gmm_alpha_lse(K, N_total, alphas, par, prep_dyn);  // beside the components
+    return;
+  }
+#endif
   double *ic = prep_dyn;
   {
     const double *icg = icf + (long long)k * P;          // one coalesced pass
@@ -192,7 +201,9 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
     for (int j = 0; j < d; j++) s = s + ic[j];           // sq[k] += icf[k, j] (in order)
     sq[k] = s;
   }
+#if !GMM_ALPHA_BLOCK
   if (k == 0 && par) gmm_alpha_lse(K, N_total, alphas, par, prep_dyn + P);
+#endif
   // qd and this component's share of the prior's Frobenius sum:
   // fro += abs2(qd![k, j]) (j <= d) or abs2(icf[k, j]) (j > d)
   double f = 0.0;
@@ -992,7 +1003,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
 #define GMM_ABLATE 0   // timing-only builds (tools/build_variants.sh): skip kernels by bit
 #endif
   if (!(GMM_ABLATE & 1))
-  k_gmm_prep<DP><<<K, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
+  k_gmm_prep<DP><<<K + GMM_ALPHA_BLOCK, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
                                              add_params ? par : nullptr, flags, N);
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
