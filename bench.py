@@ -461,6 +461,17 @@ def bessel_cpu(target_s=2.0, n_max=1 << 24):
                       f"checks (oracle/revoracle.c), {dt:.2f} s"}
 
 
+def gmm_traffic():
+    """Sum of the configs[2] GMM kernels' DRAM bytes per evaluation."""
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    v = [b for k, b in d.items() if k.startswith("k_gmm")]
+    return int(sum(v)) if v else None
+
+
 def load_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture at the
     bench's problem size (profiles/traffic.json, tools/make_traffic.py)."""
@@ -764,7 +775,9 @@ def run_gmm_ours(args, D):
         executed = 2.0 * 3 * N * K * P
         roof = {"bound": "fp64", "achieved": round(fl / (ms_step * 1e-3) / 1e12, 3),
                 "peak": round(peak, 3), "unit": "TFLOP/s",
-                "frac": round(fl / (ms_step * 1e-3) / 1e12 / peak, 4), "traffic": None,
+                "frac": round(fl / (ms_step * 1e-3) / 1e12 / peak, 4),
+                # DRAM bytes of one evaluation's kernels (ncu capture at configs[2] only)
+                "traffic": gmm_traffic() if args.workload == "gmm" else None,
                 "flops_per_eval_survey_W": fl,
                 "mat_vec_flops_executed": executed,
                 "executed_frac": round(executed / (ms_step * 1e-3) / 1e12 / peak, 4),

@@ -503,6 +503,91 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
   block_add_counters<LSE_THREADS>(0, nfail, counters);
 }
 
+// The same per-point routine with LSE_LANES lanes per point (K <= LSE_QK):
+// the exps are computed in parallel into shared memory (each exp is the
+// same value the reference computes twice), the order-dependent sums — se
+// forward, se -= ex and mx.g -= t.g in reverse — run on one lane in the
+// reference's order, so every value, code and the objective partials (64
+// points per block, the same tree) equal k_gmm_lse's bit for bit.
+constexpr int LSE_LANES = 4, LSE_QK = 96;
+__global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
+    int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
+    const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
+    uint8_t *__restrict__ fail, unsigned long long *counters) {
+  pdl_wait();
+
+  extern __shared__ double lse_ex[];                     // [LSE_THREADS][K]
+  const int q = threadIdx.x & (LSE_LANES - 1), pl = threadIdx.x / LSE_LANES;
+  const unsigned qmask = 0xFu << (threadIdx.x & 28);
+  const long long i = (long long)blockIdx.x * LSE_THREADS + pl;
+  double *ex = lse_ex + pl * K;
+  double e_pt = 0.0;
+  unsigned long long nfail = 0;
+  if (i < N) {                                           // uniform over the quad
+    const double *mt = mtT + i;
+    double *gmt = gmtT + i;
+#define MT(k) mt[(long long)(k) * N]
+#define GM(k) gmt[(long long)(k) * N]
+    int imx = 0;                                         // the argmax record (see k_gmm_lse)
+    double vmx = MT(0);
+    for (int k = 1; k < K; k++) {
+      const double v = MT(k);
+      if (v > vmx) {
+        imx = k;
+        vmx = v;
+      }
+    }
+    const double mx = 0.0 + vmx;
+    bool bad = false;
+    for (int k = q; k < K; k += LSE_LANES) {
+      const double t = 0.0 + (MT(k) - mx);
+      ex[k] = exp(t);
+      const double tr = t - (MT(k) - mx);                // the reverse sweep's t -> 0 check
+      bad = bad || fabs(tr) > tol;
+    }
+    __syncwarp(qmask);
+    double se = 0.0;
+    if (q == 0)
+      for (int k = 0; k < K; k++) se = se + ex[k];       // se += exp(t), in order
+    se = __shfl_sync(qmask, se, threadIdx.x & 28);
+    const double seg = 0.0 + (1.0 * 1.0) * (1.0 / se);
+    for (int k = q; k < K; k += LSE_LANES)
+      if (k != imx) GM(k) = 0.0 + (0.0 + seg * ex[k]);   // mt[k].g += t.g
+    bad = __any_sync(qmask, bad);
+    if (q == 0) {
+      int code = 0;
+      if (!(se > 0.0)) code = RL_ERR_DOMAIN;
+      e_pt = log(se) + mx;
+      double mxg = 0.0 + (1.0 * 1.0) * 1.0, tgi = 0.0;
+      for (int k = K - 1; k >= 0; k--) {
+        se = se - ex[k];
+        const double tg = 0.0 + seg * ex[k];
+        if (k == imx) tgi = tg;
+        mxg = mxg - tg;
+      }
+      if (chk && !code && bad) code = RL_ERR_DIRTY_ANCILLA;
+      if (chk && !code && fabs(se) > tol) code = RL_ERR_DIRTY_ANCILLA;
+      const double mxr = mx - MT(imx);
+      GM(imx) = (0.0 + tgi) + mxg;
+      if (chk && !code && fabs(mxr) > tol) code = RL_ERR_DIRTY_ANCILLA;
+      if (flagsA[i]) code = RL_ERR_DIRTY_ANCILLA;
+      fail[i] = (uint8_t)code;
+      nfail = code != 0;
+    }
+#undef MT
+#undef GM
+  }
+  __shared__ double red[LSE_THREADS];
+  if (q == 0) red[pl] = e_pt;
+  __syncthreads();
+  for (int o = LSE_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) err_part[blockIdx.x] = red[0];
+  block_add_counters<LSE_THREADS * LSE_LANES>(0, nfail, counters);
+}
+
 // ---------------------------------------------------------------------------
 // reverse: recompute Z (no tape), qxc.g = (-dmt/2)(2 Z); accumulate the
 // factor adjoint M = sum_i qxc.g_i xc_i^T (lower triangle, 16x8 DMMA tiles
@@ -1015,9 +1100,20 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
                          d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags)))
       return rc;
-    if (!(GMM_ABLATE & 2) && (rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st, K, N, mt,
-                         gmt, flags, tol, chk, errp, fail, counters)))
+#ifndef GMM_LSE_Q
+#define GMM_LSE_Q 1
+#endif
+    if (GMM_LSE_Q && K <= LSE_QK) {
+      if (!(GMM_ABLATE & 2) &&
+          (rc = launch_pdl("k_gmm_lse_q", k_gmm_lse_q, dim3(L.nerr),
+                           dim3(LSE_THREADS * LSE_LANES), (size_t)LSE_THREADS * K * 8, st, K, N,
+                           mt, gmt, flags, tol, chk, errp, fail, counters)))
+        return rc;
+    } else if (!(GMM_ABLATE & 2) &&
+               (rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st,
+                                K, N, mt, gmt, flags, tol, chk, errp, fail, counters))) {
       return rc;
+    }
     if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
                                          add_params, out, st);
     if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
