@@ -435,9 +435,14 @@ def bessel_e2e(torch, z, args, D, n_total):
     for _ in range(steps):
         kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.local)
     dt = D.max((time.perf_counter() - t0) / steps)
+    # per rank: z up; J and dJ/dz down, plus per 4 Mi-element chunk a count
+    # and a 16384-entry list of the nonzero status codes (capi.cu)
+    nch = -(-n // (1 << 22))
+    d2h = D.sum(16 * n + nch * (16384 * 4 + 4))
     return {"value": round(n_total / dt, 1), "unit": "grads/s", "h2d_bytes_per_step": 8 * n_total,
-            "d2h_bytes_per_step": 17 * n_total, "ms_per_step": round(dt * 1e3, 3),
-            "path": "rl_besselj_grad_f64_host (pinned host buffers, 3-stream pipeline)"}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 3),
+            "path": "rl_besselj_grad_f64_host (pinned host buffers, 3-stream pipeline; status "
+                    "codes as per-chunk lists of the failures)"}
 
 
 def bessel_cpu(target_s=2.0, n_max=1 << 24):

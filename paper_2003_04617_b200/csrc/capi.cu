@@ -176,6 +176,22 @@ struct Pipeline {
     for (int i = 0; i < NS; i++) st[i] = cache[device][i];
     return RL_OK;
   }
+  // pinned host scratch, cached per host thread (a D2H copy into pageable
+  // memory would block the host and serialise the chunk pipeline)
+  static int pinned(size_t bytes, void **out) {
+    static thread_local void *buf = nullptr;
+    static thread_local size_t have = 0;
+    if (bytes > have) {
+      if (buf) cudaFreeHost(buf);
+      buf = nullptr;
+      have = 0;
+      const int rc = cuda_status(cudaMallocHost(&buf, bytes), "cudaMallocHost");
+      if (rc) return rc;
+      have = bytes;
+    }
+    *out = buf;
+    return RL_OK;
+  }
   int finish() {
     int rc = RL_OK;
     for (auto &s : st)
@@ -229,6 +245,22 @@ int rl_besselj_grad_f64(int32_t nu, const double *z, int64_t n, double thr, doub
                         as_stream(stream));
 }
 
+// Per-chunk list of the nonzero status codes (index << 8 | code): almost every
+// element succeeds, so the host-buffer entry downloads this list instead of
+// one status byte per element.
+__global__ void k_compact_fail(const uint8_t *__restrict__ f, int64_t m,
+                               uint32_t *__restrict__ list, unsigned *__restrict__ count,
+                               unsigned cap) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t c = f[i];
+    if (c) {
+      const unsigned k = atomicAdd(count, 1u);
+      if (k < cap) list[k] = ((uint32_t)i << 8) | c;
+    }
+  }
+}
+
 int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
                              double seed, int64_t max_trips, int32_t invcheck, double *J,
                              double *dJdz, uint8_t *fail, unsigned long long *sum_trips,
@@ -242,39 +274,73 @@ int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr,
 #define BJ_HOST_CH_LOG2 22
 #endif
   const int64_t CH = int64_t(1) << BJ_HOST_CH_LOG2;  // elements per chunk (4 Mi = 32 MiB of z)
+  static_assert(BJ_HOST_CH_LOG2 <= 24, "chunk index must fit the 24-bit field of the fail list");
+  constexpr unsigned CAP = 16384;                    // listed failures per chunk
   const int64_t nch = (n + CH - 1) / CH;
   const int64_t bufn = std::min<int64_t>(CH, std::max<int64_t>(n, 1));
-  DevBuf dz[Pipeline::NS], dJ[Pipeline::NS], dg[Pipeline::NS], df[Pipeline::NS], dc;
+  DevBuf dz[Pipeline::NS], dJ[Pipeline::NS], dg[Pipeline::NS], df, dl, dc;
   for (int s = 0; s < Pipeline::NS && s < std::max<int64_t>(nch, 1); s++) {
     if ((rc = dz[s].alloc(bufn * 8, pl.st[s])) || (rc = dJ[s].alloc(bufn * 8, pl.st[s])) ||
-        (rc = dg[s].alloc(bufn * 8, pl.st[s])) || (rc = df[s].alloc(bufn, pl.st[s])))
+        (rc = dg[s].alloc(bufn * 8, pl.st[s])))
       return rc;
   }
-  if ((rc = dc.alloc(2 * sizeof(unsigned long long) * Pipeline::NS, pl.st[0]))) return rc;
+  // status bytes stay on the device for the whole batch (the overflow path
+  // reads them back); the lists and counts are per chunk
+  const int64_t nl = std::max<int64_t>(nch, 1);
+  if ((rc = df.alloc(std::max<int64_t>(n, 1), pl.st[0])) ||
+      (rc = dl.alloc(nl * CAP * 4, pl.st[0])) ||
+      (rc = dc.alloc(2 * sizeof(unsigned long long) * Pipeline::NS + nl * 4, pl.st[0])))
+    return rc;
   auto *cnt = (unsigned long long *)dc.p;
-  if ((rc = cuda_status(cudaMemsetAsync(cnt, 0, 2 * 8 * Pipeline::NS, pl.st[0]), "memset")))
+  auto *fcount = (unsigned *)(cnt + 2 * Pipeline::NS);
+  if ((rc = cuda_status(cudaMemsetAsync(dc.p, 0, 2 * 8 * Pipeline::NS + nl * 4, pl.st[0]),
+                        "memset")))
     return rc;
   if ((rc = pl.finish())) return rc;  // counters zeroed before any stream uses them
+  void *hp = nullptr;
+  if ((rc = Pipeline::pinned((size_t)nl * (CAP + 1) * 4, &hp))) return rc;
+  unsigned *hcount = (unsigned *)hp;
+  uint32_t *hlist = hcount + nl;
   for (int64_t c = 0; c < nch; c++) {
     const int s = (int)(c % Pipeline::NS);
     const int64_t off = c * CH, m = std::min(CH, n - off);
     cudaStream_t st = pl.st[s];
+    uint8_t *fc = (uint8_t *)df.p + off;
+    uint32_t *lc = (uint32_t *)dl.p + c * CAP;
     if ((rc = cuda_status(cudaMemcpyAsync(dz[s].p, z + off, m * 8, cudaMemcpyHostToDevice, st),
                           "H2D z")))
       return rc;
     if ((rc = launch_besselj(nu, (double *)dz[s].p, m, thr, tol, seed, max_trips, invcheck,
-                             (double *)dJ[s].p, (double *)dg[s].p, (uint8_t *)df[s].p,
-                             cnt + 2 * s, st)))
+                             (double *)dJ[s].p, (double *)dg[s].p, fc, cnt + 2 * s, st)))
       return rc;
-    if ((rc = cuda_status(cudaMemcpyAsync(J + off, dJ[s].p, m * 8, cudaMemcpyDeviceToHost, st),
+    k_compact_fail<<<(unsigned)std::min<int64_t>((m + 255) / 256, 4 * sm_count()), 256, 0, st>>>(
+        fc, m, lc, fcount + c, CAP);
+    if ((rc = cuda_status(cudaGetLastError(), "k_compact_fail")) ||
+        (rc = cuda_status(cudaMemcpyAsync(J + off, dJ[s].p, m * 8, cudaMemcpyDeviceToHost, st),
                           "D2H J")) ||
         (rc = cuda_status(cudaMemcpyAsync(dJdz + off, dg[s].p, m * 8, cudaMemcpyDeviceToHost, st),
                           "D2H dJdz")) ||
-        (rc = cuda_status(cudaMemcpyAsync(fail + off, df[s].p, m, cudaMemcpyDeviceToHost, st),
-                          "D2H fail")))
+        (rc = cuda_status(cudaMemcpyAsync(&hcount[c], fcount + c, 4, cudaMemcpyDeviceToHost, st),
+                          "D2H fail count")) ||
+        (rc = cuda_status(cudaMemcpyAsync(&hlist[(size_t)c * CAP], lc, CAP * 4,
+                                          cudaMemcpyDeviceToHost, st), "D2H fail list")))
       return rc;
   }
+  memset(fail, 0, (size_t)n);  // the host thread is idle while the copies run
   if ((rc = pl.finish())) return rc;
+  for (int64_t c = 0; c < nch; c++) {
+    const int64_t off = c * CH, m = std::min(CH, n - off);
+    if (hcount[c] > CAP) {       // more failures than the list holds: the whole chunk
+      if ((rc = cuda_status(cudaMemcpy(fail + off, (uint8_t *)df.p + off, m,
+                                       cudaMemcpyDeviceToHost), "D2H fail")))
+        return rc;
+      continue;
+    }
+    for (unsigned k = 0; k < hcount[c]; k++) {
+      const uint32_t e = hlist[(size_t)c * CAP + k];
+      fail[off + (e >> 8)] = (uint8_t)(e & 0xff);
+    }
+  }
   unsigned long long h[2 * Pipeline::NS];
   if ((rc = cuda_status(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost), "D2H counters")))
     return rc;

@@ -114,6 +114,26 @@ def test_host_entry_matches_device_entry(cuda):
     assert nfail == 0 and trips > 0
 
 
+@pytest.mark.parametrize("nbad", [37, 20000])
+def test_host_entry_failure_codes(cuda, nbad):
+    """The host entry downloads per-chunk lists of the nonzero status codes
+    (index, code) instead of one byte per element; more failures in a chunk
+    than the list holds (16384) fall back to the chunk's full status bytes.
+    Both paths equal the device entry's fail array."""
+    rng = np.random.default_rng(9)
+    n = (1 << 22) * 2 + 777
+    z = rng.uniform(0.1, 10.0, n)
+    bad = rng.choice(n, nbad, replace=False) if nbad < 100 else np.arange(5, 5 + nbad)
+    z[bad[::2]] = -1.0                                   # RevDomainError (log of z <= 0)
+    z[bad[1::2]] = 0.0
+    J, dz, fail, _ = run(z, 2, cuda)
+    Jh, dzh, fh, trips, nfail = rg.besselj_grad_host(z, 2)
+    assert np.array_equal(fail, fh) and nfail == int((fail != 0).sum()) == nbad
+    ok = fail == 0
+    assert np.array_equal(J[ok], Jh[ok]) and np.array_equal(dz[ok], dzh[ok])
+    assert np.isnan(Jh[~ok]).all()
+
+
 def test_large_batch_properties(cuda, oracle):
     """Full configs[1] size (2^26): every element restores (fail == 0), the
     trip total matches the oracle's on a strided sample scaled up, and a
