@@ -1033,10 +1033,10 @@ class _Emitter:
                 if a.name != b.name:
                     continue
                 if pres[i] is None or pres[j] is None:      # a whole cell / array
-                    self.w(f"if (!code) code = RC_ALIAS; goto {label};")
+                    self.w("if (!code) code = RC_ALIAS;")
                 elif len(pres[i]) == len(pres[j]):
                     same = " && ".join(f"{x} == {y}" for x, y in zip(pres[i], pres[j]))
-                    self.w(f"if ({same}) {{ code = RC_ALIAS; goto {label}; }}")
+                    self.w(f"if ({same} && !code) code = RC_ALIAS;")
 
     def view_ref(self, a, pre=None):
         """_Ref of an instruction operand; array offsets land in temps (the
@@ -1057,9 +1057,9 @@ class _Emitter:
         if a is None or b is None or a.root != b.root:
             return
         if a.off is None or b.off is None:
-            self.w(f"if (!code) code = RC_ALIAS; goto {label};")
+            self.w("if (!code) code = RC_ALIAS;")
         else:
-            self.w(f"if ({a.off} == {b.off}) {{ code = RC_ALIAS; goto {label}; }}")
+            self.w(f"if ({a.off} == {b.off} && !code) code = RC_ALIAS;")
 
     def infer_alloc(self, name, e):
         k = "u" if isinstance(e, Call) and e.f == "ulog" else self.expr_kind(e)
@@ -1118,7 +1118,10 @@ class _Emitter:
         return f"{prefix}{self.tmp}"
 
     def fail_check(self, label):
-        self.w(f"if (code) goto {label};")
+        """Errors do not jump: the first one is recorded in `code` (every
+        later write is guarded), loops stop on it and the element's results
+        are discarded — structured control flow keeps the warp reconverging
+        after every data-dependent loop and branch."""
 
     # expressions (conditions, bounds, allocation values) ---------------
     def expr(self, e):
@@ -1337,8 +1340,8 @@ class _Emitter:
                 raise UnsupportedProgram("codegen: @safe print has no device equivalent")
             for e in s.exprs:                 # interpreter.py:800-811
                 c = self.cond(e)
-                self.w(f"{{ const bool ok = {c}; if (code) goto {label};")
-                self.w(f"  if (!ok) {{ code = RC_ASSERT; goto {label}; }} }}")
+                self.w(f"{{ const bool ok = {c};")
+                self.w("  if (!ok && !code) code = RC_ASSERT; }")
         elif isinstance(s, Alloc):
             if s.name in self.shapes:
                 raise UnsupportedProgram(f"codegen: {s.name!r} shadows a parameter")
@@ -1357,12 +1360,12 @@ class _Emitter:
             val, vk = self.expr(s.e)
             self.fail_check(label)
             if k == "i":
-                self.w(f"if (chk && v_{_cid(s.name)} != ({val})) {{ code = RC_DIRTY; goto {label}; }}")
+                self.w(f"if (chk && v_{_cid(s.name)} != ({val}) && !code) code = RC_DIRTY;")
             else:
                 # _ancilla_residual: |cur - decl| > tol fails (NaN passes); ULog by exponent
                 d = self.new("d")
                 self.w(f"{{ const double {d} = fabs(rl_p(v_{_cid(s.name)} - R({val})));")
-                self.w(f"  if (chk && {d} > tol) {{ code = RC_DIRTY; goto {label}; }} }}")
+                self.w(f"  if (chk && {d} > tol && !code) code = RC_DIRTY; }}")
         elif isinstance(s, If):
             took = self.new("took")
             pre = self.cond(s.pre)
@@ -1379,24 +1382,22 @@ class _Emitter:
             self.w("  }")
             post = pre if s.post is SAME else self.cond(s.post)
             self.w(f"  if (chk) {{ const bool after = {post};")
-            self.w(f"    if (code) goto {label};")
-            self.w(f"    if (after != {took}) {{ code = RC_POST; goto {label}; }} }}")
+            self.w(f"    if (after != {took} && !code) code = RC_POST; }}")
             self.w("}")
         elif isinstance(s, While):
             pre, post = self.cond(s.pre), self.cond(s.post)
             self.w("{")
             self.depth += 1
-            self.w(f"if (chk) {{ const bool p0 = {post}; if (code) goto {label};")
-            self.w(f"  if (p0) {{ code = RC_POST; goto {label}; }} }}")
+            self.w(f"if (chk) {{ const bool p0 = {post};")
+            self.w("  if (p0 && !code) code = RC_POST; }")
             self.w("for (;;) {")
             self.depth += 1
-            self.w(f"const bool go = {pre};")
-            self.fail_check(label)
+            self.w(f"const bool go = ({pre}) && !code;")
             self.w("if (!go) break;")
-            self.w(f"if (++ticks > fuel) {{ code = RC_FUEL; goto {label}; }}")
+            self.w("if (++ticks > fuel) { if (!code) code = RC_FUEL; break; }")
             self.stmts(s.body, grad, label)
-            self.w(f"if (chk) {{ const bool p1 = {post}; if (code) goto {label};")
-            self.w(f"  if (!p1) {{ code = RC_POST; goto {label}; }} }}")
+            self.w(f"if (chk) {{ const bool p1 = {post};")
+            self.w("  if (!p1 && !code) code = RC_POST; }")
             self.depth -= 1
             self.w("}")
             self.depth -= 1
@@ -1412,19 +1413,19 @@ class _Emitter:
             b = self.int_expr(s.b, "loop stop")
             self.w(f"{{ const long long n1_{L} = {a}, n2_{L} = {st}, n3_{L} = {b};")
             self.fail_check(label)
-            self.w(f"  if (n2_{L} == 0) {{ code = RC_DOMAIN; goto {label}; }}")
-            self.w(f"  for (long long x_{L} = n1_{L}; n2_{L} > 0 ? x_{L} <= n3_{L} : x_{L} >= n3_{L};"
-                   f" x_{L} += n2_{L}) {{")
+            self.w(f"  if (n2_{L} == 0 && !code) code = RC_DOMAIN;")
+            self.w(f"  for (long long x_{L} = n1_{L}; !code && (n2_{L} > 0 ? x_{L} <= n3_{L} : "
+                   f"x_{L} >= n3_{L}); x_{L} += n2_{L}) {{")
             self.depth += 1
             self.kinds[s.var] = "i"
-            self.w(f"if (++ticks > fuel) {{ code = RC_FUEL; goto {label}; }}")
+            self.w("if (++ticks > fuel) { if (!code) code = RC_FUEL; break; }")
             self.w(f"v_{_cid(s.var)} = x_{L};")
             self.stmts(s.body, grad, label)
-            self.w(f"if (chk && v_{_cid(s.var)} != x_{L}) {{ code = RC_ITER; goto {label}; }}")
+            self.w(f"if (chk && v_{_cid(s.var)} != x_{L} && !code) code = RC_ITER;")
             self.depth -= 1
             self.w("  }")
             self.w(f"  if (chk && (({a}) != n1_{L} || ({st}) != n2_{L} || ({b}) != n3_{L})) "
-                   f"{{ code = RC_ITER; goto {label}; }}")
+                   f"{{ if (!code) code = RC_ITER; }}")
             self.w("}")
         else:
             raise UnsupportedProgram(f"codegen: unsupported statement {s!r}")
@@ -1463,7 +1464,7 @@ class _Emitter:
         if kind in ("INC", "DEC"):
             (a,) = refs
             if a.kind != "i":                          # _prim_plain: Int (or Fixed) only
-                self.w(f"if (!code) code = RC_KIND; goto {label};")
+                self.w("if (!code) code = RC_KIND;")
                 return
             self.w(f"{a.v} = {a.v} {'+' if kind == 'INC' else '-'} 1;")
             return
@@ -1536,7 +1537,6 @@ class _Emitter:
                 fv = self.apply_fn(s.fname, xs)
             fvv = self.new("fv")
             self.w(f"{{ const R {fvv} = {fv};")
-            self.w(f"  if (code) goto {label};")
             self.w(f"  {TV} = {TV} {'+' if s.op == '+=' else '-'} {fvv}; }}")
             if not grad:
                 return
@@ -1560,10 +1560,10 @@ class _Emitter:
                         tag, pv, x0 = p
                         cond = (f"(double)R({x0}) == 0.0" if tag == "ABS"
                                 else f"!((double)R({x0}) > 0.0)")
-                        self.w(f"  if ({cond}) {{ if (!code) code = RC_DOMAIN; goto {label}; }}")
+                        self.w(f"  if (({cond}) && !code) code = RC_DOMAIN;")
                         p = pv
                     self.w(f"  {r.g} = {r.g} + {sg} * {p};")
-            self.w(f"  if (code) goto {label}; }}")
+            self.w("}")
             return
         # *= and /= : the target is a logarithmic number
         if tk != "u":
@@ -1581,7 +1581,6 @@ class _Emitter:
             contrib = f"g_log({self.apply_fn(s.fname, [self.atom_real(a, r) for a, r in zip(args, refs)])}, code)"
         cv = self.new("c")
         self.w(f"{{ const R {cv} = {contrib};")
-        self.w(f"  if (code) goto {label};")
         self.w(f"  {TV} = {TV} {'+' if s.op == '*=' else '-'} {cv}; }}")
         if not grad:
             return
@@ -1708,8 +1707,15 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
          " double tol, int chk, long long fuel, double *__restrict__ fout,"
          " double *__restrict__ gout, unsigned char *__restrict__ fail, int dir,"
          " double *__restrict__ hout, long long *__restrict__ iout) {",
-         "  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;"
-         " i += (long long)gridDim.x * blockDim.x) {",
+         # the element loop is uniform over the warp and reconverges at every
+         # element: lanes whose loops end early wait for the rest of the warp
+         # instead of drifting onto their next element (a diverged warp ran
+         # ~3 of 32 lanes per instruction)
+         "  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;"
+         " base += (long long)gridDim.x * blockDim.x) {",
+         "    __syncwarp();",
+         "    const long long i = base + threadIdx.x;",
+         "    if (i >= n) continue;",
          "    int code = 0;", "    long long ticks = 0;"]
     # columns: leaf b of every element at fin[b * n + i] (coalesced across the batch)
     for p in floats:
@@ -1753,7 +1759,6 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     L.append("    // ---- " + ("uncall_function (~f)" if mode == "uncall" else
                                 "run_function (plain forward)") + " ----")
     L += em_f.lines
-    L.append("  fwd_done:")
     L.append("    if (code) {")
     L.append(f"      for (int e = 0; e < {NL}; ++e) {{ fout[e * n + i] = NAN;"
              + ("" if plain else " gout[e * n + i] = NAN;")
@@ -1776,7 +1781,6 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);")
     L.append("    ticks = 0;")
     L += em_g.lines
-    L.append("  grad_done:")
     L.append("    if (!code) {      // the backward pass must restore every argument")
     L += ["  " + x for x in each_leaf(
         lambda col, v, g: f"if (!(fabs(rl_p({v}) - fin[{col} * n + i]) <= tol)) code = RC_REV;")]
