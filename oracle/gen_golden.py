@@ -253,6 +253,7 @@ def gen_codegen():
         "sink": (["out!", "x", "y"], {"n": 3}, 64),
         "wloop": (["acc!", "x"], {"n": 5}, 48),
         "prims": (["a!", "b!", "c!", "th"], {"n!": 3}, 40),
+        "loose": (["y!", "x"], {}, 24),
     }
     out = {}
     for fn, (floats, ints, n) in cases.items():

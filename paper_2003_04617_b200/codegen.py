@@ -73,7 +73,7 @@ def _tokenize(src):
             while j < n and (src[j].isalnum() or src[j] == "_"):
                 j += 1
             word = src[i:j]
-            if word not in ("@routine", "~@routine", "@safe"):
+            if word not in ("@routine", "~@routine", "@safe", "@invcheckoff"):
                 raise UnsupportedProgram(f"codegen: macro {word!r} is not supported")
             toks.append(("macro", word))
             i = j
@@ -142,6 +142,13 @@ class Var:
 class IView:
     name: str
     idx: tuple             # Int index expressions (1-based)
+
+
+@dataclass(frozen=True)
+class NoCheck:
+    """@invcheckoff stmt: the statement (and every call it makes) runs with
+    the reversibility checks off (interpreter.py InvCheckOff, _checking)."""
+    body: tuple
 
 
 @dataclass(frozen=True)
@@ -323,6 +330,10 @@ class _Parser:
         if self.at("macro", "~@routine"):
             self.adv()
             return REnd()
+        if self.at("macro", "@invcheckoff"):
+            self.adv()
+            inner = self.stmt()
+            return NoCheck(inner if isinstance(inner, tuple) else (inner,))
         if self.at("macro", "@safe"):
             self.adv()
             kind = self.name()
@@ -566,6 +577,8 @@ def _invert(s):
         return While(s.post, s.pre, _invert_list(s.body))
     if isinstance(s, For):
         return For(s.var, s.b, _neg_expr(s.s), s.a, _invert_list(s.body))
+    if isinstance(s, NoCheck):         # reverser.py: InvCheckOff(invert_statement(stmt))
+        return NoCheck(_invert_list(s.body))
     if isinstance(s, Safe):
         return s                       # irreversible external statement: re-executed as is
     if isinstance(s, PCall):           # reverser.py:96-103
@@ -617,6 +630,8 @@ def _expand(stmts):
             out.append(While(s.pre, s.post, _expand(s.body)))
         elif isinstance(s, For):
             out.append(For(s.var, s.a, s.s, s.b, _expand(s.body)))
+        elif isinstance(s, NoCheck):
+            out.append(NoCheck(_expand(s.body)))
         elif isinstance(s, tuple):
             out.extend(_expand(s))
         else:
@@ -661,7 +676,7 @@ def _balanced(stmts, fname):
             cnt[s.name] = cnt.get(s.name, 0) + 1
         elif isinstance(s, Dealloc):
             cnt[s.name] = cnt.get(s.name, 0) - 1
-        elif isinstance(s, (For, While)):
+        elif isinstance(s, (For, While, NoCheck)):
             _balanced(s.body, fname)
         elif isinstance(s, If):
             _balanced(s.then, fname)
@@ -687,6 +702,8 @@ class _Inliner:
                 out.append(While(s.pre, s.post, self.run(s.body, stack)))
             elif isinstance(s, If):
                 out.append(If(s.pre, s.post, self.run(s.then, stack), self.run(s.els, stack)))
+            elif isinstance(s, NoCheck):
+                out.append(NoCheck(self.run(s.body, stack)))
             else:
                 out.append(s)
         return tuple(out)
@@ -711,7 +728,7 @@ class _Inliner:
                     return True
                 if isinstance(st, If) and (touched(st.then) or touched(st.els)):
                     return True
-                if isinstance(st, RBegin) and touched(st.body):
+                if isinstance(st, (RBegin, NoCheck)) and touched(st.body):
                     return True
                 if isinstance(st, tuple) and touched(st):
                     return True
@@ -806,6 +823,8 @@ class _Subst:
                       self.stmts(s.then), self.stmts(s.els))
         if isinstance(s, Safe):
             return Safe(s.kind, tuple(self.e(x) for x in s.exprs))
+        if isinstance(s, NoCheck):
+            return NoCheck(self.stmts(s.body))
         if isinstance(s, PCall):
             return PCall(s.f, tuple(self.view(a) for a in s.args), s.uncall)
         raise UnsupportedProgram(f"codegen: cannot inline {s!r}")
@@ -1311,6 +1330,13 @@ class _Emitter:
     def stmt(self, s, grad, label):
         if isinstance(s, Instr):
             self.instr(s, grad, label)
+        elif isinstance(s, NoCheck):
+            n = self.new("chk")
+            self.w(f"{{ const int {n} = chk; chk = 0;")
+            self.depth += 1
+            self.stmts(s.body, grad, label)
+            self.depth -= 1
+            self.w(f"  chk = {n}; }}")
         elif isinstance(s, ArgCheck):
             self.w("{")
             self.depth += 1
@@ -1611,6 +1637,8 @@ def _collect_vars(stmts, acc):
         elif isinstance(s, If):
             _collect_vars(s.then, acc)
             _collect_vars(s.els, acc)
+        elif isinstance(s, NoCheck):
+            _collect_vars(s.body, acc)
     return acc
 
 
