@@ -176,6 +176,32 @@ struct Pipeline {
     for (int i = 0; i < NS; i++) st[i] = cache[device][i];
     return RL_OK;
   }
+  // device scratch, cached per (host thread, device): a host-buffer call
+  // carves its buffers out of it instead of allocating and freeing each one
+  struct Arena {
+    void *buf[MAX_DEV] = {};
+    size_t have[MAX_DEV] = {};
+    ~Arena() {                   // thread exit: give the device memory back
+      for (int dv = 0; dv < MAX_DEV; dv++)
+        if (buf[dv]) {
+          cudaSetDevice(dv);
+          cudaFree(buf[dv]);
+        }
+    }
+  };
+  static int arena(int device, size_t bytes, void **out) {
+    static thread_local Arena a;
+    if (bytes > a.have[device]) {
+      if (a.buf[device]) cudaFree(a.buf[device]);
+      a.buf[device] = nullptr;
+      a.have[device] = 0;
+      const int rc = cuda_status(cudaMalloc(&a.buf[device], bytes), "cudaMalloc arena");
+      if (rc) return rc;
+      a.have[device] = bytes;
+    }
+    *out = a.buf[device];
+    return RL_OK;
+  }
   // pinned host scratch, cached per host thread (a D2H copy into pageable
   // memory would block the host and serialise the chunk pipeline)
   static int pinned(size_t bytes, void **out) {
@@ -591,12 +617,32 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
   const size_t P = (size_t)d * (d + 1) / 2;
   const size_t nout = 1 + K + (size_t)K * d + (size_t)K * P;
   const size_t wsb = gmm_workspace_bytes(d, K, N);
+#ifndef GMM_HOST_ARENA
+#define GMM_HOST_ARENA 1
+#endif
+#if !GMM_HOST_ARENA
   DevBuf da, dm, di, dx, dout, dfl, dws, dc;
   if ((rc = da.alloc(K * 8, st)) || (rc = dm.alloc((size_t)K * d * 8, st)) ||
       (rc = di.alloc((size_t)K * P * 8, st)) || (rc = dx.alloc((size_t)N * d * 8, st)) ||
       (rc = dout.alloc(nout * 8, st)) || (rc = dfl.alloc(N, st)) || (rc = dws.alloc(wsb, st)) ||
       (rc = dc.alloc(16, st)))
     return rc;
+#else
+  // one cached device arena per (thread, device), carved 256-byte aligned
+  const size_t sizes[8] = {(size_t)K * 8, (size_t)K * d * 8, (size_t)K * P * 8,
+                           (size_t)N * d * 8, nout * 8, (size_t)std::max<int64_t>(N, 1), wsb, 16};
+  size_t total = 0;
+  for (size_t b : sizes) total += (b + 255) & ~size_t(255);
+  void *base = nullptr;
+  if ((rc = Pipeline::arena(device, total, &base))) return rc;
+  struct Piece { void *p; } da, dm, di, dx, dout, dfl, dws, dc;
+  Piece *pieces[8] = {&da, &dm, &di, &dx, &dout, &dfl, &dws, &dc};
+  size_t off = 0;
+  for (int q = 0; q < 8; q++) {
+    pieces[q]->p = (char *)base + off;
+    off += (sizes[q] + 255) & ~size_t(255);
+  }
+#endif
   if ((rc = cuda_status(cudaMemcpyAsync(da.p, alphas, K * 8, cudaMemcpyHostToDevice, st), "H2D")) ||
       (rc = cuda_status(cudaMemcpyAsync(dm.p, means, (size_t)K * d * 8, cudaMemcpyHostToDevice, st),
                         "H2D")) ||
