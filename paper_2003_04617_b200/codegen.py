@@ -840,6 +840,7 @@ _PRELUDE = r"""
 #include <math.h>
 #include <stdint.h>
 #include <cuda_runtime.h>
+#include "fexp.cuh"
 #define RC_POST 1
 #define RC_DIRTY 2
 #define RC_DOMAIN 3
@@ -860,10 +861,20 @@ __device__ __forceinline__ double g_log(double x, int &c) {
   if (!(x > 0.0)) { if (!c) c = RC_DOMAIN; return 0.0; }
   return log(x);
 }
+// exp: the series kernels' table exp (csrc/fexp.cuh: 0.5 ulp + O(2^-60), equal
+// to the host libm's in ~99.9% of calls) inside (-708, 708), libdevice outside
+__device__ rl::Exp2Tab rl_exp2tab[1024] = RL_EXP2_TABLE_INIT_1024;
+__constant__ rl::ExpConsts1024 rl_expk = RL_EXP_CONSTS_1024_INIT;
 __device__ __forceinline__ double g_exp(double x, int &c) {
-  const double r = exp(x);
+  const double r = fabs(x) < 708.0 ? rl::fexp1024(x, rl::Exp2TabFn{rl_exp2tab}, rl_expk) : exp(x);
   if (isinf(r) && isfinite(x)) { if (!c) c = RC_OVERFLOW; }
   return r;
+}
+// log of an Int: CPython's math.log(i) for 1 <= i < 4096 from the host table
+// `logtab` (a kernel argument), libdevice beyond
+__device__ __forceinline__ double g_logi(long long k, const double *lt, int &c) {
+  if (k >= 1 && k < 4096) return lt[k];
+  return g_log((double)k, c);
 }
 // CPython float ** float (s_pow, values.py:408-421): x ** 0 and 1 ** y are 1.0,
 // 0 ** negative raises, a finite result that overflows raises OverflowError;
@@ -1187,6 +1198,8 @@ class _Emitter:
             if f == "ulog":
                 (a, _), = args
                 return f"g_log(R({a}), code)", "u"
+            if f == "log" and args[0][1] == "i":
+                return f"R(g_logi({args[0][0]}, logtab, code))", "f"
             if f in ("sqrt", "exp", "log"):
                 (a, _), = args
                 return f"g_{f}(R({a}), code)", "f"
@@ -1599,6 +1612,8 @@ class _Emitter:
             r = refs[0]
             if r is not None and r.kind == "u":
                 contrib = r.v
+            elif r is not None and r.kind == "i":
+                contrib = f"R(g_logi({r.v}, logtab, code))"
             else:
                 contrib = f"g_log({self.atom_real(a, r)}, code)"
         else:
@@ -1668,13 +1683,14 @@ _LAUNCH = r"""
 extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, const double *seeds,
                           double tol, int chk, long long fuel, double *fout, double *gout,
                           unsigned char *fail, int dir, double *hout, long long *iout,
-                          void *stream) {
+                          const double *logtab, void *stream) {
   if (n <= 0) return 0;
   const int block = 128;
   long long grid = (n + block - 1) / block;
   if (grid > 148 * 16) grid = 148 * 16;
   rlg_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(n, fin, iin, seeds, tol, chk, fuel,
-                                                                fout, gout, fail, dir, hout, iout);
+                                                                fout, gout, fail, dir, hout, iout,
+                                                                logtab);
   return (int)cudaGetLastError();
 }
 """
@@ -1734,7 +1750,8 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
          " const long long *__restrict__ iin, const double *__restrict__ seeds,"
          " double tol, int chk, long long fuel, double *__restrict__ fout,"
          " double *__restrict__ gout, unsigned char *__restrict__ fail, int dir,"
-         " double *__restrict__ hout, long long *__restrict__ iout) {",
+         " double *__restrict__ hout, long long *__restrict__ iout,"
+         " const double *__restrict__ logtab) {",
          # the element loop is uniform over the warp and reconverges at every
          # element: lanes whose loops end early wait for the rest of the warp
          # instead of drifting onto their next element (a diverged warp ran
@@ -1835,6 +1852,30 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
 # build + run
 # ---------------------------------------------------------------------------
 
+_CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
+_LOGTABS = {}
+
+
+def _logtab(dev):
+    """CPython's math.log(i), i < 4096 (index 0: -inf), on `dev`: the integer
+    logs of generated kernels are the reference's bit for bit."""
+    key = str(dev)
+    if key not in _LOGTABS:
+        v = [-math.inf] + [math.log(i) for i in range(1, 4096)]
+        _LOGTABS[key] = torch.tensor(v, dtype=torch.float64, device=dev)
+    return _LOGTABS[key]
+
+
+def _include_tag():
+    """Hash of the csrc headers generated kernels include (part of the
+    cached library's key)."""
+    h = hashlib.sha256()
+    for f in ("fexp.cuh", "exp2tab_1024.inc", "exp2tab_256.inc"):
+        with open(os.path.join(_CSRC, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _cache_dir():
     # in-tree by default (next to librevgpu.so), so generated kernels load from
     # the repository like the hand-written ones; $REVGPU_CODEGEN_CACHE overrides
@@ -1855,7 +1896,7 @@ def _nvcc():
 
 def build(source):
     """Compile generated CUDA source to a cached shared library (sm_100a)."""
-    h = hashlib.sha256(source.encode()).hexdigest()[:20]
+    h = hashlib.sha256((source + _include_tag()).encode()).hexdigest()[:20]
     so = os.path.join(_cache_dir(), f"rlg_{h}.so")
     if not os.path.exists(so):
         with tempfile.TemporaryDirectory() as td:
@@ -1864,7 +1905,7 @@ def build(source):
                 fh.write(source)
             tmp = os.path.join(td, "k.so")
             cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-fmad=false",
-                   "-shared", "-Xcompiler", "-fPIC", "-o", tmp, cu]
+                   "-I", _CSRC, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, cu]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise NativeLibraryError("codegen: nvcc failed:\n" + r.stderr[-4000:])
@@ -1903,7 +1944,7 @@ class CompiledFunction:
         lib.rlg_launch.restype = ctypes.c_int
         lib.rlg_launch.argtypes = [ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
             ctypes.c_double, ctypes.c_int, ctypes.c_longlong] + [ctypes.c_void_p] * 3 + [
-            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         return lib
 
     def _lib_for(self, mode):
@@ -2023,7 +2064,7 @@ class CompiledFunction:
                             int(bool(invcheck)), int(max_steps), fout.data_ptr(), gout.data_ptr(),
                             fail.data_ptr(), int(dir_),
                             hout.data_ptr() if hout is not None else None, iout.data_ptr(),
-                            torch.cuda.current_stream().cuda_stream)
+                            _logtab(dev).data_ptr(), torch.cuda.current_stream().cuda_stream)
         if rc:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
         primal, grads, b = {}, {}, 0
