@@ -458,10 +458,116 @@ def gen_codegen_nbody():
     print("nbody goldens:", np.array(G).shape)
 
 
+def random_program(rng, name):
+    """A random reversible function over Float cells y!, a, b, c and an Int n
+    (this repository's generator, for differential testing of codegen.py):
+    instructions with distinct operands, counted loops, branches whose
+    condition the branch does not touch, ancilla blocks, SWAP / ROT."""
+    cells = ["y!", "a", "b", "c"]
+    fns1 = ["identity", "neg", "abs2", "sin", "cos", "sqrt", "exp"]
+    fns2 = ["+", "-", "*", "/"]
+    lines = []
+
+    def instr(ind, avoid=()):
+        tgt = rng.choice([x for x in cells if x not in avoid])
+        op = rng.choice(["+=", "-="])
+        others = [x for x in cells if x != tgt]
+        if rng.random() < 0.5:
+            f = rng.choice(fns1)
+            x = rng.choice(others)
+            return f"{ind}{tgt} {op} {x}" if f == "identity" else (
+                f"{ind}{tgt} {op} -{x}" if f == "neg" else f"{ind}{tgt} {op} {f}({x})")
+        f = rng.choice(fns2)
+        x, z = rng.choice(others, 2, replace=False)
+        if rng.random() < 0.3:
+            z = repr(float(np.round(rng.uniform(0.5, 2.0), 3)))
+        return f"{ind}{tgt} {op} {x} {f} {z}"
+
+    for k in range(int(rng.integers(3, 7))):
+        r = rng.random()
+        if r < 0.45:
+            lines.append(instr("    "))
+        elif r < 0.6:
+            lines += ["    for i = 1:1:n", instr("        "), "    end"]
+        elif r < 0.72:
+            x, z = rng.choice(cells, 2, replace=False)
+            lines += [f"    if ({x} > {z}, ~)", instr("        ", (x, z)), "    else",
+                      instr("        ", (x, z)), "    end"]
+        elif r < 0.86:
+            x = rng.choice(cells)
+            t = f"t{k}"
+            f = rng.choice(["sin", "cos", "abs2"])
+            lines += [f"    {t} <- 0.0", f"    {t} += {f}({x})",
+                      f"    {rng.choice([c for c in cells if c != x])} += {t}",
+                      f"    {t} -= {f}({x})", f"    {t} -> 0.0"]
+        elif r < 0.93:
+            x, z = rng.choice(cells, 2, replace=False)
+            lines.append(f"    SWAP({x}, {z})")
+        else:
+            x, z, w = rng.choice(cells, 3, replace=False)
+            lines.append(f"    ROT({x}, {z}, {w})")
+    return f"fn {name}(y!, a, b, c, n)\n" + "\n".join(lines) + "\nend\n"
+
+
+def random_program_ulog(rng, name):
+    """random_program's constructs plus log-domain ancilla blocks (ulog,
+    *= / /= convert, += convert) and counted while loops over an Int ancilla."""
+    base = random_program(rng, name).splitlines()[1:-1]
+    cells = ["y!", "a", "b", "c"]
+    extra = []
+    for k in range(int(rng.integers(1, 3))):
+        x, z = rng.choice(cells, 2, replace=False)
+        l = f"l{k}"
+        if rng.random() < 0.5:
+            extra += [f"    {l} <- ulog(1.0)", f"    {l} *= convert({x})",
+                      f"    {z} += convert({l})", f"    {l} /= convert({x})",
+                      f"    {l} -> ulog(1.0)"]
+        else:
+            j = f"j{k}"
+            w = rng.choice([c for c in cells if c != z])
+            extra += [f"    {j} <- 0", f"    while ({j} < n, {j} > 0)", f"        {j} += 1",
+                      f"        {z} += {w} * 0.5", "    end", f"    {j} -> n"]
+    cut = int(rng.integers(0, len(base) + 1))
+    body = base[:cut] + extra + base[cut:]
+    return f"fn {name}(y!, a, b, c, n)\n" + "\n".join(body) + "\nend\n"
+
+
+def gen_codegen_random():
+    """reference gradient() of 80 random programs (40 random_program, 40
+    random_program_ulog) on 6 random inputs each: primal outputs,
+    cotangents and error classes."""
+    rng = np.random.default_rng(2024)
+    texts, X, P, G, E = [], [], [], [], []
+    for q in range(80):
+        name = f"r{q}"
+        text = random_program(rng, name) if q < 40 else random_program_ulog(rng, name)
+        prog = parse_program(text)
+        xs = rng.uniform(-2.0, 2.0, (6, 4))
+        ns = rng.integers(1, 4, 6)
+        for row, n in zip(xs, ns):
+            args = [float(v) for v in row] + [int(n)]
+            r, en = _err_name(lambda: gradient(prog, GradRequest(name, args)))
+            p = g = [np.nan] * 4
+            if r is not None:
+                prim, grads = r
+                p = [float(v) for v in prim[:4]]
+                g = [float(grads[c]) for c in ("y!", "a", "b", "c")]
+            P.append(p)
+            G.append(g)
+            E.append(en)
+            X.append(list(row) + [int(n)])
+        texts.append(text)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_random.npz"), texts=np.array(texts),
+                        x=np.array(X), primal=np.array(P), grad=np.array(G), err=np.array(E))
+    from collections import Counter
+    print("random programs:", len(texts), Counter(E))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
-                              "codegen_dropin", "codegen_nbody"]
+                              "codegen_dropin", "codegen_nbody",
+                              "codegen_random"]
     for w in which:
         globals()["gen_" + w]()
