@@ -301,9 +301,20 @@ def gradient(program, req, opts=None):
     return _HANDLERS[fdef.kernel.handler](fdef, req, opts)
 
 
+def _int_array(v):
+    """An Array-like holding Int values only (gradient-free, leaf_paths lists none)."""
+    data = getattr(v, "data", None)
+    if isinstance(v, np.ndarray):
+        return v.dtype.kind in "iu"
+    if isinstance(v, torch.Tensor):
+        return not v.is_floating_point()
+    return data is not None and not isinstance(data, memoryview) and len(list(data)) > 0 and \
+        all(_is_int(x) for x in data)
+
+
 def _leaves(v):
     """Number of differentiable leaves (None for Int)."""
-    if _is_int(v) or isinstance(v, bool):
+    if _is_int(v) or isinstance(v, bool) or _int_array(v):
         return 0
     if _is_float(v):
         return 1
@@ -311,7 +322,7 @@ def _leaves(v):
 
 
 def _flat(g, v):
-    if _is_int(v) or isinstance(v, bool):
+    if _is_int(v) or isinstance(v, bool) or _int_array(v):
         return []
     if g is None:
         return [0.0] * _leaves(v)
@@ -324,9 +335,26 @@ def jacobian(program, fname, args, opts=None):
     """Reference `jacobian` (autodiff.py:197-213): one gradient per
     differentiable leaf of every argument; rows x columns over all leaves."""
     opts = _check_opts(opts)
-    _, fdef, reg = _lookup(program, fname)
+    prog, fdef, reg = _lookup(program, fname)
     if reg and fdef.kernel.handler == "gmm":
-        raise KindError("the full gmm jacobian (over x and scratch) is not produced on device")
+        # the hand-written gmm kernel differentiates alphas / means / icf only:
+        # the full jacobian (over x and the scratch) comes from the generic path
+        from . import generic
+        names = fdef.param_names()
+        rows = []
+        for pi, pname in enumerate(names):
+            v = args[pi]
+            for li in range(_leaves(v)):
+                path = () if _is_float(v) else \
+                    (("idx", tuple(int(i) + 1 for i in
+                                   np.unravel_index(li, to_numpy(v, pname).shape))),)
+                _, grads = generic.gradient(prog, fdef, GradRequest(
+                    fname, args, seeds=[(pname, path, 1.0)]), opts)
+                row = []
+                for pj, nj in enumerate(names):
+                    row += _flat(grads.get(nj), args[pj])
+                rows.append(row)
+        return np.array(rows, dtype=float)
     names = fdef.param_names()
     rows = []
     for pi, pname in enumerate(names):
@@ -414,18 +442,16 @@ def hessian(program, fname, args, opts=None):
     device for besselj: the Float leaves are out! and z (nu is an Int), the
     only nonzero entry is H[z, z] = d2J/dz2 from rl_besselj_hess_f64, which
     runs the gradient sweeps over Dual numbers exactly as the reference does.
-    Functions without a hand-written kernel run codegen's Dual-number
-    kernel (one launch per Float leaf); the registered ba / gmm programs'
-    Hessians are not produced on device (UnsupportedProgram)."""
+    Every other function — the registered ba / gmm ones included — runs
+    codegen's Dual-number kernel (one launch per Float leaf)."""
     opts = _check_opts(opts)
     prog, fdef, reg = _lookup(program, fname)
-    if not reg:
+    if not reg or fdef.kernel.handler != "besselj":
+        # besselj has a hand-written Hessian kernel; every other function
+        # (the registered ba / gmm ones included) runs codegen's Dual kernel
         from . import generic
         H = generic.hessian(prog, fdef, list(args), opts)
         return HessianResult(H, float(np.max(np.abs(H - H.T))) if H.size else 0.0)
-    if fdef.kernel.handler != "besselj":
-        raise UnsupportedProgram(
-            f"hessian of {fname!r}: only besselj has a device Hessian kernel")
     if len(args) != 3:
         raise KindError(f"besselj takes 3 arguments, got {len(args)}")
     out0, nu, z = args

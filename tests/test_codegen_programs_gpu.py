@@ -168,3 +168,31 @@ def test_random_programs_against_the_reference(cuda, golden):
             got_g = [grads[c][0].item() for c in ("y!", "a", "b", "c")]
             assert close(got_p, P[r], 1e-12, 1e-14).all(), (q, r, text)
             assert close(got_g, G[r], 1e-12, 1e-14).all(), (q, r, text)
+
+
+def test_registered_programs_full_jacobian_and_hessian(cuda, golden):
+    """The drop-in jacobian / hessian of the registered gmm and ba_proj
+    functions: their hand-written kernels do not produce these, the generic
+    compiler does (reference hessian() goldens: codegen_programs.npz)."""
+    import paper_2003_04617_b200 as rg
+    G = golden("gmm")
+    pre = "c5_"
+    d, K, N, m = (int(v) for v in G[pre + "dims"])
+    A = lambda a: rg.Array.matrix(a.tolist()) if a.ndim == 2 else rg.Array.vector(a.tolist())  # noqa
+    Z = lambda *s: A(np.zeros(s))  # noqa: E731
+    args = [0.0, A(G[pre + "alphas"]), A(G[pre + "means"]), A(G[pre + "icf"]), A(G[pre + "x"]),
+            Z(K, d), Z(K), Z(d), Z(d), Z(K), rg.Array.vector([0] * K), float(G[pre + "gamma"]), m,
+            float(G[pre + "cst"])]
+    p = rg.load_example("gmm")
+    res = rg.hessian(p, "gmm", args)
+    assert close(res.matrix, golden("codegen_programs")["gmm_c5_hess"], 1e-10, 1e-12).all()
+    J = rg.jacobian(p, "gmm", args)
+    assert J.shape == (27, 27)
+    # row 0 (seed err!) restricted to alphas / means / icf is the gradient
+    assert close(J[0, 1:1 + K], G[pre + "g_alphas"], 1e-10, 1e-12).all()
+    B = golden("ba")
+    o = 0
+    bargs = [0.0, 0.0, rg.Array.vector(B["cams"][o].tolist()), rg.Array.vector(B["X"][o].tolist()),
+             float(B["w"][o]), float(B["feat"][o, 0]), float(B["feat"][o, 1])]
+    res = rg.hessian(rg.load_example("ba_proj"), "ba_proj", bargs)
+    assert close(res.matrix, golden("codegen_programs")["ba_hess"][o], 1e-9, 1e-11).all()
