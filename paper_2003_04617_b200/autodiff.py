@@ -503,11 +503,14 @@ def gradient_batch(program, fname, inputs, seeds=None, wrt=None, opts=None, retu
     grads: dict, restored: BoolTensor); no per-row exception is raised —
     restored[i] is False where row i's reference call would raise, and with
     `return_codes` a 4th value carries the revlang error code per row
-    (errors.CODE_NAMES).  besselj, ba_proj and ba_weight; gmm is one
-    evaluation over all points (use gradient / gmm_grad)."""
+    (errors.CODE_NAMES).  besselj, ba_proj and ba_weight run their
+    hand-written kernels; gmm (a batch of independent problems, one per row)
+    and every other function run the generic compiler's kernel."""
     opts = _check_opts(opts)
     prog, fdef, reg = _lookup(program, fname)
-    if not reg:
+    if not reg or fdef.kernel.handler == "gmm":
+        # gmm's hand-written kernel is ONE evaluation over all points: a batch
+        # of independent (small) gmm problems runs the generic kernel
         from . import generic
         primal, grads, fail = generic.gradient_batch(prog, fdef, inputs, seeds, wrt, opts)
         code = fail.to(torch.int32)

@@ -196,3 +196,29 @@ def test_registered_programs_full_jacobian_and_hessian(cuda, golden):
              float(B["w"][o]), float(B["feat"][o, 0]), float(B["feat"][o, 1])]
     res = rg.hessian(rg.load_example("ba_proj"), "ba_proj", bargs)
     assert close(res.matrix, golden("codegen_programs")["ba_hess"][o], 1e-9, 1e-11).all()
+
+
+def test_gradient_batch_of_gmm_problems(cuda, golden):
+    """gradient_batch on the registered gmm: a batch of independent problems
+    (here the reference case c0, twice, with x perturbed in the second row)
+    through the generic kernel; row 0 equals the reference's gradient()."""
+    import paper_2003_04617_b200 as rg
+    G = golden("gmm")
+    pre = "c0_"
+    d, K, N, m = (int(v) for v in G[pre + "dims"])
+    P = d * (d + 1) // 2
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=cuda)  # noqa: E731
+    x2 = np.stack([G[pre + "x"], G[pre + "x"] * 0.9])
+    inputs = {"err!": t(np.zeros(2)), "alphas": G[pre + "alphas"], "means": G[pre + "means"],
+              "icf": G[pre + "icf"], "x": t(x2), "qd!": np.zeros((K, d)), "sq!": np.zeros(K),
+              "xc!": np.zeros(d), "qxc!": np.zeros(d), "mt!": np.zeros(K),
+              "dm!": np.zeros(K, np.int64), "ga": float(G[pre + "gamma"]), "wm": m,
+              "cst": float(G[pre + "cst"])}
+    primal, grads, restored = rg.gradient_batch(rg.load_example("gmm"), "gmm", inputs,
+                                                wrt=["alphas", "means", "icf"])
+    torch.cuda.synchronize()
+    assert restored.all() and grads["icf"].shape == (2, K, P)
+    assert close(primal["err!"].cpu().numpy()[:1], [float(G[pre + "err"])], 1e-12, 0).all()
+    for nm in ("alphas", "means", "icf"):
+        assert close(grads[nm][0].cpu().numpy(), G[pre + "g_" + nm], 1e-10, 1e-12).all()
+    assert not torch.equal(grads["means"][0], grads["means"][1])
