@@ -1429,6 +1429,7 @@ class _Emitter:
             self.depth += 1
             self.w(f"if (chk) {{ const bool p0 = {post};")
             self.w("  if (p0 && !code) code = RC_POST; }")
+            self.w("#pragma unroll 1")
             self.w("for (;;) {")
             self.depth += 1
             self.w(f"const bool go = ({pre}) && !code;")
@@ -1453,6 +1454,10 @@ class _Emitter:
             self.w(f"{{ const long long n1_{L} = {a}, n2_{L} = {st}, n3_{L} = {b};")
             self.fail_check(label)
             self.w(f"  if (n2_{L} == 0 && !code) code = RC_DOMAIN;")
+            # program loops stay rolled: with array extents folded to constants
+            # nvcc would unroll nested loops around inlined bodies (minutes of
+            # compile time, hundreds of registers and spills)
+            self.w("  #pragma unroll 1")
             self.w(f"  for (long long x_{L} = n1_{L}; !code && (n2_{L} > 0 ? x_{L} <= n3_{L} : "
                    f"x_{L} >= n3_{L}); x_{L} += n2_{L}) {{")
             self.depth += 1
