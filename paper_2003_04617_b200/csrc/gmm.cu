@@ -57,6 +57,12 @@ namespace rl {
 #ifndef GMM_ALPHA_BLOCK
 #define GMM_ALPHA_BLOCK 1  // k_gmm_prep: the alphas' logsumexp in its own block (else block 0)
 #endif
+#ifndef GMM_PREP_BLOCKS
+#define GMM_PREP_BLOCKS 1  // k_gmm_prep: L^T built block by block (constant row lengths)
+#endif
+#ifndef GMM_FINAL_ERR_BLOCK
+#define GMM_FINAL_ERR_BLOCK 1  // k_gmm_final: the objective in its own block
+#endif
 #ifndef GMM_FUSE_FINAL
 #define GMM_FUSE_FINAL 1   // k_gmm_final sums the reverse partials itself (no k_gmm_reduce)
 #endif
@@ -177,12 +183,25 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
   __syncthreads();
   constexpr int LTS = ltb_size(DP);
   double *lt = LT + (long long)k * LTS;
+  (void)LTS;
+#if GMM_PREP_BLOCKS
+  // the packed layout row block by row block: the row length rl is a
+  // compile-time constant per (unrolled) block, so e -> (a, b) is a
+  // multiply-shift instead of a search and two runtime divisions
+#pragma unroll
+  for (int q = 0; q < DP / 16; q++) {
+    const int kb = 16 * q, rl = DP - kb + 4, off = ltb_off(DP, kb);
+    for (int r = threadIdx.x; r < 16 * rl; r += GMM_THREADS) {
+      const int e = off + r;
+#else
   for (int e = threadIdx.x; e < LTS; e += GMM_THREADS) {
+    {
     // invert e -> (a, b): block, row in block, column
     int q = 0;
     while (q + 1 < DP / 16 && ltb_off(DP, 16 * (q + 1)) <= e) q++;
     const int kb = 16 * q, rl = DP - kb + 4;
     const int r = e - ltb_off(DP, kb);
+#endif
     const int a = kb + r / rl, b = kb + r % rl;
     double v = 0.0;
     if (a < d && b < d) {
@@ -195,6 +214,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
       }
     }
     lt[e] = v;
+    }
   }
   if (threadIdx.x == 0) {
     double s = 0.0;
@@ -828,6 +848,36 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
   // p_0 + p_1 + ...), only over the entries used (the lower triangle)
   const int k = blockIdx.x, c = blockIdx.y, C = gridDim.y;
   const int P = d * (d + 1) / 2;
+#if GMM_FINAL_ERR_BLOCK
+  if (k == K) {                  // the extra column: the objective only (block (K, 0))
+    if (c != 0) return;
+    __shared__ double ered0[GMM_THREADS];
+    sum_err_parts(nerr, err_part, ered0);
+    __shared__ double cfro0[GMM_THREADS], csq0[GMM_THREADS];
+    double fro = 0.0, ssq = 0.0;
+    const double hg2 = 0.5 * ga * ga;
+    for (int k0 = 0; add_params && k0 < K; k0 += GMM_THREADS) {
+      const int kk = k0 + threadIdx.x;
+      if (kk < K) {
+        cfro0[threadIdx.x] = fro_k[kk];
+        csq0[threadIdx.x] = sq[kk];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int q = 0; q < GMM_THREADS && k0 + q < K; q++) {
+          fro = fro + cfro0[q];
+          ssq = ssq + csq0[q];
+        }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      double e = ered0[0];
+      if (add_params) e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
+      out[0] = e;
+    }
+    return;
+  }
+#endif
   const long long PW = (long long)DP * DP + DP + 1;
   const double hg2 = 0.5 * ga * ga;
   __shared__ double gsum[DP];
@@ -893,7 +943,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     }
   }
   __shared__ double ered[GMM_THREADS];
-  if (k == 0 && c == 0) {
+  if (!GMM_FINAL_ERR_BLOCK && k == 0 && c == 0) {
     sum_err_parts(nerr, err_part, ered);
     // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst);
     // fro and ssq summed in component order from shared-memory chunks
@@ -1132,7 +1182,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   if (GMM_ABLATE & 8) return 0;
   // enough (k, c) CTAs for about two per SM, at most 8 per component
   const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
-  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K, fc), dim3(GMM_THREADS), 0, st, d, K,
+  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K + GMM_FINAL_ERR_BLOCK, fc),
+                    dim3(GMM_THREADS), 0, st, d, K,
                     L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, part, errp, par, gamma, m, cst,
                     add_params, out);
 #else
