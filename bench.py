@@ -363,6 +363,15 @@ def run_bessel_ours(args, D):
         tr = load_traffic("k_besselj<1>")
         if tr:
             roof["traffic"] = tr
+        # cross-check: FP64 flops ncu counted for one configs[1] launch (2 per
+        # DFMA, 1 per DADD / DMUL; profiles/r01/ncu_bessel_flops.json) over
+        # this run's device time
+        fp = os.path.join(REPO, "profiles", "r01", "ncu_bessel_flops.json")
+        if os.path.exists(fp) and n_total == 1 << 26:
+            with open(fp) as fh:
+                ex = json.load(fh)["executed_fp64_flops"]
+            roof["executed_flops_per_launch_ncu"] = ex
+            roof["executed_frac"] = round(ex / (ms_step * 1e-3) / 1e12 / peak, 4)
     # objective only ("-O", the paper's objective timing): run of besselj
     o_ms = D.max(time_device(lambda: kernels.besselj_run(z, BESSEL_NU), max(3, args.steps // 4)))
     objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
