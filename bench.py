@@ -748,7 +748,7 @@ def run_gmm_ours(args, D):
     for _ in range(max(args.warmup, 3)):
         r = step()
     torch.cuda.synchronize()
-    # the step's launches (prep, memset, fwd, lse, rev, reduce, final) are
+    # the step's launches (prep, fwd, lse, rev, final) are
     # replayed as one CUDA graph: no per-launch host latency between them
     graph = None
     if not args.no_graph and D.dist is None:
