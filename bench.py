@@ -828,7 +828,7 @@ def run_gmm_ours(args, D):
                    "cuda_graph": graph is not None,
                    "per_rank": hi - lo, "parallelism": f"dp{D.world}+allreduce",
                    "l2": "256 MiB L2 flush before every evaluation"},
-        "roofline": roof, "gpu_launches": 6 * args.steps, "clocks": clocks,
+        "roofline": roof, "gpu_launches": 5 * args.steps, "clocks": clocks,
         "failed_per_step": D.sum(int(counters[1].item())) // (args.steps + max(args.warmup, 3)),
         "parity_sample": parity, "objective_only": objective,
     }
