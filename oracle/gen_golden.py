@@ -254,6 +254,7 @@ def gen_codegen():
         "wloop": (["acc!", "x"], {"n": 5}, 48),
         "prims": (["a!", "b!", "c!", "th"], {"n!": 3}, 40),
         "loose": (["y!", "x"], {}, 24),
+        "xorfold": (["y!", "x"], {"n": 5, "m!": 6}, 16),
     }
     out = {}
     for fn, (floats, ints, n) in cases.items():

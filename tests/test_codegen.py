@@ -15,7 +15,7 @@ def src(name):
     return open(os.path.join(REPO, "tests", "golden", "codegen", name + ".rnl")).read()
 
 
-@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix", "prims", "vlen", "loose"])
+@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix", "prims", "vlen", "loose", "xorfold"])
 def test_inversion_is_an_involution(name):
     for params, body in codegen._Parser(src(name)).program().values():
         assert codegen._invert_list(codegen._invert_list(body)) == body

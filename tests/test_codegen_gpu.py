@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 CASES = {"mul_acc": (["y!", "a", "b"], {}, True), "sink": (["out!", "x", "y"], {"n": 3}, False),
          "wloop": (["acc!", "x"], {"n": 5}, True),
          "prims": (["a!", "b!", "c!", "th"], {"n!": 3}, False),
-         "loose": (["y!", "x"], {}, True)}
+         "loose": (["y!", "x"], {}, True),
+         "xorfold": (["y!", "x"], {"n": 5, "m!": 6}, True)}
 
 
 def src(name):
