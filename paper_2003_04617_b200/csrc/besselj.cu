@@ -69,6 +69,9 @@ __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 #ifndef BJ_MINB
 #define BJ_MINB 3          // __launch_bounds__ min blocks per SM (80 registers, no spills)
 #endif
+#ifndef BJ_HESS_PAIRS
+#define BJ_HESS_PAIRS 1    // Hessian kernel: unpredicated trip pairs while every lane is live
+#endif
 #ifndef BJ_M
 #define BJ_M 5             // chunk = BJ_M elements per thread (z-sorted per chunk; 3 CTAs/SM fit)
 #endif
@@ -560,6 +563,59 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
     act = false;
   }
   int k = 0;
+#if BJ_HESS_PAIRS
+  // FAST main phase, as in besselj_element: while every live lane is still
+  // active the trips run in unpredicated pairs with one vote per pair (the
+  // pair's second log-domain term does not depend on the first's exp); the
+  // predicated loop below finishes the tail.  Same Dual operations in the
+  // same order per lane; dead lanes are restored afterwards.
+  if (!CAREFUL) {
+    const bool dead = !valid || code;
+    const int kend = (BJ_KP - 1) < kfuel ? (BJ_KP - 1) : kfuel;
+    if (__all_sync(FULL_MASK, act || dead) && __any_sync(FULL_MASK, act)) {
+      while (k + 2 <= kend) {
+        const double2 L1 = s_logpair[k + 1], L2 = s_logpair[k + 2];
+        Dl s1 = dadd(s, h2);
+        s1 = dsub(s1, dflt(L1.x));
+        s1 = dsub(s1, dflt(L1.y));
+        Dl s2 = dadd(s1, h2);
+        s2 = dsub(s2, dflt(L2.x));
+        s2 = dsub(s2, dflt(L2.y));
+        int cf = 0;
+        const Dl e1 = dexp<false>(s1, cf), e2 = dexp<false>(s2, cf);
+        const bool odd1 = (k + 1) & 1;
+        const Dl a1 = odd1 ? dsub(acc, e1) : dadd(acc, e1);
+        const Dl a2 = odd1 ? dadd(a1, e2) : dsub(a1, e2);
+        const bool act1 = e1.p > thr, act2 = e2.p > thr;
+        if (__all_sync(FULL_MASK, (act1 && act2) || dead)) {
+          s = s2;
+          e = e2;
+          acc = a2;
+          k += 2;
+          continue;
+        }
+        if (act1) {
+          s = s2;
+          e = e2;
+          acc = a2;
+          k += 2;
+          act = act2;
+        } else {
+          s = s1;
+          e = e1;
+          acc = a1;
+          k += 1;
+          act = false;
+        }
+        break;
+      }
+      if (dead) {
+        act = false;
+        k = 0;
+      }
+    }
+  }
+#endif
   while (__any_sync(FULL_MASK, act)) {
     if (act) {
       if (k >= kfuel) {
@@ -587,25 +643,44 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
   Dl gs = dflt(0.0), gh2 = dflt(0.0);
   if (fwd_ok && chk && e.p > thr) code = RL_ERR_POSTCONDITION;  // entry: post false
   int kr = fwd_ok ? T : 0;
-  while (__any_sync(FULL_MASK, kr >= 1)) {
-    if (kr >= 1) {
-      if (kr & 1) {                                       // acc += convert(s): sign -1
-        acc = dadd(acc, e);
-        gs = dadd(gs, dmul(dflt(-1.0 * gacc), e));
-      } else {                                            // acc -= convert(s): sign +1
-        acc = dsub(acc, e);
-        gs = dadd(gs, dmul(dflt(1.0 * gacc), e));
-      }
-      const double2 L = logpair_any(kr, nu);
-      s = dadd(s, dflt(L.y));                             // s *= kn
-      s = dadd(s, dflt(L.x));                             // s *= k
-      s = dsub(s, h2);                                    // s /= halfz2
-      gh2 = dadd(gh2, dmul(dflt(1.0), gs));
-      kr--;
-      int c = 0;
-      e = dexp<CAREFUL>(s, c);
-      if (!code) code = c ? c : ((chk && !(e.p > thr)) ? RL_ERR_POSTCONDITION : 0);
+  auto rtrip = [&](int kk) {                              // one reverse trip at kk (kr = kk)
+    if (kk & 1) {                                         // acc += convert(s): sign -1
+      acc = dadd(acc, e);
+      gs = dadd(gs, dmul(dflt(-1.0 * gacc), e));
+    } else {                                              // acc -= convert(s): sign +1
+      acc = dsub(acc, e);
+      gs = dadd(gs, dmul(dflt(1.0 * gacc), e));
     }
+    const double2 L = logpair_any(kk, nu);
+    s = dadd(s, dflt(L.y));                               // s *= kn
+    s = dadd(s, dflt(L.x));                               // s *= k
+    s = dsub(s, h2);                                      // s /= halfz2
+    gh2 = dadd(gh2, dmul(dflt(1.0), gs));
+    int c = 0;
+    e = dexp<CAREFUL>(s, c);
+    if (!code) code = c ? c : ((chk && !(e.p > thr)) ? RL_ERR_POSTCONDITION : 0);
+  };
+#if BJ_HESS_PAIRS
+  if (!CAREFUL) {
+    // predicated until every live lane is down to the warp's smallest trip
+    // count, then the rest unpredicated for all lanes (dead lanes compute
+    // values that are never stored)
+    const unsigned tmin = __reduce_min_sync(FULL_MASK, fwd_ok ? (unsigned)T : 0x7fffffffu);
+    if (tmin != 0x7fffffffu) {
+      while (__any_sync(FULL_MASK, kr > (int)tmin))
+        if (kr > (int)tmin) rtrip(kr--);
+      int kk = (int)tmin;
+      for (; kk >= 2; kk -= 2) {
+        rtrip(kk);
+        rtrip(kk - 1);
+      }
+      if (kk == 1) rtrip(1);
+      kr = 0;
+    }
+  }
+#endif
+  while (__any_sync(FULL_MASK, kr >= 1)) {
+    if (kr >= 1) rtrip(kr--);
   }
   Dl gz = dflt(0.0);
   if (fwd_ok) {
