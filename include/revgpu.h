@@ -69,7 +69,8 @@ const char *rl_last_error(void);
  * thr: the loop threshold literal of the program (1e-16); tol: the
  * ExecOptions.float_tolerance (interpreter.py:39, 1e-9); max_trips: fuel cap
  * on series terms (FuelExhausted beyond it); invcheck: ExecOptions.invcheck.
- * counters[0] += sum of series trips, counters[1] += failed elements.
+ * counters[0] += sum of the series trips of the elements that succeed (the
+ * oracle's definition), counters[1] += failed elements.
  * ---------------------------------------------------------------------- */
 int rl_besselj_grad_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
                         double seed, int64_t max_trips, int32_t invcheck, double *J,

@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
             s_dz[oi] = o.dz;
             s_d2[oi] = o.d2;
             s_fail[oi] = (uint8_t)o.code;
-            trips_sum += (unsigned long long)o.T;
+            if (!o.code) trips_sum += (unsigned long long)o.T;   // trips of the elements that succeed
             nfail += o.code != 0;
           }
           continue;
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
           s_J[oi] = o.J;
           s_dz[oi] = o.dz;
           s_fail[oi] = (uint8_t)o.code;
-          trips_sum += (unsigned long long)o.T;
+          if (!o.code) trips_sum += (unsigned long long)o.T;     // trips of the elements that succeed
           nfail += o.code != 0;
         }
       }
