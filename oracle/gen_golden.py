@@ -564,11 +564,55 @@ def gen_codegen_random():
     print("random programs:", len(texts), Counter(E))
 
 
+def gen_codegen_complex():
+    """reference gradient() (seeds y!.re, then y!.im) and hessian() of
+    tests/golden/codegen/polar.rnl (Complex parameters, field views, abs2 /
+    angle of a Complex operand, ROT by a field) on 12 random inputs."""
+    from revlang.autodiff import hessian
+    from revlang.values import Complex
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "polar.rnl")).read())
+    rng = np.random.default_rng(77)
+    X = np.concatenate([rng.uniform(-1, 1, (12, 2)), rng.uniform(-2, 2, (12, 2)) *
+                        rng.choice([-1, 1], (12, 2)), rng.uniform(-1, 1, (12, 2))], 1)
+    X[3, 2:4] = 0.0                                 # x = 0: log(0) -> RevDomainError
+    out = {"x": X}
+    for tag, path in (("re", (("field", "re"),)), ("im", (("field", "im"),))):
+        P, G, E = [], [], []
+        for row in X:
+            args = [Complex(row[0], row[1]), Complex(row[2], row[3]), row[4], row[5]]
+            r, en = _err_name(lambda: gradient(prog, GradRequest("polar", args,
+                                                                 seeds=[("y!", path, 1.0)])))
+            p = g = [np.nan] * 6
+            if r is not None:
+                prim, gr = r
+                p = [prim[0].re, prim[0].im, prim[1].re, prim[1].im, prim[2], prim[3]]
+                g = [gr["y!"].re, gr["y!"].im, gr["x"].re, gr["x"].im, gr["p!"], gr["q!"]]
+            P.append([float(v) for v in p])
+            G.append([float(v) for v in g])
+            E.append(en)
+        out[f"primal_{tag}"], out[f"grad_{tag}"], out[f"err_{tag}"] = \
+            np.array(P), np.array(G), np.array(E)
+    H, HE = [], []
+    for row in X:
+        args = [Complex(row[0], row[1]), Complex(row[2], row[3]), row[4], row[5]]
+        try:                  # the reference's Dual sqrt at 0 raises ZeroDivisionError
+            h, hn = _err_name(lambda: hessian(prog, "polar", args))
+        except ZeroDivisionError:
+            h, hn = None, "ZeroDivisionError"
+        H.append(h.matrix if h is not None else np.full((6, 6), np.nan))
+        HE.append(hn)
+    out["hess"], out["hess_err"] = np.array(H), np.array(HE)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_complex.npz"), **out)
+    from collections import Counter
+    print("complex goldens:", Counter(out["err_re"]), Counter(HE))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
-                              "codegen_random"]
+                              "codegen_random",
+                              "codegen_complex"]
     for w in which:
         globals()["gen_" + w]()

@@ -160,6 +160,13 @@ class NoCheck:
 
 
 @dataclass(frozen=True)
+class FView:
+    """x.re / x.im of a Complex cell (a Float leaf)."""
+    name: str
+    field: str
+
+
+@dataclass(frozen=True)
 class Safe:
     kind: str              # "assert" | "print"
     exprs: tuple
@@ -448,9 +455,13 @@ class _Parser:
         return tuple(views)
 
     def index_tail(self, name):
-        """name or name[i, j] (a view); field views are not supported."""
+        """name, name[i, j] or name.re / name.im (a view)."""
         if self.at("punct", "."):
-            raise UnsupportedProgram("codegen: field views are not supported")
+            self.adv()
+            field = self.name()
+            if field not in ("re", "im"):
+                raise UnsupportedProgram("codegen: records are not supported (only .re / .im)")
+            return FView(name, field)
         if not self.at("punct", "["):
             return Var(name)
         self.adv()
@@ -667,6 +678,8 @@ def _expr_names(e, acc):
         acc.add(e.name)
         for x in e.idx:
             _expr_names(x, acc)
+    elif isinstance(e, FView):
+        acc.add(e.name)
     elif isinstance(e, Un):
         _expr_names(e.e, acc)
     elif isinstance(e, Bin):
@@ -802,10 +815,15 @@ class _Subst:
             if not isinstance(base, Var):
                 raise KindError("indexing into a scalar cell")
             return IView(base.name, tuple(self.e(x) for x in v.idx))
+        if isinstance(v, FView):
+            base = self.env.get(v.name, Var(v.name + self.tag))
+            if not isinstance(base, Var):
+                raise KindError("a field of a non-Complex cell")
+            return FView(base.name, v.field)
         return v
 
     def e(self, x):
-        if isinstance(x, (Var, IView)):
+        if isinstance(x, (Var, IView, FView)):
             return self.view(x)
         if isinstance(x, Un):
             return Un(x.op, self.e(x.e))
@@ -948,6 +966,11 @@ __device__ __forceinline__ Dl g_exp(Dl x, int &c) {
   return Dl(r, x.t * r);
 }
 __device__ __forceinline__ Dl sin(Dl x) { return Dl(sin(x.p), x.t * cos(x.p)); }
+// s_atan2 over Duals (values.py): (atan2(yp, xp), (xp yt - yp xt) / (yp^2 + xp^2))
+__device__ __forceinline__ Dl atan2(Dl y, Dl x) {
+  const double r2 = y.p * y.p + x.p * x.p;
+  return Dl(atan2(y.p, x.p), (x.p * y.t - y.p * x.t) / r2);
+}
 __device__ __forceinline__ Dl cos(Dl x) { return Dl(cos(x.p), -x.t * sin(x.p)); }
 __device__ __forceinline__ double g_abs(double x, int &) { return fabs(x); }
 __device__ __forceinline__ Dl g_abs(Dl x, int &c) {
@@ -1029,10 +1052,17 @@ class _Emitter:
         if k in ("a", "ai"):
             raise KindError(f"{name!r} is an array; index it (instructions and expressions "
                             "take scalar cells)")
+        if k == "c":
+            raise KindError(f"{name!r} is Complex: use {name}.re / {name}.im, or abs / abs2 / "
+                            "angle as an instruction argument")
         return k
 
     def cell_kind(self, v):
         """Kind of a view's cell: array cells are Float ("a") or Int ("ai")."""
+        if isinstance(v, FView):
+            if self.kinds.get(v.name) != "c":
+                raise KindError(f"{v.name!r} has no field {v.field!r}")
+            return "f"
         if isinstance(v, IView):
             if v.name not in self.shapes:
                 raise KindError(f"{v.name!r} is not an array parameter")
@@ -1073,6 +1103,8 @@ class _Emitter:
                 a, b = views[i], views[j]
                 if a.name != b.name:
                     continue
+                if isinstance(a, FView) and isinstance(b, FView) and a.field != b.field:
+                    continue                                   # .re and .im are disjoint
                 if pres[i] is None or pres[j] is None:      # a whole cell / array
                     self.w("if (!code) code = RC_ALIAS;")
                 elif len(pres[i]) == len(pres[j]):
@@ -1082,6 +1114,13 @@ class _Emitter:
     def view_ref(self, a, pre=None):
         """_Ref of an instruction operand; array offsets land in temps (the
         reference's readers evaluate indices in operand order)."""
+        if isinstance(a, FView):
+            self.cell_kind(a)
+            c = _cid(a.name)
+            return _Ref(f"v_{c}_{a.field}", f"g_{c}_{a.field}", "f", a.name, ("field", a.field))
+        if isinstance(a, Var) and self.kinds.get(a.name) == "c":
+            c = _cid(a.name)                          # the whole Complex value
+            return _Ref(c, c, "c", a.name)
         if isinstance(a, IView):
             o = self.new("o")
             self.w(f"const long long {o} = {self.offset(a, pre)};")
@@ -1096,6 +1135,11 @@ class _Emitter:
         """_alias_checks (interpreter.py:624-657): same root and overlapping
         storage ids -> AliasedArguments, at run time like the reference."""
         if a is None or b is None or a.root != b.root:
+            return
+        if isinstance(a.off, tuple) or isinstance(b.off, tuple):      # Complex fields
+            if isinstance(a.off, tuple) and isinstance(b.off, tuple) and a.off != b.off:
+                return                                 # .re and .im are disjoint
+            self.w("if (!code) code = RC_ALIAS;")
             return
         if a.off is None or b.off is None:
             self.w("if (!code) code = RC_ALIAS;")
@@ -1118,7 +1162,7 @@ class _Emitter:
         if isinstance(e, Var):
             k = self.kind(e.name)
             return "f" if k == "u" else k
-        if isinstance(e, IView):
+        if isinstance(e, (IView, FView)):
             return self.cell_kind(e)
         if isinstance(e, Un):
             return self.expr_kind(e.e)
@@ -1178,6 +1222,9 @@ class _Emitter:
             return f"v_{_cid(e.name)}", k
         if isinstance(e, IView):
             return f"v_{_cid(e.name)}[{self.offset(e)}]", self.cell_kind(e)
+        if isinstance(e, FView):
+            self.cell_kind(e)
+            return f"v_{_cid(e.name)}_{e.field}", "f"
         if isinstance(e, Un):
             s, k = self.expr(e.e)
             return f"(-{s})", k
@@ -1548,6 +1595,34 @@ class _Emitter:
         self.w(f"  {a.v} = ax{n} * c{n} - bx{n} * s{n}; {b.v} = ax{n} * s{n} + bx{n} * c{n};")
         self.w(f"  {a.g} = ga{n} * c{n} - gb{n} * s{n}; {b.g} = ga{n} * s{n} + gb{n} * c{n}; }}")
 
+    def complex_instr(self, s, grad, tr, refs):
+        """y += f(x) with x Complex, f in abs / abs2 / angle (numerics.py
+        _COMPLEX_FNS: value and (d/dre, d/dim); _plus_minus_adjoint
+        accumulates (sign gy) d/dre and (sign gy) d/dim)."""
+        if s.op not in ("+=", "-=") or s.fname not in ("abs", "abs2", "angle") \
+                or len(refs) != 1 or tr.kind != "f":
+            raise UnsupportedProgram("codegen: a Complex operand takes +=/-= abs, abs2 or angle "
+                                     "into a Float target")
+        c = refs[0].v
+        a, b = f"R(v_{c}_re)", f"R(v_{c}_im)"
+        sq = f"({a} * {a} + {b} * {b})"
+        val = {"abs": f"g_sqrt({sq}, code)", "abs2": sq, "angle": f"atan2({b}, {a})"}[s.fname]
+        n = self.new("cx")
+        self.w(f"{{ const R v{n} = {val};")
+        self.w(f"  {tr.v} = {tr.v} {'+' if s.op == '+=' else '-'} v{n}; }}")
+        if not grad:
+            return
+        sign = "1.0" if s.op == "-=" else "-1.0"
+        if s.fname == "abs":
+            dre, dim = f"g_div({a}, r{n}, code)", f"g_div({b}, r{n}, code)"
+        elif s.fname == "abs2":
+            dre, dim = f"(2.0 * {a})", f"(2.0 * {b})"
+        else:
+            dre, dim = f"g_div(-{b}, {sq}, code)", f"g_div({a}, {sq}, code)"
+        self.w(f"{{ const R sg{n} = {sign} * {tr.g}; const R r{n} = {val};")
+        self.w(f"  g_{c}_re = g_{c}_re + sg{n} * {dre};")
+        self.w(f"  g_{c}_im = g_{c}_im + sg{n} * {dim}; }}")
+
     def instr(self, s, grad, label):
         self.w("{")
         self.depth += 1
@@ -1571,6 +1646,9 @@ class _Emitter:
                     self.alias(refs[i], refs[j], label)
         tk = tr.kind
         TV, TG = tr.v, tr.g
+        if any(r is not None and r.kind == "c" for r in refs):
+            self.complex_instr(s, grad, tr, refs)
+            return
         if s.op == "xor=":
             # numerics._xor_plain: Int targets with Int values (Bool is not
             # compiled); anything else is the reference's KindError, raised
@@ -1726,7 +1804,7 @@ extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, 
 """
 
 
-def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
+def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_params=()):
     """CUDA source of the batched gradient (mode "grad"), forward-over-reverse
     Hessian-column (mode "hess": the same code over Dual numbers, tangent on
     the Float leaf `dir`) or plain run / uncall (modes "run" / "uncall": one
@@ -1744,17 +1822,21 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
     params, body = fns[fname]
     int_params = set(int_params)
     shapes = _check_shapes(array_shapes, parser.arrays.get(fname, ()), params)
+    complex_params = set(complex_params)
     kinds = {p: ("ai" if p in shapes and p in int_params else "a" if p in shapes
-                 else "i" if p in int_params else "f") for p in params}
+                 else "i" if p in int_params else "c" if p in complex_params else "f")
+             for p in params}
     inliner = _Inliner(fns)
     fwd = inliner.run(_expand(body), (fname,))
     inv = inliner.run(_expand(_invert_list(body)), (fname,))
-    floats = [p for p in params if kinds[p] in ("f", "a")]
+    floats = [p for p in params if kinds[p] in ("f", "a", "c")]
     ints = [p for p in params if kinds[p] in ("i", "ai")]
     leaves, base = [], {}
     for p in floats:
         base[p] = len(leaves)
-        leaves += [(p, path) for path in (_leaf_paths(shapes[p]) if p in shapes else [()])]
+        paths = (_leaf_paths(shapes[p]) if p in shapes else
+                 [(("field", "re"),), (("field", "im"),)] if kinds[p] == "c" else [()])
+        leaves += [(p, path) for path in paths]
     locals_ = sorted(_collect_vars(fwd, set()) | _collect_vars(inv, set()))
     plain = mode in ("run", "uncall")
     em_f = _Emitter(params, kinds, inv if mode == "uncall" else fwd, fname, shapes)
@@ -1802,6 +1884,11 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
             L.append(f"      v_{c}[e] = R(fin[({b}LL + e) * n + i]"
                      + (f", dir == {b} + e ? 1.0 : 0.0);" if hess else ");"))
             L.append(f"      g_{c}[e] = R(0.0); }}")
+        elif kinds[p] == "c":                       # Complex: two Float cells, re then im
+            for q, fld in enumerate(("re", "im")):
+                L.append(f"    R v_{c}_{fld} = R(fin[{b + q}LL * n + i]"
+                         + (f", dir == {b + q} ? 1.0 : 0.0)" if hess else ")")
+                         + f", g_{c}_{fld} = R(0.0);")
         else:
             L.append(f"    R v_{c} = R(fin[{b}LL * n + i]"
                      + (f", dir == {b} ? 1.0 : 0.0)" if hess else ")") + f", g_{c} = R(0.0);")
@@ -1827,6 +1914,9 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None):
                 m = math.prod(shapes[p])
                 out.append(f"    for (int e = 0; e < {m}; ++e) {{ "
                            + fmt(f"({b}LL + e)", f"v_{c}[e]", f"g_{c}[e]") + " }")
+            elif kinds[p] == "c":
+                for q, fld in enumerate(("re", "im")):
+                    out.append("    " + fmt(f"{b + q}LL", f"v_{c}_{fld}", f"g_{c}_{fld}"))
             else:
                 out.append("    " + fmt(f"{b}LL", f"v_{c}", f"g_{c}"))
         return out
@@ -1958,11 +2048,13 @@ class CompiledFunction:
     parameter name (arrays keep their shape; Int parameters carry no
     gradient)."""
 
-    def __init__(self, source_text, fname, int_params=(), array_shapes=None):
+    def __init__(self, source_text, fname, int_params=(), array_shapes=None, complex_params=()):
         self.fname = fname
         self._text, self._ints, self._shapes = source_text, tuple(int_params), array_shapes
+        self.complex = tuple(complex_params)
         self.source, self.floats, self.ints, self.leaves = generate(
-            source_text, fname, int_params, array_shapes=array_shapes)
+            source_text, fname, int_params, array_shapes=array_shapes,
+            complex_params=self.complex)
         self.params = _Parser(source_text).program()[fname][0]
         self.shapes = _check_shapes(array_shapes, (), self.params)
         self._lib = self._load(self.source)
@@ -1980,7 +2072,8 @@ class CompiledFunction:
     def _lib_for(self, mode):
         if mode not in self._libs:
             self._libs[mode] = self._load(generate(self._text, self.fname, self._ints, mode=mode,
-                                                   array_shapes=self._shapes)[0])
+                                                   array_shapes=self._shapes,
+                                                   complex_params=self.complex)[0])
         return self._libs[mode]
 
     def run(self, inputs, direction=1, tol=1e-9, invcheck=True, max_steps=10**9):
@@ -2000,7 +2093,7 @@ class CompiledFunction:
         if not paths:
             raise KindError(f"first argument {first!r} has no differentiable leaf; "
                             "pass explicit seeds")
-        if len(paths) > 1:
+        if len(paths) > 1 and first not in self.complex:     # a Complex seeds its real part
             raise KindError(f"first argument {first!r} is not scalar; pass explicit seeds")
         return [(first, paths[0], 1.0)]
 
@@ -2031,6 +2124,14 @@ class CompiledFunction:
         for p in self.floats:
             v = inputs.get(p)
             shp = self.shapes.get(p, ())
+            if p in self.complex:
+                if isinstance(v, torch.Tensor) and v.dim() == 1:
+                    if not v.is_cuda or v.dtype != torch.complex128:
+                        raise KindError(f"{p} must be a CUDA complex128 tensor")
+                    n = v.shape[0] if n is None else n
+                    if v.shape[0] != n:
+                        raise KindError("all batched inputs need the same length")
+                continue
             if isinstance(v, torch.Tensor) and v.dim() == len(shp) + 1:
                 if not v.is_cuda or v.dtype != torch.float64 or tuple(v.shape[1:]) != shp:
                     raise KindError(f"{p} must be a CUDA float64 tensor of shape (n, *{shp})")
@@ -2044,6 +2145,14 @@ class CompiledFunction:
             shp = self.shapes.get(p, ())
             m = math.prod(shp)
             v = inputs.get(p, 0.0)
+            if p in self.complex:                          # re and im columns
+                if isinstance(v, torch.Tensor) and v.dim() == 1:
+                    cols += [v.real.reshape(1, n), v.imag.reshape(1, n)]
+                else:
+                    z = complex(v.re, v.im) if hasattr(v, "re") else complex(v)
+                    cols.append(torch.tensor([[z.real], [z.imag]], dtype=torch.float64,
+                                             device=dev).expand(2, n))
+                continue
             if isinstance(v, torch.Tensor) and v.dim() == len(shp) + 1:
                 cols.append(v.reshape(n, m).t())
             else:
@@ -2080,7 +2189,8 @@ class CompiledFunction:
                 path = ()
             if pname not in self.params:
                 raise KindError(f"seed names unknown parameter {pname!r}")
-            key = (pname, tuple((a, tuple(b)) for a, b in path))
+            key = (pname, tuple((a, tuple(b) if isinstance(b, (tuple, list)) else b)
+                                for a, b in path))
             if key not in col:
                 raise KindError("seed target is not a differentiable leaf")
             sv[col[key]] = float(val)
@@ -2099,6 +2209,11 @@ class CompiledFunction:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
         primal, grads, b = {}, {}, 0
         for p in self.floats:
+            if p in self.complex:
+                primal[p] = torch.complex(fout[b], fout[b + 1])
+                grads[p] = torch.complex(gout[b], gout[b + 1])
+                b += 2
+                continue
             shp = self.shapes.get(p, ())
             m = math.prod(shp)
             primal[p] = fout[b:b + m].t().reshape((n,) + shp)
@@ -2113,7 +2228,7 @@ class CompiledFunction:
         return primal, grads, fail, hout
 
 
-def compile_function(source_text, fname, int_params=(), array_shapes=None):
+def compile_function(source_text, fname, int_params=(), array_shapes=None, complex_params=()):
     """Compile function `fname` of reversible-DSL source to a batched CUDA
     gradient kernel (see CompiledFunction)."""
-    return CompiledFunction(source_text, fname, int_params, array_shapes)
+    return CompiledFunction(source_text, fname, int_params, array_shapes, complex_params)

@@ -58,6 +58,8 @@ def _kind(v, name):
         return "i", ()
     if _is_float(v):
         return "f", ()
+    if isinstance(v, complex) or (hasattr(v, "re") and hasattr(v, "im")):
+        return "c", ()                                 # Complex: two Float leaves
     a = _as_array(v)
     if a is None:
         raise UnsupportedProgram(f"codegen: argument {name!r} of kind {type(v).__name__} is "
@@ -73,9 +75,10 @@ def compiled(prog, fname, kinds):
         raise UnsupportedProgram(f"{fname}: no CUDA device (generated kernels have no CPU path)")
     ints = tuple(p for p, (k, _) in kinds.items() if k in ("i", "ai"))
     shapes = {p: s for p, (k, s) in kinds.items() if k in ("a", "ai")}
-    key = (prog.source, fname, ints, tuple(sorted(shapes.items())))
+    cplx = tuple(p for p, (k, _) in kinds.items() if k == "c")
+    key = (prog.source, fname, ints, tuple(sorted(shapes.items())), cplx)
     if key not in _CACHE:
-        _CACHE[key] = codegen.CompiledFunction(prog.source, fname, ints, shapes)
+        _CACHE[key] = codegen.CompiledFunction(prog.source, fname, ints, shapes, cplx)
     return _CACHE[key]
 
 
@@ -90,7 +93,9 @@ def _inputs(names, kinds, args):
     out = {}
     for p, v in zip(names, args):
         k = kinds[p][0]
-        out[p] = float(v) if k == "f" else int(v) if k == "i" else _as_array(v)
+        out[p] = float(v) if k == "f" else int(v) if k == "i" else (
+            complex(v) if k == "c" and isinstance(v, complex) else
+            v if k == "c" else _as_array(v))
     return out
 
 
@@ -101,6 +106,11 @@ def _back(template, kind, value):
         return float(v)
     if kind == "i":
         return int(v)
+    if kind == "c":                                   # the caller's Complex class
+        z = complex(v)
+        if hasattr(template, "re") and hasattr(template, "im"):
+            return type(template)(float(z.real), float(z.imag))
+        return z
     data = [int(x) for x in v.ravel()] if kind == "ai" else [float(x) for x in v.ravel()]
     if isinstance(template, torch.Tensor):
         return torch.as_tensor(v.copy())
@@ -172,6 +182,9 @@ def gradient_batch(prog, fdef, inputs, seeds, wrt, opts):
         v = inputs[p]
         if isinstance(v, torch.Tensor) and v.dtype == torch.float64 and v.dim() >= 1:
             kinds[p] = ("f", ()) if v.dim() == 1 else ("a", tuple(v.shape[1:]))
+            vals[p] = v
+        elif isinstance(v, torch.Tensor) and v.dtype == torch.complex128 and v.dim() == 1:
+            kinds[p] = ("c", ())
             vals[p] = v
         else:
             kinds[p] = _kind(v, p)

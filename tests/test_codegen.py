@@ -15,7 +15,8 @@ def src(name):
     return open(os.path.join(REPO, "tests", "golden", "codegen", name + ".rnl")).read()
 
 
-@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix", "prims", "vlen", "loose", "xorfold"])
+@pytest.mark.parametrize("name", ["mul_acc", "sink", "wloop", "quad", "mix", "prims", "vlen", "loose", "xorfold",
+                                  "polar"])
 def test_inversion_is_an_involution(name):
     for params, body in codegen._Parser(src(name)).program().values():
         assert codegen._invert_list(codegen._invert_list(body)) == body
@@ -47,10 +48,18 @@ def test_calls_are_inlined_with_fresh_locals():
 def test_unsupported_constructs_are_rejected():
     for text in ("fn f(y!, x)\n g(y!, x)\nend\n",
                  "fn f(y!, x)\n y! += 1.0fx\nend\n",
-                 "fn f(y!, x)\n y!.re += x\nend\n",
+                 "fn f(y!, x)\n y!.rec += x\nend\n",
                  "fn f(y!, x)\n @safe print(x)\nend\n"):
         with pytest.raises(UnsupportedProgram):
             codegen.generate(text, "f")
+
+
+def test_complex_field_views():
+    with pytest.raises(KindError):                      # y! is not declared Complex
+        codegen.generate("fn f(y!, x)\n y!.re += x\nend\n", "f")
+    src_, floats, ints, leaves = codegen.generate("fn f(y!, x)\n y!.re += x\nend\n", "f",
+                                                  complex_params=("y!",))
+    assert leaves == [("y!", (("field", "re"),)), ("y!", (("field", "im"),)), ("x", ())]
 
 
 def test_array_shapes_are_required_and_checked():
@@ -108,8 +117,9 @@ def test_view_argument_indexed_by_another_argument():
 def test_reference_catalog_programs_in_the_subset_compile(tmp_path, monkeypatch):
     """The reference's own catalog (stdlib.CATALOG), pretty-printed by the
     reference and compiled here: every program whose argument kinds are in
-    the subset generates and builds for sm_100a; Complex / Fixed / bijector
-    programs are rejected with UnsupportedProgram."""
+    the subset generates and builds for sm_100a (8 of 10, the Complex ones
+    included); the Fixed and the recursive bijector program are rejected with
+    UnsupportedProgram."""
     import random
     import sys
     monkeypatch.setenv("REVGPU_CODEGEN_CACHE", str(tmp_path))
@@ -128,9 +138,12 @@ def test_reference_catalog_programs_in_the_subset_compile(tmp_path, monkeypatch)
             kinds = {nm: generic._kind(v, nm) for nm, v in zip(p.get(fn).param_names(), args)}
             ints = tuple(k for k, (kk, _) in kinds.items() if kk in ("i", "ai"))
             shapes = {k: s for k, (kk, s) in kinds.items() if kk in ("a", "ai")}
-            codegen.build(codegen.generate(pretty_print(p), fn, ints, array_shapes=shapes)[0])
+            cplx = tuple(k for k, (kk, _) in kinds.items() if kk == "c")
+            codegen.build(codegen.generate(pretty_print(p), fn, ints, array_shapes=shapes,
+                                           complex_params=cplx)[0])
             built.append(name)
         except UnsupportedProgram:
             rejected.append(name)
     assert {"multiplier", "i_affine", "i_umm", "r_norm", "leapfrog_clean",
-            "leapfrog_cumulative"} <= set(built), (built, rejected)
+            "leapfrog_cumulative", "complex_log", "complex_log_ccu"} <= set(built), \
+        (built, rejected)

@@ -222,3 +222,59 @@ def test_gradient_batch_of_gmm_problems(cuda, golden):
     for nm in ("alphas", "means", "icf"):
         assert close(grads[nm][0].cpu().numpy(), G[pre + "g_" + nm], 1e-10, 1e-12).all()
     assert not torch.equal(grads["means"][0], grads["means"][1])
+
+
+def test_complex_parameters_against_the_reference(cuda, golden):
+    """tests/golden/codegen/polar.rnl: Complex parameters (two Float leaves),
+    field views as targets / operands / a ROT angle, abs2 and angle of a
+    Complex operand; batched gradient with seeds on y!.re and y!.im, and the
+    Hessian, against the reference (codegen_complex.npz)."""
+    from oracle import ERROR_NAMES
+    from test_codegen_gpu import src
+    g = golden("codegen_complex")
+    X = g["x"]
+    k = codegen.compile_function(src("polar"), "polar", complex_params=("y!", "x"))
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=cuda)  # noqa: E731
+    inputs = {"y!": t(X[:, 0] + 1j * X[:, 1]), "x": t(X[:, 2] + 1j * X[:, 3]),
+              "p!": t(X[:, 4]), "q!": t(X[:, 5])}
+    for tag in ("re", "im"):
+        primal, grads, fail = k.gradient(inputs, seeds=[("y!", (("field", tag),), 1.0)])
+        torch.cuda.synchronize()
+        names = np.array([ERROR_NAMES[int(c)] for c in fail.cpu().numpy()])
+        assert np.array_equal(names, g["err_" + tag])
+        ok = names == ""
+        P = torch.stack([primal["y!"].real, primal["y!"].imag, primal["x"].real,
+                         primal["x"].imag, primal["p!"], primal["q!"]], 1).cpu().numpy()
+        G = torch.stack([grads["y!"].real, grads["y!"].imag, grads["x"].real, grads["x"].imag,
+                         grads["p!"], grads["q!"]], 1).cpu().numpy()
+        for r in np.nonzero(ok)[0]:
+            assert close(P[r], g["primal_" + tag][r], 1e-12, 1e-14).all(), (tag, r)
+            assert close(G[r], g["grad_" + tag][r], 1e-12, 1e-14).all(), (tag, r)
+    H, fail = k.hessian(inputs)
+    torch.cuda.synchronize()
+    for r in range(X.shape[0]):
+        if g["hess_err"][r] == "":
+            assert fail[r].item() == 0
+            assert close(H[r].cpu().numpy(), g["hess"][r], 1e-10, 1e-12).all(), r
+        else:
+            assert fail[r].item() != 0                  # the reference raised too
+
+
+def test_complex_through_the_dropin_api(cuda, golden):
+    """gradient() with the reference's own Complex values round-trips the
+    Complex containers (default seed: the real part of the first argument)."""
+    import sys
+    import paper_2003_04617_b200 as rg
+    from test_codegen_gpu import src
+
+    class Complex:                                      # the reference's container shape
+        def __init__(self, re, im):
+            self.re, self.im = re, im
+    g = golden("codegen_complex")
+    row = g["x"][0]
+    args = [Complex(row[0], row[1]), Complex(row[2], row[3]), float(row[4]), float(row[5])]
+    primal, grads = rg.gradient(src("polar"), rg.GradRequest("polar", args))
+    assert isinstance(primal[0], Complex) and isinstance(grads["x"], Complex)
+    got = [grads["y!"].re, grads["y!"].im, grads["x"].re, grads["x"].im, grads["p!"], grads["q!"]]
+    assert close(got, g["grad_re"][0], 1e-12, 1e-14).all()
+    del sys
