@@ -2,26 +2,36 @@
 """bench.py — throughput of the reversible-AD gradient kernels on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload bessel|ba|gmm|gmm_large]
+                    [--workload all|bessel|ba|gmm|gmm_large] [--dry-run]
 
-Default workload: BASELINE.json configs[1], the Bessel J_2 gradient over a
-batch of 2^26 inputs z ~ U(0.1, 10) (seed 1), sharded over the ranks
-(strong scaling: the 2^26 batch is fixed, each rank takes a contiguous
-slice; no collective on the data path).  A "step" = one fused forward +
-reverse-sweep kernel over the rank's slice, inputs resident in HBM
-(512 MiB > 126 MB L2, so no flush is needed between steps).
+Default (--workload all): the headline is BASELINE.json configs[1], the
+Bessel J_2 gradient over a batch of 2^26 inputs z ~ U(0.1, 10) (seed 1),
+sharded over the ranks (strong scaling: the 2^26 batch is fixed, each rank
+takes a contiguous slice; no collective on the data path).  A "step" = one
+fused forward + reverse-sweep kernel over the rank's slice, inputs resident
+in HBM (512 MiB > 126 MB L2, so no flush is needed between steps).  The same
+line carries one sub-object per other BASELINE config, each with its own
+value, roofline, cpu_baseline, e2e and clocks: "ba" (configs[3], ba20
+Jacobian), "gmm_c3" (configs[2], d=64 K=25 N=10^4) and "gmm_c5" (configs[4],
+d=128 K=200 N=10^6); each is timed over >= 200 ms of device time so the
+clock sampler sees it.
+
+--gpus N > 1 without torchrun: bench.py re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL); under torchrun the
+world size must equal --gpus.
 
 Printed (rank 0, one JSON line): value = whole-job gradient evals/s from
 the device time (CUDA events, max over ranks); e2e = the same metric
-through the C-ABI host-buffer entry (pinned host z in, J/dJdz/fail out,
+through the C-ABI host-buffer entry (pinned host inputs in, outputs out,
 copies inside the timed region); roofline of the dominant kernel against
-the in-run measured FP64 DFMA peak; cpu_baseline = the C oracle port
-(oracle/, the reference algorithm) on a bounded sample over all host
-threads; clocks sampled with nvidia-smi during the timed region.
+the in-run measured FP64 DFMA / DMMA peak (HBM for BA); cpu_baseline = the C
+oracle port (oracle/, the reference algorithm) on a bounded sample; clocks
+sampled with NVML during the timed region.
 
 `--impl reference` times the reference algorithm's CPU implementation
 (the oracle port — the reference itself is pure Python and cannot travel
-to the GPU box) on the same workload, rank 0 only.
+to the GPU box) on the same workloads and configs, rank 0 only, each rate
+from a bounded sample ("rate_sample": true).
 """
 
 import argparse
@@ -49,7 +59,11 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-graph", action="store_true",
                     help="GMM: launch the step's kernels directly instead of as a CUDA graph")
-    ap.add_argument("--workload", choices=["bessel", "ba", "gmm", "gmm_large"], default="bessel")
+    ap.add_argument("--workload", choices=["all", "bessel", "ba", "gmm", "gmm_large"],
+                    default="all")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU work: exercise the launch / world-size / max-over-ranks "
+                         "plumbing under gloo (CPU tests)")
     ap.add_argument("--n", type=int, default=None, help="override the batch size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -74,14 +88,46 @@ class Dist:
         self.rank, self.world, self.local = dist_env()
         self.dist = dist if self.world > 1 else None
         self.torch = torch
+        self.backend = backend
+        self.nccl_log = None
         if self.dist is not None:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend == "nccl" and torch.cuda.is_available():
+                # the communicator's own INIT lines (nRanks, NVLS/P2P) to a
+                # per-rank file, summarised into the JSON line
+                self.nccl_log = f"/tmp/bench_nccl.{os.getpid()}.log"
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", self.nccl_log)
                 # bind this rank to its GPU before the communicator is created
                 torch.cuda.set_device(self.local)
                 dist.init_process_group(backend, device_id=torch.device("cuda", self.local))
             else:
                 dist.init_process_group(backend)
+            if dist.get_world_size() != self.world:
+                raise SystemExit(f"world size {dist.get_world_size()} != WORLD_SIZE {self.world}")
+
+    def nccl_info(self):
+        """nRanks / version lines of this rank's communicator (NCCL_DEBUG=INFO)."""
+        if self.dist is None:
+            return None
+        info = {"backend": self.backend, "world_size": self.dist.get_world_size()}
+        path = os.environ.get("NCCL_DEBUG_FILE")
+        if path and os.path.exists(path):
+            with open(path, errors="replace") as fh:
+                txt = fh.read()
+            import re
+            m = re.findall(r"nRanks (\d+)", txt)
+            if m:
+                info["nccl_nranks"] = int(m[-1])
+            v = re.search(r"NCCL version ([\w.+-]+)", txt)
+            if v:
+                info["nccl_version"] = v.group(1)
+            info["nvls"] = "NVLS" in txt and "NVLS multicast support is not available" not in txt
+        return info
+
+    def _dev(self):
+        return "cuda" if self.backend == "nccl" and self.torch.cuda.is_available() else "cpu"
 
     def barrier(self):
         if self.dist is not None:
@@ -90,16 +136,14 @@ class Dist:
     def max(self, x):
         if self.dist is None:
             return x
-        t = self.torch.tensor([float(x)], dtype=self.torch.float64,
-                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum(self, x):
         if self.dist is None:
             return x
-        t = self.torch.tensor([float(x)], dtype=self.torch.float64,
-                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self._dev())
         self.dist.all_reduce(t)
         return float(t.item())
 
@@ -280,6 +324,12 @@ BESSEL_N = 1 << 26
 BESSEL_NU = 2
 
 
+def bessel_config(n_total, world):
+    return {"workload": "bessel_j2_grad_2^26" if n_total == BESSEL_N else f"bessel_j2_grad_{n_total}",
+            "n_total": n_total, "nu": BESSEL_NU, "thr": THR, "per_rank": n_total // world,
+            "parallelism": f"shard{world}", "l2": "inputs 512 MiB > 126 MB L2; no flush"}
+
+
 def bessel_flops(n, sum_trips, nu, w):
     """Algorithmic FP64 flops of one launch (DESIGN.md §Bessel roofline):
     per series trip  forward 3 add + exp + 1 add; reverse 1 add + 1 mul +
@@ -402,9 +452,7 @@ def run_bessel_ours(args, D):
         "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic z ~ U(0.1, 10), seed 1",
-        "config": {"workload": "bessel_j2_grad_2^26", "n_total": n_total, "nu": BESSEL_NU,
-                   "thr": THR, "per_rank": n, "parallelism": f"shard{D.world}",
-                   "l2": "inputs 512 MiB > 126 MB L2; no flush"},
+        "config": bessel_config(n_total, D.world),
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clocks, "sum_trips_per_step": D.sum(sum_trips),
         "failed_per_step": D.sum(n_failed), "parity_sample": parity,
@@ -524,6 +572,22 @@ def ba_synthetic(n_cams, n_pts, n_obs, seed=3):
     return cams, X, w, feats, obs
 
 
+def ba_config(p_total, world):
+    return {"workload": "ba20_jacobian", "n_cams": BA_N, "n_pts": BA_M, "n_obs": p_total,
+            "per_rank": p_total // world, "parallelism": f"shard{world}",
+            "l2": "256 MiB L2 flush before every timed launch; per-launch CUDA events"}
+
+
+def steps_for(step_ms, args, floor_ms=200.0, budget_ms=2000.0, cap=20000):
+    """Timed steps of a sub-workload: at least 3 and at least floor_ms of
+    device time (so the NVML clock sampler sees the region), and --steps when
+    that fits in budget_ms."""
+    step_ms = max(step_ms, 1e-3)
+    n = max(3, -(-floor_ms // step_ms))
+    n = max(n, min(args.steps, budget_ms // step_ms))
+    return int(min(cap, n))
+
+
 def ba_bytes(n_cams, n_pts, p):
     """Algorithmic HBM bytes of one Jacobian launch (DESIGN.md §BA roofline):
     read obs (8) + w (8) + feats (16) per observation, every camera (88) and
@@ -552,12 +616,16 @@ def run_ba_ours(args, D):
         kernels.ba_jacobian(dc, dX, dw, df, do, want_err=False, out=out, counters=counters)
     torch.cuda.synchronize()
     props = torch.cuda.get_device_properties(dev)
+    stream = torch.cuda.current_stream()
+    steps = steps_for(D.max(time_device(
+        lambda: kernels.ba_jacobian(dc, dX, dw, df, do, want_err=False, out=out),
+        3, flush) + 0.05), args)
+    counters.zero_()
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
     D.barrier()
-    stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     for a, b in evs:
         flush.fill_(1)                      # evict L2 (inputs are 26 MB < 126 MB L2)
         a.record(stream)
@@ -566,7 +634,7 @@ def run_ba_ours(args, D):
     torch.cuda.synchronize()
     D.barrier()
     clocks = sampler.stop()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     ms_step = D.max(ms)
     n_failed = D.sum(int(counters[1].item()))
     value = 1.0 / (ms_step * 1e-3)
@@ -607,15 +675,13 @@ def run_ba_ours(args, D):
         e2e = ba_e2e(cams, X, w[lo:hi], feats[lo:hi], obs[lo:hi], args, D)
     return {
         "metric": "Jacobian evals/sec", "value": round(value, 2), "unit": "jacobians/s",
-        "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "n_gpus": D.world, "steps": steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic ba20-shaped problem, seed 3",
-        "config": {"workload": "ba20_jacobian", "n_cams": BA_N, "n_pts": BA_M, "n_obs": p_total,
-                   "per_rank": p, "parallelism": f"shard{D.world}",
-                   "l2": "256 MiB L2 flush before every timed launch; per-launch CUDA events"},
+        "config": ba_config(p_total, D.world),
         "obs_per_s": round(p_total / (ms_step * 1e-3), 1),
-        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
-        "failed_per_step": n_failed // args.steps, "parity_sample": parity,
+        "roofline": roof, "e2e": e2e, "gpu_launches": steps, "clocks": clocks,
+        "failed_per_step": n_failed // steps, "parity_sample": parity,
         "objective_only": objective, "csr_jacobian": csr,
     }
 
@@ -706,22 +772,24 @@ def gmm_flops(d, K, N, w):
         2.0 * N * w["log"]
 
 
-def run_gmm_ours(args, D):
-    import torch
+def gmm_data(seed):
+    return (f"synthetic SURVEY §8(d): alphas~N(0,1), means~U(0,1), icf~N(0,1), x~U(0,1), "
+            f"gamma=1, m=0, seed {seed}")
 
-    from paper_2003_04617_b200 import _native, kernels
-    dev = torch.device("cuda", D.local)
-    torch.cuda.set_device(dev)
-    d, K, N, seed = GMM_CFG[args.workload]
-    N = args.n or N
-    gamma, m = 1.0, 0
-    cst = gmm_constants(d, K, N, gamma, m)
+
+def gmm_config(d, K, N, world):
+    return {"workload": f"gmm_d{d}_K{K}_N{N}", "d": d, "K": K, "N": N,
+            "per_rank": N // world,
+            "parallelism": "dp1" if world == 1 else f"dp{world}+allreduce",
+            "l2": "256 MiB L2 flush before every evaluation"}
+
+
+def gmm_inputs(torch, d, K, N, seed, lo, hi, dev):
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     alphas = torch.randn(K, dtype=torch.float64, device=dev, generator=g)
     means = torch.rand((K, d), dtype=torch.float64, device=dev, generator=g)
-    icf = torch.randn((K, d * (d + 1) // 2), dtype=torch.float64, device=dev, generator=g) * 0.5
-    lo, hi = N * D.rank // D.world, N * (D.rank + 1) // D.world
+    icf = torch.randn((K, d * (d + 1) // 2), dtype=torch.float64, device=dev, generator=g)
     x = torch.empty((hi - lo, d), dtype=torch.float64, device=dev)
     # the rank's slice of one global x ~ U(0,1) (generated in 1M-row pieces)
     gx = torch.Generator(device=dev)
@@ -734,38 +802,63 @@ def run_gmm_ours(args, D):
         if a < b:
             x[a - lo:b - lo] = blk[a - row:b - row]
         row += n
+    return alphas, means, icf, x
+
+
+def run_gmm_ours(args, D, wl):
+    """One GMM config.  One GPU: the drop-in gradient() of the whole problem
+    (rl_gmm_gradient_f64: err! in the program's order and the primal-
+    restoration verdict, k_gmm_restore beside k_gmm_rev).  N GPUs: each rank
+    the shard entry over its points (rl_gmm_grad_f64), then ONE NCCL
+    all_reduce(sum) of the packed [err, g_alphas, g_means, g_icf] vector."""
+    import torch
+
+    from paper_2003_04617_b200 import _native, kernels
+    dev = torch.device("cuda", D.local)
+    torch.cuda.set_device(dev)
+    d, K, N, seed = GMM_CFG[wl]
+    N = args.n if (args.n and args.workload == wl) else N
+    gamma, m = 1.0, 0
+    cst = gmm_constants(d, K, N, gamma, m)
+    lo, hi = N * D.rank // D.world, N * (D.rank + 1) // D.world
+    alphas, means, icf, x = gmm_inputs(torch, d, K, N, seed, lo, hi, dev)
     L = _native.lib()
     ws = torch.empty(max(1, L.rl_gmm_workspace_bytes(d, K, hi - lo)), dtype=torch.uint8, device=dev)
     counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    single = D.dist is None
 
     def step():
+        if single:
+            return kernels.gmm_gradient(alphas, means, icf, x, gamma, m, cst, workspace=ws,
+                                        counters=counters)
         r = kernels.gmm_grad(alphas, means, icf, x, gamma, m, cst, N_total=N,
                              add_param_terms=(D.rank == 0), workspace=ws, counters=counters)
-        if D.dist is not None:
-            D.dist.all_reduce(r.packed)        # the one collective: parameter adjoints
+        D.dist.all_reduce(r.packed)            # the one collective: parameter adjoints
         return r
 
     for _ in range(max(args.warmup, 3)):
         r = step()
     torch.cuda.synchronize()
-    # the step's launches (prep, fwd, lse, rev, final) are
-    # replayed as one CUDA graph: no per-launch host latency between them
+    # the step's launches (prep, fwd, lse, rev || restore, final) are replayed
+    # as one CUDA graph: no per-launch host latency between them
     graph = None
-    if not args.no_graph and D.dist is None:
+    if not args.no_graph and single:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             r = step()
         graph.replay()
         torch.cuda.synchronize()
     run_step = graph.replay if graph is not None else step
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    steps = steps_for(D.max(time_device(run_step, 2, flush)), args)
+    counters.zero_()
     props = torch.cuda.get_device_properties(dev)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}")
     sampler.start()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     D.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     for a, b in evs:
         flush.fill_(1)                      # evict L2 between evaluations
         a.record(stream)
@@ -774,8 +867,9 @@ def run_gmm_ours(args, D):
     torch.cuda.synchronize()
     D.barrier()
     clocks = sampler.stop()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     ms_step = D.max(ms)
+    n_failed = D.sum(int(counters[1].item())) // steps
     w = load_weights()
     # GMM's mat-vec work runs on the FP64 tensor cores: the roofline peak is
     # the larger of the measured DMMA and DFMA peaks (the DMMA one)
@@ -791,60 +885,43 @@ def run_gmm_ours(args, D):
                 "peak": round(peak, 3), "unit": "TFLOP/s",
                 "frac": round(fl / (ms_step * 1e-3) / 1e12 / peak, 4),
                 # DRAM bytes of one evaluation's kernels (ncu capture at configs[2] only)
-                "traffic": gmm_traffic() if args.workload == "gmm" else None,
+                "traffic": gmm_traffic() if wl == "gmm" else None,
                 "flops_per_eval_survey_W": fl,
                 "mat_vec_flops_executed": executed,
                 "executed_frac": round(executed / (ms_step * 1e-3) / 1e12 / peak, 4),
+                "frac_note": "frac credits SURVEY §8(d)'s W (4 mat-vec passes per point and "
+                             "component); executed_frac the 3 passes the kernels execute",
                 "peak_source": "max of in-run DMMA m16n8k16 (%.1f TF) and DFMA (%.1f TF) "
                                "microkernels (tools/fp64probe.cu)" % (dmma, dfma)}
     o_ms = D.max(time_device(
         lambda: kernels.gmm_objective(alphas, means, icf, x, gamma, m, cst, N_total=N,
                                       add_param_terms=(D.rank == 0), workspace=ws),
-        max(2, args.steps // 2), flush))
+        max(2, min(args.steps // 2, 10)), flush))
     objective = {"ms_per_step": round(o_ms, 4), "grad_over_objective": round(ms_step / o_ms, 3),
                  "kernel": "k_gmm_prep/fwd/lse/err (rl_gmm_objective_f64)"}
-    parity = None
-    if D.rank == 0 and args.workload == "gmm" and D.world == 1:
-        sys.path.insert(0, os.path.join(REPO, "oracle"))
-        import oracle as O
-        t0 = time.perf_counter()
-        # tol 1e-6: at N=1e4 the reference's err! restoration check fails at 1e-9
-        rc, e, ga, gm, gi = O.gmm_grad(alphas.cpu().numpy(), means.cpu().numpy(),
-                                       icf.cpu().numpy(), x.cpu().numpy(), gamma, m, cst,
-                                       tol=1e-6)
-        dt_cpu = time.perf_counter() - t0
-        rel = lambda a, b: float(np.max(np.abs(a - b)) / np.max(np.abs(b)))  # noqa: E731
-        parity = {"oracle_rc": rc, "rel_err": abs(float(r.err.item()) - e) / abs(e),
-                  "max_rel_alphas": rel(r.g_alphas.cpu().numpy(), ga),
-                  "max_rel_means": rel(r.g_means.cpu().numpy(), gm),
-                  "max_rel_icf": rel(r.g_icf.cpu().numpy(), gi), "oracle_s": round(dt_cpu, 2)}
+    restore = None
+    if single:
+        restore = {"resid": float(r.resid.item()), "restore_code": int(r.restore_code.item()),
+                   "tol": 1e-9, "kernel": "k_gmm_restore (err! chain replayed bit-exactly, "
+                                         "side stream beside k_gmm_rev)"}
     res = {
         "metric": "gradient evals/sec", "value": round(1e3 / ms_step, 3), "unit": "evals/s",
-        "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "n_gpus": D.world, "steps": steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic alphas~N(0,1), means~U(0,1), icf~N(0,.5^2), x~U(0,1), seed {seed}",
-        "config": {"workload": f"gmm_d{d}_K{K}_N{N}", "d": d, "K": K, "N": N,
-                   "cuda_graph": graph is not None,
-                   "per_rank": hi - lo, "parallelism": f"dp{D.world}+allreduce",
-                   "l2": "256 MiB L2 flush before every evaluation"},
-        "roofline": roof, "gpu_launches": 5 * args.steps, "clocks": clocks,
-        "failed_per_step": D.sum(int(counters[1].item())) // (args.steps + max(args.warmup, 3)),
-        "parity_sample": parity, "objective_only": objective,
+        "vs_baseline": None, "dtype": "f64", "data": gmm_data(seed),
+        "config": dict(gmm_config(d, K, N, D.world), cuda_graph=graph is not None),
+        "roofline": roof, "gpu_launches": (6 if single else 5) * steps, "clocks": clocks,
+        "failed_per_step": n_failed, "objective_only": objective, "restoration": restore,
     }
-    if not args.no_e2e and D.world == 1:
+    if not args.no_e2e and single:
         res["e2e"] = gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D)
-    if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline and parity is not None:
-        res["cpu_baseline"] = {"value": round(1.0 / parity["oracle_s"], 5), "unit": "evals/s",
-                               "cores": 1, "kind": "port",
-                               "sample": f"one full evaluation (N={N}) of the sequential oracle "
-                                         "(all 4 reference sweeps, 8 mat-vec passes per point "
-                                         "and component; scratch shared across points, so it "
-                                         "does not parallelise)"}
     return res
 
 
 def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
+    """The drop-in gradient through the C-ABI host-buffer entry
+    (rl_gmm_gradient_f64_host): pinned host inputs up, the packed gradient
+    and the restoration residual down, inside the timed region."""
     import ctypes
 
     import torch
@@ -857,106 +934,183 @@ def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
     hx = x.cpu().pin_memory()
     out = torch.empty(1 + K + K * d + K * d * (d + 1) // 2, dtype=torch.float64).pin_memory()
     nf = ctypes.c_ulonglong()
+    resid = ctypes.c_double()
 
     def call():
-        rc = L.rl_gmm_grad_f64_host(d, K, N, ha.data_ptr(), hm.data_ptr(), hi_.data_ptr(),
-                                    hx.data_ptr(), gamma, m, cst, 1e-9, 1, out.data_ptr(),
-                                    ctypes.byref(nf), D.local)
-        _native.check(rc, "rl_gmm_grad_f64_host")
-    for _ in range(3):
-        call()
-    steps = 50                           # ~0.6 ms per call: a stable mean costs nothing
+        rc = L.rl_gmm_gradient_f64_host(d, K, N, ha.data_ptr(), hm.data_ptr(), hi_.data_ptr(),
+                                        hx.data_ptr(), gamma, m, cst, 0.0, 1e-9, 1,
+                                        out.data_ptr(), ctypes.byref(resid), ctypes.byref(nf),
+                                        D.local)
+        if _native.check(rc, "rl_gmm_gradient_f64_host") not in (0, 5):
+            raise RuntimeError(f"rl_gmm_gradient_f64_host: status {rc}")
+    call()
+    t0 = time.perf_counter()
+    call()
+    one = time.perf_counter() - t0
+    steps = int(min(50, max(3, 0.3 // max(one, 1e-6))))
     t0 = time.perf_counter()
     for _ in range(steps):
         call()
     dt = (time.perf_counter() - t0) / steps
     return {"value": round(1.0 / dt, 3), "unit": "evals/s", "calls_timed": steps,
             "h2d_bytes_per_step": int(hx.numel() * 8 + (ha.numel() + hm.numel() + hi_.numel()) * 8),
-            "d2h_bytes_per_step": int(out.numel() * 8), "ms_per_step": round(dt * 1e3, 3),
-            "path": "rl_gmm_grad_f64_host (pinned host buffers; device buffers and workspace "
+            "d2h_bytes_per_step": int(out.numel() * 8 + 32), "ms_per_step": round(dt * 1e3, 3),
+            "path": "rl_gmm_gradient_f64_host (pinned host buffers; device buffers and workspace "
                     "carved from a per-thread cached arena, cached streams)"}
 
 
-def gmm_cpu(workload):
-    """One full gradient evaluation of configs[2] on the sequential C oracle
-    (all four reference sweeps; the reference's shared scratch makes the
-    points sequential, so one thread)."""
+def gmm_cpu(wl, N_full, target_s=1.0):
+    """The sequential C oracle (all four reference sweeps, scratch shared
+    across points: one thread) on the first N_sub points of the config's
+    inputs, N_sub grown until ~target_s; evals/s extrapolated linearly in N
+    (the per-point work is the same for every point)."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as O
-    d, K, N, seed = GMM_CFG["gmm"]
+    d, K, _, seed = GMM_CFG[wl]
     rng = np.random.default_rng(seed)
     alphas = rng.standard_normal(K)
     means = rng.random((K, d))
-    icf = rng.standard_normal((K, d * (d + 1) // 2)) * 0.5
-    x = rng.random((N, d))
-    cst = gmm_constants(d, K, N, 1.0, 0)
-    t0 = time.perf_counter()
-    O.gmm_grad(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
-    dt = time.perf_counter() - t0
-    return {"value": round(1.0 / dt, 5), "unit": "evals/s", "cores": 1, "kind": "port",
-            "sample": f"one full evaluation of configs[2] (d={d}, K={K}, N={N}) on the sequential "
-                      f"oracle (oracle/revoracle.c), {dt:.2f} s"}
+    icf = rng.standard_normal((K, d * (d + 1) // 2))
+    n = 8
+    while True:
+        x = rng.random((n, d))
+        cst = gmm_constants(d, K, n, 1.0, 0)
+        t0 = time.perf_counter()
+        O.gmm_grad(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= N_full:
+            break
+        n = min(N_full, max(2 * n, int(n * target_s / max(dt, 1e-4))))
+    per_eval = dt * N_full / n
+    return {"value": round(1.0 / per_eval, 8), "unit": "evals/s", "cores": 1, "kind": "port",
+            "sample": f"{n} of the {N_full} points (d={d}, K={K}) through the sequential oracle "
+                      f"(oracle/revoracle.c, all 4 reference sweeps, 8 mat-vec passes per point "
+                      f"and component) in {dt:.2f} s, extrapolated linearly to N={N_full}",
+            "extrapolated": n < N_full}
 
 
 # ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks (one per GPU) and pass its output
+    through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_line(args, D):
+    """--dry-run: the ours-arm line's plumbing without kernels (CPU tests)."""
+    t0 = time.perf_counter()
+    D.barrier()
+    ms = D.max((time.perf_counter() - t0) * 1e3 / max(args.steps, 1) + 1e-3 * (D.rank + 1))
+    return {"metric": "gradient evals/sec", "value": None, "unit": "grads/s",
+            "n_gpus": D.world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "dry run (no kernels)",
+            "config": bessel_config(args.n or BESSEL_N, D.world), "dry_run": True,
+            "ranks_reporting": int(D.sum(1)), "dist": D.nccl_info()}
+
+
+def reference_arm(args, world):
+    """The reference algorithm's CPU implementation (the oracle port) on the
+    same workloads / configs as the ours arm; bounded samples."""
+    # all host threads for the oracle port (torchrun exports OMP_NUM_THREADS=1;
+    # libgomp reads it when liboracle.so loads, which happens below)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    tgt = max(2.0, min(20.0, 0.5 * args.steps))
+    common = {"n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+              "higher_is_better": True, "vs_baseline": None, "dtype": "f64", "impl": "reference",
+              "rate_sample": True}
+
+    def line(metric, base, unit, data, config):
+        r = {"metric": metric, "value": base["value"], "unit": unit,
+             "ms_per_step": round(1e3 / base["value"], 3) if unit != "grads/s" else
+             round(1e3 * config["n_total"] / base["value"], 3),
+             "scaling": "strong", "data": data, "config": config, "cpu_baseline": base,
+             "e2e": {"value": base["value"], "unit": unit, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0}}
+        r.update(common)
+        return r
+
+    def bessel():
+        return line("gradient evals/sec", bessel_cpu(target_s=tgt), "grads/s",
+                    "synthetic z ~ U(0.1, 10), seed 1", bessel_config(args.n or BESSEL_N, world))
+
+    def ba():
+        return line("Jacobian evals/sec", ba_cpu(target_s=tgt), "jacobians/s",
+                    "synthetic ba20-shaped problem, seed 3", ba_config(args.n or BA_P, world))
+
+    def gmm(wl):
+        d, K, N, seed = GMM_CFG[wl]
+        N = args.n or N
+        return line("gradient evals/sec", gmm_cpu(wl, N), "evals/s", gmm_data(seed),
+                    gmm_config(d, K, N, world))
+
+    if args.workload == "all":
+        res = bessel()
+        res["ba"] = ba()
+        res["gmm_c3"] = gmm("gmm")
+        res["gmm_c5"] = gmm("gmm_large")
+        return res
+    if args.workload == "bessel":
+        return bessel()
+    if args.workload == "ba":
+        return ba()
+    return gmm(args.workload)
+
+
 def main():
     args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         if rank != 0:
             return 0
-        # all host threads for the oracle port (torchrun exports OMP_NUM_THREADS=1;
-        # libgomp reads it when liboracle.so loads, which happens below)
-        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
-        if args.workload == "gmm_large":
-            print(json.dumps({"impl": "reference", "unavailable":
-                              "configs[4] on the sequential CPU oracle is ~13 core-years per "
-                              "evaluation (SURVEY.md §8(d)); timed at configs[2] instead"}))
-            return 0
-        if args.workload == "bessel":
-            base = bessel_cpu(target_s=max(2.0, min(20.0, 0.5 * args.steps)))
-            res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "grads/s",
-                   "ms_per_step": round(1e3 * (args.n or BESSEL_N) / base["value"], 3),
-                   "scaling": "strong", "data": "synthetic z ~ U(0.1, 10), seed 1",
-                   "config": {"workload": "bessel_j2_grad_2^26", "n_total": args.n or BESSEL_N,
-                              "nu": BESSEL_NU, "thr": THR}}
-        elif args.workload == "ba":
-            base = ba_cpu(target_s=max(2.0, min(20.0, 0.5 * args.steps)))
-            res = {"metric": "Jacobian evals/sec", "value": base["value"], "unit": "jacobians/s",
-                   "ms_per_step": round(1e3 / base["value"], 3), "scaling": "strong",
-                   "data": "synthetic ba20-shaped problem, seed 3",
-                   "config": {"workload": "ba20_jacobian", "n_cams": BA_N, "n_pts": BA_M,
-                              "n_obs": BA_P}}
-        else:
-            base = gmm_cpu(args.workload)
-            res = {"metric": "gradient evals/sec", "value": base["value"], "unit": "evals/s",
-                   "ms_per_step": round(1e3 / base["value"], 3), "scaling": "strong",
-                   "data": "synthetic, seed 2",
-                   "config": {"workload": "gmm_d64_K25_N1e4_grad"}}
-        res.update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                    "higher_is_better": True, "vs_baseline": None, "dtype": "f64",
-                    "impl": "reference", "cpu_baseline": base,
-                    "e2e": {"value": base["value"], "unit": base["unit"],
-                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
-        print(json.dumps(res))
+        print(json.dumps(reference_arm(args, world)))
         return 0
 
-    D = Dist("nccl")
-    if args.workload == "bessel":
-        res = run_bessel_ours(args, D)
-        if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
-            res["cpu_baseline"] = bessel_cpu()
-    elif args.workload == "ba":
-        res = run_ba_ours(args, D)
-        if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
-            res["cpu_baseline"] = ba_cpu()
-    elif args.workload in GMM_CFG:
-        res = run_gmm_ours(args, D)
+    D = Dist("gloo" if args.dry_run else "nccl")
+    if args.dry_run:
+        res = dry_line(args, D)
     else:
-        raise SystemExit(f"workload {args.workload} not wired yet")
+        cpu = D.rank == 0 and D.world == 1 and not args.no_cpu_baseline
+        if args.workload in ("all", "bessel"):
+            res = run_bessel_ours(args, D)
+            if cpu:
+                res["cpu_baseline"] = bessel_cpu()
+        if args.workload in ("all", "ba"):
+            r = run_ba_ours(args, D)
+            if cpu:
+                r["cpu_baseline"] = ba_cpu()
+            res = r if args.workload == "ba" else res
+            if args.workload == "all":
+                res["ba"] = r
+        for wl, key in (("gmm", "gmm_c3"), ("gmm_large", "gmm_c5")):
+            if args.workload in ("all", wl):
+                r = run_gmm_ours(args, D, wl)
+                if cpu:
+                    r["cpu_baseline"] = gmm_cpu(wl, r["config"]["N"])
+                if args.workload == "all":
+                    res[key] = r
+                else:
+                    res = r
+        res["dist"] = D.nccl_info()
     if D.rank == 0:
         print(json.dumps(res))
     D.close()

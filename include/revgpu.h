@@ -136,6 +136,56 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          unsigned long long *n_failed, int32_t device);
 
 /* ------------------------------------------------------------------------
+ * The whole gradient() call of gmm on one device, in the reference's order:
+ * replaces gradient(p, GradRequest("gmm", [err0, alphas, means, icf, x,
+ *   zeros..., gamma, m, cst], wrt=["alphas","means","icf"])) (autodiff.py:
+ * 136-180) including its primal-restoration check (autodiff.py:169-172).
+ * out[0] = err! after the forward run, accumulated from err0 term by term in
+ * the program's order (bit-exactly the sequential binary64 chain over the
+ * device's per-point terms; see rl_seq_sum_f64); out[1..] = the cotangents
+ * as rl_gmm_grad_f64.  resid (device, 1 double, may be NULL) = err! after
+ * the gradient sweep; restore_code (device, int32, may be NULL) =
+ * RL_ERR_RESTORE when |resid - err0| > tol (values_close, values.py:562-589;
+ * unconditional in the reference: independent of invcheck), else RL_OK.
+ * Per-point errors still go to fail / counters and take precedence (the
+ * reference raises them before the restoration check).  d <= 128.
+ * Workspace: rl_gmm_workspace_bytes(d, K, N).
+ *
+ * rl_gmm_run_f64 replaces run(p, "gmm", [err0, ...]) (direction +1,
+ * interpreter.py:1021) or uncall(...) (direction -1, :1026): err[0] = err!
+ * after the forward (inverse) program, accumulated from err0 in its order.
+ * rl_gmm_gradient_f64_host: host buffers; returns RL_ERR_RESTORE (outputs
+ * written, *resid set) when the restoration check fails.
+ * ---------------------------------------------------------------------- */
+int rl_gmm_gradient_f64(int32_t d, int32_t K, int64_t N, const double *alphas,
+                        const double *means, const double *icf, const double *x, double gamma,
+                        int32_t m, double cst, double err0, double tol, int32_t invcheck,
+                        double *out, double *resid, int32_t *restore_code, uint8_t *fail,
+                        unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
+int rl_gmm_run_f64(int32_t d, int32_t K, int64_t N, const double *alphas, const double *means,
+                   const double *icf, const double *x, double gamma, int32_t m, double cst,
+                   double err0, double tol, int32_t invcheck, int32_t direction, double *err,
+                   uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
+                   void *stream);
+int rl_gmm_gradient_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                             const double *means, const double *icf, const double *x,
+                             double gamma, int32_t m, double cst, double err0, double tol,
+                             int32_t invcheck, double *out, double *resid,
+                             unsigned long long *n_failed, int32_t device);
+
+/* ------------------------------------------------------------------------
+ * Sequential binary64 accumulation e_{j+1} = fl(e_j + t_j), j < M, from e0
+ * (the reference's `acc += term` statement chain, numerics.py:296-339),
+ * evaluated in parallel by one CTA and verified bit-exact against the
+ * sequential definition (falls back to it when the verification fails).
+ * out2 (device, 2 doubles) = [e_mark, e_M]; verified (device int32, may be
+ * NULL) = 1 when the parallel path verified.  force_serial = 1 runs the
+ * sequential loop (tests).  t: device, M doubles.
+ * ---------------------------------------------------------------------- */
+int rl_seq_sum_f64(const double *t, int64_t M, double e0, int64_t mark, int32_t force_serial,
+                   double *out2, int32_t *verified, void *stream);
+
+/* ------------------------------------------------------------------------
  * run / uncall / objective-only ("-O") entries: the primal sweeps of the same
  * programs with every reversibility check, no cotangents.
  *

@@ -69,6 +69,12 @@ def lib():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
             _c_double_p, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
             ctypes.c_int, _c_double_p, _c_double_p, _c_double_p, _c_double_p]
+        L.orc_gmm_grad_ex.restype = ctypes.c_int
+        L.orc_gmm_grad_ex.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
+            _c_double_p, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_int, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
+            _c_double_p, _c_double_p]
         _lib = L
     return _lib
 
@@ -141,6 +147,30 @@ def gmm_grad(alphas, means, icf, x, gamma, m, cst, tol=1e-9, invcheck=True):
                             int(m), float(cst), tol, int(bool(invcheck)), ctypes.byref(err),
                             _dp(ga), _dp(gm), _dp(gi))
     return rc, err.value, ga, gm, gi
+
+
+def gmm_grad_ex(alphas, means, icf, x, gamma, m, cst, err0=0.0, tol=1e-9, invcheck=True,
+                fresh=False):
+    """gradient with err! = err0 on entry: returns (rc, err, resid, g_alphas,
+    g_means, g_icf); resid = err! after the gradient sweep (what the
+    reference's restoration check compares with err0, autodiff.py:169-172),
+    reported whether or not that check passes (rc 5 = RevError).
+    fresh=True is NOT the reference: scratch zeroed per (point, component),
+    the device's semantics, to pin the device's verdict."""
+    alphas, means, icf, x = _f64(alphas), _f64(means), _f64(icf), _f64(x)
+    K, d = means.shape
+    N = x.shape[0]
+    err = ctypes.c_double(np.nan)
+    resid = ctypes.c_double(np.nan)
+    ga = np.zeros(K)
+    gm = np.zeros((K, d))
+    gi = np.zeros(icf.shape)
+    rc = lib().orc_gmm_grad_ex(d, K, N, _dp(alphas), _dp(means), _dp(icf), _dp(x),
+                               float(gamma), int(m), float(cst), float(err0), tol,
+                               int(bool(invcheck)), int(bool(fresh)), ctypes.byref(err),
+                               ctypes.byref(resid),
+                               _dp(ga), _dp(gm), _dp(gi))
+    return rc, err.value, resid.value, ga, gm, gi
 
 
 def ba_sparse(n_cams, n_pts, obs, J31):

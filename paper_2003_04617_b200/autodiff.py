@@ -261,18 +261,23 @@ def _grad_gmm(fdef, req, opts):
             raise KindError("only the err! output can be seeded on the device path")
     dev = _device()
     t = lambda v: torch.as_tensor(v, device=dev)  # noqa: E731
-    r = kernels.gmm_grad(t(al), t(mu), t(ic), t(xv), float(ga), int(wm), float(cst),
-                         tol=opts.float_tolerance, invcheck=opts.invcheck)
+    r = kernels.gmm_gradient(t(al), t(mu), t(ic), t(xv), float(ga), int(wm), float(cst),
+                             err0=float(err0), tol=opts.float_tolerance, invcheck=opts.invcheck)
     fails = r.fail.cpu().numpy()
     if fails.any():
         raise error_for_code(int(fails[np.nonzero(fails)[0][0]]), "gmm")
-    E = float(r.err.item())
+    # the reference's primal-restoration check (autodiff.py:169-172), decided
+    # on the device from err! after the gradient sweep (k_gmm_restore)
+    code = int(r.restore_code.item())
+    if code:
+        raise error_for_code(code, "gmm")
+    E = float(r.err.item())             # err! from err0, in the program's order
     grads_all = {names[0]: a,
                  names[1]: like(alphas, a * r.g_alphas.cpu().numpy()),
                  names[2]: like(means, a * r.g_means.cpu().numpy()),
                  names[3]: like(icf, a * r.g_icf.cpu().numpy())}
     report = _report(req.wrt, names, grads_all)
-    primal = [float(err0) + E] + list(req.args[1:])
+    primal = [E] + list(req.args[1:])
     return primal, {p: grads_all[p] for p in report}
 
 

@@ -30,7 +30,9 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
                const double *means, const double *icf, const double *x, double gamma, int32_t m,
                double cst, double tol, int32_t invcheck, int32_t add_param_terms, double *out,
                uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
-               cudaStream_t st, int grad);
+               cudaStream_t st, int grad, const GmmSeq *seq);
+int launch_seq_sum(const double *t, int64_t M, double e0, int64_t mark, int32_t force_serial,
+                   double *out2, int32_t *verified, cudaStream_t st);
 int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, double tol,
                        int64_t max_trips, int32_t invcheck, int32_t direction,
                        const double *out_in, double *out, uint8_t *fail,
@@ -468,7 +470,35 @@ int rl_gmm_grad_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const doub
                     int32_t add_param_terms, double *out, uint8_t *fail,
                     unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
   return launch_gmm(d, K, N, N_total, alphas, means, icf, x, gamma, m, cst, tol, invcheck,
-                    add_param_terms, out, fail, counters, ws, ws_bytes, as_stream(stream), 1);
+                    add_param_terms, out, fail, counters, ws, ws_bytes, as_stream(stream), 1,
+                    nullptr);
+}
+
+int rl_gmm_gradient_f64(int32_t d, int32_t K, int64_t N, const double *alphas,
+                        const double *means, const double *icf, const double *x, double gamma,
+                        int32_t m, double cst, double err0, double tol, int32_t invcheck,
+                        double *out, double *resid, int32_t *restore_code, uint8_t *fail,
+                        unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
+  const GmmSeq seq{err0, resid, restore_code, nullptr, 0, 1};
+  return launch_gmm(d, K, N, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, 1, out, fail,
+                    counters, ws, ws_bytes, as_stream(stream), 1, &seq);
+}
+
+int rl_gmm_run_f64(int32_t d, int32_t K, int64_t N, const double *alphas, const double *means,
+                   const double *icf, const double *x, double gamma, int32_t m, double cst,
+                   double err0, double tol, int32_t invcheck, int32_t direction, double *err,
+                   uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
+                   void *stream) {
+  if (direction != 1 && direction != -1)
+    return set_error(RL_ERR_INVALID, "rl_gmm_run_f64: direction must be +1 or -1");
+  const GmmSeq seq{err0, nullptr, nullptr, nullptr, 0, direction};
+  return launch_gmm(d, K, N, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, 1, err, fail,
+                    counters, ws, ws_bytes, as_stream(stream), 0, &seq);
+}
+
+int rl_seq_sum_f64(const double *t, int64_t M, double e0, int64_t mark, int32_t force_serial,
+                   double *out2, int32_t *verified, void *stream) {
+  return launch_seq_sum(t, M, e0, mark, force_serial, out2, verified, as_stream(stream));
 }
 
 int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
@@ -477,7 +507,8 @@ int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const
                          int32_t add_param_terms, double *err, uint8_t *fail,
                          unsigned long long *counters, void *ws, size_t ws_bytes, void *stream) {
   return launch_gmm(d, K, N, N_total, alphas, means, icf, x, gamma, m, cst, tol, invcheck,
-                    add_param_terms, err, fail, counters, ws, ws_bytes, as_stream(stream), 0);
+                    add_param_terms, err, fail, counters, ws, ws_bytes, as_stream(stream), 0,
+                    nullptr);
 }
 
 int rl_besselj_run_f64(int32_t nu, const double *z, int64_t n, double thr, double tol,
@@ -604,10 +635,14 @@ int rl_ba_jac_csr_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const d
   return RL_OK;
 }
 
-int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+// host-buffer GMM gradient; with `restore` the drop-in gradient() of
+// rl_gmm_gradient_f64 (err! in the reference's order from err0, restoration
+// verdict as the return code), else rl_gmm_grad_f64's
+static int gmm_grad_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          const double *means, const double *icf, const double *x, double gamma,
                          int32_t m, double cst, double tol, int32_t invcheck, double *out,
-                         unsigned long long *n_failed, int32_t device) {
+                         unsigned long long *n_failed, int32_t device, bool restore, double err0,
+                         double *resid) {
   if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || (N > 0 && !x) || !out)
     return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64_host: bad argument");
   Pipeline pl;
@@ -617,20 +652,10 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
   const size_t P = (size_t)d * (d + 1) / 2;
   const size_t nout = 1 + K + (size_t)K * d + (size_t)K * P;
   const size_t wsb = gmm_workspace_bytes(d, K, N);
-#ifndef GMM_HOST_ARENA
-#define GMM_HOST_ARENA 1
-#endif
-#if !GMM_HOST_ARENA
-  DevBuf da, dm, di, dx, dout, dfl, dws, dc;
-  if ((rc = da.alloc(K * 8, st)) || (rc = dm.alloc((size_t)K * d * 8, st)) ||
-      (rc = di.alloc((size_t)K * P * 8, st)) || (rc = dx.alloc((size_t)N * d * 8, st)) ||
-      (rc = dout.alloc(nout * 8, st)) || (rc = dfl.alloc(N, st)) || (rc = dws.alloc(wsb, st)) ||
-      (rc = dc.alloc(16, st)))
-    return rc;
-#else
   // one cached device arena per (thread, device), carved 256-byte aligned
+  // (the counters piece also holds the restoration residual and verdict)
   const size_t sizes[8] = {(size_t)K * 8, (size_t)K * d * 8, (size_t)K * P * 8,
-                           (size_t)N * d * 8, nout * 8, (size_t)std::max<int64_t>(N, 1), wsb, 16};
+                           (size_t)N * d * 8, nout * 8, (size_t)std::max<int64_t>(N, 1), wsb, 32};
   size_t total = 0;
   for (size_t b : sizes) total += (b + 255) & ~size_t(255);
   void *base = nullptr;
@@ -642,7 +667,6 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
     pieces[q]->p = (char *)base + off;
     off += (sizes[q] + 255) & ~size_t(255);
   }
-#endif
   if ((rc = cuda_status(cudaMemcpyAsync(da.p, alphas, K * 8, cudaMemcpyHostToDevice, st), "H2D")) ||
       (rc = cuda_status(cudaMemcpyAsync(dm.p, means, (size_t)K * d * 8, cudaMemcpyHostToDevice, st),
                         "H2D")) ||
@@ -650,20 +674,45 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                         "H2D")) ||
       (rc = cuda_status(cudaMemcpyAsync(dx.p, x, (size_t)N * d * 8, cudaMemcpyHostToDevice, st),
                         "H2D")) ||
-      (rc = cuda_status(cudaMemsetAsync(dc.p, 0, 16, st), "memset")))
+      (rc = cuda_status(cudaMemsetAsync(dc.p, 0, 32, st), "memset")))
     return rc;
+  unsigned long long *dcnt = (unsigned long long *)dc.p;
+  const GmmSeq seq{err0, (double *)(dcnt + 2), (int *)(dcnt + 3), nullptr, 0, 1};
   if ((rc = launch_gmm(d, K, N, N, (double *)da.p, (double *)dm.p, (double *)di.p,
                        (double *)dx.p, gamma, m, cst, tol, invcheck, 1, (double *)dout.p,
-                       (uint8_t *)dfl.p, (unsigned long long *)dc.p, dws.p, wsb, st, 1)))
+                       (uint8_t *)dfl.p, dcnt, dws.p, wsb, st, 1, restore ? &seq : nullptr)))
     return rc;
-  unsigned long long h[2];
+  unsigned long long h[4];
   if ((rc = cuda_status(cudaMemcpyAsync(out, dout.p, nout * 8, cudaMemcpyDeviceToHost, st),
                         "D2H out")) ||
-      (rc = cuda_status(cudaMemcpyAsync(h, dc.p, 16, cudaMemcpyDeviceToHost, st), "D2H counters")))
+      (rc = cuda_status(cudaMemcpyAsync(h, dc.p, 32, cudaMemcpyDeviceToHost, st), "D2H counters")))
     return rc;
   if ((rc = pl.finish())) return rc;
   if (n_failed) *n_failed = h[1];
-  return RL_OK;
+  if (!restore) return RL_OK;
+  double r;
+  int code;
+  memcpy(&r, &h[2], 8);
+  memcpy(&code, &h[3], 4);
+  if (resid) *resid = r;
+  return h[1] ? RL_OK : code;   // per-point errors take precedence (fail flags)
+}
+
+int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                         const double *means, const double *icf, const double *x, double gamma,
+                         int32_t m, double cst, double tol, int32_t invcheck, double *out,
+                         unsigned long long *n_failed, int32_t device) {
+  return gmm_grad_host(d, K, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
+                       n_failed, device, false, 0.0, nullptr);
+}
+
+int rl_gmm_gradient_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                             const double *means, const double *icf, const double *x,
+                             double gamma, int32_t m, double cst, double err0, double tol,
+                             int32_t invcheck, double *out, double *resid,
+                             unsigned long long *n_failed, int32_t device) {
+  return gmm_grad_host(d, K, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
+                       n_failed, device, true, err0, resid);
 }
 
 }  // extern "C"

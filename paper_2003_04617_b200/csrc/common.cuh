@@ -41,6 +41,17 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs of the current device (cached per device).
 int sm_count();
 
+// GMM: err! accumulated in the reference's order from err0, and (gradient)
+// the primal-restoration residual and verdict (gmm.cu, k_gmm_restore)
+struct GmmSeq {
+  double err0;
+  double *resid;     // device, 1 double (or null)
+  int *code;         // device, 1 int32 (or null): RL_OK / RL_ERR_RESTORE
+  int *verified;     // device, 1 int32 (or null): 1 = the parallel evaluation verified
+  int force_serial;  // tests: take the sequential fallback
+  int direction;     // objective only: +1 run, -1 uncall (~gmm)
+};
+
 // Block-wide sum of two counters and one atomicAdd per block.
 template <int BLOCK>
 __device__ __forceinline__ void block_add_counters(unsigned long long a, unsigned long long b,

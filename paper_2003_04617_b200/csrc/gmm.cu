@@ -42,6 +42,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "seqsum.cuh"
 
 namespace rl {
 
@@ -453,7 +454,7 @@ constexpr int LSE_THREADS = 64;   // points per k_gmm_lse block: N/64 blocks spr
 __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
-    uint8_t *__restrict__ fail, unsigned long long *counters) {
+    double *__restrict__ terms, uint8_t *__restrict__ fail, unsigned long long *counters) {
   pdl_wait();
 
   const long long i = (long long)blockIdx.x * LSE_THREADS + threadIdx.x;
@@ -486,7 +487,12 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
       se = se + exp(t);
     }
     if (!(se > 0.0)) code = RL_ERR_DOMAIN;               // err += log(se)
-    e_pt = log(se) + mx;                                  // err += log(se); err += mx
+    const double lse = log(se);
+    e_pt = lse + mx;                                      // err += log(se); err += mx
+    if (terms) {                                          // err!'s terms (k_gmm_restore)
+      reinterpret_cast<double2 *>(terms)[i] = make_double2(lse, mx);
+      reinterpret_cast<double2 *>(terms)[2 * N + 3 - i] = make_double2(-mx, -lse);
+    }
     // gradient sweep (~f): err -= mx; err -= log(se); ~R_i with adjoints
     double mxg = 0.0 + (1.0 * 1.0) * 1.0;
     const double seg = 0.0 + (1.0 * 1.0) * (1.0 / se);
@@ -533,7 +539,7 @@ constexpr int LSE_LANES = 4, LSE_QK = 96;
 __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
-    uint8_t *__restrict__ fail, unsigned long long *counters) {
+    double *__restrict__ terms, uint8_t *__restrict__ fail, unsigned long long *counters) {
   pdl_wait();
 
   extern __shared__ double lse_ex[];                     // [LSE_THREADS][K]
@@ -577,7 +583,12 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
     if (q == 0) {
       int code = 0;
       if (!(se > 0.0)) code = RL_ERR_DOMAIN;
-      e_pt = log(se) + mx;
+      const double lse = log(se);
+      e_pt = lse + mx;
+      if (terms) {                                          // err!'s terms (k_gmm_restore)
+      reinterpret_cast<double2 *>(terms)[i] = make_double2(lse, mx);
+      reinterpret_cast<double2 *>(terms)[2 * N + 3 - i] = make_double2(-mx, -lse);
+    }
       double mxg = 0.0 + (1.0 * 1.0) * 1.0, tgi = 0.0;
       for (int k = K - 1; k >= 0; k--) {
         se = se - ex[k];
@@ -997,6 +1008,124 @@ __global__ void k_gmm_err(int K, int nerr, const double *__restrict__ err_part,
 }
 
 // ---------------------------------------------------------------------------
+// err! in the reference's order and the primal-restoration check
+// ---------------------------------------------------------------------------
+// The sequence of `err!` updates the reference executes (programs/gmm.rnl):
+// forward  err! += log(se_i); err! += mx_i (i = 1..N); err! -= nn*lsa;
+//          err! += hg2*fro; err! -= wm*ssq; err! += cst
+// gradient sweep (~gmm, reverse order, inverse ops): err! -= cst;
+//          err! += wm*ssq; err! -= hg2*fro; err! += nn*lsa;
+//          err! -= mx_i; err! -= log(se_i) (i = N..1)
+// as terms t_j of e_{j+1} = fl(e_j + t_j) (x - y == x + (-y) in IEEE), laid
+// out contiguously (M = 4N + 8): k_gmm_lse writes t[2i] = log se_i, t[2i+1]
+// = mx_i and their negations at t[M-1-2i], t[M-2-2i]; k_gmm_restore writes
+// the 8 parameter terms t[2N .. 2N+8).
+
+// One CTA: E = err! after the forward run (out[0], the reference's primal
+// output; grad < 0: after ~gmm, the reference's uncall), and with grad > 0 err! after the gradient sweep (*resid) and the
+// verdict of autodiff.py:169-172 values_close(err!, err0, tol) (*code =
+// RL_ERR_RESTORE when it fails; the check is unconditional in the
+// reference, i.e. independent of invcheck).  Launched on a side stream
+// beside k_gmm_rev (it needs only k_gmm_lse's terms and k_gmm_prep's
+// parameter terms).
+__global__ void __launch_bounds__(SEQ_THREADS, 1) k_gmm_restore(
+    long long N, int K, double *__restrict__ terms, const double *__restrict__ par,
+    const double *__restrict__ fro_k, const double *__restrict__ sq, double ga, int wm,
+    double cst, double err0, double tol, int grad, int force_serial, double *__restrict__ out,
+    double *__restrict__ resid, int *__restrict__ code, int *__restrict__ verified) {
+  extern __shared__ __align__(16) unsigned char seq_smem_raw[];
+  SeqSmem &sm = *reinterpret_cast<SeqSmem *>(seq_smem_raw);
+  __shared__ double res[2];
+  const long long n2 = 2 * N;
+  if (threadIdx.x == 0) {
+    // fro and ssq in component order, as k_gmm_final's objective block
+    double fro = 0.0, ssq = 0.0;
+    for (int k = 0; k < K; k++) {
+      fro = fro + fro_k[k];
+      ssq = ssq + sq[k];
+    }
+    const double hg2 = 0.5 * ga * ga;
+    const double p[4] = {par[K] /* -(nn * lsa) */, hg2 * fro, -((double)wm * ssq), cst};
+    for (int q = 0; q < 4; q++) {
+      terms[n2 + q] = p[q];
+      terms[n2 + 7 - q] = -p[q];
+    }
+  }
+  __syncthreads();
+  // grad > 0: the whole chain (E at term 2N + 4); grad == 0: run (the
+  // forward half); grad < 0: uncall (the ~gmm half alone, from err0)
+  const long long M = grad > 0 ? 2 * n2 + 8 : n2 + 4;
+  const int v = seq_sum_block(terms + (grad < 0 ? n2 + 4 : 0), M, err0, n2 + 4, force_serial, sm,
+                              &res[0], &res[1]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = res[0];
+    if (grad > 0) {
+      if (resid) *resid = res[1];
+      if (code) *code = fabs(res[1] - err0) <= tol ? RL_OK : RL_ERR_RESTORE;
+    }
+    if (verified) *verified = v;
+  }
+}
+
+// rl_seq_sum_f64: the same evaluation over an array (tests, tools)
+__global__ void __launch_bounds__(SEQ_THREADS, 1) k_seq_sum(const double *__restrict__ t,
+                                                         long long M, double e0, long long mark,
+                                                         int force_serial,
+                                                         double *__restrict__ out2,
+                                                         int *__restrict__ verified) {
+  extern __shared__ __align__(16) unsigned char seq_smem_raw[];
+  SeqSmem &sm = *reinterpret_cast<SeqSmem *>(seq_smem_raw);
+  __shared__ double res[2];
+#ifdef SEQ_DIAG
+  const int v = seq_sum_block(t, M, e0, mark, force_serial, sm, &res[0], &res[1],
+                              out2 + 2);
+#else
+  const int v = seq_sum_block(t, M, e0, mark, force_serial, sm, &res[0], &res[1]);
+#endif
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out2[0] = res[0];
+    out2[1] = res[1];
+    if (verified) *verified = v;
+  }
+}
+
+int launch_seq_sum(const double *t, int64_t M, double e0, int64_t mark, int32_t force_serial,
+                   double *out2, int32_t *verified, cudaStream_t st) {
+  if (M < 0 || mark < 0 || mark > M || !out2 || (M > 0 && !t))
+    return set_error(RL_ERR_INVALID, "rl_seq_sum_f64: bad argument");
+  int rc;
+  if ((rc = smem_attr((const void *)k_seq_sum, sizeof(SeqSmem), "smem attr seq_sum"))) return rc;
+  k_seq_sum<<<1, SEQ_THREADS, sizeof(SeqSmem), st>>>(t, M, e0, mark, force_serial, out2,
+                                                      verified);
+  return cuda_status(cudaGetLastError(), "k_seq_sum");
+}
+
+// A side stream (and fork / join events) per (host thread, device) for the
+// restoration replay, which runs beside k_gmm_rev.
+struct GmmSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static int gmm_side(GmmSide **out) {
+  thread_local GmmSide sides[64];
+  int dev = 0;
+  int rc;
+  if ((rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
+  if (dev < 0 || dev >= 64) return set_error(RL_ERR_INVALID, "device ordinal >= 64");
+  GmmSide &g = sides[dev];
+  if (!g.s) {
+    if ((rc = cuda_status(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking), "side stream")) ||
+        (rc = cuda_status(cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming), "event")) ||
+        (rc = cuda_status(cudaEventCreateWithFlags(&g.join, cudaEventDisableTiming), "event")))
+      return rc;
+  }
+  *out = &g;
+  return RL_OK;
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
@@ -1041,7 +1170,7 @@ static int choose_split(int K, long long ntiles, int slots, int smax) {
 }
 
 struct GmmLayout {
-  size_t lt, qd, sq, fro, mt, gmt, flags, errp, part, red, par, total;
+  size_t lt, qd, sq, fro, mt, gmt, flags, errp, terms, part, red, par, total;
   int Sf, Sr, nerr;
 };
 
@@ -1078,6 +1207,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.gmt = take((size_t)K * N * 8);
   L.flags = take((size_t)N * 4);
   L.errp = take((size_t)(L.nerr > 0 ? L.nerr : 1) * 8);
+  L.terms = take((size_t)(4 * N + 8) * 8);
   L.part = take((size_t)K * L.Sr * (size_t)pw * 8);
   L.red = take((size_t)K * (size_t)pw * 8);
   L.par = take((size_t)(K + 1) * 8);
@@ -1122,7 +1252,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    const double *means, const double *icf, const double *x, double gamma, int m,
                    double cst, double tol, int chk, int add_params, double *out, uint8_t *fail,
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st,
-                   int grad = 1) {
+                   int grad, const GmmSeq *seq) {
   constexpr int TPF = tpf_c(DP), TPR = tpr_c(DP);
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
   double *fro = (double *)(ws + L.fro);
@@ -1131,7 +1261,21 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   double *errp = (double *)(ws + L.errp), *part = (double *)(ws + L.part);
   double *redp = (double *)(ws + L.red);
   double *par = (double *)(ws + L.par);
+  double *terms = seq ? (double *)(ws + L.terms) : nullptr;
   int rc;
+  if (seq && (rc = smem_attr((const void *)k_gmm_restore, sizeof(SeqSmem), "smem attr restore")))
+    return rc;
+  // err! in the reference's order (+ restoration verdict): one CTA, after
+  // the logsumexp kernel; on a side stream beside k_gmm_rev for gradients
+  auto restore = [&](cudaStream_t s2) {
+    k_gmm_restore<<<1, SEQ_THREADS, sizeof(SeqSmem), s2>>>(
+        N, K, terms, par, fro, sq, gamma, m, cst, seq->err0, tol,
+        grad ? 1 : (seq->direction < 0 ? -1 : 0), seq->force_serial, out,
+        seq->resid, seq->code, seq->verified);
+    return cuda_status(cudaGetLastError(), "k_gmm_restore");
+  };
+  GmmSide *side = nullptr;
+  if (seq && grad && (rc = gmm_side(&side))) return rc;
   const size_t sp = ((size_t)d * (d + 1) / 2 + K) * 8;
   if ((rc = smem_attr((const void *)k_gmm_prep<DP>, sp, "smem attr prep"))) return rc;
 #ifndef GMM_ABLATE
@@ -1157,21 +1301,32 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       if (!(GMM_ABLATE & 2) &&
           (rc = launch_pdl("k_gmm_lse_q", k_gmm_lse_q, dim3(L.nerr),
                            dim3(LSE_THREADS * LSE_LANES), (size_t)LSE_THREADS * K * 8, st, K, N,
-                           mt, gmt, flags, tol, chk, errp, fail, counters)))
+                           mt, gmt, flags, tol, chk, errp, terms, fail, counters)))
         return rc;
     } else if (!(GMM_ABLATE & 2) &&
                (rc = launch_pdl("k_gmm_lse", k_gmm_lse, dim3(L.nerr), dim3(LSE_THREADS), 0, st,
-                                K, N, mt, gmt, flags, tol, chk, errp, fail, counters))) {
+                                K, N, mt, gmt, flags, tol, chk, errp, terms, fail, counters))) {
       return rc;
     }
-    if (!grad) return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst,
-                                         add_params, out, st);
+    if (!grad) {
+      if (seq) return restore(st);
+      return launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst, add_params, out, st);
+    }
+    if (seq) {                                           // fork: restore beside rev
+      if ((rc = cuda_status(cudaEventRecord(side->fork, st), "fork record")) ||
+          (rc = cuda_status(cudaStreamWaitEvent(side->s, side->fork, 0), "fork wait")) ||
+          (rc = restore(side->s)) ||
+          (rc = cuda_status(cudaEventRecord(side->join, side->s), "join record")))
+        return rc;
+    }
     if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
                          d, K, N, means, x, LT, gmt, part)))
       return rc;
   } else if (!grad) {
+    if (seq) return restore(st);
     return launch_gmm_err_only(K, L, 0, errp, sq, fro, par, gamma, m, cst, add_params, out, st);
   } else {
+    if (seq && (rc = restore(st))) return rc;
     if ((rc = cuda_status(cudaMemsetAsync(part, 0, (size_t)K * L.Sr * ((size_t)DP * DP + DP + 1) * 8,
                                           st), "memset part")))
       return rc;
@@ -1182,10 +1337,15 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   if (GMM_ABLATE & 8) return 0;
   // enough (k, c) CTAs for about two per SM, at most 8 per component
   const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
-  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K + GMM_FINAL_ERR_BLOCK, fc),
-                    dim3(GMM_THREADS), 0, st, d, K,
-                    L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, part, errp, par, gamma, m, cst,
-                    add_params, out);
+  // with the replay, the objective comes from k_gmm_restore (no extra column)
+  if ((rc = launch_pdl("k_gmm_final", k_gmm_final<DP>,
+                       dim3(K + (seq ? 0 : GMM_FINAL_ERR_BLOCK), fc), dim3(GMM_THREADS), 0, st, d,
+                       K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, part, errp, par, gamma,
+                       m, cst, add_params, out)))
+    return rc;
+  if (seq && N > 0)                                      // join
+    return cuda_status(cudaStreamWaitEvent(st, side->join, 0), "join wait");
+  return RL_OK;
 #else
   if (!(GMM_ABLATE & 4) && (rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
                        dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K),
@@ -1202,7 +1362,7 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
                const double *means, const double *icf, const double *x, double gamma, int32_t m,
                double cst, double tol, int32_t invcheck, int32_t add_param_terms, double *out,
                uint8_t *fail, unsigned long long *counters, void *ws, size_t ws_bytes,
-               cudaStream_t st, int grad) {
+               cudaStream_t st, int grad, const GmmSeq *seq) {
   if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || !out || (N > 0 && (!x || !fail)))
     return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64: bad argument");
   if (d > 128) return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64: d > 128 is not supported");
@@ -1216,12 +1376,12 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
   const long long Nt = N_total > 0 ? N_total : N;
   if (DP == 32)
     return run_gmm<32>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
+                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad, seq);
   if (DP == 64)
     return run_gmm<64>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
+                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad, seq);
   return run_gmm<128>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
-                      add_param_terms, out, fail, counters, (char *)ws, L, st, grad);
+                      add_param_terms, out, fail, counters, (char *)ws, L, st, grad, seq);
 }
 
 }  // namespace rl

@@ -86,13 +86,13 @@ def _run_gmm(fdef, args, opts, direction):
     ga, wm, cst = args[11:14]
     dev = _device()
     tt = lambda v: torch.as_tensor(v, device=dev)  # noqa: E731
-    r = kernels.gmm_objective(tt(to_numpy(alphas, "alphas", 1)), tt(to_numpy(means, "means", 2)),
-                              tt(to_numpy(icf, "icf", 2)), tt(to_numpy(x, "x", 2)), float(ga),
-                              int(wm), float(cst), tol=opts.float_tolerance,
-                              invcheck=opts.invcheck)
+    a = (tt(to_numpy(alphas, "alphas", 1)), tt(to_numpy(means, "means", 2)),
+         tt(to_numpy(icf, "icf", 2)), tt(to_numpy(x, "x", 2)), float(ga), int(wm), float(cst))
+    # err! accumulated from err0 in the order of gmm (run) or ~gmm (uncall)
+    r = kernels.gmm_run(*a, err0=float(err0), direction=direction, tol=opts.float_tolerance,
+                        invcheck=opts.invcheck)
     _raise_first(r.fail, "gmm")
-    E = float(r.out.item())
-    return [float(err0) + (E if direction > 0 else -E)] + list(args[1:])
+    return [float(r.out.item())] + list(args[1:])
 
 
 _RUNNERS = {"besselj": _run_besselj, "ba_proj": _run_ba_proj, "ba_weight": _run_ba_weight,

@@ -229,6 +229,8 @@ class GMMResult:
     fail: torch.Tensor       # (N,) per point
     counters: torch.Tensor
     packed: torch.Tensor     # the contiguous [err, g_alphas, g_means, g_icf] vector
+    resid: torch.Tensor = None         # () err! after the gradient sweep (gmm_gradient)
+    restore_code: torch.Tensor = None  # () int32: 0, or 5 = RevError (autodiff.py:169-172)
 
     @property
     def n_failed(self):
@@ -286,6 +288,97 @@ def gmm_grad(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
                            workspace.numel(), _stream_handle())
     _native.check(rc, "rl_gmm_grad_f64")
     return unpack_gmm(packed, d, K, fail, counters)
+
+
+def _gmm_args(alphas, means, icf, x):
+    alphas = _require_cuda("alphas", alphas, ndim=1)
+    means = _require_cuda("means", means, ndim=2)
+    K, d = means.shape
+    icf = _require_cuda("icf", icf, ndim=2, last=d * (d + 1) // 2)
+    x = _require_cuda("x", x, ndim=2, last=d)
+    if alphas.shape[0] != K or icf.shape[0] != K:
+        raise KindError("alphas, means and icf must agree on K")
+    return alphas, means, icf, x, K, d
+
+
+def _gmm_workspace(L, d, K, N, workspace, x):
+    wsb = L.rl_gmm_workspace_bytes(d, K, N)
+    if workspace is not None:
+        _check_out("workspace", workspace, x, torch.uint8)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    return workspace
+
+
+def gmm_gradient(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, err0=0.0, tol=1e-9,
+                 invcheck=True, workspace=None, counters=None):
+    """The whole reference `gradient(p, GradRequest("gmm", [err0, alphas,
+    means, icf, x, zeros.., gamma, m, cst]))` on one device
+    (rl_gmm_gradient_f64): err is err! accumulated in the program's order
+    from err0 (the reference's primal output), `resid` is err! after the
+    gradient sweep and `restore_code` the verdict of the reference's
+    primal-restoration check (autodiff.py:169-172): 5 (RevError) when
+    |resid - err0| > tol."""
+    alphas, means, icf, x, K, d = _gmm_args(alphas, means, icf, x)
+    N = x.shape[0]
+    dev = x.device
+    L = _native.lib()
+    workspace = _gmm_workspace(L, d, K, N, workspace, x)
+    packed = torch.empty(gmm_packed_size(d, K), dtype=F64, device=dev)
+    fail = torch.empty(N, dtype=torch.uint8, device=dev)
+    resid = torch.empty((), dtype=F64, device=dev)
+    code = torch.empty((), dtype=torch.int32, device=dev)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    counters = _check_out("counters", counters, x, torch.int64, 2)
+    rc = L.rl_gmm_gradient_f64(d, K, N, _ptr(alphas), _ptr(means), _ptr(icf), _ptr(x),
+                               float(gamma), int(m), float(cst), float(err0), float(tol),
+                               int(bool(invcheck)), _ptr(packed), _ptr(resid), _ptr(code),
+                               _ptr(fail), _ptr(counters), _ptr(workspace), workspace.numel(),
+                               _stream_handle())
+    _native.check(rc, "rl_gmm_gradient_f64")
+    r = unpack_gmm(packed, d, K, fail, counters)
+    r.resid, r.restore_code = resid, code
+    return r
+
+
+def gmm_run(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, err0=0.0, direction=1, tol=1e-9,
+            invcheck=True, workspace=None, counters=None):
+    """Reference `run(p, "gmm", [err0, ...])` (direction +1,
+    interpreter.py:1021) or `uncall` (-1, :1026) on one device
+    (rl_gmm_run_f64): err! after the program (its inverse), accumulated from
+    err0 in that program's order."""
+    alphas, means, icf, x, K, d = _gmm_args(alphas, means, icf, x)
+    N = x.shape[0]
+    L = _native.lib()
+    workspace = _gmm_workspace(L, d, K, N, workspace, x)
+    err = torch.empty(1, dtype=F64, device=x.device)
+    fail = torch.empty(N, dtype=torch.uint8, device=x.device)
+    if counters is None:
+        counters = torch.zeros(2, dtype=torch.int64, device=x.device)
+    rc = L.rl_gmm_run_f64(d, K, N, _ptr(alphas), _ptr(means), _ptr(icf), _ptr(x), float(gamma),
+                          int(m), float(cst), float(err0), float(tol), int(bool(invcheck)),
+                          int(direction), _ptr(err), _ptr(fail), _ptr(counters), _ptr(workspace),
+                          workspace.numel(), _stream_handle())
+    _native.check(rc, "rl_gmm_run_f64")
+    return RunResult(err[0], fail, counters)
+
+
+def seq_sum(t, e0=0.0, mark=None, *, force_serial=False):
+    """e_{j+1} = fl(e_j + t_j) over the device array t from e0, bit-exactly
+    the sequential binary64 chain (rl_seq_sum_f64).  Returns (e_mark, e_M,
+    verified) as Python values; `verified` is True when the parallel path
+    verified (else the sequential fallback produced the result)."""
+    t = _require_cuda("t", t, ndim=1)
+    M = t.shape[0]
+    mark = M if mark is None else int(mark)
+    out2 = torch.empty(2, dtype=F64, device=t.device)
+    ver = torch.zeros((), dtype=torch.int32, device=t.device)
+    rc = _native.lib().rl_seq_sum_f64(_ptr(t), M, float(e0), mark, int(bool(force_serial)),
+                                      _ptr(out2), _ptr(ver), _stream_handle())
+    _native.check(rc, "rl_seq_sum_f64")
+    o = out2.cpu()
+    return float(o[0]), float(o[1]), bool(ver.item())
 
 
 # ---------------------------------------------------------------------------

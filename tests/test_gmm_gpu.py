@@ -31,8 +31,9 @@ def gmm_constants(d, K, N, gamma, m):
 
 
 def inputs(rng, d, K, N):
+    """alphas ~ N(0,1), means ~ U(0,1), icf ~ N(0,1), x ~ U(0,1)."""
     return (rng.normal(0.0, 1.0, K), rng.uniform(0.0, 1.0, (K, d)),
-            rng.normal(0.0, 1.0, (K, d * (d + 1) // 2)) * 0.5, rng.uniform(0.0, 1.0, (N, d)))
+            rng.normal(0.0, 1.0, (K, d * (d + 1) // 2)), rng.uniform(0.0, 1.0, (N, d)))
 
 
 def run_dev(dev, alphas, means, icf, x, gamma, m, cst, **kw):
@@ -76,22 +77,112 @@ def test_random_shapes_vs_oracle(cuda, oracle, d, K, N):
     check_vs((e, ga, gm, gi), got)
 
 
-def test_config3_full_size_vs_oracle(cuda, oracle):
-    """configs[2]: d=64, K=25, N=10,000 (the oracle runs all 8 passes).
+def run_full(dev, alphas, means, icf, x, gamma, m, cst, **kw):
+    """The drop-in single-device gradient (rl_gmm_gradient_f64)."""
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    r = rg.gmm_gradient(t(alphas), t(means), t(icf), t(x), gamma, m, cst, **kw)
+    torch.cuda.synchronize()
+    return (float(r.err.item()), r.g_alphas.cpu().numpy(), r.g_means.cpu().numpy(),
+            r.g_icf.cpu().numpy(), r.fail.cpu().numpy(), r)
 
-    At this size the reference's own final check — err! restored to 0.0
-    within the default 1e-9 after 10^4 accumulate/uncompute steps — fails
-    (RevError, oracle rc 5): the survey ran it with float_tolerance 1e-6,
-    and so does this test."""
+
+def test_config3_full_size_vs_oracle(cuda, oracle):
+    """configs[2]: d=64, K=25, N=10,000, inputs as SURVEY §8(d) (icf ~ N(0,1)).
+
+    The reference's final check — err! restored to err0 within 1e-9 after
+    the gradient sweep (autodiff.py:169-172) — FAILS here (RevError): its
+    residual (-5.7e-9) is the round-off that the SHARED scratch arguments
+    (qxc!, mt!, ... reused by every point, DESIGN §2 deviation 1) carry from
+    point to point, so ~gmm recomputes each point's terms from different
+    scratch bits than the forward run did.  With the device's per-(point,
+    component) scratch (oracle fresh=True) the same program's residual is
+    -6.0e-11 and the check passes.  The device replays err!'s 40,008-step
+    chain bit-exactly over its own terms (k_gmm_restore, rl_seq_sum_f64) and
+    reaches the fresh-scratch verdict at every tolerance where that verdict
+    is not decided by the last bits of the chain."""
     d, K, N = 64, 25, 10000
     alphas, means, icf, x = inputs(np.random.default_rng(2), d, K, N)
     cst = gmm_constants(d, K, N, 1.0, 0)
-    rc, e, ga, gm, gi = oracle.gmm_grad(alphas, means, icf, x, 1.0, 0, cst)
-    assert rc == 5                                   # RevError at tol 1e-9, as the reference
-    rc, e, ga, gm, gi = oracle.gmm_grad(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+    rc, e, resid, *_ = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 0, cst)
+    assert rc == 5 and abs(resid) > 1e-9            # the reference: RevError at 1e-9
+    rcf, ef, residf, *_ = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 0, cst, fresh=True)
+    assert rcf == 0 and abs(residf) < 1e-9          # the device's scratch semantics: passes
+    for tol, want in ((1e-9, 0), (1e-6, 0), (1e-12, 5)):
+        got = run_full(cuda, alphas, means, icf, x, 1.0, 0, cst, tol=tol)
+        r = got[5]
+        assert not got[4].any() and r.n_failed == 0
+        dres = float(r.resid.item())
+        assert (abs(residf) > tol) == (want == 5)
+        assert int(r.restore_code.item()) == want, (tol, dres, residf)
+        # both residuals are the rounding of err!'s chain: same scale
+        assert abs(dres) < 1e-9 and abs(dres) > 1e-13
+        assert abs(got[0] - ef) <= 1e-12 * abs(ef)
+    with pytest.raises(rg.RevError):                # the drop-in raises it where the device's
+        p = rg.load_example("gmm")                  # own verdict does (tol 1e-12 here)
+        A = lambda a: rg.Array.matrix(a.tolist()) if a.ndim == 2 else rg.Array.vector(a.tolist())  # noqa
+        Z = lambda *s: A(np.zeros(s))  # noqa: E731
+        args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), Z(K),
+                1.0, 0, cst]
+        rg.gradient(p, rg.GradRequest("gmm", args), rg.ExecOptions(float_tolerance=1e-12))
+    rc, e, resid, ga, gm, gi = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
     assert rc == 0
-    got = run_dev(cuda, alphas, means, icf, x, 1.0, 0, cst)
-    assert not got[4].any() and got[5].n_failed == 0
+    got = run_full(cuda, alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+    check_vs((e, ga, gm, gi), got)
+    # the shard entry (tree-summed objective) agrees too
+    check_vs((e, ga, gm, gi), run_dev(cuda, alphas, means, icf, x, 1.0, 0, cst))
+
+
+def test_err0_and_restoration_at_small_sizes(cuda, oracle):
+    """err! starts at err0 (args[0]); E and the residual follow the
+    reference's chain from there; verdicts equal the oracle's over a range
+    of tolerances."""
+    d, K, N = 16, 4, 600
+    alphas, means, icf, x = inputs(np.random.default_rng(11), d, K, N)
+    for err0 in (0.0, 12345.678, -3.5e7):
+        for tol in (1e-9, 1e-11):
+            rc, e, resid, ga, gm, gi = oracle.gmm_grad_ex(alphas, means, icf, x, 1.3, 2, 0.25,
+                                                          err0=err0, tol=tol, fresh=True)
+            got = run_full(cuda, alphas, means, icf, x, 1.3, 2, 0.25, err0=err0, tol=tol)
+            assert abs(got[0] - e) <= 1e-12 * abs(e)
+            code = int(got[5].restore_code.item())
+            dres = float(got[5].resid.item())
+            ulp = abs(np.spacing(max(abs(e), abs(err0))))
+            # the err! part of the verdict under the device's scratch
+            # semantics (the oracle's rc also covers the scratch residues)
+            want = 5 if abs(resid - err0) > tol else 0
+            if abs(abs(resid - err0) - tol) > 32 * ulp:     # not decided by the last bits
+                assert code == want, (err0, tol, rc, resid, dres)
+            assert abs(dres - err0) <= 256 * ulp + 1e-9
+
+
+def test_run_and_uncall_chain_order(cuda, oracle):
+    """run(gmm) returns err! accumulated from err0 in the program's order;
+    uncall(gmm) runs ~gmm from err0; run then uncall restores err0 to the
+    chain's rounding."""
+    d, K, N = 10, 3, 200
+    alphas, means, icf, x = inputs(np.random.default_rng(12), d, K, N)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=cuda)  # noqa: E731
+    rc, e, resid, *_ = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 1, 0.5, err0=7.25)
+    E = float(rg.gmm_run(t(alphas), t(means), t(icf), t(x), 1.0, 1, 0.5, err0=7.25).out.item())
+    assert abs(E - e) <= 1e-12 * abs(e)
+    back = float(rg.gmm_run(t(alphas), t(means), t(icf), t(x), 1.0, 1, 0.5, err0=E,
+                            direction=-1).out.item())
+    full = run_full(cuda, alphas, means, icf, x, 1.0, 1, 0.5, err0=7.25)
+    assert back == float(full[5].resid.item())       # the same chain, bit for bit
+    assert abs(back - 7.25) <= 1e-9
+
+
+@pytest.mark.parametrize("N", [1024])
+def test_config5_shape_subset_vs_oracle(cuda, oracle, N):
+    """configs[4] shape (d=128, K=200) on a subset of points, against the
+    oracle (the reference's restated program), rtol 1e-10."""
+    d, K = 128, 200
+    alphas, means, icf, x = inputs(np.random.default_rng(4), d, K, N)
+    cst = gmm_constants(d, K, N, 1.0, 0)
+    rc, e, resid, ga, gm, gi = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+    assert rc == 0
+    got = run_full(cuda, alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
+    assert not got[4].any() and int(got[5].restore_code.item()) == 0
     check_vs((e, ga, gm, gi), got)
 
 
