@@ -122,6 +122,9 @@ int rl_ba_jac_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doubl
  *   ranks); with 1 the parameter-only terms (-N_total*lse(alphas), Wishart
  *   prior, cst) are added too.  fail: N per-point flags.
  * ws: device workspace of rl_gmm_workspace_bytes() bytes.
+ * d <= 128 (the kernels' widest tile): d > 128 is RL_ERR_INVALID and
+ * rl_gmm_workspace_bytes returns 0; the Python drop-in sends such calls to
+ * the generic compiler's kernel (codegen.py).
  * ---------------------------------------------------------------------- */
 size_t rl_gmm_workspace_bytes(int32_t d, int32_t K, int64_t N);
 int rl_gmm_grad_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,

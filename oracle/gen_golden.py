@@ -607,12 +607,34 @@ def gen_codegen_complex():
     print("complex goldens:", Counter(out["err_re"]), Counter(HE))
 
 
+def gen_codegen_complex_fd():
+    """reference finite_difference() of polar.rnl (Complex arguments: re/im
+    leaves, default seed y!.re and an explicit y!.im seed), h = 1e-6."""
+    from revlang.autodiff import finite_difference
+    from revlang.values import Complex
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "polar.rnl")).read())
+    g = np.load(os.path.join(OUT_DIR, "codegen_complex.npz"))
+    X = g["x"]
+    rows = [i for i in range(X.shape[0]) if g["err_re"][i] == ""][:6]
+    out = {"rows": np.array(rows), "h": np.array(1e-6)}
+    for tag, seeds in (("re", None), ("im", [("y!", (("field", "im"),), 1.0)])):
+        G = []
+        for i in rows:
+            row = X[i]
+            args = [Complex(row[0], row[1]), Complex(row[2], row[3]), row[4], row[5]]
+            fd = finite_difference(prog, "polar", args, 1e-6, seeds=seeds)
+            G.append([fd["y!"].re, fd["y!"].im, fd["x"].re, fd["x"].im, fd["p!"], fd["q!"]])
+        out["fd_" + tag] = np.array(G, dtype=np.float64)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_complex_fd.npz"), **out)
+    print("complex fd goldens:", len(rows), "rows")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
                               "codegen_random",
-                              "codegen_complex"]
+                              "codegen_complex", "codegen_complex_fd"]
     for w in which:
         globals()["gen_" + w]()

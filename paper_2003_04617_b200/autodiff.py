@@ -246,6 +246,7 @@ def _grad_gmm(fdef, req, opts):
     ic = to_numpy(icf, "icf", 2)
     xv = to_numpy(x, "x", 2)
     K, d = mu.shape
+
     for nm, s in zip(names[5:11], scratch):
         sv = to_numpy(s, nm)
         if np.any(sv != 0.0):
@@ -300,10 +301,22 @@ def gradient(program, req, opts=None):
     kernel of a registered program, else the function compiled by codegen."""
     opts = _check_opts(opts)
     prog, fdef, reg = _lookup(program, req.fname)
-    if not reg:
+    if not reg or gmm_beyond_tiles(fdef, req.args):
         from . import generic
         return generic.gradient(prog, fdef, req, opts)
     return _HANDLERS[fdef.kernel.handler](fdef, req, opts)
+
+
+def gmm_beyond_tiles(fdef, args):
+    """gmm with d > 128 (the hand-written kernels' widest tile, gmm.cu) runs
+    through the generic compiler's kernel instead (the reference takes any d)."""
+    if fdef.kernel is None or fdef.kernel.handler != "gmm" or len(args) < 3:
+        return False
+    try:
+        shape = np.shape(to_numpy(args[2], "means", 2))
+    except Exception:  # noqa: BLE001 - malformed arguments: the handler reports them
+        return False
+    return shape[1] > kernels.GMM_MAX_D
 
 
 def _int_array(v):

@@ -22,12 +22,15 @@ generated code restates the reference interpreter's semantics:
   conditions                       interpreter.py:200-300 (ULog compares as
                                    exp(log_x), Int % as Python's modulo)
 
-The subset: scalar parameters (Float rows, or Int values uniform over the
-batch), Float / ULog / Int ancillas, `+= -= *= /=` instructions with the
-INSTR_FNS functions, `<-` / `->`, @routine / ~@routine, for / while / if.
-Arrays, records, Fixed / Complex numbers, function calls and xor= are
-rejected at compile time (UnsupportedProgram), as are the static aliasing
-patterns the reference rejects at run time (AliasedArguments).
+The subset: Float / Int / Complex scalar parameters (Float rows; Int
+values uniform over the batch; Complex as re/im leaves with field views),
+fixed-shape Float arrays (parameters and ancilla-free array arguments),
+Float / ULog / Int ancillas, `+= -= *= /=` instructions with the INSTR_FNS
+functions, `xor=` on Int cells, calls between compiled functions,
+`<-` / `->`, @routine / ~@routine, @invcheckoff, for / while / if.
+Records, Fixed values, recursion and bijector views are rejected at compile
+time (UnsupportedProgram), as are the static aliasing patterns the reference
+rejects at run time (AliasedArguments).
 
 The kernel is built with nvcc for sm_100a into a cache directory
 ($REVGPU_CODEGEN_CACHE, default paper_2003_04617_b200/_codegen_cache) and bound with

@@ -24,7 +24,7 @@
 // with -fmad=false: no contraction, IEEE add/mul/div).  Integer logs
 // log(k), log(k + nu) come from a host libm table (bit-identical to the
 // reference); exp is fexp.cuh (0.5 ulp + O(2^-60), bit-identical to the
-// host libm in ~99.8% of calls, <= 1 ulp otherwise); log(z) and the final
+// host libm in 99.92% of calls (tests/test_fexp.py), <= 1 ulp otherwise); log(z) and the final
 // division are libdevice (<= 1 ulp / correctly rounded).
 //
 // Scheduling.  The series trip count T(z) is non-decreasing in z (every

@@ -201,13 +201,25 @@ def gradient_batch(prog, fdef, inputs, seeds, wrt, opts):
     return primal, {p: grads[p] for p in report}, fail
 
 
+def _cval(v):
+    """A Complex argument (the caller's re/im class, complex or 0-d tensor) as complex."""
+    if hasattr(v, "re") and hasattr(v, "im"):
+        return complex(float(v.re), float(v.im))
+    if isinstance(v, torch.Tensor):
+        return complex(v.item())
+    return complex(v)
+
+
 def _leaf_rows(kinds, names, args):
-    """[(param, flat index or None)] over the Float leaves, leaf_paths order."""
+    """[(param, flat index / "re" / "im" / None)] over the Float leaves, in
+    leaf_paths order (a Complex is its re and im leaves, autodiff.py:46-47)."""
     out = []
     for p, v in zip(names, args):
         k, shp = kinds[p]
         if k == "f":
             out.append((p, None))
+        elif k == "c":
+            out += [(p, "re"), (p, "im")]
         elif k == "a":
             out += [(p, i) for i in range(int(np.prod(shp)))]
     return out
@@ -227,12 +239,23 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
     batch, steps = {}, []
     for p in names:
         kind, shp = kinds[p]
-        if kind in ("f", "a"):
-            a = np.asarray(base[p], dtype=np.float64)
+        if kind in ("f", "a", "c"):
+            a = np.asarray(_cval(base[p]) if kind == "c" else base[p],
+                           dtype=np.complex128 if kind == "c" else np.float64)
             batch[p] = np.broadcast_to(a, (max(n, 1),) + a.shape).copy()
         else:
             batch[p] = base[p]
     for r, (p, i) in enumerate(leaves):
+        if i in ("re", "im"):                            # a Complex leaf
+            z = _cval(base[p])
+            x = z.real if i == "re" else z.imag
+            up, dn = x + h, x - h
+            steps.append(up - dn)
+            if i == "re":
+                batch[p][2 * r], batch[p][2 * r + 1] = complex(up, z.imag), complex(dn, z.imag)
+            else:
+                batch[p][2 * r], batch[p][2 * r + 1] = complex(z.real, up), complex(z.real, dn)
+            continue
         col = batch[p] if i is None else batch[p].reshape(n, -1)
         x = float(base[p]) if i is None else float(np.asarray(base[p]).ravel()[i])
         up, dn = x + h, x - h
@@ -242,7 +265,7 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
         else:
             col[2 * r, i], col[2 * r + 1, i] = up, dn
     dev = torch.device("cuda", torch.cuda.current_device())
-    tens = {p: (torch.as_tensor(v, device=dev) if kinds[p][0] in ("f", "a") else v)
+    tens = {p: (torch.as_tensor(v, device=dev) if kinds[p][0] in ("f", "a", "c") else v)
             for p, v in batch.items()}
     out, fail = k.run(tens, 1, tol=opts.float_tolerance, invcheck=opts.invcheck,
                       max_steps=opts.max_steps)
@@ -254,13 +277,15 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
         if pname not in names:
             raise KindError(f"seed names unknown parameter {pname!r}")
         v = out[pname].cpu().numpy().reshape(max(n, 1), -1)
-        if path:
+        if path and path[0][0] == "field":               # Complex re / im (get_leaf)
+            col = v[:, 0].real if path[0][1] == "re" else v[:, 0].imag
+        elif path:
             idx = path[0][1]
             shp = kinds[pname][1]
-            j = int(np.ravel_multi_index(tuple(x - 1 for x in idx), shp))
+            col = v[:, int(np.ravel_multi_index(tuple(x - 1 for x in idx), shp))]
         else:
-            j = 0
-        total = total + float(seed) * v[:, j]
+            col = v[:, 0]
+        total = total + float(seed) * np.real(col)
     grads = {}
     for p, v in zip(names, args):
         kind, shp = kinds[p]
@@ -269,5 +294,9 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
             continue
         rows = [r for r, (q, _) in enumerate(leaves) if q == p]
         vals = [(total[2 * r] - total[2 * r + 1]) / steps[r] for r in rows]
-        grads[p] = float(vals[0]) if kind == "f" else _back(v, "a", np.asarray(vals).reshape(shp))
+        if kind == "c":                                  # Complex(grad re, grad im)
+            grads[p] = _back(v, "c", complex(vals[0], vals[1]))
+        else:
+            grads[p] = float(vals[0]) if kind == "f" else \
+                _back(v, "a", np.asarray(vals).reshape(shp))
     return grads

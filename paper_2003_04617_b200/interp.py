@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import kernels
-from .autodiff import _check_opts, _device, _is_float, _is_int, _lookup
+from .autodiff import _check_opts, _device, _is_float, _is_int, _lookup, gmm_beyond_tiles
 from .errors import KindError, RevLangError, error_for_code
 from .values import to_numpy
 
@@ -108,7 +108,7 @@ def run(program, fname, args, opts=None):
 def _dispatch(program, fname, args, opts, direction):
     opts = _check_opts(opts)
     prog, fdef, reg = _lookup(program, fname)
-    if not reg:
+    if not reg or gmm_beyond_tiles(fdef, list(args)):
         from . import generic
         return generic.run(prog, fdef, list(args), opts, direction)
     return _RUNNERS[fdef.kernel.handler](fdef, list(args), opts, direction)

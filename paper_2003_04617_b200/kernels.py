@@ -237,6 +237,9 @@ class GMMResult:
         return int(self.counters[1].item())
 
 
+GMM_MAX_D = 128      # widest tile of the hand-written GMM kernels (gmm.cu, dp_of)
+
+
 def gmm_packed_size(d, K):
     return 1 + K + K * d + K * d * (d + 1) // 2
 

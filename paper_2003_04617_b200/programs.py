@@ -240,18 +240,17 @@ def parse_program(text, filename="<string>"):
 
 
 def as_program(program):
-    """Accept our Program, program text, or a reference revlang Program
-    (pretty-printed back to text when revlang is importable)."""
+    """Accept our Program or program source text (the reference's
+    parse_program input, parser.py:593).  A reference revlang.Program object
+    is not interpreted here — the product runs no reference code — pass its
+    source (revlang.parser.pretty_print(p)) instead."""
     if isinstance(program, Program):
         return program
     if isinstance(program, str):
         return parse_program(program)
-    try:  # a reference revlang.ir.Program
-        from revlang.parser import pretty_print  # noqa: PLC0415
-        return parse_program(pretty_print(program), getattr(program, "filename", "<revlang>"))
-    except ImportError:
-        pass
-    raise UnsupportedProgram(f"cannot interpret {type(program).__name__} as a program")
+    raise UnsupportedProgram(
+        f"cannot interpret {type(program).__name__} as a program: pass program text "
+        "(e.g. revlang.parser.pretty_print(p)) or a Program from parse_program")
 
 
 _cache = {}

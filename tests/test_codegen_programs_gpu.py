@@ -278,3 +278,28 @@ def test_complex_through_the_dropin_api(cuda, golden):
     got = [grads["y!"].re, grads["y!"].im, grads["x"].re, grads["x"].im, grads["p!"], grads["q!"]]
     assert close(got, g["grad_re"][0], 1e-12, 1e-14).all()
     del sys
+
+
+def test_complex_finite_difference_against_the_reference(cuda, golden):
+    """finite_difference() with Complex arguments (re / im leaves, default
+    seed y!.re, explicit y!.im seed) against the reference's own
+    finite_difference (codegen_complex_fd.npz, h = 1e-6).  Both difference
+    the same binary64 program at the same steps; the device's libdevice
+    sin / cos / log differ from the host libm by <= 1-2 ulp, amplified by
+    1 / (2h) = 5e5: the bar is 1e-8 absolute + 1e-8 relative."""
+    import paper_2003_04617_b200 as rg
+    from test_codegen_gpu import src
+
+    class Complex:
+        def __init__(self, re, im):
+            self.re, self.im = re, im
+    g = golden("codegen_complex")
+    f = golden("codegen_complex_fd")
+    for j, i in enumerate(f["rows"]):
+        row = g["x"][i]
+        args = [Complex(row[0], row[1]), Complex(row[2], row[3]), float(row[4]), float(row[5])]
+        for tag, seeds in (("re", None), ("im", [("y!", (("field", "im"),), 1.0)])):
+            fd = rg.finite_difference(src("polar"), "polar", args, float(f["h"]), seeds=seeds)
+            assert isinstance(fd["x"], Complex)
+            got = [fd["y!"].re, fd["y!"].im, fd["x"].re, fd["x"].im, fd["p!"], fd["q!"]]
+            assert close(got, f["fd_" + tag][j], 1e-8, 1e-8).all(), (tag, i, got)

@@ -139,3 +139,25 @@ def test_gradient_batch_generic_arrays(cuda, golden):
     flat = lambda d: torch.cat([d[p].reshape(n, -1) for p in ("q!", "r!", "A", "u")], 1)  # noqa
     assert np.array_equal(flat(primal).cpu().numpy(), ga["quad_primal"])
     assert np.array_equal(flat(grads).cpu().numpy(), ga["quad_grad"])
+
+
+def test_gmm_wider_than_the_tiles_goes_generic(cuda, oracle):
+    """d > 128 is beyond the hand-written GMM tiles (gmm.cu): the drop-in
+    gradient runs the generic compiler's kernel of the same program and
+    matches the oracle (the reference takes any d)."""
+    d, K, N = 130, 2, 3
+    rng = np.random.default_rng(5)
+    alphas, means = rng.normal(0, 1, K), rng.uniform(0, 1, (K, d))
+    icf, x = rng.normal(0, 0.3, (K, d * (d + 1) // 2)), rng.uniform(0, 1, (N, d))
+    rc, e, ga, gm, gi = oracle.gmm_grad(alphas, means, icf, x, 1.0, 0, 0.5)
+    assert rc == 0
+    A = lambda a: rg.Array.matrix(a.tolist()) if a.ndim == 2 else rg.Array.vector(a.tolist())  # noqa
+    Z = lambda *s: A(np.zeros(s))  # noqa: E731
+    args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K),
+            rg.Array.vector([0] * K), 1.0, 0, 0.5]
+    primal, g = rg.gradient(rg.load_example("gmm"), rg.GradRequest("gmm", args,
+                                                                    wrt=["alphas", "icf"]))
+    assert abs(primal[0] - e) <= 1e-12 * abs(e)
+    assert np.allclose(np.array(g["alphas"].data), ga, rtol=1e-10, atol=1e-12)
+    assert np.allclose(np.array(g["icf"].data).reshape(K, -1), gi, rtol=1e-9,
+                       atol=1e-12 * np.max(np.abs(gi)))
