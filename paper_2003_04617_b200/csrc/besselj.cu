@@ -95,7 +95,9 @@ constexpr int BJ_EXPREP = 1;
 __shared__ __align__(16) Exp2Tab s_exp2tab[BJ_EXPN * BJ_EXPREP];   // 16-byte loads
 // (log k, log(k + nu)) for k < BJ_KP: one broadcast 16-byte shared load per
 // series trip (k is warp-uniform) instead of two indexed constant loads
-constexpr int BJ_KP = 512;
+#ifndef BJ_KP
+#define BJ_KP 512          // shared (log k, log(k + nu)) pairs (k beyond: the constant table)
+#endif
 __shared__ double2 s_logpair[BJ_KP];
 
 __device__ __forceinline__ double logi(int i) {

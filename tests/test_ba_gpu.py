@@ -2,7 +2,8 @@
 
 The kernel runs the reference's IEEE operation sequence (no FMA
 contraction); sin/cos (<= 2 ulp in libdevice) are the only differences, so
-the bar is |gpu - ref| <= 1e-10 |ref| + 1e-13 max|row| (entries that are
+the bar is |gpu - ref| <= 1e-12 |ref| + 3e-14 max|row| (measured: <= 6.2e-15
+max|row| over 200k observations, profiles/r02/parity_stats.json; entries that are
 exactly 0 in the reference — e.g. de1/dx0[2] — must be 0).  Indices and
 failure classes are bit-exact."""
 
@@ -19,7 +20,7 @@ def row_close(a, b):
     a = np.asarray(a)
     b = np.asarray(b)
     scale = np.max(np.abs(b), axis=-1, keepdims=True)
-    return np.abs(a - b) <= 1e-10 * np.abs(b) + 1e-13 * scale
+    return np.abs(a - b) <= 1e-12 * np.abs(b) + 3e-14 * scale
 
 
 def ba_inputs(rng, n_cams, n_pts, n_obs, shuffle=True):

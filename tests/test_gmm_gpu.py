@@ -1,9 +1,14 @@
-"""GMM objective-gradient kernels (rl_gmm_grad_f64) vs the reference.
+"""GMM objective-gradient kernels (rl_gmm_grad_f64 / rl_gmm_gradient_f64)
+vs the reference.
 
 The device computes the per-point terms in parallel (fresh scratch per
-point) and contracts products to FMA, so results match the sequential
-reference to rounding: the bar is |gpu - ref| <= 1e-10 |ref| + 1e-12 max|ref|
-per gradient array, and the objective to 1e-12 relative."""
+point), sums them in tile / tensor-core order and contracts products to
+FMA, so results match the sequential reference to rounding.  The bar per
+gradient array is |gpu - ref| <= 1e-11 |ref| + 4e-14 sqrt(N K) max|ref|:
+the floor grows with the number of point / component terms summed into an
+entry (measured <= 2.2e-12 max|ref| at d=128, K=200, N=256 and <= 5.6e-14
+for K <= 6, profiles/r02/parity_stats.json); the objective to 1e-12
+relative."""
 
 import math
 
@@ -16,10 +21,14 @@ import paper_2003_04617_b200 as rg
 pytestmark = pytest.mark.gpu
 
 
-def arr_close(a, b, rtol=1e-10, floor=1e-12):
+def arr_close(a, b, rtol=1e-11, floor=1e-12):
     a = np.asarray(a)
     b = np.asarray(b)
     return np.all(np.abs(a - b) <= rtol * np.abs(b) + floor * np.max(np.abs(b)))
+
+
+def floor_for(N, K):
+    return 4e-14 * math.sqrt(max(N, 1) * K)
 
 
 def gmm_constants(d, K, N, gamma, m):
@@ -46,10 +55,12 @@ def run_dev(dev, alphas, means, icf, x, gamma, m, cst, **kw):
 
 def check_vs(ref, got):
     e, ga, gm, gi = ref
+    N, K = got[5].fail.shape[0], ga.shape[0]
+    fl = floor_for(N, K)
     assert abs(got[0] - e) <= 1e-12 * abs(e) + 1e-9
-    assert arr_close(got[1], ga)
-    assert arr_close(got[2], gm)
-    assert arr_close(got[3], gi)
+    assert arr_close(got[1], ga, floor=fl)
+    assert arr_close(got[2], gm, floor=fl)
+    assert arr_close(got[3], gi, floor=fl)
 
 
 def test_golden_vectors(cuda, golden):
@@ -239,9 +250,10 @@ def test_against_torch_autograd_at_scale(cuda):
          + cst)
     f.backward()
     assert abs(got[0] - f.item()) <= 1e-11 * abs(f.item())
-    assert arr_close(got[1], al.grad.cpu().numpy(), rtol=1e-9, floor=1e-11)
-    assert arr_close(got[2], me.grad.cpu().numpy(), rtol=1e-9, floor=1e-11)
-    assert arr_close(got[3], ic.grad.cpu().numpy(), rtol=1e-9, floor=1e-11)
+    fl = floor_for(N, K)                      # two summation orders, neither the reference's
+    assert arr_close(got[1], al.grad.cpu().numpy(), rtol=1e-10, floor=fl)
+    assert arr_close(got[2], me.grad.cpu().numpy(), rtol=1e-10, floor=fl)
+    assert arr_close(got[3], ic.grad.cpu().numpy(), rtol=1e-10, floor=fl)
 
 
 def test_dropin_gradient(cuda, golden):
