@@ -13,6 +13,12 @@ namespace rl {
 // predecessor drains; it waits here (no-op for ordinary launches) before
 // touching anything the predecessor writes.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next kernel of the chain to launch now (its own pdl_wait still
+// waits for this grid to complete): used by short single-wave kernels so
+// the next kernel's independent prologue overlaps them.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 
 constexpr unsigned FULL_MASK = 0xffffffffu;

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
                                                           double *__restrict__ par,
                                                           unsigned *__restrict__ flags,
                                                           long long N) {
+  pdl_trigger();                 // k_gmm_fwd's prologue (x prefetch) overlaps this kernel
   const int k = blockIdx.x;
   // the per-point release flags of k_gmm_fwd start at 0 (replaces a memset,
   // so the launch chain stays kernel-to-kernel for PDL)
@@ -379,8 +380,6 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
     double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA) {
-  pdl_wait();
-
   using C = GmmCfg<DP, TP>;
   extern __shared__ __align__(16) double smem[];
   double *lt_s = smem;
@@ -392,15 +391,18 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t0 = lane & 3, t1 = lane >> 2;
   const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
-  copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
+  // independent of k_gmm_prep (inputs only): before the PDL wait
   for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;  // padding stays zero
   for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
-  const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
   const long long ntiles = (N + TP - 1) / TP;
   __syncthreads();
   long long tile = blockIdx.y;
   if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
   cp_commit();
+  pdl_wait();                                            // prep's L^T, sq and zeroed flags
+  copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
+  cp_commit();
+  const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
   int buf = 0;
   for (; tile < ntiles; tile += gridDim.y) {
     const long long nxt = tile + gridDim.y;
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
     double *__restrict__ terms, uint8_t *__restrict__ fail, unsigned long long *counters) {
+  pdl_trigger();                 // k_gmm_rev's prologue (L^T, x prefetch) overlaps this kernel
   pdl_wait();
 
   const long long i = (long long)blockIdx.x * LSE_THREADS + threadIdx.x;
@@ -540,6 +543,7 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
     int K, long long N, const double *__restrict__ mtT, double *__restrict__ gmtT,
     const unsigned *__restrict__ flagsA, double tol, int chk, double *__restrict__ err_part,
     double *__restrict__ terms, uint8_t *__restrict__ fail, unsigned long long *counters) {
+  pdl_trigger();                 // k_gmm_rev's prologue (L^T, x prefetch) overlaps this kernel
   pdl_wait();
 
   extern __shared__ double lse_ex[];                     // [LSE_THREADS][K]
@@ -647,8 +651,6 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ x,
     const double *__restrict__ LT, const double *__restrict__ gmtT,
     double *__restrict__ part /* [K][S][DP*DP + DP + 1] */) {
-  pdl_wait();
-
   using C = GmmCfg<DP, TP>;
   using MTL = MTiles<DP>;
   extern __shared__ __align__(16) double smem[];
@@ -697,6 +699,9 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   long long tile = blockIdx.y;
   if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
   cp_commit();
+  // L^T (prep), means and x are ready before k_gmm_lse ends (it launches this
+  // grid early): only mt.g below needs the wait
+  pdl_wait();
   int buf = 0;
   // Three barriers per tile: the next tile's prefetch is issued after the
   // top barrier (whose arrival means every warp has finished reading that
