@@ -896,9 +896,12 @@ __device__ __forceinline__ double g_log(double x, int &c) {
 // exp: the series kernels' table exp (csrc/fexp.cuh: 0.5 ulp + O(2^-60), equal
 // to the host libm's in ~99.9% of calls) inside (-708, 708), libdevice outside
 __device__ rl::Exp2Tab rl_exp2tab[1024] = RL_EXP2_TABLE_INIT_1024;
+__shared__ __align__(16) rl::Exp2Tab rl_exp2tab_s[1024];   // filled at kernel entry
 __constant__ rl::ExpConsts1024 rl_expk = RL_EXP_CONSTS_1024_INIT;
 __device__ __forceinline__ double g_exp(double x, int &c) {
-  const double r = fabs(x) < 708.0 ? rl::fexp1024(x, rl::Exp2TabFn{rl_exp2tab}, rl_expk) : exp(x);
+  const double r = fabs(x) < 708.0 ? rl::fexp1024(x, [](int q) {
+    const rl::Exp2Tab e = rl_exp2tab_s[q];
+    return make_double2(e.hi, e.lo); }, rl_expk) : exp(x);
   if (isinf(r) && isfinite(x)) { if (!c) c = RC_OVERFLOW; }
   return r;
 }
@@ -968,6 +971,30 @@ __device__ __forceinline__ Dl g_exp(Dl x, int &c) {
   const double r = g_exp(x.p, c);
   return Dl(r, x.t * r);
 }
+// exp of a ULog cell, memoised on the argument's bits: a while loop reads
+// convert(s) in its condition and again in its body (and gradient mode a
+// third time for the adjoint) with s unchanged in between.  exp is a pure
+// function of its argument (the error class included), so reusing the value
+// changes nothing the reference would observe.
+struct ExpMemo {
+  double in, out;
+  int code, valid;
+};
+__device__ __forceinline__ double g_expm(double x, int &c, ExpMemo &m) {
+  if (m.valid && __double_as_longlong(x) == __double_as_longlong(m.in)) {
+    if (m.code && !c) c = m.code;
+    return m.out;
+  }
+  int cc = 0;
+  const double r = g_exp(x, cc);
+  m.in = x;
+  m.out = r;
+  m.code = cc;
+  m.valid = 1;
+  if (cc && !c) c = cc;
+  return r;
+}
+__device__ __forceinline__ Dl g_expm(Dl x, int &c, ExpMemo &) { return g_exp(x, c); }
 __device__ __forceinline__ Dl sin(Dl x) { return Dl(sin(x.p), x.t * cos(x.p)); }
 // s_atan2 over Duals (values.py): (atan2(yp, xp), (xp yt - yp xt) / (yp^2 + xp^2))
 __device__ __forceinline__ Dl atan2(Dl y, Dl x) {
@@ -1221,7 +1248,7 @@ class _Emitter:
         if isinstance(e, Var):
             k = self.kind(e.name)
             if k == "u":
-                return f"g_exp(v_{_cid(e.name)}, code)", "f"       # to_real(ULog)
+                return f"g_expm(v_{_cid(e.name)}, code, xm)", "f"  # to_real(ULog)
             return f"v_{_cid(e.name)}", k
         if isinstance(e, IView):
             return f"v_{_cid(e.name)}[{self.offset(e)}]", self.cell_kind(e)
@@ -1326,7 +1353,7 @@ class _Emitter:
                 raise UnsupportedProgram("codegen: Bool arguments are not supported")
             return _c_double(a.v)
         if r.kind == "u":
-            return f"g_exp({r.v}, code)"
+            return f"g_expm({r.v}, code, xm)"
         if r.kind == "i":
             return f"R((double){r.v})"
         return r.v
@@ -1387,7 +1414,7 @@ class _Emitter:
         if fname == "sqrt":
             return [f"g_div(R(0.5), g_sqrt(R({xs[0]}), code), code)"]
         if fname == "exp":
-            return [f"g_exp(R({xs[0]}), code)"]
+            return [f"g_expm(R({xs[0]}), code, xm)"]
         if fname == "log":
             return [f"g_div(R(1.0), R({xs[0]}), code)"]
         if fname == "sin":
@@ -1698,7 +1725,7 @@ class _Emitter:
                 if self.tracked(r):
                     if r.kind == "u":
                         # d value / d exponent = value
-                        self.w(f"  {r.g} = {r.g} + {sg} * g_exp({r.v}, code);")
+                        self.w(f"  {r.g} = {r.g} + {sg} * g_expm({r.v}, code, xm);")
                     else:
                         self.w(f"  {r.g} = {r.g} + {sg};")
             else:
@@ -1807,6 +1834,82 @@ extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, 
 """
 
 
+def _rw(stmts, reads, writes):
+    """Names read and written by inlined statements; False if a statement
+    kind is not analysed (the caller then keeps every sweep)."""
+    for s in stmts:
+        if isinstance(s, Instr):
+            writes.add(s.target.name)
+            _expr_names(s.target, reads)
+            for a in s.args:
+                _expr_names(a, reads)
+        elif isinstance(s, (Alloc, Dealloc)):
+            writes.add(s.name)
+            _expr_names(s.e, reads)
+        elif isinstance(s, For):
+            writes.add(s.var)
+            for e in (s.a, s.s, s.b):
+                _expr_names(e, reads)
+            if not _rw(s.body, reads, writes):
+                return False
+        elif isinstance(s, (While, If)):
+            for e in (s.pre, s.post):
+                if e is not SAME:
+                    _expr_names(e, reads)
+            bodies = (s.body,) if isinstance(s, While) else (s.then, s.els)
+            if not all(_rw(b, reads, writes) for b in bodies):
+                return False
+        elif isinstance(s, NoCheck):
+            if not _rw(s.body, reads, writes):
+                return False
+        elif isinstance(s, PCall) and s.f in PRIM_ARITY:
+            for v in s.args:
+                writes.add(v.name)
+                _expr_names(v, reads)
+        elif isinstance(s, (ArgCheck, Safe)):
+            for v in getattr(s, "views", ()) + getattr(s, "exprs", ()):
+                _expr_names(v, reads)
+        else:
+            return False
+    return True
+
+
+def _elision_split(body, inliner, fname, params):
+    """Dead-sweep elision, the generated-kernel form of what
+    the hand-written kernels do: a body `@routine R; M; ~@routine` whose R
+    writes only its own ancillas (no parameter cells) and whose M writes
+    nothing R reads or writes.  Then sweep 2 (f's ~R) and sweep 3 (~f's R)
+    re-execute bit-identical primal arithmetic from the same state — R's
+    ancillas are allocated afresh, the parameters it reads unchanged — so the
+    gradient sweep starts from the forward's post-R state, and sweep 2's
+    checks are exactly sweep 4's (the same operations in the same order).
+    Returns (R, M, ~M ~R) as inlined statement tuples, or None."""
+    if len(body) < 2 or not isinstance(body[0], RBegin) or not isinstance(body[-1], REnd):
+        return None
+    depth = 0
+    for pos, st in enumerate(body):                 # the first open closes at the end
+        depth += isinstance(st, RBegin) - isinstance(st, REnd)
+        if depth == 0 and pos < len(body) - 1:
+            return None
+    try:
+        R = inliner.run(_expand(body[0].body), (fname,))
+        M = inliner.run(_expand(body[1:-1]), (fname,))
+        # ~M then ~R, inverted at the source level (calls become uncalls) and
+        # inlined afresh: callee ancillas live only inside their call
+        G = inliner.run(_expand(_invert_list(body[1:-1])) + _invert_list(_expand(body[0].body)),
+                        (fname,))
+    except UnsupportedProgram:
+        return None
+    r_reads, r_writes, m_reads, m_writes = set(), set(), set(), set()
+    if not (_rw(R, r_reads, r_writes) and _rw(M, m_reads, m_writes)):
+        return None
+    if r_writes & set(params):
+        return None
+    if m_writes & (r_reads | r_writes):
+        return None
+    return R, M, G
+
+
 def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_params=()):
     """CUDA source of the batched gradient (mode "grad"), forward-over-reverse
     Hessian-column (mode "hess": the same code over Dual numbers, tangent on
@@ -1840,15 +1943,29 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
         paths = (_leaf_paths(shapes[p]) if p in shapes else
                  [(("field", "re"),), (("field", "im"),)] if kinds[p] == "c" else [()])
         leaves += [(p, path) for path in paths]
-    locals_ = sorted(_collect_vars(fwd, set()) | _collect_vars(inv, set()))
     plain = mode in ("run", "uncall")
+    split = None if plain or os.environ.get("REVGPU_CODEGEN_NO_ELIDE") else \
+        _elision_split(body, inliner, fname, params)
+    locals_ = sorted(_collect_vars(fwd, set()) | _collect_vars(inv, set())
+                     | (set().union(*(_collect_vars(x, set()) for x in split)) if split else set()))
     em_f = _Emitter(params, kinds, inv if mode == "uncall" else fwd, fname, shapes)
     em_f.depth = 2
-    em_f.stmts(inv if mode == "uncall" else fwd, False, "fwd_done")
+    if split is None:
+        em_f.stmts(inv if mode == "uncall" else fwd, False, "fwd_done")
+    else:
+        # sweep 1 up to the end of R (ticks then = the ticks ~f's R would
+        # spend), then M; f's ~R and ~f's R are elided
+        R_, M_, _ = split
+        em_f.stmts(R_, False, "fwd_done")
+        em_f.w("const long long ticks_r = ticks;")
+        em_f.stmts(M_, False, "fwd_done")
     em_g = _Emitter(params, dict(em_f.kinds), inv, fname, shapes)
     em_g.depth = 2
     if not plain:
-        em_g.stmts(inv, True, "grad_done")
+        if split is None:
+            em_g.stmts(inv, True, "grad_done")
+        else:
+            em_g.stmts(split[2], True, "grad_done")
     allk = dict(em_f.kinds)
     allk.update(em_g.kinds)
     decl = []
@@ -1871,12 +1988,15 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
          # element: lanes whose loops end early wait for the rest of the warp
          # instead of drifting onto their next element (a diverged warp ran
          # ~3 of 32 lanes per instruction)
+         "  for (int q = threadIdx.x; q < 1024; q += blockDim.x) rl_exp2tab_s[q] = rl_exp2tab[q];",
+         "  __syncthreads();",
          "  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;"
          " base += (long long)gridDim.x * blockDim.x) {",
          "    __syncwarp();",
          "    const long long i = base + threadIdx.x;",
          "    if (i >= n) continue;",
-         "    int code = 0;", "    long long ticks = 0;"]
+         "    int code = 0;", "    long long ticks = 0;",
+         "    ExpMemo xm = {0.0, 0.0, 0, 0};"]
     # columns: leaf b of every element at fin[b * n + i] (coalesced across the batch)
     for p in floats:
         b, c = base[p], _cid(p)
@@ -1947,7 +2067,8 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
     L.append("    // coerce_to_kind: a seed enters as Dual(seed, 0)")
     L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);")
-    L.append("    ticks = 0;")
+    L.append("    ticks = 0;" if split is None else
+             "    ticks = ticks_r;      // ~f's elided R spends the forward R's ticks")
     L += em_g.lines
     L.append("    if (!code) {      // the backward pass must restore every argument")
     L += ["  " + x for x in each_leaf(
