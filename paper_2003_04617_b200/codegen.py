@@ -907,7 +907,9 @@ __device__ __forceinline__ double g_exp(double x, int &c) {
 }
 // log of an Int: CPython's math.log(i) for 1 <= i < 4096 from the host table
 // `logtab` (a kernel argument), libdevice beyond
+__shared__ double rl_logtab_s[512];        // lt[0, 512) staged at kernel entry
 __device__ __forceinline__ double g_logi(long long k, const double *lt, int &c) {
+  if (k >= 1 && k < 512) return rl_logtab_s[k];
   if (k >= 1 && k < 4096) return lt[k];
   return g_log((double)k, c);
 }
@@ -1037,6 +1039,78 @@ __device__ __forceinline__ long long g_imod(long long a, long long b, int &c) {
   long long r = a % b;
   if (r != 0 && ((r < 0) != (b < 0))) r += b;     // Python's modulo
   return r;
+}
+
+// Chunk sort by a loop-driving key (generate: `sort key`): each block takes
+// RLG_C elements, counting-sorts their indices by 256 linear buckets of the
+// key over the chunk's range, and runs warp rounds of 32 key-neighbours, so
+// a warp's lanes run their data-dependent loops for (nearly) the same trip
+// count (the hand-written Bessel kernel's z-bucket rounds, besselj.cu).
+#ifndef RLG_BLOCK
+#define RLG_BLOCK 128
+#endif
+#ifndef RLG_M
+#define RLG_M 16
+#endif
+#ifndef RLG_MINB
+#define RLG_MINB 6
+#endif
+#define RLG_C (RLG_BLOCK * RLG_M)
+__device__ __forceinline__ void rlg_sort_chunk(const double *__restrict__ key, int cnt, int *hist,
+                                               unsigned short *perm, double *red) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double kv[RLG_M];
+  double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < RLG_M; ++m) {
+    const int e = m * RLG_BLOCK + tid;
+    kv[m] = e < cnt ? key[e] : NAN;
+    if (isfinite(kv[m])) { lo = fmin(lo, kv[m]); hi = fmax(hi, kv[m]); }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) { red[w] = lo; red[RLG_BLOCK / 32 + w] = hi; }
+  for (int b = tid; b < 256; b += RLG_BLOCK) hist[b] = 0;
+  __syncthreads();
+  lo = red[0];
+  hi = red[RLG_BLOCK / 32];
+  for (int q = 1; q < RLG_BLOCK / 32; ++q) { lo = fmin(lo, red[q]); hi = fmax(hi, red[RLG_BLOCK / 32 + q]); }
+  const double sc = hi > lo ? 255.5 / (hi - lo) : 0.0;
+  int bk[RLG_M], rk[RLG_M];
+#pragma unroll
+  for (int m = 0; m < RLG_M; ++m) {
+    const int e = m * RLG_BLOCK + tid;
+    if (e < cnt) {
+      int b = isfinite(kv[m]) ? (int)((kv[m] - lo) * sc) : 255;
+      bk[m] = b < 0 ? 0 : (b > 255 ? 255 : b);
+      rk[m] = atomicAdd(&hist[bk[m]], 1);
+    }
+  }
+  __syncthreads();
+  if (w == 0) {                       // exclusive scan: lane l owns buckets 8l .. 8l+7
+    int loc[8], t = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { loc[q] = t; t += hist[8 * lane + q]; }
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const int basep = x - t;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) hist[8 * lane + q] = basep + loc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < RLG_M; ++m) {
+    const int e = m * RLG_BLOCK + tid;
+    if (e < cnt) perm[hist[bk[m]] + rk[m]] = (unsigned short)e;
+  }
+  __syncthreads();
 }
 """
 
@@ -1823,7 +1897,7 @@ extern "C" int rlg_launch(long long n, const double *fin, const long long *iin, 
                           unsigned char *fail, int dir, double *hout, long long *iout,
                           const double *logtab, void *stream) {
   if (n <= 0) return 0;
-  const int block = 128;
+  const int block = RLG_BLOCK;
   long long grid = (n + block - 1) / block;
   if (grid > 148 * 16) grid = 148 * 16;
   rlg_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(n, fin, iin, seeds, tol, chk, fuel,
@@ -1872,6 +1946,53 @@ def _rw(stmts, reads, writes):
         else:
             return False
     return True
+
+
+def _flat(stmts, out):
+    for st in stmts:
+        out.append(st)
+        for b in ((st.body,) if isinstance(st, (For, While, NoCheck)) else
+                  (st.then, st.els) if isinstance(st, If) else ()):
+            _flat(b, out)
+    return out
+
+
+def _loop_key(stmts, params, kinds):
+    """The one Float scalar parameter that data-dependent while loops depend
+    on (backward slice of their conditions through the statements that
+    write the variables involved), or None: the sort key of the chunk sort."""
+    flat = _flat(stmts, [])
+    need = set()
+    for st in flat:
+        if isinstance(st, While):
+            for e in (st.pre, st.post):
+                if e is not SAME:
+                    _expr_names(e, need)
+    if not need:
+        return None
+    changed = True
+    while changed:
+        changed = False
+        for st in flat:
+            src = set()
+            if isinstance(st, Instr) and st.target.name in need:
+                for a in st.args:
+                    _expr_names(a, src)
+                _expr_names(st.target, src)
+            elif isinstance(st, (Alloc, Dealloc)) and st.name in need:
+                _expr_names(st.e, src)
+            elif isinstance(st, For) and st.var in need:
+                for e in (st.a, st.s, st.b):
+                    _expr_names(e, src)
+            elif isinstance(st, PCall) and st.f in PRIM_ARITY and \
+                    any(v.name in need for v in st.args):
+                for v in st.args:
+                    _expr_names(v, src)
+            if not src <= need:
+                need |= src
+                changed = True
+    keys = [p for p in params if p in need and kinds.get(p) == "f"]
+    return keys[0] if len(keys) == 1 else None
 
 
 def _elision_split(body, inliner, fname, params):
@@ -1977,8 +2098,11 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
                     else f"    R v_{_cid(v)} = R(0.0), g_{_cid(v)} = R(0.0);")
     NL = len(leaves)
     hess = mode == "hess"
-    L = [_PRELUDE, "typedef Dl R;" if hess else "typedef double R;",
-         f"extern \"C\" __global__ void rlg_kernel(long long n, const double *__restrict__ fin,"
+    tune = [f"#define {m} {os.environ[e]}" for m, e in (
+        ("RLG_BLOCK", "REVGPU_CODEGEN_BLOCK"), ("RLG_M", "REVGPU_CODEGEN_M"),
+        ("RLG_MINB", "REVGPU_CODEGEN_MINB")) if os.environ.get(e)]   # tuning sweeps only
+    L = tune + [_PRELUDE, "typedef Dl R;" if hess else "typedef double R;",
+         f"extern \"C\" __global__ void __launch_bounds__(RLG_BLOCK, RLG_MINB) rlg_kernel(long long n, const double *__restrict__ fin,"
          " const long long *__restrict__ iin, const double *__restrict__ seeds,"
          " double tol, int chk, long long fuel, double *__restrict__ fout,"
          " double *__restrict__ gout, unsigned char *__restrict__ fail, int dir,"
@@ -1989,14 +2113,31 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
          # instead of drifting onto their next element (a diverged warp ran
          # ~3 of 32 lanes per instruction)
          "  for (int q = threadIdx.x; q < 1024; q += blockDim.x) rl_exp2tab_s[q] = rl_exp2tab[q];",
-         "  __syncthreads();",
-         "  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;"
-         " base += (long long)gridDim.x * blockDim.x) {",
-         "    __syncwarp();",
-         "    const long long i = base + threadIdx.x;",
-         "    if (i >= n) continue;",
-         "    int code = 0;", "    long long ticks = 0;",
-         "    ExpMemo xm = {0.0, 0.0, 0, 0};"]
+         "  for (int q = threadIdx.x; q < 512; q += blockDim.x) rl_logtab_s[q] = logtab[q];",
+         "  __syncthreads();"]
+    key = None if os.environ.get("REVGPU_CODEGEN_NO_SORT") else _loop_key(fwd, params, kinds)
+    if key is None:
+        L += ["  for (long long base = (long long)blockIdx.x * blockDim.x; base < n;"
+              " base += (long long)gridDim.x * blockDim.x) {",
+              "    __syncwarp();",
+              "    const long long i = base + threadIdx.x;",
+              "    if (i >= n) continue;"]
+    else:                               # rounds of key-sorted elements (rlg_sort_chunk)
+        L += [f"  // chunk sort key: {key} (drives the data-dependent loops)",
+              "  __shared__ int rlg_hist[256];",
+              "  __shared__ unsigned short rlg_perm[RLG_C];",
+              "  __shared__ double rlg_red[2 * RLG_BLOCK / 32];",
+              "  for (long long cbase = (long long)blockIdx.x * RLG_C; cbase < n;"
+              " cbase += (long long)gridDim.x * RLG_C) {",
+              "    const int cnt = n - cbase < RLG_C ? (int)(n - cbase) : RLG_C;",
+              f"    rlg_sort_chunk(fin + {base[key]}LL * n + cbase, cnt, rlg_hist, rlg_perm, rlg_red);",
+              "    for (int m = 0; m < RLG_M; ++m) {",
+              "    __syncwarp();",
+              "    const int pos = m * RLG_BLOCK + (int)threadIdx.x;",
+              "    if (pos >= cnt) continue;",
+              "    const long long i = cbase + rlg_perm[pos];"]
+    L += ["    int code = 0;", "    long long ticks = 0;",
+          "    ExpMemo xm = {0.0, 0.0, 0, 0};"]
     # columns: leaf b of every element at fin[b * n + i] (coalesced across the batch)
     for p in floats:
         b, c = base[p], _cid(p)
@@ -2060,8 +2201,9 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
                      f" iout[({ibase[p]}LL + e) * n + i] = v_{_cid(p)}[e];")
         else:
             L.append(f"    iout[{ibase[p]}LL * n + i] = v_{_cid(p)};")
+    close = ["  }", "}"] if key is None else ["    }", "    __syncthreads();", "  }", "}"]
     if plain:
-        L += ["    fail[i] = 0;", "  }", "}"]
+        L += ["    fail[i] = 0;"] + close
         L.append(_LAUNCH)
         return "\n".join(L), floats, ints, leaves
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
@@ -2086,8 +2228,7 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
     L.append(f"      for (int e = 0; e < {NL}; ++e) fout[e * n + i] = NAN;")
     L.append("    }")
     L.append("    fail[i] = (unsigned char)code;")
-    L.append("  }")
-    L.append("}")
+    L += close
     L.append(_LAUNCH)
     return "\n".join(L), floats, ints, leaves
 
