@@ -68,7 +68,12 @@ const char *rl_last_error(void);
  * Outputs: J[i] = primal out!, dJdz[i] = z.g for out!.g = seed, fail[i].
  * thr: the loop threshold literal of the program (1e-16); tol: the
  * ExecOptions.float_tolerance (interpreter.py:39, 1e-9); max_trips: fuel cap
- * on series terms (FuelExhausted beyond it); invcheck: ExecOptions.invcheck.
+ * on series terms: FuelExhausted for an element needing more trips, -1 for
+ * every element that passes the z > 0 check.  The reference's fuel
+ * (ExecOptions.max_steps, statement executions per sweep, interpreter.py:
+ * 461-466) maps exactly: besselj runs 31 + 6 nu + 22 T statements in each
+ * sweep, so max_trips = (max_steps - 31 - 6 max(nu, 0)) div 22 (floor,
+ * at least -1); invcheck: ExecOptions.invcheck.
  * counters[0] += sum of the series trips of the elements that succeed (the
  * oracle's definition), counters[1] += failed elements.
  * ---------------------------------------------------------------------- */

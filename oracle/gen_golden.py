@@ -607,6 +607,38 @@ def gen_codegen_complex():
     print("complex goldens:", Counter(out["err_re"]), Counter(HE))
 
 
+def gen_bessel_fuel():
+    """FuelExhausted boundaries of besselj (ExecOptions.max_steps counts
+    statement executions per interpreter, interpreter.py:461-466): for each
+    (nu, z) the reference's step count S of one run (read from the
+    interpreter's stats), then the outcomes of gradient(), run() and
+    hessian() at max_steps = S (fits) and S - 1 (FuelExhausted)."""
+    from revlang.autodiff import hessian
+    from revlang.interpreter import Interpreter
+    p = parse_program(open(os.path.join(PROG_DIR, "besselj.rnl")).read())
+    cases = [(nu, z) for nu in (0, 1, 2, 5) for z in (0.05, 0.7, 3.0, 8.0, 13.0)]
+    NU, Z, S, T = [], [], [], []
+    out = {}
+    for nu, z in cases:
+        it = Interpreter(p, ExecOptions())
+        it.run_function("besselj", [0.0, nu, z])
+        steps = it.stats.steps
+        NU.append(nu)
+        Z.append(z)
+        S.append(steps)
+        T.append((steps - 31 - 6 * nu) // 22)
+        for tag, fn in (("grad", lambda o: gradient(p, GradRequest("besselj", [0.0, nu, z]), o)),
+                        ("run", lambda o: run(p, "besselj", [0.0, nu, z], o)),
+                        ("hess", lambda o: hessian(p, "besselj", [0.0, nu, z], o))):
+            for off in (0, -1):
+                _, en = _err_name(lambda: fn(ExecOptions(max_steps=steps + off)))
+                out.setdefault(f"{tag}_{-off}", []).append(en)
+    np.savez_compressed(os.path.join(OUT_DIR, "bessel_fuel.npz"), nu=np.array(NU), z=np.array(Z),
+                        steps=np.array(S), trips=np.array(T),
+                        **{k: np.array(v) for k, v in out.items()})
+    print("fuel goldens:", list(zip(NU, Z, S)), {k: sorted(set(v)) for k, v in out.items()})
+
+
 def gen_codegen_complex_fd():
     """reference finite_difference() of polar.rnl (Complex arguments: re/im
     leaves, default seed y!.re and an explicit y!.im seed), h = 1e-6."""
@@ -635,6 +667,6 @@ if __name__ == "__main__":
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
                               "codegen_random",
-                              "codegen_complex", "codegen_complex_fd"]
+                              "codegen_complex", "codegen_complex_fd", "bessel_fuel"]
     for w in which:
         globals()["gen_" + w]()

@@ -268,6 +268,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   int code = 0;
   // ---------------- sweep 1: forward routine ----------------
   if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
+  if (kfuel < 0 && valid && !code) code = RL_ERR_FUEL;   // the prologue alone exceeds max_steps
   const double logz = (valid && !code) ? log(z) : 0.0;
   double halfz = 0.0 + (0.0 + logz);                     // lz = 0 + log z; halfz *= lz
   halfz = halfz - LN2;                                   // halfz /= 2
@@ -542,6 +543,7 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
   int code = 0;
   // ---------------- sweep 3 (= sweep 1 primal): R over Duals ----------------
   if (valid && !(z > 0.0)) code = RL_ERR_DOMAIN;        // lz *= convert(z)
+  if (kfuel < 0 && valid && !code) code = RL_ERR_FUEL;   // the prologue alone exceeds max_steps
   const bool zok = valid && !code;
   const Dl Z{z, 1.0};
   const Dl clz{zok ? log(z) : 0.0, zok ? 1.0 / z : 0.0};   // s_log(Dual(z, 1))
@@ -731,7 +733,8 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
     unsigned long long *counters, double sfloor, double *__restrict__ d2out) {
   constexpr bool GRAD = MODE >= BJ_GRAD;
   const int ktab = BJ_KP - 1;
-  const int kfuel = (int)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
+  // trip cap: -1 = the prologue alone exceeds the reference's max_steps
+  const int kfuel = (int)(max_trips < 0 ? -1 : (max_trips < (1LL << 30) ? max_trips : (1LL << 30)));
   __shared__ int s_hist[BJ_NB];
   __shared__ int s_wsum[BJ_WARPS];
   __shared__ int s_round;
@@ -919,7 +922,7 @@ static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, 
   const long long cap = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   const int grid = (int)(want < cap ? want : cap);
   // FAST-flavour safety bound (besselj_element): log(thr) - 2 log(kfuel + |nu| + 1)
-  const double kfuel = (double)(max_trips < (1LL << 30) ? max_trips : (1LL << 30));
+  const double kfuel = (double)(max_trips < 0 ? 0 : (max_trips < (1LL << 30) ? max_trips : (1LL << 30)));
   const double sfloor = log(thr) - 2.0 * log(kfuel + fabs((double)nu) + 1.0);
   k_besselj<MODE><<<grid, BJ_BLOCK, smem, st>>>(nu, z, n, thr, tol, seed, max_trips,
                                                 invcheck ? 1 : 0, out_in, sign, J, dJdz, fail,
@@ -930,7 +933,7 @@ static int launch_besselj_t(int32_t nu, const double *z, int64_t n, double thr, 
 int launch_besselj(int32_t nu, const double *z, int64_t n, double thr, double tol, double seed,
                    int64_t max_trips, int32_t invcheck, double *J, double *dJdz, uint8_t *fail,
                    unsigned long long *counters, cudaStream_t st) {
-  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)) || max_trips < 0)
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !fail)) || max_trips < -1)
     return set_error(RL_ERR_INVALID, "rl_besselj_grad_f64: bad argument");
   return launch_besselj_t<BJ_GRAD>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0,
                                    J, dJdz, nullptr, fail, counters, st);
@@ -940,7 +943,7 @@ int launch_besselj_hess(int32_t nu, const double *z, int64_t n, double thr, doub
                         double seed, int64_t max_trips, int32_t invcheck, double *J,
                         double *dJdz, double *d2Jdz2, uint8_t *fail,
                         unsigned long long *counters, cudaStream_t st) {
-  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !d2Jdz2 || !fail)) || max_trips < 0)
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !d2Jdz2 || !fail)) || max_trips < -1)
     return set_error(RL_ERR_INVALID, "rl_besselj_hess_f64: bad argument");
   return launch_besselj_t<BJ_HESS>(nu, z, n, thr, tol, seed, max_trips, invcheck, nullptr, 1.0,
                                    J, dJdz, d2Jdz2, fail, counters, st);
@@ -950,7 +953,7 @@ int launch_besselj_run(int32_t nu, const double *z, int64_t n, double thr, doubl
                        int64_t max_trips, int32_t invcheck, int32_t direction,
                        const double *out_in, double *out, uint8_t *fail,
                        unsigned long long *counters, cudaStream_t st) {
-  if (n < 0 || (n > 0 && (!z || !out || !fail)) || max_trips < 0 ||
+  if (n < 0 || (n > 0 && (!z || !out || !fail)) || max_trips < -1 ||
       (direction != 1 && direction != -1))
     return set_error(RL_ERR_INVALID, "rl_besselj_run_f64: bad argument");
   return launch_besselj_t<BJ_RUN>(nu, z, n, thr, tol, 0.0, max_trips, invcheck, out_in,

@@ -21,10 +21,21 @@ from . import _native
 from .errors import KindError
 
 F64 = torch.float64
-# ExecOptions.max_steps (reference interpreter.py:40) -> series-term cap.
-# One series term costs ~12 statement ticks in each of the 4 reference
-# sweeps; the cap is the corresponding trip count.
-TICKS_PER_TRIP = 48
+# ExecOptions.max_steps (reference interpreter.py:40) -> series-trip cap.
+# The reference counts one step per statement execution (Interpreter._tick,
+# interpreter.py:461-466) and raises FuelExhausted past max_steps, with a
+# fresh count for the forward run and for the gradient's uncall.  For
+# programs/besselj.rnl both sweeps execute exactly 31 + 6 nu + 22 T
+# statements for T series trips (measured on the reference and pinned by
+# tests/golden/bessel_fuel.npz), so an element exhausts the fuel iff it
+# needs more than (max_steps - 31 - 6 nu) // 22 trips; -1 = even the
+# prologue does not fit (every element that reaches the loop fails).
+BJ_TICKS_BASE, BJ_TICKS_NU, BJ_TICKS_TRIP = 31, 6, 22
+
+
+def bessel_trip_cap(max_steps, nu):
+    cap = (int(max_steps) - BJ_TICKS_BASE - BJ_TICKS_NU * max(int(nu), 0)) // BJ_TICKS_TRIP
+    return max(cap, -1)
 
 
 def _stream_handle():
@@ -104,7 +115,7 @@ def besselj_grad(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
     counters = _check_out("counters", counters, z, torch.int64, 2)
     L = _native.lib()
     rc = L.rl_besselj_grad_f64(int(nu), _ptr(z), n, float(thr), float(tol), float(seed),
-                               max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)),
+                               bessel_trip_cap(max_steps, nu), int(bool(invcheck)),
                                _ptr(J), _ptr(dz), _ptr(fail), _ptr(counters), _stream_handle())
     _native.check(rc, "rl_besselj_grad_f64")
     return BesselResult(J, dz, fail, counters)
@@ -136,7 +147,7 @@ def besselj_hess(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
         counters = torch.zeros(2, dtype=torch.int64, device=z.device)
     L = _native.lib()
     rc = L.rl_besselj_hess_f64(int(nu), _ptr(z), n, float(thr), float(tol), float(seed),
-                               max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)),
+                               bessel_trip_cap(max_steps, nu), int(bool(invcheck)),
                                _ptr(J), _ptr(dz), _ptr(d2), _ptr(fail), _ptr(counters),
                                _stream_handle())
     _native.check(rc, "rl_besselj_hess_f64")
@@ -162,7 +173,7 @@ def besselj_grad_host(z, nu=2, *, seed=1.0, thr=1e-16, tol=1e-9, invcheck=True,
     dev = torch.cuda.current_device() if device is None else int(device)
     L = _native.lib()
     rc = L.rl_besselj_grad_f64_host(int(nu), zh.ctypes.data, n, float(thr), float(tol),
-                                    float(seed), max(1, int(max_steps) // TICKS_PER_TRIP),
+                                    float(seed), bessel_trip_cap(max_steps, nu),
                                     int(bool(invcheck)), J.ctypes.data, dz.ctypes.data,
                                     fail.ctypes.data, ctypes.byref(trips), ctypes.byref(nfail),
                                     dev)
@@ -416,7 +427,7 @@ def besselj_run(z, nu=2, *, out_in=None, direction=1, thr=1e-16, tol=1e-9, invch
         counters = torch.zeros(2, dtype=torch.int64, device=z.device)
     rc = _native.lib().rl_besselj_run_f64(
         int(nu), _ptr(z), z.numel(), float(thr), float(tol),
-        max(1, int(max_steps) // TICKS_PER_TRIP), int(bool(invcheck)), int(direction),
+        bessel_trip_cap(max_steps, nu), int(bool(invcheck)), int(direction),
         _ptr(out_in), _ptr(out), _ptr(fail), _ptr(counters), _stream_handle())
     _native.check(rc, "rl_besselj_run_f64")
     return RunResult(out, fail, counters)

@@ -70,7 +70,7 @@ def test_edge_inputs_and_error_classes(cuda, oracle):
     z = np.array([0.0, -1.0, -0.0, np.nan, np.inf, 1e-300, 1e-12, 20.0, 30.0, 800.0, 1.0])
     for nu in (0, 2, -1):
         J, dz, fail, _ = run(z, nu, cuda, max_steps=48 * 5000)
-        Jo, dzo, fo, _ = oracle.besselj_grad(nu, z, max_trips=5000)
+        Jo, dzo, fo, _ = oracle.besselj_grad(nu, z, max_trips=rg.kernels.bessel_trip_cap(48 * 5000, nu))
         assert np.array_equal(fail, fo), (nu, fail, fo)
         ok = fo == 0
         assert close_series(J[ok], Jo[ok], nu, z[ok]).all()
@@ -226,3 +226,24 @@ def test_random_sweep_vs_oracle(cuda, oracle):
         # the cotangent carries the seed: its absolute floor scales with |seed|
         assert np.all(np.abs(dz[ok] - dzo[ok]) <= 1e-12 * np.abs(dzo[ok])
                       + 5e-14 * abs(seed) * scale[ok]), (nu, lo, hi, thr, seed)
+
+
+def test_fuel_boundaries_match_the_reference(cuda, golden):
+    """FuelExhausted exactly where the reference raises it: at max_steps = S
+    (the reference's statement count of one sweep) every entry point
+    succeeds, at S - 1 each raises FuelExhausted (bessel_fuel.npz, generated
+    by the reference's gradient / run / hessian)."""
+    G = golden("bessel_fuel")
+    for nu, z, steps in zip(G["nu"], G["z"], G["steps"]):
+        zt = torch.tensor([float(z)], dtype=torch.float64, device=cuda)
+        for off, want in ((0, 0), (1, 6)):
+            ms = int(steps) - off
+            assert int(rg.besselj_grad(zt, int(nu), max_steps=ms).fail[0]) == want, (nu, z, off)
+            assert int(rg.besselj_run(zt, int(nu), max_steps=ms).fail[0]) == want, (nu, z, off)
+            assert int(rg.besselj_hess(zt, int(nu), max_steps=ms).fail[0]) == want, (nu, z, off)
+        p = rg.load_example("besselj")
+        with pytest.raises(rg.FuelExhausted):
+            rg.gradient(p, rg.GradRequest("besselj", [0.0, int(nu), float(z)]),
+                        rg.ExecOptions(max_steps=int(steps) - 1))
+        rg.gradient(p, rg.GradRequest("besselj", [0.0, int(nu), float(z)]),
+                    rg.ExecOptions(max_steps=int(steps)))

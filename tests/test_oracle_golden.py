@@ -141,3 +141,17 @@ def test_oracle_hessian_bit_identical_to_reference(oracle, golden):
         assert (H[ok, 0, :] == 0).all() and (H[ok, :, 0] == 0).all()
         Jg, dzg, fg, _ = oracle.besselj_grad(int(nu), z)
         assert np.array_equal(J[ok], Jg[ok]) and np.array_equal(dz[ok], dzg[ok])
+
+
+def test_bessel_fuel_formula_matches_reference_step_counts(oracle, golden):
+    """The reference's statement count of one besselj sweep (read from its
+    interpreter, bessel_fuel.npz) is 31 + 6 nu + 22 T for T series trips
+    (the oracle's trip count): the exact fuel map kernels.bessel_trip_cap."""
+    from paper_2003_04617_b200.kernels import bessel_trip_cap
+    G = golden("bessel_fuel")
+    for nu, z, steps in zip(G["nu"], G["z"], G["steps"]):
+        _, _, f, trips = oracle.besselj_grad(int(nu), np.array([z]))
+        assert f[0] == 0
+        assert steps == 31 + 6 * int(nu) + 22 * int(trips)
+        assert bessel_trip_cap(steps, int(nu)) == int(trips)
+        assert bessel_trip_cap(steps - 1, int(nu)) == int(trips) - 1
