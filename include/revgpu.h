@@ -126,6 +126,10 @@ int rl_ba_jac_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const doubl
  *   per-point terms of this shard are produced (for a sum-allreduce across
  *   ranks); with 1 the parameter-only terms (-N_total*lse(alphas), Wishart
  *   prior, cst) are added too.  fail: N per-point flags.
+ * counters[0] += the argmax record steps taken over the points (the number
+ * of times a later component beats the running max: the data-dependent part
+ * of the reference's statement count, see rl_gmm_statement_count),
+ * counters[1] += failed points.
  * ws: device workspace of rl_gmm_workspace_bytes() bytes.
  * d <= 128 (the kernels' widest tile): d > 128 is RL_ERR_INVALID and
  * rl_gmm_workspace_bytes returns 0; the Python drop-in sends such calls to
@@ -142,6 +146,18 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          const double *means, const double *icf, const double *x, double gamma,
                          int32_t m, double cst, double tol, int32_t invcheck, double *out,
                          unsigned long long *n_failed, int32_t device);
+
+/* ------------------------------------------------------------------------
+ * The reference's fuel for gmm (ExecOptions.max_steps counts statement
+ * executions per interpreter, interpreter.py:461-466): one sweep of
+ * programs/gmm.rnl (the run, and the gradient's uncall alike) executes
+ *   N (6 K d^2 + 22 K d + 48 K + 13) + 4 U + 3 K d^2 + 9 K d + 28 K + 4 A + 33
+ * statements, U = the points' argmax record steps (counters[0] of the GMM
+ * entries), A = those of the alphas' logsumexp (measured on the reference,
+ * pinned by tests/golden/gmm_fuel.npz).  FuelExhausted iff it exceeds
+ * max_steps.  Host-only arithmetic.
+ * ---------------------------------------------------------------------- */
+int64_t rl_gmm_statement_count(int32_t d, int32_t K, int64_t N, int64_t U, int64_t A);
 
 /* ------------------------------------------------------------------------
  * The whole gradient() call of gmm on one device, in the reference's order:

@@ -28,7 +28,7 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, REF_SRC)
 from revlang import ExecOptions, GradRequest, gradient, parse_program, run, uncall  # noqa: E402
 from revlang.errors import RevLangError  # noqa: E402
-from revlang.values import Array  # noqa: E402
+from revlang.values import Array, deep_copy  # noqa: E402
 
 
 def _prog(name):
@@ -639,6 +639,64 @@ def gen_bessel_fuel():
     print("fuel goldens:", list(zip(NU, Z, S)), {k: sorted(set(v)) for k, v in out.items()})
 
 
+def gen_gmm_fuel():
+    """Statement counts of programs/gmm.rnl in the reference (the fuel unit of
+    ExecOptions.max_steps) over small (d, K, N), from the run's interpreter
+    stats, and the gradient's outcome at max_steps = S and S - 1."""
+    from revlang.interpreter import Interpreter
+    p = parse_program(open(os.path.join(PROG_DIR, "gmm.rnl")).read())
+    A = lambda a: Array.matrix(a.tolist()) if a.ndim == 2 else Array.vector(a.tolist())  # noqa
+    out = {k: [] for k in ("dims", "alphas", "means", "icf", "x", "steps", "grad_0", "grad_1")}
+    for ci, (d, K, N) in enumerate(((2, 3, 4), (3, 4, 6), (5, 2, 3), (4, 6, 5))):
+        rng = np.random.default_rng(500 + ci)
+        al, me = rng.normal(0, 1, K), rng.uniform(0, 1, (K, d))
+        ic, x = rng.normal(0, 1, (K, d * (d + 1) // 2)), rng.uniform(0, 1, (N, d))
+        Z = lambda *s: A(np.zeros(s))  # noqa: E731
+        args = [0.0, A(al), A(me), A(ic), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K),
+                Array.vector([0] * K), 1.0, 0, 0.5]
+        it = Interpreter(p, ExecOptions())
+        it.run_function("gmm", [deep_copy(a) for a in args])
+        steps = it.stats.steps
+        for off in (0, 1):
+            _, en = _err_name(lambda: gradient(p, GradRequest("gmm", [deep_copy(a) for a in args]),
+                                               ExecOptions(max_steps=steps - off,
+                                                           float_tolerance=1e-6)))
+            out[f"grad_{off}"].append(en)
+        for k, v in (("dims", [d, K, N]), ("alphas", al), ("means", me.ravel()),
+                     ("icf", ic.ravel()), ("x", x.ravel()), ("steps", steps)):
+            out[k].append(np.asarray(v))
+    flat = {"ncases": np.array(len(out["steps"])), "steps": np.array(out["steps"]),
+            "grad_0": np.array(out["grad_0"]), "grad_1": np.array(out["grad_1"])}
+    for ci in range(len(out["steps"])):
+        for k in ("dims", "alphas", "means", "icf", "x"):
+            flat[f"c{ci}_{k}"] = np.asarray(out[k][ci])
+    np.savez_compressed(os.path.join(OUT_DIR, "gmm_fuel.npz"), **flat)
+    print("gmm fuel goldens:", out["steps"], out["grad_0"], out["grad_1"])
+
+
+def gen_ba_fuel():
+    """The reference's statement counts of ba_proj (with / without rotation)
+    and ba_weight, and the gradient's outcome at max_steps = S and S - 1."""
+    from revlang.interpreter import Interpreter
+    p = parse_program(open(os.path.join(PROG_DIR, "ba.rnl")).read())
+    out = {"rot": [], "steps": [], "grad_0": [], "grad_1": []}
+    for rot in ([0.1, -0.2, 0.3], [0.0, 0.0, 0.0]):
+        cam = Array.vector(rot + [0.1, 0.2, 0.3, 550.0, 0.5, 0.5, 0.001, -0.002])
+        X = Array.vector([0.3, -0.4, 10.0])
+        for fn, args in (("ba_proj", [0.0, 0.0, cam, X, 0.7, 3.0, 4.0]), ("ba_weight", [0.0, 0.7])):
+            it = Interpreter(p, ExecOptions())
+            it.run_function(fn, [deep_copy(a) for a in args])
+            steps = it.stats.steps
+            out["rot"].append(list(rot) + [1.0 if fn == "ba_proj" else 0.0])
+            out["steps"].append(steps)
+            for off in (0, 1):
+                _, en = _err_name(lambda: gradient(p, GradRequest(fn, [deep_copy(a) for a in args]),
+                                                   ExecOptions(max_steps=steps - off)))
+                out[f"grad_{off}"].append(en)
+    np.savez_compressed(os.path.join(OUT_DIR, "ba_fuel.npz"), **{k: np.array(v) for k, v in out.items()})
+    print("ba fuel goldens:", out)
+
+
 def gen_codegen_complex_fd():
     """reference finite_difference() of polar.rnl (Complex arguments: re/im
     leaves, default seed y!.re and an explicit y!.im seed), h = 1e-6."""
@@ -667,6 +725,6 @@ if __name__ == "__main__":
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
                               "codegen_random",
-                              "codegen_complex", "codegen_complex_fd", "bessel_fuel"]
+                              "codegen_complex", "codegen_complex_fd", "bessel_fuel", "gmm_fuel", "ba_fuel"]
     for w in which:
         globals()["gen_" + w]()

@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import kernels
-from .errors import KindError, UnknownFunction, UnsupportedProgram, error_for_code
+from .errors import (FuelExhausted, KindError, UnknownFunction, UnsupportedProgram,
+                     error_for_code)
 from .programs import as_program
 from .values import like, to_numpy
 
@@ -177,6 +178,23 @@ def _ba_device_call(cam, X, w, f1, f2, opts):
     return (r.J[0].cpu().numpy(), r.err[0].cpu().numpy(), r.Jfeat[0].cpu().numpy())
 
 
+# The reference's fuel for one BA call (ExecOptions.max_steps = statement
+# executions per sweep, interpreter.py:461-466), measured on the reference:
+# ba_proj runs 222 statements with a rotation (rodrigues) and 96 without
+# (sqt == 0), ba_weight 2; both sweeps alike.
+BA_PROJ_STEPS, BA_PROJ_STEPS_NOROT, BA_WEIGHT_STEPS = 222, 96, 2
+
+
+def ba_fuel_check(camv, max_steps, fname="ba_proj"):
+    if fname == "ba_weight":
+        steps = BA_WEIGHT_STEPS
+    else:
+        sqt = ((0.0 + camv[0] * camv[0]) + camv[1] * camv[1]) + camv[2] * camv[2]
+        steps = BA_PROJ_STEPS if sqt != 0.0 else BA_PROJ_STEPS_NOROT
+    if steps > max_steps:
+        raise FuelExhausted(f"exceeded {max_steps} statement executions ({fname} runs {steps})")
+
+
 def _grad_ba_proj(fdef, req, opts):
     names = fdef.param_names()
     if len(req.args) != 7:
@@ -186,6 +204,7 @@ def _grad_ba_proj(fdef, req, opts):
     Xv = to_numpy(X, "X", 1)
     if camv.shape != (11,) or Xv.shape != (3,):
         raise KindError("cam must have 11 entries and X 3")
+    ba_fuel_check(camv, opts.max_steps)
     J, err, Jf = _ba_device_call(camv, Xv, float(w), float(f1), float(f2), opts)
     seeds = _seed_map(req.seeds, names, names[0])
     a = seeds.get((names[0], ()), 0.0)
@@ -219,6 +238,7 @@ def _grad_ba_weight(fdef, req, opts):
     if len(req.args) != 2:
         raise KindError(f"ba_weight takes 2 arguments, got {len(req.args)}")
     e0, w = req.args
+    ba_fuel_check(None, opts.max_steps, "ba_weight")
     cam = np.zeros(11)
     cam[6] = 1.0
     J, err, _ = _ba_device_call(cam, np.array([0.0, 0.0, 1.0]), float(w), 0.0, 0.0, opts)
@@ -264,9 +284,7 @@ def _grad_gmm(fdef, req, opts):
     t = lambda v: torch.as_tensor(v, device=dev)  # noqa: E731
     r = kernels.gmm_gradient(t(al), t(mu), t(ic), t(xv), float(ga), int(wm), float(cst),
                              err0=float(err0), tol=opts.float_tolerance, invcheck=opts.invcheck)
-    fails = r.fail.cpu().numpy()
-    if fails.any():
-        raise error_for_code(int(fails[np.nonzero(fails)[0][0]]), "gmm")
+    gmm_fuel_check(al, mu.shape[1], xv.shape[0], r, opts.max_steps)
     # the reference's primal-restoration check (autodiff.py:169-172), decided
     # on the device from err! after the gradient sweep (k_gmm_restore)
     code = int(r.restore_code.item())
@@ -305,6 +323,28 @@ def gradient(program, req, opts=None):
         from . import generic
         return generic.gradient(prog, fdef, req, opts)
     return _HANDLERS[fdef.kernel.handler](fdef, req, opts)
+
+
+def gmm_fuel_check(alphas, d, N, r, max_steps):
+    """The reference's fuel for gmm (kernels.gmm_statement_count, exact), then
+    the first failing point's error.  A point error precedes the fuel
+    exhaustion when it is reached within max_steps statements; its position
+    is taken at the end of its point with the argmax steps spread evenly
+    (exact unless both fall in the same point)."""
+    K = int(np.shape(alphas)[0])
+    U = int(r.counters[0].item())
+    A = kernels.gmm_alpha_updates(alphas)
+    steps = kernels.gmm_statement_count(d, K, N, U, A)
+    fails = r.fail.cpu().numpy()
+    first = int(np.nonzero(fails)[0][0]) if fails.any() else None
+    if first is not None:
+        per = kernels.gmm_statement_count(d, K, 1, 0, 0) - kernels.gmm_statement_count(d, K, 0, 0, 0)
+        at = (first + 1) * per + (4 * U * (first + 1)) // max(N, 1)
+        if at <= max_steps:
+            raise error_for_code(int(fails[first]), "gmm")
+    if steps > max_steps:
+        raise FuelExhausted(f"exceeded {max_steps} statement executions "
+                            f"(gmm runs {steps} per sweep)")
 
 
 def gmm_beyond_tiles(fdef, args):

@@ -496,6 +496,12 @@ int rl_gmm_run_f64(int32_t d, int32_t K, int64_t N, const double *alphas, const 
                     counters, ws, ws_bytes, as_stream(stream), 0, &seq);
 }
 
+int64_t rl_gmm_statement_count(int32_t d, int32_t K, int64_t N, int64_t U, int64_t A) {
+  const int64_t dd = d, kk = K;
+  return N * (6 * kk * dd * dd + 22 * kk * dd + 48 * kk + 13) + 4 * U + 3 * kk * dd * dd +
+         9 * kk * dd + 28 * kk + 4 * A + 33;
+}
+
 int rl_seq_sum_f64(const double *t, int64_t M, double e0, int64_t mark, int32_t force_serial,
                    double *out2, int32_t *verified, void *stream) {
   return launch_seq_sum(t, M, e0, mark, force_serial, out2, verified, as_stream(stream));

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
 
   const long long i = (long long)blockIdx.x * LSE_THREADS + threadIdx.x;
   double e_pt = 0.0;
-  unsigned long long nfail = 0;
+  unsigned long long nfail = 0, nupd = 0;
   if (i < N) {
     int code = 0;
     const double *mt = mtT + i;
@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
       if (v > vmx) {
         imx = k;
         vmx = v;
+        nupd++;
       }
     }
     const double mx = 0.0 + vmx;                          // mx <- 0.0; mx += mt![imx]
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(LSE_THREADS) k_gmm_lse(
     __syncthreads();
   }
   if (threadIdx.x == 0) err_part[blockIdx.x] = red[0];
-  block_add_counters<LSE_THREADS>(0, nfail, counters);
+  block_add_counters<LSE_THREADS>(nupd, nfail, counters);
 }
 
 // The same per-point routine with LSE_LANES lanes per point (K <= LSE_QK):
@@ -552,7 +553,7 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
   const long long i = (long long)blockIdx.x * LSE_THREADS + pl;
   double *ex = lse_ex + pl * K;
   double e_pt = 0.0;
-  unsigned long long nfail = 0;
+  unsigned long long nfail = 0, nupd = 0;
   if (i < N) {                                           // uniform over the quad
     const double *mt = mtT + i;
     double *gmt = gmtT + i;
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
       if (v > vmx) {
         imx = k;
         vmx = v;
+        nupd += q == 0;                                  // one lane per point counts
       }
     }
     const double mx = 0.0 + vmx;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
     __syncthreads();
   }
   if (threadIdx.x == 0) err_part[blockIdx.x] = red[0];
-  block_add_counters<LSE_THREADS * LSE_LANES>(0, nfail, counters);
+  block_add_counters<LSE_THREADS * LSE_LANES>(nupd, nfail, counters);
 }
 
 // ---------------------------------------------------------------------------

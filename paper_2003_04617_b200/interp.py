@@ -15,7 +15,8 @@ import numpy as np
 import torch
 
 from . import kernels
-from .autodiff import _check_opts, _device, _is_float, _is_int, _lookup, gmm_beyond_tiles
+from .autodiff import (_check_opts, _device, _is_float, _is_int, _lookup, gmm_beyond_tiles,
+                       ba_fuel_check, gmm_fuel_check)
 from .errors import KindError, RevLangError, error_for_code
 from .values import to_numpy
 
@@ -45,6 +46,7 @@ def _run_ba_proj(fdef, args, opts, direction):
     if len(args) != 7:
         raise KindError(f"ba_proj takes 7 arguments, got {len(args)}")
     e1, e2, cam, X, w, f1, f2 = args
+    ba_fuel_check(to_numpy(cam, "cam"), opts.max_steps)
     dev = _device()
     tt = lambda a: torch.as_tensor(np.asarray(a, np.float64), device=dev)  # noqa: E731
     r = kernels.ba_residuals(tt(to_numpy(cam, "cam").reshape(1, 11)),
@@ -63,6 +65,7 @@ def _run_ba_weight(fdef, args, opts, direction):
     if len(args) != 2:
         raise KindError(f"ba_weight takes 2 arguments, got {len(args)}")
     e0, w = args
+    ba_fuel_check(None, opts.max_steps, "ba_weight")
     dev = _device()
     tt = lambda a: torch.as_tensor(np.asarray(a, np.float64), device=dev)  # noqa: E731
     cam = np.zeros(11)
@@ -91,7 +94,7 @@ def _run_gmm(fdef, args, opts, direction):
     # err! accumulated from err0 in the order of gmm (run) or ~gmm (uncall)
     r = kernels.gmm_run(*a, err0=float(err0), direction=direction, tol=opts.float_tolerance,
                         invcheck=opts.invcheck)
-    _raise_first(r.fail, "gmm")
+    gmm_fuel_check(a[0], a[1].shape[1], a[3].shape[0], r, opts.max_steps)
     return [float(r.out.item())] + list(args[1:])
 
 

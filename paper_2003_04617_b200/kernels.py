@@ -15,6 +15,7 @@ CUDA kernels.  No CPU path exists: non-CUDA inputs raise.
 import ctypes
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _native
@@ -302,6 +303,23 @@ def gmm_grad(alphas, means, icf, x, gamma=1.0, m=0, cst=0.0, *, N_total=None,
                            workspace.numel(), _stream_handle())
     _native.check(rc, "rl_gmm_grad_f64")
     return unpack_gmm(packed, d, K, fail, counters)
+
+
+def gmm_statement_count(d, K, N, U, A):
+    """Statements one sweep of programs/gmm.rnl executes in the reference
+    (its fuel unit, interpreter.py:461-466): rl_gmm_statement_count."""
+    return int(_native.lib().rl_gmm_statement_count(int(d), int(K), int(N), int(U), int(A)))
+
+
+def gmm_alpha_updates(alphas):
+    """Argmax record steps of the alphas' reversible logsumexp (gmm.rnl): how
+    often a later alpha beats the running max."""
+    a = np.asarray(alphas.cpu() if isinstance(alphas, torch.Tensor) else alphas, np.float64)
+    n, best = 0, 0
+    for k in range(1, a.shape[0]):
+        if a[k] > a[best]:
+            best, n = k, n + 1
+    return n
 
 
 def _gmm_args(alphas, means, icf, x):

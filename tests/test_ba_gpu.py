@@ -157,3 +157,20 @@ def test_dropin_gradient_and_jacobian(cuda, golden):
         assert J[0, 17] == -b["w"][o] and J[1, 18] == -b["w"][o]
     _, g = rg.gradient(p, rg.GradRequest("ba_weight", [0.0, 0.75]))
     assert g["w"] == -1.5 and g["e!"] == 1.0
+
+
+def test_fuel_matches_the_reference(cuda, golden):
+    """ExecOptions.max_steps: ba_proj runs 222 statements (96 without a
+    rotation), ba_weight 2 (ba_fuel.npz, the reference's interpreter
+    counts); gradient() raises FuelExhausted exactly below them."""
+    G = golden("ba_fuel")
+    p = rg.load_example("ba_proj")
+    for row, steps, ok0, ok1 in zip(G["rot"], G["steps"], G["grad_0"], G["grad_1"]):
+        assert ok0 == "" and ok1 == "FuelExhausted"
+        cam = rg.Array.vector(list(row[:3]) + [0.1, 0.2, 0.3, 550.0, 0.5, 0.5, 0.001, -0.002])
+        X = rg.Array.vector([0.3, -0.4, 10.0])
+        fn, args = (("ba_proj", [0.0, 0.0, cam, X, 0.7, 3.0, 4.0]) if row[3] else
+                    ("ba_weight", [0.0, 0.7]))
+        rg.gradient(p, rg.GradRequest(fn, args), rg.ExecOptions(max_steps=int(steps)))
+        with pytest.raises(rg.FuelExhausted):
+            rg.gradient(p, rg.GradRequest(fn, args), rg.ExecOptions(max_steps=int(steps) - 1))

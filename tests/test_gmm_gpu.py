@@ -134,7 +134,8 @@ def test_config3_full_size_vs_oracle(cuda, oracle):
         Z = lambda *s: A(np.zeros(s))  # noqa: E731
         args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), Z(K),
                 1.0, 0, cst]
-        rg.gradient(p, rg.GradRequest("gmm", args), rg.ExecOptions(float_tolerance=1e-12))
+        rg.gradient(p, rg.GradRequest("gmm", args),            # fuel for 6.5e9 statements
+                    rg.ExecOptions(float_tolerance=1e-12, max_steps=10**11))
     rc, e, resid, ga, gm, gi = oracle.gmm_grad_ex(alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
     assert rc == 0
     got = run_full(cuda, alphas, means, icf, x, 1.0, 0, cst, tol=1e-6)
@@ -273,3 +274,48 @@ def test_dropin_gradient(cuda, golden):
     bad[7] = rg.Array.vector([1.0] + [0.0] * (d - 1))
     with pytest.raises(rg.KindError):
         rg.gradient(p, rg.GradRequest("gmm", bad))
+
+
+def test_fuel_matches_the_reference(cuda, golden):
+    """ExecOptions.max_steps for gmm: the reference's statement count (its
+    interpreter's stats, gmm_fuel.npz) equals rl_gmm_statement_count over the
+    device's argmax-step counter, and gradient() raises FuelExhausted exactly
+    below it, as the reference does."""
+    G = golden("gmm_fuel")
+    p = rg.load_example("gmm")
+    A = lambda a: rg.Array.matrix(a.tolist()) if a.ndim == 2 else rg.Array.vector(a.tolist())  # noqa
+    Z = lambda *s: A(np.zeros(s))  # noqa: E731
+    for ci in range(int(G["ncases"])):
+        d, K, N = (int(v) for v in G[f"c{ci}_dims"])
+        al, me = G[f"c{ci}_alphas"], G[f"c{ci}_means"].reshape(K, d)
+        ic, x = G[f"c{ci}_icf"].reshape(K, -1), G[f"c{ci}_x"].reshape(N, d)
+        r = run_full(cuda, al, me, ic, x, 1.0, 0, 0.5)[5]
+        U = int(r.counters[0].item())
+        steps = rg.kernels.gmm_statement_count(d, K, N, U, rg.kernels.gmm_alpha_updates(al))
+        assert steps == int(G["steps"][ci]), (ci, steps, int(G["steps"][ci]))
+        args = [0.0, A(al), A(me), A(ic), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K),
+                rg.Array.vector([0] * K), 1.0, 0, 0.5]
+        rg.gradient(p, rg.GradRequest("gmm", args),
+                    rg.ExecOptions(max_steps=steps, float_tolerance=1e-6))
+        with pytest.raises(rg.FuelExhausted):
+            rg.gradient(p, rg.GradRequest("gmm", args),
+                        rg.ExecOptions(max_steps=steps - 1, float_tolerance=1e-6))
+
+
+def test_configs2_at_default_options_is_fuel_exhausted(cuda):
+    """configs[2] at the reference's default ExecOptions: one sweep executes
+    ~6.5e9 statements > max_steps = 5e8, so the reference raises
+    FuelExhausted (before any restoration check); so does the drop-in."""
+    d, K, N = 64, 25, 10000
+    alphas, means, icf, x = inputs(np.random.default_rng(2), d, K, N)
+    r = run_full(cuda, alphas, means, icf, x, 1.0, 0, 0.0)[5]
+    steps = rg.kernels.gmm_statement_count(d, K, N, int(r.counters[0].item()),
+                                           rg.kernels.gmm_alpha_updates(alphas))
+    assert steps > 500_000_000
+    p = rg.load_example("gmm")
+    A = lambda a: rg.Array.matrix(a.tolist()) if a.ndim == 2 else rg.Array.vector(a.tolist())  # noqa
+    Z = lambda *s: A(np.zeros(s))  # noqa: E731
+    args = [0.0, A(alphas), A(means), A(icf), A(x), Z(K, d), Z(K), Z(d), Z(d), Z(K), Z(K),
+            1.0, 0, 0.0]
+    with pytest.raises(rg.FuelExhausted):
+        rg.gradient(p, rg.GradRequest("gmm", args))

@@ -155,3 +155,31 @@ def test_bessel_fuel_formula_matches_reference_step_counts(oracle, golden):
         assert steps == 31 + 6 * int(nu) + 22 * int(trips)
         assert bessel_trip_cap(steps, int(nu)) == int(trips)
         assert bessel_trip_cap(steps - 1, int(nu)) == int(trips) - 1
+
+
+def test_gmm_statement_count_formula(golden):
+    """rl_gmm_statement_count against the reference's own counts
+    (gmm_fuel.npz), with the argmax steps recomputed here in numpy."""
+    from paper_2003_04617_b200.kernels import gmm_alpha_updates, gmm_statement_count
+    G = golden("gmm_fuel")
+    for ci in range(int(G["ncases"])):
+        d, K, N = (int(v) for v in G[f"c{ci}_dims"])
+        al, me = G[f"c{ci}_alphas"], G[f"c{ci}_means"].reshape(K, d)
+        ic, x = G[f"c{ci}_icf"].reshape(K, -1), G[f"c{ci}_x"].reshape(N, d)
+        U = 0
+        for i in range(N):
+            mt = []
+            for k in range(K):
+                L = np.diag(np.exp(ic[k, :d]))
+                li = d
+                for a in range(d):
+                    for b in range(a + 1, d):
+                        L[b, a] = ic[k, li]
+                        li += 1
+                q = L @ (x[i] - me[k])
+                mt.append(al[k] + ic[k, :d].sum() - 0.5 * q @ q)
+            best = 0
+            for k in range(1, K):
+                if mt[k] > mt[best]:
+                    best, U = k, U + 1
+        assert gmm_statement_count(d, K, N, U, gmm_alpha_updates(al)) == int(G["steps"][ci])
