@@ -13,7 +13,7 @@ HEADER = os.path.join(REPO, "include", "revgpu.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|size_t|const char \*)\s*(rl_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int64_t|int|size_t|const char \*)\s*(rl_\w+)\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
