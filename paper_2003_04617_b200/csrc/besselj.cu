@@ -44,6 +44,22 @@
 
 namespace rl {
 
+#ifdef BJ_PHASES   // timing-only builds: cycles per phase, summed over warps (tools)
+__device__ unsigned long long g_bj_phase[16];
+__shared__ long long s_bj_t[32];
+#define BJ_MARK(ph)                                                              \
+  do {                                                                           \
+    __syncwarp();                                                                \
+    const long long now_ = clock64();                                            \
+    if ((threadIdx.x & 31) == 0) {                                               \
+      atomicAdd(&g_bj_phase[ph], (unsigned long long)(now_ - s_bj_t[threadIdx.x >> 5])); \
+      s_bj_t[threadIdx.x >> 5] = now_;                                           \
+    }                                                                            \
+  } while (0)
+#else
+#define BJ_MARK(ph) (void)0
+#endif
+
 __constant__ double c_logtab[LOGTAB_N];
 constexpr double LN2 = 0.6931471805599453;  // == math.log(2) (host libm), bit for bit
 #ifndef BJ_EXPN
@@ -299,6 +315,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     act = false;
   }
   const int kend = ktab < kfuel ? ktab : kfuel;
+  if (!CAREFUL) BJ_MARK(6);                               // prologue
   // main phase: every non-dead lane still active -> no predication.  Two
   // trips (odd k+1, even k+2) are computed speculatively per warp vote: the
   // term s of trip k+2 does not depend on exp() of trip k+1, so the two exp
@@ -405,6 +422,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     fwd_trip<CAREFUL, false, true, -1>(k, nu, h2, thr, act, s, t, acc, T, code);
   }
   if (act) code = RL_ERR_FUEL;                           // still running at the fuel cap
+  if (!CAREFUL) BJ_MARK(7);                               // forward loops
   BJOut o;
   o.J = 0.0 + acc;                                       // out! += acc
   o.T = T;
@@ -461,6 +479,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
     rev_trip<CAREFUL, true, false, 1, GRAD>(1, nu, h2, thr, paccg, naccg, chk, fwd_ok, T, acc, sg, s,
                                       h2g, t, code, ok);
   if (!CAREFUL && chk && fwd_ok && !ok && !code) code = RL_ERR_POSTCONDITION;
+  if (!CAREFUL) BJ_MARK(8);                               // reverse loops
   double zg = 0.0;
   if (fwd_ok) {
     acc = acc - t;                                       // acc -= convert(s)
@@ -492,6 +511,7 @@ __device__ __forceinline__ BJOut besselj_element(double z, bool valid, int nu, d
   o.dz = fwd_ok ? zg : qnan;
   o.code = code;
   o.bad = valid && bad;
+  if (!CAREFUL) BJ_MARK(9);                               // epilogue
   return o;
 }
 
@@ -717,6 +737,7 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
   o.d2 = fwd_ok ? gz.t : qnan;
   o.code = code;
   o.bad = valid && bad;
+  if (!CAREFUL) BJ_MARK(9);                               // epilogue
   return o;
 }
 
@@ -725,6 +746,7 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
 // primal sweeps; dzout unused): the objective-only ("-O") kernel.  MODE 2:
 // the Hessian (Dual sweeps; d2out = d2J/dz2).
 constexpr int BJ_RUN = 0, BJ_GRAD = 1, BJ_HESS = 2;
+
 template <int MODE>
 __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
     int nu, const double *__restrict__ zin, long long n, double thr, double tol, double seed,
@@ -772,6 +794,9 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
   for (long long base = (long long)blockIdx.x * BJ_C; base < n;
        base += (long long)gridDim.x * BJ_C) {
     const int cnt = (int)(n - base < BJ_C ? n - base : BJ_C);
+#ifdef BJ_PHASES
+    if ((threadIdx.x & 31) == 0) s_bj_t[threadIdx.x >> 5] = clock64();
+#endif
     // 1. bucket histogram (rank within bucket from the atomic)
     for (int b = tid; b < BJ_NB; b += BJ_BLOCK) s_hist[b] = 0;
     if (tid == 0) s_round = 0;
@@ -790,6 +815,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
     }
     __syncthreads();
     prefetch(base + (long long)gridDim.x * BJ_C);
+    BJ_MARK(0);
     // 2. exclusive scan of the 256 buckets (one per thread)
     {
       const int v = s_hist[tid];
@@ -808,6 +834,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
       s_hist[tid] = off + x - v;
     }
     __syncthreads();
+    BJ_MARK(1);
     // 3. scatter into z order
 #pragma unroll
     for (int m = 0; m < BJ_M; m++) {
@@ -819,6 +846,7 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
       }
     }
     __syncthreads();
+    BJ_MARK(2);
     // 4. rounds of 32 z-neighbours, handed out dynamically from the largest z
     //    down (longest first), so the block's warps reach the barrier together
     //    (the next round's ticket is drawn one round ahead, off the
@@ -871,8 +899,12 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
         }
       }
     }
+    BJ_MARK(3);
     __syncthreads();
-    // 5. coalesced stores in the original order
+    BJ_MARK(4);
+    // 5. coalesced stores in the original order (TMA bulk stores of s_J /
+    //    s_dz / s_fail measured no faster: the kernel is throughput-bound, the
+    //    warps' store time moved to the next chunk's wait)
 #pragma unroll
     for (int m = 0; m < BJ_M; m++) {
       const int e = m * BJ_BLOCK + tid;
@@ -890,9 +922,18 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
       }
     }
     __syncthreads();
+    BJ_MARK(5);
   }
   block_add_counters<BJ_BLOCK>(trips_sum, nfail, counters);
 }
+
+#ifdef BJ_PHASES
+extern "C" int rl_debug_bj_phases(unsigned long long *out16) {  // timing-only builds
+  cudaMemcpyFromSymbol(out16, g_bj_phase, 16 * sizeof(unsigned long long));
+  static const unsigned long long zero[16] = {0};
+  return (int)cudaMemcpyToSymbol(g_bj_phase, zero, sizeof zero);
+}
+#endif
 
 static int upload_logtab() {
   static double tab[LOGTAB_N];
