@@ -76,7 +76,67 @@ __global__ void __launch_bounds__(256) k_dmma_m16n8k16(double *out, int iters) {
   if (s == 1234.5678) out[0] = s;
 }
 
+// DMMA and DFMA issued together (each warp: `nm` m16n8k16 MMAs and 8 x `nf`
+// DFMAs per iteration): do the FP64 tensor pipe and the FP64 FMA pipe add up?
+__global__ void __launch_bounds__(256) k_mixed(double *out, int iters, int nm, int nf) {
+  double a[8], b[4];
+#pragma unroll
+  for (int j = 0; j < 8; j++) a[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll
+  for (int j = 0; j < 4; j++) b[j] = 1.0 - threadIdx.x * 1e-4 - j * 1e-5;
+  double c[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0;
+  double f0 = threadIdx.x * 1e-3, f1 = f0 + 1, f2 = f0 + 2, f3 = f0 + 3, f4 = f0 + 4, f5 = f0 + 5,
+         f6 = f0 + 6, f7 = f0 + 7;
+  const double fb = 0.999999, fc = 1e-7;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (j < nm)
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                     "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                     : "+d"(c[j][0]), "+d"(c[j][1]), "+d"(c[j][2]), "+d"(c[j][3])
+                     : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]),
+                       "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    for (int u = 0; u < nf; u++) {
+      f0 = fma(f0, fb, fc); f1 = fma(f1, fb, fc); f2 = fma(f2, fb, fc); f3 = fma(f3, fb, fc);
+      f4 = fma(f4, fb, fc); f5 = fma(f5, fb, fc); f6 = fma(f6, fb, fc); f7 = fma(f7, fb, fc);
+    }
+  }
+  double s = f0 + f1 + f2 + f3 + f4 + f5 + f6 + f7;
+#pragma unroll
+  for (int j = 0; j < 4; j++) s += c[j][0] + c[j][1] + c[j][2] + c[j][3];
+  if (s == 1234.5678) out[0] = s;
+}
+
 extern "C" {
+
+// TFLOP/s of k_mixed (DMMA 4096 flop each, DFMA 2 flop per lane)
+double probe_mixed(int iters, int nm, int nf, float *ms_out) {
+  int dev = 0, sms = 0, bps = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_mixed, 256, 0);
+  double *out;
+  cudaMalloc(&out, 8);
+  dim3 grid(sms * bps), block(256);
+  k_mixed<<<grid, block>>>(out, 16, nm, nf);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_mixed<<<grid, block>>>(out, iters, nm, nf);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(out);
+  if (ms_out) *ms_out = ms;
+  const double warps = (double)grid.x * (block.x / 32);
+  const double flops = (double)iters * warps * (nm * 4096.0 + nf * 8.0 * 32 * 2);
+  return flops / (ms * 1e-3) / 1e12;
+}
 
 // which: 0 = m8n8k4 (512 flop/mma), 1 = m16n8k16 (4096 flop/mma); TFLOP/s
 double probe_dmma_peak(int which, int iters, float *ms_out) {
