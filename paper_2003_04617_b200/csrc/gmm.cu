@@ -29,7 +29,6 @@
 //                 in registers across the block's points
 //                 (prep's block 0 also evaluates -N lse(alphas) and its
 //                 gradient; the Wishart prior and cst are added in final)
-//   k_gmm_reduce  deterministic, coalesced sum of the reverse CTAs' partials
 //   k_gmm_final   per component: the chain through qd = exp(icf) and sq, means.g =
 //                 -L^T sum_i qxc.g_i (linearity: sum_i xc.g_i = L^T sum_i qxc.g_i)
 //
@@ -61,11 +60,10 @@ namespace rl {
 #ifndef GMM_PREP_BLOCKS
 #define GMM_PREP_BLOCKS 1  // k_gmm_prep: L^T built block by block (constant row lengths)
 #endif
-#ifndef GMM_FINAL_ERR_BLOCK
-#define GMM_FINAL_ERR_BLOCK 1  // k_gmm_final: the objective in its own block
-#endif
-#ifndef GMM_FUSE_FINAL
-#define GMM_FUSE_FINAL 1   // k_gmm_final sums the reverse partials itself (no k_gmm_reduce)
+#ifndef GMM_REV_FINAL
+#define GMM_REV_FINAL 0    // 1: k_gmm_rev's last CTA per component assembles its gradient instead
+                           // of k_gmm_final (measured slower: configs[2] 0.2214 -> 0.2416 ms, one
+                           // CTA per component serialises what the K x 8 final CTAs split)
 #endif
 #ifndef GMM_MT_RR
 #define GMM_MT_RR 1        // factor-adjoint tiles dealt round-robin over the warps
@@ -161,7 +159,8 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
                                                           double *__restrict__ fro,
                                                           double *__restrict__ par,
                                                           unsigned *__restrict__ flags,
-                                                          long long N) {
+                                                          long long N,
+                                                          unsigned *__restrict__ comp_ctr) {
   pdl_trigger();                 // k_gmm_fwd's prologue (x prefetch) overlaps this kernel
   const int k = blockIdx.x;
   // the per-point release flags of k_gmm_fwd start at 0 (replaces a memset,
@@ -169,6 +168,7 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
   for (long long i = (long long)blockIdx.x * GMM_THREADS + threadIdx.x; i < N;
        i += (long long)gridDim.x * GMM_THREADS)
     flags[i] = 0u;
+  if (comp_ctr && threadIdx.x == 0 && blockIdx.x < K) comp_ctr[blockIdx.x] = 0u;
   const int P = d * (d + 1) / 2;
   extern __shared__ __align__(16) double prep_dyn[];     // icf row (P), then K scratch
 #if GMM_ALPHA_BLOCK
@@ -625,6 +625,82 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
   block_add_counters<LSE_THREADS * LSE_LANES>(nupd, nfail, counters);
 }
 
+// one component's final assembly (slice c of C of its lower triangle; c == 0
+// also alphas.g and means.g): the S per-CTA partials of k_gmm_rev are summed
+// in order (0.0 + p_0 + p_1 + ...), only over the entries used (the lower
+// triangle).  Whole CTA; gsum: DP doubles and sgp: 1 double of shared memory.
+template <int DP>
+__device__ __forceinline__ void gmm_final_component(
+    int k, int c, int C, int d, int K, int S, const double *__restrict__ icf,
+    const double *__restrict__ qd, const double *__restrict__ LT, const double *__restrict__ part,
+    const double *__restrict__ ws_par, double ga, int wm, int add_params,
+    double *__restrict__ out, double *gsum, double *sgp) {
+  const long long PW = (long long)DP * DP + DP + 1;
+  const double hg2 = 0.5 * ga * ga;
+  const int P = d * (d + 1) / 2;
+  double *g_alpha = out + 1;
+  double *g_means = out + 1 + K;
+  double *g_icf = out + 1 + K + (long long)K * d;
+  const double *pk = part + (long long)k * S * PW;
+  // column sums of qxc.g and sum of mt.g
+  for (int b = threadIdx.x; b <= DP; b += GMM_THREADS) {
+    if (c != 0 && b != DP) continue;
+    double s = 0.0;
+    for (int j = 0; j < S; j++) s += pk[j * PW + (long long)DP * DP + b];
+    if (b < DP) gsum[b] = s;
+    else *sgp = s;
+  }
+  __syncthreads();
+  const double sg = *sgp;
+  if (c == 0 && threadIdx.x == 0) {
+    const double ga_k = sg + (add_params ? ws_par[k] : 0.0);
+    g_alpha[k] = ga_k;
+  }
+  // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a):
+  // GMM_THREADS / DP lanes per row, shuffle-reduced
+  const double *lt = LT + (long long)k * ltb_size(DP);
+  if (c == 0) {
+    constexpr int LR = GMM_THREADS / DP;                 // lanes per row: 8, 4, 2
+    const int a = threadIdx.x / LR, l = threadIdx.x % LR;
+    double s = 0.0;
+    if (a < d)
+#pragma unroll 4
+      for (int b = a + l; b < d; b += LR) s = fma(gsum[b], lt[ltb_idx(DP, a, b)], s);
+#pragma unroll
+    for (int o = LR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if (a < d && l == 0) g_means[(long long)k * d + a] = -s;
+  }
+  // icf.g: diag = sq.g + qd.g exp(icf); offdiag = M[b][a] (+ prior).  The
+  // threads walk M's lower triangle (b >= a) in its stored row-major order,
+  // so the partial reads coalesce; icf index: diag j = a, off-diagonal
+  // (row b, col a) of the column-major strict lower triangle j = d + a d -
+  // a (a + 1) / 2 + (b - a - 1)
+  const double sqg = sg + (add_params ? -(double)wm : 0.0);
+  const int T = d * (d + 1) / 2;
+#pragma unroll 2
+  for (int e = c * GMM_THREADS + threadIdx.x; e < T; e += GMM_THREADS * C) {
+    int b = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    if (b * (b + 1) / 2 > e) b--;
+    if ((b + 1) * (b + 2) / 2 <= e) b++;
+    const int a = e - b * (b + 1) / 2;
+    double m = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < S; j++) m += pk[j * PW + (long long)b * DP + a];
+    double g;
+    if (a == b) {
+      const int j = a;
+      const double q = qd[(long long)k * d + j];
+      const double qdg = (add_params ? hg2 * (2.0 * q) : 0.0) + m;
+      g = (0.0 + sqg) + qdg * exp(icf[(long long)k * P + j]);
+      g_icf[(long long)k * P + j] = g;
+    } else {
+      const int j = d + a * d - a * (a + 1) / 2 + (b - a - 1);
+      g = (add_params ? hg2 * (2.0 * icf[(long long)k * P + j]) : 0.0) + m;
+      g_icf[(long long)k * P + j] = g;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // reverse: recompute Z (no tape), qxc.g = (-dmt/2)(2 Z); accumulate the
 // factor adjoint M = sum_i qxc.g_i xc_i^T (lower triangle, 16x8 DMMA tiles
@@ -652,7 +728,10 @@ template <int DP, int TP>
 __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_gmm_rev(
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ x,
     const double *__restrict__ LT, const double *__restrict__ gmtT,
-    double *__restrict__ part /* [K][S][DP*DP + DP + 1] */) {
+    double *__restrict__ part /* [K][S][DP*DP + DP + 1] */, unsigned *__restrict__ comp_ctr,
+    const double *__restrict__ icf, const double *__restrict__ qd,
+    const double *__restrict__ ws_par, double ga, int wm, int add_params,
+    double *__restrict__ gout) {
   using C = GmmCfg<DP, TP>;
   using MTL = MTiles<DP>;
   extern __shared__ __align__(16) double smem[];
@@ -812,25 +891,21 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     for (int ww = 0; ww < GMM_WARPS; ww++) s += red[ww];
     out[(long long)DP * DP + DP] = s;
   }
-}
-
-// ---------------------------------------------------------------------------
-// deterministic reduction of the reverse CTAs' partials over the S splits:
-// red[k][e] = sum_s part[k][s][e] (coalesced along e)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(GMM_THREADS) k_gmm_reduce(int S, long long PW,
-                                                            const double *__restrict__ part,
-                                                            double *__restrict__ red) {
-  pdl_wait();
-
-  const int k = blockIdx.y;
-  const long long e = (long long)blockIdx.x * GMM_THREADS + threadIdx.x;
-  if (e >= PW) return;
-  const double *pk = part + (long long)k * S * PW + e;
-  double s = 0.0;
-#pragma unroll 8
-  for (int j = 0; j < S; j++) s += pk[(long long)j * PW];
-  red[(long long)k * PW + e] = s;
+  // the last CTA of component k to finish assembles its gradient (the final
+  // kernel's work, fused: the partials are read from L2 right after they
+  // are written, and no launch separates the two)
+  if (comp_ctr) {
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (tid == 0) s_last = atomicAdd(&comp_ctr[k], 1u) == (unsigned)(S - 1);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      gmm_final_component<DP>(k, 0, 1, d, K, S, icf, qd, LT, part, ws_par, ga, wm, add_params,
+                              gout, gt, red);
+    }
+  }
 }
 
 // sum of the per-block point objectives into red[0] (whole block; the same
@@ -862,11 +937,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
 
   // grid (K, C): CTA (k, c) takes every C-th block of the triangle; c == 0
   // also alphas.g, means.g and (k == 0) the objective.  The S per-CTA
-  // partials of k_gmm_rev are summed here in k_gmm_reduce's order (0.0 +
+  // partials of k_gmm_rev are summed here in a fixed order (0.0 +
   // p_0 + p_1 + ...), only over the entries used (the lower triangle)
   const int k = blockIdx.x, c = blockIdx.y, C = gridDim.y;
   const int P = d * (d + 1) / 2;
-#if GMM_FINAL_ERR_BLOCK
   if (k == K) {                  // the extra column: the objective only (block (K, 0))
     if (c != 0) return;
     __shared__ double ered0[GMM_THREADS];
@@ -895,98 +969,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_final(
     }
     return;
   }
-#endif
-  const long long PW = (long long)DP * DP + DP + 1;
-  const double hg2 = 0.5 * ga * ga;
   __shared__ double gsum[DP];
   __shared__ double sg;
-  double *g_alpha = out + 1;
-  double *g_means = out + 1 + K;
-  double *g_icf = out + 1 + K + (long long)K * d;
-  const double *pk = part + (long long)k * S * PW;
-  // column sums of qxc.g and sum of mt.g
-  for (int b = threadIdx.x; b <= DP; b += GMM_THREADS) {
-    if (c != 0 && b != DP) continue;
-    double s = 0.0;
-    for (int j = 0; j < S; j++) s += pk[j * PW + (long long)DP * DP + b];
-    if (b < DP) gsum[b] = s;
-    else sg = s;
-  }
-  __syncthreads();
-  if (c == 0 && threadIdx.x == 0) {
-    const double ga_k = sg + (add_params ? ws_par[k] : 0.0);
-    g_alpha[k] = ga_k;
-  }
-  // means.g[a] = -sum_b gsum[b] L[b][a]   (L^T row a = packed row a):
-  // GMM_THREADS / DP lanes per row, shuffle-reduced
-  const double *lt = LT + (long long)k * ltb_size(DP);
-  if (c == 0) {
-    constexpr int LR = GMM_THREADS / DP;                 // lanes per row: 8, 4, 2
-    const int a = threadIdx.x / LR, l = threadIdx.x % LR;
-    double s = 0.0;
-    if (a < d)
-#pragma unroll 4
-      for (int b = a + l; b < d; b += LR) s = fma(gsum[b], lt[ltb_idx(DP, a, b)], s);
-#pragma unroll
-    for (int o = LR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
-    if (a < d && l == 0) g_means[(long long)k * d + a] = -s;
-  }
-  // icf.g: diag = sq.g + qd.g exp(icf); offdiag = M[b][a] (+ prior).  The
-  // threads walk M's lower triangle (b >= a) in its stored row-major order,
-  // so the partial reads coalesce; icf index: diag j = a, off-diagonal
-  // (row b, col a) of the column-major strict lower triangle j = d + a d -
-  // a (a + 1) / 2 + (b - a - 1)
-  const double sqg = sg + (add_params ? -(double)wm : 0.0);
-  const int T = d * (d + 1) / 2;
-#pragma unroll 2
-  for (int e = c * GMM_THREADS + threadIdx.x; e < T; e += GMM_THREADS * C) {
-    int b = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    if (b * (b + 1) / 2 > e) b--;
-    if ((b + 1) * (b + 2) / 2 <= e) b++;
-    const int a = e - b * (b + 1) / 2;
-    double m = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < S; j++) m += pk[j * PW + (long long)b * DP + a];
-    double g;
-    if (a == b) {
-      const int j = a;
-      const double q = qd[(long long)k * d + j];
-      const double qdg = (add_params ? hg2 * (2.0 * q) : 0.0) + m;
-      g = (0.0 + sqg) + qdg * exp(icf[(long long)k * P + j]);
-      g_icf[(long long)k * P + j] = g;
-    } else {
-      const int j = d + a * d - a * (a + 1) / 2 + (b - a - 1);
-      g = (add_params ? hg2 * (2.0 * icf[(long long)k * P + j]) : 0.0) + m;
-      g_icf[(long long)k * P + j] = g;
-    }
-  }
-  __shared__ double ered[GMM_THREADS];
-  if (!GMM_FINAL_ERR_BLOCK && k == 0 && c == 0) {
-    sum_err_parts(nerr, err_part, ered);
-    // -N lse(alphas) + 0.5 ga^2 fro - wm ssq + cst (prior routine, err += cst);
-    // fro and ssq summed in component order from shared-memory chunks
-    __shared__ double cfro[GMM_THREADS], csq[GMM_THREADS];
-    double fro = 0.0, ssq = 0.0;
-    for (int k0 = 0; add_params && k0 < K; k0 += GMM_THREADS) {
-      const int kk = k0 + threadIdx.x;
-      if (kk < K) {
-        cfro[threadIdx.x] = fro_k[kk];
-        csq[threadIdx.x] = sq[kk];
-      }
-      __syncthreads();
-      if (threadIdx.x == 0)
-        for (int q = 0; q < GMM_THREADS && k0 + q < K; q++) {
-          fro = fro + cfro[q];
-          ssq = ssq + csq[q];
-        }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      double e = ered[0];
-      if (add_params) e = e + (ws_par[K] + hg2 * fro - (double)wm * ssq + cst);
-      out[0] = e;
-    }
-  }
+  gmm_final_component<DP>(k, c, C, d, K, S, icf, qd, LT, part, ws_par, ga, wm, add_params, out,
+                          gsum, &sg);
 }
 
 // ---------------------------------------------------------------------------
@@ -1177,7 +1163,7 @@ static int choose_split(int K, long long ntiles, int slots, int smax) {
 }
 
 struct GmmLayout {
-  size_t lt, qd, sq, fro, mt, gmt, flags, errp, terms, part, red, par, total;
+  size_t lt, qd, sq, fro, mt, gmt, flags, errp, terms, part, red, par, ctr, total;
   int Sf, Sr, nerr;
 };
 
@@ -1218,6 +1204,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   L.part = take((size_t)K * L.Sr * (size_t)pw * 8);
   L.red = take((size_t)K * (size_t)pw * 8);
   L.par = take((size_t)(K + 1) * 8);
+  L.ctr = take((size_t)K * 4);
   L.total = off;
   return L;
 }
@@ -1290,7 +1277,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
 #endif
   if (!(GMM_ABLATE & 1))
   k_gmm_prep<DP><<<K + GMM_ALPHA_BLOCK, GMM_THREADS, sp, st>>>(d, K, N_total, alphas, icf, LT, qd, sq, fro,
-                                             add_params ? par : nullptr, flags, N);
+                                             add_params ? par : nullptr, flags, N,
+                                             (unsigned *)(ws + L.ctr));
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
     constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
@@ -1327,7 +1315,9 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
         return rc;
     }
     if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
-                         d, K, N, means, x, LT, gmt, part)))
+                         d, K, N, means, x, LT, gmt, part,
+                         GMM_REV_FINAL ? (unsigned *)(ws + L.ctr) : nullptr, icf, qd, par, gamma,
+                         m, add_params, out)))
       return rc;
   } else if (!grad) {
     if (seq) return restore(st);
@@ -1338,31 +1328,26 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                                           st), "memset part")))
       return rc;
   }
-  const long long PW = (long long)DP * DP + DP + 1;
-#if GMM_FUSE_FINAL
   (void)redp;
   if (GMM_ABLATE & 8) return 0;
-  // enough (k, c) CTAs for about two per SM, at most 8 per component
-  const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
-  // with the replay, the objective comes from k_gmm_restore (no extra column)
-  if ((rc = launch_pdl("k_gmm_final", k_gmm_final<DP>,
-                       dim3(K + (seq ? 0 : GMM_FINAL_ERR_BLOCK), fc), dim3(GMM_THREADS), 0, st, d,
-                       K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, part, errp, par, gamma,
-                       m, cst, add_params, out)))
-    return rc;
+  if (N > 0 && GMM_REV_FINAL) {
+    // k_gmm_rev's last CTA per component assembled the gradient; the objective
+    // comes from k_gmm_restore (drop-in) or one small block (shard entry)
+    if (!seq && (rc = launch_gmm_err_only(K, L, N, errp, sq, fro, par, gamma, m, cst, add_params,
+                                          out, st)))
+      return rc;
+  } else {
+    // enough (k, c) CTAs for about two per SM, at most 8 per component
+    const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
+    // with the replay, the objective comes from k_gmm_restore (no extra column)
+    if ((rc = launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K + (seq ? 0 : 1), fc),
+                         dim3(GMM_THREADS), 0, st, d, K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq,
+                         fro, LT, part, errp, par, gamma, m, cst, add_params, out)))
+      return rc;
+  }
   if (seq && N > 0)                                      // join
     return cuda_status(cudaStreamWaitEvent(st, side->join, 0), "join wait");
   return RL_OK;
-#else
-  if (!(GMM_ABLATE & 4) && (rc = launch_pdl("k_gmm_reduce", k_gmm_reduce,
-                       dim3((unsigned)((PW + GMM_THREADS - 1) / GMM_THREADS), K),
-                       dim3(GMM_THREADS), 0, st, L.Sr, PW, part, redp)))
-    return rc;
-  if (GMM_ABLATE & 8) return 0;
-  return launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K), dim3(GMM_THREADS), 0, st, d, K, 1,
-                    N > 0 ? L.nerr : 0, icf, qd, sq, fro, LT, redp, errp, par, gamma, m, cst,
-                    add_params, out);
-#endif
 }
 
 int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *alphas,
