@@ -71,6 +71,11 @@ namespace rl {
 #ifndef GMM_TPF
 #define GMM_TPF 64         // forward tile (points) for DP = 64
 #endif
+#ifndef GMM_X_BULK
+#define GMM_X_BULK 0       // 1: x tiles by per-row TMA bulk copies on an mbarrier instead of
+                           // cp.async per element pair (measured slower: configs[2] 0.222 ->
+                           // 0.255 ms, configs[4]-shape 45.9 -> 51.1 ms)
+#endif
 #ifndef GMM_FWD_MINB
 #define GMM_FWD_MINB 2     // forward CTAs per SM (launch bounds) for DP <= 64
 #endif
@@ -305,6 +310,57 @@ __device__ __forceinline__ void load_x_async(double *__restrict__ xs, const doub
   }
 }
 
+// x tiles by TMA bulk copies: one 1D cp.async.bulk per point row (d * 8
+// bytes, into the padded row stride), issued by warp 0, completion counted
+// on an mbarrier.  Replaces ~TP * DP / 2 cp.async with their index
+// arithmetic per tile (a quarter of the tile kernels' instructions).  Usable
+// when every row is 16-byte aligned and sized (d even, x 16-byte aligned).
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m))
+      : "memory");
+}
+// warp 0 only: rows [p0, p0 + TP) of x into xs (rows past N zero-filled)
+template <int DP, int TP>
+__device__ __forceinline__ void load_x_bulk(double *__restrict__ xs, const double *__restrict__ x,
+                                            int d, long long p0, long long N, uint64_t *mbar) {
+  using C = GmmCfg<DP, TP>;
+  const int lane = threadIdx.x & 31;
+  const long long rem = N - p0;
+  const int rows = rem < TP ? (int)rem : TP;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the generic reads
+  if (lane == 0) mbar_expect(mbar, (unsigned)rows * (unsigned)d * 8u);
+  __syncwarp();
+  for (int r = lane; r < TP; r += 32) {
+    double *dst = xs + r * C::XS;
+    if (r < rows)
+      bulk_g2s(dst, x + (p0 + r) * d, (unsigned)d * 8u, mbar);
+    else
+      for (int a = 0; a < d; a++) dst[a] = 0.0;
+  }
+}
+
 // Z tile: acc[m][h] (m-tile m of this warp, column tile h: 0 -> j1, 1 -> j2)
 // = sum_a Xc[p][a] L^T[a][b] over the upper triangle (k-steps ks <= j/2).
 // xs already holds xc = x - mu (see center_tile).  All fragments of a
@@ -392,12 +448,26 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
   const int t0 = lane & 3, t1 = lane >> 2;
   const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
   // independent of k_gmm_prep (inputs only): before the PDL wait
+  __shared__ uint64_t xbar[2];
+  const bool bulk = GMM_X_BULK && !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
+  unsigned xph[2] = {0u, 0u};
+  if (bulk && tid == 0) {
+    mbar_init(&xbar[0]);
+    mbar_init(&xbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;  // padding stays zero
   for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const long long ntiles = (N + TP - 1) / TP;
   __syncthreads();
   long long tile = blockIdx.y;
-  if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+  if (tile < ntiles) {
+    if (bulk) {
+      if (w == 0) load_x_bulk<DP, TP>(xs0, x, d, tile * TP, N, &xbar[0]);
+    } else {
+      load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+    }
+  }
   cp_commit();
   pdl_wait();                                            // prep's L^T, sq and zeroed flags
   copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
@@ -406,9 +476,21 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
   int buf = 0;
   for (; tile < ntiles; tile += gridDim.y) {
     const long long nxt = tile + gridDim.y;
-    if (nxt < ntiles) load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+    if (nxt < ntiles) {
+      if (bulk) {
+        if (w == 0) load_x_bulk<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N, &xbar[buf ^ 1]);
+      } else {
+        load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+      }
+    }
     cp_commit();
-    cp_wait<1>();
+    if (bulk) {
+      cp_wait<1>();                                      // L^T (first tile)
+      mbar_wait(&xbar[buf], xph[buf]);
+      xph[buf] ^= 1u;
+    } else {
+      cp_wait<1>();
+    }
     __syncthreads();
     double *xs = buf ? xs1 : xs0;
     center_tile<DP, TP>(xs, mu, d);
@@ -776,9 +858,23 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   double gs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};            // column sums (h, v0)
   double sgm = 0.0;
   const long long ntiles = (N + TP - 1) / TP;
+  __shared__ uint64_t xbar[2];
+  const bool bulk = GMM_X_BULK && !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
+  unsigned xph[2] = {0u, 0u};
+  if (bulk && tid == 0) {
+    mbar_init(&xbar[0]);
+    mbar_init(&xbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   long long tile = blockIdx.y;
-  if (tile < ntiles) load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+  if (tile < ntiles) {
+    if (bulk) {
+      if (w == 0) load_x_bulk<DP, TP>(xs0, x, d, tile * TP, N, &xbar[0]);
+    } else {
+      load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+    }
+  }
   cp_commit();
   // L^T (prep), means and x are ready before k_gmm_lse ends (it launches this
   // grid early): only mt.g below needs the wait
@@ -790,9 +886,19 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   for (; tile < ntiles; tile += gridDim.y) {
     const long long p0 = tile * TP;
     const long long nxt = tile + gridDim.y;
-    cp_wait<0>();                                         // this tile's x (own copies)
+    cp_wait<0>();                                         // L^T / this tile's x (own copies)
+    if (bulk) {
+      mbar_wait(&xbar[buf], xph[buf]);
+      xph[buf] ^= 1u;
+    }
     __syncthreads();
-    if (nxt < ntiles) load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+    if (nxt < ntiles) {
+      if (bulk) {
+        if (w == 0) load_x_bulk<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N, &xbar[buf ^ 1]);
+      } else {
+        load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+      }
+    }
     cp_commit();
     for (int p = tid; p < TP; p += GMM_THREADS) {
       const long long i = p0 + p;
