@@ -524,7 +524,14 @@ def bessel_cpu(target_s=2.0, n_max=1 << 24):
 
 
 def gmm_traffic():
-    """Sum of the configs[2] GMM kernels' DRAM bytes per evaluation."""
+    """DRAM bytes of one configs[2] GMM evaluation: the round-2 measurement
+    with L2 evicted before the evaluation and no flush between its kernels
+    (profiles/r02/gmm_c3_dram_per_eval.json, tools/gmm_one.py --flush under
+    ncu --cache-control none), else the per-kernel cold-cache sum."""
+    p2 = os.path.join(REPO, "profiles", "r02", "gmm_c3_dram_per_eval.json")
+    if os.path.exists(p2):
+        with open(p2) as fh:
+            return int(json.load(fh)["total_MB"] * 1e6)
     p = os.path.join(REPO, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None

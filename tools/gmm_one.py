@@ -1,5 +1,8 @@
 """A few drop-in GMM gradient evaluations (rl_gmm_gradient_f64) at a BASELINE
-config (ncu target).  usage: python tools/gmm_one.py [c3|c5|N] [reps]"""
+config (ncu target).  usage: python tools/gmm_one.py [c3|c5|N] [reps] [--flush]
+(--flush: a 256 MiB L2 eviction before every evaluation, as bench.py does; with
+`ncu --cache-control none` the DRAM counters then show one evaluation's real
+traffic: caches are not flushed between its kernels)"""
 import sys
 
 import numpy as np
@@ -18,7 +21,13 @@ cst = gmm_constants(d, K, N, 1.0, 0)
 ws = torch.empty(rg.kernels._native.lib().rl_gmm_workspace_bytes(d, K, N), dtype=torch.uint8,
                  device="cuda")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+# --flush evicts L2 by READING 256 MiB (clean lines: no write-back of the
+# eviction buffer lands in the measured kernels' DRAM-write counters)
+flush = torch.ones(32 << 20, dtype=torch.float64, device="cuda") if "--flush" in sys.argv else None
+torch.cuda.synchronize()
 for i in range(reps):
+    if flush is not None:
+        flush.sum()                # evict L2 between evaluations (bench.py writes instead)
     ev[0].record()
     r = rg.gmm_gradient(a, me, ic, x, 1.0, 0, cst, workspace=ws)
     ev[1].record()
