@@ -235,6 +235,23 @@ int rl_gmm_objective_f64(int32_t d, int32_t K, int64_t N, int64_t N_total, const
                          int32_t add_param_terms, double *err, uint8_t *fail,
                          unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
 
+/* Host-buffer forms of the entries above (pinned or pageable host memory;
+ * chunked over three streams for Bessel; n_failed = failed elements /
+ * points; gmm: argmax_steps = counters[0] for rl_gmm_statement_count). */
+int rl_besselj_run_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                            int64_t max_trips, int32_t invcheck, int32_t direction,
+                            const double *out_in, double *out, uint8_t *fail,
+                            unsigned long long *n_failed, int32_t device);
+int rl_ba_residuals_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                             const double *X, const double *w, const double *feats,
+                             const int32_t *obs, double tol, int32_t invcheck, double *err,
+                             uint8_t *fail, unsigned long long *n_failed, int32_t device);
+int rl_gmm_run_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                        const double *means, const double *icf, const double *x, double gamma,
+                        int32_t m, double cst, double err0, double tol, int32_t invcheck,
+                        int32_t direction, double *err, unsigned long long *n_failed,
+                        unsigned long long *argmax_steps, int32_t device);
+
 /* ----------------------------------------------------------------------
  * Batched forward-over-reverse Hessian of besselj:
  * replaces reference autodiff.hessian(p, "besselj", [0.0, nu, z[i]])
@@ -247,6 +264,10 @@ int rl_besselj_hess_f64(int32_t nu, const double *z, int64_t n, double thr, doub
                         double seed, int64_t max_trips, int32_t invcheck, double *J,
                         double *dJdz, double *d2Jdz2, uint8_t *fail,
                         unsigned long long *counters, void *stream);
+int rl_besselj_hess_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                             double seed, int64_t max_trips, int32_t invcheck, double *J,
+                             double *dJdz, double *d2Jdz2, uint8_t *fail,
+                             unsigned long long *n_failed, int32_t device);
 
 /* ----------------------------------------------------------------------
  * BA Jacobian in ADBench's sparse layout (BASparseMat, CSR with int row

@@ -61,6 +61,15 @@ SIGNATURES = {
                                                 ctypes.POINTER(ctypes.c_double), _ull_p, _i32]),
     "rl_seq_sum_f64": (ctypes.c_int, [_vp, _i64, _f64, _i64, _i32, _vp, _vp, _vp]),
     "rl_gmm_statement_count": (ctypes.c_int64, [_i32, _i32, _i64, _i64, _i64]),
+    "rl_besselj_run_f64_host": (ctypes.c_int, [_i32, _vp, _i64, _f64, _f64, _i64, _i32, _i32,
+                                               _vp, _vp, _vp, _ull_p, _i32]),
+    "rl_besselj_hess_f64_host": (ctypes.c_int, [_i32, _vp, _i64, _f64, _f64, _f64, _i64, _i32,
+                                                _vp, _vp, _vp, _vp, _ull_p, _i32]),
+    "rl_ba_residuals_f64_host": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
+                                                _f64, _i32, _vp, _vp, _ull_p, _i32]),
+    "rl_gmm_run_f64_host": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _f64, _i32,
+                                           _f64, _f64, _f64, _i32, _i32, _vp, _ull_p, _ull_p,
+                                           _i32]),
     "rl_besselj_run_f64": (ctypes.c_int, [_i32, _vp, _i64, _f64, _f64, _i64, _i32, _i32, _vp, _vp,
                                           _vp, _vp, _vp]),
     "rl_ba_residuals_f64": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _i32,

@@ -236,6 +236,65 @@ struct Pipeline {
   }
 };
 
+// Host-buffer pipeline of the per-element Bessel entries (run / uncall,
+// Hessian): chunks of z (and out_in) go up, `nout` double arrays and the
+// status bytes come down, over the three cached streams.  launch(s, m, dz,
+// din, douts, dfail, counters, stream) runs the device entry on one chunk.
+template <class Launch>
+static int bessel_host_chunks(int64_t n, const double *z, const double *in2, int nout,
+                              double *const outs[3], uint8_t *fail,
+                              unsigned long long *n_failed, int32_t device, Launch launch) {
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  const int64_t CH = int64_t(1) << 22;
+  const int64_t nch = (n + CH - 1) / CH;
+  const int64_t bufn = std::min<int64_t>(CH, std::max<int64_t>(n, 1));
+  DevBuf dz[Pipeline::NS], din[Pipeline::NS], dout[Pipeline::NS][3], dfl[Pipeline::NS], dc;
+  if ((rc = dc.alloc(2 * 8 * Pipeline::NS, pl.st[0])) ||
+      (rc = cuda_status(cudaMemsetAsync(dc.p, 0, 2 * 8 * Pipeline::NS, pl.st[0]), "memset")))
+    return rc;
+  for (int s = 0; s < Pipeline::NS && s < std::max<int64_t>(nch, 1); s++) {
+    if ((rc = dz[s].alloc(bufn * 8, pl.st[s])) || (rc = din[s].alloc(in2 ? bufn * 8 : 8, pl.st[s])) ||
+        (rc = dfl[s].alloc(bufn, pl.st[s])))
+      return rc;
+    for (int o = 0; o < nout; o++)
+      if ((rc = dout[s][o].alloc(bufn * 8, pl.st[s]))) return rc;
+  }
+  if ((rc = pl.finish())) return rc;              // counters zeroed before any stream uses them
+  auto *cnt = (unsigned long long *)dc.p;
+  for (int64_t c = 0; c < nch; c++) {
+    const int s = (int)(c % Pipeline::NS);
+    const int64_t off = c * CH, m = std::min(CH, n - off);
+    cudaStream_t st = pl.st[s];
+    if ((rc = cuda_status(cudaMemcpyAsync(dz[s].p, z + off, m * 8, cudaMemcpyHostToDevice, st),
+                          "H2D z")))
+      return rc;
+    if (in2 && (rc = cuda_status(cudaMemcpyAsync(din[s].p, in2 + off, m * 8,
+                                                 cudaMemcpyHostToDevice, st), "H2D in")))
+      return rc;
+    double *douts[3] = {(double *)dout[s][0].p, (double *)dout[s][1].p, (double *)dout[s][2].p};
+    if ((rc = launch(m, (const double *)dz[s].p, in2 ? (const double *)din[s].p : nullptr, douts,
+                     (uint8_t *)dfl[s].p, cnt + 2 * s, st)))
+      return rc;
+    for (int o = 0; o < nout; o++)
+      if ((rc = cuda_status(cudaMemcpyAsync(outs[o] + off, douts[o], m * 8,
+                                            cudaMemcpyDeviceToHost, st), "D2H out")))
+        return rc;
+    if ((rc = cuda_status(cudaMemcpyAsync(fail + off, dfl[s].p, m, cudaMemcpyDeviceToHost, st),
+                          "D2H fail")))
+      return rc;
+  }
+  if ((rc = pl.finish())) return rc;
+  unsigned long long h[2 * Pipeline::NS];
+  if ((rc = cuda_status(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost), "D2H counters")))
+    return rc;
+  unsigned long long nf = 0;
+  for (int q = 0; q < Pipeline::NS; q++) nf += h[2 * q + 1];
+  if (n_failed) *n_failed = nf;
+  return RL_OK;
+}
+
 }  // namespace rl
 
 using namespace rl;
@@ -379,6 +438,84 @@ int rl_besselj_grad_f64_host(int32_t nu, const double *z, int64_t n, double thr,
   }
   if (sum_trips) *sum_trips = tr;
   if (n_failed) *n_failed = nf;
+  return RL_OK;
+}
+
+int rl_besselj_run_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                            int64_t max_trips, int32_t invcheck, int32_t direction,
+                            const double *out_in, double *out, uint8_t *fail,
+                            unsigned long long *n_failed, int32_t device) {
+  if (n < 0 || (n > 0 && (!z || !out || !fail)) || (direction != 1 && direction != -1))
+    return set_error(RL_ERR_INVALID, "rl_besselj_run_f64_host: bad argument");
+  double *const outs[3] = {out, nullptr, nullptr};
+  return bessel_host_chunks(
+      n, z, out_in, 1, outs, fail, n_failed, device,
+      [&](int64_t m, const double *dz, const double *din, double *const *douts, uint8_t *dfl,
+          unsigned long long *cnt, cudaStream_t st) {
+        return launch_besselj_run(nu, dz, m, thr, tol, max_trips, invcheck, direction, din,
+                                  douts[0], dfl, cnt, st);
+      });
+}
+
+int rl_besselj_hess_f64_host(int32_t nu, const double *z, int64_t n, double thr, double tol,
+                             double seed, int64_t max_trips, int32_t invcheck, double *J,
+                             double *dJdz, double *d2Jdz2, uint8_t *fail,
+                             unsigned long long *n_failed, int32_t device) {
+  if (n < 0 || (n > 0 && (!z || !J || !dJdz || !d2Jdz2 || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_besselj_hess_f64_host: bad argument");
+  double *const outs[3] = {J, dJdz, d2Jdz2};
+  return bessel_host_chunks(
+      n, z, nullptr, 3, outs, fail, n_failed, device,
+      [&](int64_t m, const double *dz, const double *, double *const *douts, uint8_t *dfl,
+          unsigned long long *cnt, cudaStream_t st) {
+        return launch_besselj_hess(nu, dz, m, thr, tol, seed, max_trips, invcheck, douts[0],
+                                   douts[1], douts[2], dfl, cnt, st);
+      });
+}
+
+int rl_ba_residuals_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const double *cams,
+                             const double *X, const double *w, const double *feats,
+                             const int32_t *obs, double tol, int32_t invcheck, double *err,
+                             uint8_t *fail, unsigned long long *n_failed, int32_t device) {
+  if (n_obs < 0 || n_cams < 0 || n_pts < 0 ||
+      (n_obs > 0 && (!cams || !X || !w || !feats || !obs || !err || !fail)))
+    return set_error(RL_ERR_INVALID, "rl_ba_residuals_f64_host: bad argument");
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  cudaStream_t st = pl.st[0];
+  const size_t sizes[8] = {(size_t)n_cams * 88, (size_t)n_pts * 24, (size_t)n_obs * 8,
+                           (size_t)n_obs * 16, (size_t)n_obs * 8, (size_t)n_obs * 24,
+                           (size_t)std::max<int64_t>(n_obs, 1), 16};
+  size_t total = 0;
+  for (size_t b : sizes) total += (b + 255) & ~size_t(255);
+  void *base = nullptr;
+  if ((rc = Pipeline::arena(device, total, &base))) return rc;
+  char *q[8];
+  size_t off = 0;
+  for (int i = 0; i < 8; i++) {
+    q[i] = (char *)base + off;
+    off += (sizes[i] + 255) & ~size_t(255);
+  }
+  const void *src[5] = {cams, X, w, feats, obs};
+  for (int i = 0; i < 5; i++)
+    if (sizes[i] && (rc = cuda_status(cudaMemcpyAsync(q[i], src[i], sizes[i],
+                                                      cudaMemcpyHostToDevice, st), "H2D")))
+      return rc;
+  if ((rc = cuda_status(cudaMemsetAsync(q[7], 0, 16, st), "memset")) ||
+      (rc = launch_ba_residuals(n_cams, n_pts, n_obs, (double *)q[0], (double *)q[1],
+                                (double *)q[2], (double *)q[3], (int32_t *)q[4], tol, invcheck,
+                                (double *)q[5], (uint8_t *)q[6], (unsigned long long *)q[7], st)))
+    return rc;
+  unsigned long long h[2];
+  if ((n_obs > 0 && ((rc = cuda_status(cudaMemcpyAsync(err, q[5], sizes[5], cudaMemcpyDeviceToHost,
+                                                       st), "D2H err")) ||
+                     (rc = cuda_status(cudaMemcpyAsync(fail, q[6], n_obs, cudaMemcpyDeviceToHost,
+                                                       st), "D2H fail")))) ||
+      (rc = cuda_status(cudaMemcpyAsync(h, q[7], 16, cudaMemcpyDeviceToHost, st), "D2H counters")))
+    return rc;
+  if ((rc = pl.finish())) return rc;
+  if (n_failed) *n_failed = h[1];
   return RL_OK;
 }
 
@@ -719,6 +856,53 @@ int rl_gmm_gradient_f64_host(int32_t d, int32_t K, int64_t N, const double *alph
                              unsigned long long *n_failed, int32_t device) {
   return gmm_grad_host(d, K, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
                        n_failed, device, true, err0, resid);
+}
+
+int rl_gmm_run_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
+                        const double *means, const double *icf, const double *x, double gamma,
+                        int32_t m, double cst, double err0, double tol, int32_t invcheck,
+                        int32_t direction, double *err, unsigned long long *n_failed,
+                        unsigned long long *argmax_steps, int32_t device) {
+  if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || (N > 0 && !x) || !err ||
+      (direction != 1 && direction != -1))
+    return set_error(RL_ERR_INVALID, "rl_gmm_run_f64_host: bad argument");
+  Pipeline pl;
+  int rc = pl.init(device);
+  if (rc) return rc;
+  cudaStream_t st = pl.st[0];
+  const size_t P = (size_t)d * (d + 1) / 2;
+  const size_t wsb = gmm_workspace_bytes(d, K, N);
+  const size_t sizes[8] = {(size_t)K * 8, (size_t)K * d * 8, (size_t)K * P * 8,
+                           (size_t)N * d * 8, 8, (size_t)std::max<int64_t>(N, 1), wsb, 16};
+  size_t total = 0;
+  for (size_t b : sizes) total += (b + 255) & ~size_t(255);
+  void *base = nullptr;
+  if ((rc = Pipeline::arena(device, total, &base))) return rc;
+  char *q[8];
+  size_t off = 0;
+  for (int i = 0; i < 8; i++) {
+    q[i] = (char *)base + off;
+    off += (sizes[i] + 255) & ~size_t(255);
+  }
+  const void *src[4] = {alphas, means, icf, x};
+  for (int i = 0; i < 4; i++)
+    if (sizes[i] && (rc = cuda_status(cudaMemcpyAsync(q[i], src[i], sizes[i],
+                                                      cudaMemcpyHostToDevice, st), "H2D")))
+      return rc;
+  if ((rc = cuda_status(cudaMemsetAsync(q[7], 0, 16, st), "memset"))) return rc;
+  const GmmSeq seq{err0, nullptr, nullptr, nullptr, 0, direction};
+  if ((rc = launch_gmm(d, K, N, N, (double *)q[0], (double *)q[1], (double *)q[2],
+                       (double *)q[3], gamma, m, cst, tol, invcheck, 1, (double *)q[4],
+                       (uint8_t *)q[5], (unsigned long long *)q[7], q[6], wsb, st, 0, &seq)))
+    return rc;
+  unsigned long long h[2];
+  if ((rc = cuda_status(cudaMemcpyAsync(err, q[4], 8, cudaMemcpyDeviceToHost, st), "D2H err")) ||
+      (rc = cuda_status(cudaMemcpyAsync(h, q[7], 16, cudaMemcpyDeviceToHost, st), "D2H counters")))
+    return rc;
+  if ((rc = pl.finish())) return rc;
+  if (n_failed) *n_failed = h[1];
+  if (argmax_steps) *argmax_steps = h[0];
+  return RL_OK;
 }
 
 }  // extern "C"
