@@ -64,6 +64,9 @@ def parse_args():
     ap.add_argument("--dry-run", action="store_true",
                     help="no GPU work: exercise the launch / world-size / max-over-ranks "
                          "plumbing under gloo (CPU tests)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: functional check of the N>1 path with every rank "
+                         "folded onto the visible GPU(s) (timings meaningless)")
     ap.add_argument("--n", type=int, default=None, help="override the batch size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -90,6 +93,11 @@ class Dist:
         self.torch = torch
         self.backend = backend
         self.nccl_log = None
+        # this rank's GPU: LOCAL_RANK on an N-GPU node; folded onto the visible
+        # devices only for the single-GPU functional check (--dist-backend gloo)
+        self.gpu = self.local
+        if torch.cuda.is_available() and backend != "nccl":
+            self.gpu = self.local % torch.cuda.device_count()
         if self.dist is not None:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend == "nccl" and torch.cuda.is_available():
@@ -100,9 +108,11 @@ class Dist:
                 os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
                 os.environ.setdefault("NCCL_DEBUG_FILE", self.nccl_log)
                 # bind this rank to its GPU before the communicator is created
-                torch.cuda.set_device(self.local)
-                dist.init_process_group(backend, device_id=torch.device("cuda", self.local))
+                torch.cuda.set_device(self.gpu)
+                dist.init_process_group(backend, device_id=torch.device("cuda", self.gpu))
             else:
+                if torch.cuda.is_available():
+                    torch.cuda.set_device(self.gpu)
                 dist.init_process_group(backend)
             if dist.get_world_size() != self.world:
                 raise SystemExit(f"world size {dist.get_world_size()} != WORLD_SIZE {self.world}")
@@ -357,7 +367,7 @@ def run_bessel_ours(args, D):
     import paper_2003_04617_b200 as rg
     from paper_2003_04617_b200 import kernels
 
-    dev = torch.device("cuda", D.local)
+    dev = torch.device("cuda", D.gpu)
     torch.cuda.set_device(dev)
     n_total = args.n or BESSEL_N
     z, lo, hi = bessel_inputs(torch, n_total, D.rank, D.world, dev)
@@ -486,11 +496,11 @@ def bessel_e2e(torch, z, args, D, n_total):
     outs = (Jh.numpy(), dzh.numpy(), fh.numpy())
     zn = zh.numpy()
     steps = max(2, min(args.steps, 5))
-    kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.local)
+    kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.gpu)
     D.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.local)
+        kernels.besselj_grad_host(zn, BESSEL_NU, out=outs, device=D.gpu)
     dt = D.max((time.perf_counter() - t0) / steps)
     # per rank: z up; J and dJ/dz down, plus per 4 Mi-element chunk a count
     # and a 16384-entry list of the nonzero status codes (capi.cu)
@@ -606,7 +616,7 @@ def run_ba_ours(args, D):
     import torch
 
     from paper_2003_04617_b200 import kernels
-    dev = torch.device("cuda", D.local)
+    dev = torch.device("cuda", D.gpu)
     torch.cuda.set_device(dev)
     p_total = args.n or BA_P
     cams, X, w, feats, obs = ba_synthetic(BA_N, BA_M, p_total)
@@ -710,7 +720,7 @@ def ba_e2e(cams, X, w, feats, obs, args, D):
     def call():
         rc = L.rl_ba_jac_f64_host(cams.shape[0], X.shape[0], p, hc.data_ptr(), hX.data_ptr(),
                                   hw.data_ptr(), hf.data_ptr(), ho.data_ptr(), 1e-9, 1, None,
-                                  hJ.data_ptr(), hfl.data_ptr(), ctypes.byref(nf), D.local)
+                                  hJ.data_ptr(), hfl.data_ptr(), ctypes.byref(nf), D.gpu)
         _native.check(rc, "rl_ba_jac_f64_host")
     call()
     D.barrier()
@@ -821,7 +831,7 @@ def run_gmm_ours(args, D, wl):
     import torch
 
     from paper_2003_04617_b200 import _native, kernels
-    dev = torch.device("cuda", D.local)
+    dev = torch.device("cuda", D.gpu)
     torch.cuda.set_device(dev)
     d, K, N, seed = GMM_CFG[wl]
     N = args.n if (args.n and args.workload == wl) else N
@@ -920,15 +930,18 @@ def run_gmm_ours(args, D, wl):
         "roofline": roof, "gpu_launches": (6 if single else 5) * steps, "clocks": clocks,
         "failed_per_step": n_failed, "objective_only": objective, "restoration": restore,
     }
-    if not args.no_e2e and single:
-        res["e2e"] = gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D)
+    if not args.no_e2e:
+        res["e2e"] = gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D, N)
     return res
 
 
-def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
-    """The drop-in gradient through the C-ABI host-buffer entry
-    (rl_gmm_gradient_f64_host): pinned host inputs up, the packed gradient
-    and the restoration residual down, inside the timed region."""
+def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D, N_total):
+    """The drop-in gradient through the C-ABI host-buffer entries, pinned host
+    inputs up and the packed gradient down inside the timed region.  One GPU:
+    rl_gmm_gradient_f64_host (the restoration residual comes down too).  N
+    GPUs: each rank rl_gmm_grad_shard_f64_host over its points, then the packed
+    vector's sum-allreduce over NCCL (staged through the device) back to host;
+    the time is the max over ranks."""
     import ctypes
 
     import torch
@@ -937,33 +950,56 @@ def gmm_e2e(alphas, means, icf, x, gamma, m, cst, args, D):
     L = _native.lib()
     K, d = means.shape
     N = x.shape[0]
+    single = D.dist is None
     ha, hm, hi_ = alphas.cpu().pin_memory(), means.cpu().pin_memory(), icf.cpu().pin_memory()
     hx = x.cpu().pin_memory()
-    out = torch.empty(1 + K + K * d + K * d * (d + 1) // 2, dtype=torch.float64).pin_memory()
+    nout = 1 + K + K * d + K * d * (d + 1) // 2
+    out = torch.empty(nout, dtype=torch.float64).pin_memory()
+    stage = torch.empty(nout, dtype=torch.float64, device=x.device)
     nf = ctypes.c_ulonglong()
     resid = ctypes.c_double()
 
     def call():
-        rc = L.rl_gmm_gradient_f64_host(d, K, N, ha.data_ptr(), hm.data_ptr(), hi_.data_ptr(),
-                                        hx.data_ptr(), gamma, m, cst, 0.0, 1e-9, 1,
-                                        out.data_ptr(), ctypes.byref(resid), ctypes.byref(nf),
-                                        D.local)
-        if _native.check(rc, "rl_gmm_gradient_f64_host") not in (0, 5):
-            raise RuntimeError(f"rl_gmm_gradient_f64_host: status {rc}")
+        if single:
+            rc = L.rl_gmm_gradient_f64_host(d, K, N, ha.data_ptr(), hm.data_ptr(),
+                                            hi_.data_ptr(), hx.data_ptr(), gamma, m, cst, 0.0,
+                                            1e-9, 1, out.data_ptr(), ctypes.byref(resid),
+                                            ctypes.byref(nf), D.gpu)
+            if _native.check(rc, "rl_gmm_gradient_f64_host") not in (0, 5):
+                raise RuntimeError(f"rl_gmm_gradient_f64_host: status {rc}")
+            return
+        rc = L.rl_gmm_grad_shard_f64_host(d, K, N, N_total, ha.data_ptr(), hm.data_ptr(),
+                                          hi_.data_ptr(), hx.data_ptr(), gamma, m, cst, 1e-9, 1,
+                                          int(D.rank == 0), out.data_ptr(), ctypes.byref(nf),
+                                          D.gpu)
+        _native.check(rc, "rl_gmm_grad_shard_f64_host")
+        stage.copy_(out, non_blocking=True)
+        D.dist.all_reduce(stage)
+        out.copy_(stage)
+
     call()
+    D.barrier()
     t0 = time.perf_counter()
     call()
-    one = time.perf_counter() - t0
+    one = D.max(time.perf_counter() - t0)
     steps = int(min(50, max(3, 0.3 // max(one, 1e-6))))
+    D.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         call()
-    dt = (time.perf_counter() - t0) / steps
+    dt = D.max((time.perf_counter() - t0) / steps)
+    h2d = int(hx.numel() * 8 + (ha.numel() + hm.numel() + hi_.numel()) * 8)
+    d2h = int(out.numel() * 8 + 32)
+    if not single:
+        h2d += nout * 8                     # the packed shard vector staged for NCCL
+    h2d, d2h = int(D.sum(h2d)), int(D.sum(d2h))   # whole job, like the other arms
     return {"value": round(1.0 / dt, 3), "unit": "evals/s", "calls_timed": steps,
-            "h2d_bytes_per_step": int(hx.numel() * 8 + (ha.numel() + hm.numel() + hi_.numel()) * 8),
-            "d2h_bytes_per_step": int(out.numel() * 8 + 32), "ms_per_step": round(dt * 1e3, 3),
-            "path": "rl_gmm_gradient_f64_host (pinned host buffers; device buffers and workspace "
-                    "carved from a per-thread cached arena, cached streams)"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 3),
+            "path": ("rl_gmm_gradient_f64_host (pinned host buffers; device buffers and "
+                     "workspace carved from a per-thread cached arena, cached streams)" if single
+                     else "per rank rl_gmm_grad_shard_f64_host over its points (pinned host "
+                          "buffers) + NCCL sum-allreduce of the packed gradient; max over ranks")}
 
 
 def gmm_cpu(wl, N_full, target_s=1.0):
@@ -1092,7 +1128,7 @@ def main():
         print(json.dumps(reference_arm(args, world)))
         return 0
 
-    D = Dist("gloo" if args.dry_run else "nccl")
+    D = Dist("gloo" if args.dry_run else args.dist_backend)
     if args.dry_run:
         res = dry_line(args, D)
     else:

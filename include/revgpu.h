@@ -147,6 +147,15 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          int32_t m, double cst, double tol, int32_t invcheck, double *out,
                          unsigned long long *n_failed, int32_t device);
 
+/* rl_gmm_grad_f64's shard form over host buffers: this rank's N of N_total
+ * points, add_param_terms on exactly one rank; the caller sum-allreduces out
+ * across ranks (the multi-GPU drop-in, bench.py's N>1 e2e). */
+int rl_gmm_grad_shard_f64_host(int32_t d, int32_t K, int64_t N, int64_t N_total,
+                               const double *alphas, const double *means, const double *icf,
+                               const double *x, double gamma, int32_t m, double cst, double tol,
+                               int32_t invcheck, int32_t add_param_terms, double *out,
+                               unsigned long long *n_failed, int32_t device);
+
 /* ------------------------------------------------------------------------
  * The reference's fuel for gmm (ExecOptions.max_steps counts statement
  * executions per interpreter, interpreter.py:461-466): one sweep of

@@ -51,6 +51,9 @@ SIGNATURES = {
                                        _f64, _f64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rl_gmm_grad_f64_host": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _f64, _i32,
                                             _f64, _f64, _i32, _vp, _ull_p, _i32]),
+    "rl_gmm_grad_shard_f64_host": (ctypes.c_int, [_i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp,
+                                                  _f64, _i32, _f64, _f64, _i32, _i32, _vp, _ull_p,
+                                                  _i32]),
     "rl_gmm_gradient_f64": (ctypes.c_int, [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _f64, _i32,
                                            _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                            _sz, _vp]),

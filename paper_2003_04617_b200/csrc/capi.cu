@@ -781,12 +781,13 @@ int rl_ba_jac_csr_f64_host(int32_t n_cams, int32_t n_pts, int64_t n_obs, const d
 // host-buffer GMM gradient; with `restore` the drop-in gradient() of
 // rl_gmm_gradient_f64 (err! in the reference's order from err0, restoration
 // verdict as the return code), else rl_gmm_grad_f64's
-static int gmm_grad_host(int32_t d, int32_t K, int64_t N, const double *alphas,
-                         const double *means, const double *icf, const double *x, double gamma,
-                         int32_t m, double cst, double tol, int32_t invcheck, double *out,
-                         unsigned long long *n_failed, int32_t device, bool restore, double err0,
-                         double *resid) {
-  if (d <= 0 || K <= 0 || N < 0 || !alphas || !means || !icf || (N > 0 && !x) || !out)
+static int gmm_grad_host(int32_t d, int32_t K, int64_t N, int64_t N_total, int32_t add_param,
+                         const double *alphas, const double *means, const double *icf,
+                         const double *x, double gamma, int32_t m, double cst, double tol,
+                         int32_t invcheck, double *out, unsigned long long *n_failed,
+                         int32_t device, bool restore, double err0, double *resid) {
+  if (d <= 0 || K <= 0 || N < 0 || N_total < N || !alphas || !means || !icf || (N > 0 && !x) ||
+      !out)
     return set_error(RL_ERR_INVALID, "rl_gmm_grad_f64_host: bad argument");
   Pipeline pl;
   int rc = pl.init(device);
@@ -821,8 +822,8 @@ static int gmm_grad_host(int32_t d, int32_t K, int64_t N, const double *alphas,
     return rc;
   unsigned long long *dcnt = (unsigned long long *)dc.p;
   const GmmSeq seq{err0, (double *)(dcnt + 2), (int *)(dcnt + 3), nullptr, 0, 1};
-  if ((rc = launch_gmm(d, K, N, N, (double *)da.p, (double *)dm.p, (double *)di.p,
-                       (double *)dx.p, gamma, m, cst, tol, invcheck, 1, (double *)dout.p,
+  if ((rc = launch_gmm(d, K, N, N_total, (double *)da.p, (double *)dm.p, (double *)di.p,
+                       (double *)dx.p, gamma, m, cst, tol, invcheck, add_param, (double *)dout.p,
                        (uint8_t *)dfl.p, dcnt, dws.p, wsb, st, 1, restore ? &seq : nullptr)))
     return rc;
   unsigned long long h[4];
@@ -845,8 +846,17 @@ int rl_gmm_grad_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
                          const double *means, const double *icf, const double *x, double gamma,
                          int32_t m, double cst, double tol, int32_t invcheck, double *out,
                          unsigned long long *n_failed, int32_t device) {
-  return gmm_grad_host(d, K, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
+  return gmm_grad_host(d, K, N, N, 1, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
                        n_failed, device, false, 0.0, nullptr);
+}
+
+int rl_gmm_grad_shard_f64_host(int32_t d, int32_t K, int64_t N, int64_t N_total,
+                               const double *alphas, const double *means, const double *icf,
+                               const double *x, double gamma, int32_t m, double cst, double tol,
+                               int32_t invcheck, int32_t add_param_terms, double *out,
+                               unsigned long long *n_failed, int32_t device) {
+  return gmm_grad_host(d, K, N, N_total, add_param_terms ? 1 : 0, alphas, means, icf, x, gamma, m,
+                       cst, tol, invcheck, out, n_failed, device, false, 0.0, nullptr);
 }
 
 int rl_gmm_gradient_f64_host(int32_t d, int32_t K, int64_t N, const double *alphas,
@@ -854,7 +864,7 @@ int rl_gmm_gradient_f64_host(int32_t d, int32_t K, int64_t N, const double *alph
                              double gamma, int32_t m, double cst, double err0, double tol,
                              int32_t invcheck, double *out, double *resid,
                              unsigned long long *n_failed, int32_t device) {
-  return gmm_grad_host(d, K, N, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
+  return gmm_grad_host(d, K, N, N, 1, alphas, means, icf, x, gamma, m, cst, tol, invcheck, out,
                        n_failed, device, true, err0, resid);
 }
 

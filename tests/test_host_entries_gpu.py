@@ -76,3 +76,35 @@ def test_ba_residuals_and_gmm_run_host(cuda):
         assert rc == 0 and nf.value == 0
         g = rg.gmm_run(t(al), t(me), t(ic), t(x), 1.0, 0, cst, err0=2.5, direction=direction)
         assert e.value == float(g.out.item()) and up.value == int(g.counters[0].item())
+
+
+def test_gmm_grad_shard_host(cuda):
+    """rl_gmm_grad_shard_f64_host (bench.py's N>1 e2e path): each shard equals
+    the device shard entry bit for bit, and the shards' sum the whole
+    gradient to rounding."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gmm_gpu import gmm_constants, inputs
+    L = _native.lib()
+    d, K, N = 16, 6, 1001
+    al, me, ic, x = (np.ascontiguousarray(v) for v in inputs(np.random.default_rng(8), d, K, N))
+    cst = gmm_constants(d, K, N, 1.0, 0)
+    t = lambda a: torch.as_tensor(a, device=cuda)  # noqa: E731
+    nout = 1 + K + K * d + K * d * (d + 1) // 2
+    total = np.zeros(nout)
+    for lo, hi in ((0, 400), (400, N)):
+        out, nf = np.empty(nout), ctypes.c_ulonglong()
+        xs = np.ascontiguousarray(x[lo:hi])
+        rc = L.rl_gmm_grad_shard_f64_host(d, K, hi - lo, N, _p(al), _p(me), _p(ic), _p(xs), 1.0,
+                                          0, cst, 1e-9, 1, int(lo == 0), _p(out),
+                                          ctypes.byref(nf), 0)
+        assert rc == 0 and nf.value == 0
+        r = kernels.gmm_grad(t(al), t(me), t(ic), t(xs), 1.0, 0, cst, N_total=N,
+                             add_param_terms=(lo == 0))
+        assert np.array_equal(out, r.packed.cpu().numpy())
+        total += out
+    whole, nf = np.empty(nout), ctypes.c_ulonglong()
+    assert L.rl_gmm_grad_f64_host(d, K, N, _p(al), _p(me), _p(ic), _p(x), 1.0, 0, cst, 1e-9, 1,
+                                  _p(whole), ctypes.byref(nf), 0) == 0
+    assert np.allclose(total, whole, rtol=1e-12, atol=1e-9)

@@ -8,4 +8,9 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e \
   --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
-tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/ncu_bench.log
+# the N>1 path (shards, all_reduce, max-over-ranks, shard e2e) functionally,
+# both ranks folded onto this one GPU over gloo: timings meaningless
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29511 bench.py --gpus 2 --dist-backend gloo --steps 3 --warmup 3 \
+  > gpurun_out/bench_gloo2.json 2> gpurun_out/bench_gloo2.err; echo "gloo2 rc=$?" >> gpurun_out/bench_gloo2.err
+tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/ncu_bench.log; tail -1 gpurun_out/bench_gloo2.err
