@@ -38,6 +38,9 @@
 // differ from the sequential reference in rounding only (tests: 1e-10).
 #include <math.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -71,10 +74,11 @@ namespace rl {
 #ifndef GMM_TPF
 #define GMM_TPF 64         // forward tile (points) for DP = 64
 #endif
-#ifndef GMM_X_BULK
-#define GMM_X_BULK 0       // 1: x tiles by per-row TMA bulk copies on an mbarrier instead of
-                           // cp.async per element pair (measured slower: configs[2] 0.222 ->
-                           // 0.255 ms, configs[4]-shape 45.9 -> 51.1 ms)
+#ifndef GMM_X_TMA
+#define GMM_X_TMA 1        // x tiles by one 2D TMA tensor copy per tile (box [TP][DP+4]: the
+                           // padding columns past d arrive as TMA's out-of-bounds zeros) on an
+                           // mbarrier, issued by one thread; 0: cp.async per element pair.
+                           // (Per-row 1D bulk copies, tried first, were slower than cp.async.)
 #endif
 #ifndef GMM_FWD_MINB
 #define GMM_FWD_MINB 2     // forward CTAs per SM (launch bounds) for DP <= 64
@@ -310,11 +314,10 @@ __device__ __forceinline__ void load_x_async(double *__restrict__ xs, const doub
   }
 }
 
-// x tiles by TMA bulk copies: one 1D cp.async.bulk per point row (d * 8
-// bytes, into the padded row stride), issued by warp 0, completion counted
-// on an mbarrier.  Replaces ~TP * DP / 2 cp.async with their index
-// arithmetic per tile (a quarter of the tile kernels' instructions).  Usable
-// when every row is 16-byte aligned and sized (d even, x 16-byte aligned).
+// x tiles by TMA: one 2D tensor copy per tile, issued by one thread,
+// completion counted on an mbarrier.  Replaces ~TP * DP / 2 cp.async with
+// their index arithmetic per tile (a quarter of the tile kernels'
+// instructions).  Usable when the map encodes (d even, x 16-byte aligned).
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -334,31 +337,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
-}
-// warp 0 only: rows [p0, p0 + TP) of x into xs (rows past N zero-filled)
+// one thread: tile [p0, p0 + TP) of x into xs ([TP][XS]) by a 2D TMA
+// tensor copy through the map built by make_x_map (rows past N and columns
+// past d are the copy's out-of-bounds zeros), completion on the mbarrier.
+// The proxy fence orders the CTA's earlier generic reads / writes of this
+// buffer (made visible to this thread by the preceding __syncthreads) before
+// the async-proxy writes.
 template <int DP, int TP>
-__device__ __forceinline__ void load_x_bulk(double *__restrict__ xs, const double *__restrict__ x,
-                                            int d, long long p0, long long N, uint64_t *mbar) {
+__device__ __forceinline__ void load_x_tma(double *__restrict__ xs, const CUtensorMap *tm,
+                                           long long p0, uint64_t *mbar) {
   using C = GmmCfg<DP, TP>;
-  const int lane = threadIdx.x & 31;
-  const long long rem = N - p0;
-  const int rows = rem < TP ? (int)rem : TP;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the generic reads
-  if (lane == 0) mbar_expect(mbar, (unsigned)rows * (unsigned)d * 8u);
-  __syncwarp();
-  for (int r = lane; r < TP; r += 32) {
-    double *dst = xs + r * C::XS;
-    if (r < rows)
-      bulk_g2s(dst, x + (p0 + r) * d, (unsigned)d * 8u, mbar);
-    else
-      for (int a = 0; a < d; a++) dst[a] = 0.0;
-  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect(mbar, (unsigned)(TP * C::XS * 8));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(xs)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"((int)p0), "r"(smem_u32(mbar))
+      : "memory");
 }
 
 // Z tile: acc[m][h] (m-tile m of this warp, column tile h: 0 -> j1, 1 -> j2)
@@ -435,9 +430,10 @@ template <int DP, int TP>
 __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_gmm_fwd(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
-    double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA) {
+    double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA,
+    const __grid_constant__ CUtensorMap xmap, int use_tma) {
   using C = GmmCfg<DP, TP>;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);
   double *xs1 = xs0 + TP * C::XS;
@@ -449,21 +445,22 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
   const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
   // independent of k_gmm_prep (inputs only): before the PDL wait
   __shared__ uint64_t xbar[2];
-  const bool bulk = GMM_X_BULK && !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
-  unsigned xph[2] = {0u, 0u};
+  const bool bulk = use_tma != 0;
+  unsigned xph = 0u;                 // bit b: buffer b's mbarrier parity
   if (bulk && tid == 0) {
     mbar_init(&xbar[0]);
     mbar_init(&xbar[1]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;  // padding stays zero
+  if (!bulk)                     // the cp.async path never writes the padding: zero it once
+    for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;
   for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const long long ntiles = (N + TP - 1) / TP;
   __syncthreads();
   long long tile = blockIdx.y;
   if (tile < ntiles) {
     if (bulk) {
-      if (w == 0) load_x_bulk<DP, TP>(xs0, x, d, tile * TP, N, &xbar[0]);
+      if (tid == 0) load_x_tma<DP, TP>(xs0, &xmap, tile * TP, &xbar[0]);
     } else {
       load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
     }
@@ -478,7 +475,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     const long long nxt = tile + gridDim.y;
     if (nxt < ntiles) {
       if (bulk) {
-        if (w == 0) load_x_bulk<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N, &xbar[buf ^ 1]);
+        if (tid == 0) load_x_tma<DP, TP>(buf ? xs0 : xs1, &xmap, nxt * TP, &xbar[buf ^ 1]);
       } else {
         load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
       }
@@ -486,8 +483,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     cp_commit();
     if (bulk) {
       cp_wait<1>();                                      // L^T (first tile)
-      mbar_wait(&xbar[buf], xph[buf]);
-      xph[buf] ^= 1u;
+      mbar_wait(&xbar[buf], (xph >> buf) & 1u);
+      xph ^= 1u << buf;
     } else {
       cp_wait<1>();
     }
@@ -711,6 +708,24 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
 // also alphas.g and means.g): the S per-CTA partials of k_gmm_rev are summed
 // in order (0.0 + p_0 + p_1 + ...), only over the entries used (the lower
 // triangle).  Whole CTA; gsum: DP doubles and sgp: 1 double of shared memory.
+// 0.0 + p[0] + p[stride] + ... + p[(S-1) stride] in that order, the loads
+// issued eight at a time (the partials sit in L2: one round trip per eight
+// instead of one per term)
+__device__ __forceinline__ double sum_parts_ordered(const double *__restrict__ p, long long stride,
+                                                    int S) {
+  double s = 0.0;
+  int j = 0;
+  for (; j + 8 <= S; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) v[q] = p[(j + q) * stride];
+#pragma unroll
+    for (int q = 0; q < 8; q++) s += v[q];
+  }
+  for (; j < S; j++) s += p[j * stride];
+  return s;
+}
+
 template <int DP>
 __device__ __forceinline__ void gmm_final_component(
     int k, int c, int C, int d, int K, int S, const double *__restrict__ icf,
@@ -727,8 +742,7 @@ __device__ __forceinline__ void gmm_final_component(
   // column sums of qxc.g and sum of mt.g
   for (int b = threadIdx.x; b <= DP; b += GMM_THREADS) {
     if (c != 0 && b != DP) continue;
-    double s = 0.0;
-    for (int j = 0; j < S; j++) s += pk[j * PW + (long long)DP * DP + b];
+    const double s = sum_parts_ordered(pk + (long long)DP * DP + b, PW, S);
     if (b < DP) gsum[b] = s;
     else *sgp = s;
   }
@@ -765,9 +779,7 @@ __device__ __forceinline__ void gmm_final_component(
     if (b * (b + 1) / 2 > e) b--;
     if ((b + 1) * (b + 2) / 2 <= e) b++;
     const int a = e - b * (b + 1) / 2;
-    double m = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < S; j++) m += pk[j * PW + (long long)b * DP + a];
+    const double m = sum_parts_ordered(pk + (long long)b * DP + a, PW, S);
     double g;
     if (a == b) {
       const int j = a;
@@ -813,10 +825,10 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     double *__restrict__ part /* [K][S][DP*DP + DP + 1] */, unsigned *__restrict__ comp_ctr,
     const double *__restrict__ icf, const double *__restrict__ qd,
     const double *__restrict__ ws_par, double ga, int wm, int add_params,
-    double *__restrict__ gout) {
+    double *__restrict__ gout, const __grid_constant__ CUtensorMap xmap, int use_tma) {
   using C = GmmCfg<DP, TP>;
   using MTL = MTiles<DP>;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);
   double *xs1 = xs0 + TP * C::XS;
@@ -830,7 +842,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
   const int j1 = pi, j2 = C::NT - 1 - pi;
   copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
-  for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;
+  if (!use_tma)                  // the cp.async path never writes the padding: zero it once
+    for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;
   for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const double *gm = gmtT + (long long)k * N;
   // this warp's factor-adjoint tiles
@@ -859,8 +872,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   double sgm = 0.0;
   const long long ntiles = (N + TP - 1) / TP;
   __shared__ uint64_t xbar[2];
-  const bool bulk = GMM_X_BULK && !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
-  unsigned xph[2] = {0u, 0u};
+  const bool bulk = use_tma != 0;
+  unsigned xph = 0u;                 // bit b: buffer b's mbarrier parity
   if (bulk && tid == 0) {
     mbar_init(&xbar[0]);
     mbar_init(&xbar[1]);
@@ -870,7 +883,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   long long tile = blockIdx.y;
   if (tile < ntiles) {
     if (bulk) {
-      if (w == 0) load_x_bulk<DP, TP>(xs0, x, d, tile * TP, N, &xbar[0]);
+      if (tid == 0) load_x_tma<DP, TP>(xs0, &xmap, tile * TP, &xbar[0]);
     } else {
       load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
     }
@@ -888,13 +901,13 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     const long long nxt = tile + gridDim.y;
     cp_wait<0>();                                         // L^T / this tile's x (own copies)
     if (bulk) {
-      mbar_wait(&xbar[buf], xph[buf]);
-      xph[buf] ^= 1u;
+      mbar_wait(&xbar[buf], (xph >> buf) & 1u);
+      xph ^= 1u << buf;
     }
     __syncthreads();
     if (nxt < ntiles) {
       if (bulk) {
-        if (w == 0) load_x_bulk<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N, &xbar[buf ^ 1]);
+        if (tid == 0) load_x_tma<DP, TP>(buf ? xs0 : xs1, &xmap, nxt * TP, &xbar[buf ^ 1]);
       } else {
         load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
       }
@@ -1347,6 +1360,44 @@ static int launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
   return cuda_status(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
 }
 
+// the driver's tensor-map encoder, resolved once through the runtime (no
+// libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// x (N x d, row-major f64) as a 2D tensor for load_x_tma: box [TP][DP + 4],
+// the smem tile's padded row stride, so columns d..DP+3 and rows past N
+// arrive as zeros.  False (cp.async path) when TMA cannot address x: odd d
+// (row pitch not a multiple of 16 bytes), x not 16-byte aligned, N >= 2^31.
+template <int DP, int TP>
+static bool make_x_map(CUtensorMap *m, const double *x, int d, long long N) {
+  memset(m, 0, sizeof(*m));
+  if (!GMM_X_TMA || N <= 0 || N >= (1LL << 31) || (d & 1) ||
+      (reinterpret_cast<uintptr_t>(x) & 15))
+    return false;
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)N};
+  cuuint64_t gstride[1] = {(cuuint64_t)d * 8};
+  cuuint32_t box[2] = {(cuuint32_t)GmmCfg<DP, TP>::XS, (cuuint32_t)TP};
+  cuuint32_t estride[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(x), gdim, gstride, box,
+             estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int DP>
 static int run_gmm(int d, int K, long long N, long long N_total, const double *alphas,
                    const double *means, const double *icf, const double *x, double gamma, int m,
@@ -1389,11 +1440,15 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
   if (N > 0) {
     constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
     static_assert(sf <= 227 * 1024 && sr <= 227 * 1024, "shared memory budget");
+    CUtensorMap xmf, xmr;
+    const bool tma_f = make_x_map<DP, TPF>(&xmf, x, d, N);
+    const bool tma_r = grad && make_x_map<DP, TPR>(&xmr, x, d, N);
     if ((rc = smem_attr((const void *)k_gmm_fwd<DP, TPF>, sf, "smem attr fwd")) ||
         (rc = smem_attr((const void *)k_gmm_rev<DP, TPR>, sr, "smem attr rev")))
       return rc;
     if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
-                         d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags)))
+                         d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags, xmf,
+                         (int)tma_f)))
       return rc;
 #ifndef GMM_LSE_Q
 #define GMM_LSE_Q 1
@@ -1423,7 +1478,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
                          d, K, N, means, x, LT, gmt, part,
                          GMM_REV_FINAL ? (unsigned *)(ws + L.ctr) : nullptr, icf, qd, par, gamma,
-                         m, add_params, out)))
+                         m, add_params, out, xmr, (int)tma_r)))
       return rc;
   } else if (!grad) {
     if (seq) return restore(st);
