@@ -405,15 +405,26 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
 
 // xc[j] += x[i, j] - means[k, j], formed once per tile in shared memory
 // over all DP columns (padding columns hold 0 - 0; rows past N are
-// discarded downstream); shift / mask indexing
+// discarded downstream).  Each thread owns one column pair for the whole
+// tile (its two means in registers: mu_pair) and walks the rows with 16-byte
+// accesses; a warp covers contiguous row segments (conflict-free).
+template <int DP>
+__device__ __forceinline__ double2 mu_pair(const double *__restrict__ mu) {
+  return *reinterpret_cast<const double2 *>(mu + 2 * (threadIdx.x % (DP / 2)));
+}
 template <int DP, int TP>
-__device__ __forceinline__ void center_tile(double *__restrict__ xs, const double *__restrict__ mu,
-                                            int) {
+__device__ __forceinline__ void center_tile(double *__restrict__ xs, const double2 mu2) {
   using C = GmmCfg<DP, TP>;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < TP * DP; e += GMM_THREADS) {
-    const int p = e / DP, a = e % DP;
-    xs[p * C::XS + a] = xs[p * C::XS + a] - mu[a];
+  constexpr int CP = DP / 2, RS = GMM_THREADS / CP;      // column pairs / rows per sweep
+  static_assert(GMM_THREADS % CP == 0 && TP % RS == 0, "center_tile shape");
+  double *base = xs + (threadIdx.x / CP) * C::XS + 2 * (threadIdx.x % CP);
+#pragma unroll
+  for (int p = 0; p < TP; p += RS) {
+    double2 *q = reinterpret_cast<double2 *>(base + p * C::XS);
+    double2 v = *q;
+    v.x = v.x - mu2.x;
+    v.y = v.y - mu2.y;
+    *q = v;
   }
 }
 
@@ -457,6 +468,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
   for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const long long ntiles = (N + TP - 1) / TP;
   __syncthreads();
+  const double2 mu2 = mu_pair<DP>(mu);
   long long tile = blockIdx.y;
   if (tile < ntiles) {
     if (bulk) {
@@ -490,7 +502,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     }
     __syncthreads();
     double *xs = buf ? xs1 : xs0;
-    center_tile<DP, TP>(xs, mu, d);
+    center_tile<DP, TP>(xs, mu2);
     __syncthreads();
     double acc[C::MTW][2][4];
     tile_z_tc<DP, TP>(lt_s, xs, acc);
@@ -880,6 +892,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const double2 mu2 = mu_pair<DP>(mu);
   long long tile = blockIdx.y;
   if (tile < ntiles) {
     if (bulk) {
@@ -920,7 +933,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
       cg[p] = 0.0 + (-1.0 * g) * 0.5;                     // mt += sqn*0.5: sqn.g += -mt.g/2
     }
     double *xs = buf ? xs1 : xs0;
-    center_tile<DP, TP>(xs, mu, d);
+    center_tile<DP, TP>(xs, mu2);
     __syncthreads();
     double acc[C::MTW][2][4];
     tile_z_tc<DP, TP>(lt_s, xs, acc);                     // recompute qxc
