@@ -80,9 +80,45 @@ namespace rl {
                            // mbarrier, issued by one thread; 0: cp.async per element pair.
                            // (Per-row 1D bulk copies, tried first, were slower than cp.async.)
 #endif
+#ifndef GMM_FWD_REG_CENTER
+#define GMM_FWD_REG_CENTER 1  // forward (DP <= 64): x - mu formed in the MMA fragments
+                              // (no centering pass; DP = 128 keeps the pass: measured)
+#endif
+#ifndef GMM_FWD_ONE_WAVE
+#define GMM_FWD_ONE_WAVE 0    // forward: at most one wave of CTAs (longer-lived CTAs)
+#endif
+#ifndef GMM_REV_REG_CENTER
+#define GMM_REV_REG_CENTER 0  // reverse: x - mu formed in the MMA fragments (no centering pass)
+#endif
+#ifndef GMM_FWD_THREADS
+#define GMM_FWD_THREADS 256  // forward CTA size for DP <= 64
+#endif
 #ifndef GMM_FWD_MINB
 #define GMM_FWD_MINB 2     // forward CTAs per SM (launch bounds) for DP <= 64
 #endif
+#ifdef GMM_PHASES   // timing-only builds: cycles per phase, summed over warps (tools)
+__device__ unsigned long long g_gmm_phase[32];   // [0, 9): k_gmm_fwd, [16, 25): k_gmm_rev
+// per-thread register accumulators (ph is a literal), flushed once per warp
+#define GMM_MARK(ph)                                                             \
+  do {                                                                           \
+    const long long now_ = clock64();                                            \
+    ph_acc[ph] += now_ - ph_t;                                                   \
+    ph_t = now_;                                                                 \
+  } while (0)
+#define GMM_PH_FLUSH(base)                                                       \
+  do {                                                                           \
+    if ((threadIdx.x & 31) == 0)                                                 \
+      for (int q_ = 0; q_ < 9; q_++)                                             \
+        atomicAdd(&g_gmm_phase[base + q_], (unsigned long long)ph_acc[q_]);      \
+  } while (0)
+#else
+#define GMM_MARK(ph) (void)0
+#define GMM_PH_FLUSH(base) (void)0
+#endif
+#ifndef GMM_ZK_UNROLL
+#define GMM_ZK_UNROLL 1    // k-step unroll of the Z tile loop
+#endif
+constexpr int kZkUnroll = GMM_ZK_UNROLL;
 constexpr int GMM_THREADS = 256;
 constexpr int GMM_WARPS = GMM_THREADS / 32;
 
@@ -92,16 +128,17 @@ constexpr int GMM_WARPS = GMM_THREADS / 32;
 // upper triangle incl. the diagonal qd; a > b entries inside a block are
 // stored zeros).  Row strides that are 4 (mod 16) doubles make every DMMA
 // fragment load conflict-free.
-template <int DP, int TP>
+template <int DP, int TP, int NTH = GMM_THREADS>
 struct GmmCfg {
+  static constexpr int NW = NTH / 32;          // warps per CTA
   static constexpr int NT = DP / 8;            // n-tiles (8 columns) of Z
   static constexpr int NP = NT / 2;            // column-tile pairs {j, NT-1-j}
-  static constexpr int WPP = GMM_WARPS / NP;   // warps per pair
+  static constexpr int WPP = NW / NP;          // warps per pair
   static constexpr int MT = TP / 16;           // m-tiles (16 points)
   static constexpr int MTW = MT / WPP;         // m-tiles per warp
   static constexpr int XS = DP + 4;            // x tile row stride  [TP][XS]
   static constexpr int GS = TP + 4;            // qxc.g tile stride  [DP][GS]
-  static_assert(MT % WPP == 0, "tile shape");
+  static_assert(WPP >= 1 && MT % WPP == 0, "tile shape");
 };
 
 __host__ __device__ constexpr int ltb_off(int DP, int kb) {
@@ -294,12 +331,12 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
 // loop runs over the compile-time-padded [TP][DP/2] grid of column pairs
 // (shift / mask indexing, no division by the runtime d); pairs move as one
 // 16-byte copy when the rows are 16-byte aligned (d even).
-template <int DP, int TP>
+template <int DP, int TP, int NTH = GMM_THREADS>
 __device__ __forceinline__ void load_x_async(double *__restrict__ xs, const double *__restrict__ x,
                                              int d, long long p0, long long N) {
-  using C = GmmCfg<DP, TP>;
+  using C = GmmCfg<DP, TP, NTH>;
   const bool vec = !(d & 1) && !(reinterpret_cast<uintptr_t>(x) & 15);
-  for (int e = threadIdx.x; e < TP * (DP / 2); e += GMM_THREADS) {
+  for (int e = threadIdx.x; e < TP * (DP / 2); e += NTH) {
     const int p = e / (DP / 2), a = 2 * (e % (DP / 2));
     if (a >= d) continue;
     const bool in = p0 + p < N;
@@ -360,10 +397,11 @@ __device__ __forceinline__ void load_x_tma(double *__restrict__ xs, const CUtens
 // = sum_a Xc[p][a] L^T[a][b] over the upper triangle (k-steps ks <= j/2).
 // xs already holds xc = x - mu (see center_tile).  All fragments of a
 // k-step are loaded before its MMAs so the loads overlap.
-template <int DP, int TP>
+template <int DP, int TP, int NTH = GMM_THREADS, bool CENTER = false>
 __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const double *__restrict__ xs,
-                                          double (&acc)[GmmCfg<DP, TP>::MTW][2][4]) {
-  using C = GmmCfg<DP, TP>;
+                                          double (&acc)[GmmCfg<DP, TP, NTH>::MTW][2][4],
+                                          const double *__restrict__ mu = nullptr) {
+  using C = GmmCfg<DP, TP, NTH>;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t0 = lane & 3, t1 = lane >> 2;
   const int pi = w / C::WPP, mw = (w % C::WPP) * C::MTW;
@@ -376,7 +414,7 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
       for (int v = 0; v < 4; v++) acc[m][h][v] = 0.0;
   const int ks_end = j2 / 2, ks1 = j1 / 2;
   const double *xl = xs + (16 * mw + t1) * C::XS + t0;
-#pragma unroll 1
+#pragma unroll kZkUnroll
   for (int ks = 0; ks <= ks_end; ks++) {
     const int kb = 16 * ks, rl = DP - kb + 4;
     const double *ltb = lt + ltb_off(DP, kb) - kb + t0 * rl + t1;  // + 4v*rl + 8j
@@ -394,6 +432,17 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
 #pragma unroll
         for (int v0 = 0; v0 < 2; v0++)
           af[m][v0 + 2 * v1] = xl[(16 * m + 8 * v0) * C::XS + kb + 4 * v1];
+    if (CENTER) {                // xc = x - mu in registers (the tile holds raw x)
+      double mv[4];
+#pragma unroll
+      for (int v1 = 0; v1 < 4; v1++) mv[v1] = mu[kb + 4 * v1 + t0];
+#pragma unroll
+      for (int m = 0; m < C::MTW; m++)
+#pragma unroll
+        for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++) af[m][v0 + 2 * v1] = af[m][v0 + 2 * v1] - mv[v1];
+    }
 #pragma unroll
     for (int m = 0; m < C::MTW; m++) dmma16816(acc[m][1], af[m], b2);
     if (ks <= ks1) {
@@ -412,11 +461,11 @@ template <int DP>
 __device__ __forceinline__ double2 mu_pair(const double *__restrict__ mu) {
   return *reinterpret_cast<const double2 *>(mu + 2 * (threadIdx.x % (DP / 2)));
 }
-template <int DP, int TP>
+template <int DP, int TP, int NTH = GMM_THREADS>
 __device__ __forceinline__ void center_tile(double *__restrict__ xs, const double2 mu2) {
-  using C = GmmCfg<DP, TP>;
-  constexpr int CP = DP / 2, RS = GMM_THREADS / CP;      // column pairs / rows per sweep
-  static_assert(GMM_THREADS % CP == 0 && TP % RS == 0, "center_tile shape");
+  using C = GmmCfg<DP, TP, NTH>;
+  constexpr int CP = DP / 2, RS = NTH / CP;              // column pairs / rows per sweep
+  static_assert(NTH % CP == 0 && TP % RS == 0, "center_tile shape");
   double *base = xs + (threadIdx.x / CP) * C::XS + 2 * (threadIdx.x % CP);
 #pragma unroll
   for (int p = 0; p < TP; p += RS) {
@@ -428,22 +477,25 @@ __device__ __forceinline__ void center_tile(double *__restrict__ xs, const doubl
   }
 }
 
-template <int DP>
+template <int DP, int NTH = GMM_THREADS>
 __device__ __forceinline__ void copy_lt_async(double *__restrict__ lt_s, const double *__restrict__ lt_g) {
   constexpr int n2 = ltb_size(DP) / 2;
-  for (int e = threadIdx.x; e < n2; e += GMM_THREADS) cp_async16(lt_s + 2 * e, lt_g + 2 * e);
+  for (int e = threadIdx.x; e < n2; e += NTH) cp_async16(lt_s + 2 * e, lt_g + 2 * e);
 }
 
 // ---------------------------------------------------------------------------
 // forward: mt[k][i] = alphas[k] + sq[k] - |L_k (x_i - mu_k)|^2 / 2
 // ---------------------------------------------------------------------------
-template <int DP, int TP>
-__global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_gmm_fwd(
+template <int DP, int TP, int NTH>
+__global__ void __launch_bounds__(NTH, DP == 128 ? 1 : GMM_FWD_MINB) k_gmm_fwd(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ x, const double *__restrict__ LT, const double *__restrict__ sq,
     double tol, int chk, double *__restrict__ mtT, unsigned *__restrict__ flagsA,
     const __grid_constant__ CUtensorMap xmap, int use_tma) {
-  using C = GmmCfg<DP, TP>;
+  using C = GmmCfg<DP, TP, NTH>;
+#ifdef GMM_PHASES
+  long long ph_t = clock64(), ph_acc[9] = {};
+#endif
   extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);
@@ -464,8 +516,8 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!bulk)                     // the cp.async path never writes the padding: zero it once
-    for (int e = tid; e < 2 * TP * C::XS; e += GMM_THREADS) xs0[e] = 0.0;
-  for (int a = tid; a < DP; a += GMM_THREADS) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
+    for (int e = tid; e < 2 * TP * C::XS; e += NTH) xs0[e] = 0.0;
+  for (int a = tid; a < DP; a += NTH) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   const long long ntiles = (N + TP - 1) / TP;
   __syncthreads();
   const double2 mu2 = mu_pair<DP>(mu);
@@ -474,38 +526,69 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
     if (bulk) {
       if (tid == 0) load_x_tma<DP, TP>(xs0, &xmap, tile * TP, &xbar[0]);
     } else {
-      load_x_async<DP, TP>(xs0, x, d, tile * TP, N);
+      load_x_async<DP, TP, NTH>(xs0, x, d, tile * TP, N);
     }
   }
   cp_commit();
   pdl_wait();                                            // prep's L^T, sq and zeroed flags
-  copy_lt_async<DP>(lt_s, LT + (long long)k * ltb_size(DP));
+  copy_lt_async<DP, NTH>(lt_s, LT + (long long)k * ltb_size(DP));
   cp_commit();
   const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
   int buf = 0;
+  GMM_MARK(0);
   for (; tile < ntiles; tile += gridDim.y) {
     const long long nxt = tile + gridDim.y;
+#ifdef GMM_NO_XLOAD              // timing-only builds: reuse the first tile (no x traffic)
+    if (false) {
+#else
     if (nxt < ntiles) {
+#endif
       if (bulk) {
         if (tid == 0) load_x_tma<DP, TP>(buf ? xs0 : xs1, &xmap, nxt * TP, &xbar[buf ^ 1]);
       } else {
-        load_x_async<DP, TP>(buf ? xs0 : xs1, x, d, nxt * TP, N);
+        load_x_async<DP, TP, NTH>(buf ? xs0 : xs1, x, d, nxt * TP, N);
       }
     }
     cp_commit();
     if (bulk) {
       cp_wait<1>();                                      // L^T (first tile)
+#ifdef GMM_NO_XLOAD
+      if (tile == blockIdx.y)
+#endif
       mbar_wait(&xbar[buf], (xph >> buf) & 1u);
       xph ^= 1u << buf;
     } else {
       cp_wait<1>();
     }
+    GMM_MARK(1);
     __syncthreads();
+    GMM_MARK(2);
     double *xs = buf ? xs1 : xs0;
-    center_tile<DP, TP>(xs, mu2);
-    __syncthreads();
     double acc[C::MTW][2][4];
-    tile_z_tc<DP, TP>(lt_s, xs, acc);
+    if constexpr (GMM_FWD_REG_CENTER && DP <= 64) {
+      GMM_MARK(3);
+      GMM_MARK(4);
+      tile_z_tc<DP, TP, NTH, true>(lt_s, xs, acc, mu);
+    } else {
+      center_tile<DP, TP, NTH>(xs, mu2);
+      GMM_MARK(3);
+      __syncthreads();
+      GMM_MARK(4);
+      tile_z_tc<DP, TP, NTH>(lt_s, xs, acc);
+    }
+    GMM_MARK(5);
+#ifdef GMM_FWD_REPEAT            // timing-only builds: the MMA phase's marginal cost
+    for (int r = 1; r < GMM_FWD_REPEAT; r++) {
+      double a2[C::MTW][2][4];
+      tile_z_tc<DP, TP, NTH>(lt_s, xs, a2);
+#pragma unroll
+      for (int m = 0; m < C::MTW; m++)
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) acc[m][h][v] += a2[m][h][v];
+    }
+#endif
     // sqn partial over this warp's 16 columns, per point (sqn += abs2(qxc[j]))
 #pragma unroll
     for (int m = 0; m < C::MTW; m++)
@@ -520,8 +603,10 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
         s += __shfl_xor_sync(FULL_MASK, s, 2);
         if (t0 == 0) sqp[pi * TP + 16 * (mw + m) + t1 + 8 * v1] = s;
       }
+    GMM_MARK(6);
     __syncthreads();
-    for (int p = tid; p < TP; p += GMM_THREADS) {
+    GMM_MARK(7);
+    for (int p = tid; p < TP; p += NTH) {
       const long long i = tile * TP + p;
       if (i >= N) continue;
       double sqn = 0.0;
@@ -535,8 +620,10 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_FWD_MINB) k_g
       if (chk && fabs(res) > tol) atomicOr(&flagsA[i], 1u);
       mtT[(long long)k * N + i] = base_mt - sqn * 0.5;    // mt -= sqn * 0.5
     }
+    GMM_MARK(8);
     buf ^= 1;
   }
+  GMM_PH_FLUSH(0);
   cp_wait<0>();
 }
 
@@ -840,6 +927,9 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
     double *__restrict__ gout, const __grid_constant__ CUtensorMap xmap, int use_tma) {
   using C = GmmCfg<DP, TP>;
   using MTL = MTiles<DP>;
+#ifdef GMM_PHASES
+  long long ph_t = clock64(), ph_acc[9] = {};
+#endif
   extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);
@@ -893,6 +983,11 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   }
   __syncthreads();
   const double2 mu2 = mu_pair<DP>(mu);
+#if GMM_REV_REG_CENTER
+  double muq[MTL::PER];                                   // means of this warp's M-tile columns
+#pragma unroll
+  for (int q = 0; q < MTL::PER; q++) muq[q] = ti[q] < 0 ? 0.0 : mu[8 * tj[q] + t1];
+#endif
   long long tile = blockIdx.y;
   if (tile < ntiles) {
     if (bulk) {
@@ -906,6 +1001,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   // grid early): only mt.g below needs the wait
   pdl_wait();
   int buf = 0;
+  GMM_MARK(0);
   // Three barriers per tile: the next tile's prefetch is issued after the
   // top barrier (whose arrival means every warp has finished reading that
   // buffer in the previous tile's M product), so no end-of-tile barrier.
@@ -918,6 +1014,7 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
       xph ^= 1u << buf;
     }
     __syncthreads();
+    GMM_MARK(1);
     if (nxt < ntiles) {
       if (bulk) {
         if (tid == 0) load_x_tma<DP, TP>(buf ? xs0 : xs1, &xmap, nxt * TP, &xbar[buf ^ 1]);
@@ -926,24 +1023,52 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
       }
     }
     cp_commit();
+    double *xs = buf ? xs1 : xs0;
+#if GMM_REV_REG_CENTER
+    // x - mu is formed in the MMA fragments (no centering pass, no barrier);
+    // each lane reads the mt.g of its own points
+    double cgr[C::MTW][2];
+#pragma unroll
+    for (int m = 0; m < C::MTW; m++)
+#pragma unroll
+      for (int v1 = 0; v1 < 2; v1++) {
+        const long long i = p0 + 16 * (mw + m) + t1 + 8 * v1;
+        cgr[m][v1] = i < N ? gm[i] : 0.0;
+      }
+    for (int p = tid; p < TP; p += GMM_THREADS) {
+      const long long i = p0 + p;
+      sgm += i < N ? gm[i] : 0.0;                         // alphas.g, sq.g += mt.g
+    }
+    (void)mu2;
+    double acc[C::MTW][2][4];
+    tile_z_tc<DP, TP, GMM_THREADS, true>(lt_s, xs, acc, mu);  // recompute qxc
+#else
     for (int p = tid; p < TP; p += GMM_THREADS) {
       const long long i = p0 + p;
       const double g = i < N ? gm[i] : 0.0;
       sgm += g;                                           // alphas.g, sq.g += mt.g
       cg[p] = 0.0 + (-1.0 * g) * 0.5;                     // mt += sqn*0.5: sqn.g += -mt.g/2
     }
-    double *xs = buf ? xs1 : xs0;
+    GMM_MARK(2);
     center_tile<DP, TP>(xs, mu2);
+    GMM_MARK(3);
     __syncthreads();
+    GMM_MARK(4);
     double acc[C::MTW][2][4];
     tile_z_tc<DP, TP>(lt_s, xs, acc);                     // recompute qxc
+#endif
+    GMM_MARK(5);
     // qxc.g[j] = sqn.g * (2 qxc[j]) -> smem (transposed) and column sums
 #pragma unroll
     for (int m = 0; m < C::MTW; m++)
 #pragma unroll
       for (int v1 = 0; v1 < 2; v1++) {
         const int pp = 16 * (mw + m) + t1 + 8 * v1;
+#if GMM_REV_REG_CENTER
+        const double c = 0.0 + (-1.0 * cgr[m][v1]) * 0.5;  // mt += sqn*0.5: sqn.g += -mt.g/2
+#else
         const double c = cg[pp];
+#endif
 #pragma unroll
         for (int h = 0; h < 2; h++)
 #pragma unroll
@@ -953,7 +1078,9 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
             gt[(8 * (h ? j2 : j1) + 2 * t0 + v0) * C::GS + pp] = g;
           }
       }
+    GMM_MARK(6);
     __syncthreads();
+    GMM_MARK(7);
     // M[b][a] += sum_p G[p][b] Xc[p][a]: A = G^T (b x p), B = Xc (p x a)
 #pragma unroll
     for (int ks = 0; ks < TP / 16; ks++) {
@@ -975,11 +1102,17 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
         double bf[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) bf[v] = xs[(pb + t0 + 4 * v) * C::XS + cb + t1];
+#if GMM_REV_REG_CENTER
+#pragma unroll
+        for (int v = 0; v < 4; v++) bf[v] = bf[v] - muq[q];
+#endif
         dmma16816(M[q], af, bf);
       }
     }
+    GMM_MARK(8);
     buf ^= 1;
   }
+  GMM_PH_FLUSH(16);
   cp_wait<0>();
   // write this block's partial: M tiles, column sums, sum of mt.g
   const int S = gridDim.y;
@@ -1256,6 +1389,8 @@ static int gmm_side(GmmSide **out) {
 static int dp_of(int d) { return d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 0)); }
 // points per tile: forward / reverse (the reverse also stages qxc.g)
 static constexpr int tpf_c(int DP) { return DP == 64 ? GMM_TPF : 64; }
+// forward CTA size: GMM_FWD_THREADS for DP <= 64 (DP = 128 needs 8 warps)
+static constexpr int ntf_c(int DP) { return DP == 128 ? GMM_THREADS : GMM_FWD_THREADS; }
 static int tpf_of(int DP) { return tpf_c(DP); }
 static constexpr int tpr_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? GMM_TPR64 : 32); }
 static int tpr_of(int DP) { return tpr_c(DP); }
@@ -1264,9 +1399,9 @@ static int tpr_of(int DP) { return tpr_c(DP); }
 static int fwd_per_sm(int DP) { return DP == 128 ? 1 : GMM_FWD_MINB; }
 static int rev_per_sm(int DP) { return DP == 128 ? 1 : GMM_REV_MINB; }
 
-template <int DP, int TP>
+template <int DP, int TP, int NTH>
 static constexpr size_t smem_fwd() {
-  using C = GmmCfg<DP, TP>;
+  using C = GmmCfg<DP, TP, NTH>;
   return ((size_t)ltb_size(DP) + 2 * (size_t)TP * C::XS + DP + (size_t)C::NP * TP) * 8;
 }
 template <int DP, int TP>
@@ -1313,6 +1448,8 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   const long long ntf = (N + tpf_of(DP) - 1) / tpf_of(DP);
   const long long ntr = (N + tpr_of(DP) - 1) / tpr_of(DP);
   L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * fwd_per_sm(DP), 64);
+  if (GMM_FWD_ONE_WAVE)
+    L.Sf = (int)std::max<long long>(1, std::min<long long>(ntf, 148 * fwd_per_sm(DP) / K));
   // each reverse CTA writes a (DP^2 + DP + 1)-double partial: cap them at 256 MB
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
@@ -1404,7 +1541,7 @@ static bool make_x_map(CUtensorMap *m, const double *x, int d, long long N) {
   if (!enc) return false;
   cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)N};
   cuuint64_t gstride[1] = {(cuuint64_t)d * 8};
-  cuuint32_t box[2] = {(cuuint32_t)GmmCfg<DP, TP>::XS, (cuuint32_t)TP};
+  cuuint32_t box[2] = {(cuuint32_t)(DP + 4), (cuuint32_t)TP};     // GmmCfg::XS
   cuuint32_t estride[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(x), gdim, gstride, box,
              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1417,7 +1554,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                    double cst, double tol, int chk, int add_params, double *out, uint8_t *fail,
                    unsigned long long *counters, char *ws, const GmmLayout &L, cudaStream_t st,
                    int grad, const GmmSeq *seq) {
-  constexpr int TPF = tpf_c(DP), TPR = tpr_c(DP);
+  constexpr int TPF = tpf_c(DP), TPR = tpr_c(DP), NTF = ntf_c(DP);
   double *LT = (double *)(ws + L.lt), *qd = (double *)(ws + L.qd), *sq = (double *)(ws + L.sq);
   double *fro = (double *)(ws + L.fro);
   double *mt = (double *)(ws + L.mt), *gmt = (double *)(ws + L.gmt);
@@ -1451,15 +1588,15 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
                                              (unsigned *)(ws + L.ctr));
   if ((rc = cuda_status(cudaGetLastError(), "k_gmm_prep"))) return rc;
   if (N > 0) {
-    constexpr size_t sf = smem_fwd<DP, TPF>(), sr = smem_rev<DP, TPR>();
+    constexpr size_t sf = smem_fwd<DP, TPF, NTF>(), sr = smem_rev<DP, TPR>();
     static_assert(sf <= 227 * 1024 && sr <= 227 * 1024, "shared memory budget");
     CUtensorMap xmf, xmr;
     const bool tma_f = make_x_map<DP, TPF>(&xmf, x, d, N);
     const bool tma_r = grad && make_x_map<DP, TPR>(&xmr, x, d, N);
-    if ((rc = smem_attr((const void *)k_gmm_fwd<DP, TPF>, sf, "smem attr fwd")) ||
+    if ((rc = smem_attr((const void *)k_gmm_fwd<DP, TPF, NTF>, sf, "smem attr fwd")) ||
         (rc = smem_attr((const void *)k_gmm_rev<DP, TPR>, sr, "smem attr rev")))
       return rc;
-    if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF>, dim3(K, L.Sf), dim3(GMM_THREADS), sf, st,
+    if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF, NTF>, dim3(K, L.Sf), dim3(NTF), sf, st,
                          d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags, xmf,
                          (int)tma_f)))
       return rc;
@@ -1549,5 +1686,13 @@ int launch_gmm(int32_t d, int32_t K, int64_t N, int64_t N_total, const double *a
   return run_gmm<128>(d, K, N, Nt, alphas, means, icf, x, gamma, m, cst, tol, chk,
                       add_param_terms, out, fail, counters, (char *)ws, L, st, grad, seq);
 }
+
+#ifdef GMM_PHASES
+extern "C" int rl_debug_gmm_phases(unsigned long long *out32) {  // timing-only builds
+  cudaMemcpyFromSymbol(out32, g_gmm_phase, 32 * sizeof(unsigned long long));
+  static const unsigned long long zero[32] = {};
+  return (int)cudaMemcpyToSymbol(g_gmm_phase, zero, sizeof zero);
+}
+#endif
 
 }  // namespace rl
