@@ -87,6 +87,15 @@ namespace rl {
 #ifndef GMM_FWD_ONE_WAVE
 #define GMM_FWD_ONE_WAVE 0    // forward: at most one wave of CTAs (longer-lived CTAs)
 #endif
+#ifndef GMM_WS
+#define GMM_WS 1              // DP <= 64, d even: the warp-specialised tile kernels
+#endif
+#ifndef GMM_WS_FWD_MINB
+#define GMM_WS_FWD_MINB 3
+#endif
+#ifndef GMM_WS_REV_MINB
+#define GMM_WS_REV_MINB 2
+#endif
 #ifndef GMM_REV_REG_CENTER
 #define GMM_REV_REG_CENTER 0  // reverse: x - mu formed in the MMA fragments (no centering pass)
 #endif
@@ -1173,6 +1182,380 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised tile kernels (DP <= 64).  One producer warp streams the x
+// tiles by TMA into a two-slot ring (full / empty mbarriers, no CTA-wide
+// barrier per tile); each of the eight compute warps owns one (feature row
+// block i, m-tile m) of every tile: the features 16i..16i+15 of Z (n-tiles
+// 2i, 2i+1 over k-steps 0..i) for its 16 points, and in the reverse kernel
+// also the factor-adjoint row block i over those points, its G^T rows taken
+// from a warp-private scratch (no CTA barrier between the two products).
+// Warps w and w + 4 share a scheduler partition and hold the row blocks
+// i and NI - 1 - i, so every partition issues the same number of MMAs.
+// ---------------------------------------------------------------------------
+template <int DP, int TP>
+struct WsCfg {
+  static constexpr int NI = DP / 16;           // feature row blocks
+  static constexpr int MT = TP / 16;           // m-tiles of 16 points
+  static constexpr int NCW = 8;                // compute warps
+  static constexpr int NTH = (NCW + 1) * 32;   // + the producer warp
+  static constexpr int XS = DP + 4;            // x tile row stride (the TMA box row)
+  static constexpr int SS = 20;                // G scratch row stride: [16 features][16 points + 4]
+  static_assert((NI / 2) * MT == 4, "8 compute warps = 4 (block pair, m-tile) x 2");
+};
+
+template <int DP, int TP>
+__device__ __forceinline__ void ws_role(int w, int &i, int &m) {
+  using W = WsCfg<DP, TP>;
+  const int c = w & 3, u = w >> 2, pair = c / W::MT;
+  m = c % W::MT;
+  i = u == 0 ? pair : W::NI - 1 - pair;
+}
+
+__device__ __forceinline__ void mbar_init_n(uint64_t *m, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// the producer warp: tile t of this CTA into slot t & 1 once every compute
+// warp has released the slot's previous tile
+template <int DP, int TP>
+__device__ __forceinline__ void ws_producer(const CUtensorMap *xmap, long long ntiles,
+                                            double *xs0, uint64_t *full, uint64_t *empty) {
+  using W = WsCfg<DP, TP>;
+  if ((threadIdx.x & 31) != 0) return;
+  int t = 0;
+  for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y, t++) {
+    const int b = t & 1;
+    if (t >= 2) mbar_wait(&empty[b], ((t >> 1) - 1) & 1);
+    load_x_tma<DP, TP>(xs0 + b * TP * W::XS, xmap, tile * TP, &full[b]);
+  }
+}
+
+// Z[p][16i + 8h + c] for the warp's 16 points (h = 0, 1: n-tiles 2i, 2i+1),
+// xc = x - mu formed in the fragments
+template <int DP, int TP>
+__device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double *__restrict__ xs,
+                                     const double *__restrict__ mu, int i, int m,
+                                     double (&acc)[2][4]) {
+  using W = WsCfg<DP, TP>;
+  const int lane = threadIdx.x & 31, t0 = lane & 3, t1 = lane >> 2;
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int v = 0; v < 4; v++) acc[h][v] = 0.0;
+  const double *xl = xs + (16 * m + t1) * W::XS + t0;
+#pragma unroll 1
+  for (int ks = 0; ks <= i; ks++) {
+    const int kb = 16 * ks, rl = DP - kb + 4;
+    const double *ltb = lt + ltb_off(DP, kb) - kb + t0 * rl + t1 + 16 * i;
+    double b0[4], b1[4], af[8], mv[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      b0[v] = ltb[4 * v * rl];
+      b1[v] = ltb[4 * v * rl + 8];
+      mv[v] = mu[kb + 4 * v + t0];
+    }
+#pragma unroll
+    for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+      for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = xl[8 * v0 * W::XS + kb + 4 * v1] - mv[v1];
+    dmma16816(acc[0], af, b0);
+    dmma16816(acc[1], af, b1);
+  }
+}
+
+template <int DP, int TP>
+__global__ void __launch_bounds__(WsCfg<DP, TP>::NTH, GMM_WS_FWD_MINB) k_gmm_fwd_ws(
+    int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
+    const double *__restrict__ LT, const double *__restrict__ sq, double tol, int chk,
+    double *__restrict__ mtT, unsigned *__restrict__ flagsA, const __grid_constant__ CUtensorMap xmap) {
+  using W = WsCfg<DP, TP>;
+  extern __shared__ __align__(128) double smem[];
+  double *lt_s = smem;
+  double *xs0 = lt_s + ltb_size(DP);             // [2][TP][XS]
+  double *mu = xs0 + 2 * TP * W::XS;             // [DP], zero padded
+  double *sqp = mu + DP;                         // [2][NI][TP]: per-block sqn partials
+  __shared__ uint64_t full[2], empty[2];
+  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int t0 = lane & 3, t1 = lane >> 2;
+  if (tid == 0) {
+    mbar_init(&full[0]);
+    mbar_init(&full[1]);
+    mbar_init_n(&empty[0], W::NCW);
+    mbar_init_n(&empty[1], W::NCW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int a = tid; a < DP; a += W::NTH) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
+  const long long ntiles = (N + TP - 1) / TP;
+  __syncthreads();
+  if (w == W::NCW) {                             // x only: runs ahead of k_gmm_prep
+    ws_producer<DP, TP>(&xmap, ntiles, xs0, full, empty);
+    return;
+  }
+  pdl_wait();                                    // prep's L^T, sq and zeroed flags
+  copy_lt_async<DP, W::NCW * 32>(lt_s, LT + (long long)k * ltb_size(DP));
+  cp_commit();
+  const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
+  int i, m;
+  ws_role<DP, TP>(w, i, m);
+  cp_wait<0>();
+  named_bar(1, W::NCW * 32);                     // L^T in shared memory
+  int t = 0;
+  for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y, t++) {
+    const int b = t & 1;
+    mbar_wait(&full[b], (t >> 1) & 1);
+    double acc[2][4];
+    ws_z<DP, TP>(lt_s, xs0 + b * TP * W::XS, mu, i, m, acc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);       // this warp's reads of the slot are done
+    // sqn partial over the block's 16 features, per point (sqn += abs2(qxc[j]))
+    double *sq_t = sqp + b * W::NI * TP;
+#pragma unroll
+    for (int v1 = 0; v1 < 2; v1++) {
+      double s = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int v0 = 0; v0 < 2; v0++) s = fma(acc[h][v0 + 2 * v1], acc[h][v0 + 2 * v1], s);
+      s += __shfl_xor_sync(FULL_MASK, s, 1);
+      s += __shfl_xor_sync(FULL_MASK, s, 2);
+      if (t0 == 0) sq_t[i * TP + 16 * m + t1 + 8 * v1] = s;
+    }
+    named_bar(2 + m, W::NI * 32);                // the NI warps of this m-tile
+    if (i == 0 && lane < 16) {
+      const int p = 16 * m + lane;
+      const long long ii = tile * TP + p;
+      if (ii < N) {
+        double sqn = 0.0;
+#pragma unroll
+        for (int q = 0; q < W::NI; q++) sqn = sqn + sq_t[q * TP + p];
+        // the inner routine's uncompute: sqn -= abs2(qxc[j]) in reverse, then
+        // the release check sqn -> 0.0 (interpreter.py:738-745)
+        double res = sqn;
+#pragma unroll
+        for (int q = W::NI - 1; q >= 0; q--) res = res - sq_t[q * TP + p];
+        if (chk && fabs(res) > tol) atomicOr(&flagsA[ii], 1u);
+        mtT[(long long)k * N + ii] = base_mt - sqn * 0.5;  // mt -= sqn * 0.5
+      }
+    }
+  }
+}
+
+// reverse, one role (row block I, m-tile m): recompute Z, qxc.g = (-dmt/2)(2Z),
+// and the factor-adjoint tiles (I, j) over the warp's points.  With NI = 4
+// the last block's tiles j = 4..7 are taken by its partition partner (block
+// 0, same m-tile) from the last block's G^T scratch (double-buffered, one
+// 64-thread barrier per tile), so no warp holds more than six M tiles (the
+// register budget of two CTAs per SM) and each partition still issues the
+// same number of MMAs.  Warp 0 lane 0 also produces the x ring: tile t + 1
+// is issued once every warp has released tile t - 1's slot.
+template <int DP, int TP>
+struct RevWs {
+  using W = WsCfg<DP, TP>;
+  static constexpr bool SPLIT = W::NI == 4;
+  // own tiles of block I: j in [0, own(I)); the partner of block NI-1 adds 4
+  __host__ __device__ static constexpr int own(int I) { return (SPLIT && I == W::NI - 1) ? 4 : 2 * I + 2; }
+  __host__ __device__ static constexpr bool borrows(int I) { return SPLIT && I == 0; }
+  __host__ __device__ static constexpr bool lends(int I) { return SPLIT && I == W::NI - 1; }
+};
+
+template <int DP, int TP, int I>
+__device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__restrict__ lt,
+                                            double *xs0, const double *__restrict__ mu,
+                                            double *scr, const double *__restrict__ gm,
+                                            uint64_t *full, uint64_t *empty,
+                                            const CUtensorMap *xmap, double *mbuf, double *cs,
+                                            double *red) {
+  using W = WsCfg<DP, TP>;
+  using R = RevWs<DP, TP>;
+  constexpr int NO = R::own(I);                          // own tiles
+  constexpr int NB = R::borrows(I) ? 4 : 0;              // borrowed tiles (NI-1, 4..7)
+  const int lane = threadIdx.x & 31, t0 = lane & 3, t1 = lane >> 2, w = threadIdx.x >> 5;
+  const long long ntiles = (N + TP - 1) / TP;
+  const bool producer = w == 0 && lane == 0;
+  // scratch: [2][16][SS] per warp; the lending warp's is read by its partner
+  double *sc_own = scr + w * 2 * 16 * W::SS;
+  const double *sc_lend = scr + (w + 4) * 2 * 16 * W::SS;   // borrower: partner is warp w + 4
+  double M[NO + NB][4];
+#pragma unroll
+  for (int j = 0; j < NO + NB; j++)
+#pragma unroll
+    for (int v = 0; v < 4; v++) M[j][v] = 0.0;
+  double gsum[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double sgm = 0.0;
+  int t = 0;
+  for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y, t++) {
+    const int b = t & 1;
+    if (producer && tile + gridDim.y < ntiles) {         // next tile into the other slot
+      if (t >= 1) mbar_wait(&empty[b ^ 1], ((t - 1) >> 1) & 1);
+      load_x_tma<DP, TP>(xs0 + (b ^ 1) * TP * W::XS, xmap, (tile + gridDim.y) * TP, &full[b ^ 1]);
+    }
+    const long long p0 = tile * TP + 16 * m + t1;
+    const double g0 = p0 < N ? gm[p0] : 0.0, g1 = p0 + 8 < N ? gm[p0 + 8] : 0.0;
+    mbar_wait(&full[b], (t >> 1) & 1);
+    const double *xs = xs0 + b * TP * W::XS;
+    double acc[2][4];
+    ws_z<DP, TP>(lt, xs, mu, I, m, acc);                   // recompute qxc
+    if (I == 0 && t0 == 0) {
+      sgm += g0;                                           // alphas.g, sq.g += mt.g
+      sgm += g1;
+    }
+    // mt += sqn*0.5: sqn.g += -mt.g/2; qxc.g[j] = sqn.g * (2 qxc[j])
+    const double c0 = 0.0 + (-1.0 * g0) * 0.5, c1 = 0.0 + (-1.0 * g1) * 0.5;
+    double *sc = sc_own + b * 16 * W::SS;
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const double g = ((v >> 1) ? c1 : c0) * (2.0 * acc[h][v]);
+        gsum[h][v & 1] += g;
+        sc[(8 * h + 2 * t0 + (v & 1)) * W::SS + t1 + 8 * (v >> 1)] = g;
+      }
+    __syncwarp();
+    if (R::lends(I) || R::borrows(I)) named_bar(2 + m, 64);   // the lender's G^T is written
+    // M[16I + r][c] += sum_p G^T[r][p] Xc[p][c]: A = G^T (scratch), B = Xc
+    const double *xb = xs + (16 * m + t0) * W::XS + t1;
+    double af[8];
+#pragma unroll
+    for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+      for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = sc[(t1 + 8 * v0) * W::SS + t0 + 4 * v1];
+#pragma unroll
+    for (int j = 0; j < NO; j++) {
+      const double muj = mu[8 * j + t1];
+      double bf[4];
+#pragma unroll
+      for (int v = 0; v < 4; v++) bf[v] = xb[4 * v * W::XS + 8 * j] - muj;
+      dmma16816(M[j], af, bf);
+    }
+    if constexpr (NB > 0) {
+      const double *sl = sc_lend + b * 16 * W::SS;
+#pragma unroll
+      for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+        for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = sl[(t1 + 8 * v0) * W::SS + t0 + 4 * v1];
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        const double muj = mu[8 * (4 + j) + t1];
+        double bf[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) bf[v] = xb[4 * v * W::XS + 8 * (4 + j)] - muj;
+        dmma16816(M[NO + j], af, bf);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);                // slot reads done
+  }
+  // block partial: the m-tiles' M added in order through shared memory (the
+  // x ring, idle now), then column sums and sum of mt.g
+  named_bar(1, W::NCW * 32);
+  for (int r = 0; r < W::MT; r++) {
+    if (m == r) {
+#pragma unroll
+      for (int j = 0; j < NO + NB; j++) {
+        const int rb = (j < NO ? I : W::NI - 1), cb = (j < NO ? j : 4 + j - NO);
+#pragma unroll
+        for (int v1 = 0; v1 < 2; v1++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++) {
+            double *e = mbuf + (16 * rb + t1 + 8 * v1) * DP + 8 * cb + 2 * t0 + v0;
+            *e = r == 0 ? M[j][v0 + 2 * v1] : *e + M[j][v0 + 2 * v1];
+          }
+      }
+    }
+    named_bar(1, W::NCW * 32);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int v0 = 0; v0 < 2; v0++) {
+      double v = gsum[h][v0];
+      v += __shfl_xor_sync(FULL_MASK, v, 4);
+      v += __shfl_xor_sync(FULL_MASK, v, 8);
+      v += __shfl_xor_sync(FULL_MASK, v, 16);
+      if (t1 == 0) cs[m * DP + 16 * I + 8 * h + 2 * t0 + v0] = v;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sgm += __shfl_down_sync(FULL_MASK, sgm, o);
+  if (lane == 0) red[w] = sgm;
+}
+
+template <int DP, int TP>
+__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_REV_MINB) k_gmm_rev_ws(
+    int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ LT,
+    const double *__restrict__ gmtT, double *__restrict__ part /* [K][S][DP*DP + DP + 1] */,
+    const __grid_constant__ CUtensorMap xmap) {
+  using W = WsCfg<DP, TP>;
+  constexpr int NT = W::NCW * 32;
+  extern __shared__ __align__(128) double smem[];
+  double *lt_s = smem;
+  double *xs0 = lt_s + ltb_size(DP);             // [2][TP][XS]
+  double *mu = xs0 + 2 * TP * W::XS;             // [DP]
+  double *scr = mu + DP;                         // [NCW][2][16][SS]: G^T per warp
+  double *red = scr + W::NCW * 2 * 16 * W::SS;   // [NCW]
+  static_assert(DP * DP + W::MT * DP <= 2 * TP * W::XS, "block partial fits the x ring");
+  __shared__ uint64_t full[2], empty[2];
+  const int k = blockIdx.x, tid = threadIdx.x, w = tid >> 5;
+  const long long ntiles = (N + TP - 1) / TP;
+  if (tid == 0) {
+    mbar_init(&full[0]);
+    mbar_init(&full[1]);
+    mbar_init_n(&empty[0], W::NCW);
+    mbar_init_n(&empty[1], W::NCW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // x only: the first tile runs ahead of k_gmm_lse
+    if (blockIdx.y < ntiles) load_x_tma<DP, TP>(xs0, &xmap, (long long)blockIdx.y * TP, &full[0]);
+  }
+  for (int a = tid; a < DP; a += NT) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
+  // L^T (prep), means and x are ready before k_gmm_lse ends (it launches
+  // this grid early): only mt.g needs the wait
+  copy_lt_async<DP, NT>(lt_s, LT + (long long)k * ltb_size(DP));
+  cp_commit();
+  int i, m;
+  ws_role<DP, TP>(w, i, m);
+  cp_wait<0>();
+  __syncthreads();
+  pdl_wait();
+  const double *gm = gmtT + (long long)k * N;
+  double *mbuf = xs0, *cs = xs0 + DP * DP;
+  switch (i) {
+    case 0: rev_ws_role<DP, TP, 0>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); break;
+    case 1: rev_ws_role<DP, TP, 1>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); break;
+    case 2:
+      if constexpr (W::NI > 2)
+        rev_ws_role<DP, TP, 2>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red);
+      break;
+    default:
+      if constexpr (W::NI > 3)
+        rev_ws_role<DP, TP, 3>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red);
+      break;
+  }
+  __syncthreads();
+  const int S = gridDim.y;
+  const long long PW = (long long)DP * DP + DP + 1;
+  double *out = part + ((long long)k * S + blockIdx.y) * PW;
+  for (int e = tid; e < DP * DP; e += NT) {
+    const int r = e / DP, c = e % DP;
+    if ((c >> 4) <= (r >> 4)) out[e] = mbuf[e];          // the lower-triangle tiles
+  }
+  for (int bb = tid; bb < DP; bb += NT) {
+    double v = 0.0;
+    for (int q = 0; q < W::MT; q++) v += cs[q * DP + bb];
+    out[(long long)DP * DP + bb] = v;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+    for (int ww = 0; ww < W::NCW; ww++) s += red[ww];
+    out[(long long)DP * DP + DP] = s;
+  }
+}
+
 // sum of the per-block point objectives into red[0] (whole block; the same
 // order in k_gmm_final and k_gmm_err, so the objective-only run reproduces
 // the gradient's objective bit for bit)
@@ -1394,6 +1777,9 @@ static constexpr int ntf_c(int DP) { return DP == 128 ? GMM_THREADS : GMM_FWD_TH
 static int tpf_of(int DP) { return tpf_c(DP); }
 static constexpr int tpr_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? GMM_TPR64 : 32); }
 static int tpr_of(int DP) { return tpr_c(DP); }
+// the warp-specialised kernels' tile (DP <= 64): 4 (block pair, m-tile) combos
+static constexpr int tpw_c(int DP) { return DP == 32 ? 64 : 32; }
+static bool use_ws(int d) { return GMM_WS && d <= 64 && !(d & 1); }
 // concurrent CTAs per SM the split assumes: forward 2 (DP <= 64), reverse
 // GMM_REV_MINB (DP <= 64); DP = 128 runs one CTA per SM
 static int fwd_per_sm(int DP) { return DP == 128 ? 1 : GMM_FWD_MINB; }
@@ -1445,15 +1831,17 @@ static int launch_gmm_err_only(int K, const GmmLayout &L, long long N, const dou
 static GmmLayout gmm_layout(int d, int K, long long N) {
   GmmLayout L{};
   const int DP = dp_of(d);
-  const long long ntf = (N + tpf_of(DP) - 1) / tpf_of(DP);
-  const long long ntr = (N + tpr_of(DP) - 1) / tpr_of(DP);
-  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * fwd_per_sm(DP), 64);
+  const bool ws = use_ws(d);
+  const int tf = ws ? tpw_c(DP) : tpf_of(DP), tr = ws ? tpw_c(DP) : tpr_of(DP);
+  const long long ntf = (N + tf - 1) / tf;
+  const long long ntr = (N + tr - 1) / tr;
+  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * (ws ? GMM_WS_FWD_MINB : fwd_per_sm(DP)), 64);
   if (GMM_FWD_ONE_WAVE)
     L.Sf = (int)std::max<long long>(1, std::min<long long>(ntf, 148 * fwd_per_sm(DP) / K));
   // each reverse CTA writes a (DP^2 + DP + 1)-double partial: cap them at 256 MB
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
-  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * rev_per_sm(DP), smax);
+  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * (ws ? GMM_WS_REV_MINB : rev_per_sm(DP)), smax);
   L.nerr = (int)((N + LSE_THREADS - 1) / LSE_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -1596,7 +1984,27 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     if ((rc = smem_attr((const void *)k_gmm_fwd<DP, TPF, NTF>, sf, "smem attr fwd")) ||
         (rc = smem_attr((const void *)k_gmm_rev<DP, TPR>, sr, "smem attr rev")))
       return rc;
-    if (!(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF, NTF>, dim3(K, L.Sf), dim3(NTF), sf, st,
+    // the warp-specialised kernels (DP <= 64, x addressable by TMA)
+    CUtensorMap xmw;
+    bool wsk = false;
+    if constexpr (DP <= 64) {
+      constexpr int TPW = tpw_c(DP);
+      using W = WsCfg<DP, TPW>;
+      wsk = use_ws(d) && !GMM_REV_FINAL && make_x_map<DP, TPW>(&xmw, x, d, N);
+      constexpr size_t sfw = ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + 2 * W::NI * TPW) * 8;
+      constexpr size_t srw =
+          ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + W::NCW * 2 * 16 * W::SS + W::NCW) * 8;
+      if (wsk) {
+        if ((rc = smem_attr((const void *)k_gmm_fwd_ws<DP, TPW>, sfw, "smem attr fwd_ws")) ||
+            (rc = smem_attr((const void *)k_gmm_rev_ws<DP, TPW>, srw, "smem attr rev_ws")))
+          return rc;
+        if (!(GMM_ABLATE & 16) &&
+            (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPW>, dim3(K, L.Sf), dim3(W::NTH), sfw,
+                             st, d, K, N, alphas, means, LT, sq, tol, chk, mt, flags, xmw)))
+          return rc;
+      }
+    }
+    if (!wsk && !(GMM_ABLATE & 16) && (rc = launch_pdl("k_gmm_fwd", k_gmm_fwd<DP, TPF, NTF>, dim3(K, L.Sf), dim3(NTF), sf, st,
                          d, K, N, alphas, means, x, LT, sq, tol, chk, mt, flags, xmf,
                          (int)tma_f)))
       return rc;
@@ -1625,7 +2033,17 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
           (rc = cuda_status(cudaEventRecord(side->join, side->s), "join record")))
         return rc;
     }
-    if (!(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
+    if constexpr (DP <= 64) {
+      constexpr int TPW = tpw_c(DP);
+      using W = WsCfg<DP, TPW>;
+      constexpr size_t srw =
+          ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + W::NCW * 2 * 16 * W::SS + W::NCW) * 8;
+      if (wsk && !(GMM_ABLATE & 32) &&
+          (rc = launch_pdl("k_gmm_rev_ws", k_gmm_rev_ws<DP, TPW>, dim3(K, L.Sr), dim3(W::NCW * 32), srw,
+                           st, d, K, N, means, LT, gmt, part, xmw)))
+        return rc;
+    }
+    if (!wsk && !(GMM_ABLATE & 32) && (rc = launch_pdl("k_gmm_rev", k_gmm_rev<DP, TPR>, dim3(K, L.Sr), dim3(GMM_THREADS), sr, st,
                          d, K, N, means, x, LT, gmt, part,
                          GMM_REV_FINAL ? (unsigned *)(ws + L.ctr) : nullptr, icf, qd, par, gamma,
                          m, add_params, out, xmr, (int)tma_r)))
