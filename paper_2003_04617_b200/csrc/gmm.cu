@@ -90,6 +90,12 @@ namespace rl {
 #ifndef GMM_WS
 #define GMM_WS 1              // DP <= 64, d even: the warp-specialised tile kernels
 #endif
+#ifndef GMM_DIAG_M8
+#define GMM_DIAG_M8 1         // reverse: diagonal factor-adjoint tiles by m8n8k4 (half the flops)
+#endif
+#ifndef GMM_FWD_MPW
+#define GMM_FWD_MPW 1         // warp-specialised forward: m-tiles (16 points) per warp
+#endif
 #ifndef GMM_WS_FWD_MINB
 #define GMM_WS_FWD_MINB 3
 #endif
@@ -333,6 +339,21 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
         "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// m16n8k8: the first half (k 0..7) of a k16 fragment pair (a[0..3], b[0..1])
+__device__ __forceinline__ void dmma16808(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+// m8n8k4: c (row t1, cols 2 t0, 2 t0 + 1) += a (row t1, col t0) b (row t0, col t1)
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
 }
 
 // issue the async copy of tile [p0, p0 + TP) of x into xs ([TP][XS]; rows
@@ -1201,7 +1222,6 @@ struct WsCfg {
   static constexpr int NTH = (NCW + 1) * 32;   // + the producer warp
   static constexpr int XS = DP + 4;            // x tile row stride (the TMA box row)
   static constexpr int SS = 20;                // G scratch row stride: [16 features][16 points + 4]
-  static_assert((NI / 2) * MT == 4, "8 compute warps = 4 (block pair, m-tile) x 2");
 };
 
 template <int DP, int TP>
@@ -1250,14 +1270,13 @@ __device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double
 #pragma unroll
     for (int v = 0; v < 4; v++) acc[h][v] = 0.0;
   const double *xl = xs + (16 * m + t1) * W::XS + t0;
-#pragma unroll 1
-  for (int ks = 0; ks <= i; ks++) {
+  auto step = [&](int ks, bool last) {
     const int kb = 16 * ks, rl = DP - kb + 4;
     const double *ltb = lt + ltb_off(DP, kb) - kb + t0 * rl + t1 + 16 * i;
     double b0[4], b1[4], af[8], mv[4];
 #pragma unroll
     for (int v = 0; v < 4; v++) {
-      b0[v] = ltb[4 * v * rl];
+      b0[v] = (last && v >= 2) ? 0.0 : ltb[4 * v * rl];
       b1[v] = ltb[4 * v * rl + 8];
       mv[v] = mu[kb + 4 * v + t0];
     }
@@ -1265,17 +1284,67 @@ __device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double
     for (int v1 = 0; v1 < 4; v1++)
 #pragma unroll
       for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = xl[8 * v0 * W::XS + kb + 4 * v1] - mv[v1];
-    dmma16816(acc[0], af, b0);
+    // n-tile 2i needs rows a <= 16i + 7 only: its last k-step is a k8 MMA
+    if (last) dmma16808(acc[0], af, b0);
+    else dmma16816(acc[0], af, b0);
     dmma16816(acc[1], af, b1);
+  };
+#pragma unroll 1
+  for (int ks = 0; ks < i; ks++) step(ks, false);
+  step(i, true);
+}
+
+// Z for MPW consecutive m-tiles m0.. of the warp (the L^T fragments loaded
+// once per k-step for all of them)
+template <int DP, int TP, int MPW>
+__device__ __forceinline__ void ws_zm(const double *__restrict__ lt, const double *__restrict__ xs,
+                                      const double *__restrict__ mu, int i, int m0,
+                                      double (&acc)[MPW][2][4]) {
+  using W = WsCfg<DP, TP>;
+  const int lane = threadIdx.x & 31, t0 = lane & 3, t1 = lane >> 2;
+#pragma unroll
+  for (int q = 0; q < MPW; q++)
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) acc[q][h][v] = 0.0;
+  const double *xl = xs + (16 * m0 + t1) * W::XS + t0;
+#pragma unroll 1
+  for (int ks = 0; ks <= i; ks++) {
+    const int kb = 16 * ks, rl = DP - kb + 4;
+    const double *ltb = lt + ltb_off(DP, kb) - kb + t0 * rl + t1 + 16 * i;
+    double b0[4], b1[4], mv[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      b0[v] = ltb[4 * v * rl];
+      b1[v] = ltb[4 * v * rl + 8];
+      mv[v] = mu[kb + 4 * v + t0];
+    }
+#pragma unroll
+    for (int q = 0; q < MPW; q++) {
+      double af[8];
+#pragma unroll
+      for (int v1 = 0; v1 < 4; v1++)
+#pragma unroll
+        for (int v0 = 0; v0 < 2; v0++)
+          af[v0 + 2 * v1] = xl[(16 * q + 8 * v0) * W::XS + kb + 4 * v1] - mv[v1];
+      if (ks < i) dmma16816(acc[q][0], af, b0);   // n-tile 2i: last k-step k8
+      else dmma16808(acc[q][0], af, b0);
+      dmma16816(acc[q][1], af, b1);
+    }
   }
 }
 
-template <int DP, int TP>
-__global__ void __launch_bounds__(WsCfg<DP, TP>::NTH, GMM_WS_FWD_MINB) k_gmm_fwd_ws(
+// forward: warp roles (row block i, m-tiles mm*MPW..), x produced by warp 0
+// lane 0 (tile t + 1 once every warp released tile t - 1's slot)
+template <int DP, int TP, int MPW>
+__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_FWD_MINB) k_gmm_fwd_ws(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ LT, const double *__restrict__ sq, double tol, int chk,
     double *__restrict__ mtT, unsigned *__restrict__ flagsA, const __grid_constant__ CUtensorMap xmap) {
   using W = WsCfg<DP, TP>;
+  constexpr int NT = W::NCW * 32, MG = W::MT / MPW;      // m-groups
+  static_assert((W::NI / 2) * MG == 4, "8 warps = 4 (block pair, m-group) x 2");
   extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);             // [2][TP][XS]
@@ -1284,52 +1353,59 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NTH, GMM_WS_FWD_MINB) k_gmm_fwd
   __shared__ uint64_t full[2], empty[2];
   const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t0 = lane & 3, t1 = lane >> 2;
+  const long long ntiles = (N + TP - 1) / TP;
   if (tid == 0) {
     mbar_init(&full[0]);
     mbar_init(&full[1]);
     mbar_init_n(&empty[0], W::NCW);
     mbar_init_n(&empty[1], W::NCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // x only: the first tile runs ahead of k_gmm_prep
+    if (blockIdx.y < ntiles) load_x_tma<DP, TP>(xs0, &xmap, (long long)blockIdx.y * TP, &full[0]);
   }
-  for (int a = tid; a < DP; a += W::NTH) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
-  const long long ntiles = (N + TP - 1) / TP;
-  __syncthreads();
-  if (w == W::NCW) {                             // x only: runs ahead of k_gmm_prep
-    ws_producer<DP, TP>(&xmap, ntiles, xs0, full, empty);
-    return;
-  }
+  for (int a = tid; a < DP; a += NT) mu[a] = a < d ? means[(long long)k * d + a] : 0.0;
   pdl_wait();                                    // prep's L^T, sq and zeroed flags
-  copy_lt_async<DP, W::NCW * 32>(lt_s, LT + (long long)k * ltb_size(DP));
+  copy_lt_async<DP, NT>(lt_s, LT + (long long)k * ltb_size(DP));
   cp_commit();
   const double base_mt = (0.0 + alphas[k]) + sq[k];     // mt += alphas[k]; mt += sq[k]
-  int i, m;
-  ws_role<DP, TP>(w, i, m);
+  const int c = w & 3, pair = c / MG, mm = c % MG;
+  const int i = (w >> 2) == 0 ? pair : W::NI - 1 - pair;
+  const bool producer = w == 0 && lane == 0;
   cp_wait<0>();
-  named_bar(1, W::NCW * 32);                     // L^T in shared memory
+  __syncthreads();                               // L^T, means, barriers
   int t = 0;
   for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y, t++) {
     const int b = t & 1;
+    if (producer && tile + gridDim.y < ntiles) {
+      if (t >= 1) mbar_wait(&empty[b ^ 1], ((t - 1) >> 1) & 1);
+      load_x_tma<DP, TP>(xs0 + (b ^ 1) * TP * W::XS, &xmap, (tile + gridDim.y) * TP, &full[b ^ 1]);
+    }
     mbar_wait(&full[b], (t >> 1) & 1);
-    double acc[2][4];
-    ws_z<DP, TP>(lt_s, xs0 + b * TP * W::XS, mu, i, m, acc);
+    double acc[MPW][2][4];
+    ws_zm<DP, TP, MPW>(lt_s, xs0 + b * TP * W::XS, mu, i, mm * MPW, acc);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);       // this warp's reads of the slot are done
     // sqn partial over the block's 16 features, per point (sqn += abs2(qxc[j]))
     double *sq_t = sqp + b * W::NI * TP;
 #pragma unroll
-    for (int v1 = 0; v1 < 2; v1++) {
-      double s = 0.0;
+    for (int q = 0; q < MPW; q++)
 #pragma unroll
-      for (int h = 0; h < 2; h++)
+      for (int v1 = 0; v1 < 2; v1++) {
+        double s = 0.0;
 #pragma unroll
-        for (int v0 = 0; v0 < 2; v0++) s = fma(acc[h][v0 + 2 * v1], acc[h][v0 + 2 * v1], s);
-      s += __shfl_xor_sync(FULL_MASK, s, 1);
-      s += __shfl_xor_sync(FULL_MASK, s, 2);
-      if (t0 == 0) sq_t[i * TP + 16 * m + t1 + 8 * v1] = s;
-    }
-    named_bar(2 + m, W::NI * 32);                // the NI warps of this m-tile
-    if (i == 0 && lane < 16) {
-      const int p = 16 * m + lane;
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int v0 = 0; v0 < 2; v0++)
+            s = fma(acc[q][h][v0 + 2 * v1], acc[q][h][v0 + 2 * v1], s);
+        s += __shfl_xor_sync(FULL_MASK, s, 1);
+        s += __shfl_xor_sync(FULL_MASK, s, 2);
+        if (t0 == 0) sq_t[i * TP + 16 * (mm * MPW + q) + t1 + 8 * v1] = s;
+      }
+    named_bar(1 + mm, W::NI * 32);               // the NI warps of this m-group
+    // each of the group's NI warps finishes 16 MPW / NI of its points
+    constexpr int PPW = 16 * MPW / W::NI;
+    if (lane < PPW) {
+      const int p = 16 * mm * MPW + i * PPW + lane;
       const long long ii = tile * TP + p;
       if (ii < N) {
         double sqn = 0.0;
@@ -1421,6 +1497,18 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
     if (R::lends(I) || R::borrows(I)) named_bar(2 + m, 64);   // the lender's G^T is written
     // M[16I + r][c] += sum_p G^T[r][p] Xc[p][c]: A = G^T (scratch), B = Xc
     const double *xb = xs + (16 * m + t0) * W::XS + t1;
+    // the diagonal tile (rows 16 rb .. + 15, cols 16 rb + 8 .. + 15) is used
+    // in its lower 8 rows only: four m8n8k4 MMAs (k = the 16 points) into
+    // the tile's row-half v1 = 1
+    auto diag = [&](double (&Mj)[4], const double *g, int col0) {
+      const double muj = mu[col0 + t1];
+      double c2[2] = {Mj[2], Mj[3]};
+#pragma unroll
+      for (int kq = 0; kq < 4; kq++)
+        dmma884(c2, g[(8 + t1) * W::SS + 4 * kq + t0], xb[4 * kq * W::XS + col0] - muj);
+      Mj[2] = c2[0];
+      Mj[3] = c2[1];
+    };
     double af[8];
 #pragma unroll
     for (int v1 = 0; v1 < 4; v1++)
@@ -1428,6 +1516,10 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
       for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = sc[(t1 + 8 * v0) * W::SS + t0 + 4 * v1];
 #pragma unroll
     for (int j = 0; j < NO; j++) {
+      if (GMM_DIAG_M8 && j == 2 * I + 1) {
+        diag(M[j], sc, 8 * j);
+        continue;
+      }
       const double muj = mu[8 * j + t1];
       double bf[4];
 #pragma unroll
@@ -1442,6 +1534,10 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
         for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = sl[(t1 + 8 * v0) * W::SS + t0 + 4 * v1];
 #pragma unroll
       for (int j = 0; j < NB; j++) {
+        if (GMM_DIAG_M8 && j == NB - 1) {                  // tile (NI-1, 2 NI - 1)
+          diag(M[NO + j], sl, 8 * (4 + j));
+          continue;
+        }
         const double muj = mu[8 * (4 + j) + t1];
         double bf[4];
 #pragma unroll
@@ -1493,6 +1589,7 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_REV_MINB) k_gm
     const __grid_constant__ CUtensorMap xmap) {
   using W = WsCfg<DP, TP>;
   constexpr int NT = W::NCW * 32;
+  static_assert((W::NI / 2) * W::MT == 4, "8 warps = 4 (block pair, m-tile) x 2");
   extern __shared__ __align__(128) double smem[];
   double *lt_s = smem;
   double *xs0 = lt_s + ltb_size(DP);             // [2][TP][XS]
@@ -1779,6 +1876,8 @@ static constexpr int tpr_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? GMM_TPR6
 static int tpr_of(int DP) { return tpr_c(DP); }
 // the warp-specialised kernels' tile (DP <= 64): 4 (block pair, m-tile) combos
 static constexpr int tpw_c(int DP) { return DP == 32 ? 64 : 32; }
+// the warp-specialised forward: GMM_FWD_MPW m-tiles per warp
+static constexpr int tpfw_c(int DP) { return tpw_c(DP) * GMM_FWD_MPW; }
 static bool use_ws(int d) { return GMM_WS && d <= 64 && !(d & 1); }
 // concurrent CTAs per SM the split assumes: forward 2 (DP <= 64), reverse
 // GMM_REV_MINB (DP <= 64); DP = 128 runs one CTA per SM
@@ -1832,7 +1931,7 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   GmmLayout L{};
   const int DP = dp_of(d);
   const bool ws = use_ws(d);
-  const int tf = ws ? tpw_c(DP) : tpf_of(DP), tr = ws ? tpw_c(DP) : tpr_of(DP);
+  const int tf = ws ? tpfw_c(DP) : tpf_of(DP), tr = ws ? tpw_c(DP) : tpr_of(DP);
   const long long ntf = (N + tf - 1) / tf;
   const long long ntr = (N + tr - 1) / tr;
   L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * (ws ? GMM_WS_FWD_MINB : fwd_per_sm(DP)), 64);
@@ -1985,22 +2084,27 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
         (rc = smem_attr((const void *)k_gmm_rev<DP, TPR>, sr, "smem attr rev")))
       return rc;
     // the warp-specialised kernels (DP <= 64, x addressable by TMA)
-    CUtensorMap xmw;
+    CUtensorMap xmw, xmwf;
     bool wsk = false;
     if constexpr (DP <= 64) {
-      constexpr int TPW = tpw_c(DP);
+      constexpr int TPW = tpw_c(DP), TPFW = tpfw_c(DP);
       using W = WsCfg<DP, TPW>;
-      wsk = use_ws(d) && !GMM_REV_FINAL && make_x_map<DP, TPW>(&xmw, x, d, N);
-      constexpr size_t sfw = ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + 2 * W::NI * TPW) * 8;
+      using WF = WsCfg<DP, TPFW>;
+      wsk = use_ws(d) && !GMM_REV_FINAL && make_x_map<DP, TPW>(&xmw, x, d, N) &&
+            make_x_map<DP, TPFW>(&xmwf, x, d, N);
+      constexpr size_t sfw =
+          ((size_t)ltb_size(DP) + 2 * TPFW * WF::XS + DP + 2 * WF::NI * TPFW) * 8;
       constexpr size_t srw =
           ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + W::NCW * 2 * 16 * W::SS + W::NCW) * 8;
       if (wsk) {
-        if ((rc = smem_attr((const void *)k_gmm_fwd_ws<DP, TPW>, sfw, "smem attr fwd_ws")) ||
+        if ((rc = smem_attr((const void *)k_gmm_fwd_ws<DP, TPFW, GMM_FWD_MPW>, sfw,
+                            "smem attr fwd_ws")) ||
             (rc = smem_attr((const void *)k_gmm_rev_ws<DP, TPW>, srw, "smem attr rev_ws")))
           return rc;
         if (!(GMM_ABLATE & 16) &&
-            (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPW>, dim3(K, L.Sf), dim3(W::NTH), sfw,
-                             st, d, K, N, alphas, means, LT, sq, tol, chk, mt, flags, xmw)))
+            (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPFW, GMM_FWD_MPW>, dim3(K, L.Sf),
+                             dim3(WF::NCW * 32), sfw, st, d, K, N, alphas, means, LT, sq, tol, chk,
+                             mt, flags, xmwf)))
           return rc;
       }
     }
@@ -2069,7 +2173,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     // enough (k, c) CTAs for about two per SM, at most 8 per component
     const int fc = std::max(1, std::min(8, (2 * 148 + K - 1) / K));
     // with the replay, the objective comes from k_gmm_restore (no extra column)
-    if ((rc = launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K + (seq ? 0 : 1), fc),
+    if (!(GMM_ABLATE & 64) &&
+        (rc = launch_pdl("k_gmm_final", k_gmm_final<DP>, dim3(K + (seq ? 0 : 1), fc),
                          dim3(GMM_THREADS), 0, st, d, K, L.Sr, N > 0 ? L.nerr : 0, icf, qd, sq,
                          fro, LT, part, errp, par, gamma, m, cst, add_params, out)))
       return rc;

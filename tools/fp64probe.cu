@@ -110,7 +110,70 @@ __global__ void __launch_bounds__(256) k_mixed(double *out, int iters, int nm, i
   if (s == 1234.5678) out[0] = s;
 }
 
+__global__ void __launch_bounds__(256) k_dmma_m16n8k8(double *out, int iters) {
+  double a[4], b[2];
+#pragma unroll
+  for (int j = 0; j < 4; j++) a[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll
+  for (int j = 0; j < 2; j++) b[j] = 1.0 - threadIdx.x * 1e-4 - j * 1e-5;
+  double c[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]), "+d"(c[j][2]), "+d"(c[j][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) s += c[j][0] + c[j][1] + c[j][2] + c[j][3];
+  if (s == 1234.5678) out[0] = s;
+}
+
+// one warp: a dependent chain of m16n8k16 (which 1) / m16n8k8 (2) / m8n8k4 (0)
+// MMAs on one accumulator; cycles per MMA into out[0]
+__global__ void k_dmma_lat(double *out, int which, int n) {
+  double a[8], b[4], c[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < 8; j++) a[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll
+  for (int j = 0; j < 4; j++) b[j] = 1.0 - threadIdx.x * 1e-4;
+  const long long t0 = clock64();
+  for (int i = 0; i < n; i++) {
+    if (which == 1)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                   : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]),
+                     "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    else if (which == 2)
+      asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+    else
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[0]), "+d"(c[1]) : "d"(a[0]), "d"(b[0]));
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (double)(t1 - t0) / n;
+  if (c[0] + c[1] + c[2] + c[3] == 1234.5678) out[1] = 1.0;
+}
+
 extern "C" {
+
+double probe_dmma_latency(int which, int n) {
+  double *out, h = 0;
+  cudaMalloc(&out, 16);
+  k_dmma_lat<<<1, 32>>>(out, which, n);
+  k_dmma_lat<<<1, 32>>>(out, which, n);
+  cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+  cudaFree(out);
+  return h;
+}
 
 // TFLOP/s of k_mixed (DMMA 4096 flop each, DFMA 2 flop per lane)
 double probe_mixed(int iters, int nm, int nf, float *ms_out) {
@@ -145,6 +208,8 @@ double probe_dmma_peak(int which, int iters, float *ms_out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (which == 0)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dmma_m8n8k4, 256, 0);
+  else if (which == 2)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dmma_m16n8k8, 256, 0);
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dmma_m16n8k16, 256, 0);
   double *out;
@@ -156,6 +221,7 @@ double probe_dmma_peak(int which, int iters, float *ms_out) {
   for (int rep = 0; rep < 2; rep++) {
     cudaEventRecord(a);
     if (which == 0) k_dmma_m8n8k4<<<grid, block>>>(out, iters);
+    else if (which == 2) k_dmma_m16n8k8<<<grid, block>>>(out, iters);
     else k_dmma_m16n8k16<<<grid, block>>>(out, iters);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
@@ -164,7 +230,7 @@ double probe_dmma_peak(int which, int iters, float *ms_out) {
   cudaEventElapsedTime(&ms, a, b);
   cudaFree(out);
   if (ms_out) *ms_out = ms;
-  const double per_mma = which == 0 ? 2.0 * 8 * 8 * 4 : 2.0 * 16 * 8 * 16;
+  const double per_mma = which == 0 ? 2.0 * 8 * 8 * 4 : (which == 2 ? 2.0 * 16 * 8 * 8 : 2.0 * 16 * 8 * 16);
   const double mmas = (double)iters * (which == 0 ? 8 : 4) * grid.x * (block.x / 32);
   return mmas * per_mma / (ms * 1e-3) / 1e12;
 }
