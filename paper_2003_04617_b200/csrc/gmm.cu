@@ -60,9 +60,6 @@ namespace rl {
 #ifndef GMM_ALPHA_BLOCK
 #define GMM_ALPHA_BLOCK 1  // k_gmm_prep: the alphas' logsumexp in its own block (else block 0)
 #endif
-#ifndef GMM_PREP_BLOCKS
-#define GMM_PREP_BLOCKS 1  // k_gmm_prep: L^T built block by block (constant row lengths)
-#endif
 #ifndef GMM_REV_FINAL
 #define GMM_REV_FINAL 0    // 1: k_gmm_rev's last CTA per component assembles its gradient instead
                            // of k_gmm_final (measured slower: configs[2] 0.2214 -> 0.2416 ms, one
@@ -210,6 +207,34 @@ __device__ void gmm_alpha_lse(int K, long long N_total, const double *__restrict
   }
 }
 
+// element e of the packed L^T block layout from the component's icf row
+// (ic: shared memory): exp of the log-diagonal, the strict lower triangle
+// transposed, zeros elsewhere
+template <int DP>
+__device__ __forceinline__ double lt_elem(const double *__restrict__ ic, int d, int kb, int r) {
+  const int rl = DP - kb + 4;
+  const int a = kb + r / rl, b = kb + r % rl;
+  double v = 0.0;
+  if (a < d && b < d) {
+    if (b == a) {
+      v = exp(ic[a]);                                    // qd[k, j] += exp(icf[k, j])
+    } else if (b > a) {
+      // icf column-major strict lower triangle: (row b, col a), a < b
+      v = ic[d + a * d - a * (a + 1) / 2 + (b - a - 1)];
+    }
+  }
+  return v;
+}
+// the whole packed L^T of one component into dst, NT threads
+template <int DP, int NT>
+__device__ __forceinline__ void build_lt(const double *__restrict__ ic, int d, double *dst) {
+#pragma unroll
+  for (int q = 0; q < DP / 16; q++) {
+    const int kb = 16 * q, rl = DP - kb + 4, off = ltb_off(DP, kb);
+    for (int r = threadIdx.x; r < 16 * rl; r += NT) dst[off + r] = lt_elem<DP>(ic, d, kb, r);
+  }
+}
+
 template <int DP>
 __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long long N_total,
                                                           const double *__restrict__ alphas,
@@ -247,38 +272,10 @@ __global__ void __launch_bounds__(GMM_THREADS) k_gmm_prep(int d, int K, long lon
   constexpr int LTS = ltb_size(DP);
   double *lt = LT + (long long)k * LTS;
   (void)LTS;
-#if GMM_PREP_BLOCKS
   // the packed layout row block by row block: the row length rl is a
   // compile-time constant per (unrolled) block, so e -> (a, b) is a
   // multiply-shift instead of a search and two runtime divisions
-#pragma unroll
-  for (int q = 0; q < DP / 16; q++) {
-    const int kb = 16 * q, rl = DP - kb + 4, off = ltb_off(DP, kb);
-    for (int r = threadIdx.x; r < 16 * rl; r += GMM_THREADS) {
-      const int e = off + r;
-#else
-  for (int e = threadIdx.x; e < LTS; e += GMM_THREADS) {
-    {
-    // invert e -> (a, b): block, row in block, column
-    int q = 0;
-    while (q + 1 < DP / 16 && ltb_off(DP, 16 * (q + 1)) <= e) q++;
-    const int kb = 16 * q, rl = DP - kb + 4;
-    const int r = e - ltb_off(DP, kb);
-#endif
-    const int a = kb + r / rl, b = kb + r % rl;
-    double v = 0.0;
-    if (a < d && b < d) {
-      if (b == a) {
-        v = exp(ic[a]);                                  // qd[k, j] += exp(icf[k, j])
-      } else if (b > a) {
-        // icf column-major strict lower triangle: (row b, col a), a < b
-        const int li = d + a * d - a * (a + 1) / 2 + (b - a - 1);
-        v = ic[li];
-      }
-    }
-    lt[e] = v;
-    }
-  }
+  build_lt<DP, GMM_THREADS>(ic, d, lt);
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int j = 0; j < d; j++) s = s + ic[j];           // sq[k] += icf[k, j] (in order)
@@ -2103,8 +2100,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
           return rc;
         if (!(GMM_ABLATE & 16) &&
             (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPFW, GMM_FWD_MPW>, dim3(K, L.Sf),
-                             dim3(WF::NCW * 32), sfw, st, d, K, N, alphas, means, LT, sq, tol, chk,
-                             mt, flags, xmwf)))
+                             dim3(WF::NCW * 32), sfw, st, d, K, N, alphas, means, LT, sq, tol,
+                             chk, mt, flags, xmwf)))
           return rc;
       }
     }
