@@ -93,6 +93,10 @@ namespace rl {
 #ifndef GMM_FWD_MPW
 #define GMM_FWD_MPW 1         // warp-specialised forward: m-tiles (16 points) per warp
 #endif
+#ifndef GMM_WS_128
+#define GMM_WS_128 0          // 1: the warp-specialised kernels for DP = 128 too (16-point tiles,
+                              // one CTA per SM: measured 34% slower than the round-1 kernels)
+#endif
 #ifndef GMM_WS_FWD_MINB
 #define GMM_WS_FWD_MINB 3
 #endif
@@ -1335,7 +1339,7 @@ __device__ __forceinline__ void ws_zm(const double *__restrict__ lt, const doubl
 // forward: warp roles (row block i, m-tiles mm*MPW..), x produced by warp 0
 // lane 0 (tile t + 1 once every warp released tile t - 1's slot)
 template <int DP, int TP, int MPW>
-__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_FWD_MINB) k_gmm_fwd_ws(
+__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_WS_FWD_MINB) k_gmm_fwd_ws(
     int d, int K, long long N, const double *__restrict__ alphas, const double *__restrict__ means,
     const double *__restrict__ LT, const double *__restrict__ sq, double tol, int chk,
     double *__restrict__ mtT, unsigned *__restrict__ flagsA, const __grid_constant__ CUtensorMap xmap) {
@@ -1580,7 +1584,7 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
 }
 
 template <int DP, int TP>
-__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_REV_MINB) k_gmm_rev_ws(
+__global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_WS_REV_MINB) k_gmm_rev_ws(
     int d, int K, long long N, const double *__restrict__ means, const double *__restrict__ LT,
     const double *__restrict__ gmtT, double *__restrict__ part /* [K][S][DP*DP + DP + 1] */,
     const __grid_constant__ CUtensorMap xmap) {
@@ -1593,7 +1597,9 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_REV_MINB) k_gm
   double *mu = xs0 + 2 * TP * W::XS;             // [DP]
   double *scr = mu + DP;                         // [NCW][2][16][SS]: G^T per warp
   double *red = scr + W::NCW * 2 * 16 * W::SS;   // [NCW]
-  static_assert(DP * DP + W::MT * DP <= 2 * TP * W::XS, "block partial fits the x ring");
+  // the block partial is summed over the m-tiles in the x ring (idle by then);
+  // with one m-tile (DP = 128) the warps write it straight to global memory
+  static_assert(W::MT == 1 || DP * DP + W::MT * DP <= 2 * TP * W::XS, "partial fits the ring");
   __shared__ uint64_t full[2], empty[2];
   const int k = blockIdx.x, tid = threadIdx.x, w = tid >> 5;
   const long long ntiles = (N + TP - 1) / TP;
@@ -1617,23 +1623,36 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, GMM_WS_REV_MINB) k_gm
   __syncthreads();
   pdl_wait();
   const double *gm = gmtT + (long long)k * N;
-  double *mbuf = xs0, *cs = xs0 + DP * DP;
-  switch (i) {
-    case 0: rev_ws_role<DP, TP, 0>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); break;
-    case 1: rev_ws_role<DP, TP, 1>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); break;
-    case 2:
-      if constexpr (W::NI > 2)
-        rev_ws_role<DP, TP, 2>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red);
-      break;
-    default:
-      if constexpr (W::NI > 3)
-        rev_ws_role<DP, TP, 3>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red);
-      break;
-  }
-  __syncthreads();
   const int S = gridDim.y;
   const long long PW = (long long)DP * DP + DP + 1;
   double *out = part + ((long long)k * S + blockIdx.y) * PW;
+  double *mbuf = W::MT == 1 ? out : xs0;
+  double *cs = mbuf + DP * DP;
+#define REV_WS_ROLE(II)                                                                     \
+  case II:                                                                                  \
+    if constexpr (W::NI > II)                                                               \
+      rev_ws_role<DP, TP, II>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); \
+    break;
+  switch (i) {
+    REV_WS_ROLE(0)
+    REV_WS_ROLE(1)
+    REV_WS_ROLE(2)
+    REV_WS_ROLE(3)
+    REV_WS_ROLE(4)
+    REV_WS_ROLE(5)
+    REV_WS_ROLE(6)
+    REV_WS_ROLE(7)
+  }
+#undef REV_WS_ROLE
+  __syncthreads();
+  if constexpr (W::MT == 1) {                    // M and the column sums are in place
+    if (tid == 0) {
+      double s = 0.0;
+      for (int ww = 0; ww < W::NCW; ww++) s += red[ww];
+      out[(long long)DP * DP + DP] = s;
+    }
+    return;
+  }
   for (int e = tid; e < DP * DP; e += NT) {
     const int r = e / DP, c = e % DP;
     if ((c >> 4) <= (r >> 4)) out[e] = mbuf[e];          // the lower-triangle tiles
@@ -1872,10 +1891,13 @@ static int tpf_of(int DP) { return tpf_c(DP); }
 static constexpr int tpr_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? GMM_TPR64 : 32); }
 static int tpr_of(int DP) { return tpr_c(DP); }
 // the warp-specialised kernels' tile (DP <= 64): 4 (block pair, m-tile) combos
-static constexpr int tpw_c(int DP) { return DP == 32 ? 64 : 32; }
-// the warp-specialised forward: GMM_FWD_MPW m-tiles per warp
-static constexpr int tpfw_c(int DP) { return tpw_c(DP) * GMM_FWD_MPW; }
-static bool use_ws(int d) { return GMM_WS && d <= 64 && !(d & 1); }
+static constexpr int tpw_c(int DP) { return DP == 32 ? 64 : (DP == 64 ? 32 : 16); }
+// the warp-specialised forward: GMM_FWD_MPW m-tiles per warp (one for DP = 128)
+static constexpr int mpw_c(int DP) { return DP == 128 ? 1 : GMM_FWD_MPW; }
+static constexpr int tpfw_c(int DP) { return tpw_c(DP) * mpw_c(DP); }
+static bool use_ws(int d) { return GMM_WS && d <= (GMM_WS_128 ? 128 : 64) && !(d & 1); }
+static int ws_fwd_per_sm(int DP) { return DP == 128 ? 1 : GMM_WS_FWD_MINB; }
+static int ws_rev_per_sm(int DP) { return DP == 128 ? 1 : GMM_WS_REV_MINB; }
 // concurrent CTAs per SM the split assumes: forward 2 (DP <= 64), reverse
 // GMM_REV_MINB (DP <= 64); DP = 128 runs one CTA per SM
 static int fwd_per_sm(int DP) { return DP == 128 ? 1 : GMM_FWD_MINB; }
@@ -1931,13 +1953,13 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   const int tf = ws ? tpfw_c(DP) : tpf_of(DP), tr = ws ? tpw_c(DP) : tpr_of(DP);
   const long long ntf = (N + tf - 1) / tf;
   const long long ntr = (N + tr - 1) / tr;
-  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * (ws ? GMM_WS_FWD_MINB : fwd_per_sm(DP)), 64);
+  L.Sf = choose_split(K, ntf > 0 ? ntf : 1, 148 * (ws ? ws_fwd_per_sm(DP) : fwd_per_sm(DP)), 64);
   if (GMM_FWD_ONE_WAVE)
     L.Sf = (int)std::max<long long>(1, std::min<long long>(ntf, 148 * fwd_per_sm(DP) / K));
   // each reverse CTA writes a (DP^2 + DP + 1)-double partial: cap them at 256 MB
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
-  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * (ws ? GMM_WS_REV_MINB : rev_per_sm(DP)), smax);
+  L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * (ws ? ws_rev_per_sm(DP) : rev_per_sm(DP)), smax);
   L.nerr = (int)((N + LSE_THREADS - 1) / LSE_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -2083,8 +2105,8 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
     // the warp-specialised kernels (DP <= 64, x addressable by TMA)
     CUtensorMap xmw, xmwf;
     bool wsk = false;
-    if constexpr (DP <= 64) {
-      constexpr int TPW = tpw_c(DP), TPFW = tpfw_c(DP);
+    if constexpr (DP <= 128) {
+      constexpr int TPW = tpw_c(DP), TPFW = tpfw_c(DP), MPW = mpw_c(DP);
       using W = WsCfg<DP, TPW>;
       using WF = WsCfg<DP, TPFW>;
       wsk = use_ws(d) && !GMM_REV_FINAL && make_x_map<DP, TPW>(&xmw, x, d, N) &&
@@ -2094,12 +2116,12 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
       constexpr size_t srw =
           ((size_t)ltb_size(DP) + 2 * TPW * W::XS + DP + W::NCW * 2 * 16 * W::SS + W::NCW) * 8;
       if (wsk) {
-        if ((rc = smem_attr((const void *)k_gmm_fwd_ws<DP, TPFW, GMM_FWD_MPW>, sfw,
+        if ((rc = smem_attr((const void *)k_gmm_fwd_ws<DP, TPFW, MPW>, sfw,
                             "smem attr fwd_ws")) ||
             (rc = smem_attr((const void *)k_gmm_rev_ws<DP, TPW>, srw, "smem attr rev_ws")))
           return rc;
         if (!(GMM_ABLATE & 16) &&
-            (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPFW, GMM_FWD_MPW>, dim3(K, L.Sf),
+            (rc = launch_pdl("k_gmm_fwd_ws", k_gmm_fwd_ws<DP, TPFW, MPW>, dim3(K, L.Sf),
                              dim3(WF::NCW * 32), sfw, st, d, K, N, alphas, means, LT, sq, tol,
                              chk, mt, flags, xmwf)))
           return rc;
@@ -2134,7 +2156,7 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
           (rc = cuda_status(cudaEventRecord(side->join, side->s), "join record")))
         return rc;
     }
-    if constexpr (DP <= 64) {
+    if constexpr (DP <= 128) {
       constexpr int TPW = tpw_c(DP);
       using W = WsCfg<DP, TPW>;
       constexpr size_t srw =
