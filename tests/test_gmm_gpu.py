@@ -88,6 +88,30 @@ def test_random_shapes_vs_oracle(cuda, oracle, d, K, N):
     check_vs((e, ga, gm, gi), got)
 
 
+@pytest.mark.parametrize("d", [16, 64])
+def test_unaligned_x_takes_the_cp_async_kernels(cuda, oracle, d):
+    """x whose base is 8- but not 16-byte aligned cannot be addressed by the
+    TMA tensor map: the drop-in falls back to the cp.async tile kernels
+    (gmm.cu make_x_map), with the same results to rounding."""
+    K, N = 4, 333
+    rng = np.random.default_rng(77 + d)
+    alphas, means, icf, x = inputs(rng, d, K, N)
+    cst = gmm_constants(d, K, N, 1.0, 0)
+    rc, e, ga, gm, gi = oracle.gmm_grad(alphas, means, icf, x, 1.0, 0, cst)
+    assert rc == 0
+    buf = torch.empty(N * d + 1, dtype=torch.float64, device=cuda)
+    xu = buf[1:].view(N, d)
+    xu.copy_(torch.as_tensor(x))
+    assert xu.data_ptr() % 16 == 8
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=cuda)  # noqa: E731
+    r = rg.gmm_grad(t(alphas), t(means), t(icf), xu, 1.0, 0, cst)
+    torch.cuda.synchronize()
+    got = (float(r.err.item()), r.g_alphas.cpu().numpy(), r.g_means.cpu().numpy(),
+           r.g_icf.cpu().numpy(), r.fail.cpu().numpy(), r)
+    assert not got[4].any()
+    check_vs((e, ga, gm, gi), got)
+
+
 def run_full(dev, alphas, means, icf, x, gamma, m, cst, **kw):
     """The drop-in single-device gradient (rl_gmm_gradient_f64)."""
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
