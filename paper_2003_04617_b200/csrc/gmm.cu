@@ -87,6 +87,11 @@ namespace rl {
 #ifndef GMM_WS
 #define GMM_WS 1              // DP <= 64, d even: the warp-specialised tile kernels
 #endif
+#ifndef GMM_WS_CENTER_ONCE
+#define GMM_WS_CENTER_ONCE 1  // ws reverse: each tile centred once in shared memory (shared by
+                              // the eight warps, one tile ahead) instead of x - mu in every
+                              // warp's fragments (5x the FP64 adds, on the pipe DMMA uses)
+#endif
 #ifndef GMM_DIAG_M8
 #define GMM_DIAG_M8 1         // reverse: diagonal factor-adjoint tiles by m8n8k4 (half the flops)
 #endif
@@ -1260,7 +1265,7 @@ __device__ __forceinline__ void ws_producer(const CUtensorMap *xmap, long long n
 
 // Z[p][16i + 8h + c] for the warp's 16 points (h = 0, 1: n-tiles 2i, 2i+1),
 // xc = x - mu formed in the fragments
-template <int DP, int TP>
+template <int DP, int TP, bool SUBMU = true>
 __device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double *__restrict__ xs,
                                      const double *__restrict__ mu, int i, int m,
                                      double (&acc)[2][4]) {
@@ -1284,7 +1289,9 @@ __device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double
 #pragma unroll
     for (int v1 = 0; v1 < 4; v1++)
 #pragma unroll
-      for (int v0 = 0; v0 < 2; v0++) af[v0 + 2 * v1] = xl[8 * v0 * W::XS + kb + 4 * v1] - mv[v1];
+      for (int v0 = 0; v0 < 2; v0++)
+        af[v0 + 2 * v1] = SUBMU ? xl[8 * v0 * W::XS + kb + 4 * v1] - mv[v1]
+                                : xl[8 * v0 * W::XS + kb + 4 * v1];
     // n-tile 2i needs rows a <= 16i + 7 only: its last k-step is a k8 MMA
     if (last) dmma16808(acc[0], af, b0);
     else dmma16816(acc[0], af, b0);
@@ -1293,6 +1300,27 @@ __device__ __forceinline__ void ws_z(const double *__restrict__ lt, const double
 #pragma unroll 1
   for (int ks = 0; ks < i; ks++) step(ks, false);
   step(i, true);
+}
+
+// warp w's share (rows w TP/8 ..) of the tile centred in place, xc = x - mu
+// (16-byte accesses)
+template <int DP, int TP>
+__device__ __forceinline__ void ws_center_part(double *__restrict__ xs,
+                                               const double *__restrict__ mu) {
+  using W = WsCfg<DP, TP>;
+  constexpr int CP = DP / 2, RPW = TP / W::NCW, PER = RPW * CP / 32;
+  static_assert((RPW * CP) % 32 == 0, "centring share");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const int e = lane + 32 * q, r = w * RPW + e / CP, c = 2 * (e % CP);
+    double2 *p = reinterpret_cast<double2 *>(xs + r * W::XS + c);
+    const double2 mq = *reinterpret_cast<const double2 *>(mu + c);
+    double2 v = *p;
+    v.x = v.x - mq.x;
+    v.y = v.y - mq.y;
+    *p = v;
+  }
 }
 
 // Z for MPW consecutive m-tiles m0.. of the warp (the L^T fragments loaded
@@ -1446,7 +1474,7 @@ template <int DP, int TP, int I>
 __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__restrict__ lt,
                                             double *xs0, const double *__restrict__ mu,
                                             double *scr, const double *__restrict__ gm,
-                                            uint64_t *full, uint64_t *empty,
+                                            uint64_t *full, uint64_t *empty, uint64_t *cent,
                                             const CUtensorMap *xmap, double *mbuf, double *cs,
                                             double *red) {
   using W = WsCfg<DP, TP>;
@@ -1475,10 +1503,15 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
     }
     const long long p0 = tile * TP + 16 * m + t1;
     const double g0 = p0 < N ? gm[p0] : 0.0, g1 = p0 + 8 < N ? gm[p0 + 8] : 0.0;
-    mbar_wait(&full[b], (t >> 1) & 1);
     const double *xs = xs0 + b * TP * W::XS;
     double acc[2][4];
-    ws_z<DP, TP>(lt, xs, mu, I, m, acc);                   // recompute qxc
+    if (GMM_WS_CENTER_ONCE) {
+      mbar_wait(&cent[b], (t >> 1) & 1);                   // tile t landed and centred
+      ws_z<DP, TP, false>(lt, xs, mu, I, m, acc);          // recompute qxc
+    } else {
+      mbar_wait(&full[b], (t >> 1) & 1);
+      ws_z<DP, TP>(lt, xs, mu, I, m, acc);
+    }
     if (I == 0 && t0 == 0) {
       sgm += g0;                                           // alphas.g, sq.g += mt.g
       sgm += g1;
@@ -1502,7 +1535,7 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
     // in its lower 8 rows only: four m8n8k4 MMAs (k = the 16 points) into
     // the tile's row-half v1 = 1
     auto diag = [&](double (&Mj)[4], const double *g, int col0) {
-      const double muj = mu[col0 + t1];
+      const double muj = GMM_WS_CENTER_ONCE ? 0.0 : mu[col0 + t1];
       double c2[2] = {Mj[2], Mj[3]};
 #pragma unroll
       for (int kq = 0; kq < 4; kq++)
@@ -1521,10 +1554,11 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
         diag(M[j], sc, 8 * j);
         continue;
       }
-      const double muj = mu[8 * j + t1];
       double bf[4];
 #pragma unroll
-      for (int v = 0; v < 4; v++) bf[v] = xb[4 * v * W::XS + 8 * j] - muj;
+      for (int v = 0; v < 4; v++)
+        bf[v] = GMM_WS_CENTER_ONCE ? xb[4 * v * W::XS + 8 * j]
+                                   : xb[4 * v * W::XS + 8 * j] - mu[8 * j + t1];
       dmma16816(M[j], af, bf);
     }
     if constexpr (NB > 0) {
@@ -1539,15 +1573,22 @@ __device__ __forceinline__ void rev_ws_role(int m, long long N, const double *__
           diag(M[NO + j], sl, 8 * (4 + j));
           continue;
         }
-        const double muj = mu[8 * (4 + j) + t1];
         double bf[4];
 #pragma unroll
-        for (int v = 0; v < 4; v++) bf[v] = xb[4 * v * W::XS + 8 * (4 + j)] - muj;
+        for (int v = 0; v < 4; v++)
+          bf[v] = GMM_WS_CENTER_ONCE ? xb[4 * v * W::XS + 8 * (4 + j)]
+                                     : xb[4 * v * W::XS + 8 * (4 + j)] - mu[8 * (4 + j) + t1];
         dmma16816(M[NO + j], af, bf);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);                // slot reads done
+    if (GMM_WS_CENTER_ONCE && tile + gridDim.y < ntiles) {  // centre my share of tile t + 1
+      mbar_wait(&full[b ^ 1], ((t + 1) >> 1) & 1);
+      ws_center_part<DP, TP>(xs0 + (b ^ 1) * TP * W::XS, mu);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cent[b ^ 1]);
+    }
   }
   // block partial: the m-tiles' M added in order through shared memory (the
   // x ring, idle now), then column sums and sum of mt.g
@@ -1600,7 +1641,7 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
   // the block partial is summed over the m-tiles in the x ring (idle by then);
   // with one m-tile (DP = 128) the warps write it straight to global memory
   static_assert(W::MT == 1 || DP * DP + W::MT * DP <= 2 * TP * W::XS, "partial fits the ring");
-  __shared__ uint64_t full[2], empty[2];
+  __shared__ uint64_t full[2], empty[2], cent[2];
   const int k = blockIdx.x, tid = threadIdx.x, w = tid >> 5;
   const long long ntiles = (N + TP - 1) / TP;
   if (tid == 0) {
@@ -1608,6 +1649,8 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
     mbar_init(&full[1]);
     mbar_init_n(&empty[0], W::NCW);
     mbar_init_n(&empty[1], W::NCW);
+    mbar_init_n(&cent[0], W::NCW);
+    mbar_init_n(&cent[1], W::NCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // x only: the first tile runs ahead of k_gmm_lse
     if (blockIdx.y < ntiles) load_x_tma<DP, TP>(xs0, &xmap, (long long)blockIdx.y * TP, &full[0]);
@@ -1621,6 +1664,12 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
   ws_role<DP, TP>(w, i, m);
   cp_wait<0>();
   __syncthreads();
+  if (GMM_WS_CENTER_ONCE && blockIdx.y < ntiles) {      // tile 0: every warp centres its share
+    mbar_wait(&full[0], 0);
+    ws_center_part<DP, TP>(xs0, mu);
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&cent[0]);
+  }
   pdl_wait();
   const double *gm = gmtT + (long long)k * N;
   const int S = gridDim.y;
@@ -1631,7 +1680,8 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
 #define REV_WS_ROLE(II)                                                                     \
   case II:                                                                                  \
     if constexpr (W::NI > II)                                                               \
-      rev_ws_role<DP, TP, II>(m, N, lt_s, xs0, mu, scr, gm, full, empty, &xmap, mbuf, cs, red); \
+      rev_ws_role<DP, TP, II>(m, N, lt_s, xs0, mu, scr, gm, full, empty, cent, &xmap, mbuf, cs, \
+                              red);                                                       \
     break;
   switch (i) {
     REV_WS_ROLE(0)
