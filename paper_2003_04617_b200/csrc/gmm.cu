@@ -87,6 +87,10 @@ namespace rl {
 #ifndef GMM_WS
 #define GMM_WS 1              // DP <= 64, d even: the warp-specialised tile kernels
 #endif
+#ifndef GMM_FWD_CENTER_ONCE
+#define GMM_FWD_CENTER_ONCE 0  // the same for k_gmm_fwd_ws: measured slower (55.1 -> 57.6 us;
+                               // its warps have little MMA work to cover the centring wait)
+#endif
 #ifndef GMM_WS_CENTER_ONCE
 #define GMM_WS_CENTER_ONCE 1  // ws reverse: each tile centred once in shared memory (shared by
                               // the eight warps, one tile ahead) instead of x - mu in every
@@ -1325,7 +1329,7 @@ __device__ __forceinline__ void ws_center_part(double *__restrict__ xs,
 
 // Z for MPW consecutive m-tiles m0.. of the warp (the L^T fragments loaded
 // once per k-step for all of them)
-template <int DP, int TP, int MPW>
+template <int DP, int TP, int MPW, bool SUBMU = true>
 __device__ __forceinline__ void ws_zm(const double *__restrict__ lt, const double *__restrict__ xs,
                                       const double *__restrict__ mu, int i, int m0,
                                       double (&acc)[MPW][2][4]) {
@@ -1356,7 +1360,8 @@ __device__ __forceinline__ void ws_zm(const double *__restrict__ lt, const doubl
       for (int v1 = 0; v1 < 4; v1++)
 #pragma unroll
         for (int v0 = 0; v0 < 2; v0++)
-          af[v0 + 2 * v1] = xl[(16 * q + 8 * v0) * W::XS + kb + 4 * v1] - mv[v1];
+          af[v0 + 2 * v1] = SUBMU ? xl[(16 * q + 8 * v0) * W::XS + kb + 4 * v1] - mv[v1]
+                                  : xl[(16 * q + 8 * v0) * W::XS + kb + 4 * v1];
       if (ks < i) dmma16816(acc[q][0], af, b0);   // n-tile 2i: last k-step k8
       else dmma16808(acc[q][0], af, b0);
       dmma16816(acc[q][1], af, b1);
@@ -1379,7 +1384,7 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
   double *xs0 = lt_s + ltb_size(DP);             // [2][TP][XS]
   double *mu = xs0 + 2 * TP * W::XS;             // [DP], zero padded
   double *sqp = mu + DP;                         // [2][NI][TP]: per-block sqn partials
-  __shared__ uint64_t full[2], empty[2];
+  __shared__ uint64_t full[2], empty[2], cent[2];
   const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t0 = lane & 3, t1 = lane >> 2;
   const long long ntiles = (N + TP - 1) / TP;
@@ -1388,6 +1393,8 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
     mbar_init(&full[1]);
     mbar_init_n(&empty[0], W::NCW);
     mbar_init_n(&empty[1], W::NCW);
+    mbar_init_n(&cent[0], W::NCW);
+    mbar_init_n(&cent[1], W::NCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // x only: the first tile runs ahead of k_gmm_prep
     if (blockIdx.y < ntiles) load_x_tma<DP, TP>(xs0, &xmap, (long long)blockIdx.y * TP, &full[0]);
@@ -1402,6 +1409,12 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
   const bool producer = w == 0 && lane == 0;
   cp_wait<0>();
   __syncthreads();                               // L^T, means, barriers
+  if (GMM_FWD_CENTER_ONCE && blockIdx.y < ntiles) {      // tile 0: every warp centres its share
+    mbar_wait(&full[0], 0);
+    ws_center_part<DP, TP>(xs0, mu);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&cent[0]);
+  }
   int t = 0;
   for (long long tile = blockIdx.y; tile < ntiles; tile += gridDim.y, t++) {
     const int b = t & 1;
@@ -1409,9 +1422,14 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
       if (t >= 1) mbar_wait(&empty[b ^ 1], ((t - 1) >> 1) & 1);
       load_x_tma<DP, TP>(xs0 + (b ^ 1) * TP * W::XS, &xmap, (tile + gridDim.y) * TP, &full[b ^ 1]);
     }
-    mbar_wait(&full[b], (t >> 1) & 1);
     double acc[MPW][2][4];
-    ws_zm<DP, TP, MPW>(lt_s, xs0 + b * TP * W::XS, mu, i, mm * MPW, acc);
+    if (GMM_FWD_CENTER_ONCE) {
+      mbar_wait(&cent[b], (t >> 1) & 1);         // tile t landed and centred
+      ws_zm<DP, TP, MPW, false>(lt_s, xs0 + b * TP * W::XS, mu, i, mm * MPW, acc);
+    } else {
+      mbar_wait(&full[b], (t >> 1) & 1);
+      ws_zm<DP, TP, MPW>(lt_s, xs0 + b * TP * W::XS, mu, i, mm * MPW, acc);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);       // this warp's reads of the slot are done
     // sqn partial over the block's 16 features, per point (sqn += abs2(qxc[j]))
@@ -1448,6 +1466,12 @@ __global__ void __launch_bounds__(WsCfg<DP, TP>::NCW * 32, DP == 128 ? 1 : GMM_W
         if (chk && fabs(res) > tol) atomicOr(&flagsA[ii], 1u);
         mtT[(long long)k * N + ii] = base_mt - sqn * 0.5;  // mt -= sqn * 0.5
       }
+    }
+    if (GMM_FWD_CENTER_ONCE && tile + gridDim.y < ntiles) {  // centre my share of tile t + 1
+      mbar_wait(&full[b ^ 1], ((t + 1) >> 1) & 1);
+      ws_center_part<DP, TP>(xs0 + (b ^ 1) * TP * W::XS, mu);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cent[b ^ 1]);
     }
   }
 }
