@@ -2034,6 +2034,16 @@ static GmmLayout gmm_layout(int d, int K, long long N) {
   const long long pw = (long long)DP * DP + DP + 1;
   int smax = (int)std::max<long long>(1, std::min<long long>(64, (256LL << 20) / (8 * pw * K)));
   L.Sr = choose_split(K, ntr > 0 ? ntr : 1, 148 * (ws ? ws_rev_per_sm(DP) : rev_per_sm(DP)), smax);
+  if (ws) {
+    // one wave when it fills >= 85% of the slots, two left free for the
+    // drop-in's k_gmm_restore (one CTA beside the reverse grid): configs[2]
+    // 0.1761 -> 0.1648 ms against the 97%-full two-wave split (measured)
+    const int slots = 148 * ws_rev_per_sm(DP), one = (slots - 2) / K;
+    if (one >= 1 && one <= ntr && one <= smax && (double)K * one >= 0.85 * slots) L.Sr = one;
+  }
+#ifdef GMM_SR_FORCE                // timing-only builds: a fixed reverse point split
+  L.Sr = (int)std::max<long long>(1, std::min<long long>(GMM_SR_FORCE, ntr > 0 ? ntr : 1));
+#endif
   L.nerr = (int)((N + LSE_THREADS - 1) / LSE_THREADS);
   size_t off = 0;
   auto take = [&](size_t bytes) {
