@@ -91,6 +91,12 @@ namespace rl {
 #define GMM_FWD_CENTER_ONCE 0  // the same for k_gmm_fwd_ws: measured slower (55.1 -> 57.6 us;
                                // its warps have little MMA work to cover the centring wait)
 #endif
+#ifndef GMM_HALF_K8
+#define GMM_HALF_K8 0         // round-1 tile kernels: k8 MMAs for the half-needed k-steps
+#endif                        // (d = 128 shape measured 41.7 -> 45.1 ms: off)
+#ifndef GMM_HALF_DIAG
+#define GMM_HALF_DIAG 0       // round-1 reverse: m8n8k4 for the half-needed diagonal tiles
+#endif                        // (41.7 -> 42.2 ms: off)
 #ifndef GMM_WS_CENTER_ONCE
 #define GMM_WS_CENTER_ONCE 1  // ws reverse: each tile centred once in shared memory (shared by
                               // the eight warps, one tile ahead) instead of x - mu in every
@@ -483,11 +489,20 @@ __device__ __forceinline__ void tile_z_tc(const double *__restrict__ lt, const d
 #pragma unroll
           for (int v0 = 0; v0 < 2; v0++) af[m][v0 + 2 * v1] = af[m][v0 + 2 * v1] - mv[v1];
     }
+    // an even n-tile j needs rows a <= 8j + 7 only: its last k-step is k8
+    const bool h2 = GMM_HALF_K8 && ks == ks_end && !(j2 & 1);
+    const bool h1 = GMM_HALF_K8 && ks == ks1 && !(j1 & 1);
 #pragma unroll
-    for (int m = 0; m < C::MTW; m++) dmma16816(acc[m][1], af[m], b2);
+    for (int m = 0; m < C::MTW; m++) {
+      if (h2) dmma16808(acc[m][1], af[m], b2);
+      else dmma16816(acc[m][1], af[m], b2);
+    }
     if (ks <= ks1) {
 #pragma unroll
-      for (int m = 0; m < C::MTW; m++) dmma16816(acc[m][0], af[m], b1);
+      for (int m = 0; m < C::MTW; m++) {
+        if (h1) dmma16808(acc[m][0], af[m], b1);
+        else dmma16816(acc[m][0], af[m], b1);
+      }
     }
   }
 }
@@ -1138,6 +1153,17 @@ __global__ void __launch_bounds__(GMM_THREADS, DP == 128 ? 1 : GMM_REV_MINB) k_g
 #pragma unroll
             for (int v0 = 0; v0 < 2; v0++)
               af[v0 + 2 * v1] = gt[(rb + t1 + 8 * v0) * C::GS + pb + t0 + 4 * v1];
+        }
+        if (GMM_HALF_DIAG && !GMM_REV_REG_CENTER && tj[q] == 2 * ti[q] + 1) {
+          // the diagonal tile is used in its lower 8 rows only: four m8n8k4
+          double c2[2] = {M[q][2], M[q][3]};
+#pragma unroll
+          for (int kq = 0; kq < 4; kq++)
+            dmma884(c2, gt[(rb + 8 + t1) * C::GS + pb + 4 * kq + t0],
+                    xs[(pb + 4 * kq + t0) * C::XS + cb + t1]);
+          M[q][2] = c2[0];
+          M[q][3] = c2[1];
+          continue;
         }
         double bf[4];
 #pragma unroll
