@@ -780,17 +780,22 @@ __global__ void __launch_bounds__(LSE_THREADS * LSE_LANES) k_gmm_lse_q(
   pdl_trigger();                 // k_gmm_rev's prologue (L^T, x prefetch) overlaps this kernel
   pdl_wait();
 
-  extern __shared__ double lse_ex[];                     // [LSE_THREADS][K]
+  extern __shared__ double lse_ex[];                     // [LSE_THREADS][K] x 2
   const int q = threadIdx.x & (LSE_LANES - 1), pl = threadIdx.x / LSE_LANES;
   const unsigned qmask = 0xFu << (threadIdx.x & 28);
   const long long i = (long long)blockIdx.x * LSE_THREADS + pl;
   double *ex = lse_ex + pl * K;
+  double *mv = lse_ex + (LSE_THREADS + pl) * K;          // the point's mt row, staged once
   double e_pt = 0.0;
   unsigned long long nfail = 0, nupd = 0;
   if (i < N) {                                           // uniform over the quad
     const double *mt = mtT + i;
     double *gmt = gmtT + i;
-#define MT(k) mt[(long long)(k) * N]
+    // the K loads are independent: the quad issues them together (one L2
+    // round trip instead of K dependent ones in the argmax scan)
+    for (int k = q; k < K; k += LSE_LANES) mv[k] = mt[(long long)k * N];
+    __syncwarp(qmask);
+#define MT(k) mv[k]
 #define GM(k) gmt[(long long)(k) * N]
     int imx = 0;                                         // the argmax record (see k_gmm_lse)
     double vmx = MT(0);
@@ -2245,9 +2250,12 @@ static int run_gmm(int d, int K, long long N, long long N_total, const double *a
 #define GMM_LSE_Q 1
 #endif
     if (GMM_LSE_Q && K <= LSE_QK) {
+      if ((rc = smem_attr((const void *)k_gmm_lse_q, (size_t)2 * LSE_THREADS * K * 8,
+                          "smem attr lse_q")))
+        return rc;
       if (!(GMM_ABLATE & 2) &&
           (rc = launch_pdl("k_gmm_lse_q", k_gmm_lse_q, dim3(L.nerr),
-                           dim3(LSE_THREADS * LSE_LANES), (size_t)LSE_THREADS * K * 8, st, K, N,
+                           dim3(LSE_THREADS * LSE_LANES), (size_t)2 * LSE_THREADS * K * 8, st, K, N,
                            mt, gmt, flags, tol, chk, errp, terms, fail, counters)))
         return rc;
     } else if (!(GMM_ABLATE & 2) &&

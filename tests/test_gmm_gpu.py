@@ -74,7 +74,7 @@ def test_golden_vectors(cuda, golden):
         check_vs((float(G[p + "err"]), G[p + "g_alphas"], G[p + "g_means"], G[p + "g_icf"]), got)
 
 
-@pytest.mark.parametrize("d,K,N", [(7, 3, 50), (32, 4, 300), (33, 5, 129), (64, 6, 257),
+@pytest.mark.parametrize("d,K,N", [(7, 3, 50), (32, 4, 300), (33, 5, 129), (64, 6, 257), (8, 96, 200),
                                    (100, 3, 70), (128, 2, 65)])
 def test_random_shapes_vs_oracle(cuda, oracle, d, K, N):
     rng = np.random.default_rng(d * 1000 + K * 10 + N)
