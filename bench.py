@@ -687,6 +687,18 @@ def run_ba_ours(args, D):
            "bytes_per_launch": D.sum(c_bytes),
            "achieved_gbs": round(D.sum(c_bytes) / (c_ms * 1e-3) / 1e9, 1),
            "frac": round(D.sum(c_bytes) / (c_ms * 1e-3) / 1e9 / peak, 4)}
+    # SURVEY §8(d)'s gather-stress variant: the same observations with the
+    # point indices shuffled (camera rows still i mod n), so consecutive
+    # observations gather scattered points
+    obs_sh = obs[lo:hi].copy()
+    obs_sh[:, 1] = np.random.default_rng(33).permutation(obs_sh[:, 1])
+    dsh = t(obs_sh)
+    s_ms = D.max(time_device(lambda: kernels.ba_jacobian(dc, dX, dw, df, dsh, want_err=False,
+                                                         out=out),
+                             max(3, args.steps // 4), flush))
+    shuffled = {"ms_per_step": round(s_ms, 4), "value": round(1.0 / (s_ms * 1e-3), 2),
+                "frac": round(D.sum(byts) / (s_ms * 1e-3) / 1e9 / peak, 4),
+                "obs": "point index permuted (seed 33), camera index i mod n"}
     e2e = None
     if not args.no_e2e:
         e2e = ba_e2e(cams, X, w[lo:hi], feats[lo:hi], obs[lo:hi], args, D)
@@ -699,7 +711,7 @@ def run_ba_ours(args, D):
         "obs_per_s": round(p_total / (ms_step * 1e-3), 1),
         "roofline": roof, "e2e": e2e, "gpu_launches": steps, "clocks": clocks,
         "failed_per_step": n_failed // steps, "parity_sample": parity,
-        "objective_only": objective, "csr_jacobian": csr,
+        "objective_only": objective, "csr_jacobian": csr, "shuffled_obs": shuffled,
     }
 
 
