@@ -719,12 +719,77 @@ def gen_codegen_complex_fd():
     print("complex fd goldens:", len(rows), "rows")
 
 
+def gen_codegen_fixed():
+    """fxmix.rnl (Fixed / Q31.32 cells) through the reference: run, uncall,
+    gradient with the default seed (acc!, a Fixed leaf: Fixed cotangents,
+    each accumulation quantized to 2^-32) and with a y! seed, and
+    finite_difference (the measured Fixed step).  Fixed values are stored as
+    their raw int64; errors as the exception class name."""
+    from revlang import GradRequest, gradient, run, uncall
+    from revlang.autodiff import finite_difference
+    from revlang.values import Fixed
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "fxmix.rnl")).read())
+    rng = np.random.default_rng(61)
+    cases = [(0.0, 0.0, 1.3, 5), (0.75, -2.0, 1.9, 7), (0.0, 0.0, 0.3, 5), (-1.5, 0.5, 0.5, 3),
+             (0.0, 0.0, 1.9, 45), (0.0, 0.0, 1.9, 2000), (2.0, 1.0, 1.05, 0), (0.0, 0.0, -3.0, 4)]
+    cases += [(float(rng.uniform(-2, 2)), float(rng.uniform(-2, 2)), float(rng.uniform(0.2, 2.2)),
+               int(rng.integers(0, 12))) for _ in range(24)]
+    out = {"cases": np.array([c[:3] for c in cases]), "k": np.array([c[3] for c in cases])}
+
+    def rawv(v):
+        return v.raw if isinstance(v, Fixed) else v
+
+    for tag, fn in (("run", run), ("uncall", uncall)):
+        R, E = [], []
+        for a0, y0, b, k in cases:
+            try:
+                o = fn(prog, "fxmix", [Fixed.from_real(a0), y0, Fixed.from_real(b), k])
+                R.append([o[0].raw, np.float64(o[1]).view(np.int64), o[2].raw])
+                E.append("")
+            except Exception as err:  # noqa: BLE001
+                R.append([0, 0, 0])
+                E.append(type(err).__name__)
+        out[tag] = np.array(R, dtype=np.int64)
+        out[tag + "_err"] = np.array(E)
+    for tag, seeds in (("gacc", None), ("gy", [("y!", (), 1.0)])):
+        R, E = [], []
+        for a0, y0, b, k in cases:
+            try:
+                prim, g = gradient(prog, GradRequest("fxmix", [Fixed.from_real(a0), y0,
+                                                               Fixed.from_real(b), k],
+                                                     seeds=seeds))
+                R.append([prim[0].raw, np.float64(prim[1]).view(np.int64), prim[2].raw,
+                          g["acc!"].raw, np.float64(g["y!"]).view(np.int64), g["b"].raw])
+                E.append("")
+            except Exception as err:  # noqa: BLE001
+                R.append([0] * 6)
+                E.append(type(err).__name__)
+        out[tag] = np.array(R, dtype=np.int64)
+        out[tag + "_err"] = np.array(E)
+    F, E = [], []
+    for a0, y0, b, k in cases:
+        try:
+            fd = finite_difference(prog, "fxmix", [Fixed.from_real(a0), y0, Fixed.from_real(b), k],
+                                   1e-6)
+            F.append([fd["acc!"], fd["y!"], fd["b"]])
+            E.append("")
+        except Exception as err:  # noqa: BLE001
+            F.append([0.0] * 3)
+            E.append(type(err).__name__)
+    out["fd"] = np.array(F, dtype=np.float64)
+    out["fd_err"] = np.array(E)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_fixed.npz"), **out)
+    print("fixed goldens:", len(cases), "cases; errors:", sorted(set(out["run_err"]) - {""}),
+          sorted(set(out["gacc_err"]) - {""}))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
                               "codegen_random",
-                              "codegen_complex", "codegen_complex_fd", "bessel_fuel", "gmm_fuel", "ba_fuel"]
+                              "codegen_complex", "codegen_complex_fd", "codegen_fixed", "bessel_fuel",
+                              "gmm_fuel", "ba_fuel"]
     for w in which:
         globals()["gen_" + w]()

@@ -27,11 +27,11 @@ from .kernels import (BACsr, BAResult, BesselHessResult, BesselResult, GMMResult
                       besselj_grad, besselj_grad_host, besselj_hess, besselj_run, gmm_grad, gmm_gradient,
                       gmm_objective, gmm_run, seq_sum)
 from .programs import CATALOG, Program, entry_function, load_example, parse_program
-from .values import Array
+from .values import Array, Fixed
 
 __all__ = [
     "HessianResult", "finite_difference", "hessian", "gradient_batch", "CompiledFunction", "compile_function", "BesselHessResult", "besselj_hess",
-    "AliasedArguments", "AssertFailed", "Array", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
+    "AliasedArguments", "AssertFailed", "Array", "Fixed", "BACsr", "BAResult", "ba_jacobian_csr", "ba_jacobian_csr_host", "BesselResult", "CATALOG", "CheckReport",
     "DirtyAncilla", "RunResult", "ba_residuals", "besselj_run", "check_reversibility",
     "gmm_objective", "gmm_gradient", "gmm_run", "seq_sum", "run", "uncall",
     "ExecOptions", "FuelExhausted", "GMMResult", "GradRequest", "IndexOutOfBounds",

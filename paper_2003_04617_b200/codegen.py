@@ -22,15 +22,18 @@ generated code restates the reference interpreter's semantics:
   conditions                       interpreter.py:200-300 (ULog compares as
                                    exp(log_x), Int % as Python's modulo)
 
-The subset: Float / Int / Complex scalar parameters (Float rows; Int
-values uniform over the batch; Complex as re/im leaves with field views),
+The subset: Float / Int / Complex / Fixed scalar parameters (Float rows;
+Int values uniform over the batch; Complex as re/im leaves with field views;
+Fixed as raw int64 Q31.32 cells with `0.5fx` literals: + / - wrap mod 2^64,
+a Float value enters through from_real, cotangents are Fixed and quantized
+at every accumulation, values.py:28-86 / numerics.py:305-306, 419-428),
 fixed-shape Float arrays (parameters and ancilla-free array arguments),
-Float / ULog / Int ancillas, `+= -= *= /=` instructions with the INSTR_FNS
-functions, `xor=` on Int cells, calls between compiled functions,
+Float / ULog / Int / Fixed ancillas, `+= -= *= /=` instructions with the
+INSTR_FNS functions, `xor=` on Int cells, calls between compiled functions,
 `<-` / `->`, @routine / ~@routine, @invcheckoff, for / while / if.
-Records, Fixed values, recursion and bijector views are rejected at compile
-time (UnsupportedProgram), as are the static aliasing patterns the reference
-rejects at run time (AliasedArguments).
+Records, recursion, bijector views and Fixed arithmetic inside expressions
+are rejected at compile time (UnsupportedProgram), as are the static
+aliasing patterns the reference rejects at run time (AliasedArguments).
 
 The kernel is built with nvcc for sm_100a into a cache directory
 ($REVGPU_CODEGEN_CACHE, default paper_2003_04617_b200/_codegen_cache) and bound with
@@ -116,11 +119,17 @@ def _tokenize(src):
                 j += 2
                 while j < n and src[j].isdigit():
                     j += 1
-            if j < n and src[j].isalpha():
-                raise UnsupportedProgram("codegen: Fixed / imaginary literals are not supported")
-            body = src[i:j]
-            toks.append(("num", float(body) if is_float else int(body)))
-            i = j
+            k = j
+            while k < n and src[k].isalpha():
+                k += 1
+            body, suffix = src[i:j], src[j:k]
+            if suffix == "fx":                     # parser.py:133
+                toks.append(("num", FixLit(_fx_from_real(float(body)))))
+            elif suffix:
+                raise UnsupportedProgram("codegen: imaginary literals are not supported")
+            else:
+                toks.append(("num", float(body) if is_float else int(body)))
+            i = k
             continue
         two = src[i:i + 2]
         if two in _PUNCT2:
@@ -143,6 +152,32 @@ def _tokenize(src):
 @dataclass(frozen=True)
 class Lit:
     v: object
+
+
+_FX_WRAP, _FX_SIGN = 1 << 64, 1 << 63
+
+
+def _fx_wrap(raw):
+    """values._wrap64: two's-complement wrap of a Q31.32 raw value."""
+    raw &= _FX_WRAP - 1
+    return raw - _FX_WRAP if raw & _FX_SIGN else raw
+
+
+def _fx_from_real(v):
+    """values.Fixed.from_real: round(float(v) * 2^32), half-even, wrapped."""
+    return _fx_wrap(round(float(v) * (1 << 32)))
+
+
+@dataclass(frozen=True)
+class FixLit:
+    """A Fixed (Q31.32) literal (parser.py:133: `1.5fx` = Fixed.from_real(1.5))."""
+    raw: int
+
+    def __neg__(self):
+        return FixLit(_fx_wrap(-self.raw))
+
+    def real(self):
+        return self.raw / (1 << 32)          # values.Fixed.to_float (correctly rounded)
 
 
 @dataclass(frozen=True)
@@ -881,6 +916,33 @@ _PRELUDE = r"""
 #define RC_REV 5
 #define RC_FUEL 6
 #define RC_OVERFLOW 9
+#define RC_VALUE 12
+// Fixed (Q31.32, values.py:28-86): raw int64 cells, + / - wrap mod 2^64;
+// to_float = raw / 2^32 (correctly rounded); from_real = round(v * 2^32)
+// half-even, wrapped; round(inf) is Python's OverflowError, round(nan) its
+// ValueError
+__device__ __forceinline__ long long rl_fx_add(long long a, long long b) {
+  return (long long)((unsigned long long)a + (unsigned long long)b);
+}
+__device__ __forceinline__ long long rl_fx_sub(long long a, long long b) {
+  return (long long)((unsigned long long)a - (unsigned long long)b);
+}
+__device__ __forceinline__ long long rl_fx_neg(long long a) {
+  return (long long)(0ULL - (unsigned long long)a);
+}
+__device__ __forceinline__ double rl_fx_tof(long long raw) {
+  return __ll2double_rn(raw) * 0x1p-32;
+}
+__device__ __forceinline__ long long rl_fx_from(double v, int &code) {
+  const double p = v * 4294967296.0;
+  if (isnan(p)) { if (!code) code = RC_VALUE; return 0; }
+  if (isinf(p)) { if (!code) code = RC_OVERFLOW; return 0; }
+  const double r = rint(p);                              // round half to even
+  if (fabs(r) < 9223372036854775808.0) return (long long)r;
+  double m = fmod(r, 18446744073709551616.0);            // exact: r is an integer
+  if (m < 0.0) m += 18446744073709551616.0;
+  return (long long)(unsigned long long)m;
+}
 // values.s_* with the reference's error classes (values.py:343-431)
 __device__ __forceinline__ double g_div(double a, double b, int &c) {
   if (b == 0.0) { if (!c) c = RC_DOMAIN; return 0.0; }
@@ -1253,7 +1315,8 @@ class _Emitter:
 
     def infer_alloc(self, name, e):
         k = "u" if isinstance(e, Call) and e.f == "ulog" else self.expr_kind(e)
-        k = {"i": "i", "f": "f", "u": "u"}[k]
+        if k not in ("i", "f", "u", "x"):
+            raise UnsupportedProgram(f"codegen: {name!r} is allocated with a {k!r} value")
         old = self.kinds.get(name)
         if old is not None and old != k:
             raise UnsupportedProgram(f"codegen: {name!r} is re-allocated with another kind")
@@ -1263,6 +1326,8 @@ class _Emitter:
         if isinstance(e, Lit):
             if isinstance(e.v, bool):
                 return "b"
+            if isinstance(e.v, FixLit):
+                return "x"
             return "i" if isinstance(e.v, int) else "f"
         if isinstance(e, Var):
             k = self.kind(e.name)
@@ -1278,12 +1343,18 @@ class _Emitter:
                 return "i"
             if e.f in ("min", "max"):
                 ks = {self.expr_kind(a) for a in e.args}
+                if "x" in ks:
+                    raise UnsupportedProgram("codegen: min / max of Fixed values are not compiled")
                 return "i" if ks == {"i"} else "f"
             return "f"
         if isinstance(e, Bin):
             if e.op in ("&&", "||", "==", "!=", "<", "<=", ">", ">="):
                 return "b"
             lk, rk = self.expr_kind(e.l), self.expr_kind(e.r)
+            if "x" in (lk, rk):
+                raise UnsupportedProgram("codegen: Fixed arithmetic inside expressions is not "
+                                         "compiled (Fixed cells take +=, -=, convert and "
+                                         "comparisons)")
             if e.op == "%":
                 if lk != "i" or rk != "i":
                     raise UnsupportedProgram("codegen: % needs Int operands")
@@ -1319,6 +1390,8 @@ class _Emitter:
         if isinstance(e, Lit):
             if isinstance(e.v, bool):
                 return ("true" if e.v else "false"), "b"
+            if isinstance(e.v, FixLit):
+                return f"{e.v.raw}LL", "x"
             return (f"{e.v}LL" if isinstance(e.v, int) else _c_double(e.v)), self.expr_kind(e)
         if isinstance(e, Var):
             k = self.kind(e.name)
@@ -1332,6 +1405,8 @@ class _Emitter:
             return f"v_{_cid(e.name)}_{e.field}", "f"
         if isinstance(e, Un):
             s, k = self.expr(e.e)
+            if k == "x":
+                return f"rl_fx_neg({s})", "x"            # Fixed.__neg__: wrapped raw
             return f"(-{s})", k
         if isinstance(e, Call) and e.f in ("length", "size"):
             # numerics._expr_length / _expr_size: shapes are compile-time here
@@ -1376,7 +1451,9 @@ class _Emitter:
                 (a, k), = args
                 return f"(({a}) * ({a}))", k
             if f == "float":
-                (a, _), = args
+                (a, ka), = args
+                if ka == "x":
+                    return "rl_fx_tof(" + a + ")", "f"   # float(Fixed): raw / 2^32
                 return f"R((double)({a}))", "f"          # float(Dual) is its primal
             if f in ("min", "max"):
                 (a, ka), (b, kb) = args
@@ -1393,6 +1470,18 @@ class _Emitter:
             if op in ("&&", "||"):
                 return f"(({ls}) {op} ({rs}))", "b"
             if op in ("==", "!=", "<", "<=", ">", ">="):
+                if "x" in (lk, rk):
+                    # Fixed.__eq__ is False against any non-Fixed value; the
+                    # orderings coerce the other side with from_real (values.py)
+                    if lk == rk:
+                        return f"(({ls}) {op} ({rs}))", "b"
+                    if op in ("==", "!="):
+                        return ("false" if op == "==" else "true"), "b"
+                    if lk != "x":
+                        ls = f"rl_fx_from((double)R({ls}), code)"
+                    if rk != "x":
+                        rs = f"rl_fx_from((double)R({rs}), code)"
+                    return f"(({ls}) {op} ({rs}))", "b"
                 if lk == "i" and rk == "i":
                     return f"(({ls}) {op} ({rs}))", "b"
                 return f"((double)R({ls}) {op} (double)R({rs}))", "b"
@@ -1426,16 +1515,28 @@ class _Emitter:
         if isinstance(a, Lit):
             if isinstance(a.v, bool):
                 raise UnsupportedProgram("codegen: Bool arguments are not supported")
+            if isinstance(a.v, FixLit):
+                return _c_double(a.v.real())
             return _c_double(a.v)
         if r.kind == "u":
             return f"g_expm({r.v}, code, xm)"
+        if r.kind == "x":
+            return f"rl_fx_tof({r.v})"                    # to_real(Fixed)
         if r.kind == "i":
             return f"R((double){r.v})"
         return r.v
 
     @staticmethod
     def tracked(r):
-        return r is not None and r.kind in ("f", "u")
+        return r is not None and r.kind in ("f", "u", "x")
+
+    def gacc(self, r, delta, indent=""):
+        """_g_accum (numerics.py:419-428): a Fixed cotangent takes
+        Fixed.from_real(delta), anything else the plain sum."""
+        if r.kind == "x":
+            self.w(f"{indent}{r.g} = rl_fx_add({r.g}, rl_fx_from((double)({delta}), code));")
+        else:
+            self.w(f"{indent}{r.g} = {r.g} + {delta};")
 
     def apply_fn(self, fname, xs):
         if fname == "identity":
@@ -1552,6 +1653,10 @@ class _Emitter:
             val, vk = self.expr(s.e)
             if k == "i":
                 self.w(f"v_{_cid(s.name)} = {val};")
+            elif k == "x":
+                self.w(f"v_{_cid(s.name)} = {val};")
+                if grad:
+                    self.w(f"g_{_cid(s.name)} = 0;")        # zero_like(Fixed) = Fixed(0)
             else:
                 self.w(f"v_{_cid(s.name)} = {val};")
                 if grad:
@@ -1563,6 +1668,12 @@ class _Emitter:
             self.fail_check(label)
             if k == "i":
                 self.w(f"if (chk && v_{_cid(s.name)} != ({val}) && !code) code = RC_DIRTY;")
+            elif k == "x":
+                # values_close: Fixed values match only as equal raw Fixed values
+                if vk == "x":
+                    self.w(f"if (chk && v_{_cid(s.name)} != ({val}) && !code) code = RC_DIRTY;")
+                else:
+                    self.w("if (chk && !code) code = RC_DIRTY;")
             else:
                 # _ancilla_residual: |cur - decl| > tol fails (NaN passes); ULog by exponent
                 d = self.new("d")
@@ -1773,7 +1884,7 @@ class _Emitter:
                 raise KindError("+=/-= on a logarithmic number")
             if tk == "i":
                 if s.fname not in ("identity", "add", "sub", "neg") or any(
-                        isinstance(a, Lit) and isinstance(a.v, float) or
+                        isinstance(a, Lit) and isinstance(a.v, (float, FixLit)) or
                         (r is not None and r.kind != "i") for a, r in zip(args, refs)):
                     raise UnsupportedProgram("codegen: Int targets take Int +, - and identity")
                 xs = [(f"{a.v}LL" if isinstance(a, Lit) else r.v) for a, r in zip(args, refs)]
@@ -1781,28 +1892,48 @@ class _Emitter:
                       "sub": lambda: f"({xs[0]} - {xs[1]})", "neg": lambda: f"(-{xs[0]})"}[s.fname]()
                 self.w(f"{TV} = {TV} {'+' if s.op == '+=' else '-'} ({fv});")
                 return
+            fixed_lit = lambda a: isinstance(a, Lit) and isinstance(a.v, FixLit)  # noqa: E731
             if s.fname == "convert":
                 (a,), xs = args, None
                 fv = self.atom_real(a, refs[0])
             else:
                 xs = [self.atom_real(a, r) for a, r in zip(args, refs)]
-                fv = self.apply_fn(s.fname, xs)
-            fvv = self.new("fv")
-            self.w(f"{{ const R {fvv} = {fv};")
-            self.w(f"  {TV} = {TV} {'+' if s.op == '+=' else '-'} {fvv}; }}")
+                if tk == "x" and s.fname in ("identity", "add", "sub") and all(
+                        fixed_lit(a) or (r is not None and r.kind == "x")
+                        for a, r in zip(args, refs)):
+                    xr = [(f"{a.v.raw}LL" if isinstance(a, Lit) else r.v)
+                          for a, r in zip(args, refs)]
+                    fv = {"identity": lambda: xr[0], "add": lambda: f"rl_fx_add({xr[0]}, {xr[1]})",
+                          "sub": lambda: f"rl_fx_sub({xr[0]}, {xr[1]})"}[s.fname]()
+                    fv = ("RAW", fv)                   # Fixed values add raw
+                else:
+                    fv = self.apply_fn(s.fname, xs)   # a Fixed argument enters as its float
+            if tk == "x":
+                # numerics._plus_minus_plain, Fixed target: a Fixed value adds
+                # raw, any other value enters as Fixed.from_real(float(fv));
+                # both wrap mod 2^64
+                inc = fv[1] if isinstance(fv, tuple) else f"rl_fx_from((double)({fv}), code)"
+                iv = self.new("fi")
+                self.w(f"{{ const long long {iv} = {inc};")
+                self.w(f"  {TV} = {'rl_fx_add' if s.op == '+=' else 'rl_fx_sub'}({TV}, {iv}); }}")
+            else:
+                fvv = self.new("fv")
+                self.w(f"{{ const R {fvv} = {fv};")
+                self.w(f"  {TV} = {TV} {'+' if s.op == '+=' else '-'} {fvv}; }}")
             if not grad:
                 return
             sign = "1.0" if s.op == "-=" else "-1.0"
             sg = self.new("sg")
-            self.w(f"{{ const R {sg} = {sign} * {TG};")
+            gy = f"rl_fx_tof({TG})" if tk == "x" else TG          # _gy_real
+            self.w(f"{{ const R {sg} = {sign} * {gy};")
             if s.fname == "convert":
                 r = refs[0]
                 if self.tracked(r):
                     if r.kind == "u":
                         # d value / d exponent = value
-                        self.w(f"  {r.g} = {r.g} + {sg} * g_expm({r.v}, code, xm);")
+                        self.gacc(r, f"{sg} * g_expm({r.v}, code, xm)", "  ")
                     else:
-                        self.w(f"  {r.g} = {r.g} + {sg};")
+                        self.gacc(r, sg, "  ")
             else:
                 parts = self.partials(s.fname, xs)
                 for r, p in zip(refs, parts):
@@ -1814,7 +1945,7 @@ class _Emitter:
                                 else f"!((double)R({x0}) > 0.0)")
                         self.w(f"  if (({cond}) && !code) code = RC_DOMAIN;")
                         p = pv
-                    self.w(f"  {r.g} = {r.g} + {sg} * {p};")
+                    self.gacc(r, f"{sg} * {p}", "  ")
             self.w("}")
             return
         # *= and /= : the target is a logarithmic number
@@ -1845,7 +1976,8 @@ class _Emitter:
             if r.kind == "u":
                 self.w(f"{r.g} = {r.g} + {sign} * {TG};")
             else:
-                self.w(f"{r.g} = {r.g} + g_div({sign} * {TG}, {self.atom_real(a, r)}, code);")
+                # exponent contribution log(value(a)): a.g += sign * gy / a
+                self.gacc(r, f"g_div({sign} * {TG}, {self.atom_real(a, r)}, code)")
                 self.fail_check(label)
 
 
@@ -2032,7 +2164,8 @@ def _elision_split(body, inliner, fname, params):
     return R, M, G
 
 
-def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_params=()):
+def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_params=(),
+             fixed_params=()):
     """CUDA source of the batched gradient (mode "grad"), forward-over-reverse
     Hessian-column (mode "hess": the same code over Dual numbers, tangent on
     the Float leaf `dir`) or plain run / uncall (modes "run" / "uncall": one
@@ -2051,13 +2184,17 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
     int_params = set(int_params)
     shapes = _check_shapes(array_shapes, parser.arrays.get(fname, ()), params)
     complex_params = set(complex_params)
+    fixed_params = set(fixed_params)
+    if fixed_params and mode == "hess":
+        raise UnsupportedProgram("codegen: Hessians of Fixed parameters are not compiled")
     kinds = {p: ("ai" if p in shapes and p in int_params else "a" if p in shapes
-                 else "i" if p in int_params else "c" if p in complex_params else "f")
+                 else "i" if p in int_params else "c" if p in complex_params
+                 else "x" if p in fixed_params else "f")
              for p in params}
     inliner = _Inliner(fns)
     fwd = inliner.run(_expand(body), (fname,))
     inv = inliner.run(_expand(_invert_list(body)), (fname,))
-    floats = [p for p in params if kinds[p] in ("f", "a", "c")]
+    floats = [p for p in params if kinds[p] in ("f", "a", "c", "x")]   # leaf columns
     ints = [p for p in params if kinds[p] in ("i", "ai")]
     leaves, base = [], {}
     for p in floats:
@@ -2096,6 +2233,7 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
             raise UnsupportedProgram(f"codegen: {v!r} shadows a parameter")
         k = allk.get(v, "f")
         decl.append(f"    long long v_{_cid(v)} = 0;" if k == "i"
+                    else f"    long long v_{_cid(v)} = 0, g_{_cid(v)} = 0;" if k == "x"
                     else f"    R v_{_cid(v)} = R(0.0), g_{_cid(v)} = R(0.0);")
     NL = len(leaves)
     hess = mode == "hess"
@@ -2149,6 +2287,8 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
             L.append(f"      v_{c}[e] = R(fin[({b}LL + e) * n + i]"
                      + (f", dir == {b} + e ? 1.0 : 0.0);" if hess else ");"))
             L.append(f"      g_{c}[e] = R(0.0); }}")
+        elif kinds[p] == "x":                       # Fixed: the raw int64 in the column's bits
+            L.append(f"    long long v_{c} = __double_as_longlong(fin[{b}LL * n + i]), g_{c} = 0;")
         elif kinds[p] == "c":                       # Complex: two Float cells, re then im
             for q, fld in enumerate(("re", "im")):
                 L.append(f"    R v_{c}_{fld} = R(fin[{b + q}LL * n + i]"
@@ -2170,11 +2310,15 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
             nib += 1
     L += decl
 
-    def each_leaf(fmt):
-        """C lines applying fmt(col_expr, value_lvalue, grad_lvalue) to every leaf."""
+    def each_leaf(fmt, fmt_x=None):
+        """C lines applying fmt(col_expr, value_lvalue, grad_lvalue) to every
+        leaf (fmt_x to the Fixed ones: raw int64 cells)."""
         out = []
         for p in floats:
             b, c = base[p], _cid(p)
+            if kinds[p] == "x":
+                out.append("    " + fmt_x(f"{b}LL", f"v_{c}", f"g_{c}"))
+                continue
             if p in shapes:
                 m = math.prod(shapes[p])
                 out.append(f"    for (int e = 0; e < {m}; ++e) {{ "
@@ -2195,7 +2339,8 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
              + (" hout[e * n + i] = NAN;" if hess else "") + " }")
     L.append(f"      for (int e = 0; e < {nib}; ++e) iout[e * n + i] = 0;")
     L.append("      fail[i] = (unsigned char)code; continue; }")
-    L += each_leaf(lambda col, v, g: f"fout[{col} * n + i] = rl_p({v});")
+    L += each_leaf(lambda col, v, g: f"fout[{col} * n + i] = rl_p({v});",
+                   lambda col, v, g: f"fout[{col} * n + i] = __longlong_as_double({v});")
     for p in ints:
         if p in shapes:
             L.append(f"    for (int e = 0; e < {math.prod(shapes[p])}; ++e)"
@@ -2209,13 +2354,15 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
         return "\n".join(L), floats, ints, leaves
     L.append("    // ---- uncall_function in gradient mode (seeded) ----")
     L.append("    // coerce_to_kind: a seed enters as Dual(seed, 0)")
-    L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);")
+    L += each_leaf(lambda col, v, g: f"{g} = R(seeds[{col}]);",
+                   lambda col, v, g: f"{g} = __double_as_longlong(seeds[{col}]);")
     L.append("    ticks = 0;" if split is None else
              "    ticks = ticks_r;      // ~f's elided R spends the forward R's ticks")
     L += em_g.lines
     L.append("    if (!code) {      // the backward pass must restore every argument")
     L += ["  " + x for x in each_leaf(
-        lambda col, v, g: f"if (!(fabs(rl_p({v}) - fin[{col} * n + i]) <= tol)) code = RC_REV;")]
+        lambda col, v, g: f"if (!(fabs(rl_p({v}) - fin[{col} * n + i]) <= tol)) code = RC_REV;",
+        lambda col, v, g: f"if ({v} != __double_as_longlong(fin[{col} * n + i])) code = RC_REV;")]
     for p in ints:
         if p in shapes:
             L.append(f"      for (int e = 0; e < {math.prod(shapes[p])}; ++e)"
@@ -2224,7 +2371,8 @@ def generate(src, fname, int_params=(), mode="grad", array_shapes=None, complex_
             L.append(f"      if (v_{_cid(p)} != iin[{ibase[p]}]) code = RC_REV;")
     L.append("    }")
     L += each_leaf(lambda col, v, g: f"gout[{col} * n + i] = code ? NAN : rl_p({g});"
-                   + (f" hout[{col} * n + i] = code ? NAN : rl_t({g});" if hess else ""))
+                   + (f" hout[{col} * n + i] = code ? NAN : rl_t({g});" if hess else ""),
+                   lambda col, v, g: f"gout[{col} * n + i] = __longlong_as_double({g});")
     L.append("    if (code) {")
     L.append(f"      for (int e = 0; e < {NL}; ++e) fout[e * n + i] = NAN;")
     L.append("    }")
@@ -2325,13 +2473,15 @@ class CompiledFunction:
     parameter name (arrays keep their shape; Int parameters carry no
     gradient)."""
 
-    def __init__(self, source_text, fname, int_params=(), array_shapes=None, complex_params=()):
+    def __init__(self, source_text, fname, int_params=(), array_shapes=None, complex_params=(),
+                 fixed_params=()):
         self.fname = fname
         self._text, self._ints, self._shapes = source_text, tuple(int_params), array_shapes
         self.complex = tuple(complex_params)
+        self.fixed = tuple(fixed_params)
         self.source, self.floats, self.ints, self.leaves = generate(
             source_text, fname, int_params, array_shapes=array_shapes,
-            complex_params=self.complex)
+            complex_params=self.complex, fixed_params=self.fixed)
         self.params = _Parser(source_text).program()[fname][0]
         self.shapes = _check_shapes(array_shapes, (), self.params)
         self._lib = self._load(self.source)
@@ -2350,7 +2500,8 @@ class CompiledFunction:
         if mode not in self._libs:
             self._libs[mode] = self._load(generate(self._text, self.fname, self._ints, mode=mode,
                                                    array_shapes=self._shapes,
-                                                   complex_params=self.complex)[0])
+                                                   complex_params=self.complex,
+                                                   fixed_params=self.fixed)[0])
         return self._libs[mode]
 
     def run(self, inputs, direction=1, tol=1e-9, invcheck=True, max_steps=10**9):
@@ -2401,6 +2552,14 @@ class CompiledFunction:
         for p in self.floats:
             v = inputs.get(p)
             shp = self.shapes.get(p, ())
+            if p in self.fixed:                            # raw int64 tensor (n,) or one Fixed
+                if isinstance(v, torch.Tensor) and v.dim() == 1:
+                    if not v.is_cuda or v.dtype != torch.int64:
+                        raise KindError(f"{p} must be a CUDA int64 tensor of Fixed raw values")
+                    n = v.shape[0] if n is None else n
+                    if v.shape[0] != n:
+                        raise KindError("all batched inputs need the same length")
+                continue
             if p in self.complex:
                 if isinstance(v, torch.Tensor) and v.dim() == 1:
                     if not v.is_cuda or v.dtype != torch.complex128:
@@ -2422,6 +2581,14 @@ class CompiledFunction:
             shp = self.shapes.get(p, ())
             m = math.prod(shp)
             v = inputs.get(p, 0.0)
+            if p in self.fixed:                            # the raw value's bits
+                if isinstance(v, torch.Tensor) and v.dim() == 1:
+                    cols.append(v.view(torch.float64).reshape(1, n))
+                else:
+                    raw = v.raw if hasattr(v, "raw") else _fx_from_real(v)
+                    cols.append(torch.tensor([raw], dtype=torch.int64, device=dev)
+                                .view(torch.float64).reshape(1, 1).expand(1, n))
+                continue
             if p in self.complex:                          # re and im columns
                 if isinstance(v, torch.Tensor) and v.dim() == 1:
                     cols += [v.real.reshape(1, n), v.imag.reshape(1, n)]
@@ -2460,7 +2627,7 @@ class CompiledFunction:
             ivals.append(v)
         iin = torch.tensor(ivals or [0], dtype=torch.int64, device=dev)
         col = {leaf: k for k, leaf in enumerate(self.leaves)}
-        sv = [0.0] * max(1, len(self.leaves))
+        sv = [0] * max(1, len(self.leaves))           # bit patterns (Fixed leaves: raw)
         for pname, path, val in (self._default_seeds() if seeds is None else seeds):
             if path is None:
                 path = ()
@@ -2470,8 +2637,10 @@ class CompiledFunction:
                                 for a, b in path))
             if key not in col:
                 raise KindError("seed target is not a differentiable leaf")
-            sv[col[key]] = float(val)
-        sv = torch.tensor(sv, dtype=torch.float64, device=dev)
+            # coerce_to_kind: a Fixed leaf's seed is Fixed.from_real(seed)
+            sv[col[key]] = (_fx_from_real(val) if pname in self.fixed
+                            else int(np.float64(float(val)).view(np.int64)))
+        sv = torch.tensor(sv, dtype=torch.int64, device=dev).view(torch.float64)
         fout = torch.empty_like(fin)
         gout = torch.empty_like(fin)
         hout = torch.empty_like(fin) if dir_ >= 0 else None
@@ -2486,6 +2655,11 @@ class CompiledFunction:
             raise NativeLibraryError(f"codegen kernel launch failed (cudaError {rc})")
         primal, grads, b = {}, {}, 0
         for p in self.floats:
+            if p in self.fixed:                            # raw int64 values / cotangents
+                primal[p] = fout[b].contiguous().view(torch.int64)
+                grads[p] = gout[b].contiguous().view(torch.int64)
+                b += 1
+                continue
             if p in self.complex:
                 primal[p] = torch.complex(fout[b], fout[b + 1])
                 grads[p] = torch.complex(gout[b], gout[b + 1])
@@ -2505,7 +2679,9 @@ class CompiledFunction:
         return primal, grads, fail, hout
 
 
-def compile_function(source_text, fname, int_params=(), array_shapes=None, complex_params=()):
+def compile_function(source_text, fname, int_params=(), array_shapes=None, complex_params=(),
+                     fixed_params=()):
     """Compile function `fname` of reversible-DSL source to a batched CUDA
     gradient kernel (see CompiledFunction)."""
-    return CompiledFunction(source_text, fname, int_params, array_shapes, complex_params)
+    return CompiledFunction(source_text, fname, int_params, array_shapes, complex_params,
+                            fixed_params)

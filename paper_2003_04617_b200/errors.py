@@ -119,12 +119,13 @@ _CODE_CLASSES = {
     9: OverflowError,  # CPython math.exp raises OverflowError (values.py:362)
     10: AliasedArguments,
     11: AssertFailed,
+    12: ValueError,    # round(nan) in Fixed.from_real (generated kernels only)
 }
 
 CODE_NAMES = {0: "", 1: "PostconditionMismatch", 2: "DirtyAncilla", 3: "RevDomainError",
               4: "LoopIteratorMutated", 5: "RevError", 6: "FuelExhausted", 7: "KindError",
               8: "IndexOutOfBounds", 9: "OverflowError", 10: "AliasedArguments",
-              11: "AssertFailed"}
+              11: "AssertFailed", 12: "ValueError"}
 
 _MESSAGES = {
     1: "branch or loop postcondition mismatch",
@@ -138,6 +139,7 @@ _MESSAGES = {
     9: "math range error",
     10: "instruction arguments share storage",
     11: "@safe assertion failed",
+    12: "cannot convert float NaN to integer",
 }
 
 
@@ -146,8 +148,8 @@ def error_for_code(code, where=""):
     msg = _MESSAGES.get(int(code), f"device status {int(code)}")
     if where:
         msg = f"{msg} ({where})"
-    if cls is OverflowError:
-        return OverflowError(msg)
+    if cls in (OverflowError, ValueError):
+        return cls(msg)
     return cls(msg)
 
 

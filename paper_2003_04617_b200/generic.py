@@ -8,8 +8,9 @@ interp.run / uncall / check_reversibility when the program's function is not
 one of the registered benchmark kernels (besselj, ba_proj, ba_weight, gmm).
 Argument kinds follow the reference's values: Python int -> Int, float ->
 Float, Array (ours, the reference's, numpy, torch) of floats -> Float array,
-of ints -> Int array; ULog / Complex / Fixed / Record / Bool arguments are
-outside the compiled subset (UnsupportedProgram).  Results come back in the
+of ints -> Int array, Complex -> two Float leaves, Fixed (anything with the
+reference Fixed's `raw` / `to_float`) -> a raw int64 Q31.32 cell; ULog /
+Record / Bool arguments are outside the compiled subset (UnsupportedProgram).  Results come back in the
 reference's containers (floats, ints, Arrays of the caller's class) and a
 device error raises the reference's exception class for that row.
 """
@@ -30,6 +31,16 @@ def _is_int(v):
 
 def _is_float(v):
     return isinstance(v, (float, np.floating))
+
+
+def _is_fixed(v):
+    """The reference's Fixed (values.py:28): a Q31.32 raw integer."""
+    return hasattr(v, "raw") and hasattr(v, "to_float")
+
+
+def _fx_float(raw):
+    """values.Fixed.to_float of raw int64 values (numpy arrays): raw / 2^32."""
+    return np.asarray(raw, dtype=np.int64).astype(np.float64) * 2.0 ** -32
 
 
 def _as_array(v):
@@ -58,6 +69,8 @@ def _kind(v, name):
         return "i", ()
     if _is_float(v):
         return "f", ()
+    if _is_fixed(v):
+        return "x", ()
     if isinstance(v, complex) or (hasattr(v, "re") and hasattr(v, "im")):
         return "c", ()                                 # Complex: two Float leaves
     a = _as_array(v)
@@ -76,9 +89,10 @@ def compiled(prog, fname, kinds):
     ints = tuple(p for p, (k, _) in kinds.items() if k in ("i", "ai"))
     shapes = {p: s for p, (k, s) in kinds.items() if k in ("a", "ai")}
     cplx = tuple(p for p, (k, _) in kinds.items() if k == "c")
-    key = (prog.source, fname, ints, tuple(sorted(shapes.items())), cplx)
+    fixed = tuple(p for p, (k, _) in kinds.items() if k == "x")
+    key = (prog.source, fname, ints, tuple(sorted(shapes.items())), cplx, fixed)
     if key not in _CACHE:
-        _CACHE[key] = codegen.CompiledFunction(prog.source, fname, ints, shapes, cplx)
+        _CACHE[key] = codegen.CompiledFunction(prog.source, fname, ints, shapes, cplx, fixed)
     return _CACHE[key]
 
 
@@ -95,7 +109,7 @@ def _inputs(names, kinds, args):
         k = kinds[p][0]
         out[p] = float(v) if k == "f" else int(v) if k == "i" else (
             complex(v) if k == "c" and isinstance(v, complex) else
-            v if k == "c" else _as_array(v))
+            v if k in ("c", "x") else _as_array(v))
     return out
 
 
@@ -106,6 +120,9 @@ def _back(template, kind, value):
         return float(v)
     if kind == "i":
         return int(v)
+    if kind == "x":                                   # the caller's Fixed class, from raw
+        raw = int(v)
+        return type(template)(raw) if _is_fixed(template) else raw
     if kind == "c":                                   # the caller's Complex class
         z = complex(v)
         if hasattr(template, "re") and hasattr(template, "im"):
@@ -216,7 +233,7 @@ def _leaf_rows(kinds, names, args):
     out = []
     for p, v in zip(names, args):
         k, shp = kinds[p]
-        if k == "f":
+        if k in ("f", "x"):
             out.append((p, None))
         elif k == "c":
             out += [(p, "re"), (p, "im")]
@@ -243,9 +260,18 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
             a = np.asarray(_cval(base[p]) if kind == "c" else base[p],
                            dtype=np.complex128 if kind == "c" else np.float64)
             batch[p] = np.broadcast_to(a, (max(n, 1),) + a.shape).copy()
+        elif kind == "x":                                # raw int64 rows
+            batch[p] = np.full(max(n, 1), int(base[p].raw), dtype=np.int64)
         else:
             batch[p] = base[p]
     for r, (p, i) in enumerate(leaves):
+        if kinds[p][0] == "x":
+            # the step is measured after Q31.32 quantization (autodiff.py:299-301)
+            x = float(base[p].to_float())
+            up, dn = codegen._fx_from_real(x + h), codegen._fx_from_real(x - h)
+            steps.append(float(_fx_float(up) - _fx_float(dn)))
+            batch[p][2 * r], batch[p][2 * r + 1] = up, dn
+            continue
         if i in ("re", "im"):                            # a Complex leaf
             z = _cval(base[p])
             x = z.real if i == "re" else z.imag
@@ -265,7 +291,7 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
         else:
             col[2 * r, i], col[2 * r + 1, i] = up, dn
     dev = torch.device("cuda", torch.cuda.current_device())
-    tens = {p: (torch.as_tensor(v, device=dev) if kinds[p][0] in ("f", "a", "c") else v)
+    tens = {p: (torch.as_tensor(v, device=dev) if kinds[p][0] in ("f", "a", "c", "x") else v)
             for p, v in batch.items()}
     out, fail = k.run(tens, 1, tol=opts.float_tolerance, invcheck=opts.invcheck,
                       max_steps=opts.max_steps)
@@ -285,6 +311,8 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
             col = v[:, int(np.ravel_multi_index(tuple(x - 1 for x in idx), shp))]
         else:
             col = v[:, 0]
+        if kinds[pname][0] == "x":                       # to_real(Fixed)
+            col = _fx_float(col)
         total = total + float(seed) * np.real(col)
     grads = {}
     for p, v in zip(names, args):
@@ -297,6 +325,6 @@ def finite_difference(prog, fdef, args, h, seeds, opts):
         if kind == "c":                                  # Complex(grad re, grad im)
             grads[p] = _back(v, "c", complex(vals[0], vals[1]))
         else:
-            grads[p] = float(vals[0]) if kind == "f" else \
+            grads[p] = float(vals[0]) if kind in ("f", "x") else \
                 _back(v, "a", np.asarray(vals).reshape(shp))
     return grads

@@ -3,11 +3,60 @@
 `Array` is the reference's rectangular, 1-based, row-major container; the
 drop-in `gradient()` also accepts the reference's own `revlang.values.Array`
 (anything with `.data` and `.shape`), numpy arrays and torch tensors.
+`Fixed` is the reference's Q31.32 number (values.py:28-86); the drop-in also
+accepts the reference's own `revlang.values.Fixed` (anything with `.raw` and
+`.to_float()`) and returns results in the caller's class.
 """
 
 import numpy as np
 
 from .errors import IndexOutOfBounds, KindError
+
+
+_FRAC = 32
+_SCALE = 1 << _FRAC
+
+
+def _wrap64(raw):
+    raw &= (1 << 64) - 1
+    return raw - (1 << 64) if raw & (1 << 63) else raw
+
+
+class Fixed:
+    """Q31.32 fixed point: `raw` is a signed 64-bit integer, value raw / 2^32;
+    + and - wrap mod 2^64 (exactly invertible); from_real rounds half-even."""
+
+    __slots__ = ("raw",)
+
+    def __init__(self, raw):
+        self.raw = _wrap64(int(raw))
+
+    @classmethod
+    def from_real(cls, v):
+        if isinstance(v, Fixed):
+            return v
+        return cls(round(float(v) * _SCALE))
+
+    def to_float(self):
+        return self.raw / _SCALE
+
+    def __add__(self, other):
+        return Fixed(self.raw + Fixed.from_real(other).raw)
+
+    def __sub__(self, other):
+        return Fixed(self.raw - Fixed.from_real(other).raw)
+
+    def __neg__(self):
+        return Fixed(-self.raw)
+
+    def __eq__(self, other):
+        return isinstance(other, Fixed) and self.raw == other.raw
+
+    def __hash__(self):
+        return hash(("Fixed", self.raw))
+
+    def __repr__(self):
+        return f"Fixed({self.to_float()!r})"
 
 
 class Array:

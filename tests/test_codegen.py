@@ -47,7 +47,7 @@ def test_calls_are_inlined_with_fresh_locals():
 
 def test_unsupported_constructs_are_rejected():
     for text in ("fn f(y!, x)\n g(y!, x)\nend\n",
-                 "fn f(y!, x)\n y! += 1.0fx\nend\n",
+                 "fn f(y!, x)\n y! += 1.0im\nend\n",
                  "fn f(y!, x)\n y!.rec += x\nend\n",
                  "fn f(y!, x)\n @safe print(x)\nend\n"):
         with pytest.raises(UnsupportedProgram):
@@ -117,9 +117,9 @@ def test_view_argument_indexed_by_another_argument():
 def test_reference_catalog_programs_in_the_subset_compile(tmp_path, monkeypatch):
     """The reference's own catalog (stdlib.CATALOG), pretty-printed by the
     reference and compiled here: every program whose argument kinds are in
-    the subset generates and builds for sm_100a (8 of 10, the Complex ones
-    included); the Fixed and the recursive bijector program are rejected with
-    UnsupportedProgram."""
+    the subset generates and builds for sm_100a (9 of 10, the Complex and
+    the Fixed ones included); the recursive bijector program is rejected
+    with UnsupportedProgram."""
     import random
     import sys
     monkeypatch.setenv("REVGPU_CODEGEN_CACHE", str(tmp_path))
@@ -139,11 +139,41 @@ def test_reference_catalog_programs_in_the_subset_compile(tmp_path, monkeypatch)
             ints = tuple(k for k, (kk, _) in kinds.items() if kk in ("i", "ai"))
             shapes = {k: s for k, (kk, s) in kinds.items() if kk in ("a", "ai")}
             cplx = tuple(k for k, (kk, _) in kinds.items() if kk == "c")
+            fixed = tuple(k for k, (kk, _) in kinds.items() if kk == "x")
             codegen.build(codegen.generate(pretty_print(p), fn, ints, array_shapes=shapes,
-                                           complex_params=cplx)[0])
+                                           complex_params=cplx, fixed_params=fixed)[0])
             built.append(name)
         except UnsupportedProgram:
             rejected.append(name)
     assert {"multiplier", "i_affine", "i_umm", "r_norm", "leapfrog_clean",
-            "leapfrog_cumulative", "complex_log", "complex_log_ccu"} <= set(built), \
+            "leapfrog_cumulative", "complex_log", "complex_log_ccu", "mypower_log"} <= set(built), \
         (built, rejected)
+
+
+def test_fixed_literals_and_rounding():
+    """Q31.32 from_real: round half to even, wrapped mod 2^64 (values.py:23-41);
+    the package's Fixed and the compiler's literal conversion agree."""
+    import paper_2003_04617_b200 as rg
+    assert codegen._fx_from_real(1.5) == 3 << 31
+    assert codegen._fx_from_real(2.5 / 2 ** 32) == 2          # half to even
+    assert codegen._fx_from_real(3.5 / 2 ** 32) == 4
+    assert codegen._fx_from_real(2.0 ** 31) == -(1 << 63)     # wraps
+    assert codegen._fx_from_real(-2.0 ** 31) == -(1 << 63)
+    for v in (0.0, -1.25, 1e9, -3e9, 1.3, 7.1e-10):
+        assert rg.Fixed.from_real(v).raw == codegen._fx_from_real(v)
+    toks = codegen._tokenize("x != 0fx + 2.25fx")
+    assert toks[2] == ("num", codegen.FixLit(0)) and toks[4] == ("num", codegen.FixLit(9 << 30))
+
+
+def test_fixed_program_generates_and_builds(tmp_path, monkeypatch):
+    """tests/golden/codegen/fxmix.rnl: Fixed parameters, literals, a Fixed
+    ancilla, Fixed += Float, Float += f(Fixed): all modes generate and build."""
+    monkeypatch.setenv("REVGPU_CODEGEN_CACHE", str(tmp_path))
+    text = open(os.path.join(os.path.dirname(__file__), "golden", "codegen", "fxmix.rnl")).read()
+    for mode in ("grad", "run", "uncall"):
+        code, floats, ints, leaves = codegen.generate(text, "fxmix", ("k",), mode=mode,
+                                                      fixed_params=("acc!", "b"))
+        assert "rl_fx_from" in code and floats == ["acc!", "y!", "b"] and ints == ["k"]
+        codegen.build(code)
+    with pytest.raises(UnsupportedProgram):
+        codegen.generate(text, "fxmix", ("k",), mode="hess", fixed_params=("acc!", "b"))
