@@ -783,13 +783,30 @@ def gen_codegen_fixed():
           sorted(set(out["gacc_err"]) - {""}))
 
 
+def gen_codegen_recursion():
+    """countdown.rnl (recursion through bijector-view arguments, Int cells)
+    through the reference: run and uncall of chain for n = 0..12 and of tri
+    for k = 0..20."""
+    from revlang import run, uncall
+    prog = parse_program(open(os.path.join(OUT_DIR, "codegen", "countdown.rnl")).read())
+    ns = np.arange(13)
+    out = {"n": ns, "k": np.arange(21)}
+    out["chain_run"] = np.array([run(prog, "chain", [0, int(n)]) for n in ns], dtype=np.int64)
+    out["chain_uncall"] = np.array([uncall(prog, "chain", [100, int(n)]) for n in ns],
+                                   dtype=np.int64)
+    out["tri_run"] = np.array([run(prog, "tri", [7, int(k)]) for k in out["k"]], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT_DIR, "codegen_recursion.npz"), **out)
+    print("recursion goldens:", len(ns), "chain cases")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT_DIR, exist_ok=True)
     which = sys.argv[1:] or ["bessel", "ba", "gmm", "run", "hess", "codegen",
                               "codegen_arrays", "codegen_programs",
                               "codegen_dropin", "codegen_nbody",
                               "codegen_random",
-                              "codegen_complex", "codegen_complex_fd", "codegen_fixed", "bessel_fuel",
+                              "codegen_complex", "codegen_complex_fd", "codegen_fixed",
+                              "codegen_recursion", "bessel_fuel",
                               "gmm_fuel", "ba_fuel"]
     for w in which:
         globals()["gen_" + w]()

@@ -10,7 +10,7 @@ failures detected on device raise the reference's exception classes.
 
 Differences to the reference, all documented in DESIGN.md:
   * no CPU path: a function outside codegen's subset (records, ULog
-    arguments, recursion, bijector views) raises UnsupportedProgram;
+    arguments) raises UnsupportedProgram;
   * binary64 only (ExecOptions.float_dtype must be None), no tracing;
   * seeds on input leaves are added to the returned cotangent (as the
     reference's GVar initial value would be); several output seeds on BA

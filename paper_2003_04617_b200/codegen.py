@@ -29,11 +29,14 @@ a Float value enters through from_real, cotangents are Fixed and quantized
 at every accumulation, values.py:28-86 / numerics.py:305-306, 419-428),
 fixed-shape Float arrays (parameters and ancilla-free array arguments),
 Float / ULog / Int / Fixed ancillas, `+= -= *= /=` instructions with the
-INSTR_FNS functions, `xor=` on Int cells, calls between compiled functions,
-`<-` / `->`, @routine / ~@routine, @invcheckoff, for / while / if.
-Records, recursion, bijector views and Fixed arithmetic inside expressions
-are rejected at compile time (UnsupportedProgram), as are the static
-aliasing patterns the reference rejects at run time (AliasedArguments).
+INSTR_FNS functions, `xor=` on Int cells, calls between compiled functions
+(inlined; recursive calls level by level up to REVGPU_CODEGEN_DEPTH, past
+which the kernel reports the interpreter's RecursionError), bijector-view
+call arguments over Int cells (`k |> addconst(-1)`: copy in through fwd,
+write back through inv), `<-` / `->`, @routine / ~@routine, @invcheckoff,
+for / while / if.  Records and Fixed arithmetic inside expressions are
+rejected at compile time (UnsupportedProgram), as are the static aliasing
+patterns the reference rejects at run time (AliasedArguments).
 
 The kernel is built with nvcc for sm_100a into a cache directory
 ($REVGPU_CODEGEN_CACHE, default paper_2003_04617_b200/_codegen_cache) and bound with
@@ -226,6 +229,46 @@ class ArgCheck:
     """Entry checks of an inlined call (interpreter.py:969-978): the strict
     alias pairs over its argument views, then their reads (bounds)."""
     views: tuple
+
+
+# numerics.py:189-193: name -> number of constant arguments
+BIJECTORS = {"neg": 0, "addconst": 1, "mulconst": 1}
+
+
+@dataclass(frozen=True)
+class BView:
+    """`base |> bij(c...)` (ir.BijView): a call argument the callee reads as
+    bij.fwd(base) and writes back through bij.inv (interpreter.py:565-583);
+    storage identity is the base's (bijectors do not change identity)."""
+    base: object
+    bij: str
+    args: tuple
+
+    @property
+    def name(self):
+        return self.base.name
+
+    def root(self):
+        return self.base.root() if isinstance(self.base, BView) else self.base
+
+
+@dataclass(frozen=True)
+class BijIn:
+    """Copy-in of a bijector-view argument into the callee's cell `tmp`."""
+    tmp: str
+    view: BView
+
+
+@dataclass(frozen=True)
+class BijOut:
+    """Write-back of the callee's cell `tmp` through the view's inverses."""
+    tmp: str
+    view: BView
+
+
+@dataclass(frozen=True)
+class DepthErr:
+    """A recursive call past the compiled inlining depth (RecursionError)."""
 
 
 # numerics.py:30-33
@@ -487,7 +530,30 @@ class _Parser:
         self.expect("punct", "(")
         views = []
         while not self.at("punct", ")"):
-            views.append(self.index_tail(self.name()))
+            v = self.index_tail(self.name())
+            while self.at("punct", "|>"):                # bijector views (numerics.py:189)
+                self.adv()
+                bij = self.name()
+                cargs = []
+                if self.at("punct", "("):
+                    self.adv()
+                    while not self.at("punct", ")"):
+                        neg = self.at("punct", "-")
+                        if neg:
+                            self.adv()
+                        if not self.at("num") or isinstance(self.cur[1], FixLit):
+                            raise KindError("bijector arguments are numeric constants")
+                        c = self.adv()[1]
+                        cargs.append(-c if neg else c)
+                        if self.at("punct", ","):
+                            self.adv()
+                    self.adv()
+                if bij not in BIJECTORS:
+                    raise KindError(f"no bijector named {bij!r}")
+                if len(cargs) != BIJECTORS[bij] or (bij == "mulconst" and cargs[0] == 0):
+                    raise KindError(f"invalid arguments for bijector {bij!r}")
+                v = BView(v, bij, tuple(cargs))
+            views.append(v)
             if self.at("punct", ","):
                 self.adv()
         self.adv()
@@ -749,6 +815,16 @@ def _balanced(stmts, fname):
                                  "in the same block")
 
 
+_MAX_DEPTH = int(os.environ.get("REVGPU_CODEGEN_DEPTH", "24"))   # inlined recursion levels
+
+
+def _unwrap(v):
+    """The storage view under bijector views (their identity, interpreter.py:619)."""
+    while isinstance(v, BView):
+        v = v.base
+    return v
+
+
 class _Inliner:
     def __init__(self, fns):
         self.fns = fns
@@ -809,8 +885,11 @@ class _Inliner:
     def call(self, s, stack):
         if s.f not in self.fns:
             raise UnsupportedProgram(f"codegen: no function named {s.f!r}")
-        if s.f in stack:
-            raise UnsupportedProgram(f"codegen: recursive call of {s.f!r} cannot be inlined")
+        if stack.count(s.f) >= _MAX_DEPTH:
+            # recursion is inlined level by level (a fresh copy of the body per
+            # level); a call past the compiled depth is the interpreter's
+            # RecursionError when it runs
+            return (ArgCheck(tuple(_unwrap(a) for a in s.args)), DepthErr())
         params, body = self.fns[s.f]
         if len(params) != len(s.args):
             raise KindError(f"{s.f} takes {len(params)} arguments, got {len(s.args)}")
@@ -829,10 +908,20 @@ class _Inliner:
         body = _expand(_invert_list(body) if s.uncall else body)
         _balanced(body, s.f)
         self.n += 1
-        env = dict(zip(params, s.args))
+        args, pre, post = [], [], []
+        for a in s.args:                     # bijector views: copy in, run, write back
+            if isinstance(a, BView):
+                tmp = f"__bv{self.n}_{len(pre)}"
+                pre.append(BijIn(tmp, a))
+                post.append(BijOut(tmp, a))
+                args.append(Var(tmp))
+            else:
+                args.append(a)
+        env = dict(zip(params, args))
         tag = f"__{s.f}{self.n}"
         inl = _Subst(env, tag, set(params))
-        return (ArgCheck(s.args),) + self.run(inl.stmts(body), stack + (s.f,))
+        return ((ArgCheck(tuple(_unwrap(a) for a in s.args)),) + tuple(pre)
+                + self.run(inl.stmts(body), stack + (s.f,)) + tuple(post))
 
 
 class _Subst:
@@ -847,6 +936,8 @@ class _Subst:
         return n + self.tag
 
     def view(self, v):
+        if isinstance(v, BView):
+            return BView(self.view(v.base), v.bij, v.args)
         if isinstance(v, Var):
             return self.env.get(v.name, Var(v.name + self.tag))
         if isinstance(v, IView):
@@ -917,6 +1008,12 @@ _PRELUDE = r"""
 #define RC_FUEL 6
 #define RC_OVERFLOW 9
 #define RC_VALUE 12
+#define RC_DEPTH 13
+// mulconst's Int write-back (numerics._div_const): exact division or KindError
+__device__ __forceinline__ long long rl_idivc(long long v, long long c, int &code) {
+  if (v % c != 0) { if (!code) code = 7; return 0; }
+  return v / c;
+}
 // Fixed (Q31.32, values.py:28-86): raw int64 cells, + / - wrap mod 2^64;
 // to_float = raw / 2^32 (correctly rounded); from_real = round(v * 2^32)
 // half-even, wrapped; round(inf) is Python's OverflowError, round(nan) its
@@ -1614,6 +1711,10 @@ class _Emitter:
             self.stmts(s.body, grad, label)
             self.depth -= 1
             self.w(f"  chk = {n}; }}")
+        elif isinstance(s, (BijIn, BijOut)):
+            self.bijector(s)
+        elif isinstance(s, DepthErr):
+            self.w("if (!code) code = RC_DEPTH;")
         elif isinstance(s, ArgCheck):
             self.w("{")
             self.depth += 1
@@ -1747,6 +1848,38 @@ class _Emitter:
             self.w("}")
         else:
             raise UnsupportedProgram(f"codegen: unsupported statement {s!r}")
+
+    def bijector(self, s):
+        """Copy-in / write-back of a bijector-view call argument (numerics.py:
+        153-193 on Int cells: neg, addconst, mulconst with Int constants;
+        a mulconst write-back that does not divide exactly is the
+        reference's KindError)."""
+        base = _unwrap(s.view)
+        if not isinstance(base, Var) or self.kind(base.name) != "i":
+            raise UnsupportedProgram("codegen: bijector views are compiled over Int scalar cells")
+        chain = []
+        v = s.view
+        while isinstance(v, BView):
+            if any(not isinstance(c, int) or isinstance(c, bool) for c in v.args):
+                raise UnsupportedProgram("codegen: bijector constants on Int cells must be Int")
+            chain.append((v.bij, v.args))
+            v = v.base
+        chain.reverse()                                  # base outward
+        if isinstance(s, BijIn):
+            self.kinds[s.tmp] = "i"
+            val = f"v_{_cid(base.name)}"
+            for bij, args in chain:
+                val = {"neg": lambda: f"(-({val}))",
+                       "addconst": lambda: f"(({val}) + {args[0]}LL)",
+                       "mulconst": lambda: f"(({val}) * {args[0]}LL)"}[bij]()
+            self.w(f"v_{_cid(s.tmp)} = {val};")
+            return
+        val = f"v_{_cid(s.tmp)}"
+        for bij, args in reversed(chain):
+            val = {"neg": lambda: f"(-({val}))",
+                   "addconst": lambda: f"(({val}) - {args[0]}LL)",
+                   "mulconst": lambda: f"rl_idivc({val}, {args[0]}LL, code)"}[bij]()
+        self.w(f"v_{_cid(base.name)} = {val};")
 
     def prim(self, s, grad, label):
         """SWAP / ROT / IROT / NEG / INC / DEC (numerics.py:391-415 plain,
@@ -1989,6 +2122,8 @@ def _collect_vars(stmts, acc):
     for s in stmts:
         if isinstance(s, (Alloc, Dealloc)):
             acc.add(s.name)
+        elif isinstance(s, BijIn):
+            acc.add(s.tmp)
         elif isinstance(s, For):
             acc.add(s.var)
             _collect_vars(s.body, acc)

@@ -120,12 +120,13 @@ _CODE_CLASSES = {
     10: AliasedArguments,
     11: AssertFailed,
     12: ValueError,    # round(nan) in Fixed.from_real (generated kernels only)
+    13: RecursionError,  # a recursive call past the generated kernel's inlined depth
 }
 
 CODE_NAMES = {0: "", 1: "PostconditionMismatch", 2: "DirtyAncilla", 3: "RevDomainError",
               4: "LoopIteratorMutated", 5: "RevError", 6: "FuelExhausted", 7: "KindError",
               8: "IndexOutOfBounds", 9: "OverflowError", 10: "AliasedArguments",
-              11: "AssertFailed", 12: "ValueError"}
+              11: "AssertFailed", 12: "ValueError", 13: "RecursionError"}
 
 _MESSAGES = {
     1: "branch or loop postcondition mismatch",
@@ -140,6 +141,7 @@ _MESSAGES = {
     10: "instruction arguments share storage",
     11: "@safe assertion failed",
     12: "cannot convert float NaN to integer",
+    13: "recursion deeper than the generated kernel's inlined levels (REVGPU_CODEGEN_DEPTH)",
 }
 
 
@@ -148,7 +150,7 @@ def error_for_code(code, where=""):
     msg = _MESSAGES.get(int(code), f"device status {int(code)}")
     if where:
         msg = f"{msg} ({where})"
-    if cls in (OverflowError, ValueError):
+    if cls in (OverflowError, ValueError, RecursionError):
         return cls(msg)
     return cls(msg)
 

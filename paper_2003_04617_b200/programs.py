@@ -30,7 +30,7 @@ _UNICODE = {"←": "<-", "→": "->", "⊻=": "xor="}
 _TOKEN = re.compile(r"""
     (?P<num>(?:\d+\.\d*|\.\d+|\d+)(?:[eE][+-]?\d+)?(?:fx|ul|im)?)
   | (?P<name>~?@?[A-Za-z_][A-Za-z_0-9]*!?)
-  | (?P<punct><-|->|\+=|-=|\*=|/=|xor=|==|!=|<=|>=|&&|\|\||::|[-+*/^%(),\[\]<>~:.=!])
+  | (?P<punct><-|->|\+=|-=|\*=|/=|xor=|==|!=|<=|>=|&&|\|\||\|>|::|[-+*/^%(),\[\]<>~:.=!])
   | (?P<ws>\s+)
 """, re.VERBOSE)
 
