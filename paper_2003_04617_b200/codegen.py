@@ -816,6 +816,7 @@ def _balanced(stmts, fname):
 
 
 _MAX_DEPTH = int(os.environ.get("REVGPU_CODEGEN_DEPTH", "24"))   # inlined recursion levels
+_MAX_INLINED = 4096                                   # inlined calls per generated kernel
 
 
 def _unwrap(v):
@@ -908,6 +909,9 @@ class _Inliner:
         body = _expand(_invert_list(body) if s.uncall else body)
         _balanced(body, s.f)
         self.n += 1
+        if self.n > _MAX_INLINED:
+            raise UnsupportedProgram(f"codegen: more than {_MAX_INLINED} inlined calls (a recursion "
+                                     "with several call sites per level grows exponentially)")
         args, pre, post = [], [], []
         for a in s.args:                     # bijector views: copy in, run, write back
             if isinstance(a, BView):

@@ -42,6 +42,8 @@ def test_calls_are_inlined_with_fresh_locals():
     # recursion is inlined level by level; past REVGPU_CODEGEN_DEPTH the kernel
     # reports the interpreter's RecursionError (an endless self-call here)
     assert "code = RC_DEPTH" in codegen.generate("fn f(y!, x)\n f(y!, x)\nend\n", "f")[0]
+    with pytest.raises(UnsupportedProgram):               # two self-calls per level: 2^24 copies
+        codegen.generate("fn f(y!, x)\n f(y!, x)\n f(y!, x)\nend\n", "f")
     with pytest.raises(UnsupportedProgram):                 # leaks an ancilla (DirtyAncilla)
         codegen.generate("fn g(y!)\n t <- 0.0\nend\nfn f(y!)\n g(y!)\nend\n", "f")
 
