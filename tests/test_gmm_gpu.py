@@ -112,6 +112,20 @@ def test_unaligned_x_takes_the_cp_async_kernels(cuda, oracle, d):
     check_vs((e, ga, gm, gi), got)
 
 
+@pytest.mark.parametrize("d,K,N", [(2, 1, 1), (2, 3, 5), (64, 1, 33), (62, 2, 31), (30, 7, 64)])
+def test_tiny_shapes_vs_oracle(cuda, oracle, d, K, N):
+    """Edge shapes of the tile kernels: one point, one component, a single
+    partial tile, d just below a padding boundary (TMA out-of-bounds columns)."""
+    rng = np.random.default_rng(500 + d * 10 + K + N)
+    alphas, means, icf, x = inputs(rng, d, K, N)
+    cst = gmm_constants(d, K, N, 1.0, 0)
+    rc, e, ga, gm, gi = oracle.gmm_grad(alphas, means, icf, x, 1.0, 0, cst)
+    assert rc == 0
+    got = run_dev(cuda, alphas, means, icf, x, 1.0, 0, cst)
+    assert not got[4].any()
+    check_vs((e, ga, gm, gi), got)
+
+
 def run_full(dev, alphas, means, icf, x, gamma, m, cst, **kw):
     """The drop-in single-device gradient (rl_gmm_gradient_f64)."""
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
