@@ -1588,6 +1588,11 @@ class _Emitter:
                 return f"((double)R({ls}) {op} (double)R({rs}))", "b"
             k = self.expr_kind(e)
             if op == "%":
+                if isinstance(e.r, Lit) and type(e.r.v) is int and e.r.v > 0 and \
+                        e.r.v & (e.r.v - 1) == 0:
+                    # Python's x % 2^m (non-negative for a positive divisor)
+                    # is the two's-complement low bits
+                    return f"(({ls}) & {e.r.v - 1}LL)", "i"
                 return f"g_imod({ls}, {rs}, code)", "i"
             if op == "/":
                 return f"g_div(R({ls}), R({rs}), code)", "f"
