@@ -82,8 +82,15 @@ __constant__ ExpConsts c_expk = RL_EXP_CONSTS_INIT;
 #ifndef BJ_SPEC
 #define BJ_SPEC 2          // speculative trips per warp vote (2: fewer live registers -> 3 CTAs/SM, measured best)
 #endif
+#ifndef BJ_PAIR
+#define BJ_PAIR 0          // 1: two z-neighbours per lane in the gradient / run kernels
+#endif
 #ifndef BJ_MINB
+#if BJ_PAIR
+#define BJ_MINB 2          // two elements per lane: up to 128 registers
+#else
 #define BJ_MINB 3          // __launch_bounds__ min blocks per SM (80 registers, no spills)
+#endif
 #endif
 #ifndef BJ_HESS_PAIRS
 #define BJ_HESS_PAIRS 1    // Hessian kernel: unpredicated trip pairs while every lane is live
@@ -745,6 +752,213 @@ __device__ __forceinline__ BJHOut besselj_hess_element(double z, bool valid, int
 // uncall of besselj (Jout = out_in + sign * J with every check of the two
 // primal sweeps; dzout unused): the objective-only ("-O") kernel.  MODE 2:
 // the Hessian (Dual sweeps; d2out = d2J/dz2).
+// ---------------------------------------------------------------------------
+// Two elements per lane (BJ_PAIR): besselj_element<false, GRAD>'s
+// per-element operation sequence (bit-identical results) over two
+// z-neighbours, interleaved so each warp carries two independent dependency
+// chains; the warp votes and the trip bounds cover both.  Elements failing
+// the FAST bound are recomputed by the single-element CAREFUL path.
+// ---------------------------------------------------------------------------
+struct BJS {
+  double z, logz, halfz, h2, s, t, acc, sg, h2g, J;
+  int code, code0, T;
+  bool valid, act, dead, bad, fwd_ok, ok;
+};
+
+__device__ __forceinline__ void bjp_prologue(BJS &e, int nu, double thr, int kfuel, double sfloor) {
+  e.code = 0;
+  if (e.valid && !(e.z > 0.0)) e.code = RL_ERR_DOMAIN;       // lz *= convert(z)
+  if (kfuel < 0 && e.valid && !e.code) e.code = RL_ERR_FUEL;
+  e.logz = (e.valid && !e.code) ? log(e.z) : 0.0;
+  double halfz = 0.0 + (0.0 + e.logz);                      // lz = 0 + log z; halfz *= lz
+  halfz = halfz - LN2;                                       // halfz /= 2
+  double h2 = 0.0 + halfz;                                   // halfz2 *= halfz (x2)
+  h2 = h2 + halfz;
+  double s = 0.0;
+  for (int q = 1; q <= nu; q++) {                            // for i = 1:1:nu
+    s = s + halfz;
+    s = s - (q < BJ_KP ? s_logpair[q].x : logi(q));
+  }
+  e.halfz = halfz;
+  e.h2 = h2;
+  e.s = s;
+  e.t = rexp<false>(s).t;                                    // acc += convert(s)
+  e.acc = 0.0 + e.t;
+  e.bad = e.valid && !e.code &&
+          !(e.z < 700.0 && s > -700.0 && s < 700.0 && h2 + sfloor > -700.0);
+  e.T = 0;
+  e.act = e.valid && !e.code && (e.t > thr);                 // while (s > thr, k != 0)
+  e.dead = !e.valid || e.code;
+  e.code0 = e.code;
+}
+
+// one speculative pair of forward trips (odd k + 1, even k + 2) of one element
+struct BJSpec {
+  double s1, s2, t1, t2, a1, a2;
+  bool act1, act2;
+};
+__device__ __forceinline__ BJSpec bjp_spec(const BJS &e, double2 L1, double2 L2, double thr) {
+  BJSpec p;
+  p.s1 = e.s + e.h2;                                         // trip k+1 (odd)
+  p.s1 = p.s1 - L1.x;
+  p.s1 = p.s1 - L1.y;
+  p.s2 = p.s1 + e.h2;                                        // trip k+2 (even)
+  p.s2 = p.s2 - L2.x;
+  p.s2 = p.s2 - L2.y;
+  p.t1 = rexp<false>(p.s1).t;
+  p.t2 = rexp<false>(p.s2).t;
+  p.a1 = e.acc - p.t1;                                       // odd k subtracts
+  p.a2 = p.a1 + p.t2;                                        // even k adds
+  p.act1 = p.t1 > thr;
+  p.act2 = p.t2 > thr;
+  return p;
+}
+
+template <bool GRAD>
+__device__ __forceinline__ BJOut bjp_epilogue(BJS &e, int nu, double tol, double accg, int chk) {
+  double zg = 0.0;
+  if (e.fwd_ok) {
+    double acc = e.acc - e.t;                                // acc -= convert(s)
+    double sg = e.sg;
+    if (GRAD) sg = sg + (1.0 * accg) * e.t;
+    double s = e.s, hzg = 0.0;
+    for (int q = nu; q >= 1; q--) {                          // for i = nu:-1:1
+      s = s + (q < BJ_KP ? s_logpair[q].x : logi(q));
+      s = s - e.halfz;
+      hzg = hzg + 1.0 * sg;
+    }
+    double h2 = e.h2 - e.halfz;                              // halfz2 /= halfz (x2)
+    hzg = hzg + 1.0 * e.h2g;
+    h2 = h2 - e.halfz;
+    hzg = hzg + 1.0 * e.h2g;
+    double lz = 0.0 + e.logz;
+    double halfz = e.halfz + LN2;                            // halfz *= 2
+    halfz = halfz - lz;                                      // halfz /= lz
+    const double lzg = 0.0 + 1.0 * hzg;
+    lz = lz - e.logz;                                        // lz /= convert(z)
+    if (GRAD) zg = zg + (1.0 * lzg) / e.z;
+    if (chk && !e.code) {                                    // releases
+      if (fabs(acc - 0.0) > tol || fabs(s - 0.0) > tol || fabs(h2 - 0.0) > tol ||
+          fabs(halfz - 0.0) > tol || fabs(lz - 0.0) > tol)
+        e.code = RL_ERR_DIRTY_ANCILLA;
+    }
+  }
+  const double qnan = __longlong_as_double(0x7ff8000000000000ULL);
+  BJOut o;
+  o.J = e.fwd_ok ? e.J : qnan;
+  o.dz = e.fwd_ok ? zg : qnan;
+  o.T = e.T;
+  o.code = e.code;
+  o.bad = e.valid && e.bad;
+  return o;
+}
+
+template <bool GRAD>
+__device__ __forceinline__ void besselj_pair(BJS &A, BJS &B, int nu, double thr, double tol,
+                                             double seed, int ktab, int kfuel, int chk,
+                                             double sfloor, BJOut &oa, BJOut &ob) {
+  // ---------------- sweep 1: forward routine ----------------
+  bjp_prologue(A, nu, thr, kfuel, sfloor);
+  bjp_prologue(B, nu, thr, kfuel, sfloor);
+  int k = 0;
+  if (nu < 0 && __any_sync(FULL_MASK, A.act || B.act)) {     // first trip: s /= kn, kn <= 0
+    if (A.act) A.code = kfuel > 0 ? RL_ERR_DOMAIN : RL_ERR_FUEL;
+    if (B.act) B.code = kfuel > 0 ? RL_ERR_DOMAIN : RL_ERR_FUEL;
+    A.act = B.act = false;
+  }
+  const int kend = ktab < kfuel ? ktab : kfuel;
+  if (__all_sync(FULL_MASK, (A.act || A.dead) && (B.act || B.dead)) &&
+      __any_sync(FULL_MASK, A.act || B.act)) {
+    while (k + 2 <= kend) {
+      const double2 L1 = s_logpair[k + 1], L2 = s_logpair[k + 2];
+      const BJSpec pa = bjp_spec(A, L1, L2, thr), pb = bjp_spec(B, L1, L2, thr);
+      if (__all_sync(FULL_MASK, ((pa.act1 && pa.act2) || A.dead) &&
+                                    ((pb.act1 && pb.act2) || B.dead))) {
+        A.s = pa.s2; A.t = pa.t2; A.acc = pa.a2;
+        B.s = pb.s2; B.t = pb.t2; B.acc = pb.a2;
+        k += 2;
+        A.T = k;
+        B.T = k;
+        continue;
+      }
+      auto commit = [&](BJS &e, const BJSpec &p) {
+        if (p.act1) {
+          e.s = p.s2; e.t = p.t2; e.acc = p.a2; e.T = k + 2; e.act = p.act2;
+        } else {
+          e.s = p.s1; e.t = p.t1; e.acc = p.a1; e.T = k + 1; e.act = false;
+        }
+      };
+      commit(A, pa);
+      commit(B, pb);
+      k += 2;
+      break;
+    }
+    if (A.dead) { A.act = false; A.T = 0; A.code = A.code0; }   // undo the unpredicated trips
+    if (B.dead) { B.act = false; B.T = 0; B.code = B.code0; }
+  }
+  // tail: predicated
+  while (k < kend && __any_sync(FULL_MASK, A.act || B.act)) {
+    k++;
+    fwd_trip<false, true, true, -1>(k, nu, A.h2, thr, A.act, A.s, A.t, A.acc, A.T, A.code);
+    fwd_trip<false, true, true, -1>(k, nu, B.h2, thr, B.act, B.s, B.t, B.acc, B.T, B.code);
+  }
+  while (k < kfuel && __any_sync(FULL_MASK, A.act || B.act)) {   // beyond the table
+    k++;
+    fwd_trip<false, false, true, -1>(k, nu, A.h2, thr, A.act, A.s, A.t, A.acc, A.T, A.code);
+    fwd_trip<false, false, true, -1>(k, nu, B.h2, thr, B.act, B.s, B.t, B.acc, B.T, B.code);
+  }
+  if (A.act) A.code = RL_ERR_FUEL;                           // still running at the fuel cap
+  if (B.act) B.code = RL_ERR_FUEL;
+  A.J = 0.0 + A.acc;                                         // out! += acc
+  B.J = 0.0 + B.acc;
+  A.fwd_ok = A.valid && !A.code;
+  B.fwd_ok = B.valid && !B.code;
+
+  // ---------------- sweep 4: ~routine with adjoints ----------------
+  const double accg = 0.0 + (1.0 * seed) * 1.0;              // out! -= acc: acc.g += out.g
+  const double paccg = 1.0 * accg, naccg = -1.0 * accg;
+  A.sg = A.h2g = B.sg = B.h2g = 0.0;
+  A.ok = B.ok = true;
+  if (A.fwd_ok && chk && A.t > thr) A.code = RL_ERR_POSTCONDITION;   // entry: post false
+  if (B.fwd_ok && chk && B.t > thr) B.code = RL_ERR_POSTCONDITION;
+  const int TA = A.fwd_ok ? A.T : 0, TB = B.fwd_ok ? B.T : 0;
+  const int Tmax = __reduce_max_sync(FULL_MASK, TA > TB ? TA : TB);
+  const unsigned Tmin = __reduce_min_sync(
+      FULL_MASK, (unsigned)min(A.fwd_ok ? A.T : 0x7fffffff, B.fwd_ok ? B.T : 0x7fffffff));
+  int kr = Tmax;
+#define BJP_REV(CAR, TAB, PRED, ODD, UNIT, KK)                                               \
+  do {                                                                                       \
+    rev_trip<CAR, TAB, PRED, ODD, GRAD, UNIT>(KK, nu, A.h2, thr, paccg, naccg, chk, A.fwd_ok, \
+                                              PRED ? TA : A.T, A.acc, A.sg, A.s, A.h2g, A.t,  \
+                                              A.code, A.ok);                                 \
+    rev_trip<CAR, TAB, PRED, ODD, GRAD, UNIT>(KK, nu, B.h2, thr, paccg, naccg, chk, B.fwd_ok, \
+                                              PRED ? TB : B.T, B.acc, B.sg, B.s, B.h2g, B.t,  \
+                                              B.code, B.ok);                                 \
+  } while (0)
+  for (; kr > ktab; kr--) BJP_REV(false, false, true, -1, false, kr);   // beyond the table
+  for (; kr > (int)Tmin; kr--) BJP_REV(false, true, true, -1, false, kr);   // tail: predicated
+  if (kr >= 1 && !(kr & 1)) {                                // align: pairs start at odd k
+    BJP_REV(false, true, false, 0, false, kr);
+    kr--;
+  }
+  if (accg == 1.0) {                                         // the default seed (uniform branch)
+    for (; kr >= 2; kr -= 2) {
+      BJP_REV(false, true, false, 1, true, kr);
+      BJP_REV(false, true, false, 0, true, kr - 1);
+    }
+  }
+  for (; kr >= 2; kr -= 2) {
+    BJP_REV(false, true, false, 1, false, kr);
+    BJP_REV(false, true, false, 0, false, kr - 1);
+  }
+  if (kr == 1) BJP_REV(false, true, false, 1, false, 1);
+#undef BJP_REV
+  if (chk && A.fwd_ok && !A.ok && !A.code) A.code = RL_ERR_POSTCONDITION;
+  if (chk && B.fwd_ok && !B.ok && !B.code) B.code = RL_ERR_POSTCONDITION;
+  oa = bjp_epilogue<GRAD>(A, nu, tol, accg, chk);
+  ob = bjp_epilogue<GRAD>(B, nu, tol, accg, chk);
+}
+
 constexpr int BJ_RUN = 0, BJ_GRAD = 1, BJ_HESS = 2;
 
 template <int MODE>
@@ -851,7 +1065,8 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
     //    down (longest first), so the block's warps reach the barrier together
     //    (the next round's ticket is drawn one round ahead, off the
     //    critical path)
-    const int nrounds = (cnt + 31) >> 5;
+    constexpr int RW = (BJ_PAIR && MODE != BJ_HESS) ? 64 : 32;  // elements per warp round
+    const int nrounds = (cnt + RW - 1) / RW;
     int ticket = 0;
     if (lane == 0) ticket = atomicAdd(&s_round, 1);
 #pragma unroll 1
@@ -860,6 +1075,39 @@ __global__ void __launch_bounds__(BJ_BLOCK, MODE == 2 ? 2 : BJ_MINB) k_besselj(
       if (got >= nrounds) break;
       if (lane == 0) ticket = atomicAdd(&s_round, 1);
       const int r = nrounds - 1 - got;
+#if BJ_PAIR
+      if (MODE != BJ_HESS) {
+        BJS A, B;
+        const int pa = r * 64 + 2 * lane, pb = pa + 1;
+        A.valid = pa < cnt;
+        B.valid = pb < cnt;
+        if (!__any_sync(FULL_MASK, A.valid)) continue;
+        A.z = A.valid ? s_z[pa] : 1.0;
+        B.z = B.valid ? s_z[pb] : 1.0;
+        BJOut oa, ob;
+        besselj_pair<GRAD>(A, B, nu, thr, tol, seed, ktab, kfuel, chk, sfloor, oa, ob);
+        if (__any_sync(FULL_MASK, oa.bad || ob.bad)) {          // |exp arg| >= 708 somewhere
+          const BJOut ca =
+              besselj_element<true, GRAD>(A.z, oa.bad, nu, thr, tol, seed, ktab, kfuel, chk, sfloor);
+          if (oa.bad) oa = ca;
+          const BJOut cb =
+              besselj_element<true, GRAD>(B.z, ob.bad, nu, thr, tol, seed, ktab, kfuel, chk, sfloor);
+          if (ob.bad) ob = cb;
+        }
+        auto put = [&](int pos, bool valid, const BJOut &o) {
+          if (!valid) return;
+          const int oi = s_idx[pos];
+          s_J[oi] = o.J;
+          s_dz[oi] = o.dz;
+          s_fail[oi] = (uint8_t)o.code;
+          if (!o.code) trips_sum += (unsigned long long)o.T;   // trips of the elements that succeed
+          nfail += o.code != 0;
+        };
+        put(pa, A.valid, oa);
+        put(pb, B.valid, ob);
+        continue;
+      }
+#endif
       const int pos = r * 32 + lane;
       const bool valid = pos < cnt;
       if (__any_sync(FULL_MASK, valid)) {
