@@ -112,7 +112,8 @@ def test_unaligned_x_takes_the_cp_async_kernels(cuda, oracle, d):
     check_vs((e, ga, gm, gi), got)
 
 
-@pytest.mark.parametrize("d,K,N", [(2, 1, 1), (2, 3, 5), (64, 1, 33), (62, 2, 31), (30, 7, 64)])
+@pytest.mark.parametrize("d,K,N", [(2, 1, 1), (2, 3, 5), (64, 1, 33), (62, 2, 31), (30, 7, 64),
+                                   (16, 120, 300)])
 def test_tiny_shapes_vs_oracle(cuda, oracle, d, K, N):
     """Edge shapes of the tile kernels: one point, one component, a single
     partial tile, d just below a padding boundary (TMA out-of-bounds columns)."""
