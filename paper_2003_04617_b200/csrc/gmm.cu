@@ -16,9 +16,12 @@
 //
 //   k_gmm_prep    per component: qd = exp(diag icf), sq = sum(diag icf) (the
 //                 top routine) and the transposed factor L_k^T, packed by rows
-//   k_gmm_fwd     forward mat-vec tiles Z = Xc L^T (FP64 DFMA, register
-//                 tiled, smem-staged) -> sqn -> mt[k][i]; sqn's uncompute
-//                 residual is checked on device (DirtyAncilla)
+//   k_gmm_fwd     forward mat-vec tiles Z = Xc L^T on the FP64 tensor cores
+//                 (mma.sync m16n8k16 / k8 f64, x tiles by TMA) -> sqn ->
+//                 mt[k][i]; sqn's uncompute residual is checked on device
+//                 (DirtyAncilla).  d <= 64, d even: k_gmm_fwd_ws (warp-
+//                 specialised: one feature row block x 16 points per warp,
+//                 full / empty mbarrier ring, no CTA barrier per tile)
 //   k_gmm_lse     per point: the reversible argmax / logsumexp forward, then its
 //                 reverse sweep with adjoints -> dmt = d err / d mt[k][i],
 //                 release and branch-postcondition checks
@@ -26,9 +29,15 @@
 //                 the forward values are rebuilt, not stored), forms
 //                 qxc.g = (-dmt/2)(2 Z), and accumulates the factor adjoint
 //                 M = sum_i qxc.g_i xc_i^T (lower triangle) and sum_i qxc.g_i
-//                 in registers across the block's points
-//                 (prep's block 0 also evaluates -N lse(alphas) and its
+//                 in registers across the block's points (k_gmm_rev_ws for
+//                 d <= 64, d even: G^T through warp-private scratch, tiles
+//                 centred once per CTA, m8n8k4 for the half-needed diagonal
+//                 factor tiles)
+//                 (prep's extra block evaluates -N lse(alphas) and its
 //                 gradient; the Wishart prior and cst are added in final)
+//   k_gmm_restore (drop-in gradient only, side stream beside rev): err! in
+//                 the program's order, bit-exact, and the primal-restoration
+//                 verdict (seqsum.cuh)
 //   k_gmm_final   per component: the chain through qd = exp(icf) and sq, means.g =
 //                 -L^T sum_i qxc.g_i (linearity: sum_i xc.g_i = L^T sum_i qxc.g_i)
 //
